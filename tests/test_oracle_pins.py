@@ -1,0 +1,383 @@
+"""Pins for the float64 oracle (-m "not gpu").  Each check ties the oracle to
+something other than itself: the SPEC/paper worked values in
+tests/golden/spec_examples.json, closed forms, invariants, textbook/library
+routines (scipy.signal.correlate), brute force on tiny inputs, and central
+finite differences (SPEC S:300-308 gradcheck protocol)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ops, nets
+from oracle.autograd import Var, backward, VersionError
+from oracle.optim import sgd_step
+from oracle.step import train_step
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def V(a, rg=False):
+    return Var(np.asarray(a, np.float64), requires_grad=rg)
+
+
+# ------------------------------------------------------------ worked values
+def test_matmul_worked():
+    g = GOLD["matmul_2x2"]
+    assert np.array_equal(ops.matmul(V(g["a"]), V(g["b"])).value, np.array(g["out"], float))
+
+
+def test_linear_worked():
+    g = GOLD["linear_n1"]
+    assert np.array_equal(ops.linear(V(g["x"]), V(g["w"]), V(g["b"])).value, np.array(g["out"]))
+
+
+def test_broadcast_add_worked():
+    g = GOLD["broadcast_add"]
+    assert np.array_equal(ops.add(V(g["a"]), V(g["b"])).value, np.array(g["out"], float))
+
+
+def test_relu_worked():
+    g = GOLD["relu"]
+    assert np.array_equal(ops.relu(V(g["x"])).value, np.array(g["out"], float))
+
+
+def test_softmax_worked():
+    for x, out, tol in GOLD["softmax"]["cases"]:
+        assert np.max(np.abs(ops.softmax(np.array([x], float))[0] - out)) <= tol
+
+
+def test_conv_worked():
+    g = GOLD["conv_all_ones"]
+    y = ops.conv2d(V(np.ones(g["x_shape"])), V(np.ones(g["w_shape"])), None)
+    assert y.value.shape == tuple(g["out_shape"]) and np.all(y.value == g["out_value"])
+    g = GOLD["conv_listing1_shape"]
+    y = ops.conv2d(V(np.zeros(g["x_shape"])), V(np.zeros(g["w_shape"])), None)
+    assert y.value.shape == tuple(g["out_shape"])
+
+
+def test_backward_worked():
+    g = GOLD["backward_sum_sq"]
+    x = V(g["x"], True)
+    backward(ops.sum_all(ops.mul(x, x)))
+    assert np.array_equal(x.grad, np.array(g["grad"], float))
+
+
+def test_accumulate_worked():
+    g = GOLD["accumulate_two_backwards"]
+    x = V([0.0], True)
+    for gi in g["grads"]:
+        backward(ops.sum_all(ops.mul(x, V(gi))))
+    assert np.array_equal(x.grad, np.array(g["out"], float))
+
+
+def test_sgd_worked():
+    for c in GOLD["sgd"]["cases"]:
+        p, _ = sgd_step({"p": np.array(c["p"])}, {"p": np.array(c["g"])}, c["lr"], 0.0, c["wd"])
+        assert abs(float(p["p"]) - c["out"]) < 1e-15
+
+
+def test_sgd_momentum_closed_form():
+    # v1 = g', v2 = mu*v1 + g' ; p2 = p1 - lr*v2
+    p = {"p": np.array(1.0)}
+    g = {"p": np.array(0.5)}
+    p1, b1 = sgd_step(p, g, 0.1, 0.9, 0.0)
+    p2, b2 = sgd_step(p1, g, 0.1, 0.9, 0.0, b1)
+    assert abs(float(p1["p"]) - 0.95) < 1e-15
+    assert abs(float(p2["p"]) - (0.95 - 0.1 * (0.9 * 0.5 + 0.5))) < 1e-15
+
+
+# ------------------------------------------------------------ closed forms
+def test_mlp_closed_form_zero_last_layer():
+    """W2 = 0, b2 = 0 ⇒ logits uniform ⇒ loss = ln C exactly, dz = (1/C − onehot)/B,
+    dW2 = Hᵀdz, dH = 0 ⇒ dW1 = 0, db1 = 0 (SURVEY §8(c) pin table)."""
+    net = nets.MLP((784, 128, 10))
+    P = synth.make_params(net.param_specs(), seed=3)
+    P["fc1.w"][:] = 0
+    P["fc1.b"][:] = 0
+    x = synth.uniform((64, 784), 3, 1)
+    y = synth.labels(64, 10, 3)
+    out = train_step(net, P, (x, y), lr=0.01)
+    assert abs(out["loss"] - math.log(10)) < 1e-14
+    H = np.maximum(x.astype(np.float64) @ P["fc0.w"] + P["fc0.b"], 0)
+    dz = np.full((64, 10), 0.1)
+    dz[np.arange(64), y] -= 1
+    dz /= 64
+    assert np.allclose(out["grads"]["fc1.w"], H.T @ dz, rtol=1e-12, atol=1e-15)
+    assert np.allclose(out["grads"]["fc1.b"], dz.sum(0), atol=1e-16)
+    assert np.all(out["grads"]["fc0.w"] == 0) and np.all(out["grads"]["fc0.b"] == 0)
+
+
+def test_xent_rows_sum_zero_and_stable():
+    z = V(np.array([[1000.0, 1000.0], [1.0, 2.0]]), True)
+    loss = ops.softmax_cross_entropy(z, np.array([0, 1]))
+    backward(loss)
+    assert np.isfinite(loss.value)
+    assert abs(float(loss.value) - 0.5 * (math.log(2) + math.log(1 + math.exp(-1)))) < 1e-12
+    assert np.allclose(z.grad.sum(1), 0, atol=1e-17)
+
+
+def test_bce_equals_softplus_closed_form():
+    """2-class CE on [0,z] == mean(softplus(z) − y·z); dz = (σ(z) − y)/B."""
+    rng = np.random.default_rng(0)
+    z = V(rng.standard_normal((16, 1)) * 3, True)
+    y = (rng.random(16) < 0.3).astype(np.int64)
+    loss = ops.bce_as_two_class_ce(z, y)
+    backward(loss)
+    zz = z.value[:, 0]
+    ref = np.mean(np.logaddexp(0, zz) - y * zz)
+    assert abs(float(loss.value) - ref) < 1e-14
+    sig = 1 / (1 + np.exp(-zz))
+    assert np.allclose(z.grad[:, 0], (sig - y) / 16, atol=1e-16)
+
+
+# ------------------------------------------------------------ brute force
+def _direct_conv(x, w, b, stride, pad):
+    """7-loop direct cross-correlation (textbook definition)."""
+    N, C, H, W = x.shape
+    K, _, R, S = w.shape
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    y = np.zeros((N, K, P, Q))
+    for n in range(N):
+        for k in range(K):
+            for p in range(P):
+                for q in range(Q):
+                    acc = 0.0 if b is None else b[k]
+                    for c in range(C):
+                        for r in range(R):
+                            for u in range(S):
+                                h, ww = p * stride - pad + r, q * stride - pad + u
+                                if 0 <= h < H and 0 <= ww < W:
+                                    acc += x[n, c, h, ww] * w[k, c, r, u]
+                    y[n, k, p, q] = acc
+    return y
+
+
+@pytest.mark.parametrize("stride,pad", [(1, 0), (1, 1), (2, 0), (2, 1)])
+def test_conv_brute_force(stride, pad):
+    rng = np.random.default_rng(stride * 10 + pad)
+    x = rng.standard_normal((2, 3, 5, 5))
+    w = rng.standard_normal((4, 3, 3, 3))
+    b = rng.standard_normal(4)
+    y = ops.conv2d(V(x), V(w), V(b), stride, pad).value
+    assert np.allclose(y, _direct_conv(x, w, b, stride, pad), rtol=1e-12, atol=1e-12)
+
+
+def test_conv_vs_scipy_correlate():
+    from scipy.signal import correlate
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 3, 7, 6))
+    w = rng.standard_normal((4, 3, 3, 2))
+    y = ops.conv2d(V(x), V(w), None, 1, 0).value
+    ref = np.zeros_like(y)
+    for n in range(2):
+        for k in range(4):
+            ref[n, k] = correlate(x[n], w[k], mode="valid")[0]
+    assert np.allclose(y, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_im2col_table_brute_enumeration():
+    N, C, H, W, R, S, st, pd = 2, 3, 5, 4, 3, 2, 2, 1
+    T = ops.im2col_table(N, C, H, W, R, S, st, pd)
+    P, Q = ops.conv_out_size(H, R, st, pd), ops.conv_out_size(W, S, st, pd)
+    m = 0
+    for n in range(N):
+        for p in range(P):
+            for q in range(Q):
+                k = 0
+                for r in range(R):
+                    for u in range(S):
+                        for c in range(C):
+                            h, w = p * st - pd + r, q * st - pd + u
+                            exp = ((n * H + h) * W + w) * C + c if (0 <= h < H and 0 <= w < W) else -1
+                            assert T[m, k] == exp
+                            k += 1
+                m += 1
+    assert m == T.shape[0]
+
+
+def test_maxpool_brute_force_and_ties():
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((2, 3, 7, 7))
+    x[0, 0, :3, :3] = 0.0     # all-zero window → first index (0,0)
+    for k, s, p in [(3, 2, 0), (3, 2, 1)]:
+        y, am = ops.maxpool2d(V(x), k, s, p)
+        N, C, H, W = x.shape
+        P = (H + 2 * p - k) // s + 1
+        for n in range(N):
+            for c in range(C):
+                for i in range(P):
+                    for j in range(P):
+                        best, bi = -np.inf, -1
+                        for r in range(k):
+                            for u in range(k):
+                                h, w = i * s - p + r, j * s - p + u
+                                if 0 <= h < H and 0 <= w < W and (bi < 0 or x[n, c, h, w] > best):
+                                    best, bi = x[n, c, h, w], h * W + w
+                        assert y.value[n, c, i, j] == best and am[n, c, i, j] == bi
+    y, am = ops.maxpool2d(V(x), 3, 2, 0)
+    assert am[0, 0, 0, 0] == 0
+
+
+def test_maxpool_mass_conservation():
+    rng = np.random.default_rng(2)
+    x = V(rng.standard_normal((2, 2, 9, 9)), True)
+    y, _ = ops.maxpool2d(x, 3, 2, 1)
+    g = rng.standard_normal(y.value.shape)
+    backward(y, g)
+    assert abs(x.grad.sum() - g.sum()) < 1e-12
+
+
+def test_embedding_brute_force():
+    rng = np.random.default_rng(3)
+    E = V(rng.standard_normal((7, 4)), True)
+    ids = np.array([1, 3, 1, 6, 1])
+    r = ops.embedding(E, ids)
+    g = rng.standard_normal((5, 4))
+    backward(r, g)
+    ref = np.zeros((7, 4))
+    for i, t in enumerate(ids):
+        ref[t] += g[i]
+    assert np.array_equal(r.value, E.value[ids]) and np.allclose(E.grad, ref, atol=0)
+
+
+# ------------------------------------------------------------ invariants
+def test_batchnorm_invariants():
+    rng = np.random.default_rng(4)
+    x = V(rng.standard_normal((4, 3, 5, 5)) * 2 + 1, True)
+    gam = V(rng.standard_normal(3), True)
+    bet = V(rng.standard_normal(3), True)
+    y, _ = ops.batchnorm2d(x, gam, bet)
+    var = x.value.var(axis=(0, 2, 3))
+    assert np.allclose(y.value.mean(axis=(0, 2, 3)), bet.value, atol=1e-12)
+    assert np.allclose(y.value.var(axis=(0, 2, 3)), gam.value ** 2 * var / (var + 1e-5), rtol=1e-10)
+    g = rng.standard_normal(y.value.shape)
+    backward(y, g)
+    xhat = (x.value - x.value.mean(axis=(0, 2, 3), keepdims=True)) / np.sqrt(var + 1e-5)[None, :, None, None]
+    assert np.allclose(x.grad.sum(axis=(0, 2, 3)), 0, atol=1e-10)
+    # Σ dx·x̂ = γ/√(σ²+ε) · Σ(dy·x̂) · ε/(σ²+ε)  (Σx̂² = cnt·σ²/(σ²+ε); it is 0 only at ε=0)
+    inv = 1 / np.sqrt(var + 1e-5)
+    exp = gam.value * inv * (g * xhat).sum(axis=(0, 2, 3)) * 1e-5 / (var + 1e-5)
+    assert np.allclose((x.grad * xhat).sum(axis=(0, 2, 3)), exp, rtol=1e-8, atol=1e-13)
+
+
+def test_fanout_sum():
+    """grad through y=f(x), z=g(x), L=y+z equals the sum of
+    per-path gradients."""
+    rng = np.random.default_rng(6)
+    xv = rng.standard_normal(5)
+    x = V(xv, True)
+    backward(ops.sum_all(ops.add(ops.mul(x, x), ops.relu(x))))
+    x1 = V(xv, True)
+    backward(ops.sum_all(ops.mul(x1, x1)))
+    x2 = V(xv, True)
+    backward(ops.sum_all(ops.relu(x2)))
+    assert np.allclose(x.grad, x1.grad + x2.grad, atol=0)
+
+
+def test_version_error():
+    """PAPER.md:161-165 / SPEC S:268: mutation of a saved tensor → user error."""
+    w = V([1.0, 2.0], True)
+    x = V([3.0, 4.0])
+    y = ops.sum_all(ops.mul(w, x))
+    x.value += 1
+    x.bump_version()
+    with pytest.raises(VersionError):
+        backward(y)
+
+
+def test_double_backward_error():
+    x = V([3.0], True)
+    y = ops.sum_all(ops.mul(x, x))
+    backward(y)
+    with pytest.raises(RuntimeError, match="DoubleBackward"):
+        backward(y)
+
+
+def test_dp_emulation_equals_global_batch():
+    """BN-free net: R-shard average of gradients equals the global-batch
+    gradient exactly (up to f64 rounding) — mean-reduced loss."""
+    net = nets.MLP((20, 16, 5))
+    P = synth.make_params(net.param_specs(), 1)
+    x = synth.normal((8, 20), 1, 1)
+    y = synth.labels(8, 5, 1)
+    a = train_step(net, P, (x, y), replicas=1)
+    b = train_step(net, P, (x, y), replicas=4)
+    for k in P:
+        assert np.allclose(a["grads"][k], b["grads"][k], rtol=1e-12, atol=1e-15)
+        assert np.allclose(a["params"][k], b["params"][k], rtol=1e-12, atol=1e-15)
+
+
+# ------------------------------------------------------------ gradcheck
+def _gradcheck(make_loss, leaves, h=1e-6, tol=1e-4, n_coords=12, seed=0):
+    """Central differences on sampled coordinates."""
+    loss = make_loss()
+    backward(loss)
+    rng = np.random.default_rng(seed)
+    for leaf in leaves:
+        flat = leaf.value.reshape(-1)
+        idx = rng.choice(flat.size, size=min(n_coords, flat.size), replace=False)
+        for i in idx:
+            old = flat[i]
+            flat[i] = old + h
+            fp = float(make_loss().value)
+            flat[i] = old - h
+            fm = float(make_loss().value)
+            flat[i] = old
+            num = (fp - fm) / (2 * h)
+            an = leaf.grad.reshape(-1)[i]
+            assert abs(num - an) / max(1.0, abs(an)) <= tol, (leaf.name, i, num, an)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_gradcheck_ops(seed):
+    rng = np.random.default_rng(seed)
+    x = Var(rng.standard_normal((2, 3, 6, 6)), True, "x")
+    w = Var(rng.standard_normal((4, 3, 3, 3)) * 0.3, True, "w")
+    b = Var(rng.standard_normal(4), True, "b")
+    g = Var(rng.standard_normal(4) + 1.0, True, "g")
+    be = Var(rng.standard_normal(4), True, "be")
+    fw = Var(rng.standard_normal((4, 5)) * 0.3, True, "fw")
+    fb = Var(rng.standard_normal(5), True, "fb")
+    y = rng.integers(0, 5, 2)
+
+    def f():
+        h = ops.conv2d(x, w, b, 2, 1)
+        h, _ = ops.batchnorm2d(h, g, be)
+        h = ops.relu(ops.add(h, h))
+        h, _ = ops.maxpool2d(h, 3, 2, 1)
+        h = ops.avgpool_global(h)
+        return ops.softmax_cross_entropy(ops.linear(h, fw, fb), y)
+    for v in (x, w, b, g, be, fw, fb):
+        v.grad = None
+    _gradcheck(f, [x, w, b, g, be, fw, fb], seed=seed)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_gradcheck_ncf_tiny(seed):
+    net = nets.NCF(n_users=11, n_items=7, gmf=4, mlp=(8, 8, 4))
+    P0 = synth.make_params(net.param_specs(), seed)
+    users, items, yy = synth.ncf_batch(6, 11, 7, seed)
+    P = {k: Var(v.astype(np.float64), True, k) for k, v in P0.items()}
+    _gradcheck(lambda: net.loss(P, (users, items, yy))[0], list(P.values()), seed=seed, n_coords=4)
+
+
+def test_gradcheck_tiny_resnet_block():
+    net = nets.ResNet50(layers=(1, 1), base=4, classes=5)
+    P0 = synth.make_params(net.param_specs(), 2)
+    x = synth.normal((2, 3, 16, 16), 2, 1).astype(np.float64)
+    y = synth.labels(2, 5, 2)
+    P = {k: Var(v.astype(np.float64), True, k) for k, v in P0.items()}
+    _gradcheck(lambda: net.loss(P, (x, y))[0], [P["conv1.w"], P["l1.0.c2.w"], P["l2.0.ds.w"],
+                                                 P["l2.0.bn3.g"], P["fc.w"]], n_coords=5)
+
+
+def test_param_counts():
+    """ResNet-50 v1.5 has 25,557,032 parameters (SURVEY §8(c) reading 9);
+    AlexNet single tower 61,100,840 (torchvision form)."""
+    cnt = lambda net: sum(int(np.prod(s[1])) for s in net.param_specs())
+    assert cnt(nets.ResNet50()) == 25557032
+    assert cnt(nets.AlexNet()) == 61100840
