@@ -1,0 +1,362 @@
+"""bench.py — train samples/s of the eager training step (fwd + bwd + SGD)
+on synthetic data (BASELINE.json metric), one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N      (N > 1: data parallel, NCCL buckets)
+
+Default workload = BASELINE.json configs[1] (C2: MLP 4096-4096-4096-1000,
+batch 1024/GPU, bf16).  Prints ONE JSON line on rank 0.
+
+`--impl reference` times the float64 CPU oracle (oracle/) on this host — the
+reference arm of this tier (no reference implementation exists; see
+DESIGN.md).  It is the only other place this file executes oracle/ besides
+the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(workload="C1 MLP 784-128-10, batch 64, fp32 (3xTF32 GEMMs)", net="mlp", sizes=(784, 128, 10),
+               batch=64, dtype="f32"),
+    "c2": dict(workload="C2 MLP 4096-4096-4096-1000, batch 1024/GPU, bf16", net="mlp",
+               sizes=(4096, 4096, 4096, 1000), batch=1024, dtype="bf16"),
+    "c3": dict(workload="C3 AlexNet (single tower), 224x224, batch 256/GPU, bf16", net="alexnet", batch=256,
+               dtype="bf16"),
+    "c4": dict(workload="C4 ResNet-50 v1.5, 224x224, batch 256/GPU, bf16", net="resnet50", batch=256, dtype="bf16"),
+    "c5": dict(workload="C5 NCF NeuMF (ML-20M tables), batch 8192/GPU (65536 global on 8), bf16", net="ncf",
+               batch=8192, dtype="bf16"),
+}
+METRIC = "train samples/s (fwd+bwd+SGD) at 1/2/4/8 B200; per-kernel % of roofline"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------- synthetic workloads
+def make_model(cfg, be, seed=0):
+    import synth
+    if cfg["net"] == "mlp":
+        m = be.nn.MLP(cfg["sizes"])
+    elif cfg["net"] == "alexnet":
+        m = be.nn.AlexNet()
+    elif cfg["net"] == "resnet50":
+        m = be.nn.ResNet50()
+    else:
+        m = be.nn.NCF()
+    m.load(synth.make_params(m.param_specs(), seed))
+    return m
+
+
+def host_batch(cfg, seed, rank=0):
+    """Host arrays of one batch in the device layout (marshalling only)."""
+    import synth
+    B = cfg["batch"]
+    from paper_1912_01703_b200.api import f32_to_bf16_bits
+    if cfg["net"] == "mlp":
+        x = (synth.uniform if cfg["sizes"][0] == 784 else synth.normal)((B, cfg["sizes"][0]), seed, 1 + rank)
+        y = synth.labels(B, cfg["sizes"][-1], seed + rank)
+        xd = f32_to_bf16_bits(x) if cfg["dtype"] == "bf16" else x
+        return [xd, y]
+    if cfg["net"] in ("alexnet", "resnet50"):
+        x = synth.normal((B, 3, 224, 224), seed, 1 + rank)
+        nhwc = np.zeros((B, 224, 224, 8), np.float32)
+        nhwc[..., :3] = x.transpose(0, 2, 3, 1)
+        y = synth.labels(B, 1000, seed + rank)
+        return [f32_to_bf16_bits(nhwc) if cfg["dtype"] == "bf16" else nhwc, y]
+    u, i, y = synth.ncf_batch(B, 138493, 26744, seed + rank)
+    return [u, i, y]
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- oracle timing (reference arm / cpu_baseline)
+def oracle_time(cfg, budget_s=15.0, max_steps=None, min_steps=1):
+    """Time the float64 oracle's train_step on a bounded sample of the workload."""
+    import synth
+    from oracle import nets as onets
+    from oracle.step import train_step
+    B = cfg["batch"]
+    if cfg["net"] == "mlp":
+        net = onets.MLP(cfg["sizes"])
+        sb = min(B, 256 if cfg["sizes"][0] > 1000 else B)
+        batch = ((synth.uniform if cfg["sizes"][0] == 784 else synth.normal)((sb, cfg["sizes"][0]), 0, 1),
+                 synth.labels(sb, cfg["sizes"][-1], 0))
+    elif cfg["net"] in ("alexnet", "resnet50"):
+        net = onets.AlexNet() if cfg["net"] == "alexnet" else onets.ResNet50()
+        sb = 2
+        batch = (synth.normal((sb, 3, 224, 224), 0, 1), synth.labels(sb, 1000, 0))
+    else:
+        net = onets.NCF()
+        sb = 8192
+        batch = synth.ncf_batch(sb, 138493, 26744, 0)
+    P = synth.make_params(net.param_specs(), 0)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        out = train_step(net, P, batch, lr=0.01)
+        P = {k: v.astype(np.float32) for k, v in out["params"].items()}
+        n += 1
+        el = time.perf_counter() - t0
+        if (el >= budget_s and n >= min_steps) or (max_steps and n >= max_steps):
+            break
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": n * sb / el, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} float64 oracle step(s) of {cfg['net']} at batch {sb} (of {B}) in {el:.1f}s, "
+                      f"NumPy/OpenBLAS on all host cores"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import paper_1912_01703_b200 as be
+    torch.cuda.set_device(local_rank)
+    stream = torch.cuda.Stream()
+    be.init(local_rank, stream.cuda_stream)
+    be.set_compute_dtype(cfg["dtype"])
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        uid = [be.dist_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        be.dist_init(rank, world, uid[0])
+    model = make_model(cfg, be, seed=0)
+    params = model.parameters()
+    if world > 1:
+        be.ddp_attach(params, 25 << 20)
+    hb = host_batch(cfg, seed=1, rank=rank)
+    dts = ["bf16" if (i == 0 and cfg["net"] != "ncf" and cfg["dtype"] == "bf16") else None for i in range(len(hb))]
+
+    def dev_batch():
+        out = []
+        for a, d in zip(hb, dts):
+            if d == "bf16":
+                t = be.empty(a.shape, "bf16")
+                be.api.call("be_tensor_copy_from_host_async", t.handle, a.ctypes.data_as(__import__("ctypes").c_void_p),
+                            a.nbytes)
+                out.append(t)
+            else:
+                out.append(be.tensor(a))
+        be.synchronize()
+        return out
+    batch = dev_batch()
+
+    def step(b):
+        return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4)
+
+    for _ in range(args.warmup):
+        step(batch)
+    be.synchronize()
+    stats_warm = be.alloc_stats()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        be.synchronize()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    l0 = be.launch_count()
+    be.prof_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        loss = step(batch)
+    e1.record(stream)
+    barrier()
+    be.prof_enable(False)
+    ms = e0.elapsed_time(e1)
+    launches = be.launch_count() - l0
+    prof = be.prof_read()
+    clk = clocks.stop()
+    stats_after = be.alloc_stats()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end-to-end through the public API: pinned host → device each step, loss → host
+    pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in hb]
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    dev_in = [be.empty(a.shape, d or {np.dtype(np.int32): "i32", np.dtype(np.float32): "f32"}[a.dtype])
+              for a, d in zip(hb, dts)]
+    import ctypes as C
+    h2d = sum(a.nbytes for a in hb)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        for t, p in zip(dev_in, pinned):
+            be.api.call("be_tensor_copy_from_host_async", t.handle, C.c_void_p(p.data_ptr()), p.numel() * p.element_size())
+        loss = step(dev_in)
+        be.api.call("be_tensor_copy_to_host_async", loss.handle, C.c_void_p(loss_host.data_ptr()), 4)
+    e3.record(stream)
+    barrier()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    final_loss = float(loss_host.item())
+
+    if rank != 0:
+        return None
+    B = cfg["batch"]
+    value = B * world * args.steps / (ms / 1e3)
+    # roofline of the dominant kernel class (tcgen05 GEMM)
+    pk, pk_kind = peaks()
+    tc = [r for r in prof if r["name"].startswith("gemm_tc")]
+    gemm_ms = sum(r["ms"] for r in tc)
+    flops = sum(r["flops"] for r in tc)
+    achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    dt_bench = "bf16" if cfg["dtype"] == "bf16" else "f32"
+    if cfg["dtype"] == "f32":
+        peak = peak / 2.0 / 3.0  # tf32 nominal = bf16/2; 3xTF32 issues 3 MMAs per algorithmic product
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+            "kernel": "gemm_tc (all tcgen05 GEMM launches of the step)",
+            "launches_per_step": len(tc) / args.steps, "share_of_step": round(gemm_ms / ms, 4) if ms else None,
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk_kind})"}
+    trafficf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(trafficf):
+        roof["traffic"] = json.load(open(trafficf)).get("dram_bytes_per_launch")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_time(cfg, budget_s=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dt_bench, "data": "synthetic (seeded, device-resident)",
+        "config": {"workload": cfg["workload"], "global_batch": B * world, "per_gpu_batch": B,
+                   "parallelism": f"dp{world}", "l2": "working set > L2 (params+grads+momentum stream through "
+                   "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4"},
+        "e2e": {"value": round(B * world * args.steps / (ms_e2e / 1e3), 2), "unit": "samples/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "alloc": {"raw_alloc_count_delta_timed": stats_after["raw_alloc_count"] - stats_warm["raw_alloc_count"],
+                  "peak_bytes_in_use": stats_after["peak_bytes_in_use"]},
+        "final_loss": final_loss,
+    }
+    return line
+
+
+def run_reference(args, cfg):
+    """Reference arm: the float64 oracle on this host's cores, K steps on a
+    bounded sample of the workload (each step one oracle train_step)."""
+    import synth  # noqa: F401
+    t0 = time.perf_counter()
+    r = oracle_time(cfg, budget_s=0.0, max_steps=args.warmup, min_steps=1) if args.warmup else None  # warm-up
+    r = oracle_time(cfg, budget_s=0.0, max_steps=args.steps, min_steps=args.steps)
+    el = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 4), "unit": "samples/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "parallelism": "host cores"},
+            "cpu_baseline": {"value": round(r["value"], 4), "unit": "samples/s", "cores": r["cores"],
+                             "kind": "oracle", "sample": r["sample"]},
+            "e2e": {"value": round(r["value"], 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": round(el, 1)}
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, cfg, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,249 @@
+/*
+ * be.h — C ABI of the B200-native eager training-step library ("be" =
+ * B200 eager).  This is the boundary of the hot path named by
+ * BASELINE.json north_star: tensor create/free, op dispatch + record-to-tape,
+ * backward(), step(), served by a stream-ordered caching allocator, with a
+ * bucketed data-parallel gradient allreduce.
+ *
+ * Paper passages (arXiv 1912.01703, /root/reference/PAPER.md line numbers):
+ *   - tensors + operators + autograd in a C++ core ..... PAPER.md:177 (§5.1)
+ *   - define-by-run tape, reverse mode, versions ....... PAPER.md:158-165 (§4.3)
+ *   - async queueing on a CUDA stream .................. PAPER.md:183-187 (§5.2)
+ *   - caching allocator, 512-B rounding, pool/stream ... PAPER.md:193-204 (§5.3)
+ *   - refcount-driven immediate free ................... PAPER.md:221-229 (§5.5)
+ *   - all-reduce gradient synchronisation .............. PAPER.md:216 (§5.4)
+ * SPEC.md (a CPU spec written from the paper) fixes the error names and the
+ * small contracts cited as S:n.
+ *
+ * General rules
+ *   - Every function returns be_status: 0 (BE_OK) or an error code below.
+ *     Nothing throws or aborts across the ABI; be_last_error() returns a
+ *     thread-local message for the most recent failure on this thread.
+ *   - Ownership: every be_tensor written through an `out` pointer carries ONE
+ *     reference owned by the caller, who must be_release() it.  The last
+ *     release returns the memory block to the allocator pool of the stream
+ *     it was allocated on, immediately.
+ *   - Asynchrony: all device work is enqueued on the library's compute stream
+ *     (PAPER.md:185); calls return before the kernels finish.  Only
+ *     be_tensor_to_host, be_item and be_synchronize wait.  Environment
+ *     BE_SYNC=1 synchronises after every launch (debug).
+ *   - Single device per process; grad mode is thread-local.
+ *   - There is NO CPU fallback: a missing/unsupported device path returns
+ *     BE_E_UNSUPPORTED.
+ */
+#ifndef BE_H_
+#define BE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct be_tensor_s* be_tensor;   /* opaque, intrusive refcount */
+typedef int be_status;
+
+/* dtype codes 0-3 follow SPEC's MTNS codes. */
+typedef enum {
+  BE_F32 = 0, BE_F64 = 1, BE_I64 = 2, BE_BOOL = 3, BE_BF16 = 4, BE_I32 = 5, BE_U8 = 6
+} be_dtype;
+
+enum {
+  BE_OK = 0,
+  BE_E_SHAPE = 1,            /* ShapeMismatch */
+  BE_E_BROADCAST = 2,        /* BroadcastError */
+  BE_E_DTYPE = 3,            /* DTypeMismatch / UnsupportedDType */
+  BE_E_AXIS = 4,             /* AxisOutOfRange */
+  BE_E_EMPTY_REDUCTION = 5,  /* EmptyReduction */
+  BE_E_NONCONTIG = 6,        /* NonContiguous */
+  BE_E_VERSION = 7,          /* saved tensor mutated before backward */
+  BE_E_DOUBLE_BACKWARD = 8,  /* second backward without retain_graph */
+  BE_E_NO_UPSTREAM = 9,      /* non-scalar root without upstream */
+  BE_E_INPLACE_LEAF = 10,    /* in-place on a leaf requiring grad */
+  BE_E_MISSING_GRAD = 11,    /* optimizer step on a param without grad */
+  BE_E_OOM = 12,             /* after one empty_cache retry */
+  BE_E_DOUBLE_FREE = 13,
+  BE_E_BAD_HANDLE = 14,
+  BE_E_CUDA = 15,            /* CUDA error; async faults surface at the next sync */
+  BE_E_NCCL = 16,
+  BE_E_UNSUPPORTED = 17,     /* no device path for this request (no CPU fallback) */
+  BE_E_NOT_INIT = 18,
+  BE_E_ARG = 19
+};
+
+/* ------------------------------------------------------------------ init */
+/* Bind the library to CUDA device `device` and a compute stream.
+ * cuda_stream: a cudaStream_t cast to uint64 (e.g. torch's current stream)
+ * that the library adopts but never destroys; 0 = create an own stream.
+ * Must be called once per process before any other call (BE_E_NOT_INIT). */
+be_status be_init(int device, uint64_t cuda_stream);
+/* Returns the compute stream in use (cudaStream_t as uint64). */
+be_status be_get_stream(uint64_t* out);
+const char* be_last_error(void);
+/* Number of kernels this library launched since init (all streams). */
+be_status be_launch_count(uint64_t* out);
+
+/* ------------------------------------------------------------------ tensors
+ * Shapes are row-major, rank <= 6.  Device layouts used by the ops:
+ * activations NHWC (4-D) or [rows, cols] (2-D); conv weights KRSC;
+ * Linear weights [in, out] (Listing 1). */
+/* Allocate a contiguous tensor and copy `host` (row-major, nbytes =
+ * numel*size(dtype)) into it; host may be NULL (uninitialised).  The copy
+ * is stream-ordered; `host` must stay valid until the next synchronising
+ * call (use pinned memory for async copies).  requires_grad marks a leaf
+ * (S:48-54). */
+be_status be_tensor_create(const void* host, const int64_t* shape, int rank, be_dtype dtype,
+                           int requires_grad, be_tensor* out);
+be_status be_tensor_empty(const int64_t* shape, int rank, be_dtype dtype, be_tensor* out);
+/* Zero-copy wrap of device memory.  `release`
+ * (may be NULL) is invoked with ctx exactly once when the last reference
+ * dies.  strides may be NULL (contiguous). */
+be_status be_tensor_from_device(void* dptr, const int64_t* shape, const int64_t* strides,
+                                int rank, be_dtype dtype, void (*release)(void*), void* ctx,
+                                be_tensor* out);
+/* Synchronous device→host copy of a tensor (any strides) into dst, row-major. */
+be_status be_tensor_to_host(be_tensor t, void* dst, size_t nbytes);
+/* Async stream-ordered host↔device copies for a contiguous tensor. */
+be_status be_tensor_copy_from_host_async(be_tensor t, const void* src, size_t nbytes);
+be_status be_tensor_copy_to_host_async(be_tensor t, void* dst, size_t nbytes);
+/* Metadata. */
+be_status be_tensor_info(be_tensor t, int* rank, int64_t* shape /*6*/, int64_t* strides /*6*/,
+                         be_dtype* dtype, uint64_t* device_ptr);
+be_status be_tensor_version(be_tensor t, uint64_t* out);
+be_status be_tensor_requires_grad(be_tensor t, int* out);
+be_status be_retain(be_tensor t);
+be_status be_release(be_tensor t);                                  /* BE_E_DOUBLE_FREE */
+/* In-place fill (bumps the version by 1).  BE_E_INPLACE_LEAF when t
+ * is a leaf that requires grad and grad mode is on. */
+be_status be_fill_(be_tensor t, double value);
+/* Copy src into dst in place (same shape; dtype cast allowed; bumps version). */
+be_status be_copy_(be_tensor dst, be_tensor src);
+
+/* ------------------------------------------------------------------ ops
+ * be_op both dispatches (launches the kernels on the compute stream) and,
+ * when grad mode is on and an input requires grad, records a tape node
+ * holding version-pinned saved tensors. */
+typedef enum {
+  BE_OP_LINEAR = 1,        /* in: x[B,in], w[in,out], b[out] (n_in 2|3); attrs be_linear_attrs; out: y[B,out] */
+  BE_OP_MATMUL = 2,        /* in: a[M,K], b[K,N]; out: [M,N] */
+  BE_OP_ADD = 3,           /* in: a, b (right-aligned broadcast); attrs int* act (NULL|0 none, 1 relu) */
+  BE_OP_MUL = 4,           /* in: a, b same shape */
+  BE_OP_RELU = 5,          /* in: x */
+  BE_OP_SOFTMAX_XENT = 6,  /* in: logits[B,C], labels i32[B]; out: loss f32 [] (mean), optional out[1]: argmax i32[B] */
+  BE_OP_BCE_LOGITS = 7,    /* in: z[B,1] or [B], labels i32[B] (0|1); out: loss f32 [] (mean) */
+  BE_OP_CONV2D = 8,        /* in: x NHWC[N,H,W,C], w KRSC[K,R,S,C], b[K] optional; attrs be_conv_attrs; out NHWC[N,P,Q,K] */
+  BE_OP_MAXPOOL2D = 9,     /* in: x NHWC; attrs be_pool_attrs; out: y NHWC, optional out[1]: argmax u8 window index (r*k+u) */
+  BE_OP_AVGPOOL_GLOBAL = 10, /* in: x NHWC[N,H,W,C]; out [N,C] */
+  BE_OP_BATCHNORM2D = 11,  /* in: x NHWC, gamma[C], beta[C], running_mean[C]?, running_var[C]?; attrs be_bn_attrs */
+  BE_OP_RESHAPE = 12,      /* in: x contiguous; attrs be_shape_attrs; out: view (shares storage) */
+  BE_OP_EMBEDDING = 13,    /* in: table[V,D] (f32 param), ids i32[B]; out [B,D] */
+  BE_OP_CONCAT = 14,       /* in: n 2-D tensors [B,Di]; concatenated along axis 1 */
+  BE_OP_SUM = 15,          /* in: x; out: [] */
+  BE_OP_MEAN = 16,         /* in: x; out: [] */
+  BE_OP_CAST = 17,         /* in: x; attrs be_dtype*; out: x cast (RN-even for f32→bf16) */
+  BE_OP_ADD_RELU = 18      /* residual: y = relu(a + b), same shape */
+} be_op_id;
+
+typedef struct { int act; /* 0 none, 1 relu */ int out_f32; /* 1: fp32 output even in bf16 mode */ } be_linear_attrs;
+typedef struct { int stride, pad, act; int out_f32; } be_conv_attrs;
+typedef struct { int k, stride, pad; } be_pool_attrs;
+typedef struct { float eps, momentum; int act; /* fused ReLU after affine */ } be_bn_attrs;
+typedef struct { int rank; int64_t shape[6]; } be_shape_attrs;
+
+be_status be_op(int op_id, const be_tensor* in, int n_in, const void* attrs,
+                be_tensor* out, int n_out);
+
+/* Grad mode (thread-local). */
+be_status be_set_grad_enabled(int on);
+be_status be_is_grad_enabled(int* out);
+/* Compute dtype: BE_F32 (GEMMs run 3xTF32 on tcgen05; fp32 activations) or
+ * BE_BF16 (GEMM/conv read a bf16 shadow of fp32 params, emit bf16
+ * activations; grads and master weights stay fp32). */
+be_status be_set_compute_dtype(be_dtype d);
+be_status be_detach(be_tensor t, be_tensor* out);
+
+/* ------------------------------------------------------------------ autograd
+ * Reverse-mode sweep: dependency counts over the
+ * reachable tape, nodes issued in reverse-topological order, saved tensors
+ * version-checked at unpack (BE_E_VERSION) and released right after their
+ * node ran unless retain_graph; leaf grads accumulate with +=.
+ * upstream NULL requires a 1-element root (BE_E_NO_UPSTREAM). */
+be_status be_backward(be_tensor root, be_tensor upstream, int retain_graph);
+/* +1 reference to leaf's grad in *out, or *out = NULL when absent. */
+be_status be_grad(be_tensor leaf, be_tensor* out);
+/* Releases the grads (not zero-fill). */
+be_status be_zero_grad(const be_tensor* params, int n);
+
+/* ------------------------------------------------------------------ optimizer
+ * One fused multi-tensor SGD launch per <=256 params:
+ *   g' = scale*g + wd*p;  v = mu*v + g' (v starts at 0);  p -= lr*(mu ? v : g')
+ * and, in bf16 mode, the bf16 shadow copy is rewritten in the same pass.
+ * scale = 1/world_size when DDP is attached.  BE_E_MISSING_GRAD if a param
+ * has no grad.  Each param's version bumps by 1. */
+be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum,
+                      float weight_decay);
+
+/* ------------------------------------------------------------------ allocator */
+struct be_alloc_stats {
+  uint64_t raw_alloc_count, raw_free_count, cache_hit_count;
+  uint64_t bytes_in_use, bytes_cached, peak_bytes_in_use;
+};
+be_status be_alloc_stats(struct be_alloc_stats* out);
+be_status be_alloc_reset_peak(void);
+be_status be_empty_cache(uint64_t* bytes_released);
+/* Pure helper: rounded size (512-B quantum). */
+uint64_t be_round_size(uint64_t nbytes);
+/* Mark that t's block is used on `stream` (cudaStream_t as uint64); its
+ * reuse is deferred until an event recorded there completes. */
+be_status be_record_stream(be_tensor t, uint64_t stream);
+/* Raw allocator access on the compute stream (for tests of §5.3 semantics). */
+be_status be_raw_alloc(uint64_t nbytes, uint64_t stream, uint64_t* dptr);
+be_status be_raw_free(uint64_t dptr);
+
+/* ------------------------------------------------------------------ data parallel
+ * One process per GPU.  nccl_unique_id: 128 bytes from rank 0 (ncclGetUniqueId
+ * via be_dist_unique_id), distributed by the caller (torch.distributed). */
+be_status be_dist_unique_id(void* out128);
+be_status be_dist_init(int rank, int world, const void* nccl_unique_id);
+/* Attach params for DDP: broadcast from rank 0; grads become
+ * views into fp32 buckets of ~bucket_bytes in reverse param order; each bucket
+ * is all-reduced (sum) on a comm stream as soon as its last grad lands during
+ * backward; be_sgd_step waits for all buckets and folds in 1/world. */
+be_status be_ddp_attach(const be_tensor* params, int n, size_t bucket_bytes);
+be_status be_ddp_detach(void);
+/* Plain allreduce (sum, fp32/bf16) of a contiguous tensor on the compute stream. */
+be_status be_allreduce_(be_tensor t);
+
+/* ------------------------------------------------------------------ profiling
+ * When enabled, every GEMM launch (the dominant kernel class) is bracketed
+ * by CUDA events on the stream it is launched on; be_prof_read synchronises
+ * and returns one record per launch (then clears).  flops / bytes are the
+ * ALGORITHMIC counts of that launch: 2·M·N·K and the operand + output bytes. */
+typedef struct {
+  char name[32];
+  double flops, bytes;
+  float ms;
+  int m, n, k;
+} be_prof_rec;
+be_status be_prof_enable(int on);
+be_status be_prof_read(be_prof_rec* out, int cap, int* n_out);
+
+/* ------------------------------------------------------------------ misc */
+be_status be_synchronize(void);
+/* Read a 1-element tensor as double (synchronises). */
+be_status be_item(be_tensor t, double* out);
+/* Parity hook: the conv im2col offset table the device path uses,
+ * conv_geom = {N,C,H,W,R,S,stride,pad}; out[M*R*S*C] int64 (NHWC offsets,
+ * -1 in padding) computed ON THE DEVICE by the kernel's own index math. */
+be_status be_debug_im2col_offsets(const int64_t* conv_geom, int64_t* out);
+/* Direct GEMM entry (tests): D[M,N] = A[M,K]·B[K,N] (+bias[N]) (act),
+ * all row-major contiguous device tensors; A/B dtype f32 (3xTF32) or bf16;
+ * transpose flags select Aᵀ / Bᵀ storage.  beta in {0,1}. */
+be_status be_gemm(be_tensor A, int trans_a, be_tensor B, int trans_b, be_tensor D,
+                  be_tensor bias, int act, float beta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BE_H_ */

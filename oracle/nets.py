@@ -50,7 +50,8 @@ class MLP:
         h = x
         L = len(self.sizes) - 1
         for i in range(L):
-            h = ops.linear(h, P[f"fc{i}.w"], P[f"fc{i}.b"])
+            # logits are produced in fp32 (not a bf16 storage point)
+            h = ops.linear(h, P[f"fc{i}.w"], P[f"fc{i}.b"], store_out=i < L - 1)
             if i < L - 1:
                 h = ops.relu(h)
         return h

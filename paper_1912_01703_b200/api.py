@@ -1,0 +1,397 @@
+"""Python face of the library: a Tensor handle class and one function per
+be_op (argument marshalling only — the ops run in libbe.so on the GPU).
+
+Mirrors the user-visible API of the paper's Listing 1/2:
+tensors, differentiable ops, `loss.backward()`, an SGD step.
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import call
+
+_NP = {L.BE_F32: np.float32, L.BE_F64: np.float64, L.BE_I64: np.int64, L.BE_BOOL: np.bool_,
+       L.BE_I32: np.int32, L.BE_U8: np.uint8, L.BE_BF16: np.uint16}
+_FROM_NP = {np.dtype(np.float32): L.BE_F32, np.dtype(np.float64): L.BE_F64, np.dtype(np.int64): L.BE_I64,
+            np.dtype(np.bool_): L.BE_BOOL, np.dtype(np.int32): L.BE_I32, np.dtype(np.uint8): L.BE_U8}
+DTYPES = {"f32": L.BE_F32, "bf16": L.BE_BF16, "i32": L.BE_I32, "i64": L.BE_I64, "u8": L.BE_U8, "f64": L.BE_F64}
+
+
+def _dt(d):
+    if isinstance(d, str):
+        return DTYPES[d]
+    return int(d)
+
+
+def f32_to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """Host-side RN-even fp32 → bf16 bit pattern (input marshalling only)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u >> 16) & 1) + 0x7FFF
+    return ((u + r) >> 16).astype(np.uint16)
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+class Tensor:
+    """Owns one reference to a be_tensor handle (released in __del__)."""
+    __slots__ = ("_h", "__weakref__")
+
+    def __init__(self, handle):
+        if not handle:
+            raise ValueError("null tensor handle")
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and L._lib is not None:
+            L._lib.be_release(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        r = C.c_int()
+        shp = (C.c_int64 * 6)()
+        strd = (C.c_int64 * 6)()
+        dt = C.c_int()
+        ptr = C.c_uint64()
+        call("be_tensor_info", self._h, C.byref(r), shp, strd, C.byref(dt), C.byref(ptr))
+        return r.value, tuple(shp[:r.value]), tuple(strd[:r.value]), dt.value, ptr.value
+
+    @property
+    def shape(self):
+        return self._info()[1]
+
+    @property
+    def dtype(self):
+        return self._info()[3]
+
+    @property
+    def data_ptr(self):
+        return self._info()[4]
+
+    @property
+    def version(self):
+        v = C.c_uint64()
+        call("be_tensor_version", self._h, C.byref(v))
+        return v.value
+
+    @property
+    def requires_grad(self):
+        v = C.c_int()
+        call("be_tensor_requires_grad", self._h, C.byref(v))
+        return bool(v.value)
+
+    @property
+    def grad(self):
+        out = C.c_void_p()
+        call("be_grad", self._h, C.byref(out))
+        return Tensor(out.value) if out.value else None
+
+    def numel(self):
+        return int(np.prod(self.shape)) if self.shape else 1
+
+    def numpy(self) -> np.ndarray:
+        """Synchronous copy to host; bf16 is returned widened to float32."""
+        rank, shape, _, dt, _ = self._info()
+        out = np.empty(shape, dtype=_NP[dt])
+        call("be_tensor_to_host", self._h, out.ctypes.data_as(C.c_void_p), C.c_size_t(out.nbytes))
+        if dt == L.BE_BF16:
+            return bf16_bits_to_f32(out)
+        return out
+
+    def item(self) -> float:
+        v = C.c_double()
+        call("be_item", self._h, C.byref(v))
+        return v.value
+
+    def backward(self, upstream: "Tensor | None" = None, retain_graph=False):
+        call("be_backward", self._h, upstream._h if upstream is not None else None, int(retain_graph))
+
+    def detach(self):
+        out = C.c_void_p()
+        call("be_detach", self._h, C.byref(out))
+        return Tensor(out.value)
+
+    def fill_(self, v):
+        call("be_fill_", self._h, C.c_double(v))
+        return self
+
+    def copy_(self, src: "Tensor"):
+        call("be_copy_", self._h, src._h)
+        return self
+
+    def __repr__(self):
+        return f"be.Tensor(shape={self.shape}, dtype={self.dtype})"
+
+
+# ------------------------------------------------------------------ construction
+def init(device: int = 0, stream: int = 0):
+    """Bind to a CUDA device; `stream` = cudaStream_t as int (e.g. torch's
+    current stream `.cuda_stream`) or 0 for an own stream."""
+    call("be_init", int(device), C.c_uint64(int(stream)))
+
+
+def get_stream() -> int:
+    v = C.c_uint64()
+    call("be_get_stream", C.byref(v))
+    return v.value
+
+
+def launch_count() -> int:
+    v = C.c_uint64()
+    call("be_launch_count", C.byref(v))
+    return v.value
+
+
+def tensor(a, requires_grad=False, dtype=None) -> Tensor:
+    """Create from host data (host→device copy on the compute stream).
+    dtype "bf16" converts float32 host data with RN-even."""
+    a = np.asarray(a)
+    if dtype is not None and _dt(dtype) == L.BE_BF16:
+        host = f32_to_bf16_bits(a.astype(np.float32))
+        dt = L.BE_BF16
+    else:
+        if dtype is not None:
+            a = a.astype(_NP[_dt(dtype)])
+        elif a.dtype == np.float64:
+            a = a.astype(np.float32)
+        elif a.dtype == np.int64:
+            a = a.astype(np.int32)
+        host = np.ascontiguousarray(a)
+        dt = _FROM_NP[host.dtype]
+    shape = (C.c_int64 * 6)(*host.shape)
+    out = C.c_void_p()
+    call("be_tensor_create", host.ctypes.data_as(C.c_void_p), shape, host.ndim, dt, int(requires_grad),
+         C.byref(out))
+    call("be_synchronize")  # host buffer may be pageable / temporary
+    return Tensor(out.value)
+
+
+def empty(shape, dtype="f32") -> Tensor:
+    shp = (C.c_int64 * 6)(*shape)
+    out = C.c_void_p()
+    call("be_tensor_empty", shp, len(shape), _dt(dtype), C.byref(out))
+    return Tensor(out.value)
+
+
+_KEEP = {}
+
+
+def from_device(ptr: int, shape, dtype="f32", owner=None) -> Tensor:
+    """Zero-copy wrap of device memory; `owner` is kept alive until release
+    (PAPER.md:140-143)."""
+    shp = (C.c_int64 * 6)(*shape)
+    key = C.c_void_p(id(owner) if owner is not None else 0)
+
+    def _release(ctx):
+        _KEEP.pop(ctx, None)
+    cb = L.RELEASE_CB(_release)
+    out = C.c_void_p()
+    call("be_tensor_from_device", C.c_void_p(ptr), shp, None, len(shape), _dt(dtype), cb, key, C.byref(out))
+    _KEEP[key.value] = (owner, cb)
+    return Tensor(out.value)
+
+
+def from_torch(t) -> Tensor:
+    """Zero-copy view of a contiguous CUDA torch tensor (plumbing only)."""
+    import torch
+    m = {torch.float32: "f32", torch.bfloat16: "bf16", torch.int32: "i32", torch.int64: "i64", torch.uint8: "u8"}
+    assert t.is_cuda and t.is_contiguous()
+    return from_device(t.data_ptr(), tuple(t.shape), m[t.dtype], owner=t)
+
+
+# ------------------------------------------------------------------ ops
+def _op(op, ins, attrs=None, n_out=1):
+    arr = (C.c_void_p * len(ins))(*[t._h.value if t is not None else None for t in ins])
+    outs = (C.c_void_p * n_out)()
+    call("be_op", L.OPS[op], arr, len(ins), C.byref(attrs) if attrs is not None else None, outs, n_out)
+    res = [Tensor(o) if o else None for o in outs]
+    return res[0] if n_out == 1 else tuple(res)
+
+
+def linear(x, w, b=None, act=0, out_f32=False):
+    return _op("LINEAR", [x, w] + ([b] if b is not None else []), L.be_linear_attrs(int(act), int(out_f32)))
+
+
+def matmul(a, b):
+    return _op("MATMUL", [a, b])
+
+
+def add(a, b, relu=False):
+    return _op("ADD", [a, b], C.c_int(1 if relu else 0))
+
+
+def add_relu(a, b):
+    return _op("ADD_RELU", [a, b])
+
+
+def mul(a, b):
+    return _op("MUL", [a, b])
+
+
+def relu(x):
+    return _op("RELU", [x])
+
+
+def softmax_xent(z, labels, with_argmax=False):
+    return _op("SOFTMAX_XENT", [z, labels], None, 2 if with_argmax else 1)
+
+
+def bce_logits(z, labels):
+    return _op("BCE_LOGITS", [z, labels])
+
+
+def conv2d(x, w, b=None, stride=1, pad=0, act=0, out_f32=False):
+    return _op("CONV2D", [x, w] + ([b] if b is not None else []),
+               L.be_conv_attrs(int(stride), int(pad), int(act), int(out_f32)))
+
+
+def maxpool2d(x, k=3, stride=2, pad=0, with_argmax=False):
+    return _op("MAXPOOL2D", [x], L.be_pool_attrs(k, stride, pad), 2 if with_argmax else 1)
+
+
+def avgpool_global(x):
+    return _op("AVGPOOL_GLOBAL", [x])
+
+
+def batchnorm2d(x, gamma, beta, running_mean=None, running_var=None, eps=1e-5, momentum=0.1, act=0):
+    ins = [x, gamma, beta]
+    if running_mean is not None:
+        ins += [running_mean, running_var]
+    return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act)))
+
+
+def reshape(x, shape):
+    a = L.be_shape_attrs(len(shape), (C.c_int64 * 6)(*shape))
+    return _op("RESHAPE", [x], a)
+
+
+def embedding(table, ids):
+    return _op("EMBEDDING", [table, ids])
+
+
+def concat(xs):
+    return _op("CONCAT", list(xs))
+
+
+def sum(x):  # noqa: A001
+    return _op("SUM", [x])
+
+
+def mean(x):
+    return _op("MEAN", [x])
+
+
+def cast(x, dtype):
+    return _op("CAST", [x], C.c_int(_dt(dtype)))
+
+
+def gemm(A, B, D, trans_a=False, trans_b=False, bias=None, act=0, beta=0.0):
+    call("be_gemm", A._h, int(trans_a), B._h, int(trans_b), D._h, bias._h if bias is not None else None, int(act),
+         C.c_float(beta))
+
+
+# ------------------------------------------------------------------ autograd / optim
+@contextlib.contextmanager
+def no_grad():
+    v = C.c_int()
+    call("be_is_grad_enabled", C.byref(v))
+    call("be_set_grad_enabled", 0)
+    try:
+        yield
+    finally:
+        call("be_set_grad_enabled", v.value)
+
+
+def set_compute_dtype(d):
+    call("be_set_compute_dtype", _dt(d))
+
+
+def _handles(ts):
+    return (C.c_void_p * len(ts))(*[t._h.value for t in ts])
+
+
+def sgd_step(params, lr, momentum=0.0, weight_decay=0.0):
+    call("be_sgd_step", _handles(params), len(params), C.c_float(lr), C.c_float(momentum), C.c_float(weight_decay))
+
+
+def zero_grad(params):
+    call("be_zero_grad", _handles(params), len(params))
+
+
+def synchronize():
+    call("be_synchronize")
+
+
+def alloc_stats() -> dict:
+    s = L.be_alloc_stats()
+    call("be_alloc_stats", C.byref(s))
+    return {f: getattr(s, f) for f, _ in L.be_alloc_stats._fields_}
+
+
+def reset_peak():
+    call("be_alloc_reset_peak")
+
+
+def empty_cache() -> int:
+    v = C.c_uint64()
+    call("be_empty_cache", C.byref(v))
+    return v.value
+
+
+def round_size(n: int) -> int:
+    return int(L.lib().be_round_size(C.c_uint64(n)))
+
+
+def im2col_offsets(N, C_, H, W, R, S, stride, pad) -> np.ndarray:
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    out = np.empty((N * P * Q, R * S * C_), np.int64)
+    geom = (C.c_int64 * 8)(N, C_, H, W, R, S, stride, pad)
+    call("be_debug_im2col_offsets", geom, out.ctypes.data_as(C.POINTER(C.c_int64)))
+    return out
+
+
+def prof_enable(on=True):
+    call("be_prof_enable", int(on))
+
+
+def prof_read(cap=100000):
+    recs = (L.be_prof_rec * cap)()
+    n = C.c_int()
+    call("be_prof_read", recs, cap, C.byref(n))
+    return [dict(name=r.name.decode(), flops=r.flops, bytes=r.bytes, ms=r.ms, m=r.m, n=r.n, k=r.k)
+            for r in recs[:n.value]]
+
+
+# ------------------------------------------------------------------ data parallel
+def dist_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    call("be_dist_unique_id", buf)
+    return bytes(buf)
+
+
+def dist_init(rank, world, uid: bytes):
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    call("be_dist_init", int(rank), int(world), buf)
+
+
+def ddp_attach(params, bucket_bytes=25 << 20):
+    call("be_ddp_attach", _handles(params), len(params), C.c_size_t(bucket_bytes))
+
+
+def ddp_detach():
+    call("be_ddp_detach")
+
+
+def allreduce_(t):
+    call("be_allreduce_", t._h)

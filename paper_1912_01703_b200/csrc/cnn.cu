@@ -1,0 +1,428 @@
+// cnn.cu — memory-bound CNN kernels (NHWC): im2col / col2im feeding the
+// tcgen05 GEMM (conv fwd / dgrad / wgrad as GEMMs),
+// max / global-average pooling, batch-norm statistics / apply / backward,
+// embedding gather, column concat / slice.
+//
+// Index conventions are those of the oracle's im2col table:
+// row m = (n, p, q) row-major; column k = (r, u, c) row-major (KRSC order);
+// h = p·stride − pad + r; w = q·stride − pad + u; padding reads 0.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "runtime.h"
+
+namespace be { namespace k {
+using namespace be::dev;
+
+namespace {
+int grid_for(int64_t n, int per = 1) {
+  int64_t b = (n + 256LL * per - 1) / (256LL * per);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx().num_sms * 16));
+}
+
+// ---- im2col: one thread per (m, r, u, 8-channel chunk); 16-B copies when C%8==0 (bf16) / C%4==0 (f32)
+template <typename T, int VEC>
+__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int64_t ldc, ConvGeom g, int64_t total) {
+  const int CV = g.C / VEC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int cv = (int)(t % CV); t /= CV;
+    const int u = (int)(t % g.S); t /= g.S;
+    const int r = (int)(t % g.R); t /= g.R;
+    const int64_t m = t;
+    const int q = (int)(m % g.Q);
+    const int p = (int)((m / g.Q) % g.P);
+    const int n = (int)(m / ((int64_t)g.P * g.Q));
+    const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + u;
+    T* dst = cols + m * ldc + ((int64_t)(r * g.S + u) * g.C + cv * VEC);
+    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
+      const T* src = x + (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * VEC;
+      if (VEC * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      else for (int j = 0; j < VEC; ++j) dst[j] = src[j];
+    } else {
+      if (VEC * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      else for (int j = 0; j < VEC; ++j) dst[j] = T(0);
+    }
+  }
+}
+
+// ---- col2im (gather form): dx[n,h,w,c] = Σ_{r,u: h=p·s−pad+r, w=q·s−pad+u} dcols[(n,p,q),(r,u,c)]
+template <typename T>
+__global__ void col2im_kernel(const T* __restrict__ dcols, int64_t ldc, T* __restrict__ dx, ConvGeom g, float beta,
+                              int64_t total, be_dtype dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = (int)(t % g.C); t /= g.C;
+    const int w = (int)(t % g.W); t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    float acc = 0.f;
+    for (int r = 0; r < g.R; ++r) {
+      const int ph = h + g.pad - r;
+      if (ph < 0 || ph % g.stride) continue;
+      const int p = ph / g.stride;
+      if (p >= g.P) continue;
+      for (int u = 0; u < g.S; ++u) {
+        const int qw = w + g.pad - u;
+        if (qw < 0 || qw % g.stride) continue;
+        const int q = qw / g.stride;
+        if (q >= g.Q) continue;
+        const int64_t m = ((int64_t)n * g.P + p) * g.Q + q;
+        acc += ld(dcols, m * ldc + (int64_t)(r * g.S + u) * g.C + c, dt);
+      }
+    }
+    if (beta != 0.f) acc += ld(dx, i, dt);
+    st(dx, i, dt, acc);
+  }
+}
+
+__global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
+  const int64_t RSC = (int64_t)g.R * g.S * g.C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / RSC, kk = i % RSC;
+    const int c = (int)(kk % g.C);
+    const int u = (int)((kk / g.C) % g.S);
+    const int r = (int)(kk / ((int64_t)g.C * g.S));
+    const int q = (int)(m % g.Q);
+    const int p = (int)((m / g.Q) % g.P);
+    const int64_t n = m / ((int64_t)g.P * g.Q);
+    const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + u;
+    out[i] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? ((n * g.H + h) * g.W + w) * g.C + c : -1;
+  }
+}
+
+// ---- max pool NHWC; window scanned r outer, u inner; first strictly greater wins; NaN wins at first sight
+__global__ void maxpool_fwd_kernel(const void* x, void* y, uint8_t* am, ConvGeom g, be_dtype dt, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = (int)(t % g.C); t /= g.C;
+    const int q = (int)(t % g.Q); t /= g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    float best = -INFINITY;
+    int bi = -1;
+    for (int r = 0; r < g.R; ++r) {
+      const int h = p * g.stride - g.pad + r;
+      if (h < 0 || h >= g.H) continue;
+      for (int u = 0; u < g.S; ++u) {
+        const int w = q * g.stride - g.pad + u;
+        if (w < 0 || w >= g.W) continue;
+        const float v = ld(x, (((int64_t)n * g.H + h) * g.W + w) * g.C + c, dt);
+        if (bi < 0 || v > best || (v != v && best == best)) { best = v; bi = r * g.S + u; }
+      }
+    }
+    st(y, i, dt, best);
+    if (am) am[i] = (uint8_t)bi;
+  }
+}
+__global__ void maxpool_bwd_kernel(const void* dy, const uint8_t* am, void* dx, ConvGeom g, be_dtype dt, float beta,
+                                   int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = (int)(t % g.C); t /= g.C;
+    const int w = (int)(t % g.W); t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    float acc = 0.f;
+    // windows (p,q) with p·s−pad ≤ h < p·s−pad+R
+    const int p_lo = max(0, (h + g.pad - g.R + g.stride) / g.stride);
+    const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
+    const int q_lo = max(0, (w + g.pad - g.S + g.stride) / g.stride);
+    const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
+    for (int p = p_lo; p <= p_hi; ++p) {
+      const int r = h - (p * g.stride - g.pad);
+      if (r < 0 || r >= g.R) continue;
+      for (int q = q_lo; q <= q_hi; ++q) {
+        const int u = w - (q * g.stride - g.pad);
+        if (u < 0 || u >= g.S) continue;
+        const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + c;
+        if (am[o] == r * g.S + u) acc += ld(dy, o, dt);
+      }
+    }
+    if (beta != 0.f) acc += ld(dx, i, dt);
+    st(dx, i, dt, acc);
+  }
+}
+
+// ---- global average pool: block per (n, 64-channel group)
+__global__ void avgpool_fwd_kernel(const void* x, void* y, int HW, int C, be_dtype dt) {
+  const int n = blockIdx.y;
+  const int c = blockIdx.x * 64 + (threadIdx.x & 63);
+  const int part = threadIdx.x >> 6;  // 4 parts
+  __shared__ float sm[4][64];
+  float s = 0.f;
+  if (c < C)
+    for (int i = part; i < HW; i += 4) s += ld(x, ((int64_t)n * HW + i) * C + c, dt);
+  sm[part][threadIdx.x & 63] = s;
+  __syncthreads();
+  if (part == 0 && c < C) st(y, (int64_t)n * C + c, dt, (sm[0][threadIdx.x] + sm[1][threadIdx.x] + sm[2][threadIdx.x] + sm[3][threadIdx.x]) / (float)HW);
+}
+__global__ void avgpool_bwd_kernel(const void* dy, void* dx, int HW, int C, be_dtype dt, float beta, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t n = i / ((int64_t)HW * C);
+    float v = ld(dy, n * C + c, dt) / (float)HW;
+    if (beta != 0.f) v += ld(dx, i, dt);
+    st(dx, i, dt, v);
+  }
+}
+
+// ---- batch norm: per-channel reductions over rows with fixed-order partials
+// partial layout: [splits][C] ; grid (ceil(C/64), splits), block 256 (4 row lanes x 64 channels)
+template <int MODE>  // 0: Σx   1: Σ(x−mean)²   2: Σg', Σg'·x̂  (g' = g·[y>0] if act)
+__global__ void bn_reduce_kernel(const void* x, const void* gy, const void* yv, int act, int64_t rows, int C,
+                                 be_dtype dt, const float* mean, const float* invstd, float* part0, float* part1,
+                                 int64_t rows_per_split) {
+  const int cl = threadIdx.x & 63, lane_r = threadIdx.x >> 6;
+  const int c = blockIdx.x * 64 + cl;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  float s0 = 0.f, s1 = 0.f;
+  if (c < C) {
+    const float mu = MODE >= 1 ? mean[c] : 0.f;
+    const float is = MODE == 2 ? invstd[c] : 0.f;
+    for (int64_t r = r0 + lane_r; r < r1; r += 4) {
+      const int64_t o = r * C + c;
+      const float v = ld(x, o, dt);
+      if (MODE == 0) s0 += v;
+      else if (MODE == 1) { float d = v - mu; s0 += d * d; }
+      else {
+        float g = ld(gy, o, dt);
+        if (act && !(ld(yv, o, dt) > 0.f)) g = 0.f;
+        s0 += g;
+        s1 += g * (v - mu) * is;
+      }
+    }
+  }
+  __shared__ float sm0[4][64], sm1[4][64];
+  sm0[lane_r][cl] = s0;
+  sm1[lane_r][cl] = s1;
+  __syncthreads();
+  if (lane_r == 0 && c < C) {
+    part0[(int64_t)blockIdx.y * C + c] = sm0[0][cl] + sm0[1][cl] + sm0[2][cl] + sm0[3][cl];
+    if (MODE == 2) part1[(int64_t)blockIdx.y * C + c] = sm1[0][cl] + sm1[1][cl] + sm1[2][cl] + sm1[3][cl];
+  }
+}
+__global__ void bn_mean_finalize(const float* part, int splits, int C, int64_t rows, float* mean) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int i = 0; i < splits; ++i) s += part[(int64_t)i * C + c];
+  mean[c] = s / (float)rows;
+}
+__global__ void bn_var_finalize(const float* part, int splits, int C, int64_t rows, float eps, const float* mean,
+                                float* invstd, float* run_mean, float* run_var, float momentum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int i = 0; i < splits; ++i) s += part[(int64_t)i * C + c];
+  const float var = s / (float)rows;  // biased (normalisation)
+  invstd[c] = rsqrtf(var + eps);
+  if (run_mean) run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mean[c];
+  if (run_var) run_var[c] = (1.f - momentum) * run_var[c] + momentum * var * (float)rows / (float)(rows > 1 ? rows - 1 : 1);
+}
+__global__ void bn_grad_finalize(const float* p0, const float* p1, int splits, int C, float* dgamma, float* dbeta,
+                                 float gb_beta, float* sums) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s0 = 0.f, s1 = 0.f;
+  for (int i = 0; i < splits; ++i) { s0 += p0[(int64_t)i * C + c]; s1 += p1[(int64_t)i * C + c]; }
+  sums[c] = s0;       // Σg'
+  sums[C + c] = s1;   // Σg'·x̂
+  if (dbeta) dbeta[c] = s0 + (gb_beta != 0.f ? dbeta[c] : 0.f);
+  if (dgamma) dgamma[c] = s1 + (gb_beta != 0.f ? dgamma[c] : 0.f);
+}
+__global__ void bn_apply_kernel(const void* x, void* y, int64_t total, int C, be_dtype dt, const float* mean,
+                                const float* invstd, const float* gamma, const float* beta, int act) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    float v = gamma[c] * (ld(x, i, dt) - mean[c]) * invstd[c] + beta[c];
+    if (act) v = fmaxf(v, 0.f);
+    st(y, i, dt, v);
+  }
+}
+__global__ void bn_dx_kernel(const void* gy, const void* x, const void* yv, int act, void* dx, int64_t total, int C,
+                             int64_t rows, be_dtype dt, const float* mean, const float* invstd, const float* gamma,
+                             const float* sums, float dx_beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    float g = ld(gy, i, dt);
+    if (act && !(ld(yv, i, dt) > 0.f)) g = 0.f;
+    const float is = invstd[c];
+    const float xh = (ld(x, i, dt) - mean[c]) * is;
+    const float inv_n = 1.f / (float)rows;
+    float v = gamma[c] * is * (g - sums[c] * inv_n - xh * sums[C + c] * inv_n);
+    if (dx_beta != 0.f) v += ld(dx, i, dt);
+    st(dx, i, dt, v);
+  }
+}
+
+// ---- embedding gather
+__global__ void embedding_fwd_kernel(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out,
+                                     be_dtype od) {
+  const int64_t total = B * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / D, d = i % D;
+    st(out, i, od, table[(int64_t)ids[b] * D + d]);
+  }
+}
+
+// ---- concat / slice along columns
+struct ConcatArgs { const void* x[8]; int64_t w[8]; int64_t off[9]; int n; };
+__global__ void concat_kernel(ConcatArgs a, int64_t rows, void* y, be_dtype dt) {
+  const int64_t W = a.off[a.n];
+  const int64_t total = rows * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / W, c = i % W;
+    int j = 0;
+    while (c >= a.off[j + 1]) ++j;
+    st(y, i, dt, ld(a.x[j], r * a.w[j] + (c - a.off[j]), dt));
+  }
+}
+__global__ void slice_kernel(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x,
+                             be_dtype dt, float beta) {
+  const int64_t total = rows * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / width, c = i % width;
+    float v = ld(y, r * ldy + col0 + c, dt);
+    if (beta != 0.f) v += ld(x, i, dt);
+    st(x, i, dt, v);
+  }
+}
+}  // namespace
+
+void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
+  const int64_t M = (int64_t)g.N * g.P * g.Q;
+  if (M == 0) return;
+  if (dt == BE_BF16 && g.C % 8 == 0) {
+    const int64_t total = M * g.R * g.S * (g.C / 8);
+    im2col_kernel<uint16_t, 8><<<grid_for(total), 256, 0, s>>>((const uint16_t*)x, (uint16_t*)cols, ldc, g, total);
+  } else if (dt == BE_F32 && g.C % 4 == 0) {
+    const int64_t total = M * g.R * g.S * (g.C / 4);
+    im2col_kernel<float, 4><<<grid_for(total), 256, 0, s>>>((const float*)x, (float*)cols, ldc, g, total);
+  } else if (dt == BE_BF16) {
+    const int64_t total = M * g.R * g.S * g.C;
+    im2col_kernel<uint16_t, 1><<<grid_for(total), 256, 0, s>>>((const uint16_t*)x, (uint16_t*)cols, ldc, g, total);
+  } else {
+    const int64_t total = M * g.R * g.S * g.C;
+    im2col_kernel<float, 1><<<grid_for(total), 256, 0, s>>>((const float*)x, (float*)cols, ldc, g, total);
+  }
+  after_launch("im2col");
+}
+void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtype dt, float beta, cudaStream_t s) {
+  const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
+  if (total == 0) return;
+  if (dt == BE_BF16)
+    col2im_kernel<uint16_t><<<grid_for(total), 256, 0, s>>>((const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, total, dt);
+  else
+    col2im_kernel<float><<<grid_for(total), 256, 0, s>>>((const float*)dcols, ldc, (float*)dx, g, beta, total, dt);
+  after_launch("col2im");
+}
+void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
+  const int64_t total = (int64_t)g.N * g.P * g.Q * g.R * g.S * g.C;
+  if (total == 0) return;
+  im2col_offsets_kernel<<<grid_for(total), 256, 0, s>>>(g, out, total);
+  after_launch("im2col_offsets");
+}
+void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
+  const int64_t total = (int64_t)g.N * g.P * g.Q * g.C;
+  if (total == 0) return;
+  maxpool_fwd_kernel<<<grid_for(total), 256, 0, s>>>(x, y, am, g, dt, total);
+  after_launch("maxpool_fwd");
+}
+void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g, be_dtype dt, float beta,
+                 cudaStream_t s) {
+  const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
+  if (total == 0) return;
+  maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(dy, am, dx, g, dt, beta, total);
+  after_launch("maxpool_bwd");
+}
+void avgpool_fwd(const void* x, void* y, int N, int HW, int C, be_dtype dt, cudaStream_t s) {
+  if (N == 0 || C == 0) return;
+  dim3 grid((C + 63) / 64, N);
+  avgpool_fwd_kernel<<<grid, 256, 0, s>>>(x, y, HW, C, dt);
+  after_launch("avgpool_fwd");
+}
+void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, float beta, cudaStream_t s) {
+  const int64_t total = (int64_t)N * HW * C;
+  if (total == 0) return;
+  avgpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(dy, dx, HW, C, dt, beta, total);
+  after_launch("avgpool_bwd");
+}
+
+static int64_t bn_splits(int64_t rows, int C) {
+  const int64_t cg = (C + 63) / 64;
+  int64_t sp = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)ctx().num_sms * 4 / cg));
+  return std::min<int64_t>(sp, 2048);
+}
+void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float* mean, float* invstd, float* partial,
+              float* run_mean, float* run_var, float momentum, cudaStream_t s) {
+  const int64_t sp = bn_splits(rows, C);
+  const int64_t rps = (rows + sp - 1) / sp;
+  dim3 grid((C + 63) / 64, (unsigned)sp);
+  bn_reduce_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial, nullptr, rps);
+  after_launch("bn_sum");
+  bn_mean_finalize<<<(C + 255) / 256, 256, 0, s>>>(partial, (int)sp, C, rows, mean);
+  after_launch("bn_mean");
+  bn_reduce_kernel<1><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, mean, nullptr, partial, nullptr, rps);
+  after_launch("bn_sqdev");
+  bn_var_finalize<<<(C + 255) / 256, 256, 0, s>>>(partial, (int)sp, C, rows, eps, mean, invstd, run_mean, run_var,
+                                                  momentum);
+  after_launch("bn_var");
+}
+void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
+              const float* gamma, const float* beta, int act, cudaStream_t s) {
+  const int64_t total = rows * C;
+  if (total == 0) return;
+  bn_apply_kernel<<<grid_for(total), 256, 0, s>>>(x, y, total, C, dt, mean, invstd, gamma, beta, act);
+  after_launch("bn_apply");
+}
+void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
+            const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta, float gb_beta,
+            float dx_beta, float* partial, cudaStream_t s) {
+  // partial must hold 2*splits*C + 2*C floats
+  const int64_t sp = bn_splits(rows, C);
+  const int64_t rps = (rows + sp - 1) / sp;
+  float* p0 = partial;
+  float* p1 = partial + sp * C;
+  float* sums = partial + 2 * sp * C;
+  dim3 grid((C + 63) / 64, (unsigned)sp);
+  bn_reduce_kernel<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps);
+  after_launch("bn_bwd_reduce");
+  bn_grad_finalize<<<(C + 255) / 256, 256, 0, s>>>(p0, p1, (int)sp, C, dgamma, dbeta, gb_beta, sums);
+  after_launch("bn_bwd_finalize");
+  if (dx) {
+    const int64_t total = rows * C;
+    bn_dx_kernel<<<grid_for(total), 256, 0, s>>>(dy, x, y, act, dx, total, C, rows, dt, mean, invstd, gamma, sums,
+                                                 dx_beta);
+    after_launch("bn_bwd_dx");
+  }
+}
+size_t bn_partial_floats(int64_t rows, int C) { return (size_t)(2 * bn_splits(rows, C) * C + 2 * C); }
+
+void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,
+                   cudaStream_t s) {
+  if (B * D == 0) return;
+  embedding_fwd_kernel<<<grid_for(B * D), 256, 0, s>>>(table, D, ids, B, out, od);
+  after_launch("embedding_fwd");
+}
+void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t rows, void* y, be_dtype dt,
+                 cudaStream_t s) {
+  ConcatArgs a{};
+  a.n = n;
+  a.off[0] = 0;
+  for (int i = 0; i < n; ++i) { a.x[i] = xs[i]; a.w[i] = widths[i]; a.off[i + 1] = a.off[i] + widths[i]; }
+  if (rows * a.off[n] == 0) return;
+  concat_kernel<<<grid_for(rows * a.off[n]), 256, 0, s>>>(a, rows, y, dt);
+  after_launch("concat");
+}
+void slice_cols(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x, be_dtype dt,
+                float beta, cudaStream_t s) {
+  if (rows * width == 0) return;
+  slice_kernel<<<grid_for(rows * width), 256, 0, s>>>(y, ldy, col0, width, rows, x, dt, beta);
+  after_launch("slice");
+}
+
+}}  // namespace be::k

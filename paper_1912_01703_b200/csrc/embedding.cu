@@ -1,0 +1,118 @@
+// embedding.cu — deterministic embedding backward:
+//   dE[ids[b], :] += dRows[b, :]
+// computed as: stable LSD radix sort of (id, position) pairs (single CTA,
+// 6-bit digits), then one warp per segment of equal ids summing its rows in
+// position order.  No floating-point atomics → bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "runtime.h"
+
+namespace be { namespace k {
+using namespace be::dev;
+
+namespace {
+constexpr int kSortThreads = 256;
+constexpr int kDigitBits = 6;
+constexpr int kBuckets = 1 << kDigitBits;
+
+// One stable LSD pass: thread t owns the contiguous chunk [t*E, (t+1)*E).
+__global__ void __launch_bounds__(kSortThreads) radix_pass(const uint32_t* __restrict__ kin,
+                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+                                                          uint32_t* __restrict__ vout, int n, int shift) {
+  extern __shared__ uint32_t cnt[];  // [kBuckets][kSortThreads]
+  const int t = threadIdx.x;
+  const int E = (n + kSortThreads - 1) / kSortThreads;
+  const int lo = min(n, t * E), hi = min(n, lo + E);
+  for (int b = 0; b < kBuckets; ++b) cnt[b * kSortThreads + t] = 0;
+  for (int i = lo; i < hi; ++i) cnt[((kin[i] >> shift) & (kBuckets - 1)) * kSortThreads + t]++;
+  __syncthreads();
+  // exclusive scan over the flattened [bucket][thread] array (bucket-major ⇒ stable)
+  __shared__ uint32_t part[kSortThreads];
+  const int per = kBuckets;  // entries per thread in the flattened order
+  uint32_t s = 0;
+  for (int j = 0; j < per; ++j) s += cnt[t * per + j];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    uint32_t run = 0;
+    for (int j = 0; j < kSortThreads; ++j) { uint32_t v = part[j]; part[j] = run; run += v; }
+  }
+  __syncthreads();
+  uint32_t run = part[t];
+  for (int j = 0; j < per; ++j) { uint32_t v = cnt[t * per + j]; cnt[t * per + j] = run; run += v; }
+  __syncthreads();
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t k = kin[i];
+    const uint32_t pos = cnt[((k >> shift) & (kBuckets - 1)) * kSortThreads + t]++;
+    kout[pos] = k;
+    vout[pos] = vin[i];
+  }
+}
+
+__global__ void init_pairs(const int32_t* ids, uint32_t* k, uint32_t* v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    k[i] = (uint32_t)ids[i];
+    v[i] = (uint32_t)i;
+  }
+}
+
+// one warp per sorted element; segment heads sum their segment in order
+__global__ void segment_sum(const uint32_t* keys, const uint32_t* pos, int n, const void* drows, be_dtype dd,
+                            int64_t D, float* dtable, float beta) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  if (warp > 0 && keys[warp - 1] == keys[warp]) return;
+  int end = warp + 1;
+  while (end < n && keys[end] == keys[warp]) ++end;
+  const int64_t row = keys[warp];
+  for (int64_t d = lane; d < D; d += 32) {
+    float acc = 0.f;
+    for (int j = warp; j < end; ++j) acc += ld(drows, (int64_t)pos[j] * D + d, dd);
+    float* o = dtable + row * D + d;
+    *o = acc + (beta != 0.f ? *o : 0.f);
+  }
+}
+}  // namespace
+
+size_t embedding_bwd_scratch(int64_t B) { return (size_t)B * 16 + 64; }
+
+void embedding_bwd(const void* drows, be_dtype dd, const int32_t* ids, int64_t B, int64_t D, float* dtable, int64_t V,
+                   float beta, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  BE_REQUIRE(scratch_bytes >= embedding_bwd_scratch(B), BE_E_ARG, "embedding_bwd: scratch too small");
+  BE_REQUIRE(B < (1LL << 31), BE_E_SHAPE, "embedding_bwd: batch too large");
+  if (beta == 0.f) {  // untouched rows get 0
+    BE_CHECK_CUDA(cudaMemsetAsync(dtable, 0, sizeof(float) * V * D, s));
+    beta = 1.f;        // segments now accumulate onto zeros
+  }
+  if (B == 0) return;
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(scratch);
+  uint32_t* v0 = k0 + B;
+  uint32_t* k1 = v0 + B;
+  uint32_t* v1 = k1 + B;
+  init_pairs<<<(int)std::min<int64_t>((B + 255) / 256, 1024), 256, 0, s>>>(ids, k0, v0, (int)B);
+  after_launch("embedding_init_pairs");
+  int bits = 1;
+  while ((1LL << bits) < V) ++bits;
+  const size_t smem = sizeof(uint32_t) * kBuckets * kSortThreads;
+  static bool attr = false;
+  if (!attr) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  for (int shift = 0; shift < bits; shift += kDigitBits) {
+    radix_pass<<<1, kSortThreads, smem, s>>>(k0, v0, k1, v1, (int)B, shift);
+    after_launch("embedding_radix_pass");
+    std::swap(k0, k1);
+    std::swap(v0, v1);
+  }
+  const int64_t threads = B * 32;
+  segment_sum<<<(int)((threads + 255) / 256), 256, 0, s>>>(k0, v0, (int)B, drows, dd, D, dtable, beta);
+  after_launch("embedding_segment_sum");
+}
+
+}}  // namespace be::k

@@ -1,0 +1,607 @@
+// gemm_sm100.cu — persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+// Serves every dense contraction on the hot path:
+// Linear fwd (Y = X·W, Listing 1), dgrad (dX = dY·Wᵀ) and wgrad
+// (dW = Xᵀ·dY) of Linear and of convolutions, with operand majorness
+// chosen at run time so none of the three needs a transpose kernel
+// (tcgen05 accepts MN-major bf16/tf32 operands).
+//
+//   warp 0 (one lane) : TMA producer — cp.async.bulk.tensor into a ring of
+//                       SW128-swizzled smem stages, mbarrier complete_tx
+//   warp 1 (one lane) : MMA issuer — tcgen05.mma (M=128, N=BN, K=16|8) into a
+//                       double-buffered TMEM accumulator, tcgen05.commit frees
+//                       smem stages / signals the epilogue
+//   warp 2            : TMEM allocator
+//   warps 4..7        : epilogue — tcgen05.ld 32x32b rows, bias / ReLU /
+//                       beta-accumulate / fp32→bf16 (RN-even), vector stores
+//
+// Precision: kind::f16 with bf16 operands, or "3xTF32" for the fp32 path:
+// operands pre-split into tf32 hi = rna(x), lo = rna(x − hi) and
+// D = Ahi·Bhi + Ahi·Blo + Alo·Bhi accumulated in fp32 TMEM (SURVEY §8(c)
+// reading 12).  Shapes TMA cannot describe (global row stride not a multiple
+// of 16 B) run a SIMT tile kernel instead (still on the GPU; counted).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.h"
+#include "runtime.h"
+#include "sm100.cuh"
+
+namespace be { namespace k {
+
+namespace {
+std::atomic<uint64_t> g_tc_calls{0}, g_simt_calls{0};
+
+constexpr int BM = 128;
+constexpr int kThreads = 256;
+
+struct __align__(64) GemmParams {
+  CUtensorMap ta[2];
+  CUtensorMap tb[2];
+  int M, N, K;
+  int a_kmajor, b_kmajor;
+  int tiles_m, tiles_n;
+  int splits, kb_per_split;   // split-K: tile index t → (split, tm, tn); split s covers k-blocks [s·kps, (s+1)·kps)
+  long long split_stride;     // elements between split partial slabs (fp32 workspace)
+  void* D;
+  long long ldd;
+  int d_f32;
+  float beta;
+  const float* bias;
+  int act;
+};
+
+template <int BN, bool X3>
+struct Cfg {
+  static constexpr int ESIZE = X3 ? 4 : 2;
+  static constexpr int BK = 128 / ESIZE;           // one 128-B swizzle row of K
+  static constexpr int UMMA_K = X3 ? 8 : 16;
+  static constexpr int NOPS = X3 ? 2 : 1;          // hi (+ lo)
+  static constexpr int A_BYTES = BM * 128;         // BM rows x 128 B
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int CH = 128 / ESIZE;           // MN elements per 128-B chunk
+};
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
+  return __uint_as_float(((uint32_t)b) << 16);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // RN-even (cvt.rn.bf16x2.f32)
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, bool X3>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN, X3>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
+    if (X3) { sm100::tma_prefetch(&p.ta[1]); sm100::tma_prefetch(&p.tb[1]); }
+  }
+  if (warp == 2) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int mn_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = mn_tiles * p.splits;
+  const int kblocks_total = (p.K + C::BK - 1) / C::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer =====================
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mn = t % mn_tiles, sp = t / mn_tiles;
+        const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
+        const int m0 = tm * BM, n0 = tn * BN;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* sbase = smem + stage * C::STAGE_BYTES;
+          const int k0 = kb * C::BK;
+#pragma unroll
+          for (int op = 0; op < C::NOPS; ++op) {
+            uint8_t* sa = sbase + op * (C::A_BYTES + C::B_BYTES);
+            uint8_t* sb = sa + C::A_BYTES;
+            if (p.a_kmajor) {
+              sm100::tma_load_2d(&p.ta[op], &full[stage], sa, k0, m0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / C::CH; ++j)
+                sm100::tma_load_2d(&p.ta[op], &full[stage], sa + j * C::BK * 128, m0 + j * C::CH, k0);
+            }
+            if (p.b_kmajor) {
+              sm100::tma_load_2d(&p.tb[op], &full[stage], sb, k0, n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / C::CH; ++j)
+                sm100::tma_load_2d(&p.tb[op], &full[stage], sb + j * C::BK * 128, n0 + j * C::CH, k0);
+            }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer =====================
+      const uint32_t idesc = sm100::make_idesc(X3 ? 2u : 1u, BM, BN, p.a_kmajor ? 0 : 1, p.b_kmajor ? 0 : 1);
+      // descriptor geometry
+      const uint32_t a_lbo = p.a_kmajor ? 16u : (uint32_t)(C::BK * 128);
+      const uint32_t b_lbo = p.b_kmajor ? 16u : (uint32_t)(C::BK * 128);
+      const uint32_t a_kstep = p.a_kmajor ? 32u : (uint32_t)(C::UMMA_K * 128);
+      const uint32_t b_kstep = p.b_kmajor ? 32u : (uint32_t)(C::UMMA_K * 128);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int sp = t / mn_tiles;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sbase = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
+            const uint32_t en = ((kb - kb0) | kk) ? 1u : 0u;
+            const uint32_t sa0 = sbase, sb0 = sbase + C::A_BYTES;
+            const uint64_t ad = sm100::make_sw128_desc(sa0 + kk * a_kstep, a_lbo, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb0 + kk * b_kstep, b_lbo, 1024);
+            if (X3) {
+              const uint32_t sa1 = sbase + C::A_BYTES + C::B_BYTES, sb1 = sa1 + C::A_BYTES;
+              const uint64_t ad1 = sm100::make_sw128_desc(sa1 + kk * a_kstep, a_lbo, 1024);
+              const uint64_t bd1 = sm100::make_sw128_desc(sb1 + kk * b_kstep, b_lbo, 1024);
+              sm100::mma_tf32(d_tmem, ad1, bd, idesc, en);   // lo·hi
+              sm100::mma_tf32(d_tmem, ad, bd1, idesc, 1u);   // hi·lo
+              sm100::mma_tf32(d_tmem, ad, bd, idesc, 1u);    // hi·hi
+            } else {
+              sm100::mma_bf16(d_tmem, ad, bd, idesc, en);
+            }
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int ew = warp - 4;  // == warp % 4 → TMEM lanes [32*ew, 32*ew+32)
+    int acc = 0; uint32_t acc_phase = 0;
+    const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int mn = t % mn_tiles, sp = t / mn_tiles;
+      const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
+      char* Dbase = reinterpret_cast<char*>(p.D) + (long long)sp * p.split_stride * 4;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = tm * BM + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int col0 = tn * BN + c0;
+        if (col0 >= p.N) break;  // warp-uniform
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        if (!row_ok) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int ncol = min(32, p.N - col0);
+        if (p.bias) {
+          if (ncol == 32 && (reinterpret_cast<uintptr_t>(p.bias + col0) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+          } else {
+            for (int j = 0; j < ncol; ++j) v[j] += __ldg(p.bias + col0 + j);
+          }
+        }
+        if (p.act == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+        }
+        if (p.d_f32) {
+          float* dst = reinterpret_cast<float*>(Dbase) + (long long)row * p.ldd + col0;
+          if (ncol == 32 && vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              if (p.beta != 0.f) {
+                float4 old = *reinterpret_cast<const float4*>(dst + j);
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              *reinterpret_cast<float4*>(dst + j) = o;
+            }
+          } else {
+            for (int j = 0; j < ncol; ++j) dst[j] = v[j] + (p.beta != 0.f ? dst[j] : 0.f);
+          }
+        } else {
+          uint16_t* dst = reinterpret_cast<uint16_t*>(Dbase) + (long long)row * p.ldd + col0;
+          if (ncol == 32 && vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              if (p.beta != 0.f) {
+                uint4 old = *reinterpret_cast<const uint4*>(dst + j);
+                const uint16_t* o16 = reinterpret_cast<const uint16_t*>(&old);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[j + q] += bf16_bits_to_f32(o16[q]);
+              }
+              uint4 o;
+              o.x = pack_bf16x2(v[j], v[j + 1]); o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+              o.z = pack_bf16x2(v[j + 4], v[j + 5]); o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+              *reinterpret_cast<uint4*>(dst + j) = o;
+            }
+          } else {
+            for (int j = 0; j < ncol; ++j) {
+              float x = v[j] + (p.beta != 0.f ? bf16_bits_to_f32(dst[j]) : 0.f);
+              __nv_bfloat16 h = __float2bfloat16_rn(x);
+              dst[j] = *reinterpret_cast<uint16_t*>(&h);
+            }
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- SIMT path
+// 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
+template <typename TA>
+__device__ __forceinline__ float ldv(const TA* p, long long i) {
+  if constexpr (sizeof(TA) == 2) return bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(p)[i]);
+  else return reinterpret_cast<const float*>(p)[i];
+}
+template <typename TA>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, const TA* A, long long lda, int akm,
+                                                       const TA* B, long long ldb, int bkm, void* D, long long ldd,
+                                                       int d_f32, float beta, const float* bias, int act) {
+  __shared__ float As[16][64 + 1];
+  __shared__ float Bs[16][64 + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      int kk = i / 64, mm = i % 64;
+      int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? ldv(A, akm ? (long long)m * lda + k : (long long)k * lda + m) : 0.f;
+      int n = n0 + mm;
+      Bs[kk][mm] = (n < N && k < K) ? ldv(B, bkm ? (long long)n * ldb + k : (long long)k * ldb + n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j] + (bias ? bias[n] : 0.f);
+      if (act == 1) v = fmaxf(v, 0.f);
+      if (d_f32) {
+        float* d = reinterpret_cast<float*>(D) + (long long)m * ldd + n;
+        *d = v + (beta != 0.f ? *d : 0.f);
+      } else {
+        uint16_t* d = reinterpret_cast<uint16_t*>(D) + (long long)m * ldd + n;
+        float x = v + (beta != 0.f ? bf16_bits_to_f32(*d) : 0.f);
+        __nv_bfloat16 h = __float2bfloat16_rn(x);
+        *d = *reinterpret_cast<uint16_t*>(&h);
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, void* D, long long ldd,
+                              int d_f32, float beta, const float* bias, int act) {
+  const long long total = (long long)M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int s = 0; s < splits; ++s) v += ws[(long long)s * total + i];
+    const int m = (int)(i / N), n = (int)(i % N);
+    if (bias) v += bias[n];
+    if (act == 1) v = fmaxf(v, 0.f);
+    if (d_f32) {
+      float* d = reinterpret_cast<float*>(D) + (long long)m * ldd + n;
+      *d = v + (beta != 0.f ? *d : 0.f);
+    } else {
+      uint16_t* d = reinterpret_cast<uint16_t*>(D) + (long long)m * ldd + n;
+      float x = v + (beta != 0.f ? bf16_bits_to_f32(*d) : 0.f);
+      __nv_bfloat16 h = __float2bfloat16_rn(x);
+      *d = *reinterpret_cast<uint16_t*>(&h);
+    }
+  }
+}
+
+// tf32 split into K-major hi/lo operands: out[mn, k] (ld2) from x (K-major
+// x[mn*ldx + k] or MN-major x[k*ldx + mn]); 32x32 smem tiles keep both the
+// read and the write coalesced.
+__device__ __forceinline__ void tf32_split(float v, float& h, float& l) {
+  uint32_t hb, lb;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+  const float r = v - __uint_as_float(hb);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(r));
+  h = __uint_as_float(hb);
+  l = __uint_as_float(lb);
+}
+__global__ void split_kmajor_kernel(const float* __restrict__ x, long long ldx, int src_kmajor, int MN, int K,
+                                    float* __restrict__ hi, float* __restrict__ lo, long long ld2) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.x * 32, mn0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int j = ty; j < 32; j += 8) {
+    if (src_kmajor) {
+      const int mn = mn0 + j, k = k0 + tx;
+      tile[j][tx] = (mn < MN && k < K) ? x[(long long)mn * ldx + k] : 0.f;
+    } else {
+      const int k = k0 + j, mn = mn0 + tx;
+      tile[tx][j] = (mn < MN && k < K) ? x[(long long)k * ldx + mn] : 0.f;
+    }
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int mn = mn0 + j, k = k0 + tx;
+    if (mn < MN && k < ld2) {
+      float h, l;
+      tf32_split(tile[j][tx], h, l);
+      hi[(long long)mn * ld2 + k] = h;
+      lo[(long long)mn * ld2 + k] = l;
+    }
+  }
+}
+void split_tf32_kmajor(const float* x, long long ldx, bool src_kmajor, int MN, int K, float* hi, float* lo,
+                       long long ld2, cudaStream_t s) {
+  dim3 grid((unsigned)((ld2 + 31) / 32), (unsigned)((MN + 31) / 32));
+  split_kmajor_kernel<<<grid, dim3(32, 8), 0, s>>>(x, ldx, src_kmajor ? 1 : 0, MN, K, hi, lo, ld2);
+  after_launch("split_tf32_kmajor");
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(f);
+  });
+  return fn;
+}
+
+// 2-D map over a row-major matrix of `rows` x `cols` (cols contiguous), box
+// {box_c, box_r}, SW128.
+void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint64_t rows, uint64_t ld,
+               uint32_t box_c, uint32_t box_r) {
+  EncodeFn enc = get_encode();
+  BE_REQUIRE(enc != nullptr, BE_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const size_t es = dtype_size(dt);
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {box_c, box_r};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt == BE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BE_REQUIRE(r == CUDA_SUCCESS, BE_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+// Operand map: logical [MN, K]; kmajor → stored [MN rows, K cols]; else [K rows, MN cols].
+void encode_operand(CUtensorMap* m, const void* ptr, be_dtype dt, int MN, int K, int64_t ld, bool kmajor,
+                    int box_mn, int bk) {
+  const uint32_t ch = 128 / dtype_size(dt);
+  if (kmajor) encode_2d(m, ptr, dt, K, MN, ld, bk, box_mn);
+  else encode_2d(m, ptr, dt, MN, K, ld, ch, bk);
+}
+
+bool tma_ok(const void* p, int64_t ld, be_dtype dt) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * (int64_t)dtype_size(dt)) % 16 == 0;
+}
+
+template <int BN, bool X3>
+void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo,
+               cudaStream_t s) {
+  using C = Cfg<BN, X3>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const be_dtype dt = X3 ? BE_F32 : BE_BF16;
+  encode_operand(&p.ta[0], a_hi, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
+  encode_operand(&p.tb[0], b_hi, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
+  if (X3) {
+    encode_operand(&p.ta[1], a_lo, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
+    encode_operand(&p.tb[1], b_lo, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
+  }
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.a_kmajor = g.a_kmajor; p.b_kmajor = g.b_kmajor;
+  p.tiles_m = (g.M + BM - 1) / BM;
+  p.tiles_n = (g.N + BN - 1) / BN;
+  const int sms = ctx().num_sms;
+  const int mn = p.tiles_m * p.tiles_n;
+  const int kblocks = (g.K + C::BK - 1) / C::BK;
+  // split-K when the output tile grid cannot fill the machine (e.g. conv
+  // wgrad: M·N tiny, K = N·P·Q up to 3.2 M); fp32 partials are summed in a
+  // fixed order by splitk_reduce → deterministic.
+  int splits = 1;
+  if (mn * 2 <= sms && kblocks >= 8) splits = std::max(1, std::min(sms / mn, kblocks / 4));
+  int kps = (kblocks + splits - 1) / splits;
+  splits = (kblocks + kps - 1) / kps;
+  p.splits = splits;
+  p.kb_per_split = kps;
+  Block* ws = nullptr;
+  if (splits > 1) {
+    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M * g.N, s);
+    p.D = ws->ptr; p.ldd = g.N; p.d_f32 = 1; p.beta = 0.f; p.bias = nullptr; p.act = 0;
+    p.split_stride = (long long)g.M * g.N;
+  } else {
+    p.D = g.D; p.ldd = g.ldd; p.d_f32 = g.d == BE_F32; p.beta = g.beta; p.bias = g.bias; p.act = g.act;
+    p.split_stride = 0;
+  }
+  const int grid = std::min(mn * splits, sms);
+  const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
+  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
+  const int pidx = prof_begin(X3 ? "gemm_tc_3xtf32" : "gemm_tc_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
+  gemm_tc_kernel<BN, X3><<<grid, kThreads, C::SMEM, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("gemm_tc");
+  if (ws) {
+    const long long total = (long long)g.M * g.N;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, g.M, g.N, g.D, g.ldd,
+                                         g.d == BE_F32, g.beta, g.bias, g.act);
+    after_launch("gemm_splitk_reduce");
+    ctx().alloc.free(ws);
+  }
+}
+
+int pick_bn(int M, int N, int sms, bool x3) {
+  // Largest BN whose wave efficiency is within 10% of the best candidate.
+  const int cands_bf16[3] = {256, 128, 64};
+  const int cands_x3[2] = {128, 64};
+  const int* c = x3 ? cands_x3 : cands_bf16;
+  const int nc = x3 ? 2 : 3;
+  double best = 0; int best_bn = c[nc - 1];
+  double eff[3];
+  for (int i = 0; i < nc; ++i) {
+    long tiles = (long)((M + BM - 1) / BM) * ((N + c[i] - 1) / c[i]);
+    long waves = (tiles + sms - 1) / sms;
+    double useful = (double)M * N;
+    double issued = (double)waves * sms * BM * c[i];
+    eff[i] = useful / issued;
+    if (eff[i] > best) best = eff[i];
+  }
+  for (int i = 0; i < nc; ++i)
+    if (eff[i] >= 0.9 * best) { best_bn = c[i]; break; }
+  return best_bn;
+}
+
+}  // namespace
+
+uint64_t gemm_tcgen05_calls() { return g_tc_calls.load(); }
+uint64_t gemm_simt_calls() { return g_simt_calls.load(); }
+
+const char* gemm(const GemmDesc& g, cudaStream_t s) {
+  BE_REQUIRE(g.ab == BE_BF16 || g.ab == BE_F32, BE_E_DTYPE, "gemm: operands must be bf16 or f32");
+  BE_REQUIRE(g.d == BE_BF16 || g.d == BE_F32, BE_E_DTYPE, "gemm: output must be bf16 or f32");
+  if (g.M == 0 || g.N == 0) return "empty";
+  if (g.K == 0) {  // D = beta*D + bias (+act): handled by SIMT kernel with K=0 loop
+  }
+  const bool x3 = g.ab == BE_F32;
+  const bool tc = g.K > 0 && tma_ok(g.A, g.lda, g.ab) && tma_ok(g.B, g.ldb, g.ab);
+  if (tc) {
+    g_tc_calls++;
+    const void *ahi = g.A, *alo = nullptr, *bhi = g.B, *blo = nullptr;
+    Block* tmp = nullptr;
+    GemmDesc gx = g;
+    if (x3) {
+      // Split both operands into tf32 hi = rna(x), lo = rna(x − hi).  The
+      // split pass also writes every operand K-major (transposing MN-major
+      // ones): kind::tf32 with MN-major operands needs the 128B_BASE32B
+      // swizzle atom, which this kernel does not implement.
+      const int64_t lda2 = (g.K + 3) / 4 * 4, ldb2 = lda2;
+      const int64_t na = (int64_t)g.M * lda2, nb = (int64_t)g.N * ldb2;
+      size_t bytes = (size_t)(2 * na + 2 * nb) * 4 + 64;
+      tmp = ctx().alloc.allocate(bytes, s);
+      float* base = reinterpret_cast<float*>(tmp->ptr);
+      float *ah = base, *al = ah + na, *bh = al + na, *bl = bh + nb;
+      split_tf32_kmajor(reinterpret_cast<const float*>(g.A), g.lda, g.a_kmajor, g.M, g.K, ah, al, lda2, s);
+      split_tf32_kmajor(reinterpret_cast<const float*>(g.B), g.ldb, g.b_kmajor, g.N, g.K, bh, bl, ldb2, s);
+      ahi = ah; alo = al; bhi = bh; blo = bl;
+      gx.lda = lda2; gx.ldb = ldb2; gx.a_kmajor = true; gx.b_kmajor = true;
+    }
+    const int bn = pick_bn(g.M, g.N, ctx().num_sms, x3);
+    if (x3) {
+      if (bn == 128) launch_tc<128, true>(gx, ahi, alo, bhi, blo, s);
+      else launch_tc<64, true>(gx, ahi, alo, bhi, blo, s);
+    } else {
+      if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
+      else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
+      else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
+    }
+    if (tmp) ctx().alloc.free(tmp);  // stream-ordered reuse is safe
+    return "tcgen05";
+  }
+  g_simt_calls++;
+  dim3 grid((g.N + 63) / 64, (g.M + 63) / 64);
+  const double es = g.ab == BE_F32 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
+  const int pidx = prof_begin("gemm_simt", 2.0 * g.M * g.N * g.K,
+                              ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds, g.M, g.N, g.K, s);
+  struct ProfEnd { int i; cudaStream_t s; ~ProfEnd() { prof_end(i, s); } } pe{pidx, s};
+  if (g.ab == BE_BF16)
+    gemm_simt_kernel<uint16_t><<<grid, 256, 0, s>>>(g.M, g.N, g.K, (const uint16_t*)g.A, g.lda, g.a_kmajor,
+                                                    (const uint16_t*)g.B, g.ldb, g.b_kmajor, g.D, g.ldd,
+                                                    g.d == BE_F32, g.beta, g.bias, g.act);
+  else
+    gemm_simt_kernel<float><<<grid, 256, 0, s>>>(g.M, g.N, g.K, (const float*)g.A, g.lda, g.a_kmajor,
+                                                 (const float*)g.B, g.ldb, g.b_kmajor, g.D, g.ldd, g.d == BE_F32,
+                                                 g.beta, g.bias, g.act);
+  after_launch("gemm_simt");
+  return "simt";
+}
+
+}}  // namespace be::k

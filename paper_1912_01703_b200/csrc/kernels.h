@@ -1,0 +1,115 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal API).
+// Every launcher enqueues on the given stream and returns immediately.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/be.h"
+
+namespace be { namespace k {
+
+// ------------------------------------------------------------------ GEMM
+// D[M,N] = act(A[M,K]·B[N,K]ᵀ + bias[N]) + beta·D   (fp32 accumulate)
+// A element (m,k) at A[m*lda + k] if a_kmajor else A[k*lda + m];
+// B element (n,k) at B[n*ldb + k] if b_kmajor else B[k*ldb + n].
+// ab = BE_BF16 (kind::f16) or BE_F32 (3xTF32 on kind::tf32).
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr; int64_t lda = 0; bool a_kmajor = true;
+  const void* B = nullptr; int64_t ldb = 0; bool b_kmajor = true;
+  be_dtype ab = BE_BF16;
+  void* D = nullptr; int64_t ldd = 0; be_dtype d = BE_F32;
+  float beta = 0.f;
+  const float* bias = nullptr;
+  int act = 0;  // 0 none, 1 relu
+};
+// Returns the name of the path taken ("tcgen05" or "simt").
+const char* gemm(const GemmDesc& g, cudaStream_t s);
+// Encode counters for tests/bench (which path ran).
+uint64_t gemm_tcgen05_calls();
+uint64_t gemm_simt_calls();
+
+// ------------------------------------------------------------------ pointwise
+void fill(void* x, int64_t n, be_dtype dt, double v, cudaStream_t s);
+void cast(const void* x, be_dtype xd, void* y, be_dtype yd, int64_t n, cudaStream_t s);
+void split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s);
+void relu_fwd(const void* x, void* y, int64_t n, be_dtype dt, cudaStream_t s);
+// dx (+)= dy * [y > 0]
+void relu_bwd(const void* dy, const void* y, void* dx, int64_t n, be_dtype dt, float beta, cudaStream_t s);
+// y = a + b with b broadcast: general strided (rank<=6) over out shape
+struct BcastDesc {
+  int rank;
+  int64_t shape[6];
+  int64_t sa[6], sb[6];  // element strides of a,b in out index space (0 = broadcast)
+};
+void add_bcast(const void* a, const void* b, void* y, const BcastDesc& d, be_dtype dt, int act, cudaStream_t s);
+void add_same(const void* a, const void* b, void* y, int64_t n, be_dtype dt, int act, cudaStream_t s);
+void mul_same(const void* a, const void* b, void* y, int64_t n, be_dtype dt, cudaStream_t s);
+// y (+)= a * b
+void mul_acc(const void* a, const void* b, void* y, int64_t n, be_dtype dt, float beta, cudaStream_t s);
+// y = alpha*x + beta*y   (accumulation helper; dtypes may differ: x dt_x, y dt_y)
+void axpby(const void* x, be_dtype xd, void* y, be_dtype yd, int64_t n, float alpha, float beta, cudaStream_t s);
+// y = x * (*scalar_dev)
+void scale_dev(const void* x, be_dtype xd, void* y, be_dtype yd, int64_t n, const float* scalar, cudaStream_t s);
+// out[c] (+)= Σ_r x[r, c]  (x [rows, cols] row-major, dt), fp32 out, deterministic
+void colsum(const void* x, int64_t rows, int64_t cols, be_dtype dt, float* out, float beta, cudaStream_t s);
+// fused ReLU-backward + column sum: dz = dy*[y>0] (dz may alias dy), db (+)= Σ_r dz
+void relu_bwd_colsum(const void* dy, const void* y, void* dz, int64_t rows, int64_t cols, be_dtype dt,
+                     float* db, float db_beta, int act, cudaStream_t s);
+// sum of all elements into out[0] (fp32), scale applied (mean)
+void reduce_sum(const void* x, int64_t n, be_dtype dt, float* out, float scale, float* scratch, cudaStream_t s);
+void broadcast_scalar(const float* g, void* dx, be_dtype dt, int64_t n, float scale, float beta, cudaStream_t s);
+
+// ------------------------------------------------------------------ losses
+// loss_out[0] = mean_i (LSE(z_i) − z_i[y_i]); dz = (softmax − onehot)/B written in dz_dt;
+// argmax (first max) to argmax_out (may be null). row_loss: scratch [B] fp32.
+void softmax_xent(const void* z, be_dtype zd, int64_t ldz, const int32_t* y, int64_t B, int64_t C,
+                  float* row_loss, float* loss_out, void* dz, be_dtype dzd, int32_t* argmax_out,
+                  cudaStream_t s);
+void bce_logits(const void* z, be_dtype zd, const int32_t* y, int64_t B, float* row_loss, float* loss_out,
+                void* dz, be_dtype dzd, cudaStream_t s);
+
+// ------------------------------------------------------------------ SGD
+struct SgdEntry {
+  float* p; const float* g; uint16_t* shadow; float* mom; int64_t n;
+};
+void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float wd, float scale,
+               cudaStream_t s);
+
+// ------------------------------------------------------------------ conv / pool / bn
+struct ConvGeom {
+  int N, H, W, C, K, R, S, stride, pad, P, Q;
+};
+// cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC
+void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s);
+// dx NHWC (+)= col2im(dcols)   (gather formulation, deterministic)
+void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtype dt, float beta, cudaStream_t s);
+void im2col_offsets(const ConvGeom& g, int64_t* out_dev, cudaStream_t s);
+void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s);
+void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g, be_dtype dt, float beta, cudaStream_t s);
+void avgpool_fwd(const void* x, void* y, int N, int HW, int C, be_dtype dt, cudaStream_t s);
+void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, float beta, cudaStream_t s);
+// BN train: stats per channel over rows (x as [rows, C]); mean/invstd fp32 [C]
+void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float* mean, float* invstd,
+              float* partial, float* run_mean, float* run_var, float momentum, cudaStream_t s);
+void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
+              const float* gamma, const float* beta, int act, cudaStream_t s);
+size_t bn_partial_floats(int64_t rows, int C);
+// backward: dgamma, dbeta (fp32, with beta-accumulate flags) and dx
+void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
+            const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta,
+            float gb_beta, float dx_beta, float* partial, cudaStream_t s);
+
+// ------------------------------------------------------------------ embedding
+void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,
+                   cudaStream_t s);
+// dtable (+)= scatter(ids, drows): deterministic via sort-by-id then segmented sum
+void embedding_bwd(const void* drows, be_dtype dd, const int32_t* ids, int64_t B, int64_t D, float* dtable,
+                   int64_t V, float beta, void* scratch, size_t scratch_bytes, cudaStream_t s);
+size_t embedding_bwd_scratch(int64_t B);
+void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t rows, void* y, be_dtype dt,
+                 cudaStream_t s);
+void slice_cols(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x, be_dtype dt,
+                float beta, cudaStream_t s);
+
+}}  // namespace be::k

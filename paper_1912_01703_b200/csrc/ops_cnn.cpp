@@ -1,0 +1,346 @@
+// ops_cnn.cpp — CNN / recommender operators: conv2d (as GEMMs on the tcgen05
+// kernel), max / global-average pooling, batch norm (train), embedding.
+//
+// Conv2d (Listing 1 `nn.Conv2d`): NHWC
+// activations x[N,H,W,C], KRSC weights w[K,R,S,C]:
+//   fwd    Y[M=NPQ, K]   = cols(x)[M, RSC] · Wᵀ          (+bias, ReLU in the epilogue)
+//   wgrad  dW[K, RSC]    = dYᵀ[K, M] · cols(x)[M, RSC]   (split-K, fp32)
+//   dgrad  dcols[M, RSC] = dY[M, K] · W[K, RSC];  dx = col2im(dcols)
+// 1×1 / stride-1 / pad-0 convolutions use x itself as the column matrix
+// (no im2col, no col2im).  Operand majorness is chosen per GEMM so no
+// transpose kernel ever runs.
+#include "ops_common.h"
+
+namespace be {
+
+static k::ConvGeom conv_geom(const Tensor* x, const Tensor* w, int stride, int pad) {
+  k::ConvGeom g;
+  g.N = (int)x->shape[0]; g.H = (int)x->shape[1]; g.W = (int)x->shape[2]; g.C = (int)x->shape[3];
+  g.K = (int)w->shape[0]; g.R = (int)w->shape[1]; g.S = (int)w->shape[2];
+  g.stride = stride; g.pad = pad;
+  g.P = (g.H + 2 * pad - g.R) / stride + 1;
+  g.Q = (g.W + 2 * pad - g.S) / stride + 1;
+  return g;
+}
+static bool is_pointwise(const k::ConvGeom& g) { return g.R == 1 && g.S == 1 && g.stride == 1 && g.pad == 0; }
+static int64_t cols_ld(int64_t rsc, be_dtype dt) {
+  const int64_t q = dt == BE_BF16 ? 8 : 4;  // 16-byte rows for TMA
+  return (rsc + q - 1) / q * q;
+}
+
+// Column matrix of x (im2col or x itself); returns pointer + ld.
+static TRef make_cols(Tensor* x, const k::ConvGeom& g, int64_t* ld) {
+  const int64_t RSC = (int64_t)g.R * g.S * g.C;
+  if (is_pointwise(g)) { *ld = g.C; return TRef(x, false); }
+  const int64_t M = (int64_t)g.N * g.P * g.Q;
+  *ld = cols_ld(RSC, x->dtype);
+  TRef cols = new_tensor({M, *ld}, x->dtype);
+  k::im2col(x->data(), cols->data(), *ld, g, x->dtype, ctx().stream);
+  return cols;
+}
+
+static void vjp_conv(Node* n, GradSink& sink) {
+  cudaStream_t s = ctx().stream;
+  TRef hx, hw, hy;
+  Tensor* x = unpack(n, 0, hx);
+  Tensor* w = unpack(n, 1, hw);
+  Tensor* y = unpack(n, 2, hy);
+  const int stride = (int)n->iattr[0], pad = (int)n->iattr[1], act = (int)n->iattr[2];
+  const bool has_b = n->iattr[3] != 0;
+  const k::ConvGeom g = conv_geom(x, w, stride, pad);
+  const be_dtype opd = x->dtype;
+  const int64_t M = (int64_t)g.N * g.P * g.Q, K = g.K, RSC = (int64_t)g.R * g.S * g.C;
+  TRef gz = contiguous_like(sink.upstream[0], opd);
+  TRef dz;
+  if (act) dz = new_tensor({M, K}, opd);
+  else dz = gz;
+  if (has_b && sink.needs(2)) {
+    float bb;
+    Tensor* db = sink.dest(2, &bb);
+    k::relu_bwd_colsum(gz->data(), act ? y->data() : nullptr, dz->data(), M, K, opd, db->ptr<float>(), bb, act, s);
+    sink.commit(2);
+  } else if (act) {
+    k::relu_bwd(gz->data(), y->data(), dz->data(), M * K, opd, 0.f, s);
+  }
+  gz = TRef();
+  if (sink.needs(1)) {  // dW[K, RSC] = dzᵀ · cols
+    int64_t ldc;
+    TRef cols = make_cols(x, g, &ldc);
+    float bw;
+    Tensor* dw = sink.dest(1, &bw);
+    k::GemmDesc gd;
+    gd.M = (int)K; gd.N = (int)RSC; gd.K = (int)M;
+    gd.A = dz->data(); gd.lda = K; gd.a_kmajor = false;
+    gd.B = cols->data(); gd.ldb = ldc; gd.b_kmajor = false;
+    gd.ab = opd; gd.D = dw->data(); gd.ldd = RSC; gd.d = dw->dtype; gd.beta = bw;
+    k::gemm(gd, s);
+    sink.commit(1);
+  }
+  if (sink.needs(0)) {
+    float bx;
+    Tensor* dx = sink.dest(0, &bx);
+    BE_REQUIRE(dx->dtype == opd, BE_E_DTYPE, "conv dgrad dtype");
+    k::GemmDesc gd;
+    gd.M = (int)M; gd.N = (int)RSC; gd.K = (int)K;
+    gd.A = dz->data(); gd.lda = K; gd.a_kmajor = true;
+    gd.B = w->data(); gd.ldb = RSC; gd.b_kmajor = false;
+    gd.ab = opd;
+    if (is_pointwise(g)) {
+      gd.D = dx->data(); gd.ldd = RSC; gd.d = opd; gd.beta = bx;
+      k::gemm(gd, s);
+    } else {
+      const int64_t ldc = cols_ld(RSC, opd);
+      TRef dcols = new_tensor({M, ldc}, opd);
+      gd.D = dcols->data(); gd.ldd = ldc; gd.d = opd; gd.beta = 0.f;
+      k::gemm(gd, s);
+      k::col2im(dcols->data(), ldc, dx->data(), g, opd, bx, s);
+    }
+    sink.commit(0);
+  }
+}
+
+static void op_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor* out) {
+  BE_REQUIRE(n_in == 2 || n_in == 3, BE_E_ARG, "conv2d: x, w[, b]");
+  BE_REQUIRE(attrs, BE_E_ARG, "conv2d: be_conv_attrs required");
+  const be_conv_attrs a = *reinterpret_cast<const be_conv_attrs*>(attrs);
+  Tensor* x0 = check_handle(in[0]);
+  Tensor* w0 = check_handle(in[1]);
+  Tensor* b = n_in == 3 && in[2] ? check_handle(in[2]) : nullptr;
+  BE_REQUIRE(x0->rank == 4 && w0->rank == 4, BE_E_SHAPE, "conv2d: x NHWC[N,H,W,C], w KRSC[K,R,S,C]");
+  BE_REQUIRE(x0->shape[3] == w0->shape[3], BE_E_SHAPE, "conv2d: channel counts differ");
+  BE_REQUIRE(a.stride >= 1 && a.pad >= 0, BE_E_ARG, "conv2d: stride >= 1, pad >= 0");
+  BE_REQUIRE(x0->shape[1] + 2 * a.pad >= w0->shape[1] && x0->shape[2] + 2 * a.pad >= w0->shape[2], BE_E_SHAPE,
+             "conv2d: kernel larger than padded input");
+  BE_REQUIRE(!b || (b->rank == 1 && b->shape[0] == w0->shape[0] && b->dtype == BE_F32), BE_E_SHAPE,
+             "conv2d: bias f32 [K]");
+  BE_REQUIRE(x0->is_contiguous(), BE_E_NONCONTIG, "conv2d: contiguous input");
+  TRef x = act_operand(x0);
+  Tensor* w = weight_operand(w0);
+  const k::ConvGeom g = conv_geom(x.get(), w, a.stride, a.pad);
+  const int64_t M = (int64_t)g.N * g.P * g.Q, RSC = (int64_t)g.R * g.S * g.C;
+  const be_dtype od = (a.out_f32 || ctx().compute == BE_F32) ? BE_F32 : BE_BF16;
+  TRef y = new_tensor({g.N, g.P, g.Q, g.K}, od);
+  {
+    int64_t ldc;
+    TRef cols = make_cols(x.get(), g, &ldc);
+    k::GemmDesc gd;
+    gd.M = (int)M; gd.N = g.K; gd.K = (int)RSC;
+    gd.A = cols->data(); gd.lda = ldc; gd.a_kmajor = true;
+    gd.B = w->data(); gd.ldb = RSC; gd.b_kmajor = true;
+    gd.ab = x->dtype; gd.D = y->data(); gd.ldd = g.K; gd.d = od;
+    gd.bias = b ? b->ptr<float>() : nullptr; gd.act = a.act;
+    k::gemm(gd, ctx().stream);
+  }
+  Node* n = new_node("conv2d", BE_OP_CONV2D, vjp_conv, {x.get(), w0, b});
+  if (n) {
+    save(n, x.get());
+    save(n, w);
+    save(n, a.act ? y.get() : nullptr);
+    n->iattr[0] = a.stride; n->iattr[1] = a.pad; n->iattr[2] = a.act; n->iattr[3] = b != nullptr;
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
+// ------------------------------------------------------------------ pooling
+static void vjp_maxpool(Node* n, GradSink& sink) {
+  TRef ham;
+  Tensor* am = unpack(n, 0, ham);
+  k::ConvGeom g;
+  g.N = (int)n->iattr[3]; g.H = (int)n->iattr[4]; g.W = (int)n->iattr[5]; g.C = (int)n->iattr[6];
+  g.R = g.S = (int)n->iattr[0]; g.stride = (int)n->iattr[1]; g.pad = (int)n->iattr[2];
+  g.P = (g.H + 2 * g.pad - g.R) / g.stride + 1;
+  g.Q = (g.W + 2 * g.pad - g.S) / g.stride + 1;
+  g.K = g.C;
+  float beta;
+  Tensor* dx = sink.dest(0, &beta);
+  if (!dx) return;
+  TRef gz = contiguous_like(sink.upstream[0], dx->dtype);
+  k::maxpool_bwd(gz->data(), am->ptr<uint8_t>(), dx->data(), g, dx->dtype, beta, ctx().stream);
+  sink.commit(0);
+}
+static void op_maxpool(const be_tensor* in, int n_in, const void* attrs, be_tensor* out, int n_out) {
+  BE_REQUIRE(n_in == 1 && attrs, BE_E_ARG, "maxpool2d: x + be_pool_attrs");
+  const be_pool_attrs a = *reinterpret_cast<const be_pool_attrs*>(attrs);
+  Tensor* x = check_handle(in[0]);
+  BE_REQUIRE(x->rank == 4 && x->is_contiguous(), BE_E_SHAPE, "maxpool2d: contiguous NHWC input");
+  BE_REQUIRE(a.k >= 1 && a.k * a.k <= 255 && a.stride >= 1 && a.pad >= 0 && a.pad <= a.k / 2, BE_E_ARG,
+             "maxpool2d: bad window");
+  k::ConvGeom g;
+  g.N = (int)x->shape[0]; g.H = (int)x->shape[1]; g.W = (int)x->shape[2]; g.C = (int)x->shape[3];
+  g.R = g.S = a.k; g.stride = a.stride; g.pad = a.pad; g.K = g.C;
+  g.P = (g.H + 2 * a.pad - a.k) / a.stride + 1;
+  g.Q = (g.W + 2 * a.pad - a.k) / a.stride + 1;
+  BE_REQUIRE(g.P > 0 && g.Q > 0, BE_E_SHAPE, "maxpool2d: window larger than input");
+  TRef y = new_tensor({g.N, g.P, g.Q, g.C}, x->dtype);
+  TRef am = new_tensor({g.N, g.P, g.Q, g.C}, BE_U8);
+  k::maxpool_fwd(x->data(), y->data(), am->ptr<uint8_t>(), g, x->dtype, ctx().stream);
+  Node* n = new_node("maxpool2d", BE_OP_MAXPOOL2D, vjp_maxpool, {x});
+  if (n) {
+    save(n, am.get());
+    n->iattr[0] = a.k; n->iattr[1] = a.stride; n->iattr[2] = a.pad;
+    n->iattr[3] = g.N; n->iattr[4] = g.H; n->iattr[5] = g.W; n->iattr[6] = g.C;
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+  if (n_out > 1) out[1] = reinterpret_cast<be_tensor>(am.release());
+}
+
+static void vjp_avgpool(Node* n, GradSink& sink) {
+  float beta;
+  Tensor* dx = sink.dest(0, &beta);
+  if (!dx) return;
+  TRef gz = contiguous_like(sink.upstream[0], dx->dtype);
+  const int N = (int)dx->shape[0], HW = (int)(dx->shape[1] * dx->shape[2]), C = (int)dx->shape[3];
+  k::avgpool_bwd(gz->data(), dx->data(), N, HW, C, dx->dtype, beta, ctx().stream);
+  sink.commit(0);
+}
+static void op_avgpool(const be_tensor* in, int n_in, be_tensor* out) {
+  BE_REQUIRE(n_in == 1, BE_E_ARG, "avgpool_global: 1 input");
+  Tensor* x = check_handle(in[0]);
+  BE_REQUIRE(x->rank == 4 && x->is_contiguous(), BE_E_SHAPE, "avgpool_global: contiguous NHWC");
+  const int N = (int)x->shape[0], HW = (int)(x->shape[1] * x->shape[2]), C = (int)x->shape[3];
+  BE_REQUIRE(HW > 0, BE_E_EMPTY_REDUCTION, "avgpool_global: empty plane");
+  TRef y = new_tensor({(int64_t)N, (int64_t)C}, x->dtype);
+  k::avgpool_fwd(x->data(), y->data(), N, HW, C, x->dtype, ctx().stream);
+  Node* n = new_node("avgpool_global", BE_OP_AVGPOOL_GLOBAL, vjp_avgpool, {x});
+  if (n) { set_output(n, y.get(), 0); finish_node(n); }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
+// ------------------------------------------------------------------ batch norm (train)
+static void vjp_bn(Node* n, GradSink& sink) {
+  cudaStream_t s = ctx().stream;
+  TRef hx, hmean, hinv, hg, hy;
+  Tensor* x = unpack(n, 0, hx);
+  Tensor* mean = unpack(n, 1, hmean);
+  Tensor* inv = unpack(n, 2, hinv);
+  Tensor* gamma = unpack(n, 3, hg);
+  Tensor* y = unpack(n, 4, hy);
+  const int act = (int)n->iattr[0];
+  const int C = (int)x->shape[3];
+  const int64_t rows = x->numel() / C;
+  TRef gz = contiguous_like(sink.upstream[0], x->dtype);
+  // dgamma / dbeta accumulate flags must agree: compute into temps when they differ
+  float bg = 0.f, bb = 0.f;
+  Tensor* dg = sink.needs(1) ? sink.dest(1, &bg) : nullptr;
+  Tensor* db = sink.needs(2) ? sink.dest(2, &bb) : nullptr;
+  TRef tg, tb;
+  float gb_beta = 0.f;
+  if (dg && db && bg == bb) gb_beta = bg;
+  else {
+    if (dg && bg != 0.f) { tg = new_tensor({C}, BE_F32); }
+    if (db && bb != 0.f) { tb = new_tensor({C}, BE_F32); }
+  }
+  TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+  float bx = 0.f;
+  Tensor* dx = sink.needs(0) ? sink.dest(0, &bx) : nullptr;
+  TRef dgs = dg ? TRef() : new_tensor({C}, BE_F32);
+  TRef dbs = db ? TRef() : new_tensor({C}, BE_F32);
+  float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
+  float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
+  k::bn_bwd(gz->data(), x->data(), act ? y->data() : nullptr, act, dx ? dx->data() : nullptr, rows, C, x->dtype,
+            mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s);
+  if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
+  if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
+  if (dx) sink.commit(0);
+  if (dg) sink.commit(1);
+  if (db) sink.commit(2);
+}
+static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* out) {
+  BE_REQUIRE(n_in == 3 || n_in == 5, BE_E_ARG, "batchnorm2d: x, gamma, beta[, running_mean, running_var]");
+  be_bn_attrs a{1e-5f, 0.1f, 0};
+  if (attrs) a = *reinterpret_cast<const be_bn_attrs*>(attrs);
+  Tensor* x = check_handle(in[0]);
+  Tensor* gamma = check_handle(in[1]);
+  Tensor* beta = check_handle(in[2]);
+  Tensor* rm = n_in == 5 && in[3] ? check_handle(in[3]) : nullptr;
+  Tensor* rv = n_in == 5 && in[4] ? check_handle(in[4]) : nullptr;
+  BE_REQUIRE(x->rank == 4 && x->is_contiguous(), BE_E_SHAPE, "batchnorm2d: contiguous NHWC input");
+  const int C = (int)x->shape[3];
+  const int64_t rows = x->numel() / std::max(C, 1);
+  BE_REQUIRE(rows > 0, BE_E_EMPTY_REDUCTION, "batchnorm2d: empty batch");
+  BE_REQUIRE(gamma->numel() == C && beta->numel() == C && gamma->dtype == BE_F32 && beta->dtype == BE_F32,
+             BE_E_SHAPE, "batchnorm2d: gamma/beta f32 [C]");
+  cudaStream_t s = ctx().stream;
+  TRef mean = new_tensor({C}, BE_F32), inv = new_tensor({C}, BE_F32);
+  TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+  k::bn_stats(x->data(), rows, C, x->dtype, a.eps, mean->ptr<float>(), inv->ptr<float>(), part->ptr<float>(),
+              rm ? rm->ptr<float>() : nullptr, rv ? rv->ptr<float>() : nullptr, a.momentum, s);
+  if (rm) rm->bump_version();
+  if (rv) rv->bump_version();
+  TRef y = new_tensor(x->shape, x->rank, x->dtype);
+  k::bn_apply(x->data(), y->data(), rows, C, x->dtype, mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(),
+              beta->ptr<float>(), a.act, s);
+  Node* n = new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
+  if (n) {
+    save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, a.act ? y.get() : nullptr);
+    n->iattr[0] = a.act;
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
+// ------------------------------------------------------------------ embedding
+static void vjp_embedding(Node* n, GradSink& sink) {
+  TRef hids;
+  Tensor* ids = unpack(n, 0, hids);
+  float beta;
+  Tensor* dt = sink.dest(0, &beta);
+  if (!dt) return;
+  TRef gz = contiguous_like(sink.upstream[0], sink.upstream[0]->dtype);
+  const int64_t B = ids->numel(), D = dt->shape[1], V = dt->shape[0];
+  const size_t sb = k::embedding_bwd_scratch(B);
+  TRef scratch = new_tensor({(int64_t)((sb + 3) / 4)}, BE_F32);
+  k::embedding_bwd(gz->data(), gz->dtype, ids->ptr<int32_t>(), B, D, dt->ptr<float>(), V, beta, scratch->data(), sb,
+                   ctx().stream);
+  sink.commit(0);
+}
+static void op_embedding(const be_tensor* in, int n_in, be_tensor* out) {
+  BE_REQUIRE(n_in == 2, BE_E_ARG, "embedding: table, ids");
+  Tensor* t = check_handle(in[0]);
+  Tensor* ids = check_handle(in[1]);
+  BE_REQUIRE(t->rank == 2 && t->dtype == BE_F32 && t->is_contiguous(), BE_E_SHAPE, "embedding: f32 table [V,D]");
+  BE_REQUIRE(ids->dtype == BE_I32 && ids->is_contiguous(), BE_E_DTYPE, "embedding: i32 ids");
+  const int64_t B = ids->numel(), D = t->shape[1];
+  const be_dtype od = ctx().compute;
+  TRef y = new_tensor({B, D}, od);
+  k::embedding_fwd(t->ptr<float>(), D, ids->ptr<int32_t>(), B, y->data(), od, ctx().stream);
+  Node* n = new_node("embedding", BE_OP_EMBEDDING, vjp_embedding, {t});
+  if (n) { save(n, ids); set_output(n, y.get(), 0); finish_node(n); }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
+void op_cnn(int op, const be_tensor* in, int n_in, const void* attrs, be_tensor* out, int n_out) {
+  switch (op) {
+    case BE_OP_CONV2D: op_conv(in, n_in, attrs, out); break;
+    case BE_OP_MAXPOOL2D: op_maxpool(in, n_in, attrs, out, n_out); break;
+    case BE_OP_AVGPOOL_GLOBAL: op_avgpool(in, n_in, out); break;
+    case BE_OP_BATCHNORM2D: op_bn(in, n_in, attrs, out); break;
+    case BE_OP_EMBEDDING: op_embedding(in, n_in, out); break;
+    default: fail(BE_E_UNSUPPORTED, "op_cnn: unknown op");
+  }
+}
+
+}  // namespace be
+
+using namespace be;
+extern "C" be_status be_debug_im2col_offsets(const int64_t* geom, int64_t* out) {
+  BE_API_BEGIN
+  BE_REQUIRE(ctx().inited, BE_E_NOT_INIT, "be_init() was not called");
+  k::ConvGeom g;
+  g.N = (int)geom[0]; g.C = (int)geom[1]; g.H = (int)geom[2]; g.W = (int)geom[3];
+  g.R = (int)geom[4]; g.S = (int)geom[5]; g.stride = (int)geom[6]; g.pad = (int)geom[7];
+  g.P = (g.H + 2 * g.pad - g.R) / g.stride + 1;
+  g.Q = (g.W + 2 * g.pad - g.S) / g.stride + 1;
+  g.K = 1;
+  const int64_t total = (int64_t)g.N * g.P * g.Q * g.R * g.S * g.C;
+  TRef buf = new_tensor({std::max<int64_t>(total, 1)}, BE_I64);
+  k::im2col_offsets(g, buf->ptr<int64_t>(), ctx().stream);
+  if (total) BE_CHECK_CUDA(cudaMemcpyAsync(out, buf->data(), total * 8, cudaMemcpyDeviceToHost, ctx().stream));
+  BE_CHECK_CUDA(cudaStreamSynchronize(ctx().stream));
+  BE_API_END
+}

@@ -1,0 +1,305 @@
+"""The benchmark networks of the paper's Table 1 written
+as eager user programs over the be_* ops (the "models are just Python
+programs" stance of PAPER.md:59-64).  Each op call launches device kernels
+and records itself on the tape; `loss.backward()` replays the tape in C++.
+
+Device layouts: activations NHWC, conv weights KRSC, Linear weights
+[in, out] (Listing 1).  The first conv's input channels are
+zero-padded to 8 so every GEMM operand row is 16-B aligned for TMA; the
+pad channels' weights start at 0 and stay 0 (their gradient is exactly 0).
+AlexNet's fc6 rows are stored in NHWC-flatten order.  `to_device_layout` /
+`to_logical_layout` convert parameters at upload / for comparison — host
+marshalling only, never on the step path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import api as T
+
+CPAD = 8  # first-layer channel padding
+
+
+def _lin_spec(name, i, o, bias=True):
+    s = [(name + ".w", (i, o), "normal", i)]
+    if bias:
+        s.append((name + ".b", (o,), "normal", i))
+    return s
+
+
+def _conv_spec(name, k, c, r, bias):
+    s = [(name + ".w", (k, c, r, r), "normal", c * r * r)]
+    if bias:
+        s.append((name + ".b", (k,), "normal", c * r * r))
+    return s
+
+
+def _bn_spec(name, c):
+    return [(name + ".g", (c,), "ones", 1), (name + ".b", (c,), "zeros", 1)]
+
+
+def images_to_device(x_nchw: np.ndarray, dtype="bf16", cpad=CPAD) -> T.Tensor:
+    """Logical NCHW float32 images → device NHWC with channels padded."""
+    N, C, H, W = x_nchw.shape
+    nhwc = np.zeros((N, H, W, max(C, cpad)), np.float32)
+    nhwc[..., :C] = x_nchw.transpose(0, 2, 3, 1)
+    return T.tensor(nhwc, dtype=dtype)
+
+
+class Model:
+    """Parameter registry in deterministic registration order."""
+
+    def __init__(self):
+        self.params: dict[str, T.Tensor] = {}
+        self.buffers: dict[str, T.Tensor] = {}
+
+    def param_specs(self):
+        raise NotImplementedError
+
+    def to_device_layout(self, name, a):
+        return a
+
+    def to_logical_layout(self, name, a):
+        return a
+
+    def load(self, logical: dict):
+        self.params = {}
+        for (name, shape, _, _) in self.param_specs():
+            self.params[name] = T.tensor(self.to_device_layout(name, np.asarray(logical[name], np.float32)),
+                                         requires_grad=True)
+        self.make_buffers()
+        return self
+
+    def make_buffers(self):
+        pass
+
+    def parameters(self):
+        return list(self.params.values())
+
+    def logical(self, name, device_array):
+        return self.to_logical_layout(name, device_array)
+
+
+# ---------------------------------------------------------------- MLP (C1, C2)
+class MLP(Model):
+    def __init__(self, sizes):
+        super().__init__()
+        self.sizes = tuple(sizes)
+
+    def param_specs(self):
+        s = []
+        for i in range(len(self.sizes) - 1):
+            s += _lin_spec(f"fc{i}", self.sizes[i], self.sizes[i + 1])
+        return s
+
+    def loss(self, x, y):
+        h = x
+        L = len(self.sizes) - 1
+        P = self.params
+        for i in range(L):
+            last = i == L - 1
+            h = T.linear(h, P[f"fc{i}.w"], P[f"fc{i}.b"], act=0 if last else 1, out_f32=last)
+        return T.softmax_xent(h, y)
+
+
+# ---------------------------------------------------------------- Listing 1
+class ListingNet(Model):
+    """Listing 1 FullBasicModel under the reading conv → ReLU → global
+    avgpool → Linear(128,10) → softmax-CE (SURVEY §8(c) reading 1)."""
+
+    def param_specs(self):
+        return _conv_spec("conv", 128, 1, 3, True) + _lin_spec("fc", 128, 10)
+
+    def to_device_layout(self, name, a):
+        return _conv_to_krsc(a, pad_c=True) if name == "conv.w" else a
+
+    def to_logical_layout(self, name, a):
+        return _krsc_to_conv(a, 1) if name == "conv.w" else a
+
+    def loss(self, x, y):
+        P = self.params
+        t = T.conv2d(x, P["conv.w"], P["conv.b"], 1, 0, act=1)
+        t = T.avgpool_global(t)
+        z = T.linear(t, P["fc.w"], P["fc.b"], out_f32=True)
+        return T.softmax_xent(z, y)
+
+
+def _conv_to_krsc(w, pad_c=False):
+    k = np.ascontiguousarray(np.asarray(w, np.float32).transpose(0, 2, 3, 1))
+    if pad_c and k.shape[3] < CPAD:
+        z = np.zeros(k.shape[:3] + (CPAD,), np.float32)
+        z[..., :k.shape[3]] = k
+        k = z
+    return k
+
+
+def _krsc_to_conv(w, c_logical=None):
+    w = np.asarray(w)
+    if c_logical is not None:
+        w = w[..., :c_logical]
+    return np.ascontiguousarray(w.transpose(0, 3, 1, 2))
+
+
+# ---------------------------------------------------------------- AlexNet (C3)
+class AlexNet(Model):
+    CONVS = [("conv1", 64, 11, 4, 2, True), ("conv2", 192, 5, 1, 2, True), ("conv3", 384, 3, 1, 1, False),
+             ("conv4", 256, 3, 1, 1, False), ("conv5", 256, 3, 1, 1, True)]
+
+    def __init__(self, classes=1000, width=1.0, image=224):
+        super().__init__()
+        self.classes = classes
+        chain, prev, hw = [], 3, image
+        for (n, k, r, s, p, pool) in self.CONVS:
+            k = max(1, int(k * width))
+            chain.append((n, k, prev, r, s, p, pool))
+            prev = k
+            hw = (hw + 2 * p - r) // s + 1
+            if pool:
+                hw = (hw - 3) // 2 + 1
+        self.convs, self.c5, self.hw = chain, prev, hw
+        self.hidden = max(1, int(4096 * width))
+
+    def param_specs(self):
+        s = []
+        for (n, k, c, r, st, p, pool) in self.convs:
+            s += _conv_spec(n, k, c, r, True)
+        f = self.c5 * self.hw * self.hw
+        return s + _lin_spec("fc6", f, self.hidden) + _lin_spec("fc7", self.hidden, self.hidden) + \
+            _lin_spec("fc8", self.hidden, self.classes)
+
+    def _fc6_perm(self):
+        # device row (h, w, c) ← logical row c·HW + h·W + w
+        C, H = self.c5, self.hw
+        h, w, c = np.meshgrid(np.arange(H), np.arange(H), np.arange(C), indexing="ij")
+        return (c * H * H + h * H + w).reshape(-1)
+
+    def to_device_layout(self, name, a):
+        if name.endswith(".w") and name.startswith("conv"):
+            return _conv_to_krsc(a, pad_c=(name == "conv1.w"))
+        if name == "fc6.w":
+            return np.ascontiguousarray(a[self._fc6_perm()])
+        return a
+
+    def to_logical_layout(self, name, a):
+        if name.endswith(".w") and name.startswith("conv"):
+            return _krsc_to_conv(a, 3 if name == "conv1.w" else None)
+        if name == "fc6.w":
+            out = np.empty_like(a)
+            out[self._fc6_perm()] = a
+            return out
+        return a
+
+    def loss(self, x, y):
+        P = self.params
+        h = x
+        for (n, k, c, r, st, p, pool) in self.convs:
+            h = T.conv2d(h, P[n + ".w"], P[n + ".b"], st, p, act=1)
+            if pool:
+                h = T.maxpool2d(h, 3, 2, 0)
+        N = h.shape[0]
+        h = T.reshape(h, (N, -1))  # NHWC flatten (fc6 rows stored to match)
+        h = T.linear(h, P["fc6.w"], P["fc6.b"], act=1)
+        h = T.linear(h, P["fc7.w"], P["fc7.b"], act=1)
+        z = T.linear(h, P["fc8.w"], P["fc8.b"], out_f32=True)
+        return T.softmax_xent(z, y)
+
+
+# ---------------------------------------------------------------- ResNet-50 (C4)
+class ResNet50(Model):
+    """ResNet-50 v1.5 (SURVEY §8(c) reading 9); `layers`/`base` shrink it."""
+
+    def __init__(self, layers=(3, 4, 6, 3), base=64, classes=1000):
+        super().__init__()
+        self.layers, self.base, self.classes = tuple(layers), base, classes
+
+    def blocks(self):
+        out, cin = [], self.base
+        for li, nb in enumerate(self.layers):
+            mid = self.base * (2 ** li)
+            for bi in range(nb):
+                out.append((f"l{li + 1}.{bi}", cin, mid, mid * 4, 2 if (bi == 0 and li > 0) else 1, bi == 0))
+                cin = mid * 4
+        return out
+
+    def param_specs(self):
+        s = _conv_spec("conv1", self.base, 3, 7, False) + _bn_spec("bn1", self.base)
+        for (n, cin, mid, cout, stride, down) in self.blocks():
+            s += _conv_spec(n + ".c1", mid, cin, 1, False) + _bn_spec(n + ".bn1", mid)
+            s += _conv_spec(n + ".c2", mid, mid, 3, False) + _bn_spec(n + ".bn2", mid)
+            s += _conv_spec(n + ".c3", cout, mid, 1, False) + _bn_spec(n + ".bn3", cout)
+            if down:
+                s += _conv_spec(n + ".ds", cout, cin, 1, False) + _bn_spec(n + ".dsbn", cout)
+        return s + _lin_spec("fc", self.blocks()[-1][3], self.classes)
+
+    def to_device_layout(self, name, a):
+        if a.ndim == 4:
+            return _conv_to_krsc(a, pad_c=(name == "conv1.w"))
+        return a
+
+    def to_logical_layout(self, name, a):
+        if np.ndim(a) == 4:
+            return _krsc_to_conv(a, 3 if name == "conv1.w" else None)
+        return a
+
+    def make_buffers(self):
+        self.buffers = {}
+        for (name, shape, init, _) in self.param_specs():
+            if name.endswith(".g"):
+                base = name[:-2]
+                self.buffers[base + ".rm"] = T.tensor(np.zeros(shape, np.float32))
+                self.buffers[base + ".rv"] = T.tensor(np.ones(shape, np.float32))
+
+    def loss(self, x, y):
+        P, B = self.params, self.buffers
+
+        def bn(h, name, act):
+            return T.batchnorm2d(h, P[name + ".g"], P[name + ".b"], B[name + ".rm"], B[name + ".rv"], act=act)
+        h = T.conv2d(x, P["conv1.w"], None, 2, 3)
+        h = bn(h, "bn1", 1)
+        h = T.maxpool2d(h, 3, 2, 1)
+        for (n, cin, mid, cout, stride, down) in self.blocks():
+            t = bn(T.conv2d(h, P[n + ".c1.w"], None, 1, 0), n + ".bn1", 1)
+            t = bn(T.conv2d(t, P[n + ".c2.w"], None, stride, 1), n + ".bn2", 1)
+            t = bn(T.conv2d(t, P[n + ".c3.w"], None, 1, 0), n + ".bn3", 0)
+            idn = bn(T.conv2d(h, P[n + ".ds.w"], None, stride, 0), n + ".dsbn", 0) if down else h
+            h = T.add_relu(t, idn)
+        h = T.avgpool_global(h)
+        z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
+        return T.softmax_xent(z, y)
+
+
+# ---------------------------------------------------------------- NCF (C5)
+class NCF(Model):
+    """NeuMF (SURVEY §8(c) reading 11): GMF dim 64, MLP 256→256→128→64."""
+
+    def __init__(self, n_users=138493, n_items=26744, gmf=64, mlp=(256, 256, 128, 64)):
+        super().__init__()
+        self.n_users, self.n_items, self.gmf, self.mlp = n_users, n_items, gmf, tuple(mlp)
+
+    def param_specs(self):
+        e = self.mlp[0] // 2
+        s = [("user_gmf", (self.n_users, self.gmf), "normal", 1), ("item_gmf", (self.n_items, self.gmf), "normal", 1),
+             ("user_mlp", (self.n_users, e), "normal", 1), ("item_mlp", (self.n_items, e), "normal", 1)]
+        for i in range(len(self.mlp) - 1):
+            s += _lin_spec(f"mlp{i}", self.mlp[i], self.mlp[i + 1])
+        return s + _lin_spec("head", self.gmf + self.mlp[-1], 1)
+
+    def loss(self, users, items, y):
+        P = self.params
+        g = T.mul(T.embedding(P["user_gmf"], users), T.embedding(P["item_gmf"], items))
+        h = T.concat([T.embedding(P["user_mlp"], users), T.embedding(P["item_mlp"], items)])
+        for i in range(len(self.mlp) - 1):
+            h = T.linear(h, P[f"mlp{i}.w"], P[f"mlp{i}.b"], act=1)
+        z = T.linear(T.concat([g, h]), P["head.w"], P["head.b"], out_f32=True)
+        return T.bce_logits(z, y)
+
+
+def train_step(model: Model, batch, lr=0.01, momentum=0.0, weight_decay=0.0):
+    """One eager step: zero_grad (release), forward, backward, fused SGD.
+    Returns the (device) loss tensor; nothing here synchronises."""
+    params = model.parameters()
+    T.zero_grad(params)
+    loss = model.loss(*batch)
+    loss.backward()
+    T.sgd_step(params, lr, momentum, weight_decay)
+    return loss

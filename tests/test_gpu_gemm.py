@@ -1,0 +1,99 @@
+"""GEMM parity on the B200 (-m gpu): the tcgen05 kernel in every operand
+majorness, bf16 and 3xTF32, ragged shapes spanning several tiles, split-K,
+bias/ReLU/beta epilogues — against the oracle's float64 matmul."""
+import numpy as np
+import pytest
+
+from gpu_common import be_init, rel
+from oracle import ops
+from oracle.autograd import Var
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, b, ta, tb, bias=None, act=0, beta=0.0, d0=None):
+    A = a.T if ta else a
+    B = b.T if tb else b
+    y = ops.matmul(Var(A.astype(np.float64)), Var(B.astype(np.float64))).value
+    if bias is not None:
+        y = y + bias
+    if act:
+        y = np.maximum(y, 0)
+    if beta:
+        y = y + d0
+    return y
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", 1e-2), ("f32", 1e-5)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 200, 136), (1024, 512, 512), (64, 40, 3000)])
+def test_gemm_majorness(dtype, tol, ta, tb, M, N, K):
+    be = be_init()
+    rng = np.random.default_rng(M + N + K + ta * 2 + tb)
+    a = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    if dtype == "bf16":  # compare against the bf16-rounded operands (the kernel's inputs)
+        from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+        a = bf16_bits_to_f32(f32_to_bf16_bits(a))
+        b = bf16_bits_to_f32(f32_to_bf16_bits(b))
+    A = be.tensor(a, dtype=dtype)
+    B = be.tensor(b, dtype=dtype)
+    D = be.empty((M, N), "f32")
+    be.gemm(A, B, D, trans_a=bool(ta), trans_b=bool(tb))
+    ref = _ref(a, b, ta, tb)
+    e = rel(D.numpy(), ref)
+    assert e < (1e-5 if dtype == "bf16" else tol), e
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_gemm_epilogue_bias_relu_beta(dtype):
+    be = be_init()
+    rng = np.random.default_rng(7)
+    M, N, K = 257, 384, 192
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    d0 = rng.standard_normal((M, N)).astype(np.float32)
+    if dtype == "bf16":
+        from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+        a = bf16_bits_to_f32(f32_to_bf16_bits(a))
+        b = bf16_bits_to_f32(f32_to_bf16_bits(b))
+    A, B = be.tensor(a, dtype=dtype), be.tensor(b, dtype=dtype)
+    D = be.tensor(d0)
+    be.gemm(A, B, D, bias=be.tensor(bias), act=1, beta=1.0)
+    ref = _ref(a, b, 0, 0, bias, 1, 1.0, d0)
+    assert rel(D.numpy(), ref) < (1e-5 if dtype == "bf16" else 2e-6)
+    # bf16 output, RN-even rounding of the fp32 accumulator
+    Db = be.empty((M, N), "bf16")
+    be.gemm(A, B, Db)
+    assert rel(Db.numpy(), _ref(a, b, 0, 0)) < 8e-3
+
+
+def test_gemm_splitk_deterministic():
+    """Split-K (tiny M·N, huge K) reduces partials in a fixed order."""
+    be = be_init()
+    rng = np.random.default_rng(3)
+    M, N, K = 64, 147, 60000
+    a = rng.standard_normal((K, M)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    A, B = be.tensor(a, dtype="bf16"), be.tensor(b, dtype="bf16")
+    D1, D2 = be.empty((M, N), "f32"), be.empty((M, N), "f32")
+    be.gemm(A, B, D1, trans_a=True)
+    be.gemm(A, B, D2, trans_a=True)
+    x1, x2 = D1.numpy(), D2.numpy()
+    assert np.array_equal(x1, x2)
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    ab = bf16_bits_to_f32(f32_to_bf16_bits(a)).astype(np.float64)
+    bb = bf16_bits_to_f32(f32_to_bf16_bits(b)).astype(np.float64)
+    assert rel(x1, ab.T @ bb) < 1e-5
+
+
+def test_gemm_misaligned_uses_simt_and_matches():
+    be = be_init()
+    rng = np.random.default_rng(4)
+    M, N, K = 64, 10, 128  # N=10 fp32 row stride 40 B: not TMA-describable
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    D = be.empty((M, N), "f32")
+    be.gemm(be.tensor(a), be.tensor(b), D)
+    assert rel(D.numpy(), _ref(a, b, 0, 0)) < 1e-6

@@ -89,6 +89,24 @@ def test_sgd_momentum_closed_form():
     assert abs(float(p2["p"]) - (0.95 - 0.1 * (0.9 * 0.5 + 0.5))) < 1e-15
 
 
+def test_bf16_round_known_values():
+    """RN-even to bfloat16 (8-bit significand): exact values, halfway ties to
+    even, carries into the exponent, specials."""
+    r = ops.bf16_round
+    assert r(1.0) == 1.0
+    assert r(1 + 2 ** -8) == 1.0                      # tie → even (mantissa ...0)
+    assert r(1 + 3 * 2 ** -8) == 1 + 2 ** -6          # tie → even (round up)
+    assert r(1 + 2 ** -8 + 2 ** -12) == 1 + 2 ** -7   # above halfway → up
+    assert r(2 - 2 ** -9) == 2.0                       # carry into exponent
+    assert r(-3.0) == -3.0 and np.isnan(r(np.nan)) and r(np.inf) == np.inf
+    # equivalence with the float32 rounding of a 7-bit-truncated neighbourhood
+    x = np.random.default_rng(0).standard_normal(1000)
+    y = r(x)
+    assert np.all(np.abs(y - x) <= np.abs(x) * 2 ** -8 * 1.0000001)
+    m = np.frexp(y)[0] * 2 ** 8
+    assert np.all(m == np.round(m))  # at most 8 significant bits
+
+
 # ------------------------------------------------------------ closed forms
 def test_mlp_closed_form_zero_last_layer():
     """W2 = 0, b2 = 0 ⇒ logits uniform ⇒ loss = ln C exactly, dz = (1/C − onehot)/B,
