@@ -87,45 +87,48 @@ def host_batch(cfg, seed, rank=0):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML every 10 ms while the
+    timed region runs (the recipe's clocks line; nvidia-smi -lms cannot
+    sample a few-ms region)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, index=0):
-        self.index, self.samples, self.proc = index, [], None
+        self.index, self.samples, self.stop_flag = index, [], False
 
     def start(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.nv = None
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.samples.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.01)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            for nm, v in zip(names, s[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        self.stop_flag = True
+        if getattr(self, "nv", None) is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "unavailable"}
+        self.thread.join(timeout=1)
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({nm for _, r in self.samples for nm, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(sm), "source": "nvml 10 ms"}
 
 
 # ---------------------------------------------------------------- oracle timing (reference arm / cpu_baseline)
@@ -279,6 +282,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             "kernel": "gemm_tc (all tcgen05 GEMM launches of the step)",
             "launches_per_step": len(tc) / args.steps, "share_of_step": round(gemm_ms / ms, 4) if ms else None,
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk_kind})"}
+    shapes = {}
+    for r in tc:
+        key = f"{r['m']}x{r['n']}x{r['k']}"
+        s = shapes.setdefault(key, [0, 0.0, r["flops"]])
+        s[0] += 1
+        s[1] += r["ms"]
+    roof["per_shape"] = {k: {"launches": v[0], "avg_us": round(v[1] / v[0] * 1e3, 2),
+                             "tflops": round(v[2] / (v[1] / v[0] / 1e3) / 1e12, 1)} for k, v in shapes.items()}
     trafficf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(trafficf):
         roof["traffic"] = json.load(open(trafficf)).get("dram_bytes_per_launch")
@@ -328,7 +339,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
