@@ -571,7 +571,11 @@ static void op_concat(const be_tensor* in, int n_in, be_tensor* out) {
     bool any = false;
     for (Tensor* x : xs) any |= x->requires_grad;
     if (any) {
-      nd = new_node("concat", BE_OP_CONCAT, vjp_concat, {});
+      nd = new Node();
+      nd->name = "concat";
+      nd->op = BE_OP_CONCAT;
+      nd->vjp = vjp_concat;
+      nd->seq = ctx().seq.fetch_add(1);
       for (Tensor* x : xs) {
         Edge e;
         if (x->requires_grad) {

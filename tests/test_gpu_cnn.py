@@ -1,0 +1,184 @@
+"""CNN / recommender parity on the B200 (-m gpu): conv2d (fwd, dgrad, wgrad),
+max / average pooling, batch norm, residual add, embedding — per op and
+whole training steps — against the float64 oracle.  Index tensors (im2col
+offsets, max-pool argmax) must match bit-exactly."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_common import be_init, rel, run_product_step, compare_step
+from oracle import ops as oops, nets as onets
+from oracle.autograd import Var, backward
+from oracle.step import train_step
+
+pytestmark = pytest.mark.gpu
+
+
+def nchw_to_nhwc(a):
+    return np.ascontiguousarray(np.asarray(a).transpose(0, 2, 3, 1))
+
+
+def nhwc_to_nchw(a):
+    return np.ascontiguousarray(np.asarray(a).transpose(0, 3, 1, 2))
+
+
+@pytest.mark.parametrize("geom", [(2, 3, 5, 5, 3, 3, 1, 1), (2, 8, 9, 7, 3, 3, 2, 1), (1, 4, 11, 11, 11, 11, 4, 2),
+                                  (3, 16, 6, 6, 1, 1, 2, 0), (1, 1, 28, 28, 3, 3, 1, 0)])
+def test_im2col_offsets_bit_exact(geom):
+    be = be_init()
+    N, C, H, W, R, S, st, pd = geom
+    dev = be.im2col_offsets(N, C, H, W, R, S, st, pd)
+    ref = oops.im2col_table(N, C, H, W, R, S, st, pd)
+    assert np.array_equal(dev, ref)
+
+
+@pytest.mark.parametrize("cfg", [(2, 8, 9, 9, 16, 3, 1, 1), (2, 8, 10, 10, 12, 3, 2, 1), (3, 16, 7, 7, 32, 1, 1, 0),
+                                 (2, 16, 8, 8, 24, 1, 2, 0), (2, 8, 23, 23, 16, 11, 4, 2), (1, 8, 12, 12, 8, 5, 1, 2)])
+@pytest.mark.parametrize("act", [0, 1])
+def test_conv_op_fp32(cfg, act):
+    """conv2d forward + backward (dX, dW, db) in f32 (3xTF32) at 1e-4."""
+    be = be_init()
+    be.set_compute_dtype("f32")
+    N, C, H, W, K, R, st, pd = cfg
+    rng = np.random.default_rng(sum(cfg) + act)
+    x = rng.standard_normal((N, C, H, W)).astype(np.float32)
+    w = (rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R)).astype(np.float32)
+    b = rng.standard_normal(K).astype(np.float32)
+    xo, wo, bo = Var(x.astype(np.float64), True), Var(w.astype(np.float64), True), Var(b.astype(np.float64), True)
+    yo = oops.conv2d(xo, wo, bo, st, pd)
+    if act:
+        yo = oops.relu(yo)
+    g = rng.standard_normal(yo.value.shape)
+    backward(yo, g)
+    xd = be.tensor(nchw_to_nhwc(x), requires_grad=True)
+    wd = be.tensor(nchw_to_nhwc(w), requires_grad=True)
+    bd = be.tensor(b, requires_grad=True)
+    yd = be.conv2d(xd, wd, bd, st, pd, act=act)
+    yd.backward(be.tensor(nchw_to_nhwc(g).astype(np.float32)))
+    assert rel(nhwc_to_nchw(yd.numpy()), yo.value) < 1e-4
+    assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-4
+    assert rel(nhwc_to_nchw(wd.grad.numpy()), wo.grad) < 1e-4
+    assert rel(bd.grad.numpy(), bo.grad) < 1e-4
+
+
+@pytest.mark.parametrize("k,s,p", [(3, 2, 0), (3, 2, 1)])
+def test_maxpool_op_and_argmax_bit_exact(k, s, p):
+    be = be_init()
+    be.set_compute_dtype("f32")
+    rng = np.random.default_rng(k + s + p)
+    x = rng.standard_normal((2, 5, 13, 13)).astype(np.float32)
+    x[0, 0, :4, :4] = 0.0  # tied windows → first index
+    xo = Var(x.astype(np.float64), True)
+    yo, am = oops.maxpool2d(xo, k, s, p)
+    g = rng.standard_normal(yo.value.shape)
+    backward(yo, g)
+    xd = be.tensor(nchw_to_nhwc(x), requires_grad=True)
+    yd, amd = be.maxpool2d(xd, k, s, p, with_argmax=True)
+    yd.backward(be.tensor(nchw_to_nhwc(g).astype(np.float32)))
+    assert np.array_equal(nhwc_to_nchw(yd.numpy()), yo.value.astype(np.float32))
+    # device window index (r*k+u) → plane index h*W+w, compared bit-exactly
+    win = nhwc_to_nchw(amd.numpy()).astype(np.int64)
+    P = yo.value.shape[2]
+    pi = np.arange(P)[:, None]
+    qi = np.arange(P)[None, :]
+    h = pi * s - p + win // k
+    w = qi * s - p + win % k
+    assert np.array_equal(h * x.shape[3] + w, am)
+    assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-6
+
+
+def test_avgpool_bn_add_ops_fp32():
+    be = be_init()
+    be.set_compute_dtype("f32")
+    rng = np.random.default_rng(11)
+    x = (rng.standard_normal((4, 6, 5, 5)) * 2 + 0.5).astype(np.float32)
+    r = rng.standard_normal((4, 6, 5, 5)).astype(np.float32)
+    gam = (rng.standard_normal(6) + 1).astype(np.float32)
+    bet = rng.standard_normal(6).astype(np.float32)
+    xo, ro = Var(x.astype(np.float64), True), Var(r.astype(np.float64), True)
+    go, bo = Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
+    yo, (rm, rv) = oops.batchnorm2d(xo, go, bo)
+    zo = oops.avgpool_global(oops.relu(oops.add(yo, ro)))
+    g = rng.standard_normal(zo.value.shape)
+    backward(zo, g)
+    xd, rd = be.tensor(nchw_to_nhwc(x), requires_grad=True), be.tensor(nchw_to_nhwc(r), requires_grad=True)
+    gd, bd = be.tensor(gam, requires_grad=True), be.tensor(bet, requires_grad=True)
+    rmd, rvd = be.tensor(np.zeros(6, np.float32)), be.tensor(np.ones(6, np.float32))
+    yd = be.batchnorm2d(xd, gd, bd, rmd, rvd)
+    zd = be.avgpool_global(be.add_relu(yd, rd))
+    zd.backward(be.tensor(g.astype(np.float32)))
+    assert rel(zd.numpy(), zo.value) < 1e-5
+    for dev, orc in ((xd, xo), (rd, ro), (gd, go), (bd, bo)):
+        d = dev.grad.numpy()
+        assert rel(nhwc_to_nchw(d) if d.ndim == 4 else d, orc.grad) < 1e-4
+    assert rel(rmd.numpy(), rm) < 1e-5 and rel(rvd.numpy(), rv) < 1e-5
+
+
+def test_embedding_op_deterministic():
+    be = be_init()
+    be.set_compute_dtype("f32")
+    rng = np.random.default_rng(12)
+    E = rng.standard_normal((97, 24)).astype(np.float32)
+    ids = rng.integers(0, 97, 3000).astype(np.int32)
+    ids[:50] = 5  # a hot row
+    g = rng.standard_normal((3000, 24))
+    Eo = Var(E.astype(np.float64), True)
+    backward(oops.embedding(Eo, ids), g)
+    grads = []
+    for _ in range(2):
+        Ed = be.tensor(E, requires_grad=True)
+        rows = be.embedding(Ed, be.tensor(ids))
+        assert np.array_equal(rows.numpy(), E[ids])
+        rows.backward(be.tensor(g.astype(np.float32)))
+        grads.append(Ed.grad.numpy())
+    assert np.array_equal(grads[0], grads[1])  # bitwise reproducible
+    assert rel(grads[0], Eo.grad) < 1e-5
+
+
+# ------------------------------------------------------------ whole training steps (fp32 at 1e-4)
+def _step_case(onet, pnet, batch_o, batch_d, dtype="f32", seed=0, tol=1e-4):
+    be = be_init()
+    be.set_compute_dtype(dtype)
+    assert onet.param_specs() == pnet.param_specs()
+    P = synth.make_params(onet.param_specs(), seed)
+    ref = train_step(onet, P, batch_o, lr=0.01)
+    loss, grads, new = run_product_step(be, pnet, P, batch_d)
+    return compare_step(ref, loss, grads, new, tol)
+
+
+def test_listing1_net_fp32():
+    be = be_init()
+    x = synth.uniform((8, 1, 28, 28), 0, 1)
+    y = synth.labels(8, 10, 0)
+    errs = _step_case(onets.ListingNet(), be.nn.ListingNet(), (x, y),
+                      (be.nn.images_to_device(x, "f32"), be.tensor(y)))
+    print("listing max err", max(errs.values()))
+
+
+def test_alexnet_small_fp32():
+    be = be_init()
+    x = synth.normal((2, 3, 127, 127), 1, 1)
+    y = synth.labels(2, 10, 1)
+    errs = _step_case(onets.AlexNet(classes=10, width=1 / 16, image=127),
+                      be.nn.AlexNet(classes=10, width=1 / 16, image=127), (x, y),
+                      (be.nn.images_to_device(x, "f32"), be.tensor(y)), seed=1)
+    print("alexnet max err", max(errs.values()))
+
+
+def test_resnet_small_fp32():
+    be = be_init()
+    x = synth.normal((4, 3, 64, 64), 2, 1)
+    y = synth.labels(4, 10, 2)
+    errs = _step_case(onets.ResNet50(layers=(1, 1, 1, 1), base=8, classes=10),
+                      be.nn.ResNet50(layers=(1, 1, 1, 1), base=8, classes=10), (x, y),
+                      (be.nn.images_to_device(x, "f32"), be.tensor(y)), seed=2)
+    print("resnet max err", max(errs.values()))
+
+
+def test_ncf_small_fp32():
+    be = be_init()
+    users, items, y = synth.ncf_batch(256, 50, 30, 3)
+    onet = onets.NCF(n_users=50, n_items=30, gmf=8, mlp=(16, 16, 8))
+    pnet = be.nn.NCF(n_users=50, n_items=30, gmf=8, mlp=(16, 16, 8))
+    errs = _step_case(onet, pnet, (users, items, y), (be.tensor(users), be.tensor(items), be.tensor(y)), seed=3)
+    print("ncf max err", max(errs.values()))
