@@ -212,6 +212,14 @@ be_status be_dist_init(int rank, int world, const void* nccl_unique_id);
  * backward; be_sgd_step waits for all buckets and folds in 1/world. */
 be_status be_ddp_attach(const be_tensor* params, int n, size_t bucket_bytes);
 be_status be_ddp_detach(void);
+/* Pure host function (no GPU needed): the bucket plan be_ddp_attach uses.
+ * numels[n] = parameter sizes in registration order.  Buckets are filled in
+ * REVERSE registration order (the order backward produces gradients) until
+ * they reach bucket_bytes (fp32); each parameter's offset inside its bucket
+ * is 64-element (256-B) aligned.  Outputs: bucket_of[n], offset_of[n]
+ * (elements), bucket_numel[*n_buckets] (cap entries). */
+be_status be_ddp_plan(const int64_t* numels, int n, size_t bucket_bytes, int* bucket_of, int64_t* offset_of,
+                      int64_t* bucket_numel, int cap, int* n_buckets);
 /* Plain allreduce (sum, fp32/bf16) of a contiguous tensor on the compute stream. */
 be_status be_allreduce_(be_tensor t);
 

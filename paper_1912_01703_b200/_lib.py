@@ -120,6 +120,8 @@ def lib():
             "be_item": [T, P(C.c_double)],
             "be_debug_im2col_offsets": [P(C.c_int64), P(C.c_int64)],
             "be_gemm": [T, C.c_int, T, C.c_int, T, T, C.c_int, C.c_float],
+            "be_ddp_plan": [P(C.c_int64), C.c_int, C.c_size_t, P(C.c_int), P(C.c_int64), P(C.c_int64), C.c_int,
+                            P(C.c_int)],
             "be_prof_enable": [C.c_int],
             "be_prof_read": [P(be_prof_rec), C.c_int, P(C.c_int)],
         }
@@ -152,5 +154,5 @@ EXPORTED = [
     "be_backward", "be_grad", "be_zero_grad", "be_sgd_step", "be_alloc_stats", "be_alloc_reset_peak",
     "be_empty_cache", "be_round_size", "be_record_stream", "be_raw_alloc", "be_raw_free", "be_dist_unique_id",
     "be_dist_init", "be_ddp_attach", "be_ddp_detach", "be_allreduce_", "be_synchronize", "be_item",
-    "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read",
+    "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
 ]

@@ -385,6 +385,18 @@ def dist_init(rank, world, uid: bytes):
     call("be_dist_init", int(rank), int(world), buf)
 
 
+def ddp_plan(numels, bucket_bytes=25 << 20):
+    """Bucket plan of be_ddp_attach (pure host function): (bucket_of, offset_of, bucket_numel)."""
+    n = len(numels)
+    arr = (C.c_int64 * max(n, 1))(*numels)
+    bof = (C.c_int * max(n, 1))()
+    off = (C.c_int64 * max(n, 1))()
+    bnum = (C.c_int64 * (n + 1))()
+    nb = C.c_int()
+    call("be_ddp_plan", arr, n, C.c_size_t(bucket_bytes), bof, off, bnum, n + 1, C.byref(nb))
+    return list(bof[:n]), list(off[:n]), list(bnum[:nb.value])
+
+
 def ddp_attach(params, bucket_bytes=25 << 20):
     call("be_ddp_attach", _handles(params), len(params), C.c_size_t(bucket_bytes))
 

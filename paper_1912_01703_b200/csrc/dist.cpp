@@ -99,6 +99,33 @@ void launch_bucket(Bucket& b) {
   b.launched = true;
   d.allreduce_calls++;
 }
+// Bucket plan: reverse registration order, 64-element aligned offsets, a new
+// bucket once the current one reaches bucket_bytes of fp32.
+void plan_buckets(const int64_t* numels, int n, size_t bucket_bytes, int* bucket_of, int64_t* offset_of,
+                  int64_t* bucket_numel, int cap, int* n_buckets) {
+  if (bucket_bytes == 0) bucket_bytes = 25u << 20;
+  int nb = 0;
+  int64_t cur = 0;
+  bool open = false;
+  for (int i = n - 1; i >= 0; --i) {
+    const int64_t aligned = (cur + 63) / 64 * 64;
+    offset_of[i] = aligned;
+    bucket_of[i] = nb;
+    cur = aligned + numels[i];
+    open = true;
+    if ((size_t)cur * 4 >= bucket_bytes) {
+      BE_REQUIRE(nb < cap, BE_E_ARG, "ddp_plan: bucket capacity exceeded");
+      bucket_numel[nb++] = cur;
+      cur = 0;
+      open = false;
+    }
+  }
+  if (open) {
+    BE_REQUIRE(nb < cap, BE_E_ARG, "ddp_plan: bucket capacity exceeded");
+    bucket_numel[nb++] = cur;
+  }
+  *n_buckets = nb;
+}
 }  // namespace
 
 bool ddp_active() { return ddp().active; }
@@ -207,19 +234,20 @@ be_status be_ddp_attach(const be_tensor* params, int n, size_t bucket_bytes) {
   d.offset_of.assign(n, 0);
   d.ready.assign(n, 0);
   d.buckets.clear();
-  // reverse registration order ≈ the order backward produces gradients
-  Bucket cur;
-  for (int i = n - 1; i >= 0; --i) {
-    Tensor* p = d.params[i];
-    size_t ne = (size_t)p->numel();
-    size_t aligned = (cur.numel + 63) / 64 * 64;  // 256-B aligned views
-    d.offset_of[i] = aligned;
-    d.bucket_of[i] = (int)d.buckets.size();
-    cur.numel = aligned + ne;
-    cur.params.push_back(i);
-    if (cur.numel * 4 >= bucket_bytes) { d.buckets.push_back(cur); cur = Bucket(); }
+  {
+    std::vector<int64_t> numels(n), offs(n), bnum(n + 1);
+    std::vector<int> bof(n);
+    for (int i = 0; i < n; ++i) numels[i] = d.params[i]->numel();
+    int nb = 0;
+    plan_buckets(numels.data(), n, bucket_bytes, bof.data(), offs.data(), bnum.data(), n + 1, &nb);
+    d.buckets.resize(nb);
+    for (int b = 0; b < nb; ++b) d.buckets[b].numel = (size_t)bnum[b];
+    for (int i = n - 1; i >= 0; --i) {  // params listed in the order gradients arrive
+      d.bucket_of[i] = bof[i];
+      d.offset_of[i] = (size_t)offs[i];
+      d.buckets[bof[i]].params.push_back(i);
+    }
   }
-  if (!cur.params.empty()) d.buckets.push_back(cur);
   for (Bucket& b : d.buckets) {
     Storage* st = new Storage();
     st->nbytes = std::max<size_t>(b.numel, 1) * 4;
@@ -252,6 +280,14 @@ be_status be_ddp_detach(void) {
   d.buckets.clear();
   d.params.clear();
   d.active = false;
+  BE_API_END
+}
+
+be_status be_ddp_plan(const int64_t* numels, int n, size_t bucket_bytes, int* bucket_of, int64_t* offset_of,
+                      int64_t* bucket_numel, int cap, int* n_buckets) {
+  BE_API_BEGIN
+  BE_REQUIRE(n >= 0 && numels && bucket_of && offset_of && bucket_numel && n_buckets, BE_E_ARG, "ddp_plan: bad args");
+  plan_buckets(numels, n, bucket_bytes, bucket_of, offset_of, bucket_numel, cap, n_buckets);
   BE_API_END
 }
 
