@@ -28,6 +28,8 @@
 #include <atomic>
 #include <cstdio>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 
 #include "kernels.h"
 #include "runtime.h"
@@ -79,6 +81,80 @@ __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // RN-even (cvt.rn.bf16x2.f32)
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue for 32 accumulator columns of one output row held by this thread:
+// bias, ReLU, beta-accumulate, fp32 or RN-even bf16 store.  Tails use
+// predicated fully-unrolled loops (no local-memory spills).
+__device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bool vec_ok, int row, int col0,
+                                            const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  const int ncol = min(32, p.N - col0);
+  const bool full = ncol == 32;
+  if (p.bias) {
+    if (full && (reinterpret_cast<uintptr_t>(p.bias + col0) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+        v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < ncol) v[j] += __ldg(p.bias + col0 + j);
+    }
+  }
+  if (p.act == 1) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  const bool acc = p.beta != 0.f;
+  if (p.d_f32) {
+    float* dst = reinterpret_cast<float*>(Dbase) + (long long)row * p.ldd + col0;
+    if (full && vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (acc) {
+          float4 old = *reinterpret_cast<const float4*>(dst + j);
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *reinterpret_cast<float4*>(dst + j) = o;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < ncol) dst[j] = v[j] + (acc ? dst[j] : 0.f);
+    }
+  } else {
+    uint16_t* dst = reinterpret_cast<uint16_t*>(Dbase) + (long long)row * p.ldd + col0;
+    if (full && vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        if (acc) {
+          uint4 old = *reinterpret_cast<const uint4*>(dst + j);
+          const uint16_t* o16 = reinterpret_cast<const uint16_t*>(&old);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[j + q] += bf16_bits_to_f32(o16[q]);
+        }
+        uint4 o;
+        o.x = pack_bf16x2(v[j], v[j + 1]); o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+        o.z = pack_bf16x2(v[j + 4], v[j + 5]); o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+        *reinterpret_cast<uint4*>(dst + j) = o;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < ncol) {
+          float x = v[j] + (acc ? bf16_bits_to_f32(dst[j]) : 0.f);
+          __nv_bfloat16 h = __float2bfloat16_rn(x);
+          dst[j] = *reinterpret_cast<uint16_t*>(&h);
+        }
+      }
+    }
+  }
 }
 
 template <int BN, bool X3>
@@ -214,65 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (!row_ok) continue;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int ncol = min(32, p.N - col0);
-        if (p.bias) {
-          if (ncol == 32 && (reinterpret_cast<uintptr_t>(p.bias + col0) & 15) == 0) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-          } else {
-            for (int j = 0; j < ncol; ++j) v[j] += __ldg(p.bias + col0 + j);
-          }
-        }
-        if (p.act == 1) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-        }
-        if (p.d_f32) {
-          float* dst = reinterpret_cast<float*>(Dbase) + (long long)row * p.ldd + col0;
-          if (ncol == 32 && vec_ok) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-              if (p.beta != 0.f) {
-                float4 old = *reinterpret_cast<const float4*>(dst + j);
-                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-              }
-              *reinterpret_cast<float4*>(dst + j) = o;
-            }
-          } else {
-            for (int j = 0; j < ncol; ++j) dst[j] = v[j] + (p.beta != 0.f ? dst[j] : 0.f);
-          }
-        } else {
-          uint16_t* dst = reinterpret_cast<uint16_t*>(Dbase) + (long long)row * p.ldd + col0;
-          if (ncol == 32 && vec_ok) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              if (p.beta != 0.f) {
-                uint4 old = *reinterpret_cast<const uint4*>(dst + j);
-                const uint16_t* o16 = reinterpret_cast<const uint16_t*>(&old);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) v[j + q] += bf16_bits_to_f32(o16[q]);
-              }
-              uint4 o;
-              o.x = pack_bf16x2(v[j], v[j + 1]); o.y = pack_bf16x2(v[j + 2], v[j + 3]);
-              o.z = pack_bf16x2(v[j + 4], v[j + 5]); o.w = pack_bf16x2(v[j + 6], v[j + 7]);
-              *reinterpret_cast<uint4*>(dst + j) = o;
-            }
-          } else {
-            for (int j = 0; j < ncol; ++j) {
-              float x = v[j] + (p.beta != 0.f ? bf16_bits_to_f32(dst[j]) : 0.f);
-              __nv_bfloat16 h = __float2bfloat16_rn(x);
-              dst[j] = *reinterpret_cast<uint16_t*>(&h);
-            }
-          }
-        }
+        if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -285,6 +303,156 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   if (warp == 2) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- CTA-pair kernel
+// cta_group::2, bf16: a cluster of 2 CTAs computes a 256×256 tile with
+// M=256 MMAs issued by the leader; each CTA stages its own 128 rows of A and
+// its own 128 rows (N-half) of B, so every byte is fetched from L2 once per
+// pair (the 1-CTA 128×256 tile is L2-bandwidth bound, profiles/r01_summary).
+namespace pair {
+constexpr int TM = 256, TN = 256;         // pair tile
+constexpr int HM = 128, HN = 128;         // per-CTA halves
+constexpr int BK = 64;                    // bf16: one 128-B swizzle row
+constexpr int A_BYTES = HM * 128, B_BYTES = HN * 128;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB per CTA
+constexpr int STAGES = 6;
+constexpr int TMEM_COLS = 512;            // 2 accumulators × 256 columns
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+}  // namespace pair
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ GemmParams p) {
+  using namespace pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 2) sm100::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int mn_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = mn_tiles * p.splits;
+  const int kblocks_total = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer (both CTAs) =====================
+      int stage = 0; uint32_t phase = 0;
+      for (int t = pair_id; t < num_tiles; t += npairs) {
+        const int mn = t % mn_tiles, sp = t / mn_tiles;
+        const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
+        const int m0 = tm * TM + rank * HM, n0 = tn * TN + rank * HN;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const int k0 = kb * BK;
+          if (p.a_kmajor) {
+            sm100::tma_load_2d_2sm(&p.ta[0], &full[stage], sa, k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < HM / 64; ++j) sm100::tma_load_2d_2sm(&p.ta[0], &full[stage], sa + j * BK * 128, m0 + j * 64, k0);
+          }
+          if (p.b_kmajor) {
+            sm100::tma_load_2d_2sm(&p.tb[0], &full[stage], sb, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < HN / 64; ++j) sm100::tma_load_2d_2sm(&p.tb[0], &full[stage], sb + j * BK * 128, n0 + j * 64, k0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===================== MMA issuer (leader CTA only) =====================
+      const uint32_t idesc = sm100::make_idesc(1u, TM, TN, p.a_kmajor ? 0 : 1, p.b_kmajor ? 0 : 1);
+      const uint32_t a_lbo = p.a_kmajor ? 16u : (uint32_t)(BK * 128);
+      const uint32_t b_lbo = p.b_kmajor ? 16u : (uint32_t)(BK * 128);
+      const uint32_t a_kstep = p.a_kmajor ? 32u : 16u * 128u;
+      const uint32_t b_kstep = p.b_kmajor ? 32u : 16u * 128u;
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = pair_id; t < num_tiles; t += npairs) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * TN;
+        const int sp = t / mn_tiles;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = sm100::make_sw128_desc(sa + kk * a_kstep, a_lbo, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb + kk * b_kstep, b_lbo, 1024);
+            sm100::mma_bf16_2sm(d_tmem, ad, bd, idesc, ((kb - kb0) | kk) ? 1u : 0u);
+          }
+          sm100::mma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit_2sm(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (both CTAs, own TMEM half) =====================
+    const int ew = warp - 4;
+    int acc = 0; uint32_t acc_phase = 0;
+    const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
+    for (int t = pair_id; t < num_tiles; t += npairs) {
+      const int mn = t % mn_tiles, sp = t / mn_tiles;
+      const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
+      char* Dbase = reinterpret_cast<char*>(p.D) + (long long)sp * p.split_stride * 4;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = tm * TM + rank * HM + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c0 = 0; c0 < TN; c0 += 32) {
+        const int col0 = tn * TN + c0;
+        if (col0 >= p.N) break;
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::cluster_sync();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
   }
 }
 
@@ -519,6 +687,110 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   }
 }
 
+void launch_tc2(const GemmDesc& g, cudaStream_t s) {
+  using namespace pair;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr_set = true;
+  }
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  encode_operand(&p.ta[0], g.A, BE_BF16, g.M, g.K, g.lda, g.a_kmajor, HM, BK);
+  encode_operand(&p.tb[0], g.B, BE_BF16, g.N, g.K, g.ldb, g.b_kmajor, HN, BK);
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.a_kmajor = g.a_kmajor; p.b_kmajor = g.b_kmajor;
+  p.tiles_m = (g.M + TM - 1) / TM;
+  p.tiles_n = (g.N + TN - 1) / TN;
+  const int pairs = ctx().num_sms / 2;
+  const int mn = p.tiles_m * p.tiles_n;
+  const int kblocks = (g.K + BK - 1) / BK;
+  int splits = 1;
+  if (mn * 2 <= pairs && kblocks >= 8) splits = std::max(1, std::min(pairs / mn, kblocks / 4));
+  int kps = (kblocks + splits - 1) / splits;
+  splits = (kblocks + kps - 1) / kps;
+  p.splits = splits;
+  p.kb_per_split = kps;
+  Block* ws = nullptr;
+  if (splits > 1) {
+    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M * g.N, s);
+    p.D = ws->ptr; p.ldd = g.N; p.d_f32 = 1; p.beta = 0.f; p.bias = nullptr; p.act = 0;
+    p.split_stride = (long long)g.M * g.N;
+  } else {
+    p.D = g.D; p.ldd = g.ldd; p.d_f32 = g.d == BE_F32; p.beta = g.beta; p.bias = g.bias; p.act = g.act;
+  }
+  const int grid = 2 * std::min(mn * splits, pairs);
+  const double ds = g.d == BE_F32 ? 4.0 : 2.0;
+  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
+  const int pidx = prof_begin("gemm_tc2_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
+  gemm_tc2_kernel<<<grid, kThreads, SMEM, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("gemm_tc2");
+  if (ws) {
+    const long long total = (long long)g.M * g.N;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, g.M, g.N, g.D, g.ldd,
+                                         g.d == BE_F32, g.beta, g.bias, g.act);
+    after_launch("gemm_splitk_reduce");
+    ctx().alloc.free(ws);
+  }
+}
+
+// Variant choice for bf16: 1-CTA (BN from pick_bn) or CTA pair 256×256.
+// BE_GEMM_PAIR=0/1 forces; otherwise shapes where both are plausible are
+// autotuned on the fly: the first two launches of a shape run one variant
+// each bracketed by CUDA events (no synchronisation), and once both events
+// have completed the faster variant is used for that shape from then on.
+struct TuneEntry {
+  int tried = 0;
+  int choice = -1;  // 0 = 1-CTA, 1 = pair
+  cudaEvent_t ev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+};
+std::mutex g_tune_mu;
+std::unordered_map<std::string, TuneEntry> g_tune;
+
+int pair_mode() {
+  static int mode = [] { const char* e = getenv("BE_GEMM_PAIR"); return e ? atoi(e) : -1; }();
+  return mode;
+}
+bool pair_plausible(const GemmDesc& g) {
+  const long tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
+  return g.M >= 256 && g.N >= 192 && tiles >= 8;
+}
+std::string tune_key(const GemmDesc& g) {
+  return std::to_string(g.M) + "x" + std::to_string(g.N) + "x" + std::to_string(g.K) + (g.a_kmajor ? "k" : "m") +
+         (g.b_kmajor ? "k" : "m") + (g.d == BE_F32 ? "f" : "h");
+}
+// returns variant to run and (optionally) the event pair to bracket it with
+int tune_pick(const GemmDesc& g, cudaEvent_t* ev0, cudaEvent_t* ev1) {
+  *ev0 = *ev1 = nullptr;
+  const int mode = pair_mode();
+  if (mode == 0) return 0;
+  if (!pair_plausible(g)) return 0;
+  if (mode == 1) return 1;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  TuneEntry& e = g_tune[tune_key(g)];
+  if (e.choice >= 0) return e.choice;
+  if (e.tried < 2) {
+    const int v = e.tried++;
+    cudaEventCreate(&e.ev[v][0]);
+    cudaEventCreate(&e.ev[v][1]);
+    *ev0 = e.ev[v][0];
+    *ev1 = e.ev[v][1];
+    return v;
+  }
+  if (cudaEventQuery(e.ev[1][1]) == cudaSuccess && cudaEventQuery(e.ev[0][1]) == cudaSuccess) {
+    float t0 = 0, t1 = 0;
+    cudaEventElapsedTime(&t0, e.ev[0][0], e.ev[0][1]);
+    cudaEventElapsedTime(&t1, e.ev[1][0], e.ev[1][1]);
+    e.choice = t1 < t0 ? 1 : 0;
+    for (auto& pr : e.ev) for (auto& x : pr) cudaEventDestroy(x);
+    return e.choice;
+  }
+  cudaGetLastError();
+  return 1;  // not measured yet: pairs are never much worse when plausible
+}
+
 int pick_bn(int M, int N, int sms, bool x3) {
   // Largest BN whose wave efficiency is within 10% of the best candidate.
   const int cands_bf16[3] = {256, 128, 64};
@@ -579,9 +851,14 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       if (bn == 128) launch_tc<128, true>(gx, ahi, alo, bhi, blo, s);
       else launch_tc<64, true>(gx, ahi, alo, bhi, blo, s);
     } else {
-      if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
+      cudaEvent_t ev0, ev1;
+      const int v = tune_pick(g, &ev0, &ev1);
+      if (ev0) cudaEventRecord(ev0, s);
+      if (v == 1) launch_tc2(g, s);
+      else if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
       else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
       else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
+      if (ev1) cudaEventRecord(ev1, s);
     }
     if (tmp) ctx().alloc.free(tmp);  // stream-ordered reuse is safe
     return "tcgen05";
