@@ -79,6 +79,115 @@ __global__ void col2im_kernel(const T* __restrict__ dcols, int64_t ldc, T* __res
   }
 }
 
+// col2im, 8 channels per thread (16-B loads of dcols / stores of dx)
+__global__ void col2im_v(const void* __restrict__ dcols, int64_t ldc, void* __restrict__ dx, ConvGeom g, float beta,
+                         int64_t nvec, be_dtype dt) {
+  const int CV = g.C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int cv = (int)(t % CV); t /= CV;
+    const int w = (int)(t % g.W); t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < g.R; ++r) {
+      const int ph = h + g.pad - r;
+      if (ph < 0 || ph % g.stride) continue;
+      const int p = ph / g.stride;
+      if (p >= g.P) continue;
+      for (int u = 0; u < g.S; ++u) {
+        const int qw = w + g.pad - u;
+        if (qw < 0 || qw % g.stride) continue;
+        const int q = qw / g.stride;
+        if (q >= g.Q) continue;
+        const int64_t m = ((int64_t)n * g.P + p) * g.Q + q;
+        V8 a = ld8(dcols, m * ldc + (int64_t)(r * g.S + u) * g.C + cv * 8, dt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += a.v[j];
+      }
+    }
+    V8 o;
+    if (beta != 0.f) o = ld8(dx, i * 8, dt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o.v[j] = acc[j] + (beta != 0.f ? o.v[j] : 0.f);
+    st8(dx, i * 8, dt, o);
+  }
+}
+
+// max pool, 8 channels per thread
+__global__ void maxpool_fwd_v(const void* __restrict__ x, void* __restrict__ y, uint8_t* __restrict__ am, ConvGeom g,
+                              be_dtype dt, int64_t nvec) {
+  const int CV = g.C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int cv = (int)(t % CV); t /= CV;
+    const int q = (int)(t % g.Q); t /= g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    float best[8];
+    int bi[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; bi[j] = -1; }
+    for (int r = 0; r < g.R; ++r) {
+      const int h = p * g.stride - g.pad + r;
+      if (h < 0 || h >= g.H) continue;
+      for (int u = 0; u < g.S; ++u) {
+        const int w = q * g.stride - g.pad + u;
+        if (w < 0 || w >= g.W) continue;
+        V8 a = ld8(x, (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * 8, dt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float v = a.v[j];
+          if (bi[j] < 0 || v > best[j] || (v != v && best[j] == best[j])) { best[j] = v; bi[j] = r * g.S + u; }
+        }
+      }
+    }
+    V8 o;
+    uint2 packed;
+    uint8_t* pb = reinterpret_cast<uint8_t*>(&packed);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { o.v[j] = best[j]; pb[j] = (uint8_t)bi[j]; }
+    st8(y, i * 8, dt, o);
+    if (am) *reinterpret_cast<uint2*>(am + i * 8) = packed;
+  }
+}
+__global__ void maxpool_bwd_v(const void* __restrict__ dy, const uint8_t* __restrict__ am, void* __restrict__ dx,
+                              ConvGeom g, be_dtype dt, float beta, int64_t nvec) {
+  const int CV = g.C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int cv = (int)(t % CV); t /= CV;
+    const int w = (int)(t % g.W); t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int p_lo = max(0, (h + g.pad - g.R + g.stride) / g.stride);
+    const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
+    const int q_lo = max(0, (w + g.pad - g.S + g.stride) / g.stride);
+    const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
+    for (int p = p_lo; p <= p_hi; ++p) {
+      const int r = h - (p * g.stride - g.pad);
+      if (r < 0 || r >= g.R) continue;
+      for (int q = q_lo; q <= q_hi; ++q) {
+        const int u = w - (q * g.stride - g.pad);
+        if (u < 0 || u >= g.S) continue;
+        const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
+        const uint2 packed = *reinterpret_cast<const uint2*>(am + o);
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&packed);
+        V8 d = ld8(dy, o, dt);
+        const int widx = r * g.S + u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += pb[j] == widx ? d.v[j] : 0.f;
+      }
+    }
+    V8 o2;
+    if (beta != 0.f) o2 = ld8(dx, i * 8, dt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o2.v[j] = acc[j] + (beta != 0.f ? o2.v[j] : 0.f);
+    st8(dx, i * 8, dt, o2);
+  }
+}
+
 __global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
   const int64_t RSC = (int64_t)g.R * g.S * g.C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -259,6 +368,203 @@ __global__ void bn_dx_kernel(const void* gy, const void* x, const void* yv, int 
   }
 }
 
+// ---- vectorised BN (C % 8 == 0, 16-B aligned): thread owns 8 consecutive
+// channels of one row; a block covers up to 2048 channels × (256/(C/8)) rows
+// per iteration; fixed-order smem combine → deterministic partials.
+constexpr int kBnCG = 2048;  // channels per block group
+template <int MODE>  // 0: Σ(x−K), Σ(x−K)² with K = x[0,c] (shifted sums); 2: Σg', Σg'·x̂
+__global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, const void* __restrict__ gy,
+                                                   const void* __restrict__ yv, int act, int64_t rows, int C,
+                                                   be_dtype dt, const float* __restrict__ mean,
+                                                   const float* __restrict__ invstd, float* __restrict__ part0,
+                                                   float* __restrict__ part1, int64_t rows_per_split) {
+  __shared__ float sm0[kBnCG], sm1[kBnCG];
+  const int base = blockIdx.x * kBnCG;
+  const int Cg = min(kBnCG, C - base);
+  const int lanes = Cg / 8, rpi = 256 / lanes;
+  const int t = threadIdx.x, v = t % lanes, rl = t / lanes;
+  const int c = base + v * 8;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (rl < rpi) {
+    float k[8], is[8];
+    if (MODE == 0) {
+      V8 kk = ld8(x, c, dt);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) k[j] = kk.v[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { k[j] = mean[c + j]; is[j] = invstd[c + j]; }
+    }
+    for (int64_t r = r0 + rl; r < r1; r += rpi) {
+      const int64_t o = r * C + c;
+      V8 a = ld8(x, o, dt);
+      if (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { const float d = a.v[j] - k[j]; s0[j] += d; s1[j] += d * d; }
+      } else {
+        V8 g = ld8(gy, o, dt);
+        if (act) {
+          V8 yy = ld8(yv, o, dt);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { s0[j] += g.v[j]; s1[j] += g.v[j] * (a.v[j] - k[j]) * is[j]; }
+      }
+    }
+  }
+  // rpi·Cg ≤ 2048: every lane's partials fit; combine over row lanes in order
+  if (rl < rpi) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { sm0[rl * Cg + v * 8 + j] = s0[j]; sm1[rl * Cg + v * 8 + j] = s1[j]; }
+  }
+  __syncthreads();
+  for (int i = t; i < Cg; i += 256) {
+    float a0 = 0.f, a1 = 0.f;
+    for (int w = 0; w < rpi; ++w) { a0 += sm0[w * Cg + i]; a1 += sm1[w * Cg + i]; }
+    part0[(int64_t)blockIdx.y * C + base + i] = a0;
+    part1[(int64_t)blockIdx.y * C + base + i] = a1;
+  }
+}
+__global__ void bn_stats_finalize_v(const float* p0, const float* p1, int splits, int C, int64_t rows, const void* x,
+                                    be_dtype dt, float eps, float* mean, float* invstd, float* run_mean,
+                                    float* run_var, float momentum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s1 = 0, s2 = 0;
+  for (int i = 0; i < splits; ++i) { s1 += p0[(int64_t)i * C + c]; s2 += p1[(int64_t)i * C + c]; }
+  const double n = (double)rows;
+  const double ms = s1 / n;
+  double var = s2 / n - ms * ms;  // biased (normalisation)
+  if (var < 0) var = 0;
+  const float mu = ld(x, c, dt) + (float)ms;
+  mean[c] = mu;
+  invstd[c] = rsqrtf((float)var + eps);
+  if (run_mean) run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mu;
+  if (run_var) run_var[c] = (1.f - momentum) * run_var[c] + momentum * (float)(var * n / (rows > 1 ? n - 1 : 1));
+}
+// Element-wise BN kernels with a 2-D mapping: thread t owns channel vector
+// t % lanes for the whole launch (per-channel constants live in registers)
+// and walks rows (t / lanes) + k·rpi of its row block.
+__global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, void* __restrict__ y, int64_t rows,
+                                                  int C, be_dtype dt, const float* __restrict__ mean,
+                                                  const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                                  const float* __restrict__ beta, int act, int64_t rows_per_block) {
+  const int base = blockIdx.x * kBnCG;
+  const int Cg = min(kBnCG, C - base);
+  const int lanes = Cg / 8, rpi = 256 / lanes;
+  const int t = threadIdx.x, v = t % lanes, rl = t / lanes;
+  if (rl >= rpi) return;
+  const int c = base + v * 8;
+  float sc[8], sh[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sc[j] = gamma[c + j] * invstd[c + j];
+    sh[j] = beta[c + j] - mean[c + j] * sc[j];
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  for (int64_t r = r0 + rl; r < r1; r += rpi) {
+    const int64_t o = r * C + c;
+    V8 a = ld8(x, o, dt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float val = fmaf(a.v[j], sc[j], sh[j]);
+      a.v[j] = act ? fmaxf(val, 0.f) : val;
+    }
+    st8(y, o, dt, a);
+  }
+}
+__global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, const void* __restrict__ x,
+                                               const void* __restrict__ yv, int act, void* dx, int64_t rows, int C,
+                                               be_dtype dt, const float* __restrict__ mean,
+                                               const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                               const float* __restrict__ sums, float dx_beta, int64_t rows_per_block) {
+  const int base = blockIdx.x * kBnCG;
+  const int Cg = min(kBnCG, C - base);
+  const int lanes = Cg / 8, rpi = 256 / lanes;
+  const int t = threadIdx.x, v = t % lanes, rl = t / lanes;
+  if (rl >= rpi) return;
+  const int c = base + v * 8;
+  // dx = γ·is·(g' − Σg'/n − x̂·Σg'x̂/n),  x̂ = (x − μ)·is   ⇒  dx = k1·g' + k2·x + k3
+  const float inv_n = 1.f / (float)rows;
+  float k1[8], k2[8], k3[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float is = invstd[c + j], a = gamma[c + j] * is;
+    const float m1 = sums[c + j] * inv_n, m2 = sums[C + c + j] * inv_n;
+    k1[j] = a;
+    k2[j] = -a * m2 * is;
+    k3[j] = -a * m1 + a * m2 * is * mean[c + j];
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  for (int64_t r = r0 + rl; r < r1; r += rpi) {
+    const int64_t o = r * C + c;
+    V8 g = ld8(gy, o, dt), a = ld8(x, o, dt);
+    if (act) {
+      V8 yy = ld8(yv, o, dt);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
+    }
+    V8 out;
+    if (dx_beta != 0.f) out = ld8(dx, o, dt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float val = fmaf(k1[j], g.v[j], fmaf(k2[j], a.v[j], k3[j]));
+      out.v[j] = val + (dx_beta != 0.f ? out.v[j] : 0.f);
+    }
+    st8(dx, o, dt, out);
+  }
+}
+// Cooperative fixed-order finalize: 8 threads per channel each sum a strided
+// subset of the split partials, then combine in lane order.
+template <int MODE>  // 0: stats, 2: grads
+__global__ void __launch_bounds__(1024) bn_finalize_v(const float* __restrict__ p0, const float* __restrict__ p1,
+                                                      int splits, int C, int64_t rows, const void* x, be_dtype dt,
+                                                      float eps, float* mean, float* invstd, float* run_mean,
+                                                      float* run_var, float momentum, float* dgamma, float* dbeta,
+                                                      float gb_beta, float* sums) {
+  // 32 channels × 32 sub-lanes; each sub-lane sums every 32nd split (4 loads in flight)
+  __shared__ double s0[32][33], s1[32][33];
+  const int cl = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  double a0 = 0, a1 = 0;
+  if (c < C) {
+    int i = sub;
+    for (; i + 96 < splits; i += 128) {
+      const float x0 = p0[(int64_t)i * C + c], x1 = p0[(int64_t)(i + 32) * C + c];
+      const float x2 = p0[(int64_t)(i + 64) * C + c], x3 = p0[(int64_t)(i + 96) * C + c];
+      const float y0 = p1[(int64_t)i * C + c], y1 = p1[(int64_t)(i + 32) * C + c];
+      const float y2 = p1[(int64_t)(i + 64) * C + c], y3 = p1[(int64_t)(i + 96) * C + c];
+      a0 += (double)x0; a0 += (double)x1; a0 += (double)x2; a0 += (double)x3;
+      a1 += (double)y0; a1 += (double)y1; a1 += (double)y2; a1 += (double)y3;
+    }
+    for (; i < splits; i += 32) { a0 += p0[(int64_t)i * C + c]; a1 += p1[(int64_t)i * C + c]; }
+  }
+  s0[sub][cl] = a0;
+  s1[sub][cl] = a1;
+  __syncthreads();
+  if (sub != 0 || c >= C) return;
+  double t0 = 0, t1 = 0;
+  for (int k = 0; k < 32; ++k) { t0 += s0[k][cl]; t1 += s1[k][cl]; }
+  if (MODE == 0) {
+    const double n = (double)rows;
+    const double ms = t0 / n;
+    double var = t1 / n - ms * ms;  // biased (normalisation)
+    if (var < 0) var = 0;
+    const float mu = ld(x, c, dt) + (float)ms;
+    mean[c] = mu;
+    invstd[c] = rsqrtf((float)var + eps);
+    if (run_mean) run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mu;
+    if (run_var) run_var[c] = (1.f - momentum) * run_var[c] + momentum * (float)(var * n / (rows > 1 ? n - 1 : 1));
+  } else {
+    sums[c] = (float)t0;
+    sums[C + c] = (float)t1;
+    if (dbeta) dbeta[c] = (float)t0 + (gb_beta != 0.f ? dbeta[c] : 0.f);
+    if (dgamma) dgamma[c] = (float)t1 + (gb_beta != 0.f ? dgamma[c] : 0.f);
+  }
+}
+
 // ---- embedding gather
 __global__ void embedding_fwd_kernel(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out,
                                      be_dtype od) {
@@ -314,6 +620,11 @@ void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype 
 void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtype dt, float beta, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
+  if (g.C % 8 == 0 && ldc % 8 == 0 && aligned16(dcols) && aligned16(dx)) {
+    col2im_v<<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, total / 8, dt);
+    after_launch("col2im_v");
+    return;
+  }
   if (dt == BE_BF16)
     col2im_kernel<uint16_t><<<grid_for(total), 256, 0, s>>>((const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, total, dt);
   else
@@ -329,6 +640,11 @@ void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
 void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.C;
   if (total == 0) return;
+  if (g.C % 8 == 0 && aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
+    maxpool_fwd_v<<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, total / 8);
+    after_launch("maxpool_fwd_v");
+    return;
+  }
   maxpool_fwd_kernel<<<grid_for(total), 256, 0, s>>>(x, y, am, g, dt, total);
   after_launch("maxpool_fwd");
 }
@@ -336,6 +652,11 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
                  cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
+  if (g.C % 8 == 0 && aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
+    maxpool_bwd_v<<<grid_for(total / 8), 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
+    after_launch("maxpool_bwd_v");
+    return;
+  }
   maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(dy, am, dx, g, dt, beta, total);
   after_launch("maxpool_bwd");
 }
@@ -357,8 +678,43 @@ static int64_t bn_splits(int64_t rows, int C) {
   int64_t sp = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)ctx().num_sms * 4 / cg));
   return std::min<int64_t>(sp, 2048);
 }
+static bool bn_vec_ok(const void* a, int C) { return C % 8 == 0 && aligned16(a); }
+// 2-D grid for the element-wise BN kernels: ~16 row-iterations per thread,
+// capped at 16 blocks per SM worth of row blocks.
+static int64_t bn_rows_per_block(int64_t rows, int C, dim3* grid) {
+  const int64_t cg = (C + kBnCG - 1) / kBnCG;
+  const int64_t lanes = std::max(1, std::min(C, kBnCG) / 8);
+  const int64_t rpi = std::max<int64_t>(1, 256 / lanes);
+  int64_t rpb = rpi * 16;
+  int64_t nb = (rows + rpb - 1) / rpb;
+  const int64_t cap = (int64_t)ctx().num_sms * 16 / cg;
+  if (nb > cap) { nb = cap; rpb = (rows + nb - 1) / nb; }
+  *grid = dim3((unsigned)cg, (unsigned)std::max<int64_t>(1, nb));
+  return rpb;
+}
+static int64_t bn_splits_v(int64_t rows, int C) {
+  const int64_t cg = (C + kBnCG - 1) / kBnCG;
+  const int64_t lanes = std::max(1, std::min(C, kBnCG) / 8);
+  const int64_t rpi = std::max<int64_t>(1, 256 / lanes);
+  // ≥ 8 rows per thread, ≈ 4 blocks per SM
+  int64_t sp = std::max<int64_t>(1, std::min<int64_t>(rows / (rpi * 8) + 1, (int64_t)ctx().num_sms * 4 / cg));
+  return std::min<int64_t>(sp, 4096);
+}
 void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float* mean, float* invstd, float* partial,
               float* run_mean, float* run_var, float momentum, cudaStream_t s) {
+  if (bn_vec_ok(x, C)) {
+    const int64_t sp = bn_splits_v(rows, C);
+    const int64_t rps = (rows + sp - 1) / sp;
+    dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
+    bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
+                                        partial + sp * C, rps);
+    after_launch("bn_stats_v");
+    bn_finalize_v<0><<<(C + 31) / 32, 1024, 0, s>>>(partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
+                                                    invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
+                                                    nullptr);
+    after_launch("bn_stats_finalize_v");
+    return;
+  }
   const int64_t sp = bn_splits(rows, C);
   const int64_t rps = (rows + sp - 1) / sp;
   dim3 grid((C + 63) / 64, (unsigned)sp);
@@ -376,6 +732,13 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
               const float* gamma, const float* beta, int act, cudaStream_t s) {
   const int64_t total = rows * C;
   if (total == 0) return;
+  if (bn_vec_ok(x, C) && aligned16(y)) {
+    dim3 grid;
+    const int64_t rpb = bn_rows_per_block(rows, C, &grid);
+    bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb);
+    after_launch("bn_apply_v");
+    return;
+  }
   bn_apply_kernel<<<grid_for(total), 256, 0, s>>>(x, y, total, C, dt, mean, invstd, gamma, beta, act);
   after_launch("bn_apply");
 }
@@ -383,6 +746,26 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta, float gb_beta,
             float dx_beta, float* partial, cudaStream_t s) {
   // partial must hold 2*splits*C + 2*C floats
+  if (bn_vec_ok(x, C) && aligned16(dy) && (!act || aligned16(y)) && (!dx || aligned16(dx))) {
+    const int64_t sp = bn_splits_v(rows, C);
+    const int64_t rps = (rows + sp - 1) / sp;
+    float* p0 = partial;
+    float* p1 = partial + sp * C;
+    float* sums = partial + 2 * sp * C;
+    dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
+    bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps);
+    after_launch("bn_bwd_reduce_v");
+    bn_finalize_v<2><<<(C + 31) / 32, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
+                                                    nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
+    after_launch("bn_bwd_finalize_v");
+    if (dx) {
+      dim3 g2;
+      const int64_t rpb = bn_rows_per_block(rows, C, &g2);
+      bn_dx_v<<<g2, 256, 0, s>>>(dy, x, y, act, dx, rows, C, dt, mean, invstd, gamma, sums, dx_beta, rpb);
+      after_launch("bn_bwd_dx_v");
+    }
+    return;
+  }
   const int64_t sp = bn_splits(rows, C);
   const int64_t rps = (rows + sp - 1) / sp;
   float* p0 = partial;
@@ -400,7 +783,9 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
     after_launch("bn_bwd_dx");
   }
 }
-size_t bn_partial_floats(int64_t rows, int C) { return (size_t)(2 * bn_splits(rows, C) * C + 2 * C); }
+size_t bn_partial_floats(int64_t rows, int C) {
+  return (size_t)(2 * std::max(bn_splits(rows, C), bn_splits_v(rows, C)) * C + 2 * C);
+}
 
 void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,
                    cudaStream_t s) {

@@ -57,6 +57,9 @@ struct __align__(64) GemmParams {
   float beta;
   const float* bias;
   int act;
+  // implicit-GEMM convolution (A gathered from NHWC x; unused by plain GEMMs)
+  const uint16_t* x;
+  int cN, cH, cW, cC, cR, cS, cstride, cpad, cP, cQ;
 };
 
 template <int BN, bool X3>
@@ -456,6 +459,184 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- implicit-GEMM convolution
+// Y[m = (n,p,q), k] = Σ_{r,s,c} x[n, p·st−pad+r, q·st−pad+s, c] · W[k, r, s, c]
+// without materialising im2col: 4 producer warps gather the A tile (one
+// output pixel per thread, 8 × 16-B cp.async per 64-channel k-block, zero
+// fill in the padding) straight into the SW128 layout UMMA expects (16-B
+// chunk j of row r stored at j ^ (r & 7)); B (KRSC weights, K-major) comes
+// by TMA; MMA issue / TMEM / epilogue as gemm_tc_kernel.  Requires C % 64 == 0
+// so a k-block is 64 channels of one filter tap.
+namespace conv {
+constexpr int kThreads = 384;   // w0-3 A gather, w4 B TMA, w5 MMA, w6 TMEM, w7 idle, w8-11 epilogue
+constexpr int LAG = 3;          // cp.async groups kept in flight per producer thread
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+}  // namespace conv
+
+template <int BN>
+__global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid_constant__ GemmParams p) {
+  using C = conv::Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    // full: 128 gather threads + 1 TMA expect_tx arrival
+    for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 129); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 6) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int CB = p.cC / 64;                          // k-blocks per tap
+  const int kblocks = p.cR * p.cS * CB;
+
+  if (warp < 4) {
+    // ===================== A gather producers =====================
+    const int tid = threadIdx.x;  // tile row
+    int stage = 0; uint32_t phase = 0;
+    int pend_stage[conv::LAG + 1];
+    int npend = 0;  // groups committed but not yet signalled (FIFO)
+    int head = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int tm = t % p.tiles_m;
+      const int m = tm * BM + tid;
+      const bool row_ok = m < p.M;
+      int n = 0, hb = 0, wb = 0;
+      if (row_ok) {
+        const int q = m % p.cQ;
+        const int pq = m / p.cQ;
+        const int pp = pq % p.cP;
+        n = pq / p.cP;
+        hb = pp * p.cstride - p.cpad;
+        wb = q * p.cstride - p.cpad;
+      }
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int tap = kb / CB, cb = kb - tap * CB;
+        const int r = tap / p.cS, s = tap - r * p.cS;
+        const int h = hb + r, w = wb + s;
+        const bool ok = row_ok && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
+        const uint16_t* src = ok ? p.x + (((long long)n * p.cH + h) * p.cW + w) * p.cC + cb * 64 : p.x;
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t dst = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + tid * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          sm100::cp_async_16(dst + ((j ^ (tid & 7)) << 4), src + j * 8, ok ? 16u : 0u);
+        sm100::cp_async_commit();
+        pend_stage[(head + npend) % (conv::LAG + 1)] = stage;
+        ++npend;
+        if (npend > conv::LAG) {
+          // oldest group complete → make it visible to the async proxy, then signal
+          sm100::cp_async_wait<conv::LAG>();
+          sm100::fence_proxy_async();
+          sm100::mbar_arrive(&full[pend_stage[head]]);
+          head = (head + 1) % (conv::LAG + 1);
+          --npend;
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    while (npend > 0) {
+      sm100::mbar_arrive(&full[pend_stage[head]]);
+      head = (head + 1) % (conv::LAG + 1);
+      --npend;
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      // ===================== B (weights) TMA producer =====================
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int tn = t / p.tiles_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
+          sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ===================== MMA issuer =====================
+      const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 0, 0);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * C::STAGE_BYTES), sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sm100::make_sw128_desc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb + kk * 32, 16, 1024);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue =====================
+    const int ew = warp - 8;
+    int acc = 0; uint32_t acc_phase = 0;
+    const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = tm * BM + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int col0 = tn * BN + c0;
+        if (col0 >= p.N) break;
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -813,6 +994,50 @@ int pick_bn(int M, int N, int sms, bool x3) {
 }
 
 }  // namespace
+
+template <int BN>
+void launch_conv(GemmParams& p, cudaStream_t s) {
+  using C = conv::Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_n = (p.N + BN - 1) / BN;
+  const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
+  conv_tc_kernel<BN><<<grid, conv::kThreads, C::SMEM, s>>>(p);
+}
+
+bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
+                   float beta, cudaStream_t s) {
+  if (g.C % 64 != 0 || g.K % 16 != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+  const char* e = getenv("BE_CONV_IMPLICIT");
+  if (e && e[0] == '0') return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const int RSC = g.R * g.S * g.C;
+  p.M = g.N * g.P * g.Q; p.N = g.K; p.K = RSC;
+  p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
+  p.D = y; p.ldd = g.K; p.d_f32 = yd == BE_F32; p.beta = beta; p.bias = bias; p.act = act;
+  p.x = reinterpret_cast<const uint16_t*>(x);
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
+  p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
+  const int bn = g.K >= 256 ? 256 : (g.K >= 128 ? 128 : 64);
+  encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
+  const double flops = 2.0 * p.M * (double)g.K * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 +
+                       (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
+  const int pidx = prof_begin("conv_tc_implicit", flops, bytes, p.M, g.K, RSC, s);
+  if (bn == 256) launch_conv<256>(p, s);
+  else if (bn == 128) launch_conv<128>(p, s);
+  else launch_conv<64>(p, s);
+  prof_end(pidx, s);
+  after_launch("conv_tc_implicit");
+  g_tc_calls++;
+  return true;
+}
 
 uint64_t gemm_tcgen05_calls() { return g_tc_calls.load(); }
 uint64_t gemm_simt_calls() { return g_simt_calls.load(); }

@@ -36,6 +36,9 @@ void split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s)
 void relu_fwd(const void* x, void* y, int64_t n, be_dtype dt, cudaStream_t s);
 // dx (+)= dy * [y > 0]
 void relu_bwd(const void* dy, const void* y, void* dx, int64_t n, be_dtype dt, float beta, cudaStream_t s);
+// d1 (+)= dy·[y>0], d2 (+)= dy·[y>0] in one pass (residual add+ReLU backward); d1/d2 may be null
+void relu_bwd2(const void* dy, const void* y, void* d1, float b1, void* d2, float b2, int64_t n, be_dtype dt,
+               cudaStream_t s);
 // y = a + b with b broadcast: general strided (rank<=6) over out shape
 struct BcastDesc {
   int rank;
@@ -80,6 +83,10 @@ void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float
 struct ConvGeom {
   int N, H, W, C, K, R, S, stride, pad, P, Q;
 };
+// Implicit-GEMM convolution on tcgen05 (bf16, C % 64 == 0): y[NPQ, K] =
+// conv(x NHWC, w KRSC) (+bias, act, beta). Returns false when unsupported.
+bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
+                   float beta, cudaStream_t s);
 // cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC
 void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s);
 // dx NHWC (+)= col2im(dcols)   (gather formulation, deterministic)

@@ -289,6 +289,35 @@ static bool trailing_block(const Tensor* out, const Tensor* in) {
 static void vjp_add(Node* n, GradSink& sink) {
   Tensor* g = sink.upstream[0];
   const int act = (int)n->iattr[0];
+  if (act && g->is_contiguous()) {
+    // fused: both inputs receive dy·1[y>0] from one pass when shapes match
+    TRef hy;
+    Tensor* y = unpack(n, 0, hy);
+    const int64_t ne = g->numel();
+    float b0 = 0.f, b1 = 0.f;
+    Tensor* d0 = sink.needs(0) ? sink.dest(0, &b0) : nullptr;
+    Tensor* d1 = sink.needs(1) ? sink.dest(1, &b1) : nullptr;
+    const bool ok0 = !d0 || (d0->numel() == ne && d0->dtype == g->dtype && d0->is_contiguous());
+    const bool ok1 = !d1 || (d1->numel() == ne && d1->dtype == g->dtype && d1->is_contiguous() && d1 != d0);
+    if (ok0 && ok1) {
+      k::relu_bwd2(g->data(), y->data(), d0 ? d0->data() : nullptr, b0, d1 ? d1->data() : nullptr, b1, ne, g->dtype,
+                   ctx().stream);
+      if (d0) sink.commit(0);
+      if (d1) sink.commit(1);
+      return;
+    }
+    // general path below (broadcast or aliasing): destinations already acquired
+    TRef dz = new_tensor(g->shape, g->rank, g->dtype);
+    k::relu_bwd(g->data(), y->data(), dz->data(), ne, g->dtype, 0.f, ctx().stream);
+    if (d0) { unbroadcast_into(dz.get(), d0, b0); sink.commit(0); }
+    if (d1) {
+      float bb = b1;
+      if (d1 == d0) bb = 1.f;  // same tensor added twice
+      unbroadcast_into(dz.get(), d1, bb);
+      sink.commit(1);
+    }
+    return;
+  }
   TRef dz;
   if (act) {
     TRef hy;

@@ -120,7 +120,9 @@ static void op_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor*
   const int64_t M = (int64_t)g.N * g.P * g.Q, RSC = (int64_t)g.R * g.S * g.C;
   const be_dtype od = (a.out_f32 || ctx().compute == BE_F32) ? BE_F32 : BE_BF16;
   TRef y = new_tensor({g.N, g.P, g.Q, g.K}, od);
-  {
+  if (is_pointwise(g) || x->dtype != BE_BF16 ||
+      !k::conv_implicit(x->data(), w->data(), y->data(), g, od, b ? b->ptr<float>() : nullptr, a.act, 0.f,
+                        ctx().stream)) {
     int64_t ldc;
     TRef cols = make_cols(x.get(), g, &ldc);
     k::GemmDesc gd;

@@ -103,6 +103,30 @@ struct ReluBwdF {
     st8(dx, i, dt, o);
   }
 };
+// residual add+ReLU backward: both inputs get dy·1[y>0] in one pass
+struct ReluBwd2F {
+  const void* dy; const void* y; void* d1; float b1; void* d2; float b2; be_dtype dt;
+  __device__ void one(int64_t i) const {
+    const float g = ld(y, i, dt) > 0.f ? ld(dy, i, dt) : 0.f;
+    if (d1) st(d1, i, dt, g + (b1 != 0.f ? ld(d1, i, dt) : 0.f));
+    if (d2) st(d2, i, dt, g + (b2 != 0.f ? ld(d2, i, dt) : 0.f));
+  }
+  __device__ void vec(int64_t i) const {
+    V8 g = ld8(dy, i, dt), yy = ld8(y, i, dt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
+    if (d1) {
+      V8 o = g;
+      if (b1 != 0.f) { V8 p = ld8(d1, i, dt); for (int j = 0; j < 8; ++j) o.v[j] += p.v[j]; }
+      st8(d1, i, dt, o);
+    }
+    if (d2) {
+      V8 o = g;
+      if (b2 != 0.f) { V8 p = ld8(d2, i, dt); for (int j = 0; j < 8; ++j) o.v[j] += p.v[j]; }
+      st8(d2, i, dt, o);
+    }
+  }
+};
 struct AddF {
   const void* a; const void* b; void* y; be_dtype dt; int act;
   __device__ void one(int64_t i) const {
@@ -480,6 +504,11 @@ void relu_fwd(const void* x, void* y, int64_t n, be_dtype dt, cudaStream_t s) {
 }
 void relu_bwd(const void* dy, const void* y, void* dx, int64_t n, be_dtype dt, float beta, cudaStream_t s) {
   launch_ew(n, aligned16(dy) && aligned16(y) && aligned16(dx), ReluBwdF{dy, y, dx, dt, beta}, s, "relu_bwd");
+}
+void relu_bwd2(const void* dy, const void* y, void* d1, float b1, void* d2, float b2, int64_t n, be_dtype dt,
+               cudaStream_t s) {
+  const bool vec = aligned16(dy) && aligned16(y) && (!d1 || aligned16(d1)) && (!d2 || aligned16(d2));
+  launch_ew(n, vec, ReluBwd2F{dy, y, d1, b1, d2, b2, dt}, s, "relu_bwd2");
 }
 void add_same(const void* a, const void* b, void* y, int64_t n, be_dtype dt, int act, cudaStream_t s) {
   launch_ew(n, aligned16(a) && aligned16(b) && aligned16(y), AddF{a, b, y, dt, act}, s, "add");

@@ -61,12 +61,36 @@ def test_conv_op_fp32(cfg, act):
     assert rel(bd.grad.numpy(), bo.grad) < 1e-4
 
 
+@pytest.mark.parametrize("cfg", [(2, 64, 9, 9, 64, 3, 1, 1), (2, 64, 10, 10, 128, 3, 2, 1), (1, 128, 7, 7, 256, 3, 1, 1),
+                                 (2, 64, 14, 14, 64, 1, 2, 0), (3, 64, 17, 13, 96, 3, 1, 1), (1, 192, 5, 5, 320, 3, 1, 1)])
+def test_conv_op_bf16_implicit_gemm(cfg):
+    """bf16 conv forward through the implicit-GEMM kernel (cp.async gather, no
+    im2col) vs the oracle on the same bf16-rounded x and W: fp32 accumulate,
+    one bf16 rounding of the output (≤ 2^-8 relative) → gate 1e-2."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    N, C, H, W, K, R, st, pd = cfg
+    rng = np.random.default_rng(sum(cfg))
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(a.astype(np.float32)))
+    x = q(rng.standard_normal((N, C, H, W)))
+    w = q(rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R))
+    b = rng.standard_normal(K).astype(np.float32)
+    yo = oops.relu(oops.conv2d(Var(x.astype(np.float64)), Var(w.astype(np.float64)), Var(b.astype(np.float64)), st, pd))
+    calls0 = be.launch_count()
+    yd = be.conv2d(be.tensor(nchw_to_nhwc(x), dtype="bf16"), be.tensor(nchw_to_nhwc(w), requires_grad=True),
+                   be.tensor(b), st, pd, act=1)
+    assert rel(nhwc_to_nchw(yd.numpy()), yo.value) < 1e-2
+    assert be.launch_count() - calls0 <= 3  # weight shadow cast + one conv kernel (no im2col)
+
+
+@pytest.mark.parametrize("C", [5, 16])
 @pytest.mark.parametrize("k,s,p", [(3, 2, 0), (3, 2, 1)])
-def test_maxpool_op_and_argmax_bit_exact(k, s, p):
+def test_maxpool_op_and_argmax_bit_exact(k, s, p, C):
     be = be_init()
     be.set_compute_dtype("f32")
     rng = np.random.default_rng(k + s + p)
-    x = rng.standard_normal((2, 5, 13, 13)).astype(np.float32)
+    x = rng.standard_normal((2, C, 13, 13)).astype(np.float32)
     x[0, 0, :4, :4] = 0.0  # tied windows → first index
     xo = Var(x.astype(np.float64), True)
     yo, am = oops.maxpool2d(xo, k, s, p)
@@ -87,14 +111,15 @@ def test_maxpool_op_and_argmax_bit_exact(k, s, p):
     assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-6
 
 
-def test_avgpool_bn_add_ops_fp32():
+@pytest.mark.parametrize("C", [6, 24])
+def test_avgpool_bn_add_ops_fp32(C):
     be = be_init()
     be.set_compute_dtype("f32")
     rng = np.random.default_rng(11)
-    x = (rng.standard_normal((4, 6, 5, 5)) * 2 + 0.5).astype(np.float32)
-    r = rng.standard_normal((4, 6, 5, 5)).astype(np.float32)
-    gam = (rng.standard_normal(6) + 1).astype(np.float32)
-    bet = rng.standard_normal(6).astype(np.float32)
+    x = (rng.standard_normal((4, C, 5, 5)) * 2 + 0.5).astype(np.float32)
+    r = rng.standard_normal((4, C, 5, 5)).astype(np.float32)
+    gam = (rng.standard_normal(C) + 1).astype(np.float32)
+    bet = rng.standard_normal(C).astype(np.float32)
     xo, ro = Var(x.astype(np.float64), True), Var(r.astype(np.float64), True)
     go, bo = Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
     yo, (rm, rv) = oops.batchnorm2d(xo, go, bo)
@@ -103,7 +128,7 @@ def test_avgpool_bn_add_ops_fp32():
     backward(zo, g)
     xd, rd = be.tensor(nchw_to_nhwc(x), requires_grad=True), be.tensor(nchw_to_nhwc(r), requires_grad=True)
     gd, bd = be.tensor(gam, requires_grad=True), be.tensor(bet, requires_grad=True)
-    rmd, rvd = be.tensor(np.zeros(6, np.float32)), be.tensor(np.ones(6, np.float32))
+    rmd, rvd = be.tensor(np.zeros(C, np.float32)), be.tensor(np.ones(C, np.float32))
     yd = be.batchnorm2d(xd, gd, bd, rmd, rvd)
     zd = be.avgpool_global(be.add_relu(yd, rd))
     zd.backward(be.tensor(g.astype(np.float32)))
