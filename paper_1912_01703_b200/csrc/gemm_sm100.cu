@@ -468,8 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // by TMA; MMA issue / TMEM / epilogue as gemm_tc_kernel.  Requires C % 64 == 0
 // so a k-block is 64 channels of one filter tap.
 namespace conv {
-constexpr int kThreads = 384;   // w0-3 A gather, w4 B TMA, w5 MMA, w6 TMEM, w7 idle, w8-11 epilogue
-constexpr int LAG = 3;          // cp.async groups kept in flight per producer thread
+constexpr int kThreads = 256;   // w0 TMA gather/tile producer, w1 MMA, w2 TMEM, w4-7 epilogue
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
@@ -495,12 +494,12 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
 
   if (threadIdx.x == 0) {
     // full: 128 gather threads + 1 TMA expect_tx arrival
-    for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 129); sm100::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
     sm100::fence_barrier_init();
-    sm100::tma_prefetch(&p.tb[0]);
+    sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
   }
-  if (warp == 6) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 2) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -510,73 +509,48 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   const int CB = p.cC / 64;                          // k-blocks per tap
   const int kblocks = p.cR * p.cS * CB;
 
-  if (warp < 4) {
-    // ===================== A gather producers =====================
-    const int tid = threadIdx.x;  // tile row
+  if (warp == 0) {
+    // ===================== producer: A by TMA row-gather, B by TMA tile =====================
+    // lane l owns tile rows 4l..4l+3; per k-block (tap r,s; 64 channels) it
+    // issues one tile::gather4 of those rows (−1 = padding → zero fill).
     int stage = 0; uint32_t phase = 0;
-    int pend_stage[conv::LAG + 1];
-    int npend = 0;  // groups committed but not yet signalled (FIFO)
-    int head = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int tm = t % p.tiles_m;
-      const int m = tm * BM + tid;
-      const bool row_ok = m < p.M;
-      int n = 0, hb = 0, wb = 0;
-      if (row_ok) {
-        const int q = m % p.cQ;
-        const int pq = m / p.cQ;
-        const int pp = pq % p.cP;
-        n = pq / p.cP;
-        hb = pp * p.cstride - p.cpad;
-        wb = q * p.cstride - p.cpad;
+      const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      int nb[4], hb[4], wb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = tm * BM + lane * 4 + i;
+        if (m < p.M) {
+          const int q = m % p.cQ, pq = m / p.cQ;
+          const int pp = pq % p.cP;
+          nb[i] = (pq / p.cP) * p.cH;
+          hb[i] = pp * p.cstride - p.cpad;
+          wb[i] = q * p.cstride - p.cpad;
+        } else {
+          nb[i] = 0; hb[i] = -(1 << 20); wb[i] = 0;  // always out of range
+        }
       }
       for (int kb = 0; kb < kblocks; ++kb) {
         const int tap = kb / CB, cb = kb - tap * CB;
         const int r = tap / p.cS, s = tap - r * p.cS;
-        const int h = hb + r, w = wb + s;
-        const bool ok = row_ok && h >= 0 && h < p.cH && w >= 0 && w < p.cW;
-        const uint16_t* src = ok ? p.x + (((long long)n * p.cH + h) * p.cW + w) * p.cC + cb * 64 : p.x;
-        sm100::mbar_wait(&empty[stage], phase ^ 1);
-        const uint32_t dst = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + tid * 128;
+        int rc[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          sm100::cp_async_16(dst + ((j ^ (tid & 7)) << 4), src + j * 8, ok ? 16u : 0u);
-        sm100::cp_async_commit();
-        pend_stage[(head + npend) % (conv::LAG + 1)] = stage;
-        ++npend;
-        if (npend > conv::LAG) {
-          // oldest group complete → make it visible to the async proxy, then signal
-          sm100::cp_async_wait<conv::LAG>();
-          sm100::fence_proxy_async();
-          sm100::mbar_arrive(&full[pend_stage[head]]);
-          head = (head + 1) % (conv::LAG + 1);
-          --npend;
+        for (int i = 0; i < 4; ++i) {
+          const int h = hb[i] + r, w = wb[i] + s;
+          rc[i] = (h >= 0 && h < p.cH && w >= 0 && w < p.cW) ? (nb[i] + h) * p.cW + w : -1;
         }
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
+        }
+        __syncwarp();
+        const uint32_t dst = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + lane * 4 * 128;
+        sm100::tma_gather4(&p.ta[0], &full[stage], dst, cb * 64, rc[0], rc[1], rc[2], rc[3]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    sm100::cp_async_wait<0>();
-    sm100::fence_proxy_async();
-    while (npend > 0) {
-      sm100::mbar_arrive(&full[pend_stage[head]]);
-      head = (head + 1) % (conv::LAG + 1);
-      --npend;
-    }
-  } else if (warp == 4) {
-    if (lane == 0) {
-      // ===================== B (weights) TMA producer =====================
-      int stage = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int tn = t / p.tiles_m;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
-          sm100::mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
-          sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 5) {
+  } else if (warp == 1) {
     if (lane == 0) {
       // ===================== MMA issuer =====================
       const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 0, 0);
@@ -603,9 +577,9 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int ew = warp - 8;
+    const int ew = warp - 4;
     int acc = 0; uint32_t acc_phase = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -631,7 +605,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 6) {
+  if (warp == 2) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
@@ -1026,6 +1000,8 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
   const int bn = g.K >= 256 ? 256 : (g.K >= 128 ? 128 : 64);
   encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
+  // x as a 2-D [N·H·W, C] matrix; tile::gather4 needs box {64, 1}
+  encode_2d(&p.ta[0], x, BE_BF16, (uint64_t)g.C, (uint64_t)g.N * g.H * g.W, (uint64_t)g.C, 64, 1);
   const double flops = 2.0 * p.M * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 +
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);

@@ -54,6 +54,19 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar,
         "r"(c0), "r"(c1) : "memory");
 }
 
+// TMA row gather (sm_100a): 4 rows (row coords r0..r3, any order; out-of-range
+// or negative rows are zero-filled) × one box width of columns starting at c0,
+// landing in 4 consecutive smem rows with the map's swizzle.  The tensor map
+// must be 2-D with boxDim = {width, 1} (probed: tools/gather4_probe.cu).
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar, uint32_t dst, int32_t c0, int32_t r0,
+                                            int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
+        "r"(r3) : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {  // whole warp
