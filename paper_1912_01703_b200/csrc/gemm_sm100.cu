@@ -51,6 +51,7 @@ struct __align__(64) GemmParams {
   int tiles_m, tiles_n;
   int splits, kb_per_split;   // split-K: tile index t → (split, tm, tn); split s covers k-blocks [s·kps, (s+1)·kps)
   long long split_stride;     // elements between split partial slabs (fp32 workspace)
+  int split_rows;             // rows per slab (M rounded up to the tile height)
   void* D;
   long long ldd;
   int d_f32;
@@ -60,7 +61,11 @@ struct __align__(64) GemmParams {
   // implicit-GEMM convolution (A gathered from NHWC x; unused by plain GEMMs)
   const uint16_t* x;
   int cN, cH, cW, cC, cR, cS, cstride, cpad, cP, cQ;
+  // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
+  int tma_store;
+  CUtensorMap td;
 };
+constexpr int kEpiBytes = 32768;  // 4 epilogue warps × 2 staging buffers × 4 KB
 
 template <int BN, bool X3>
 struct Cfg {
@@ -71,10 +76,10 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;         // BM rows x 128 B
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (226 * 1024 - kEpiBytes - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
   static constexpr int CH = 128 / ESIZE;           // MN elements per 128-B chunk
 };
 
@@ -160,12 +165,69 @@ __device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bo
   }
 }
 
+// TMA-store epilogue for one 32-row × 32-column chunk held by a warp (lane =
+// row): bias / ReLU / convert, write the lane's row into the warp's staging
+// buffer in the store map's swizzle (bf16: 64-B rows, SW64 — chunk c at
+// c ^ ((row>>1)&3); fp32: 128-B rows, SW128 — c ^ (row&7)), fence, and lane 0
+// issues one bulk tensor store (out-of-range rows/columns are clipped by TMA).
+// `buf_idx` alternates between the warp's two buffers; the buffer is reused
+// only after the store issued from it two chunks earlier has read smem.
+__device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* stage_base, int lane, int& buf_idx,
+                                          int store_row, int col0, const uint32_t (&r)[32]) {
+  uint8_t* buf = stage_base + buf_idx * 4096;
+  if (lane == 0) sm100::bulk_wait_read<1>();
+  __syncwarp();
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (p.bias) {
+    const int ncol = min(32, p.N - col0);
+    if (ncol == 32 && (reinterpret_cast<uintptr_t>(p.bias + col0) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+        v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < ncol) v[j] += __ldg(p.bias + col0 + j);
+    }
+  }
+  if (p.act == 1) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  if (p.d_f32) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<float4*>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint4 o;
+      o.x = pack_bf16x2(v[8 * c], v[8 * c + 1]); o.y = pack_bf16x2(v[8 * c + 2], v[8 * c + 3]);
+      o.z = pack_bf16x2(v[8 * c + 4], v[8 * c + 5]); o.w = pack_bf16x2(v[8 * c + 6], v[8 * c + 7]);
+      *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = o;
+    }
+  }
+  sm100::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    sm100::tma_store_2d(&p.td, buf, col0, store_row);
+    sm100::bulk_commit();
+  }
+  buf_idx ^= 1;
+}
+
 template <int BN, bool X3>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, X3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -277,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // ===================== epilogue =====================
     const int ew = warp - 4;  // == warp % 4 → TMEM lanes [32*ew, 32*ew+32)
     int acc = 0; uint32_t acc_phase = 0;
+    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int mn = t % mn_tiles, sp = t / mn_tiles;
@@ -286,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       sm100::tc_fence_after();
       const int row = tm * BM + ew * 32 + lane;
       const bool row_ok = row < p.M;
+      const int store_row = sp * p.split_rows + tm * BM + ew * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         const int col0 = tn * BN + c0;
@@ -293,13 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, store_row, col0, r);
+        else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // TMA stores complete before exit
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -322,7 +388,7 @@ constexpr int A_BYTES = HM * 128, B_BYTES = HN * 128;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB per CTA
 constexpr int STAGES = 6;
 constexpr int TMEM_COLS = 512;            // 2 accumulators × 256 columns
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
 }  // namespace pair
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -330,7 +396,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using namespace pair;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -425,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== epilogue (both CTAs, own TMEM half) =====================
     const int ew = warp - 4;
     int acc = 0; uint32_t acc_phase = 0;
+    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     for (int t = pair_id; t < num_tiles; t += npairs) {
@@ -435,6 +503,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       const int row = tm * TM + rank * HM + ew * 32 + lane;
       const bool row_ok = row < p.M;
+      const int store_row = sp * p.split_rows + tm * TM + rank * HM + ew * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < TN; c0 += 32) {
         const int col0 = tn * TN + c0;
@@ -442,13 +511,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + acc * TN + c0 + ((uint32_t)(ew * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, store_row, col0, r);
+        else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_cluster(tempty_leader + acc * 8);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // TMA stores complete before exit
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -473,10 +544,10 @@ template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (226 * 1024 - kEpiBytes - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
 };
 }  // namespace conv
 
@@ -485,7 +556,8 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   using C = conv::Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -581,6 +653,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
     // ===================== epilogue =====================
     const int ew = warp - 4;
     int acc = 0; uint32_t acc_phase = 0;
+    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
@@ -595,13 +668,15 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
         uint32_t r[32];
         sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, tm * BM + ew * 32, col0, r);
+        else if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // TMA stores complete before exit
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -671,12 +746,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, con
   }
 }
 
-__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, void* D, long long ldd,
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, long long sstride, int M, int N, void* D, long long ldd,
                               int d_f32, float beta, const float* bias, int act) {
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     float v = 0.f;
-    for (int s = 0; s < splits; ++s) v += ws[(long long)s * total + i];
+    for (int s = 0; s < splits; ++s) v += ws[(long long)s * sstride + i];
     const int m = (int)(i / N), n = (int)(i % N);
     if (bias) v += bias[n];
     if (act == 1) v = fmaxf(v, 0.f);
@@ -754,8 +829,8 @@ EncodeFn get_encode() {
 
 // 2-D map over a row-major matrix of `rows` x `cols` (cols contiguous), box
 // {box_c, box_r}, SW128.
-void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint64_t rows, uint64_t ld,
-               uint32_t box_c, uint32_t box_r) {
+void encode_2d_sw(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint64_t rows, uint64_t ld,
+                  uint32_t box_c, uint32_t box_r, CUtensorMapSwizzle sw) {
   EncodeFn enc = get_encode();
   BE_REQUIRE(enc != nullptr, BE_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   const size_t es = dtype_size(dt);
@@ -764,10 +839,26 @@ void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint
   cuuint32_t box[2] = {box_c, box_r};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt == BE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   BE_REQUIRE(r == CUDA_SUCCESS, BE_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint64_t rows, uint64_t ld,
+               uint32_t box_c, uint32_t box_r) {
+  encode_2d_sw(m, ptr, dt, cols, rows, ld, box_c, box_r, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+// TMA-store epilogue map over the output (rows × N, row stride ld) when
+// possible: beta = 0 (no read of old D), 16-B aligned rows. Box 32×32 with
+// SW128 (fp32, 128-B rows) or SW64 (bf16, 64-B rows) — epi_tma32's layout.
+void setup_store(GemmParams& p, void* D, bool f32, long long rows, int N, long long ld) {
+  p.tma_store = 0;
+  static const int enabled = [] { const char* e = getenv("BE_TMA_STORE"); return e ? atoi(e) : 1; }();
+  if (!enabled || p.beta != 0.f) return;
+  const int es = f32 ? 4 : 2;
+  if ((ld * es) % 16 != 0 || (reinterpret_cast<uintptr_t>(D) & 15) != 0 || rows <= 0 || N <= 0) return;
+  encode_2d_sw(&p.td, D, f32 ? BE_F32 : BE_BF16, (uint64_t)N, (uint64_t)rows, (uint64_t)ld, 32, 32,
+               f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+  p.tma_store = 1;
 }
 
 // Operand map: logical [MN, K]; kmajor → stored [MN rows, K cols]; else [K rows, MN cols].
@@ -818,13 +909,17 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   p.kb_per_split = kps;
   Block* ws = nullptr;
   if (splits > 1) {
-    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M * g.N, s);
+    // one slab per split, BM-row padded so a tile never spills into the next slab
+    p.split_rows = p.tiles_m * BM;
+    p.split_stride = (long long)p.split_rows * g.N;
+    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * p.split_stride, s);
     p.D = ws->ptr; p.ldd = g.N; p.d_f32 = 1; p.beta = 0.f; p.bias = nullptr; p.act = 0;
-    p.split_stride = (long long)g.M * g.N;
   } else {
     p.D = g.D; p.ldd = g.ldd; p.d_f32 = g.d == BE_F32; p.beta = g.beta; p.bias = g.bias; p.act = g.act;
     p.split_stride = 0;
+    p.split_rows = 0;
   }
+  setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = std::min(mn * splits, sms);
   const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
@@ -835,7 +930,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   if (ws) {
     const long long total = (long long)g.M * g.N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, g.M, g.N, g.D, g.ldd,
+    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -868,12 +963,14 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   p.kb_per_split = kps;
   Block* ws = nullptr;
   if (splits > 1) {
-    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M * g.N, s);
+    p.split_rows = p.tiles_m * TM;
+    p.split_stride = (long long)p.split_rows * g.N;
+    ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * p.split_stride, s);
     p.D = ws->ptr; p.ldd = g.N; p.d_f32 = 1; p.beta = 0.f; p.bias = nullptr; p.act = 0;
-    p.split_stride = (long long)g.M * g.N;
   } else {
     p.D = g.D; p.ldd = g.ldd; p.d_f32 = g.d == BE_F32; p.beta = g.beta; p.bias = g.bias; p.act = g.act;
   }
+  setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = 2 * std::min(mn * splits, pairs);
   const double ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
@@ -884,7 +981,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   if (ws) {
     const long long total = (long long)g.M * g.N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, g.M, g.N, g.D, g.ldd,
+    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -1006,6 +1103,7 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 +
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_implicit", flops, bytes, p.M, g.K, RSC, s);
+  setup_store(p, y, p.d_f32 != 0, p.M, g.K, g.K);
   if (bn == 256) launch_conv<256>(p, s);
   else if (bn == 128) launch_conv<128>(p, s);
   else launch_conv<64>(p, s);
