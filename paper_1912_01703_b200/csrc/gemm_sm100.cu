@@ -41,7 +41,8 @@ namespace {
 std::atomic<uint64_t> g_tc_calls{0}, g_simt_calls{0};
 
 constexpr int BM = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle, w4-11 epilogue (2 per TMEM lane quarter)
+constexpr int kEpiWarps = 8;
 
 struct __align__(64) GemmParams {
   CUtensorMap ta[2];
@@ -61,11 +62,12 @@ struct __align__(64) GemmParams {
   // implicit-GEMM convolution (A gathered from NHWC x; unused by plain GEMMs)
   const uint16_t* x;
   int cN, cH, cW, cC, cR, cS, cstride, cpad, cP, cQ;
+  int use_im2col;             // conv A operand via TMA im2col map (ta[1]) instead of gather4 (ta[0])
   // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
   int tma_store;
   CUtensorMap td;
 };
-constexpr int kEpiBytes = 32768;  // 4 epilogue warps × 2 staging buffers × 4 KB
+constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
 template <int BN, bool X3>
 struct Cfg {
@@ -170,12 +172,11 @@ __device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bo
 // buffer in the store map's swizzle (bf16: 64-B rows, SW64 — chunk c at
 // c ^ ((row>>1)&3); fp32: 128-B rows, SW128 — c ^ (row&7)), fence, and lane 0
 // issues one bulk tensor store (out-of-range rows/columns are clipped by TMA).
-// `buf_idx` alternates between the warp's two buffers; the buffer is reused
-// only after the store issued from it two chunks earlier has read smem.
-__device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* stage_base, int lane, int& buf_idx,
-                                          int store_row, int col0, const uint32_t (&r)[32]) {
-  uint8_t* buf = stage_base + buf_idx * 4096;
-  if (lane == 0) sm100::bulk_wait_read<1>();
+// Each warp owns one 4 KB staging buffer, reused once the previous store
+// from it has finished reading shared memory.
+__device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* buf, int lane, int store_row, int col0,
+                                          const uint32_t (&r)[32]) {
+  if (lane == 0) sm100::bulk_wait_read<0>();
   __syncwarp();
   float v[32];
 #pragma unroll
@@ -218,7 +219,6 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* stage_ba
     sm100::tma_store_2d(&p.td, buf, col0, store_row);
     sm100::bulk_commit();
   }
-  buf_idx ^= 1;
 }
 
 template <int BN, bool X3>
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
     sm100::fence_barrier_init();
     sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
     if (X3) { sm100::tma_prefetch(&p.ta[1]); sm100::tma_prefetch(&p.tb[1]); }
@@ -337,9 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int ew = warp - 4;  // == warp % 4 → TMEM lanes [32*ew, 32*ew+32)
+    const int ew = warp - 4;               // 0..7
+    const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int acc = 0; uint32_t acc_phase = 0;
-    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int mn = t % mn_tiles, sp = t / mn_tiles;
@@ -347,17 +347,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       char* Dbase = reinterpret_cast<char*>(p.D) + (long long)sp * p.split_stride * 4;
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const int row = tm * BM + ew * 32 + lane;
+      const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
-      const int store_row = sp * p.split_rows + tm * BM + ew * 32;
+      const int store_row = sp * p.split_rows + tm * BM + eq * 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 32) {
         const int col0 = tn * BN + c0;
         if (col0 >= p.N) break;  // warp-uniform
         uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, store_row, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, store_row, col0, r);
         else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
@@ -410,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 2 * kEpiWarps); }
     sm100::fence_barrier_init();
     sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
   }
@@ -490,9 +490,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs, own TMEM half) =====================
-    const int ew = warp - 4;
+    const int ew = warp - 4;               // 0..7
+    const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int acc = 0; uint32_t acc_phase = 0;
-    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     for (int t = pair_id; t < num_tiles; t += npairs) {
@@ -501,17 +501,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       char* Dbase = reinterpret_cast<char*>(p.D) + (long long)sp * p.split_stride * 4;
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const int row = tm * TM + rank * HM + ew * 32 + lane;
+      const int row = tm * TM + rank * HM + eq * 32 + lane;
       const bool row_ok = row < p.M;
-      const int store_row = sp * p.split_rows + tm * TM + rank * HM + ew * 32;
+      const int store_row = sp * p.split_rows + tm * TM + rank * HM + eq * 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TN; c0 += 32) {
+      for (int c0 = eh * (TN / 2); c0 < (eh + 1) * (TN / 2); c0 += 32) {
         const int col0 = tn * TN + c0;
         if (col0 >= p.N) break;
         uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TN + c0 + ((uint32_t)(eq * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, store_row, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, store_row, col0, r);
         else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
@@ -539,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // by TMA; MMA issue / TMEM / epilogue as gemm_tc_kernel.  Requires C % 64 == 0
 // so a k-block is 64 channels of one filter tap.
 namespace conv {
-constexpr int kThreads = 256;   // w0 TMA gather/tile producer, w1 MMA, w2 TMEM, w4-7 epilogue
+constexpr int kThreads = 384;   // w0 TMA producer, w1 MMA, w2 TMEM, w4-11 epilogue
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   if (threadIdx.x == 0) {
     // full: 128 gather threads + 1 TMA expect_tx arrival
     for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
     sm100::fence_barrier_init();
     sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
   }
@@ -581,7 +581,31 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   const int CB = p.cC / 64;                          // k-blocks per tap
   const int kblocks = p.cR * p.cS * CB;
 
-  if (warp == 0) {
+  if (warp == 0 && p.use_im2col) {
+    // ===================== producer: A by TMA im2col, B by TMA tile =====================
+    // one im2col op per k-block loads the tap (r,s) / 64-channel slice of the
+    // tile's 128 output pixels (zero fill in the padding).
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+        const int m0 = tm * BM;
+        const int q0 = m0 % p.cQ, pq = m0 / p.cQ;
+        const int p0 = pq % p.cP, n0 = pq / p.cP;
+        const int ws = q0 * p.cstride - p.cpad, hs = p0 * p.cstride - p.cpad;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          const int tap = kb / CB, cb = kb - tap * CB;
+          const int r = tap / p.cS, s = tap - r * p.cS;
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* sbase = smem + stage * C::STAGE_BYTES;
+          sm100::tma_load_2d(&p.tb[0], &full[stage], sbase + C::A_BYTES, kb * 64, tn * BN);
+          sm100::tma_load_im2col_4d(&p.ta[1], &full[stage], sbase, cb * 64, ws, hs, n0, (uint16_t)s, (uint16_t)r);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ===================== producer: A by TMA row-gather, B by TMA tile =====================
     // lane l owns tile rows 4l..4l+3; per k-block (tap r,s; 64 channels) it
     // issues one tile::gather4 of those rows (−1 = padding → zero fill).
@@ -651,24 +675,24 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int ew = warp - 4;
+    const int ew = warp - 4;               // 0..7
+    const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int acc = 0; uint32_t acc_phase = 0;
-    int buf_idx = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const int row = tm * BM + ew * 32 + lane;
+      const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 32) {
         const int col0 = tn * BN + c0;
         if (col0 >= p.N) break;
         uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16), r);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 8192, lane, buf_idx, tm * BM + ew * 32, col0, r);
+        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, tm * BM + eq * 32, col0, r);
         else if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r);
       }
       sm100::tc_fence_before();
@@ -847,6 +871,34 @@ void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint
                uint32_t box_c, uint32_t box_r) {
   encode_2d_sw(m, ptr, dt, cols, rows, ld, box_c, box_r, CU_TENSOR_MAP_SWIZZLE_128B);
 }
+// 4-D NHWC im2col map for a convolution's input (bf16): box = `pixels`
+// output positions × `chans` channels, SW128; corners per CUTLASS's
+// convention: lower = −pad, upper = pad − (R−1); traversal stride = conv stride.
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool encode_im2col_4d(CUtensorMap* m, const void* x, const ConvGeom& g, int chans, int pixels) {
+  static EncodeIm2colFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeIm2colFn) nullptr;
+    return reinterpret_cast<EncodeIm2colFn>(f);
+  }();
+  if (!fn || g.R - 1 - g.pad > 255 || g.S - 1 > 255) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+  cuuint64_t strides[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)g.W * g.C * 2, (cuuint64_t)g.H * g.W * g.C * 2};
+  int lower[2] = {-g.pad, -g.pad};
+  int upper[2] = {g.pad - (g.S - 1), g.pad - (g.R - 1)};
+  cuuint32_t es[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
+                  (cuuint32_t)chans, (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // TMA-store epilogue map over the output (rows × N, row stride ld) when
 // possible: beta = 0 (no read of old D), 16-B aligned rows. Box 32×32 with
 // SW128 (fp32, 128-B rows) or SW64 (bf16, 64-B rows) — epi_tma32's layout.
@@ -1099,6 +1151,9 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
   // x as a 2-D [N·H·W, C] matrix; tile::gather4 needs box {64, 1}
   encode_2d(&p.ta[0], x, BE_BF16, (uint64_t)g.C, (uint64_t)g.N * g.H * g.W, (uint64_t)g.C, 64, 1);
+  // x as 4-D NHWC im2col map: window starts from −pad to W+pad−R (stride), 128 pixels × 64 channels
+  static const int im2col_on = [] { const char* e = getenv("BE_CONV_IM2COL"); return e ? atoi(e) : 1; }();
+  if (im2col_on && encode_im2col_4d(&p.ta[1], x, g, 64, BM)) p.use_im2col = 1;
   const double flops = 2.0 * p.M * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 +
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);

@@ -67,6 +67,20 @@ __device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar,
         "r"(r3) : "memory");
 }
 
+// TMA im2col load (4-D NHWC map encoded with cuTensorMapEncodeIm2col):
+// loads pixelsPerColumn consecutive output pixels' window taps, i.e. the
+// pixels at window start (w, h, n) + (offw, offh), traversing w, then h,
+// then n inside the map's bounding box with its element strides; padding
+// positions are zero-filled (probed: tools/im2col_probe.cu).
+__device__ __forceinline__ void tma_load_im2col_4d(const CUtensorMap* m, uint64_t* bar, void* dst, int32_t c,
+                                                   int32_t w, int32_t h, int32_t n, uint16_t offw, uint16_t offh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+        "h"(offw), "h"(offh) : "memory");
+}
+
 // TMA store of a swizzled smem box; bulk-group completion tracking.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
