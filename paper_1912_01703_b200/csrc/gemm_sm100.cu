@@ -172,11 +172,18 @@ __device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bo
 // buffer in the store map's swizzle (bf16: 64-B rows, SW64 — chunk c at
 // c ^ ((row>>1)&3); fp32: 128-B rows, SW128 — c ^ (row&7)), fence, and lane 0
 // issues one bulk tensor store (out-of-range rows/columns are clipped by TMA).
-// Each warp owns one 4 KB staging buffer, reused once the previous store
-// from it has finished reading shared memory.
-__device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* buf, int lane, int store_row, int col0,
-                                          const uint32_t (&r)[32]) {
-  if (lane == 0) sm100::bulk_wait_read<0>();
+// Each warp owns a 4 KB staging area: two 2 KB buffers alternating for bf16
+// (the store issued from a buffer two chunks earlier must have read it), one
+// 4 KB buffer for fp32.
+__device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf, int& slot, int lane, int store_row,
+                                          int col0, const uint32_t (&r)[32]) {
+  uint8_t* buf = warp_buf;
+  if (p.d_f32) {
+    if (lane == 0) sm100::bulk_wait_read<0>();
+  } else {
+    buf += slot * 2048;
+    if (lane == 0) sm100::bulk_wait_read<1>();
+  }
   __syncwarp();
   float v[32];
 #pragma unroll
@@ -216,9 +223,11 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* buf, int
   sm100::fence_proxy_async();
   __syncwarp();
   if (lane == 0) {
-    sm100::tma_store_2d(&p.td, buf, col0, store_row);
+    if (p.tma_store == 2) sm100::tma_reduce_add_2d(&p.td, buf, col0, store_row);  // beta = 1
+    else sm100::tma_store_2d(&p.td, buf, col0, store_row);
     sm100::bulk_commit();
   }
+  slot ^= 1;
 }
 
 template <int BN, bool X3>
@@ -339,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // ===================== epilogue =====================
     const int ew = warp - 4;               // 0..7
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
+    int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -351,14 +361,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const bool row_ok = row < p.M;
       const int store_row = sp * p.split_rows + tm * BM + eq * 32;
 #pragma unroll 1
-      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 32) {
-        const int col0 = tn * BN + c0;
-        if (col0 >= p.N) break;  // warp-uniform
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16), r);
+      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, store_row, col0, r);
-        else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, Dbase, vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -492,6 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== epilogue (both CTAs, own TMEM half) =====================
     const int ew = warp - 4;               // 0..7
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
+    int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
@@ -505,14 +525,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool row_ok = row < p.M;
       const int store_row = sp * p.split_rows + tm * TM + rank * HM + eq * 32;
 #pragma unroll 1
-      for (int c0 = eh * (TN / 2); c0 < (eh + 1) * (TN / 2); c0 += 32) {
-        const int col0 = tn * TN + c0;
-        if (col0 >= p.N) break;
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TN + c0 + ((uint32_t)(eq * 32) << 16), r);
+      for (int c0 = eh * (TN / 2); c0 < (eh + 1) * (TN / 2); c0 += 64) {
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * TN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (TN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * TN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, store_row, col0, r);
-        else if (row_ok) epi_store32(p, Dbase, vec_ok, row, col0, r);
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, Dbase, vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -677,6 +706,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
     // ===================== epilogue =====================
     const int ew = warp - 4;               // 0..7
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
+    int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -686,14 +716,23 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
       const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
 #pragma unroll 1
-      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 32) {
-        const int col0 = tn * BN + c0;
-        if (col0 >= p.N) break;
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16), r);
+      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, lane, tm * BM + eq * 32, col0, r);
-        else if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r);
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -900,17 +939,18 @@ bool encode_im2col_4d(CUtensorMap* m, const void* x, const ConvGeom& g, int chan
 }
 
 // TMA-store epilogue map over the output (rows × N, row stride ld) when
-// possible: beta = 0 (no read of old D), 16-B aligned rows. Box 32×32 with
+// possible: 16-B aligned rows; beta = 0 → bulk tensor store, beta = 1 →
+// bulk tensor reduce-add (one add per element: deterministic). Box 32×32 with
 // SW128 (fp32, 128-B rows) or SW64 (bf16, 64-B rows) — epi_tma32's layout.
 void setup_store(GemmParams& p, void* D, bool f32, long long rows, int N, long long ld) {
   p.tma_store = 0;
   static const int enabled = [] { const char* e = getenv("BE_TMA_STORE"); return e ? atoi(e) : 1; }();
-  if (!enabled || p.beta != 0.f) return;
+  if (!enabled || (p.beta != 0.f && p.beta != 1.f)) return;
   const int es = f32 ? 4 : 2;
   if ((ld * es) % 16 != 0 || (reinterpret_cast<uintptr_t>(D) & 15) != 0 || rows <= 0 || N <= 0) return;
   encode_2d_sw(&p.td, D, f32 ? BE_F32 : BE_BF16, (uint64_t)N, (uint64_t)rows, (uint64_t)ld, 32, 32,
                f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-  p.tma_store = 1;
+  p.tma_store = p.beta == 1.f ? 2 : 1;  // 2: bulk tensor reduce-add (D += result)
 }
 
 // Operand map: logical [MN, K]; kmajor → stored [MN rows, K cols]; else [K rows, MN cols].
