@@ -377,7 +377,11 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
                                                    const void* __restrict__ yv, int act, int64_t rows, int C,
                                                    be_dtype dt, const float* __restrict__ mean,
                                                    const float* __restrict__ invstd, float* __restrict__ part0,
-                                                   float* __restrict__ part1, int64_t rows_per_split) {
+                                                   float* __restrict__ part1, int64_t rows_per_split,
+                                                   const float* __restrict__ gam = nullptr,
+                                                   const float* __restrict__ bsh = nullptr) {
+  // act with gam/bsh: the ReLU mask is recomputed as fma(x, γ·is, β − μ·γ·is) > 0
+  // — the forward's exact expression — instead of reading the saved output.
   __shared__ float sm0[kBnCG], sm1[kBnCG];
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
@@ -387,14 +391,18 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
   float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (rl < rpi) {
-    float k[8], is[8];
+    float k[8], is[8], sc[8], sh[8];
     if (MODE == 0) {
       V8 kk = ld8(x, c, dt);
 #pragma unroll
       for (int j = 0; j < 8; ++j) k[j] = kk.v[j];
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) { k[j] = mean[c + j]; is[j] = invstd[c + j]; }
+      for (int j = 0; j < 8; ++j) {
+        k[j] = mean[c + j]; is[j] = invstd[c + j];
+        sc[j] = gam ? gam[c + j] * is[j] : 0.f;
+        sh[j] = gam ? bsh[c + j] - k[j] * sc[j] : 0.f;
+      }
     }
     for (int64_t r = r0 + rl; r < r1; r += rpi) {
       const int64_t o = r * C + c;
@@ -404,7 +412,10 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
         for (int j = 0; j < 8; ++j) { const float d = a.v[j] - k[j]; s0[j] += d; s1[j] += d * d; }
       } else {
         V8 g = ld8(gy, o, dt);
-        if (act) {
+        if (act && gam) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
+        } else if (act) {
           V8 yy = ld8(yv, o, dt);
 #pragma unroll
           for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
@@ -479,7 +490,8 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
                                                const void* __restrict__ yv, int act, void* dx, int64_t rows, int C,
                                                be_dtype dt, const float* __restrict__ mean,
                                                const float* __restrict__ invstd, const float* __restrict__ gamma,
-                                               const float* __restrict__ sums, float dx_beta, int64_t rows_per_block) {
+                                               const float* __restrict__ sums, float dx_beta, int64_t rows_per_block,
+                                               const float* __restrict__ bsh = nullptr) {
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -488,10 +500,12 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
   const int c = base + v * 8;
   // dx = γ·is·(g' − Σg'/n − x̂·Σg'x̂/n),  x̂ = (x − μ)·is   ⇒  dx = k1·g' + k2·x + k3
   const float inv_n = 1.f / (float)rows;
-  float k1[8], k2[8], k3[8];
+  float k1[8], k2[8], k3[8], sc[8], sh[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float is = invstd[c + j], a = gamma[c + j] * is;
+    sc[j] = a;
+    sh[j] = bsh ? bsh[c + j] - mean[c + j] * a : 0.f;
     const float m1 = sums[c + j] * inv_n, m2 = sums[C + c + j] * inv_n;
     k1[j] = a;
     k2[j] = -a * m2 * is;
@@ -501,7 +515,10 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
   for (int64_t r = r0 + rl; r < r1; r += rpi) {
     const int64_t o = r * C + c;
     V8 g = ld8(gy, o, dt), a = ld8(x, o, dt);
-    if (act) {
+    if (act && bsh) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
+    } else if (act) {
       V8 yy = ld8(yv, o, dt);
 #pragma unroll
       for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
@@ -744,16 +761,17 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
 }
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta, float gb_beta,
-            float dx_beta, float* partial, cudaStream_t s) {
+            float dx_beta, float* partial, cudaStream_t s, const float* bn_beta) {
   // partial must hold 2*splits*C + 2*C floats
-  if (bn_vec_ok(x, C) && aligned16(dy) && (!act || aligned16(y)) && (!dx || aligned16(dx))) {
+  if (bn_vec_ok(x, C) && aligned16(dy) && (!act || bn_beta || aligned16(y)) && (!dx || aligned16(dx))) {
     const int64_t sp = bn_splits_v(rows, C);
     const int64_t rps = (rows + sp - 1) / sp;
     float* p0 = partial;
     float* p1 = partial + sp * C;
     float* sums = partial + 2 * sp * C;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-    bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps);
+    bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
+                                        bn_beta ? gamma : nullptr, bn_beta);
     after_launch("bn_bwd_reduce_v");
     bn_finalize_v<2><<<(C + 31) / 32, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                     nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
@@ -761,7 +779,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
     if (dx) {
       dim3 g2;
       const int64_t rpb = bn_rows_per_block(rows, C, &g2);
-      bn_dx_v<<<g2, 256, 0, s>>>(dy, x, y, act, dx, rows, C, dt, mean, invstd, gamma, sums, dx_beta, rpb);
+      bn_dx_v<<<g2, 256, 0, s>>>(dy, x, y, act, dx, rows, C, dt, mean, invstd, gamma, sums, dx_beta, rpb, bn_beta);
       after_launch("bn_bwd_dx_v");
     }
     return;

@@ -105,7 +105,7 @@ size_t bn_partial_floats(int64_t rows, int C);
 // backward: dgamma, dbeta (fp32, with beta-accumulate flags) and dx
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta,
-            float gb_beta, float dx_beta, float* partial, cudaStream_t s);
+            float gb_beta, float dx_beta, float* partial, cudaStream_t s, const float* bn_beta = nullptr);
 
 // ------------------------------------------------------------------ embedding
 void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,

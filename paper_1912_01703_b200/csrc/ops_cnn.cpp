@@ -215,12 +215,13 @@ static void op_avgpool(const be_tensor* in, int n_in, be_tensor* out) {
 // ------------------------------------------------------------------ batch norm (train)
 static void vjp_bn(Node* n, GradSink& sink) {
   cudaStream_t s = ctx().stream;
-  TRef hx, hmean, hinv, hg, hy;
+  TRef hx, hmean, hinv, hg, hy, hb;
   Tensor* x = unpack(n, 0, hx);
   Tensor* mean = unpack(n, 1, hmean);
   Tensor* inv = unpack(n, 2, hinv);
   Tensor* gamma = unpack(n, 3, hg);
   Tensor* y = unpack(n, 4, hy);
+  Tensor* bshift = unpack(n, 5, hb);  // β: the ReLU mask is recomputed from x
   const int act = (int)n->iattr[0];
   const int C = (int)x->shape[3];
   const int64_t rows = x->numel() / C;
@@ -244,7 +245,8 @@ static void vjp_bn(Node* n, GradSink& sink) {
   float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
   float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
   k::bn_bwd(gz->data(), x->data(), act ? y->data() : nullptr, act, dx ? dx->data() : nullptr, rows, C, x->dtype,
-            mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s);
+            mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s,
+            act ? bshift->ptr<float>() : nullptr);
   if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
   if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
   if (dx) sink.commit(0);
@@ -279,6 +281,7 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   Node* n = new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
   if (n) {
     save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, a.act ? y.get() : nullptr);
+    save(n, beta);
     n->iattr[0] = a.act;
     set_output(n, y.get(), 0);
     finish_node(n);
