@@ -188,6 +188,20 @@ __global__ void maxpool_bwd_v(const void* __restrict__ dy, const uint8_t* __rest
   }
 }
 
+// Transposed + spatially flipped weights for dgrad-as-convolution:
+// wf[c, r, s, k] = w[k, R−1−r, S−1−s, c]
+__global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ wf, int K, int R, int S,
+                                    int C, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int k = (int)(t % K); t /= K;
+    const int s = (int)(t % S); t /= S;
+    const int r = (int)(t % R);
+    const int c = (int)(t / R);
+    wf[i] = w[(((int64_t)k * R + (R - 1 - r)) * S + (S - 1 - s)) * C + c];
+  }
+}
+
 __global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
   const int64_t RSC = (int64_t)g.R * g.S * g.C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -647,6 +661,12 @@ void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtyp
   else
     col2im_kernel<float><<<grid_for(total), 256, 0, s>>>((const float*)dcols, ldc, (float*)dx, g, beta, total, dt);
   after_launch("col2im");
+}
+void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s) {
+  const int64_t total = (int64_t)K * R * S * C;
+  if (total == 0) return;
+  flip_weights_kernel<<<grid_for(total), 256, 0, s>>>((const uint16_t*)w, (uint16_t*)wf, K, R, S, C, total);
+  after_launch("flip_weights");
 }
 void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.R * g.S * g.C;

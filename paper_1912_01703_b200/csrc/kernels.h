@@ -87,6 +87,8 @@ struct ConvGeom {
 // conv(x NHWC, w KRSC) (+bias, act, beta). Returns false when unsupported.
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
                    float beta, cudaStream_t s);
+// bf16 wf[C,R,S,K] = w[K,R−1−r,S−1−s,C] (dgrad of a stride-1 conv as a convolution)
+void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s);
 // cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC
 void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s);
 // dx NHWC (+)= col2im(dcols)   (gather formulation, deterministic)

@@ -76,12 +76,20 @@ def test_conv_op_bf16_implicit_gemm(cfg):
     x = q(rng.standard_normal((N, C, H, W)))
     w = q(rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R))
     b = rng.standard_normal(K).astype(np.float32)
-    yo = oops.relu(oops.conv2d(Var(x.astype(np.float64)), Var(w.astype(np.float64)), Var(b.astype(np.float64)), st, pd))
+    xo, wo = Var(x.astype(np.float64), True), Var(w.astype(np.float64), True)
+    yo = oops.conv2d(xo, wo, Var(b.astype(np.float64)), st, pd)
     calls0 = be.launch_count()
-    yd = be.conv2d(be.tensor(nchw_to_nhwc(x), dtype="bf16"), be.tensor(nchw_to_nhwc(w), requires_grad=True),
-                   be.tensor(b), st, pd, act=1)
+    xd = be.tensor(nchw_to_nhwc(x), requires_grad=True)
+    wd = be.tensor(nchw_to_nhwc(w), requires_grad=True)
+    yd = be.conv2d(be.cast(xd, "bf16"), wd, be.tensor(b), st, pd, act=0)
     assert rel(nhwc_to_nchw(yd.numpy()), yo.value) < 1e-2
-    assert be.launch_count() - calls0 <= 3  # weight shadow cast + one conv kernel (no im2col)
+    assert be.launch_count() - calls0 <= 4  # input cast, weight shadow cast, one conv kernel (no im2col)
+    # backward with a bf16 upstream: dgrad (stride 1 → flipped-weight implicit conv) and wgrad
+    g = q(rng.standard_normal(yo.value.shape))
+    backward(yo, g.astype(np.float64))
+    yd.backward(be.tensor(nchw_to_nhwc(g), dtype="bf16"))
+    assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-2
+    assert rel(nhwc_to_nchw(wd.grad.numpy()), wo.grad) < 1e-3
 
 
 @pytest.mark.parametrize("C", [5, 16])
