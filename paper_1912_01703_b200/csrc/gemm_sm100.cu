@@ -63,6 +63,7 @@ struct __align__(64) GemmParams {
   const uint16_t* x;
   int cN, cH, cW, cC, cR, cS, cstride, cpad, cP, cQ;
   int use_im2col;             // conv A operand via TMA im2col map (ta[1]) instead of gather4 (ta[0])
+  int b_im2col;               // conv wgrad: MN-major B operand = im2col(x) via TMA im2col map (tb[1])
   // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
   int tma_store;
   CUtensorMap td;
@@ -289,6 +290,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             }
             if (p.b_kmajor) {
               sm100::tma_load_2d(&p.tb[op], &full[stage], sb, k0, n0);
+            } else if (!X3 && p.b_im2col) {
+              // conv wgrad: B = im2col(x) read in place — 64-pixel block k0 ×
+              // 64 channels of one filter tap per MN chunk (TMA im2col map tb[1])
+              const int q = k0 % p.cQ, pq = k0 / p.cQ;
+              const int ws = q * p.cstride - p.cpad, hs = (pq % p.cP) * p.cstride - p.cpad, ni = pq / p.cP;
+#pragma unroll
+              for (int j = 0; j < BN / C::CH; ++j) {
+                const int col = n0 + j * C::CH;
+                const int tap = col / p.cC, cb = (col - tap * p.cC) / 64;
+                sm100::tma_load_im2col_4d(&p.tb[1], &full[stage], sb + j * C::BK * 128, cb * 64, ws, hs, ni,
+                                          (uint16_t)(tap % p.cS), (uint16_t)(tap / p.cS));
+              }
             } else {
 #pragma unroll
               for (int j = 0; j < BN / C::CH; ++j)
@@ -978,7 +991,18 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   memset(&p, 0, sizeof(p));
   const be_dtype dt = X3 ? BE_F32 : BE_BF16;
   encode_operand(&p.ta[0], a_hi, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
-  encode_operand(&p.tb[0], b_hi, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
+  if (!X3 && g.conv_x) {
+    // wgrad B = im2col(x): tb[1] im2col map (64 pixels × 64 channels per op);
+    // tb[0] = x as a plain 2-D map (only prefetched)
+    const ConvGeom& cg = g.conv_g;
+    BE_REQUIRE(encode_im2col_4d(&p.tb[1], g.conv_x, cg, 64, C::BK), BE_E_CUDA, "im2col map encode failed");
+    encode_2d(&p.tb[0], g.conv_x, BE_BF16, (uint64_t)cg.C, (uint64_t)cg.N * cg.H * cg.W, (uint64_t)cg.C, 64, 64);
+    p.b_im2col = 1;
+    p.cN = cg.N; p.cH = cg.H; p.cW = cg.W; p.cC = cg.C; p.cR = cg.R; p.cS = cg.S;
+    p.cstride = cg.stride; p.cpad = cg.pad; p.cP = cg.P; p.cQ = cg.Q;
+  } else {
+    encode_operand(&p.tb[0], b_hi, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
+  }
   if (X3) {
     encode_operand(&p.ta[1], a_lo, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
     encode_operand(&p.tb[1], b_lo, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
@@ -1244,6 +1268,11 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
     if (x3) {
       if (bn == 128) launch_tc<128, true>(gx, ahi, alo, bhi, blo, s);
       else launch_tc<64, true>(gx, ahi, alo, bhi, blo, s);
+    } else if (g.conv_x) {
+      BE_REQUIRE(!g.b_kmajor && g.conv_g.C % 64 == 0, BE_E_ARG, "im2col B needs MN-major B and C % 64 == 0");
+      if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
+      else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
+      else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
     } else {
       cudaEvent_t ev0, ev1;
       const int v = tune_pick(g, &ev0, &ev1);

@@ -8,6 +8,10 @@
 
 namespace be { namespace k {
 
+struct ConvGeom {
+  int N, H, W, C, K, R, S, stride, pad, P, Q;
+};
+
 // ------------------------------------------------------------------ GEMM
 // D[M,N] = act(A[M,K]·B[N,K]ᵀ + bias[N]) + beta·D   (fp32 accumulate)
 // A element (m,k) at A[m*lda + k] if a_kmajor else A[k*lda + m];
@@ -22,6 +26,10 @@ struct GemmDesc {
   float beta = 0.f;
   const float* bias = nullptr;
   int act = 0;  // 0 none, 1 relu
+  // conv wgrad: B (MN-major, [K = pixels, N = R·S·C]) is im2col(conv_x) read in
+  // place by TMA im2col (bf16, C % 64 == 0); B / ldb are then ignored
+  const void* conv_x = nullptr;
+  ConvGeom conv_g{};
 };
 // Returns the name of the path taken ("tcgen05" or "simt").
 const char* gemm(const GemmDesc& g, cudaStream_t s);
@@ -80,9 +88,6 @@ void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float
                cudaStream_t s);
 
 // ------------------------------------------------------------------ conv / pool / bn
-struct ConvGeom {
-  int N, H, W, C, K, R, S, stride, pad, P, Q;
-};
 // Implicit-GEMM convolution on tcgen05 (bf16, C % 64 == 0): y[NPQ, K] =
 // conv(x NHWC, w KRSC) (+bias, act, beta). Returns false when unsupported.
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,

@@ -64,15 +64,22 @@ static void vjp_conv(Node* n, GradSink& sink) {
   }
   gz = TRef();
   if (sink.needs(1)) {  // dW[K, RSC] = dzᵀ · cols
-    int64_t ldc;
-    TRef cols = make_cols(x, g, &ldc);
     float bw;
     Tensor* dw = sink.dest(1, &bw);
     k::GemmDesc gd;
     gd.M = (int)K; gd.N = (int)RSC; gd.K = (int)M;
     gd.A = dz->data(); gd.lda = K; gd.a_kmajor = false;
-    gd.B = cols->data(); gd.ldb = ldc; gd.b_kmajor = false;
     gd.ab = opd; gd.D = dw->data(); gd.ldd = RSC; gd.d = dw->dtype; gd.beta = bw;
+    gd.b_kmajor = false;
+    TRef cols;
+    if (!is_pointwise(g) && opd == BE_BF16 && g.C % 64 == 0 && (K * 2) % 16 == 0) {
+      gd.conv_x = x->data();  // B = im2col(x) read in place by TMA im2col
+      gd.conv_g = g;
+    } else {
+      int64_t ldc;
+      cols = make_cols(x, g, &ldc);
+      gd.B = cols->data(); gd.ldb = ldc;
+    }
     k::gemm(gd, s);
     sink.commit(1);
   }
