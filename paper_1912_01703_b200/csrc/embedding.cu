@@ -81,14 +81,34 @@ __global__ void segment_sum(const uint32_t* keys, const uint32_t* pos, int n, co
 
 size_t embedding_bwd_scratch(int64_t B) { return (size_t)B * 16 + 64; }
 
+// Sort phase only: (id, position) pairs sorted by id (stable) into
+// sorted[0..B) = ids, sorted[B..2B) = positions.  `scratch` ≥ 16·B bytes; the
+// result lives in its first 8·B bytes.
+void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cudaStream_t s);
+
 void embedding_bwd(const void* drows, be_dtype dd, const int32_t* ids, int64_t B, int64_t D, float* dtable, int64_t V,
                    float beta, void* scratch, size_t scratch_bytes, cudaStream_t s) {
   BE_REQUIRE(scratch_bytes >= embedding_bwd_scratch(B), BE_E_ARG, "embedding_bwd: scratch too small");
-  BE_REQUIRE(B < (1LL << 31), BE_E_SHAPE, "embedding_bwd: batch too large");
+  embedding_sort(ids, B, V, scratch, s);
+  embedding_bwd_sorted(drows, dd, B, D, dtable, V, beta, scratch, s);
+}
+
+void embedding_bwd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, float* dtable, int64_t V, float beta,
+                          const void* sorted, cudaStream_t s) {
   if (beta == 0.f) {  // untouched rows get 0
     BE_CHECK_CUDA(cudaMemsetAsync(dtable, 0, sizeof(float) * V * D, s));
     beta = 1.f;        // segments now accumulate onto zeros
   }
+  if (B == 0) return;
+  const uint32_t* k0 = reinterpret_cast<const uint32_t*>(sorted);
+  const uint32_t* v0 = k0 + B;
+  const int64_t threads = B * 32;
+  segment_sum<<<(int)((threads + 255) / 256), 256, 0, s>>>(k0, v0, (int)B, drows, dd, D, dtable, beta);
+  after_launch("embedding_segment_sum");
+}
+
+void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cudaStream_t s) {
+  BE_REQUIRE(B < (1LL << 31), BE_E_SHAPE, "embedding_bwd: batch too large");
   if (B == 0) return;
   uint32_t* k0 = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* v0 = k0 + B;
@@ -110,9 +130,9 @@ void embedding_bwd(const void* drows, be_dtype dd, const int32_t* ids, int64_t B
     std::swap(k0, k1);
     std::swap(v0, v1);
   }
-  const int64_t threads = B * 32;
-  segment_sum<<<(int)((threads + 255) / 256), 256, 0, s>>>(k0, v0, (int)B, drows, dd, D, dtable, beta);
-  after_launch("embedding_segment_sum");
+  uint32_t* base = reinterpret_cast<uint32_t*>(scratch);
+  if (k0 != base)  // odd number of passes: result sits in the second half
+    BE_CHECK_CUDA(cudaMemcpyAsync(base, k0, sizeof(uint32_t) * 2 * B, cudaMemcpyDeviceToDevice, s));
 }
 
 }}  // namespace be::k

@@ -772,19 +772,26 @@ __device__ __forceinline__ float ldv(const TA* p, long long i) {
 template <typename TA>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, const TA* A, long long lda, int akm,
                                                        const TA* B, long long ldb, int bkm, void* D, long long ldd,
-                                                       int d_f32, float beta, const float* bias, int act) {
+                                                       int d_f32, float beta, const float* bias, int act,
+                                                       int kchunk, float* ws) {
+  // split-K over blockIdx.z when ws != null: partial sums to ws[z][M][N]
+  // (reduced in fixed order by splitk_reduce, which then applies bias/act/beta)
   __shared__ float As[16][64 + 1];
   __shared__ float Bs[16][64 + 1];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int kbeg = blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
+  if (ws) {
+    D = ws + (long long)blockIdx.z * M * N; ldd = N; d_f32 = 1; beta = 0.f; bias = nullptr; act = 0;
+  }
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += 16) {
+  for (int k0 = kbeg; k0 < kend; k0 += 16) {
     for (int i = threadIdx.x; i < 16 * 64; i += 256) {
       int kk = i / 64, mm = i % 64;
       int m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < M && k < K) ? ldv(A, akm ? (long long)m * lda + k : (long long)k * lda + m) : 0.f;
+      As[kk][mm] = (m < M && k < kend) ? ldv(A, akm ? (long long)m * lda + k : (long long)k * lda + m) : 0.f;
       int n = n0 + mm;
-      Bs[kk][mm] = (n < N && k < K) ? ldv(B, bkm ? (long long)n * ldb + k : (long long)k * ldb + n) : 0.f;
+      Bs[kk][mm] = (n < N && k < kend) ? ldv(B, bkm ? (long long)n * ldb + k : (long long)k * ldb + n) : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -1287,20 +1294,37 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
     return "tcgen05";
   }
   g_simt_calls++;
-  dim3 grid((g.N + 63) / 64, (g.M + 63) / 64);
+  const int tiles = ((g.N + 63) / 64) * ((g.M + 63) / 64);
+  // split-K so small-output / long-K shapes (e.g. a [128 x 1] head's wgrad, K = batch) fill the GPU
+  int splits = 1;
+  if (tiles < ctx().num_sms && g.K >= 1024)
+    splits = std::max(1, std::min<int>(std::min(ctx().num_sms * 2 / tiles, g.K / 256), 256));
+  const int kchunk = ((g.K + splits - 1) / splits + 15) / 16 * 16;
+  splits = std::max(1, (g.K + kchunk - 1) / kchunk);
+  Block* ws = splits > 1 ? ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M * g.N, s) : nullptr;
+  float* wsp = ws ? reinterpret_cast<float*>(ws->ptr) : nullptr;
+  dim3 grid((g.N + 63) / 64, (g.M + 63) / 64, splits);
   const double es = g.ab == BE_F32 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
   const int pidx = prof_begin("gemm_simt", 2.0 * g.M * g.N * g.K,
                               ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds, g.M, g.N, g.K, s);
-  struct ProfEnd { int i; cudaStream_t s; ~ProfEnd() { prof_end(i, s); } } pe{pidx, s};
   if (g.ab == BE_BF16)
     gemm_simt_kernel<uint16_t><<<grid, 256, 0, s>>>(g.M, g.N, g.K, (const uint16_t*)g.A, g.lda, g.a_kmajor,
                                                     (const uint16_t*)g.B, g.ldb, g.b_kmajor, g.D, g.ldd,
-                                                    g.d == BE_F32, g.beta, g.bias, g.act);
+                                                    g.d == BE_F32, g.beta, g.bias, g.act, kchunk, wsp);
   else
     gemm_simt_kernel<float><<<grid, 256, 0, s>>>(g.M, g.N, g.K, (const float*)g.A, g.lda, g.a_kmajor,
                                                  (const float*)g.B, g.ldb, g.b_kmajor, g.D, g.ldd, g.d == BE_F32,
-                                                 g.beta, g.bias, g.act);
+                                                 g.beta, g.bias, g.act, kchunk, wsp);
   after_launch("gemm_simt");
+  if (ws) {
+    const long long total = (long long)g.M * g.N;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+    splitk_reduce<<<blocks, 256, 0, s>>>(wsp, splits, total, g.M, g.N, g.D, g.ldd, g.d == BE_F32, g.beta, g.bias,
+                                         g.act);
+    after_launch("gemm_simt_splitk_reduce");
+    ctx().alloc.free(ws);
+  }
+  prof_end(pidx, s);
   return "simt";
 }
 

@@ -121,6 +121,11 @@ void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B,
 void embedding_bwd(const void* drows, be_dtype dd, const int32_t* ids, int64_t B, int64_t D, float* dtable,
                    int64_t V, float beta, void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t embedding_bwd_scratch(int64_t B);
+// the two phases of embedding_bwd: stable sort of (id, position) into scratch
+// [0, 8·B) (needs 16·B bytes), then per-id segment sums from that sorted list
+void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cudaStream_t s);
+void embedding_bwd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, float* dtable, int64_t V, float beta,
+                          const void* sorted, cudaStream_t s);
 void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t rows, void* y, be_dtype dt,
                  cudaStream_t s);
 void slice_cols(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x, be_dtype dt,

@@ -322,10 +322,30 @@ static void vjp_embedding(Node* n, GradSink& sink) {
   if (!dt) return;
   TRef gz = contiguous_like(sink.upstream[0], sink.upstream[0]->dtype);
   const int64_t B = ids->numel(), D = dt->shape[1], V = dt->shape[0];
-  const size_t sb = k::embedding_bwd_scratch(B);
-  TRef scratch = new_tensor({(int64_t)((sb + 3) / 4)}, BE_F32);
-  k::embedding_bwd(gz->data(), gz->dtype, ids->ptr<int32_t>(), B, D, dt->ptr<float>(), V, beta, scratch->data(), sb,
-                   ctx().stream);
+  // Tables looked up with the same ids (NeuMF: GMF and MLP tables of a side)
+  // share one sort: cache keyed by the ids storage, its version and V.
+  static struct {
+    Storage* st = nullptr;
+    uint64_t version = 0;
+    int64_t B = -1, V = -1, off = 0;
+    TRef sorted;
+  } cache;
+  const bool hit = cache.st == ids->storage && cache.version == ids->version() && cache.B == B && cache.V == V &&
+                   cache.off == ids->offset && cache.sorted;
+  if (!hit) {
+    const size_t sb = k::embedding_bwd_scratch(B);
+    TRef scratch = new_tensor({(int64_t)((sb + 3) / 4)}, BE_F32);
+    k::embedding_sort(ids->ptr<int32_t>(), B, V, scratch->data(), ctx().stream);
+    if (cache.st) cache.st->drop();
+    cache.st = ids->storage;
+    cache.st->retain();
+    cache.version = ids->version();
+    cache.B = B;
+    cache.V = V;
+    cache.off = ids->offset;
+    cache.sorted = scratch;
+  }
+  k::embedding_bwd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), V, beta, cache.sorted->data(), ctx().stream);
   sink.commit(0);
 }
 static void op_embedding(const be_tensor* in, int n_in, be_tensor* out) {
