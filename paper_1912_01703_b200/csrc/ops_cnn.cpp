@@ -72,8 +72,20 @@ static void vjp_conv(Node* n, GradSink& sink) {
     gd.ab = opd; gd.D = dw->data(); gd.ldd = RSC; gd.d = dw->dtype; gd.beta = bw;
     gd.b_kmajor = false;
     TRef cols;
+    // variant 0: B = im2col(x) read in place by TMA im2col; variant 1:
+    // materialised columns + GEMM.  TMA im2col moves ~0.13 pixel/cycle/SM,
+    // so which one wins depends on the shape: autotuned per shape.
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int variant = 1;
     if (!is_pointwise(g) && opd == BE_BF16 && g.C % 64 == 0 && (K * 2) % 16 == 0) {
-      gd.conv_x = x->data();  // B = im2col(x) read in place by TMA im2col
+      char key[160];
+      snprintf(key, sizeof(key), "conv_wgrad:%d,%d,%d,%d,%d,%d,%d,%d,%d", g.N, g.H, g.W, g.C, g.K, g.R, g.S,
+               g.stride, g.pad);
+      variant = tune_choose(key, 2, 0, &e0, &e1);
+    }
+    if (e0) cudaEventRecord(e0, s);
+    if (variant == 0) {
+      gd.conv_x = x->data();
       gd.conv_g = g;
     } else {
       int64_t ldc;
@@ -81,6 +93,7 @@ static void vjp_conv(Node* n, GradSink& sink) {
       gd.B = cols->data(); gd.ldb = ldc;
     }
     k::gemm(gd, s);
+    if (e1) cudaEventRecord(e1, s);
     sink.commit(1);
   }
   if (sink.needs(0)) {

@@ -106,6 +106,52 @@ void prof_end(int idx, cudaStream_t s) {
   cudaEventRecord(g_prof[idx].b, s);
 }
 
+// ------------------------------------------------------------------ autotuning
+namespace {
+struct TuneState {
+  int tried = 0;
+  int choice = -1;
+  std::vector<cudaEvent_t> ev;  // 2 per variant
+};
+std::mutex g_tune_mu;
+std::unordered_map<std::string, TuneState> g_tune;
+}  // namespace
+
+int tune_choose(const std::string& key, int n, int dflt, cudaEvent_t* ev0, cudaEvent_t* ev1) {
+  *ev0 = *ev1 = nullptr;
+  static const int enabled = [] { const char* e = getenv("BE_TUNE"); return e ? atoi(e) : 1; }();
+  if (!enabled || n <= 1) return dflt;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  TuneState& t = g_tune[key];
+  if (t.choice >= 0) return t.choice;
+  if (t.tried < 2 * n) {
+    // round 1 warms each variant up (first-touch allocations, descriptor
+    // caches); round 2 is timed
+    const int v = t.tried % n;
+    if (t.tried++ >= n) {
+      t.ev.resize(2 * n, nullptr);
+      cudaEventCreate(&t.ev[2 * v]);
+      cudaEventCreate(&t.ev[2 * v + 1]);
+      *ev0 = t.ev[2 * v];
+      *ev1 = t.ev[2 * v + 1];
+    }
+    return v;
+  }
+  for (int v = 0; v < n; ++v)
+    if (cudaEventQuery(t.ev[2 * v + 1]) != cudaSuccess) { cudaGetLastError(); return dflt; }
+  float best = 1e30f;
+  int bv = dflt;
+  for (int v = 0; v < n; ++v) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.ev[2 * v], t.ev[2 * v + 1]);
+    if (ms < best) { best = ms; bv = v; }
+  }
+  for (cudaEvent_t e : t.ev) cudaEventDestroy(e);
+  t.ev.clear();
+  t.choice = bv;
+  return bv;
+}
+
 // ------------------------------------------------------------------ allocator
 void CachingAllocator::process_deferred_locked() {
   for (size_t i = 0; i < deferred_.size();) {
