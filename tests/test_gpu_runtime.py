@@ -1,0 +1,250 @@
+"""Runtime semantics on the B200 (-m gpu): caching allocator (PAPER.md:193-204
+§5.3), immediate free, BE_SYNC bitwise
+equivalence, bf16 end-to-end CNN parity (R8),
+and the DDP code path through NCCL at world size 1."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from gpu_common import be_init, rel
+from oracle import nets as onets, ops as oops
+from oracle.step import train_step
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _fro(x, o):
+    x, o = np.asarray(x, np.float64), np.asarray(o, np.float64)
+    return float(np.linalg.norm(x - o) / max(np.linalg.norm(o), 1e-30))
+
+
+def test_allocator_round_reuse_and_streams():
+    be = be_init()
+    import ctypes as C
+    import torch
+    call = be.api.call
+    be.synchronize()
+    be.empty_cache()  # start from an empty cache (other tests leave cached blocks)
+    s0 = be.alloc_stats()
+    p = C.c_uint64()
+    call("be_raw_alloc", C.c_uint64(1000), C.c_uint64(0), C.byref(p))
+    s1 = be.alloc_stats()
+    assert s1["bytes_in_use"] - s0["bytes_in_use"] == 1024  # round_size(1000)
+    call("be_raw_free", p)
+    s2 = be.alloc_stats()
+    assert s2["bytes_in_use"] == s0["bytes_in_use"] and s2["bytes_cached"] - s0["bytes_cached"] >= 1024
+    # same size, same stream → cache hit, no raw allocation
+    call("be_raw_alloc", C.c_uint64(1000), C.c_uint64(0), C.byref(p))
+    s3 = be.alloc_stats()
+    assert s3["cache_hit_count"] == s2["cache_hit_count"] + 1 and s3["raw_alloc_count"] == s2["raw_alloc_count"]
+    call("be_raw_free", p)
+    # another stream never reuses the first stream's pool
+    other = torch.cuda.Stream()
+    q = C.c_uint64()
+    call("be_raw_alloc", C.c_uint64(1000), C.c_uint64(other.cuda_stream), C.byref(q))
+    s4 = be.alloc_stats()
+    assert s4["raw_alloc_count"] == s3["raw_alloc_count"] + 1
+    call("be_raw_free", q)
+    # double free is an error
+    with pytest.raises(be.BeError) as e:
+        call("be_raw_free", q)
+    assert e.value.name in ("BE_E_DOUBLE_FREE", "BE_E_BAD_HANDLE")
+    # conservation and empty_cache
+    rel_bytes = be.empty_cache()
+    s5 = be.alloc_stats()
+    assert rel_bytes > 0 and s5["bytes_cached"] == 0
+    assert be.empty_cache() == 0
+
+
+def test_record_stream_defers_reuse():
+    be = be_init()
+    import torch
+    be.synchronize()
+    be.empty_cache()
+    t = be.empty((1 << 18,), "f32")
+    side = torch.cuda.Stream()
+    be.api.call("be_record_stream", t.handle, __import__("ctypes").c_uint64(side.cuda_stream))
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)  # keep the side stream busy
+    s0 = be.alloc_stats()
+    del t  # freed while still "in use" on the side stream → parked, not pooled
+    u = be.empty((1 << 18,), "f32")
+    s1 = be.alloc_stats()
+    assert s1["raw_alloc_count"] == s0["raw_alloc_count"] + 1  # could not reuse the parked block
+    side.synchronize()
+    del u
+
+
+def test_immediate_free_flat_peak():
+    """a create/drop loop keeps peak bytes flat (blocks return to
+    the pool the moment their last reference dies)."""
+    be = be_init()
+    be.reset_peak()
+    for _ in range(2000):
+        a = be.empty((4096,), "f32")
+        b = be.empty((4096,), "f32")
+        del a, b
+    s = be.alloc_stats()
+    assert s["peak_bytes_in_use"] - s["bytes_in_use"] <= 2 * 16384
+
+
+_SYNC_SCRIPT = r"""
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1912_01703_b200 as be, synth
+be.init(0)
+be.set_compute_dtype("bf16")
+net = be.nn.ResNet50(layers=(1, 1, 1, 1), base=16, classes=10)
+net.load(synth.make_params(net.param_specs(), 0))
+x = be.nn.images_to_device(synth.normal((4, 3, 64, 64), 0, 1), "bf16")
+y = be.tensor(synth.labels(4, 10, 0))
+for _ in range(2):
+    be.nn.train_step(net, (x, y), lr=0.01, momentum=0.9)
+h = __import__("hashlib").sha256()
+for k, p in net.params.items():
+    h.update(np.ascontiguousarray(p.numpy()).tobytes())
+print(json.dumps({{"digest": h.hexdigest()}}))
+"""
+
+
+def _run_sync_script(env_extra):
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", _SYNC_SCRIPT.format(root=ROOT)], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])["digest"]
+
+
+def test_sync_mode_bitwise_equivalence():
+    """BE_SYNC=1 (synchronise after every launch) gives bitwise the same
+    parameters as the asynchronous run (acceptance #3), and two
+    async runs agree bitwise (determinism: no floating-point atomics)."""
+    a = _run_sync_script({"BE_SYNC": "0"})
+    b = _run_sync_script({"BE_SYNC": "1"})
+    c = _run_sync_script({"BE_SYNC": "0"})
+    assert a == b == c
+
+
+@pytest.mark.parametrize("C,act", [(64, 1), (64, 0), (256, 1), (24, 1)])
+def test_bf16_bn_pool_residual_ops(C, act):
+    """Per-op bf16 parity with identical (bf16-valued) inputs on both sides:
+    BN(+ReLU) fwd/bwd, residual add+ReLU, 3×3/2 max pool (argmax included),
+    global avg pool.  Outputs are single bf16 roundings of fp32 results →
+    element-wise gate 1e-2 (bf16 has 8 significant bits)."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    from oracle.autograd import Var, backward
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(np.asarray(a, np.float32)))
+    t = lambda a: np.ascontiguousarray(np.asarray(a).transpose(0, 2, 3, 1))
+    tb = lambda a: np.ascontiguousarray(np.asarray(a).transpose(0, 3, 1, 2))
+    rng = np.random.default_rng(C + act)
+    N, H = 8, 14
+    x = q(rng.standard_normal((N, C, H, H)) * 1.5 + 0.3)
+    r = q(rng.standard_normal((N, C, H, H)))
+    gam = (rng.standard_normal(C) * 0.3 + 1).astype(np.float32)
+    bet = (rng.standard_normal(C) * 0.3).astype(np.float32)
+    # oracle on the same values
+    xo, ro = Var(x.astype(np.float64), True), Var(r.astype(np.float64), True)
+    go, bo = Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
+    yo, _ = oops.batchnorm2d(xo, go, bo)
+    if act:
+        yo = oops.relu(yo)
+    # device
+    xd, rd = be.tensor(t(x), requires_grad=True), be.tensor(t(r), requires_grad=True)
+    gd, bd = be.tensor(gam, requires_grad=True), be.tensor(bet, requires_grad=True)
+    yd = be.batchnorm2d(be.cast(xd, "bf16"), gd, bd, act=act)
+    assert rel(tb(yd.numpy()), yo.value) < 1e-2
+    # residual add + ReLU, then max pool and global average pool, fed the device's own y
+    yv = tb(yd.numpy())
+    zo = oops.relu(oops.add(Var(yv.astype(np.float64)), ro))
+    zd = be.add_relu(yd, be.cast(rd, "bf16"))
+    assert rel(tb(zd.numpy()), zo.value) < 1e-2
+    zv = tb(zd.numpy())
+    po, am = oops.maxpool2d(Var(zv.astype(np.float64)), 3, 2, 1)
+    pd_, amd = be.maxpool2d(zd, 3, 2, 1, with_argmax=True)
+    assert np.array_equal(tb(pd_.numpy()), po.value)  # max of stored values: exact
+    win = tb(amd.numpy()).astype(np.int64)
+    P = po.value.shape[2]
+    hh = np.arange(P)[:, None] * 2 - 1 + win // 3
+    ww = np.arange(P)[None, :] * 2 - 1 + win % 3
+    assert np.array_equal(hh * H + ww, am)  # bit-exact winners on identical inputs
+    ao = oops.avgpool_global(Var(tb(pd_.numpy()).astype(np.float64)))
+    ad = be.avgpool_global(pd_)
+    assert rel(ad.numpy(), ao.value) < 1e-2
+    # backward through BN(+ReLU) with a bf16 upstream (mask from the device output)
+    g = q(rng.standard_normal(yo.value.shape))
+    backward(yo, g.astype(np.float64))
+    yd2 = be.batchnorm2d(be.cast(xd, "bf16"), gd, bd, act=act)
+    yd2.backward(be.tensor(t(g), dtype="bf16"))
+    assert rel(tb(xd.grad.numpy()), xo.grad) < 2e-2
+    assert rel(gd.grad.numpy(), go.grad) < 1e-2 and rel(bd.grad.numpy(), bo.grad) < 1e-2
+
+
+def test_resnet_small_bf16_end_to_end():
+    """bf16 ResNet block stack vs the float64 oracle.  Deep bf16 + BN error
+    is "parity unpinned" (SURVEY §8(c) reading 15, R8): one-ulp
+    activation differences flip ReLU masks and BN re-normalisation amplifies
+    them layer by layer (measured ≈2-3 % at fc, up to ≈50 % norm-wise on the
+    cancellation-heavy early-layer β gradients).  Every op is gated
+    element-wise on identical bf16 inputs (test_bf16_bn_pool_residual_ops,
+    test_conv_op_bf16_implicit_gemm) and the same network is gated at 1e-4
+    in fp32 (test_gpu_cnn.py); here: loss at 2e-2, the fc gradient norm-wise
+    at 5e-2, and every other gradient must keep its direction (cosine ≥ 0.8)
+    and magnitude (±25 %)."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    onet = onets.ResNet50(layers=(1, 1, 1, 1), base=16, classes=10)
+    pnet = be.nn.ResNet50(layers=(1, 1, 1, 1), base=16, classes=10)
+    P = synth.make_params(onet.param_specs(), 4)
+    x = bf16_bits_to_f32(f32_to_bf16_bits(synth.normal((8, 3, 64, 64), 4, 1)))
+    y = synth.labels(8, 10, 4)
+    ref = train_step(onet, P, (x, y), lr=0.01)
+    pnet.load(P)
+    loss = pnet.loss(be.nn.images_to_device(x, "bf16"), be.tensor(y))
+    loss.backward()
+    assert rel(np.array(loss.item()), np.array(ref["loss"])) < 2e-2
+    worst = 0.0
+    for k, p in pnet.params.items():
+        g = pnet.logical(k, p.grad.numpy()).astype(np.float64).ravel()
+        o = ref["grads"][k].ravel()
+        e = _fro(g, o)
+        worst = max(worst, e)
+        if k.startswith("fc."):
+            assert e < 5e-2, (k, e)
+        cos = float(g @ o / max(np.linalg.norm(g) * np.linalg.norm(o), 1e-30))
+        ratio = float(np.linalg.norm(g) / max(np.linalg.norm(o), 1e-30))
+        assert cos >= 0.8 and 0.75 <= ratio <= 1.25, (k, cos, ratio)
+    print("resnet-small bf16 worst norm-wise grad err", worst)
+
+
+def test_ddp_world1_through_nccl_matches_single():
+    """The DDP path (ncclBroadcast at attach, bucketed ncclAllReduce during
+    backward on the comm stream, 1/world folded into SGD) at world size 1
+    gives bitwise the same step as the plain path."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    import torch  # noqa: F401  (loads libnccl.so.2 for the library's dlopen)
+    sizes = (256, 512, 256, 10)
+    P = synth.make_params(onets.MLP(sizes).param_specs(), 5)
+    x = be.tensor(synth.normal((64, 256), 5, 1), dtype="bf16")
+    y = be.tensor(synth.labels(64, 10, 5))
+    plain = be.nn.MLP(sizes).load(P)
+    for _ in range(2):
+        be.nn.train_step(plain, (x, y), lr=0.05, momentum=0.9)
+    ddp = be.nn.MLP(sizes).load(P)
+    be.dist_init(0, 1, be.dist_unique_id())
+    be.ddp_attach(ddp.parameters(), bucket_bytes=1 << 18)  # several buckets
+    for _ in range(2):
+        be.nn.train_step(ddp, (x, y), lr=0.05, momentum=0.9)
+    be.synchronize()
+    for k in P:
+        assert np.array_equal(ddp.params[k].numpy(), plain.params[k].numpy()), k
+    be.ddp_detach()
