@@ -221,16 +221,26 @@ def run_ours(args, cfg, rank, world, local_rank):
     clocks.start()
     barrier()
     l0 = be.launch_count()
-    be.prof_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         loss = step(batch)
     e1.record(stream)
     barrier()
-    be.prof_enable(False)
     ms = e0.elapsed_time(e1)
     launches = be.launch_count() - l0
+    # second, profiled pass of the same K steps: every tcgen05 GEMM / conv launch
+    # bracketed by CUDA events on its stream (the brackets cost a little, so the
+    # headline value comes from the unprofiled pass above)
+    be.prof_enable(True)
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record(stream)
+    for _ in range(args.steps):
+        loss = step(batch)
+    e5.record(stream)
+    barrier()
+    be.prof_enable(False)
+    ms_prof = e4.elapsed_time(e5)
     prof = be.prof_read()
     clk = clocks.stop()
     stats_after = be.alloc_stats()
@@ -239,21 +249,34 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- end-to-end through the public API: pinned host → device each step, loss → host
+    # ---- end-to-end through the public API: every step's batch goes pinned host → device
+    # (double-buffered on a copy stream so batch i+1 transfers while step i computes, the
+    # data loader's pinned-memory path) and the loss comes back device → host
     pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in hb]
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    dev_in = [be.empty(a.shape, d or {np.dtype(np.int32): "i32", np.dtype(np.float32): "f32"}[a.dtype])
+    shapes = [(a.shape, d or {np.dtype(np.int32): "i32", np.dtype(np.float32): "f32"}[a.dtype])
               for a, d in zip(hb, dts)]
+    pipe = be.api.InputPipeline(shapes)
+    host = [(p.data_ptr(), p.numel() * p.element_size()) for p in pinned]
     import ctypes as C
     h2d = sum(a.nbytes for a in hb)
+
+    def e2e_loop(n):
+        pipe.put(0, host)
+        loss = None
+        for i in range(n):
+            cur = i % 2
+            loss = step(pipe.get(cur))
+            pipe.release(cur)
+            if i + 1 < n:
+                pipe.put(1 - cur, host)
+            be.api.call("be_tensor_copy_to_host_async", loss.handle, C.c_void_p(loss_host.data_ptr()), 4)
+        return loss
+    e2e_loop(args.warmup)  # warm the copy stream / pipeline like the device loop
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for _ in range(args.steps):
-        for t, p in zip(dev_in, pinned):
-            be.api.call("be_tensor_copy_from_host_async", t.handle, C.c_void_p(p.data_ptr()), p.numel() * p.element_size())
-        loss = step(dev_in)
-        be.api.call("be_tensor_copy_to_host_async", loss.handle, C.c_void_p(loss_host.data_ptr()), 4)
+    e2e_loop(args.steps)
     e3.record(stream)
     barrier()
     ms_e2e = e2.elapsed_time(e3)
@@ -280,7 +303,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
             "kernel": "tcgen05 GEMM + implicit-GEMM conv launches of the step (gemm_tc*, conv_tc*)",
-            "launches_per_step": len(tc) / args.steps, "share_of_step": round(gemm_ms / ms, 4) if ms else None,
+            "launches_per_step": len(tc) / args.steps,
+            "share_of_step": round(gemm_ms / ms_prof, 4) if ms_prof else None,
+            "profiled_pass_ms_per_step": round(ms_prof / args.steps, 4),
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk_kind})"}
     shapes = {}
     for r in tc:

@@ -237,6 +237,21 @@ typedef struct {
 be_status be_prof_enable(int on);
 be_status be_prof_read(be_prof_rec* out, int cap, int* n_out);
 
+/* ------------------------------------------------------------------ streams / events
+ * Side streams and events for overlapping host↔device traffic with the
+ * compute stream (PAPER.md:185 FIFO queues; :147-149 the data loader's
+ * pinned-memory hand-off).  Handles are cudaStream_t / cudaEvent_t as uint64.
+ * A tensor written on a side stream must be ordered before its use on the
+ * compute stream with be_stream_wait_event(0, ev) (0 = compute stream). */
+be_status be_stream_create(uint64_t* stream);
+be_status be_stream_destroy(uint64_t stream);
+be_status be_event_create(uint64_t* event);
+be_status be_event_destroy(uint64_t event);
+be_status be_event_record(uint64_t event, uint64_t stream /*0 = compute*/);
+be_status be_stream_wait_event(uint64_t stream /*0 = compute*/, uint64_t event);
+/* Async host→device copy into contiguous t on `stream` (0 = compute); bumps t's version. */
+be_status be_tensor_copy_from_host_on(be_tensor t, const void* src, size_t nbytes, uint64_t stream);
+
 /* ------------------------------------------------------------------ misc */
 be_status be_synchronize(void);
 /* Read a 1-element tensor as double (synchronises). */

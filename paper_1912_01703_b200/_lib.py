@@ -122,6 +122,13 @@ def lib():
             "be_gemm": [T, C.c_int, T, C.c_int, T, T, C.c_int, C.c_float],
             "be_ddp_plan": [P(C.c_int64), C.c_int, C.c_size_t, P(C.c_int), P(C.c_int64), P(C.c_int64), C.c_int,
                             P(C.c_int)],
+            "be_stream_create": [P(C.c_uint64)],
+            "be_stream_destroy": [C.c_uint64],
+            "be_event_create": [P(C.c_uint64)],
+            "be_event_destroy": [C.c_uint64],
+            "be_event_record": [C.c_uint64, C.c_uint64],
+            "be_stream_wait_event": [C.c_uint64, C.c_uint64],
+            "be_tensor_copy_from_host_on": [T, C.c_void_p, C.c_size_t, C.c_uint64],
             "be_prof_enable": [C.c_int],
             "be_prof_read": [P(be_prof_rec), C.c_int, P(C.c_int)],
         }
@@ -155,4 +162,6 @@ EXPORTED = [
     "be_empty_cache", "be_round_size", "be_record_stream", "be_raw_alloc", "be_raw_free", "be_dist_unique_id",
     "be_dist_init", "be_ddp_attach", "be_ddp_detach", "be_allreduce_", "be_synchronize", "be_item",
     "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
+    "be_stream_create", "be_stream_destroy", "be_event_create", "be_event_destroy", "be_event_record",
+    "be_stream_wait_event", "be_tensor_copy_from_host_on",
 ]

@@ -49,9 +49,12 @@ class Tensor:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and L._lib is not None:
-            L._lib.be_release(h)
-            self._h = None
+        try:
+            if h is not None and h.value and L._lib is not None:
+                L._lib.be_release(h)
+                self._h = None
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals already cleared
+            pass
 
     @property
     def handle(self):
@@ -359,6 +362,62 @@ def im2col_offsets(N, C_, H, W, R, S, stride, pad) -> np.ndarray:
     geom = (C.c_int64 * 8)(N, C_, H, W, R, S, stride, pad)
     call("be_debug_im2col_offsets", geom, out.ctypes.data_as(C.POINTER(C.c_int64)))
     return out
+
+
+def stream_create() -> int:
+    v = C.c_uint64()
+    call("be_stream_create", C.byref(v))
+    return v.value
+
+
+def event_create() -> int:
+    v = C.c_uint64()
+    call("be_event_create", C.byref(v))
+    return v.value
+
+
+def event_record(ev: int, stream: int = 0):
+    call("be_event_record", C.c_uint64(ev), C.c_uint64(stream))
+
+
+def stream_wait_event(stream: int, ev: int):
+    call("be_stream_wait_event", C.c_uint64(stream), C.c_uint64(ev))
+
+
+def copy_from_host_on(t: Tensor, src_ptr: int, nbytes: int, stream: int = 0):
+    call("be_tensor_copy_from_host_on", t.handle, C.c_void_p(src_ptr), C.c_size_t(nbytes), C.c_uint64(stream))
+
+
+class InputPipeline:
+    """Double-buffered pinned-host → device batch hand-off on a copy stream
+    (the data loader's pinned-memory path): batch i+1 is
+    copied while step i computes.  `shapes_dtypes` = [(shape, dtype), ...]."""
+
+    def __init__(self, shapes_dtypes):
+        self.copy_stream = stream_create()
+        self.bufs = [[empty(sh, dt) for sh, dt in shapes_dtypes] for _ in range(2)]
+        self.ready = [event_create(), event_create()]
+        self.free = [event_create(), event_create()]
+        self.primed = [False, False]
+
+    def put(self, slot, host_ptrs_nbytes):
+        """Enqueue (non-blocking) the copy of a batch — list of (pinned ptr,
+        nbytes) — into buffer `slot`, after its previous user released it."""
+        if self.primed[slot]:
+            stream_wait_event(self.copy_stream, self.free[slot])
+        for t, (ptr, nb) in zip(self.bufs[slot], host_ptrs_nbytes):
+            copy_from_host_on(t, ptr, nb, self.copy_stream)
+        event_record(self.ready[slot], self.copy_stream)
+
+    def get(self, slot):
+        """Tensors of buffer `slot`; the compute stream waits for its copy."""
+        stream_wait_event(0, self.ready[slot])
+        return self.bufs[slot]
+
+    def release(self, slot):
+        """Buffer `slot` is free once the compute work enqueued so far is done."""
+        event_record(self.free[slot], 0)
+        self.primed[slot] = True
 
 
 def prof_enable(on=True):

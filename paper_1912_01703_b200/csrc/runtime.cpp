@@ -591,6 +591,56 @@ be_status be_item(be_tensor h, double* out) {
   BE_API_END
 }
 
+static cudaStream_t as_stream(uint64_t s) { return s ? reinterpret_cast<cudaStream_t>(s) : ctx().stream; }
+
+be_status be_stream_create(uint64_t* out) {
+  BE_API_BEGIN
+  require_init();
+  cudaStream_t s;
+  BE_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = reinterpret_cast<uint64_t>(s);
+  BE_API_END
+}
+be_status be_stream_destroy(uint64_t s) {
+  BE_API_BEGIN
+  BE_REQUIRE(s != 0, BE_E_ARG, "cannot destroy the compute stream");
+  BE_CHECK_CUDA(cudaStreamDestroy(reinterpret_cast<cudaStream_t>(s)));
+  BE_API_END
+}
+be_status be_event_create(uint64_t* out) {
+  BE_API_BEGIN
+  cudaEvent_t e;
+  BE_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = reinterpret_cast<uint64_t>(e);
+  BE_API_END
+}
+be_status be_event_destroy(uint64_t e) {
+  BE_API_BEGIN
+  BE_CHECK_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(e)));
+  BE_API_END
+}
+be_status be_event_record(uint64_t e, uint64_t s) {
+  BE_API_BEGIN
+  require_init();
+  BE_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(e), as_stream(s)));
+  BE_API_END
+}
+be_status be_stream_wait_event(uint64_t s, uint64_t e) {
+  BE_API_BEGIN
+  require_init();
+  BE_CHECK_CUDA(cudaStreamWaitEvent(as_stream(s), reinterpret_cast<cudaEvent_t>(e), 0));
+  BE_API_END
+}
+be_status be_tensor_copy_from_host_on(be_tensor h, const void* src, size_t nbytes, uint64_t s) {
+  BE_API_BEGIN
+  Tensor* t = check_handle(h);
+  BE_REQUIRE(t->is_contiguous(), BE_E_NONCONTIG, "copy_from_host needs a contiguous tensor");
+  BE_REQUIRE(nbytes == (size_t)t->numel() * dtype_size(t->dtype), BE_E_ARG, "size mismatch");
+  BE_CHECK_CUDA(cudaMemcpyAsync(t->data(), src, nbytes, cudaMemcpyHostToDevice, as_stream(s)));
+  t->bump_version();
+  BE_API_END
+}
+
 be_status be_prof_enable(int on) {
   BE_API_BEGIN
   std::lock_guard<std::mutex> g(g_prof_mu);
