@@ -205,6 +205,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     def step(b):
         return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4)
 
+    # setup: on-line kernel-variant autotuning (each tuned shape runs every
+    # candidate twice, cudnn.benchmark-style) before the W warm-up steps
+    for _ in range(args.tune_steps):
+        step(batch)
     for _ in range(args.warmup):
         step(batch)
     be.synchronize()
@@ -327,7 +331,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": dt_bench, "data": "synthetic (seeded, device-resident)",
         "config": {"workload": cfg["workload"], "global_batch": B * world, "per_gpu_batch": B,
                    "parallelism": f"dp{world}", "l2": "working set > L2 (params+grads+momentum stream through "
-                   "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4"},
+                   "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4",
+                   "autotune_steps": args.tune_steps},
         "e2e": {"value": round(B * world * args.steps / (ms_e2e / 1e3), 2), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
@@ -369,6 +374,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--tune-steps", type=int, default=10, help="untimed autotuning steps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

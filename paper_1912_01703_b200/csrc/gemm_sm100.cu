@@ -987,7 +987,7 @@ bool tma_ok(const void* p, int64_t ld, be_dtype dt) {
 
 template <int BN, bool X3>
 void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo,
-               cudaStream_t s) {
+               cudaStream_t s, int force_splits = 0) {
   using C = Cfg<BN, X3>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1025,7 +1025,8 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   // wgrad: M·N tiny, K = N·P·Q up to 3.2 M); fp32 partials are summed in a
   // fixed order by splitk_reduce → deterministic.
   int splits = 1;
-  if (mn * 2 <= sms && kblocks >= 8) splits = std::max(1, std::min(sms / mn, kblocks / 4));
+  if (force_splits > 0) splits = std::max(1, std::min(force_splits, kblocks));
+  else if (mn * 2 <= sms && kblocks >= 8) splits = std::max(1, std::min(sms / mn, kblocks / 4));
   int kps = (kblocks + splits - 1) / splits;
   splits = (kblocks + kps - 1) / kps;
   p.splits = splits;
@@ -1281,13 +1282,35 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
       else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
     } else {
-      cudaEvent_t ev0, ev1;
-      const int v = tune_pick(g, &ev0, &ev1);
+      // candidate list (autotuned per shape): the 1-CTA kernel
+      // with pick_bn's tile and its default split rule; the CTA pair; and,
+      // when the tile grid under-fills the 148 SMs, BN=256 / BN=128 with
+      // split-K sized to fill the machine.
+      struct Cand { int kind, bn, splits; };
+      Cand cands[5];
+      int nc = 0;
+      cands[nc++] = {0, bn, 0};
+      const int pm = pair_mode();
+      if (pm != 0 && pair_plausible(g)) cands[nc++] = {1, 256, 0};
+      const int sms = ctx().num_sms;
+      const int kbl = (g.K + 63) / 64;
+      for (int cbn : {256, 128}) {
+        const int tiles = ((g.M + BM - 1) / BM) * ((g.N + cbn - 1) / cbn);
+        if (tiles < sms && kbl >= 16 && g.N > cbn / 2) {
+          const int sp = std::max(2, std::min(sms / tiles, kbl / 4));
+          if (!(cbn == bn && sp == 1)) cands[nc++] = {0, cbn, sp};
+        }
+      }
+      int v = 0;
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      if (pm == 1 && pair_plausible(g)) v = 1;
+      else if (nc > 1) v = tune_choose("gemm:" + tune_key(g), nc, 0, &ev0, &ev1);
+      const Cand c = cands[v];
       if (ev0) cudaEventRecord(ev0, s);
-      if (v == 1) launch_tc2(g, s);
-      else if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
-      else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
-      else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
+      if (c.kind == 1) launch_tc2(g, s);
+      else if (c.bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s, c.splits);
+      else if (c.bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s, c.splits);
+      else launch_tc<64, false>(g, ahi, alo, bhi, blo, s, c.splits);
       if (ev1) cudaEventRecord(ev1, s);
     }
     if (tmp) ctx().alloc.free(tmp);  // stream-ordered reuse is safe
