@@ -418,25 +418,34 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
         sh[j] = gam ? bsh[c + j] - k[j] * sc[j] : 0.f;
       }
     }
-    for (int64_t r = r0 + rl; r < r1; r += rpi) {
-      const int64_t o = r * C + c;
-      V8 a = ld8(x, o, dt);
+    // two rows per iteration, all loads issued before any use (more bytes in
+    // flight per thread; the duplicate load of a missing second row hits L1)
+    auto accum = [&](const V8& a, V8 g, const V8& yy) {
       if (MODE == 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) { const float d = a.v[j] - k[j]; s0[j] += d; s1[j] += d * d; }
       } else {
-        V8 g = ld8(gy, o, dt);
         if (act && gam) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
         } else if (act) {
-          V8 yy = ld8(yv, o, dt);
 #pragma unroll
           for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) { s0[j] += g.v[j]; s1[j] += g.v[j] * (a.v[j] - k[j]) * is[j]; }
       }
+    };
+    for (int64_t r = r0 + rl; r < r1; r += 2 * rpi) {
+      const bool two = r + rpi < r1;
+      const int64_t o0 = r * C + c, o1 = two ? o0 + (int64_t)rpi * C : o0;
+      V8 a0 = ld8(x, o0, dt), a1 = ld8(x, o1, dt), g0, g1, y0, y1;
+      if (MODE != 0) {
+        g0 = ld8(gy, o0, dt); g1 = ld8(gy, o1, dt);
+        if (act && !gam) { y0 = ld8(yv, o0, dt); y1 = ld8(yv, o1, dt); }
+      }
+      accum(a0, g0, y0);
+      if (two) accum(a1, g1, y1);
     }
   }
   // rpi·Cg ≤ 2048: every lane's partials fit; combine over row lanes in order
@@ -489,15 +498,20 @@ __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, vo
     sh[j] = beta[c + j] - mean[c + j] * sc[j];
   }
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  for (int64_t r = r0 + rl; r < r1; r += rpi) {
-    const int64_t o = r * C + c;
-    V8 a = ld8(x, o, dt);
+  auto row = [&](int64_t o, V8 a) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float val = fmaf(a.v[j], sc[j], sh[j]);
       a.v[j] = act ? fmaxf(val, 0.f) : val;
     }
     st8(y, o, dt, a);
+  };
+  for (int64_t r = r0 + rl; r < r1; r += 2 * rpi) {
+    const bool two = r + rpi < r1;
+    const int64_t o0 = r * C + c, o1 = two ? o0 + (int64_t)rpi * C : o0;
+    V8 a0 = ld8(x, o0, dt), a1 = ld8(x, o1, dt);
+    row(o0, a0);
+    if (two) row(o1, a1);
   }
 }
 __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, const void* __restrict__ x,
@@ -526,25 +540,31 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
     k3[j] = -a * m1 + a * m2 * is * mean[c + j];
   }
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  for (int64_t r = r0 + rl; r < r1; r += rpi) {
-    const int64_t o = r * C + c;
-    V8 g = ld8(gy, o, dt), a = ld8(x, o, dt);
+  auto row = [&](int64_t o, V8 g, const V8& a, const V8& yy, const V8& prev) {
     if (act && bsh) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
     } else if (act) {
-      V8 yy = ld8(yv, o, dt);
 #pragma unroll
       for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
     }
     V8 out;
-    if (dx_beta != 0.f) out = ld8(dx, o, dt);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float val = fmaf(k1[j], g.v[j], fmaf(k2[j], a.v[j], k3[j]));
-      out.v[j] = val + (dx_beta != 0.f ? out.v[j] : 0.f);
+      out.v[j] = val + (dx_beta != 0.f ? prev.v[j] : 0.f);
     }
     st8(dx, o, dt, out);
+  };
+  // two rows per iteration, loads first (bytes in flight)
+  for (int64_t r = r0 + rl; r < r1; r += 2 * rpi) {
+    const bool two = r + rpi < r1;
+    const int64_t o0 = r * C + c, o1 = two ? o0 + (int64_t)rpi * C : o0;
+    V8 g0 = ld8(gy, o0, dt), a0 = ld8(x, o0, dt), g1 = ld8(gy, o1, dt), a1 = ld8(x, o1, dt), y0, y1, p0, p1;
+    if (act && !bsh) { y0 = ld8(yv, o0, dt); y1 = ld8(yv, o1, dt); }
+    if (dx_beta != 0.f) { p0 = ld8(dx, o0, dt); p1 = ld8(dx, o1, dt); }
+    row(o0, g0, a0, y0, p0);
+    if (two) row(o1, g1, a1, y1, p1);
   }
 }
 // Cooperative fixed-order finalize: 8 threads per channel each sum a strided

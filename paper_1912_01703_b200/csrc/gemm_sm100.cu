@@ -762,6 +762,207 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   }
 }
 
+// ---------------------------------------------------------------- small-C implicit-GEMM convolution
+// Y[m, k] = Σ_{r,s,c} x[n, p·st−pad+r, q·st−pad+s, c] · W[k, r, s, c] for C ∈ {8, 16, 32}
+// (the channel-padded image of conv1: C = 8).  A 64-wide k-block then spans
+// 64/C filter taps, so neither TMA im2col (one tap per op, ~0.13 pixel/cycle)
+// nor a materialised im2col (2.5 GB at ResNet conv1) fits.  4 gather warps own
+// one output pixel (tile row) each and copy its eight 16-B chunks per k-block
+// with cp.async (zero fill for padding and for taps past R·S) into the SW128
+// layout (chunk j of row r at j ^ (r & 7)); a per-CTA table maps each 8-channel
+// chunk kc of the K = R·S·C axis to (offset (r·W + s)·C + c0, r, s).  B (KRSC
+// weights) by TMA; MMA / TMEM / epilogue as conv_tc_kernel.
+namespace convs {
+constexpr int kThreads = 512;   // w0-3 gather, w4 TMA, w5 MMA, w6 TMEM, w8-15 epilogue
+constexpr int LAG = 3;          // cp.async groups in flight per gather thread
+constexpr int kMaxChunks = 256; // R·S·C/8 ≤ 256
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (226 * 1024 - kEpiBytes - 1280 - kMaxChunks * 16) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + kMaxChunks * 16 + 1024 + 256;
+};
+}  // namespace convs
+
+template <int BN>
+__global__ void __launch_bounds__(convs::kThreads, 1) conv_small_c_kernel(const __grid_constant__ GemmParams p) {
+  using C = convs::Cfg<BN>;
+  static_assert(C::STAGES > convs::LAG, "gather pipeline needs more stages than cp.async groups in flight");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
+  int4* chunk_tab = reinterpret_cast<int4*>(epi_smem + kEpiBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(chunk_tab + convs::kMaxChunks);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int RSC = p.cR * p.cS * p.cC;
+  const int kblocks = (RSC + 63) / 64;
+  const int lc = __ffs(p.cC) - 1;  // log2 C
+
+  for (int kc = threadIdx.x; kc < kblocks * 8; kc += blockDim.x) {
+    const int k0 = kc * 8, tap = k0 >> lc, c0 = k0 & (p.cC - 1);
+    const int r = tap / p.cS, s = tap - r * p.cS;
+    // taps past R·S: r = huge → always out of range → zero fill
+    chunk_tab[kc] = tap < p.cR * p.cS ? make_int4((r * p.cW + s) * p.cC + c0, r, s, 0)
+                                      : make_int4(0, 1 << 24, 0, 0);
+  }
+  if (threadIdx.x == 0) {
+    // full: 128 gather threads + 1 TMA expect_tx arrival
+    for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 129); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 6) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.tiles_m * p.tiles_n;
+
+  if (warp < 4) {
+    // ===================== A gather producers (one tile row per thread) =====================
+    const int tid = threadIdx.x;
+    int stage = 0; uint32_t phase = 0;
+    int pend_stage[convs::LAG + 1];
+    int npend = 0, head = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int tm = t % p.tiles_m;
+      const int m = tm * BM + tid;
+      const bool row_ok = m < p.M;
+      int hb = -(1 << 25), wb = 0;
+      long long base = 0;
+      if (row_ok) {
+        const int q = m % p.cQ, pq = m / p.cQ;
+        const int pp = pq % p.cP, n = pq / p.cP;
+        hb = pp * p.cstride - p.cpad;
+        wb = q * p.cstride - p.cpad;
+        base = (((long long)n * p.cH + hb) * p.cW + wb) * p.cC;
+      }
+      for (int kb = 0; kb < kblocks; ++kb) {
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t dst = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + tid * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int4 e = chunk_tab[kb * 8 + j];
+          const bool ok = (unsigned)(hb + e.y) < (unsigned)p.cH && (unsigned)(wb + e.z) < (unsigned)p.cW;
+          const uint16_t* src = ok ? p.x + base + e.x : p.x;
+          sm100::cp_async_16(dst + ((j ^ (tid & 7)) << 4), src, ok ? 16u : 0u);
+        }
+        sm100::cp_async_commit();
+        pend_stage[(head + npend) % (convs::LAG + 1)] = stage;
+        ++npend;
+        if (npend > convs::LAG) {
+          // oldest group complete → visible to the async proxy, then signal
+          sm100::cp_async_wait<convs::LAG>();
+          sm100::fence_proxy_async();
+          sm100::mbar_arrive(&full[pend_stage[head]]);
+          head = (head + 1) % (convs::LAG + 1);
+          --npend;
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    while (npend > 0) {
+      sm100::mbar_arrive(&full[pend_stage[head]]);
+      head = (head + 1) % (convs::LAG + 1);
+      --npend;
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      // ===================== B (weights) TMA producer =====================
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int tn = t / p.tiles_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
+          sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ===================== MMA issuer =====================
+      const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 0, 0);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * C::STAGE_BYTES), sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sm100::make_sw128_desc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb + kk * 32, 16, 1024);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue =====================
+    const int ew = warp - 8;               // 0..7
+    const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
+    int slot = 0;
+    int acc = 0; uint32_t acc_phase = 0;
+    const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = tm * BM + eq * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) sm100::bulk_wait<0>();  // TMA stores complete before exit
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -1204,9 +1405,56 @@ void launch_conv(GemmParams& p, cudaStream_t s) {
   conv_tc_kernel<BN><<<grid, conv::kThreads, C::SMEM, s>>>(p);
 }
 
+template <int BN>
+void launch_conv_small_c(GemmParams& p, cudaStream_t s) {
+  using C = convs::Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_small_c_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  p.tiles_m = (p.M + BM - 1) / BM;
+  p.tiles_n = (p.N + BN - 1) / BN;
+  const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
+  conv_small_c_kernel<BN><<<grid, convs::kThreads, C::SMEM, s>>>(p);
+}
+
+static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
+                         int act, float beta, cudaStream_t s) {
+  const int RSC = g.R * g.S * g.C;
+  if (!(g.C == 8 || g.C == 16 || g.C == 32) || g.K % 16 != 0 || (RSC + 63) / 64 * 8 > convs::kMaxChunks) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = g.N * g.P * g.Q; p.N = g.K; p.K = RSC;
+  p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
+  p.D = y; p.ldd = g.K; p.d_f32 = yd == BE_F32; p.beta = beta; p.bias = bias; p.act = act;
+  p.x = reinterpret_cast<const uint16_t*>(x);
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
+  p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
+  const int bn = g.K >= 128 ? 128 : 64;
+  encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
+  const double flops = 2.0 * p.M * (double)g.K * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 +
+                       (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
+  const int pidx = prof_begin("conv_tc_small_c", flops, bytes, p.M, g.K, RSC, s);
+  setup_store(p, y, p.d_f32 != 0, p.M, g.K, g.K);
+  if (bn == 128) launch_conv_small_c<128>(p, s);
+  else launch_conv_small_c<64>(p, s);
+  prof_end(pidx, s);
+  after_launch("conv_tc_small_c");
+  g_tc_calls++;
+  return true;
+}
+
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
                    float beta, cudaStream_t s) {
-  if (g.C % 64 != 0 || g.K % 16 != 0) return false;
+  if (g.C % 64 != 0) {
+    const char* e = getenv("BE_CONV_SMALLC");
+    if (e && e[0] == '0') return false;
+    return conv_small_c(x, w, y, g, yd, bias, act, beta, s);
+  }
+  if (g.K % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
   const char* e = getenv("BE_CONV_IMPLICIT");
   if (e && e[0] == '0') return false;

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Per-round profile capture (1 GPU, under gpurun):
+#   bench lines for every config, and for each config the ncu launch list of
+#   the K timed steps only (NVTX range "timed" pushed by bench.py).
+# usage: tools/prof_round.sh r01 "c2 c4 c3 c5 c1"
+R=${1:-r01}
+CFGS=${2:-"c2 c4 c3 c5 c1"}
+mkdir -p gpurun_out
+for c in $CFGS; do
+  python bench.py --config $c --steps 30 --warmup 5 --cpu-budget 10 > gpurun_out/${R}_${c}_bench.json 2> gpurun_out/${R}_${c}_bench.err
+  ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/${R}_${c}_launches.csv \
+      python bench.py --config $c --steps 2 --warmup 3 --tune-steps 4 --no-cpu-baseline > /dev/null 2>&1
+done
+ls -la gpurun_out
