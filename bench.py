@@ -172,7 +172,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import paper_1912_01703_b200 as be
     torch.cuda.set_device(local_rank)
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.Stream(priority=-1)  # compute stream outranks the side streams
     be.init(local_rank, stream.cuda_stream)
     be.set_compute_dtype(cfg["dtype"])
     dist = None
@@ -202,13 +202,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         return out
     batch = dev_batch()
 
-    def step(b):
-        return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4)
+    def step(b, overlap=args.sgd == "overlap"):
+        return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4, overlap_sgd=overlap)
 
     # setup: on-line kernel-variant autotuning (each tuned shape runs every
     # candidate twice, cudnn.benchmark-style) before the W warm-up steps
+    # (tuned with the update after backward: an overlapped update running
+    # beside a candidate would skew its timing)
     for _ in range(args.tune_steps):
-        step(batch)
+        step(batch, overlap=False)
     for _ in range(args.warmup):
         step(batch)
     be.synchronize()
@@ -278,11 +280,28 @@ def run_ours(args, cfg, rank, world, local_rank):
                 pipe.put(1 - cur, host)
             be.api.call("be_tensor_copy_to_host_async", loss.handle, C.c_void_p(loss_host.data_ptr()), 4)
         return loss
-    e2e_loop(args.warmup)  # warm the copy stream / pipeline like the device loop
-    barrier()
+    # warm the copy stream / pipeline like the device loop; the host link needs
+    # tens of ms of traffic after the device-only passes before it copies at
+    # full rate (measured: first 30-step pass 0.58 ms/step, then 0.46-0.47)
+    tw = time.perf_counter()
+    while True:
+        e2e_loop(max(args.warmup, 3))
+        barrier()
+        if time.perf_counter() - tw > 0.1:
+            break
+    if os.environ.get("BENCH_E2E_DEBUG"):
+        for rep in range(3):
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            e2e_loop(args.steps)
+            d1.record(stream)
+            barrier()
+            print(f"e2e rep {rep}: {d0.elapsed_time(d1) / args.steps:.4f} ms/step", file=sys.stderr, flush=True)
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
+    th0 = time.perf_counter()
     e2e_loop(args.steps)
+    host_ms_e2e = (time.perf_counter() - th0) * 1e3 / args.steps
     e3.record(stream)
     barrier()
     ms_e2e = e2.elapsed_time(e3)
@@ -333,10 +352,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": dt_bench, "data": "synthetic (seeded, device-resident)",
         "config": {"workload": cfg["workload"], "global_batch": B * world, "per_gpu_batch": B,
                    "parallelism": f"dp{world}", "l2": "working set > L2 (params+grads+momentum stream through "
-                   "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4",
+                   "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4, "
+                   + ("overlapped with backward (be_sgd_overlap)" if args.sgd == "overlap" else "fused after backward"),
                    "autotune_steps": args.tune_steps},
         "e2e": {"value": round(B * world * args.steps / (ms_e2e / 1e3), 2), "unit": "samples/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+                "host_enqueue_ms_per_step": round(host_ms_e2e, 4)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -378,6 +399,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--tune-steps", type=int, default=10, help="untimed autotuning steps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sgd", default="overlap", choices=["overlap", "fused"],
+                    help="overlap: per-parameter SGD inside backward on a side stream; fused: one launch after")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]

@@ -183,6 +183,18 @@ be_status be_zero_grad(const be_tensor* params, int n);
  * has no grad.  Each param's version bumps by 1. */
 be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum,
                       float weight_decay);
+/* Overlapped SGD (the optimizer step inside backward; "overlap
+ * ... execution"): registers params (f32 leaves, one ref each is taken) for the
+ * same update as be_sgd_step, applied by every later be_backward as soon as a
+ * param's gradient is final (all edges to it processed), on a side stream
+ * that overlaps the remaining backward kernels; with DDP attached, on the comm
+ * stream right behind the param's bucket allreduce.  be_backward returns with
+ * the compute stream ordered after every update, so the next op sees the new
+ * values.  Results are bitwise those of be_sgd_step.  Registered params must
+ * not be passed to be_sgd_step (BE_E_ARG).  n = 0 unregisters all.
+ * Params that get no gradient in a backward are not updated. */
+be_status be_sgd_overlap(const be_tensor* params, int n, float lr, float momentum,
+                         float weight_decay);
 
 /* ------------------------------------------------------------------ allocator */
 struct be_alloc_stats {
@@ -224,7 +236,7 @@ be_status be_ddp_plan(const int64_t* numels, int n, size_t bucket_bytes, int* bu
 be_status be_allreduce_(be_tensor t);
 
 /* ------------------------------------------------------------------ profiling
- * When enabled, every GEMM launch (the dominant kernel class) is bracketed
+ * When enabled, every GEMM / conv / SGD launch (the dominant kernel classes) is bracketed
  * by CUDA events on the stream it is launched on; be_prof_read synchronises
  * and returns one record per launch (then clears).  flops / bytes are the
  * ALGORITHMIC counts of that launch: 2·M·N·K and the operand + output bytes. */
@@ -233,6 +245,7 @@ typedef struct {
   double flops, bytes;
   float ms;
   int m, n, k;
+  float t_start_ms;  /* start relative to the first record's start (timeline across streams) */
 } be_prof_rec;
 be_status be_prof_enable(int on);
 be_status be_prof_read(be_prof_rec* out, int cap, int* n_out);

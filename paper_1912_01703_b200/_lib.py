@@ -41,7 +41,7 @@ class be_alloc_stats(C.Structure):
 
 class be_prof_rec(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("flops", C.c_double), ("bytes", C.c_double), ("ms", C.c_float),
-                ("m", C.c_int), ("n", C.c_int), ("k", C.c_int)]
+                ("m", C.c_int), ("n", C.c_int), ("k", C.c_int), ("t_start_ms", C.c_float)]
 
 
 class be_linear_attrs(C.Structure):
@@ -105,6 +105,7 @@ def lib():
             "be_grad": [T, P(T)],
             "be_zero_grad": [P(T), C.c_int],
             "be_sgd_step": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
+            "be_sgd_overlap": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
             "be_alloc_stats": [P(be_alloc_stats)],
             "be_alloc_reset_peak": [],
             "be_empty_cache": [P(C.c_uint64)],
@@ -163,5 +164,5 @@ EXPORTED = [
     "be_dist_init", "be_ddp_attach", "be_ddp_detach", "be_allreduce_", "be_synchronize", "be_item",
     "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
     "be_stream_create", "be_stream_destroy", "be_event_create", "be_event_destroy", "be_event_record",
-    "be_stream_wait_event", "be_tensor_copy_from_host_on",
+    "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap",
 ]

@@ -327,6 +327,13 @@ def sgd_step(params, lr, momentum=0.0, weight_decay=0.0):
     call("be_sgd_step", _handles(params), len(params), C.c_float(lr), C.c_float(momentum), C.c_float(weight_decay))
 
 
+def sgd_overlap(params, lr=0.0, momentum=0.0, weight_decay=0.0):
+    """Register params for the overlapped SGD update inside every later
+    backward (be_sgd_overlap); sgd_overlap([]) unregisters."""
+    call("be_sgd_overlap", _handles(params) if params else None, len(params), C.c_float(lr), C.c_float(momentum),
+         C.c_float(weight_decay))
+
+
 def zero_grad(params):
     call("be_zero_grad", _handles(params), len(params))
 
@@ -428,7 +435,7 @@ def prof_read(cap=100000):
     recs = (L.be_prof_rec * cap)()
     n = C.c_int()
     call("be_prof_read", recs, cap, C.byref(n))
-    return [dict(name=r.name.decode(), flops=r.flops, bytes=r.bytes, ms=r.ms, m=r.m, n=r.n, k=r.k)
+    return [dict(name=r.name.decode(), flops=r.flops, bytes=r.bytes, ms=r.ms, m=r.m, n=r.n, k=r.k, t0=r.t_start_ms)
             for r in recs[:n.value]]
 
 

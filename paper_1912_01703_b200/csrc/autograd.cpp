@@ -163,6 +163,7 @@ void accumulate_leaf(Tensor* leaf, Tensor* g) {
     leaf->grad->bump_version();
   }
   if (ddp_active()) ddp_on_leaf_grad_ready(leaf);
+  else if (opt_param(leaf)) opt_on_grad_final(leaf);
 }
 }  // namespace
 
@@ -183,10 +184,14 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
   if (ddp_active()) ddp_begin_backward();
   if (!root->grad_fn) {  // leaf root
     accumulate_leaf(root, seed.get());
+    opt_end_backward();
     return;
   }
-  // 1. dependency counts
+  // 1. dependency counts (+ per-leaf use counts for the overlapped optimizer:
+  // a registered parameter's gradient is final once every edge to it is done)
+  const bool opt = opt_active() && !ddp_active();
   std::unordered_map<Node*, int> deps;
+  std::unordered_map<Tensor*, int> leaf_uses;
   std::vector<Node*> stack{root->grad_fn};
   std::unordered_set<Node*> seen{root->grad_fn};
   while (!stack.empty()) {
@@ -195,11 +200,15 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
     BE_REQUIRE(!n->consumed, BE_E_DOUBLE_BACKWARD,
                std::string("backward through ") + n->name + " a second time without retain_graph");
     for (Edge& e : n->edges) {
+      if (opt && e.kind == Edge::LEAF && opt_param(e.leaf)) leaf_uses[e.leaf]++;
       if (e.kind != Edge::NODE) continue;
       deps[e.node]++;
       if (seen.insert(e.node).second) stack.push_back(e.node);
     }
   }
+  std::vector<Tensor*> final_leaves;             // completed by the current node's VJP
+  std::vector<Tensor*> ddp_leaves;               // DDP: grads landed in the current node's VJP
+  std::unordered_set<Tensor*> partial_leaves;    // got a gradient, some edges never ran
   // 2. reverse-topological sweep
   std::unordered_map<PKey, Tensor*, PKeyHash> pending;  // owned refs
   pending[{root->grad_fn, root->output_nr}] = seed.release();
@@ -271,7 +280,11 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
         Edge& e = n->edges[i];
         if (e.kind == Edge::LEAF) {
           t->bump_version();
-          if (ddp_active()) ddp_on_leaf_grad_ready(e.leaf);
+          if (ddp_active()) ddp_leaves.push_back(e.leaf);
+          else if (opt && opt_param(e.leaf)) {
+            partial_leaves.insert(e.leaf);
+            if (--leaf_uses[e.leaf] == 0) { final_leaves.push_back(e.leaf); partial_leaves.erase(e.leaf); }
+          }
         }
       };
       if (any) {
@@ -282,6 +295,14 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
                                    " was modified in place after it was saved");
         }
         n->vjp(n, sink);
+        // updates are enqueued only after every kernel of this VJP (which may
+        // still read the parameter or its bf16 shadow after committing dW)
+        for (Tensor* leaf : final_leaves) opt_on_grad_final(leaf);
+        final_leaves.clear();
+        // likewise DDP bucket launches (their allreduce may be followed by
+        // the overlapped update of the bucket's parameters)
+        for (Tensor* leaf : ddp_leaves) ddp_on_leaf_grad_ready(leaf);
+        ddp_leaves.clear();
       }
       n->upstream_is_ones = false;
       for (int k2 = 0; k2 < (int)n->outs.size(); ++k2) {
@@ -299,6 +320,8 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
     throw;
   }
   for (auto& kv : pending) tensor_drop(kv.second);
+  for (Tensor* leaf : partial_leaves) opt_on_grad_final(leaf);
+  opt_end_backward();
 }
 
 }  // namespace be

@@ -95,6 +95,14 @@ void launch_bucket(Bucket& b) {
   BE_CHECK_CUDA(cudaEventRecord(b.ready, c.stream));
   BE_CHECK_CUDA(cudaStreamWaitEvent(c.comm_stream, b.ready, 0));
   BE_CHECK_NCCL(nccl().allReduce(b.storage->ptr, b.storage->ptr, b.numel, ncclFloat, ncclSum, d.comm, c.comm_stream));
+  if (opt_active()) {
+    // overlapped SGD: the bucket's parameters are updated on the comm stream
+    // right behind their allreduce (1/world folded into the kernel)
+    std::vector<Tensor*> ps;
+    for (int i : b.params)
+      if (d.ready[i]) ps.push_back(d.params[i]);
+    opt_launch_params(ps, c.comm_stream, 1.f / (float)d.world);
+  }
   BE_CHECK_CUDA(cudaEventRecord(b.done, c.comm_stream));
   b.launched = true;
   d.allreduce_calls++;

@@ -232,7 +232,7 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
 }
 
 template <int BN, bool X3>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, X3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -423,7 +423,7 @@ constexpr int TMEM_COLS = 512;            // 2 accumulators × 256 columns
 constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
 }  // namespace pair
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
     gemm_tc2_kernel(const __grid_constant__ GemmParams p) {
   using namespace pair;
   extern __shared__ uint8_t smem_raw[];
@@ -594,7 +594,7 @@ struct Cfg {
 }  // namespace conv
 
 template <int BN>
-__global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __maxnreg__(128) conv_tc_kernel(const __grid_constant__ GemmParams p) {
   using C = conv::Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

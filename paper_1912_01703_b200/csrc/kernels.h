@@ -84,8 +84,9 @@ void bce_logits(const void* z, be_dtype zd, const int32_t* y, int64_t B, float* 
 struct SgdEntry {
   float* p; const float* g; uint16_t* shadow; float* mom; int64_t n;
 };
+// blocks_per_sm: persistent grid of num_sms × blocks_per_sm blocks
 void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float wd, float scale,
-               cudaStream_t s);
+               cudaStream_t s, int blocks_per_sm = 8);
 
 // ------------------------------------------------------------------ conv / pool / bn
 // Implicit-GEMM convolution on tcgen05 (bf16, C % 64 == 0): y[NPQ, K] =

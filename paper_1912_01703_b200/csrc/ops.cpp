@@ -686,44 +686,6 @@ be_status be_copy_(be_tensor dst, be_tensor src) {
   BE_API_END
 }
 
-be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum, float weight_decay) {
-  BE_API_BEGIN
-  std::vector<k::SgdEntry> es;
-  es.reserve(n);
-  std::vector<Tensor*> ts;
-  for (int i = 0; i < n; ++i) {
-    Tensor* p = check_handle(params[i]);
-    BE_REQUIRE(p->dtype == BE_F32 && p->is_contiguous(), BE_E_DTYPE, "sgd: params must be contiguous f32");
-    BE_REQUIRE(p->grad != nullptr, BE_E_MISSING_GRAD, "sgd: parameter " + std::to_string(i) + " has no grad");
-    k::SgdEntry e{};
-    e.p = p->ptr<float>();
-    e.g = p->grad->ptr<float>();
-    e.n = p->numel();
-    if (momentum != 0.f) {
-      if (!p->mom_block) {
-        p->mom_block = ctx().alloc.allocate(sizeof(float) * std::max<int64_t>(1, e.n), ctx().stream);
-        p->mom = reinterpret_cast<float*>(p->mom_block->ptr);
-        k::fill(p->mom, e.n, BE_F32, 0.0, ctx().stream);  // v0 = 0 ⇒ v1 = g'
-      }
-      e.mom = p->mom;
-    }
-    // keep the bf16 shadow in lock-step when it exists (mixed precision)
-    if (p->shadow && p->shadow_version == p->version()) e.shadow = p->shadow->ptr<uint16_t>();
-    es.push_back(e);
-    ts.push_back(p);
-  }
-  if (ddp_active()) ddp_wait_all();
-  k::sgd_multi(es.data(), (int)es.size(), lr, momentum, weight_decay, ddp_active() ? ddp_grad_scale() : 1.f,
-               ctx().stream);
-  for (size_t i = 0; i < ts.size(); ++i) {
-    Tensor* p = ts[i];
-    const bool shadow_synced = es[i].shadow != nullptr;
-    p->bump_version();
-    if (shadow_synced) { p->shadow->bump_version(); p->shadow_version = p->version(); }
-  }
-  BE_API_END
-}
-
 be_status be_gemm(be_tensor A, int trans_a, be_tensor Bt, int trans_b, be_tensor D, be_tensor bias, int act,
                   float beta) {
   BE_API_BEGIN

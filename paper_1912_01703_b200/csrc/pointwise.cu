@@ -437,9 +437,15 @@ __global__ void bce_kernel(const void* z, be_dtype zd, const int32_t* y, int64_t
 constexpr int kSgdMax = 256;
 struct SgdTable {
   int n;
-  int64_t start[kSgdMax + 1];  // prefix sums of chunks (in units of 1024 elements)
+  int64_t start[kSgdMax + 1];  // prefix sums of chunks (in units of kSgdChunk elements)
   SgdEntry e[kSgdMax];
 };
+// One chunk = 4096 elements; each thread owns 4 float4 of it (stride 1024
+// elements → coalesced) and issues all its loads before any arithmetic:
+// ~192 B in flight per thread, so the kernel keeps HBM busy even with only a
+// couple of blocks per SM (when it overlaps backward GEMMs, be_sgd_overlap).
+constexpr int kSgdChunk = 4096;
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdTable t, float lr, float mu, float wd,
                                                   float scale) {
   const int64_t total_chunks = t.start[t.n];
@@ -450,31 +456,39 @@ __global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdTab
       if (t.start[mid] <= c) lo = mid; else hi = mid - 1;
     }
     const SgdEntry& e = t.e[lo];
-    const int64_t base = (c - t.start[lo]) * 1024;
-    const int64_t end = min(e.n, base + 1024);
+    const int64_t base = (c - t.start[lo]) * kSgdChunk;
+    const int64_t end = min(e.n, base + kSgdChunk);
     const bool vec = ((reinterpret_cast<uintptr_t>(e.p) | reinterpret_cast<uintptr_t>(e.g) |
                        reinterpret_cast<uintptr_t>(e.mom)) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(e.shadow) & 7) == 0;
-    if (vec && base + 1024 <= e.n) {
-      const int64_t i = base + threadIdx.x * 4;
-      float4 p = *reinterpret_cast<const float4*>(e.p + i);
-      float4 g = *reinterpret_cast<const float4*>(e.g + i);
-      float pv[4] = {p.x, p.y, p.z, p.w}, gv[4] = {g.x, g.y, g.z, g.w};
-      float mv[4] = {0, 0, 0, 0};
-      if (e.mom) { float4 m4 = *reinterpret_cast<const float4*>(e.mom + i); mv[0] = m4.x; mv[1] = m4.y; mv[2] = m4.z; mv[3] = m4.w; }
+    if (vec && base + kSgdChunk <= e.n) {
+      float4 p4[4], g4[4], m4[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float gg = gv[j] * scale + wd * pv[j];
-        if (e.mom) { mv[j] = mu * mv[j] + gg; gg = mv[j]; }
-        pv[j] = pv[j] - lr * gg;
+      for (int k = 0; k < 4; ++k) {
+        const int64_t i = base + (threadIdx.x + k * 256) * 4;
+        p4[k] = ld4(e.p + i);
+        g4[k] = ld4(e.g + i);
+        m4[k] = e.mom ? ld4(e.mom + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      *reinterpret_cast<float4*>(e.p + i) = make_float4(pv[0], pv[1], pv[2], pv[3]);
-      if (e.mom) *reinterpret_cast<float4*>(e.mom + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-      if (e.shadow) {
-        uint2 u;
-        u.x = (uint32_t)f2bf(pv[0]) | ((uint32_t)f2bf(pv[1]) << 16);
-        u.y = (uint32_t)f2bf(pv[2]) | ((uint32_t)f2bf(pv[3]) << 16);
-        *reinterpret_cast<uint2*>(e.shadow + i) = u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t i = base + (threadIdx.x + k * 256) * 4;
+        float pv[4] = {p4[k].x, p4[k].y, p4[k].z, p4[k].w}, gv[4] = {g4[k].x, g4[k].y, g4[k].z, g4[k].w};
+        float mv[4] = {m4[k].x, m4[k].y, m4[k].z, m4[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float gg = gv[j] * scale + wd * pv[j];
+          if (e.mom) { mv[j] = mu * mv[j] + gg; gg = mv[j]; }
+          pv[j] = pv[j] - lr * gg;
+        }
+        *reinterpret_cast<float4*>(e.p + i) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+        if (e.mom) *reinterpret_cast<float4*>(e.mom + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+        if (e.shadow) {
+          uint2 u;
+          u.x = (uint32_t)f2bf(pv[0]) | ((uint32_t)f2bf(pv[1]) << 16);
+          u.y = (uint32_t)f2bf(pv[2]) | ((uint32_t)f2bf(pv[3]) << 16);
+          *reinterpret_cast<uint2*>(e.shadow + i) = u;
+        }
       }
     } else {
       for (int64_t i = base + threadIdx.x; i < end; i += 256) {
@@ -566,7 +580,7 @@ void bce_logits(const void* z, be_dtype zd, const int32_t* y, int64_t B, float* 
   reduce_final<<<1, 1024, 0, s>>>(row_loss, (int)B, loss_out, 1.f / (float)B);
   after_launch("bce_mean");
 }
-void sgd_multi(const SgdEntry* e, int n, float lr, float mu, float wd, float scale, cudaStream_t s) {
+void sgd_multi(const SgdEntry* e, int n, float lr, float mu, float wd, float scale, cudaStream_t s, int blocks_per_sm) {
   for (int off = 0; off < n; off += kSgdMax) {
     SgdTable t;
     memset(&t, 0, sizeof(t));
@@ -574,11 +588,16 @@ void sgd_multi(const SgdEntry* e, int n, float lr, float mu, float wd, float sca
     t.start[0] = 0;
     for (int i = 0; i < t.n; ++i) {
       t.e[i] = e[off + i];
-      t.start[i + 1] = t.start[i] + (t.e[i].n + 1023) / 1024;
+      t.start[i + 1] = t.start[i] + (t.e[i].n + kSgdChunk - 1) / kSgdChunk;
     }
     if (t.start[t.n] == 0) continue;
-    const int grid = (int)std::min<int64_t>(t.start[t.n], (int64_t)ctx().num_sms * 8);
+    const int grid = (int)std::min<int64_t>(t.start[t.n], (int64_t)ctx().num_sms * blocks_per_sm);
+    double bytes = 0;
+    for (int i = 0; i < t.n; ++i)
+      bytes += (double)t.e[i].n * (12 + (t.e[i].mom ? 8 : 0) + (t.e[i].shadow ? 2 : 0));
+    const int pidx = prof_begin("sgd", 0.0, bytes, t.n, 0, 0, s);
     sgd_kernel<<<grid, 256, 0, s>>>(t, lr, mu, wd, scale);
+    prof_end(pidx, s);
     after_launch("sgd_multi");
   }
 }

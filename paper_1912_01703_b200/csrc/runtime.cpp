@@ -388,7 +388,10 @@ be_status be_init(int device, uint64_t cuda_stream) {
     c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     c.own_stream = false;
   } else {
-    BE_CHECK_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    // highest priority: side streams (overlapped SGD, copies) yield to it
+    int least = 0, greatest = 0;
+    BE_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    BE_CHECK_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, greatest));
     c.own_stream = true;
   }
   const char* sm = getenv("BE_SYNC");
@@ -663,6 +666,7 @@ be_status be_prof_read(be_prof_rec* out, int cap, int* n_out) {
       o.bytes = r.bytes;
       o.m = r.m; o.n = r.n; o.k = r.k;
       cudaEventElapsedTime(&o.ms, r.a, r.b);
+      cudaEventElapsedTime(&o.t_start_ms, g_prof.front().a, r.a);
     }
     ++n;
     g_ev_pool.push_back(r.a);

@@ -122,6 +122,7 @@ struct Tensor {
   float* mom = nullptr;       // SGD momentum buffer (fp32), owned
   Block* mom_block = nullptr;
   int ddp_slot = -1;          // index in DDP param table
+  int opt_slot = -1;          // index in the overlapped-SGD table
 
   int64_t numel() const {
     int64_t n = 1;
@@ -236,6 +237,7 @@ struct Context {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t opt_stream = nullptr;   // overlapped SGD
   be_dtype compute = BE_F32;
   bool sync_mode = false;
   CachingAllocator alloc;
@@ -262,5 +264,16 @@ Tensor* ddp_grad_view(Tensor* leaf);     // bucket view for a param grad or null
 void ddp_wait_all();                     // compute stream waits on all bucket allreduces
 float ddp_grad_scale();
 void ddp_begin_backward();
+// DDP: params of a reduced bucket (for the overlapped optimizer, launched on
+// the comm stream right after the bucket's allreduce)
+void opt_launch_params(const std::vector<Tensor*>& ps, cudaStream_t s, float scale);
+
+// Overlapped SGD (optim.cpp; be_sgd_overlap): the engine reports each
+// registered parameter whose gradient is final; its update runs on a side
+// stream while backward continues.
+bool opt_active();
+bool opt_param(const Tensor* leaf);      // registered for overlapped SGD
+void opt_on_grad_final(Tensor* leaf);    // (non-DDP) grad complete for this backward
+void opt_end_backward();                 // flush; compute stream waits for every update
 
 }  // namespace be

@@ -294,12 +294,20 @@ class NCF(Model):
         return T.bce_logits(z, y)
 
 
-def train_step(model: Model, batch, lr=0.01, momentum=0.0, weight_decay=0.0):
-    """One eager step: zero_grad (release), forward, backward, fused SGD.
+def train_step(model: Model, batch, lr=0.01, momentum=0.0, weight_decay=0.0, overlap_sgd=False):
+    """One eager step: zero_grad (release), forward, backward, SGD.
+    overlap_sgd=False: one fused multi-tensor SGD launch after backward;
+    True: each parameter is updated inside backward as soon as its gradient
+    is final, on a side stream (be_sgd_overlap) — same values, bitwise.
     Returns the (device) loss tensor; nothing here synchronises."""
     params = model.parameters()
+    key = (lr, momentum, weight_decay) if overlap_sgd else None
+    if getattr(model, "_overlap", None) != key:
+        T.sgd_overlap(params, lr, momentum, weight_decay) if overlap_sgd else T.sgd_overlap([])
+        model._overlap = key
     T.zero_grad(params)
     loss = model.loss(*batch)
     loss.backward()
-    T.sgd_step(params, lr, momentum, weight_decay)
+    if not overlap_sgd:
+        T.sgd_step(params, lr, momentum, weight_decay)
     return loss

@@ -248,3 +248,58 @@ def test_ddp_world1_through_nccl_matches_single():
     for k in P:
         assert np.array_equal(ddp.params[k].numpy(), plain.params[k].numpy()), k
     be.ddp_detach()
+    # DDP + overlapped SGD: each bucket's params are updated on the comm stream
+    # right behind its allreduce — still bitwise the plain step
+    ddp2 = be.nn.MLP(sizes).load(P)
+    be.ddp_attach(ddp2.parameters(), bucket_bytes=1 << 18)
+    for _ in range(2):
+        be.nn.train_step(ddp2, (x, y), lr=0.05, momentum=0.9, overlap_sgd=True)
+    be.synchronize()
+    for k in P:
+        assert np.array_equal(ddp2.params[k].numpy(), plain.params[k].numpy()), k
+    be.sgd_overlap([])
+    be.ddp_detach()
+
+
+@pytest.mark.parametrize("net", ["mlp", "resnet"])
+def test_overlapped_sgd_bitwise_equals_fused(net):
+    """be_sgd_overlap (each parameter updated inside backward, on a side
+    stream, as soon as its gradient is final) gives bitwise the parameters of
+    the fused be_sgd_step after several momentum steps — i.e. no update reads
+    a partial gradient and no forward reads a stale parameter or bf16 shadow."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    if net == "mlp":
+        sizes = (1024, 2048, 1536, 10)  # 2.1 M + 3.1 M params: several overlap groups
+        P = synth.make_params(onets.MLP(sizes).param_specs(), 6)
+        mk = lambda: be.nn.MLP(sizes).load(P)  # noqa: E731
+        batch = (be.tensor(synth.normal((128, 1024), 6, 1), dtype="bf16"), be.tensor(synth.labels(128, 10, 6)))
+    else:
+        P = synth.make_params(onets.ResNet50(layers=(1, 1, 1, 1), base=16, classes=10).param_specs(), 6)
+        mk = lambda: be.nn.ResNet50(layers=(1, 1, 1, 1), base=16, classes=10).load(P)  # noqa: E731
+        x = bf16_bits_to_f32(f32_to_bf16_bits(synth.normal((8, 3, 64, 64), 6, 1)))
+        batch = (be.nn.images_to_device(x, "bf16"), be.tensor(synth.labels(8, 10, 6)))
+    # settle the per-shape kernel autotuner first (while it is still trying
+    # candidates, two models stepping alternately would get different GEMM
+    # variants — different, equally valid summation orders)
+    scratch = mk()
+    for _ in range(12):
+        be.nn.train_step(scratch, batch, lr=0.05)
+    be.synchronize()
+    for _ in range(2):
+        be.nn.train_step(scratch, batch, lr=0.05)
+    fused, over = mk(), mk()
+    lf = lo = None
+    for _ in range(3):
+        lf = be.nn.train_step(fused, batch, lr=0.05, momentum=0.9, weight_decay=1e-4)
+        lo = be.nn.train_step(over, batch, lr=0.05, momentum=0.9, weight_decay=1e-4, overlap_sgd=True)
+    be.synchronize()
+    assert lf.item() == lo.item()
+    for k in P:
+        assert np.array_equal(over.params[k].numpy(), fused.params[k].numpy()), k
+    # a registered parameter cannot also be stepped by be_sgd_step
+    with pytest.raises(be.BeError) as ei:
+        be.sgd_step(over.parameters(), 0.1)
+    assert ei.value.name == "BE_E_ARG"
+    be.sgd_overlap([])

@@ -11,7 +11,7 @@ import bench  # noqa: E402
 import paper_1912_01703_b200 as be  # noqa: E402
 
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-stream = torch.cuda.Stream()
+stream = torch.cuda.Stream(priority=-1)  # compute stream outranks the side streams
 be.init(0, stream.cuda_stream)
 be.set_compute_dtype(cfg["dtype"])
 model = bench.make_model(cfg, be)
