@@ -276,6 +276,19 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
         pending[key] = t;
         return true;
       };
+      sink.fuse = [&](int i, k::SgdFuse* f) -> bool {
+        if (!opt) return false;
+        Edge& e = n->edges[i];
+        if (e.kind != Edge::LEAF || !opt_param(e.leaf) || e.leaf->grad) return false;
+        auto it = leaf_uses.find(e.leaf);
+        if (it == leaf_uses.end() || it->second != 1) return false;  // more contributions to come
+        return opt_fuse_desc(e.leaf, f);
+      };
+      sink.fused = [&](int i) {
+        Edge& e = n->edges[i];
+        --leaf_uses[e.leaf];
+        opt_fused_done(e.leaf);
+      };
       sink.finalize = [&](int i, Tensor* t) {
         Edge& e = n->edges[i];
         if (e.kind == Edge::LEAF) {

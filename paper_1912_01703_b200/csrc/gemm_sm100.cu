@@ -33,6 +33,7 @@
 
 #include "kernels.h"
 #include "runtime.h"
+#include "sgd_math.cuh"
 #include "sm100.cuh"
 
 namespace be { namespace k {
@@ -67,10 +68,25 @@ struct __align__(64) GemmParams {
   // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
   int tma_store;
   CUtensorMap td;
+  // fused SGD epilogue (kernels.h SgdFuse): acc = gradient of P[M, N]
+  int upd;
+  float* upd_p;
+  float* upd_v;
+  uint16_t* upd_shadow;
+  float lr, mu, wd, gscale;
+  CUtensorMap tp[2];          // P, V as fp32 [M, N] maps, box 32 × 32 (fused-SGD epilogue loads)
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
-template <int BN, bool X3>
+// Fused-SGD epilogue: 4 warps (one per TMEM lane quarter), each with three
+// 10 KB buffers; a buffer holds one 32 × 32 chunk of P (4 KB) and V (4 KB) in
+// the TMA SW128 layout, updated in place, + its bf16 shadow (2 KB, SW64).
+constexpr int kUpdWarps = 4;
+constexpr int kUpdBufs = 3;
+constexpr int kUpdBufBytes = 4096 + 4096 + 2048;
+constexpr int kUpdWarpBytes = kUpdBufs * kUpdBufBytes;
+
+template <int BN, bool X3, bool UPD = false>
 struct Cfg {
   static constexpr int ESIZE = X3 ? 4 : 2;
   static constexpr int BK = 128 / ESIZE;           // one 128-B swizzle row of K
@@ -79,10 +95,11 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;         // BM rows x 128 B
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int STAGES_RAW = (226 * 1024 - kEpiBytes - 1280) / STAGE_BYTES;
+  static constexpr int EPI_BYTES = UPD ? kUpdWarps * kUpdWarpBytes : kEpiBytes;
+  static constexpr int STAGES_RAW = (226 * 1024 - EPI_BYTES - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr int CH = 128 / ESIZE;           // MN elements per 128-B chunk
 };
 
@@ -168,6 +185,48 @@ __device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bo
   }
 }
 
+// Fused SGD epilogue for one 32-row × 32-column accumulator chunk held by a
+// warp (lane = row): the accumulator is the fp32 gradient g of parameter
+// elements P[row, col] (never stored).  All global traffic is TMA: the
+// chunk's P and V arrive in smem in the SW128 layout (row r's 16-B piece c at
+// c ^ (r & 7): a lane reading its own row is bank-conflict-optimal), are
+// updated in place with sgd_elem (the multi-tensor SGD kernel's arithmetic →
+// bitwise the same parameters), the bf16 shadow row is written in the SW64
+// layout, and lane 0 issues three bulk tensor stores (edges clipped by TMA).
+// The caller waited for the loads (mbarrier) before calling.
+__device__ __forceinline__ void epi_sgd32(const GemmParams& p, uint8_t* buf, int lane, int row0, int col0,
+                                          const uint32_t (&r)[32]) {
+  uint8_t* sp = buf;
+  uint8_t* sv = buf + 4096;
+  uint8_t* ss = buf + 8192;
+  const bool mom = p.upd_v != nullptr;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int off = lane * 128 + ((c ^ (lane & 7)) << 4);
+    const float4 p4 = *reinterpret_cast<const float4*>(sp + off);
+    const float4 v4 = mom ? *reinterpret_cast<const float4*>(sv + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float pv[4] = {p4.x, p4.y, p4.z, p4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sgd_elem(pv[j], __uint_as_float(r[4 * c + j]), vv[j], mom, p.lr, p.mu, p.wd, p.gscale);
+    *reinterpret_cast<float4*>(sp + off) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    if (mom) *reinterpret_cast<float4*>(sv + off) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    if (p.upd_shadow) {
+      // 8 bf16 per 16-B SW64 piece: fp32 pieces 2h, 2h+1 → bf16 piece h
+      const int h = c >> 1;
+      uint2* dst = reinterpret_cast<uint2*>(ss + lane * 64 + ((h ^ ((lane >> 1) & 3)) << 4) + (c & 1) * 8);
+      *dst = make_uint2(pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]));
+    }
+  }
+  sm100::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    sm100::tma_store_2d(&p.tp[0], sp, col0, row0);
+    if (mom) sm100::tma_store_2d(&p.tp[1], sv, col0, row0);
+    if (p.upd_shadow) sm100::tma_store_2d(&p.td, ss, col0, row0);
+    sm100::bulk_commit();
+  }
+}
+
 // TMA-store epilogue for one 32-row × 32-column chunk held by a warp (lane =
 // row): bias / ReLU / convert, write the lane's row into the warp's staging
 // buffer in the store map's swizzle (bf16: 64-B rows, SW64 — chunk c at
@@ -231,24 +290,106 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
   slot ^= 1;
 }
 
-template <int BN, bool X3>
-__global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg<BN, X3>;
+// Fused-SGD epilogue of a persistent GEMM (warp = TMEM lane quarter eq):
+// 32 rows × TILE_N columns per tile, as a flat sequence of 32-column chunks
+// over this CTA's tiles (t0, t0 + tstride, …).  Chunk i's P,V are TMA-loaded
+// two chunks ahead into buffer i % 3 (no dependence on the accumulator), then
+// updated in place and TMA-stored with the shadow (epi_sgd32).  CLUSTER: the
+// accumulator-empty arrival goes to the pair leader's barrier.
+template <int TILE_N, bool CLUSTER>
+__device__ __forceinline__ void upd_epilogue(const GemmParams& p, uint8_t* epi_smem, uint64_t* ubar, uint64_t* tfull,
+                                             uint64_t* tempty, uint32_t tempty_leader, uint32_t tmem_base, int eq,
+                                             int lane, int t0, int tstride, int num_tiles, int mn_tiles, int tile_m,
+                                             int row_off) {
+  uint8_t* bufs = epi_smem + eq * kUpdWarpBytes;
+  uint64_t* mb = ubar + eq * kUpdBufs;
+  const uint32_t tx = p.upd_v ? 8192u : 4096u;
+  const int cpt = (min(p.N, TILE_N) + 31) / 32;  // chunks per tile (tail chunks past N skipped)
+  auto chunk_at = [&](int i, int* row0, int* col0) -> bool {
+    const int t = t0 + (i / cpt) * tstride;
+    if (t >= num_tiles) return false;
+    const int tm = (t % mn_tiles) % p.tiles_m, tn = (t % mn_tiles) / p.tiles_m;
+    *row0 = tm * tile_m + row_off + eq * 32;
+    *col0 = tn * TILE_N + (i % cpt) * 32;
+    return true;
+  };
+  auto issue = [&](int i) {
+    int r0, c0;
+    if (!chunk_at(i, &r0, &c0) || c0 >= p.N) return;
+    if (lane == 0) {
+      uint8_t* b = bufs + (i % kUpdBufs) * kUpdBufBytes;
+      uint64_t* bar = &mb[i % kUpdBufs];
+      sm100::mbar_arrive_expect_tx(bar, tx);
+      sm100::tma_load_2d(&p.tp[0], bar, b, c0, r0);
+      if (p.upd_v) sm100::tma_load_2d(&p.tp[1], bar, b + 4096, c0, r0);
+    }
+  };
+  uint32_t uph = 0u;  // bit k: phase of buffer k
+  issue(0);
+  issue(1);
+  int acc = 0; uint32_t acc_phase = 0;
+  int i = 0;
+  for (int t = t0; t < num_tiles; t += tstride) {
+    sm100::mbar_wait(&tfull[acc], acc_phase);
+    sm100::tc_fence_after();
+    for (int j = 0; j < cpt; ++j, ++i) {
+      int row0, col0;
+      chunk_at(i, &row0, &col0);
+      const bool live = col0 < p.N;
+      if (live) {
+        uint32_t ru[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TILE_N + j * 32 + ((uint32_t)(eq * 32) << 16), ru);
+        sm100::tmem_ld_wait();
+        const int k = i % kUpdBufs;
+        sm100::mbar_wait(&mb[k], (uph >> k) & 1u);
+        uph ^= 1u << k;
+        epi_sgd32(p, bufs + k * kUpdBufBytes, lane, row0, col0, ru);
+      }
+      // buffer (i+2) % 3 was last used by chunk i−1, whose stores went out
+      // one commit group ago: wait until they have read it, then refill
+      if (lane == 0) {
+        if (live) sm100::bulk_wait_read<1>();
+        else sm100::bulk_wait_read<0>();
+      }
+      __syncwarp();
+      issue(i + 2);
+    }
+    sm100::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (CLUSTER) sm100::mbar_arrive_cluster(tempty_leader + acc * 8);
+      else sm100::mbar_arrive(&tempty[acc]);
+    }
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+  if (lane == 0) sm100::bulk_wait<0>();  // stores complete before exit
+}
+
+template <int BN, bool X3, bool UPD = false>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN, X3, UPD>;
+  static_assert(C::STAGES >= 2, "pipeline needs at least two stages");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ubar = tempty + 2;  // UPD: one barrier per P/V buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ubar + (UPD ? kUpdWarps * kUpdBufs : 0));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&tfull[a], 1);
+      sm100::mbar_init(&tempty[a], UPD ? kUpdWarps : kEpiWarps);
+    }
+    if (UPD)
+      for (int i = 0; i < kUpdWarps * kUpdBufs; ++i) sm100::mbar_init(&ubar[i], 1);
     sm100::fence_barrier_init();
     sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
     if (X3) { sm100::tma_prefetch(&p.ta[1]); sm100::tma_prefetch(&p.tb[1]); }
@@ -357,7 +498,10 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ GemmPara
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (UPD && warp >= 4 && warp < 4 + kUpdWarps) {
+    upd_epilogue<BN, false>(p, epi_smem, ubar, tfull, tempty, 0u, tmem_base, warp & 3, lane, blockIdx.x, gridDim.x,
+                            num_tiles, mn_tiles, BM, 0);
+  } else if (!UPD && warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;               // 0..7
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
@@ -379,8 +523,8 @@ __global__ void __maxnreg__(128) gemm_tc_kernel(const __grid_constant__ GemmPara
         const int col0 = tn * BN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
         if (!h0) break;
-        uint32_t r0[32], r1[32];
         const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        uint32_t r0[32], r1[32];
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
@@ -421,19 +565,26 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB per CTA
 constexpr int STAGES = 6;
 constexpr int TMEM_COLS = 512;            // 2 accumulators × 256 columns
 constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
+// fused-SGD variant: fewer stages, the 4-warp triple-buffered update epilogue
+constexpr int STAGES_UPD = 3;
+constexpr int SMEM_UPD = STAGES_UPD * STAGE_BYTES + kUpdWarps * kUpdWarpBytes + 1024 + 256;
 }  // namespace pair
 
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
+template <bool UPD = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ GemmParams p) {
   using namespace pair;
+  constexpr int NST = UPD ? STAGES_UPD : STAGES;
+  constexpr int EPI = UPD ? kUpdWarps * kUpdWarpBytes : kEpiBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* epi_smem = smem + NST * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + EPI);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ubar = tempty + 2;  // UPD: one barrier per P/V buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ubar + (UPD ? kUpdWarps * kUpdBufs : 0));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
@@ -441,8 +592,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
   const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 2 * kEpiWarps); }
+    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&tfull[a], 1);
+      sm100::mbar_init(&tempty[a], 2 * (UPD ? kUpdWarps : kEpiWarps));
+    }
+    if (UPD)
+      for (int i = 0; i < kUpdWarps * kUpdBufs; ++i) sm100::mbar_init(&ubar[i], 1);
     sm100::fence_barrier_init();
     sm100::tma_prefetch(&p.ta[0]); sm100::tma_prefetch(&p.tb[0]);
   }
@@ -483,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
 #pragma unroll
             for (int j = 0; j < HN / 64; ++j) sm100::tma_load_2d_2sm(&p.tb[0], &full[stage], sb + j * BK * 128, n0 + j * 64, k0);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -514,13 +670,16 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
             sm100::mma_bf16_2sm(d_tmem, ad, bd, idesc, ((kb - kb0) | kk) ? 1u : 0u);
           }
           sm100::mma_commit_2sm(&empty[stage], 0x3);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         sm100::mma_commit_2sm(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (UPD && warp >= 4 && warp < 4 + kUpdWarps) {
+    upd_epilogue<TN, true>(p, epi_smem, ubar, tfull, tempty, sm100::mapa(sm100::smem_u32(&tempty[0]), 0), tmem_base,
+                           warp & 3, lane, pair_id, npairs, num_tiles, mn_tiles, TM, (int)rank * HM);
+  } else if (!UPD && warp >= 4) {
     // ===================== epilogue (both CTAs, own TMEM half) =====================
     const int ew = warp - 4;               // 0..7
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
@@ -543,8 +702,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
         const int col0 = tn * TN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (TN / 2);
         if (!h0) break;
-        uint32_t r0[32], r1[32];
         const uint32_t ta = tmem_base + acc * TN + c0 + ((uint32_t)(eq * 32) << 16);
+        uint32_t r0[32], r1[32];
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
@@ -594,7 +753,7 @@ struct Cfg {
 }  // namespace conv
 
 template <int BN>
-__global__ void __maxnreg__(128) conv_tc_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid_constant__ GemmParams p) {
   using C = conv::Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1186,6 +1345,38 @@ bool tma_ok(const void* p, int64_t ld, be_dtype dt) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * (int64_t)dtype_size(dt)) % 16 == 0;
 }
 
+// fused SGD epilogue parameters (GemmDesc::upd): P is [M, N] with ld = ldd
+}  // namespace
+bool gemm_update_ok(const GemmDesc& g) {
+  if (!g.upd || g.ab != BE_BF16) return false;
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(g.upd->p), va = reinterpret_cast<uintptr_t>(g.upd->v),
+                  sa = reinterpret_cast<uintptr_t>(g.upd->shadow);
+  return g.ldd % 8 == 0 && ((pa | va | sa) & 15) == 0;  // TMA: 16-B aligned bases and row pitches
+}
+namespace {
+void set_update(GemmParams& p, const GemmDesc& g) {
+  BE_REQUIRE(gemm_update_ok(g), BE_E_ARG, "gemm: update epilogue needs 16-B aligned P/V rows, 8-B aligned shadow");
+  // P / V chunks are TMA-loaded as 32 × 32 fp32 boxes (zero fill past the edges)
+  encode_2d_sw(&p.tp[0], g.upd->p, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
+               CU_TENSOR_MAP_SWIZZLE_128B);
+  if (g.upd->v)
+    encode_2d_sw(&p.tp[1], g.upd->v, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_128B);
+  if (g.upd->shadow)
+    encode_2d_sw(&p.td, g.upd->shadow, BE_BF16, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_64B);
+  p.upd = 1;
+  p.upd_p = g.upd->p; p.upd_v = g.upd->v; p.upd_shadow = g.upd->shadow;
+  p.lr = g.upd->lr; p.mu = g.upd->mu; p.wd = g.upd->wd; p.gscale = g.upd->scale;
+  p.ldd = g.ldd;
+  p.tma_store = 0;
+  p.D = nullptr;
+}
+// per parameter element: p read+write, v read+write (momentum), shadow write
+double update_bytes(const GemmDesc& g) {
+  return 8.0 + (g.upd->v ? 8.0 : 0.0) + (g.upd->shadow ? 2.0 : 0.0);
+}
+
 template <int BN, bool X3>
 void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo,
                cudaStream_t s, int force_splits = 0) {
@@ -1226,7 +1417,8 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   // wgrad: M·N tiny, K = N·P·Q up to 3.2 M); fp32 partials are summed in a
   // fixed order by splitk_reduce → deterministic.
   int splits = 1;
-  if (force_splits > 0) splits = std::max(1, std::min(force_splits, kblocks));
+  if (g.upd) splits = 1;  // the update epilogue needs the complete gradient
+  else if (force_splits > 0) splits = std::max(1, std::min(force_splits, kblocks));
   else if (mn * 2 <= sms && kblocks >= 8) splits = std::max(1, std::min(sms / mn, kblocks / 4));
   int kps = (kblocks + splits - 1) / splits;
   splits = (kblocks + kps - 1) / kps;
@@ -1244,12 +1436,30 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
     p.split_stride = 0;
     p.split_rows = 0;
   }
-  setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
+  if (g.upd) set_update(p, g);
+  else setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = std::min(mn * splits, sms);
   const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
-  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
-  const int pidx = prof_begin(X3 ? "gemm_tc_3xtf32" : "gemm_tc_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
-  gemm_tc_kernel<BN, X3><<<grid, kThreads, C::SMEM, s>>>(p);
+  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es +
+                           (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
+  const int pidx = prof_begin(g.upd ? "gemm_upd" : (X3 ? "gemm_tc_3xtf32" : "gemm_tc_bf16"), 2.0 * g.M * g.N * g.K,
+                              alg_bytes, g.M, g.N, g.K, s);
+  if (g.upd) {
+    if constexpr (!X3) {
+      using CU = Cfg<BN, false, true>;
+      static bool upd_attr = false;
+      if (!upd_attr) {
+        BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           CU::SMEM));
+        upd_attr = true;
+      }
+      gemm_tc_kernel<BN, false, true><<<grid, kThreads, CU::SMEM, s>>>(p);
+    } else {
+      fail(BE_E_ARG, "gemm: the update epilogue runs on the bf16 kernel");
+    }
+  } else {
+    gemm_tc_kernel<BN, X3><<<grid, kThreads, C::SMEM, s>>>(p);
+  }
   prof_end(pidx, s);
   after_launch("gemm_tc");
   if (ws) {
@@ -1266,7 +1476,8 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   using namespace pair;
   static bool attr_set = false;
   if (!attr_set) {
-    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_UPD));
     attr_set = true;
   }
   GemmParams p;
@@ -1281,7 +1492,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   const int mn = p.tiles_m * p.tiles_n;
   const int kblocks = (g.K + BK - 1) / BK;
   int splits = 1;
-  if (mn * 2 <= pairs && kblocks >= 8) splits = std::max(1, std::min(pairs / mn, kblocks / 4));
+  if (!g.upd && mn * 2 <= pairs && kblocks >= 8) splits = std::max(1, std::min(pairs / mn, kblocks / 4));
   int kps = (kblocks + splits - 1) / splits;
   splits = (kblocks + kps - 1) / kps;
   p.splits = splits;
@@ -1295,12 +1506,15 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   } else {
     p.D = g.D; p.ldd = g.ldd; p.d_f32 = g.d == BE_F32; p.beta = g.beta; p.bias = g.bias; p.act = g.act;
   }
-  setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
+  if (g.upd) set_update(p, g);
+  else setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = 2 * std::min(mn * splits, pairs);
   const double ds = g.d == BE_F32 ? 4.0 : 2.0;
-  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 + (double)g.M * g.N * ds * (g.beta != 0.f ? 2 : 1);
-  const int pidx = prof_begin("gemm_tc2_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
-  gemm_tc2_kernel<<<grid, kThreads, SMEM, s>>>(p);
+  const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 +
+                           (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
+  const int pidx = prof_begin(g.upd ? "gemm_upd2" : "gemm_tc2_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
+  if (g.upd) gemm_tc2_kernel<true><<<grid, kThreads, SMEM_UPD, s>>>(p);
+  else gemm_tc2_kernel<false><<<grid, kThreads, SMEM, s>>>(p);
   prof_end(pidx, s);
   after_launch("gemm_tc2");
   if (ws) {
@@ -1491,6 +1705,11 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
 uint64_t gemm_tcgen05_calls() { return g_tc_calls.load(); }
 uint64_t gemm_simt_calls() { return g_simt_calls.load(); }
 
+bool gemm_tc_ok(const GemmDesc& g) {
+  return g.K > 0 && g.M > 0 && g.N > 0 && (g.ab == BE_BF16 || g.ab == BE_F32) && tma_ok(g.A, g.lda, g.ab) &&
+         tma_ok(g.B, g.ldb, g.ab) && g.conv_x == nullptr;
+}
+
 const char* gemm(const GemmDesc& g, cudaStream_t s) {
   BE_REQUIRE(g.ab == BE_BF16 || g.ab == BE_F32, BE_E_DTYPE, "gemm: operands must be bf16 or f32");
   BE_REQUIRE(g.d == BE_BF16 || g.d == BE_F32, BE_E_DTYPE, "gemm: output must be bf16 or f32");
@@ -1499,6 +1718,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
   }
   const bool x3 = g.ab == BE_F32;
   const bool tc = g.K > 0 && tma_ok(g.A, g.lda, g.ab) && tma_ok(g.B, g.ldb, g.ab);
+  BE_REQUIRE(!g.upd || (tc && !g.conv_x), BE_E_ARG, "gemm: the SGD update epilogue needs the tcgen05 path");
   if (tc) {
     g_tc_calls++;
     const void *ahi = g.A, *alo = nullptr, *bhi = g.B, *blo = nullptr;
@@ -1529,6 +1749,16 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       if (bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
       else if (bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
       else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
+    } else if (g.upd) {
+      // fused SGD epilogue: 1-CTA kernel BN 256 / 128 / 64 or the CTA pair (autotuned)
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      const int v = tune_choose("gemm:" + tune_key(g) + "u", 4, 0, &ev0, &ev1);
+      if (ev0) cudaEventRecord(ev0, s);
+      if (v == 3 && pair_plausible(g)) launch_tc2(g, s);
+      else if (v == 0 || v == 3) launch_tc<256, false>(g, ahi, alo, bhi, blo, s);
+      else if (v == 1) launch_tc<128, false>(g, ahi, alo, bhi, blo, s);
+      else launch_tc<64, false>(g, ahi, alo, bhi, blo, s);
+      if (ev1) cudaEventRecord(ev1, s);
     } else {
       // candidate list (autotuned per shape): the 1-CTA kernel
       // with pick_bn's tile and its default split rule; the CTA pair; and,

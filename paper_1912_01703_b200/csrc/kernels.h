@@ -30,9 +30,21 @@ struct GemmDesc {
   // place by TMA im2col (bf16, C % 64 == 0); B / ldb are then ignored
   const void* conv_x = nullptr;
   ConvGeom conv_g{};
+  // fused SGD epilogue: when set, D is not written; the accumulator is the
+  // gradient g of the parameter P[M, N] (row-major, ld = ldd) and the epilogue
+  // applies the SGD update to P, its momentum V and its bf16 shadow directly
+  const struct SgdFuse* upd = nullptr;
+};
+struct SgdFuse {
+  float* p = nullptr; float* v = nullptr; uint16_t* shadow = nullptr;
+  float lr = 0.f, mu = 0.f, wd = 0.f, scale = 1.f;
 };
 // Returns the name of the path taken ("tcgen05" or "simt").
 const char* gemm(const GemmDesc& g, cudaStream_t s);
+// true when g runs on the tcgen05 path (the only one with the update epilogue)
+bool gemm_tc_ok(const GemmDesc& g);
+// true when g.upd can run (bf16, 16-B aligned P/V rows, 8-B aligned shadow)
+bool gemm_update_ok(const GemmDesc& g);
 // Encode counters for tests/bench (which path ran).
 uint64_t gemm_tcgen05_calls();
 uint64_t gemm_simt_calls();

@@ -130,15 +130,27 @@ static void vjp_linear(Node* n, GradSink& sink) {
     k::relu_bwd(gz->data(), y->data(), dz->data(), B * OUT, opd, 0.f, s);
   }
   gz = TRef();
-  if (sink.needs(1)) {  // dW[in,out] = xᵀ·dz  (A = xᵀ MN-major, B = dzᵀ MN-major), fp32
+  // dW[in,out] = xᵀ·dz  (A = xᵀ MN-major, B = dzᵀ MN-major), fp32
+  k::GemmDesc gw;
+  gw.M = (int)IN; gw.N = (int)OUT; gw.K = (int)B;
+  gw.A = x->data(); gw.lda = IN; gw.a_kmajor = false;
+  gw.B = dz->data(); gw.ldb = OUT; gw.b_kmajor = false;
+  gw.ab = opd; gw.ldd = OUT;
+  // overlapped SGD: when this is the weight's only gradient contribution, the
+  // wgrad GEMM applies the update in its epilogue (no dW tensor, no separate
+  // SGD pass) — after dX, which still reads the pre-update weight
+  k::SgdFuse fz;
+  bool fuse = sink.needs(1) && opd == BE_BF16 && k::gemm_tc_ok(gw) && sink.fuse && sink.fuse(1, &fz);
+  if (fuse) {
+    gw.upd = &fz;
+    fuse = k::gemm_update_ok(gw);
+    gw.upd = nullptr;
+  }
+  if (sink.needs(1) && !fuse) {
     float bw;
     Tensor* dw = sink.dest(1, &bw);
-    k::GemmDesc gd;
-    gd.M = (int)IN; gd.N = (int)OUT; gd.K = (int)B;
-    gd.A = x->data(); gd.lda = IN; gd.a_kmajor = false;
-    gd.B = dz->data(); gd.ldb = OUT; gd.b_kmajor = false;
-    gd.ab = opd; gd.D = dw->data(); gd.ldd = OUT; gd.d = dw->dtype; gd.beta = bw;
-    k::gemm(gd, s);
+    gw.D = dw->data(); gw.d = dw->dtype; gw.beta = bw;
+    k::gemm(gw, s);
     sink.commit(1);
   }
   if (sink.needs(0)) {  // dX[B,in] = dz·Wᵀ  (A = dz K-major, B = W K-major)
@@ -155,6 +167,11 @@ static void vjp_linear(Node* n, GradSink& sink) {
     k::gemm(gd, s);
     if (dxc) k::axpby(dxc->data(), opd, dx->data(), dx->dtype, dx->numel(), 1.f, bx, s);
     sink.commit(0);
+  }
+  if (fuse) {
+    gw.upd = &fz;
+    k::gemm(gw, s);
+    sink.fused(1);
   }
 }
 

@@ -105,6 +105,32 @@ void opt_on_grad_final(Tensor* leaf) {
   if (o.group_numel >= kGroupNumel) flush_group();
 }
 
+bool opt_fuse_desc(Tensor* p, k::SgdFuse* f) {
+  static const bool on = [] { const char* e = getenv("BE_FUSE_SGD"); return !(e && e[0] == '0'); }();
+  Overlap& o = ov();
+  if (!on || !o.active || p->opt_slot < 0 || p->grad) return false;
+  cudaStream_t s = ctx().stream;
+  *f = k::SgdFuse{};
+  f->p = p->ptr<float>();
+  if (o.momentum != 0.f) {
+    if (!p->mom_block) {
+      p->mom_block = ctx().alloc.allocate(sizeof(float) * std::max<int64_t>(1, p->numel()), s);
+      p->mom = reinterpret_cast<float*>(p->mom_block->ptr);
+      k::fill(p->mom, p->numel(), BE_F32, 0.0, s);  // v0 = 0 ⇒ v1 = g'
+    }
+    f->v = p->mom;
+  }
+  if (p->shadow && p->shadow_version == p->version()) f->shadow = p->shadow->ptr<uint16_t>();
+  f->lr = o.lr; f->mu = o.momentum; f->wd = o.wd; f->scale = 1.f;
+  return true;
+}
+
+void opt_fused_done(Tensor* p) {
+  const bool sh = p->shadow && p->shadow_version == p->version();
+  p->bump_version();
+  if (sh) { p->shadow->bump_version(); p->shadow_version = p->version(); }
+}
+
 void opt_launch_params(const std::vector<Tensor*>& ps, cudaStream_t s, float scale) {
   std::vector<Tensor*> mine;
   for (Tensor* p : ps)
@@ -142,9 +168,9 @@ be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum, 
   for (int i = 0; i < n; ++i) {
     Tensor* p = check_handle(params[i]);
     BE_REQUIRE(p->dtype == BE_F32 && p->is_contiguous(), BE_E_DTYPE, "sgd: params must be contiguous f32");
-    BE_REQUIRE(p->grad != nullptr, BE_E_MISSING_GRAD, "sgd: parameter " + std::to_string(i) + " has no grad");
     BE_REQUIRE(!opt_param(p), BE_E_ARG, "sgd: parameter " + std::to_string(i) +
                                            " is registered for overlapped SGD (updated during backward)");
+    BE_REQUIRE(p->grad != nullptr, BE_E_MISSING_GRAD, "sgd: parameter " + std::to_string(i) + " has no grad");
     es.push_back(sgd_entry(p, momentum, ctx().stream));
     ts.push_back(p);
   }

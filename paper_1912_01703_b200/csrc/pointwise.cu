@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sgd_math.cuh"
 #include "kernels.h"
 #include "runtime.h"
 
@@ -476,11 +477,7 @@ __global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdTab
         float pv[4] = {p4[k].x, p4[k].y, p4[k].z, p4[k].w}, gv[4] = {g4[k].x, g4[k].y, g4[k].z, g4[k].w};
         float mv[4] = {m4[k].x, m4[k].y, m4[k].z, m4[k].w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float gg = gv[j] * scale + wd * pv[j];
-          if (e.mom) { mv[j] = mu * mv[j] + gg; gg = mv[j]; }
-          pv[j] = pv[j] - lr * gg;
-        }
+        for (int j = 0; j < 4; ++j) sgd_elem(pv[j], gv[j], mv[j], e.mom != nullptr, lr, mu, wd, scale);
         *reinterpret_cast<float4*>(e.p + i) = make_float4(pv[0], pv[1], pv[2], pv[3]);
         if (e.mom) *reinterpret_cast<float4*>(e.mom + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
         if (e.shadow) {
@@ -492,10 +489,9 @@ __global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdTab
       }
     } else {
       for (int64_t i = base + threadIdx.x; i < end; i += 256) {
-        float pv = e.p[i];
-        float gg = e.g[i] * scale + wd * pv;
-        if (e.mom) { float m = mu * e.mom[i] + gg; e.mom[i] = m; gg = m; }
-        pv = pv - lr * gg;
+        float pv = e.p[i], mv = e.mom ? e.mom[i] : 0.f;
+        sgd_elem(pv, e.g[i], mv, e.mom != nullptr, lr, mu, wd, scale);
+        if (e.mom) e.mom[i] = mv;
         e.p[i] = pv;
         if (e.shadow) e.shadow[i] = f2bf(pv);
       }

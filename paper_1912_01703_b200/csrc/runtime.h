@@ -178,6 +178,7 @@ struct Edge {
 };
 
 struct GradSink;
+namespace k { struct SgdFuse; }
 using VjpFn = void (*)(Node* n, GradSink& sink);
 
 struct OutMeta {
@@ -218,6 +219,14 @@ struct GradSink {
   bool upstream_ones() const { return node->upstream_is_ones; }
   bool retain = false;
   std::function<bool(int, Tensor*)> adopt;      // engine callback: try to adopt t as input i's grad
+  // Fused SGD (overlapped optimizer): true when input i is a parameter
+  // registered with be_sgd_overlap whose gradient is complete with this one
+  // contribution; *f then describes the update the VJP's weight-gradient GEMM
+  // applies in its epilogue (no gradient tensor is stored), after which the
+  // VJP calls fused(i).  Every reader of the parameter in this VJP must be
+  // enqueued before that GEMM.
+  std::function<bool(int, k::SgdFuse*)> fuse;
+  std::function<void(int)> fused;
   // engine internals
   struct Slot { Tensor* target = nullptr; Tensor* tmp = nullptr; bool acc = false; bool used = false; };
   std::vector<Slot> slots;
@@ -275,5 +284,7 @@ bool opt_active();
 bool opt_param(const Tensor* leaf);      // registered for overlapped SGD
 void opt_on_grad_final(Tensor* leaf);    // (non-DDP) grad complete for this backward
 void opt_end_backward();                 // flush; compute stream waits for every update
+bool opt_fuse_desc(Tensor* leaf, k::SgdFuse* f);  // fill the update-epilogue descriptor (BE_FUSE_SGD=0: off)
+void opt_fused_done(Tensor* leaf);       // versions after the fused update was enqueued
 
 }  // namespace be

@@ -298,6 +298,11 @@ def test_overlapped_sgd_bitwise_equals_fused(net):
     assert lf.item() == lo.item()
     for k in P:
         assert np.array_equal(over.params[k].numpy(), fused.params[k].numpy()), k
+    if net == "mlp":
+        # the 2-D weights' updates ran inside their wgrad GEMM's epilogue
+        # (fused SGD): no gradient tensor was ever materialised for them
+        assert over.params["fc0.w"].grad is None and over.params["fc1.w"].grad is None
+        assert over.params["fc0.b"].grad is not None
     # a registered parameter cannot also be stepped by be_sgd_step
     with pytest.raises(be.BeError) as ei:
         be.sgd_step(over.parameters(), 0.1)
