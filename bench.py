@@ -317,7 +317,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     value = B * world * args.steps / (ms / 1e3)
     # roofline of the dominant kernel class (tcgen05 GEMM)
     pk, pk_kind = peaks()
-    tc = [r for r in prof if r["name"].startswith("gemm_tc") or r["name"].startswith("conv_tc")]
+    tc = [r for r in prof if r["name"].startswith(("gemm_tc", "conv_tc"))]
+    upd = [r for r in prof if r["name"].startswith("gemm_upd")]
     gemm_ms = sum(r["ms"] for r in tc)
     flops = sum(r["flops"] for r in tc)
     achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
@@ -340,6 +341,23 @@ def run_ours(args, cfg, rank, world, local_rank):
         s[1] += r["ms"]
     roof["per_shape"] = {k: {"launches": v[0], "avg_us": round(v[1] / v[0] * 1e3, 2),
                              "tflops": round(v[2] / (v[1] / v[0] / 1e3) / 1e12, 1)} for k, v in shapes.items()}
+    # SURVEY §8(d)'s per-kernel roofline: each launch's ideal time is
+    # max(flops / tensor peak, algorithmic bytes / HBM peak); the class figure
+    # is Σ ideal / Σ measured (memory-bound shapes — K = 64 1×1 convs, the
+    # fused-SGD wgrads — are held to the HBM roof instead of the tensor roof)
+    hbm = pk.get("hbm_gbs", 6650.0) * 1e9
+    ideal = sum(max(r["flops"] / (peak * 1e12), r["bytes"] / hbm) for r in tc)
+    roof["frac_per_kernel_roofline"] = round(ideal / (gemm_ms / 1e3), 4) if gemm_ms else None
+    roof["hbm_peak_gbs"] = pk.get("hbm_gbs")
+    if upd:
+        # wgrad GEMMs carrying the SGD update in their epilogue (be_sgd_overlap):
+        # bound by the P/V/shadow traffic (18 B/param) + operand stream
+        ums = sum(r["ms"] for r in upd)
+        ub = sum(r["bytes"] for r in upd)
+        roof["fused_sgd_gemm"] = {"launches_per_step": len(upd) / args.steps, "ms_per_step": round(ums / args.steps, 4),
+                                  "achieved_gbs": round(ub / (ums / 1e3) / 1e9, 1), "peak_gbs": pk.get("hbm_gbs"),
+                                  "frac": round(ub / (ums / 1e3) / hbm, 4),
+                                  "tflops": round(sum(r["flops"] for r in upd) / (ums / 1e3) / 1e12, 1)}
     trafficf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(trafficf):
         roof["traffic"] = json.load(open(trafficf)).get("dram_bytes_per_launch")

@@ -135,7 +135,7 @@ typedef enum {
   BE_OP_CONV2D = 8,        /* in: x NHWC[N,H,W,C], w KRSC[K,R,S,C], b[K] optional; attrs be_conv_attrs; out NHWC[N,P,Q,K] */
   BE_OP_MAXPOOL2D = 9,     /* in: x NHWC; attrs be_pool_attrs; out: y NHWC, optional out[1]: argmax u8 window index (r*k+u) */
   BE_OP_AVGPOOL_GLOBAL = 10, /* in: x NHWC[N,H,W,C]; out [N,C] */
-  BE_OP_BATCHNORM2D = 11,  /* in: x NHWC, gamma[C], beta[C], running_mean[C]?, running_var[C]?; attrs be_bn_attrs */
+  BE_OP_BATCHNORM2D = 11,  /* in: x NHWC, gamma[C], beta[C], running_mean[C]?, running_var[C]?, residual?; attrs be_bn_attrs */
   BE_OP_RESHAPE = 12,      /* in: x contiguous; attrs be_shape_attrs; out: view (shares storage) */
   BE_OP_EMBEDDING = 13,    /* in: table[V,D] (f32 param), ids i32[B]; out [B,D] */
   BE_OP_CONCAT = 14,       /* in: n 2-D tensors [B,Di]; concatenated along axis 1 */
@@ -148,7 +148,12 @@ typedef enum {
 typedef struct { int act; /* 0 none, 1 relu */ int out_f32; /* 1: fp32 output even in bf16 mode */ } be_linear_attrs;
 typedef struct { int stride, pad, act; int out_f32; } be_conv_attrs;
 typedef struct { int k, stride, pad; } be_pool_attrs;
-typedef struct { float eps, momentum; int act; /* fused ReLU after affine */ } be_bn_attrs;
+typedef struct {
+  float eps, momentum;
+  int act;       /* fused ReLU after the affine (and after the residual add) */
+  int residual;  /* 1: the LAST input is a residual r (x's shape/dtype): y = act(bn(x) + r) — the ResNet block
+                    output in one pass; r receives the gradient act'(y)·dy */
+} be_bn_attrs;
 typedef struct { int rank; int64_t shape[6]; } be_shape_attrs;
 
 be_status be_op(int op_id, const be_tensor* in, int n_in, const void* attrs,

@@ -57,7 +57,7 @@ class be_pool_attrs(C.Structure):
 
 
 class be_bn_attrs(C.Structure):
-    _fields_ = [("eps", C.c_float), ("momentum", C.c_float), ("act", C.c_int)]
+    _fields_ = [("eps", C.c_float), ("momentum", C.c_float), ("act", C.c_int), ("residual", C.c_int)]
 
 
 class be_shape_attrs(C.Structure):

@@ -266,11 +266,15 @@ def avgpool_global(x):
     return _op("AVGPOOL_GLOBAL", [x])
 
 
-def batchnorm2d(x, gamma, beta, running_mean=None, running_var=None, eps=1e-5, momentum=0.1, act=0):
+def batchnorm2d(x, gamma, beta, running_mean=None, running_var=None, eps=1e-5, momentum=0.1, act=0, residual=None):
+    """Train-mode batch norm; `residual` fuses the ResNet block output
+    act(bn(x) + residual) into the same pass."""
     ins = [x, gamma, beta]
     if running_mean is not None:
         ins += [running_mean, running_var]
-    return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act)))
+    if residual is not None:
+        ins += [residual]
+    return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act), int(residual is not None)))
 
 
 def reshape(x, shape):

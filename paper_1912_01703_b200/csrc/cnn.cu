@@ -358,10 +358,12 @@ __global__ void bn_grad_finalize(const float* p0, const float* p1, int splits, i
   if (dgamma) dgamma[c] = s1 + (gb_beta != 0.f ? dgamma[c] : 0.f);
 }
 __global__ void bn_apply_kernel(const void* x, void* y, int64_t total, int C, be_dtype dt, const float* mean,
-                                const float* invstd, const float* gamma, const float* beta, int act) {
+                                const float* invstd, const float* gamma, const float* beta, int act,
+                                const void* res) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     float v = gamma[c] * (ld(x, i, dt) - mean[c]) * invstd[c] + beta[c];
+    if (res) v += ld(res, i, dt);
     if (act) v = fmaxf(v, 0.f);
     st(y, i, dt, v);
   }
@@ -484,7 +486,8 @@ __global__ void bn_stats_finalize_v(const float* p0, const float* p1, int splits
 __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, void* __restrict__ y, int64_t rows,
                                                   int C, be_dtype dt, const float* __restrict__ mean,
                                                   const float* __restrict__ invstd, const float* __restrict__ gamma,
-                                                  const float* __restrict__ beta, int act, int64_t rows_per_block) {
+                                                  const float* __restrict__ beta, int act, int64_t rows_per_block,
+                                                  const void* __restrict__ res) {
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -498,10 +501,11 @@ __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, vo
     sh[j] = beta[c + j] - mean[c + j] * sc[j];
   }
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  auto row = [&](int64_t o, V8 a) {
+  auto row = [&](int64_t o, V8 a, const V8& rr) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float val = fmaf(a.v[j], sc[j], sh[j]);
+      float val = fmaf(a.v[j], sc[j], sh[j]);
+      if (res) val += rr.v[j];  // fused residual add (ResNet block output)
       a.v[j] = act ? fmaxf(val, 0.f) : val;
     }
     st8(y, o, dt, a);
@@ -509,9 +513,10 @@ __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, vo
   for (int64_t r = r0 + rl; r < r1; r += 2 * rpi) {
     const bool two = r + rpi < r1;
     const int64_t o0 = r * C + c, o1 = two ? o0 + (int64_t)rpi * C : o0;
-    V8 a0 = ld8(x, o0, dt), a1 = ld8(x, o1, dt);
-    row(o0, a0);
-    if (two) row(o1, a1);
+    V8 a0 = ld8(x, o0, dt), a1 = ld8(x, o1, dt), r0v, r1v;
+    if (res) { r0v = ld8(res, o0, dt); r1v = ld8(res, o1, dt); }
+    row(o0, a0, r0v);
+    if (two) row(o1, a1, r1v);
   }
 }
 __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, const void* __restrict__ x,
@@ -786,17 +791,17 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
   after_launch("bn_var");
 }
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
-              const float* gamma, const float* beta, int act, cudaStream_t s) {
+              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res) {
   const int64_t total = rows * C;
   if (total == 0) return;
-  if (bn_vec_ok(x, C) && aligned16(y)) {
+  if (bn_vec_ok(x, C) && aligned16(y) && (!res || aligned16(res))) {
     dim3 grid;
     const int64_t rpb = bn_rows_per_block(rows, C, &grid);
-    bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb);
+    bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb, res);
     after_launch("bn_apply_v");
     return;
   }
-  bn_apply_kernel<<<grid_for(total), 256, 0, s>>>(x, y, total, C, dt, mean, invstd, gamma, beta, act);
+  bn_apply_kernel<<<grid_for(total), 256, 0, s>>>(x, y, total, C, dt, mean, invstd, gamma, beta, act, res);
   after_launch("bn_apply");
 }
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,

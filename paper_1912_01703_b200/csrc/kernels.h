@@ -119,8 +119,9 @@ void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, fl
 // BN train: stats per channel over rows (x as [rows, C]); mean/invstd fp32 [C]
 void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float* mean, float* invstd,
               float* partial, float* run_mean, float* run_var, float momentum, cudaStream_t s);
+// y = act(γ·(x − μ)·is + β [+ res])   (res: optional residual, same layout/dtype as x)
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
-              const float* gamma, const float* beta, int act, cudaStream_t s);
+              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr);
 size_t bn_partial_floats(int64_t rows, int C);
 // backward: dgamma, dbeta (fp32, with beta-accumulate flags) and dx
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,

@@ -260,9 +260,16 @@ static void vjp_bn(Node* n, GradSink& sink) {
   Tensor* y = unpack(n, 4, hy);
   Tensor* bshift = unpack(n, 5, hb);  // β: the ReLU mask is recomputed from x
   const int act = (int)n->iattr[0];
+  const bool residual = n->iattr[1] != 0;
   const int C = (int)x->shape[3];
   const int64_t rows = x->numel() / C;
   TRef gz = contiguous_like(sink.upstream[0], x->dtype);
+  if (residual && act) {
+    // y = relu(bn(x) + r): g = dy·1[y > 0] is both r's gradient and the BN's upstream
+    TRef g = new_tensor(x->shape, x->rank, x->dtype);
+    k::relu_bwd(gz->data(), y->data(), g->data(), x->numel(), x->dtype, 0.f, s);
+    gz = g;
+  }
   // dgamma / dbeta accumulate flags must agree: compute into temps when they differ
   float bg = 0.f, bb = 0.f;
   Tensor* dg = sink.needs(1) ? sink.dest(1, &bg) : nullptr;
@@ -281,25 +288,36 @@ static void vjp_bn(Node* n, GradSink& sink) {
   TRef dbs = db ? TRef() : new_tensor({C}, BE_F32);
   float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
   float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
-  k::bn_bwd(gz->data(), x->data(), act ? y->data() : nullptr, act, dx ? dx->data() : nullptr, rows, C, x->dtype,
+  const int bact = residual ? 0 : act;  // with a residual the mask is already in gz
+  k::bn_bwd(gz->data(), x->data(), bact ? y->data() : nullptr, bact, dx ? dx->data() : nullptr, rows, C, x->dtype,
             mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s,
-            act ? bshift->ptr<float>() : nullptr);
+            bact ? bshift->ptr<float>() : nullptr);
   if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
   if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
   if (dx) sink.commit(0);
   if (dg) sink.commit(1);
   if (db) sink.commit(2);
+  // the residual's gradient (last edge) is g itself: handed over without a copy
+  // when nothing else has been accumulated for it yet
+  if (residual && sink.needs((int)n->edges.size() - 1)) sink.give((int)n->edges.size() - 1, std::move(gz));
 }
 static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* out) {
-  BE_REQUIRE(n_in == 3 || n_in == 5, BE_E_ARG, "batchnorm2d: x, gamma, beta[, running_mean, running_var]");
-  be_bn_attrs a{1e-5f, 0.1f, 0};
+  be_bn_attrs a{1e-5f, 0.1f, 0, 0};
   if (attrs) a = *reinterpret_cast<const be_bn_attrs*>(attrs);
+  const int nb = n_in - (a.residual ? 1 : 0);
+  BE_REQUIRE(nb == 3 || nb == 5, BE_E_ARG, "batchnorm2d: x, gamma, beta[, running_mean, running_var][, residual]");
   Tensor* x = check_handle(in[0]);
   Tensor* gamma = check_handle(in[1]);
   Tensor* beta = check_handle(in[2]);
-  Tensor* rm = n_in == 5 && in[3] ? check_handle(in[3]) : nullptr;
-  Tensor* rv = n_in == 5 && in[4] ? check_handle(in[4]) : nullptr;
+  Tensor* rm = nb == 5 && in[3] ? check_handle(in[3]) : nullptr;
+  Tensor* rv = nb == 5 && in[4] ? check_handle(in[4]) : nullptr;
+  Tensor* res = a.residual ? check_handle(in[n_in - 1]) : nullptr;
   BE_REQUIRE(x->rank == 4 && x->is_contiguous(), BE_E_SHAPE, "batchnorm2d: contiguous NHWC input");
+  if (res) {
+    BE_REQUIRE(res->rank == 4 && res->is_contiguous(), BE_E_SHAPE, "batchnorm2d: contiguous residual");
+    for (int d = 0; d < 4; ++d) BE_REQUIRE(res->shape[d] == x->shape[d], BE_E_SHAPE, "batchnorm2d: residual shape");
+    BE_REQUIRE(res->dtype == x->dtype, BE_E_DTYPE, "batchnorm2d: residual dtype must match x");
+  }
   const int C = (int)x->shape[3];
   const int64_t rows = x->numel() / std::max(C, 1);
   BE_REQUIRE(rows > 0, BE_E_EMPTY_REDUCTION, "batchnorm2d: empty batch");
@@ -314,12 +332,14 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   if (rv) rv->bump_version();
   TRef y = new_tensor(x->shape, x->rank, x->dtype);
   k::bn_apply(x->data(), y->data(), rows, C, x->dtype, mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(),
-              beta->ptr<float>(), a.act, s);
-  Node* n = new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
+              beta->ptr<float>(), a.act, s, res ? res->data() : nullptr);
+  Node* n = res ? new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta, res})
+                : new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
   if (n) {
     save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, a.act ? y.get() : nullptr);
     save(n, beta);
     n->iattr[0] = a.act;
+    n->iattr[1] = res != nullptr;
     set_output(n, y.get(), 0);
     finish_node(n);
   }

@@ -252,17 +252,18 @@ class ResNet50(Model):
     def loss(self, x, y):
         P, B = self.params, self.buffers
 
-        def bn(h, name, act):
-            return T.batchnorm2d(h, P[name + ".g"], P[name + ".b"], B[name + ".rm"], B[name + ".rv"], act=act)
+        def bn(h, name, act, residual=None):
+            return T.batchnorm2d(h, P[name + ".g"], P[name + ".b"], B[name + ".rm"], B[name + ".rv"], act=act,
+                                 residual=residual)
         h = T.conv2d(x, P["conv1.w"], None, 2, 3)
         h = bn(h, "bn1", 1)
         h = T.maxpool2d(h, 3, 2, 1)
         for (n, cin, mid, cout, stride, down) in self.blocks():
             t = bn(T.conv2d(h, P[n + ".c1.w"], None, 1, 0), n + ".bn1", 1)
             t = bn(T.conv2d(t, P[n + ".c2.w"], None, stride, 1), n + ".bn2", 1)
-            t = bn(T.conv2d(t, P[n + ".c3.w"], None, 1, 0), n + ".bn3", 0)
             idn = bn(T.conv2d(h, P[n + ".ds.w"], None, stride, 0), n + ".dsbn", 0) if down else h
-            h = T.add_relu(t, idn)
+            # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN)
+            h = bn(T.conv2d(t, P[n + ".c3.w"], None, 1, 0), n + ".bn3", 1, residual=idn)
         h = T.avgpool_global(h)
         z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
         return T.softmax_xent(z, y)
