@@ -240,10 +240,16 @@ __global__ void colsum_kernel(const void* x, const void* yv, void* dz, int64_t r
 // Vectorised variant (cols % 8 == 0, 16-B aligned): thread (tx, ty) owns 8
 // consecutive columns (one 128-bit bf16 vector) and every 8th row of its
 // split; 4 rows in flight per thread; fixed-order smem combine.
+// The last block of each 256-column group to finish (arrival counter) also
+// reduces that group's split partials into out[] (+ beta·out) in a fixed order
+// — no separate finalize launch, and the result does not depend on which
+// block arrived last.
 template <int MODE>
 __global__ void __launch_bounds__(256) colsum_v_kernel(const void* __restrict__ x, const void* __restrict__ yv,
                                                        void* __restrict__ dz, int64_t rows, int64_t cols, be_dtype dt,
-                                                       float* __restrict__ partial, int64_t rows_per_split) {
+                                                       float* __restrict__ partial, int64_t rows_per_split,
+                                                       unsigned* __restrict__ counters, float* __restrict__ out,
+                                                       float beta) {
   __shared__ float sm[8][257];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t c = ((int64_t)blockIdx.x * 32 + tx) * 8;
@@ -294,6 +300,33 @@ __global__ void __launch_bounds__(256) colsum_v_kernel(const void* __restrict__ 
     for (int w = 0; w < 8; ++w) t += sm[w][cc];
     partial[(int64_t)blockIdx.y * cols + col] = t;
   }
+  // ---- last arriving block of this column group: final fixed-order reduce
+  __shared__ unsigned last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int64_t rem = cols - (int64_t)blockIdx.x * 256;
+  const int ncol = rem < 256 ? (int)rem : 256;
+  const int per = 256 / ncol >= 8 ? 8 : (256 / ncol >= 4 ? 4 : (256 / ncol >= 2 ? 2 : 1));  // threads per column
+  const int cidx = threadIdx.x / per, part = threadIdx.x % per;
+  float t = 0.f;
+  if (cidx < ncol) {
+    const int64_t c2 = (int64_t)blockIdx.x * 256 + cidx;
+    for (int sp = part; sp < (int)gridDim.y; sp += per) t += __ldcg(&partial[(int64_t)sp * cols + c2]);
+  }
+  __syncthreads();
+  sm[0][threadIdx.x] = t;
+  __syncthreads();
+  if (part == 0 && cidx < ncol) {
+    float u = 0.f;
+    for (int k = 0; k < per; ++k) u += sm[0][threadIdx.x + k];
+    const int64_t c2 = (int64_t)blockIdx.x * 256 + cidx;
+    out[c2] = u + (beta != 0.f ? out[c2] : 0.f);
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;  // ready for the next launch
 }
 
 __global__ void colsum_finalize(const float* partial, int splits, int64_t cols, float* out, float beta) {
@@ -302,6 +335,22 @@ __global__ void colsum_finalize(const float* partial, int splits, int64_t cols, 
     for (int s = 0; s < splits; ++s) t += partial[(int64_t)s * cols + c];
     out[c] = t + (beta != 0.f ? out[c] : 0.f);
   }
+}
+
+// Zero-initialised arrival counters (one per 256-column group), reset by the
+// kernel itself; one buffer per process is enough because launches on the
+// compute stream are serialised.
+unsigned* colsum_counters(int64_t groups) {
+  static unsigned* buf = nullptr;
+  static int64_t cap = 0;
+  if (groups > cap) {
+    BE_CHECK_CUDA(cudaDeviceSynchronize());  // the old buffer may still be in use
+    if (buf) cudaFree(buf);
+    cap = std::max<int64_t>(groups, 4096);
+    BE_CHECK_CUDA(cudaMalloc(&buf, sizeof(unsigned) * cap));
+    BE_CHECK_CUDA(cudaMemset(buf, 0, sizeof(unsigned) * cap));
+  }
+  return buf;
 }
 
 void colsum_impl(int mode, const void* x, const void* y, void* dz, int64_t rows, int64_t cols, be_dtype dt,
@@ -315,12 +364,12 @@ void colsum_impl(int mode, const void* x, const void* y, void* dz, int64_t rows,
     Block* tmp = ctx().alloc.allocate(sizeof(float) * splits * cols, s);
     float* partial = reinterpret_cast<float*>(tmp->ptr);
     dim3 grid((unsigned)cg, (unsigned)splits);
-    if (mode == 0) colsum_v_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, rows, cols, dt, partial, rps);
-    else colsum_v_kernel<1><<<grid, 256, 0, s>>>(x, y, dz, rows, cols, dt, partial, rps);
+    unsigned* counters = colsum_counters(cg);
+    if (mode == 0)
+      colsum_v_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, rows, cols, dt, partial, rps, counters, out, beta);
+    else
+      colsum_v_kernel<1><<<grid, 256, 0, s>>>(x, y, dz, rows, cols, dt, partial, rps, counters, out, beta);
     after_launch(mode == 0 ? "colsum_v" : "relu_bwd_colsum_v");
-    colsum_finalize<<<(unsigned)std::min<int64_t>((cols + 255) / 256, 1024), 256, 0, s>>>(partial, (int)splits,
-                                                                                            cols, out, beta);
-    after_launch("colsum_finalize");
     ctx().alloc.free(tmp);
     return;
   }
