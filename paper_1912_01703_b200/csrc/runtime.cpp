@@ -121,31 +121,44 @@ int tune_choose(const std::string& key, int n, int dflt, cudaEvent_t* ev0, cudaE
   *ev0 = *ev1 = nullptr;
   static const int enabled = [] { const char* e = getenv("BE_TUNE"); return e ? atoi(e) : 1; }();
   if (!enabled || n <= 1) return dflt;
+  // round 0 warms each variant up (first-touch allocations, descriptor
+  // caches); rounds 1..kRounds are timed; a variant's score is its fastest
+  // timed run (robust to a run that shared the GPU with other work)
+  constexpr int kRounds = 3;
   std::lock_guard<std::mutex> lk(g_tune_mu);
   TuneState& t = g_tune[key];
   if (t.choice >= 0) return t.choice;
-  if (t.tried < 2 * n) {
-    // round 1 warms each variant up (first-touch allocations, descriptor
-    // caches); round 2 is timed
-    const int v = t.tried % n;
-    if (t.tried++ >= n) {
-      t.ev.resize(2 * n, nullptr);
-      cudaEventCreate(&t.ev[2 * v]);
-      cudaEventCreate(&t.ev[2 * v + 1]);
-      *ev0 = t.ev[2 * v];
-      *ev1 = t.ev[2 * v + 1];
+  if (t.tried < (1 + kRounds) * n) {
+    const int v = t.tried % n, round = t.tried / n;
+    ++t.tried;
+    if (round >= 1) {
+      t.ev.resize(2 * n * kRounds, nullptr);
+      const int i = 2 * ((round - 1) * n + v);
+      cudaEventCreate(&t.ev[i]);
+      cudaEventCreate(&t.ev[i + 1]);
+      *ev0 = t.ev[i];
+      *ev1 = t.ev[i + 1];
     }
     return v;
   }
-  for (int v = 0; v < n; ++v)
-    if (cudaEventQuery(t.ev[2 * v + 1]) != cudaSuccess) { cudaGetLastError(); return dflt; }
+  for (size_t i = 1; i < t.ev.size(); i += 2)
+    if (cudaEventQuery(t.ev[i]) != cudaSuccess) { cudaGetLastError(); return dflt; }
+  static const bool log = [] { const char* e = getenv("BE_TUNE_LOG"); return e && e[0] == '1'; }();
   float best = 1e30f;
   int bv = dflt;
+  std::string msg;
   for (int v = 0; v < n; ++v) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, t.ev[2 * v], t.ev[2 * v + 1]);
-    if (ms < best) { best = ms; bv = v; }
+    float vbest = 1e30f;
+    for (int r = 0; r < kRounds; ++r) {
+      float ms = 0.f;
+      const int i = 2 * (r * n + v);
+      cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]);
+      vbest = std::min(vbest, ms);
+      if (log) msg += (r ? "," : " [") + std::to_string((int)(ms * 1000.f)) + (r == kRounds - 1 ? "]" : "");
+    }
+    if (vbest < best) { best = vbest; bv = v; }
   }
+  if (log) fprintf(stderr, "tune %s ->%d (us)%s\n", key.c_str(), bv, msg.c_str());
   for (cudaEvent_t e : t.ev) cudaEventDestroy(e);
   t.ev.clear();
   t.choice = bv;

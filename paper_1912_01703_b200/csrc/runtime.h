@@ -256,10 +256,11 @@ struct Context {
 Context& ctx();
 bool grad_enabled();
 // On-line variant autotuning (cudnn.benchmark-style, no synchronisation):
-// the first n calls for `key` run variants 0..n-1 bracketed by events
-// (returned in *ev0/*ev1, to be recorded around the launch by the caller);
-// once all those events have completed, the fastest variant is returned
-// for every later call.  BE_TUNE=0 pins variant `dflt`.
+// the first n calls for `key` run variants 0..n-1 (warm-up), the next 3n
+// run them again bracketed by events (returned in *ev0/*ev1, to be recorded
+// around the launch by the caller); once all those events have completed,
+// the variant with the fastest single timed run is returned for every later
+// call.  BE_TUNE=0 pins variant `dflt`.
 int tune_choose(const std::string& key, int n_variants, int dflt, cudaEvent_t* ev0, cudaEvent_t* ev1);
 // GEMM launch profiling (be_prof_enable): returns a record index or -1
 int prof_begin(const char* name, double flops, double bytes, int m, int n, int k, cudaStream_t s);

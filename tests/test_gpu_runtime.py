@@ -287,8 +287,9 @@ def test_overlapped_sgd_bitwise_equals_fused(net):
     # candidates, two models stepping alternately would get different GEMM
     # variants — different, equally valid summation orders)
     scratch = mk()
-    for _ in range(12):
+    for _ in range(30):  # ≥ 4 calls per candidate (1 warm-up + 3 timed rounds)
         be.nn.train_step(scratch, batch, lr=0.05)
+        be.nn.train_step(scratch, batch, lr=0.05, overlap_sgd=True)
     be.synchronize()
     for _ in range(2):
         be.nn.train_step(scratch, batch, lr=0.05)

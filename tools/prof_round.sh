@@ -10,6 +10,6 @@ for c in $CFGS; do
   python bench.py --config $c --steps 30 --warmup 5 --cpu-budget 10 > gpurun_out/${R}_${c}_bench.json 2> gpurun_out/${R}_${c}_bench.err
   ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/${R}_${c}_launches.csv \
-      python bench.py --config $c --steps 2 --warmup 3 --tune-steps 4 --no-cpu-baseline > /dev/null 2>&1
+      python bench.py --config $c --steps 2 --warmup 3 --tune-steps 24 --no-cpu-baseline > /dev/null 2>&1
 done
 ls -la gpurun_out
