@@ -146,7 +146,12 @@ typedef enum {
 } be_op_id;
 
 typedef struct { int act; /* 0 none, 1 relu */ int out_f32; /* 1: fp32 output even in bf16 mode */ } be_linear_attrs;
-typedef struct { int stride, pad, act; int out_f32; } be_conv_attrs;
+typedef struct {
+  int stride, pad, act;
+  int out_f32;
+  int bn_stats;  /* 1: the output feeds a batchnorm2d — the conv's epilogue also produces the per-channel
+                    statistics of the stored values (no bias/act only), so the BN skips its reduction pass */
+} be_conv_attrs;
 typedef struct { int k, stride, pad; } be_pool_attrs;
 typedef struct {
   float eps, momentum;

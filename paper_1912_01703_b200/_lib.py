@@ -49,7 +49,7 @@ class be_linear_attrs(C.Structure):
 
 
 class be_conv_attrs(C.Structure):
-    _fields_ = [("stride", C.c_int), ("pad", C.c_int), ("act", C.c_int), ("out_f32", C.c_int)]
+    _fields_ = [("stride", C.c_int), ("pad", C.c_int), ("act", C.c_int), ("out_f32", C.c_int), ("bn_stats", C.c_int)]
 
 
 class be_pool_attrs(C.Structure):

@@ -253,9 +253,11 @@ def bce_logits(z, labels):
     return _op("BCE_LOGITS", [z, labels])
 
 
-def conv2d(x, w, b=None, stride=1, pad=0, act=0, out_f32=False):
+def conv2d(x, w, b=None, stride=1, pad=0, act=0, out_f32=False, bn_stats=False):
+    """bn_stats=True: the output feeds batchnorm2d — its statistics come from
+    the conv's epilogue (be_conv_attrs.bn_stats)."""
     return _op("CONV2D", [x, w] + ([b] if b is not None else []),
-               L.be_conv_attrs(int(stride), int(pad), int(act), int(out_f32)))
+               L.be_conv_attrs(int(stride), int(pad), int(act), int(out_f32), int(bn_stats)))
 
 
 def maxpool2d(x, k=3, stride=2, pad=0, with_argmax=False):

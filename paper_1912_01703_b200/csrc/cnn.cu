@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(1024) bn_finalize_v(const float* __restrict__ 
     const double ms = t0 / n;
     double var = t1 / n - ms * ms;  // biased (normalisation)
     if (var < 0) var = 0;
-    const float mu = ld(x, c, dt) + (float)ms;
+    const float mu = (x ? ld(x, c, dt) : 0.f) + (float)ms;  // x = nullptr: unshifted partials
     mean[c] = mu;
     invstd[c] = rsqrtf((float)var + eps);
     if (run_mean) run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mu;
@@ -789,6 +789,13 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
   bn_var_finalize<<<(C + 255) / 256, 256, 0, s>>>(partial, (int)sp, C, rows, eps, mean, invstd, run_mean, run_var,
                                                   momentum);
   after_launch("bn_var");
+}
+void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C, float eps, float* mean,
+                            float* invstd, float* run_mean, float* run_var, float momentum, cudaStream_t s) {
+  bn_finalize_v<0><<<(C + 31) / 32, 1024, 0, s>>>(partial, partial + (int64_t)parts * C, parts, C, rows, nullptr,
+                                                  BE_F32, eps, mean, invstd, run_mean, run_var, momentum, nullptr,
+                                                  nullptr, 0.f, nullptr);
+  after_launch("bn_stats_from_partials");
 }
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
               const float* gamma, const float* beta, int act, cudaStream_t s, const void* res) {

@@ -75,6 +75,10 @@ struct __align__(64) GemmParams {
   uint16_t* upd_shadow;
   float lr, mu, wd, gscale;
   CUtensorMap tp[2];          // P, V as fp32 [M, N] maps, box 32 × 32 (fused-SGD epilogue loads)
+  // per-column Σ / Σx² of the stored output (batch-norm statistics from the
+  // epilogue): partial rows [gridDim.x·4][N] (Σ) then [gridDim.x·4][N] (Σx²);
+  // row = CTA·4 + TMEM lane quarter; zeroed by the host before the launch
+  float* stats;
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
@@ -184,6 +188,66 @@ __device__ __forceinline__ void epi_store32(const GemmParams& p, char* Dbase, bo
     }
   }
 }
+
+// ---- column statistics of the stored output (BN statistics in the epilogue)
+// lane = row of a 32 × 32 chunk: the value stored for (row, col0 + j) is the
+// accumulator rounded to the output type (callers guarantee no bias / act /
+// beta); rows ≥ M count 0.  A transpose-reduce (16+8+4+2+1 shuffles) leaves
+// lane L with column col0 + L's sum over the 32 rows.
+__device__ __forceinline__ float col_reduce32(float (&a)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float send = up ? a[j] : a[j + off];
+      const float keep = up ? a[j + off] : a[j];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return a[0];
+}
+__device__ __forceinline__ void colstats32(const GemmParams& p, const uint32_t (&r)[32], bool row_ok, int lane,
+                                           float& s, float& q) {
+  float a[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    float v = __uint_as_float(r[j]);
+    if (!p.d_f32) v = __bfloat162float(__float2bfloat16_rn(v));
+    a[j] = row_ok ? v : 0.f;
+  }
+  s = col_reduce32(a, lane);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    float v = __uint_as_float(r[j]);
+    if (!p.d_f32) v = __bfloat162float(__float2bfloat16_rn(v));
+    a[j] = row_ok ? v * v : 0.f;
+  }
+  q = col_reduce32(a, lane);
+}
+// per-warp running column sums over a CTA's tiles with the same column block
+template <int NCH>
+struct ColStats {
+  float s[NCH], q[NCH];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) { s[k] = 0.f; q[k] = 0.f; }
+  }
+  // write this warp's partial row for columns col_base + k·32 + lane, k < nch
+  // (the warp's own 32-column chunks only)
+  __device__ __forceinline__ void flush(const GemmParams& p, int part, int col_base, int lane, int nch) {
+    const long long parts = (long long)gridDim.x * 4;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int col = col_base + k * 32 + lane;
+      if (k < nch && col < p.N) {
+        p.stats[(long long)part * p.N + col] = s[k];
+        p.stats[(parts + part) * p.N + col] = q[k];
+      }
+    }
+    reset();
+  }
+};
 
 // Fused SGD epilogue for one 32-row × 32-column accumulator chunk held by a
 // warp (lane = row): the accumulator is the fp32 gradient g of parameter
@@ -507,6 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
+    ColStats<(BN / 64 > 2 ? BN / 64 : 2)> cst;
+    cst.reset();
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int mn = t % mn_tiles, sp = t / mn_tiles;
@@ -517,8 +583,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
       const int store_row = sp * p.split_rows + tm * BM + eq * 32;
-#pragma unroll 1
-      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in registers
+      #pragma unroll
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        uint32_t r0[32], r1[32];
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        if (p.stats) {  // batch-norm statistics of the stored values
+          float s_, q_;
+          colstats32(p, r0, row_ok, lane, s_, q_);
+          cst.s[2 * it] += s_; cst.q[2 * it] += q_;
+          if (h1) {
+            colstats32(p, r1, row_ok, lane, s_, q_);
+            cst.s[2 * it + 1] += s_; cst.q[2 * it + 1] += q_;
+          }
+        }
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, Dbase, vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
+        }
+      }
+      } else {
+      #pragma unroll 1
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
         // two TMEM loads in flight per wait (warp-uniform predicates)
         const int col0 = tn * BN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
@@ -535,6 +633,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
         }
+      }
+      }
+      if (p.stats) {
+        const int tn_next = t + (int)gridDim.x < num_tiles ? ((t + (int)gridDim.x) % mn_tiles) / p.tiles_m : -1;
+        if (tn_next != tn) cst.flush(p, blockIdx.x * 4 + eq, tn * BN + eh * (BN / 2), lane, BN / 64 > 0 ? BN / 64 : 1);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -685,6 +788,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
+    ColStats<(TN / 64 > 2 ? TN / 64 : 2)> cst;
+    cst.reset();
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[0]), 0);
     for (int t = pair_id; t < num_tiles; t += npairs) {
@@ -696,8 +801,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = tm * TM + rank * HM + eq * 32 + lane;
       const bool row_ok = row < p.M;
       const int store_row = sp * p.split_rows + tm * TM + rank * HM + eq * 32;
-#pragma unroll 1
-      for (int c0 = eh * (TN / 2); c0 < (eh + 1) * (TN / 2); c0 += 64) {
+if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in registers
+      #pragma unroll
+      for (int it = 0; it < (TN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (TN / 2) + it * 64;
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * TN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (TN / 2);
+        if (!h0) break;
+        const uint32_t ta = tmem_base + acc * TN + c0 + ((uint32_t)(eq * 32) << 16);
+        uint32_t r0[32], r1[32];
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        if (p.stats) {  // batch-norm statistics of the stored values
+          float s_, q_;
+          colstats32(p, r0, row_ok, lane, s_, q_);
+          cst.s[2 * it] += s_; cst.q[2 * it] += q_;
+          if (h1) {
+            colstats32(p, r1, row_ok, lane, s_, q_);
+            cst.s[2 * it + 1] += s_; cst.q[2 * it + 1] += q_;
+          }
+        }
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, Dbase, vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
+        }
+      }
+      } else {
+      #pragma unroll 1
+      for (int it = 0; it < (TN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (TN / 2) + it * 64;
         // two TMEM loads in flight per wait (warp-uniform predicates)
         const int col0 = tn * TN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (TN / 2);
@@ -714,6 +851,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
         }
+      }
+      }
+      if (p.stats) {
+        const int tn_next = t + npairs < num_tiles ? ((t + npairs) % mn_tiles) / p.tiles_m : -1;
+        if (tn_next != tn) cst.flush(p, blockIdx.x * 4 + eq, tn * TN + eh * (TN / 2), lane, TN / 64 > 0 ? TN / 64 : 1);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -880,6 +1022,8 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
+    ColStats<(BN / 64 > 2 ? BN / 64 : 2)> cst;
+    cst.reset();
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
@@ -887,8 +1031,40 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
       sm100::tc_fence_after();
       const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
-#pragma unroll 1
-      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in registers
+      #pragma unroll
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
+        // two TMEM loads in flight per wait (warp-uniform predicates)
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        if (p.stats) {  // batch-norm statistics of the stored values
+          float s_, q_;
+          colstats32(p, r0, row_ok, lane, s_, q_);
+          cst.s[2 * it] += s_; cst.q[2 * it] += q_;
+          if (h1) {
+            colstats32(p, r1, row_ok, lane, s_, q_);
+            cst.s[2 * it + 1] += s_; cst.q[2 * it + 1] += q_;
+          }
+        }
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
+        }
+      }
+      } else {
+      #pragma unroll 1
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
         // two TMEM loads in flight per wait (warp-uniform predicates)
         const int col0 = tn * BN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
@@ -905,6 +1081,11 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
           epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
           if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
         }
+      }
+      }
+      if (p.stats) {
+        const int tn_next = t + (int)gridDim.x < num_tiles ? (t + (int)gridDim.x) / p.tiles_m : -1;
+        if (tn_next != tn) cst.flush(p, blockIdx.x * 4 + eq, tn * BN + eh * (BN / 2), lane, BN / 64 > 0 ? BN / 64 : 1);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -1082,6 +1263,8 @@ __global__ void __launch_bounds__(convs::kThreads, 1) conv_small_c_kernel(const 
     const int eq = warp & 3, eh = ew >> 2;  // TMEM lane quarter (= warp % 4), column half
     int slot = 0;
     int acc = 0; uint32_t acc_phase = 0;
+    ColStats<(BN / 64 > 2 ? BN / 64 : 2)> cst;
+    cst.reset();
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
@@ -1089,8 +1272,39 @@ __global__ void __launch_bounds__(convs::kThreads, 1) conv_small_c_kernel(const 
       sm100::tc_fence_after();
       const int row = tm * BM + eq * 32 + lane;
       const bool row_ok = row < p.M;
-#pragma unroll 1
-      for (int c0 = eh * (BN / 2); c0 < (eh + 1) * (BN / 2); c0 += 64) {
+if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in registers
+      #pragma unroll
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
+        const int col0 = tn * BN + c0, col1 = col0 + 32;
+        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        if (!h0) break;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        if (p.stats) {  // batch-norm statistics of the stored values
+          float s_, q_;
+          colstats32(p, r0, row_ok, lane, s_, q_);
+          cst.s[2 * it] += s_; cst.q[2 * it] += q_;
+          if (h1) {
+            colstats32(p, r1, row_ok, lane, s_, q_);
+            cst.s[2 * it + 1] += s_; cst.q[2 * it + 1] += q_;
+          }
+        }
+        if (p.tma_store) {
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
+        }
+      }
+      } else {
+      #pragma unroll 1
+      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
         const int col0 = tn * BN + c0, col1 = col0 + 32;
         const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
         if (!h0) break;
@@ -1106,6 +1320,11 @@ __global__ void __launch_bounds__(convs::kThreads, 1) conv_small_c_kernel(const 
           epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
           if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
         }
+      }
+      }
+      if (p.stats) {
+        const int tn_next = t + (int)gridDim.x < num_tiles ? (t + (int)gridDim.x) / p.tiles_m : -1;
+        if (tn_next != tn) cst.flush(p, blockIdx.x * 4 + eq, tn * BN + eh * (BN / 2), lane, BN / 64 > 0 ? BN / 64 : 1);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -1373,6 +1592,15 @@ void set_update(GemmParams& p, const GemmDesc& g) {
   p.D = nullptr;
 }
 // per parameter element: p read+write, v read+write (momentum), shadow write
+// BN statistics epilogue (GemmDesc::stats)
+void set_stats(GemmParams& p, const GemmDesc& g, int grid) {
+  p.stats = nullptr;
+  if (!g.stats) return;
+  BE_REQUIRE(!g.bias && !g.act && g.beta == 0.f && p.splits == 1, BE_E_ARG,
+             "gemm: statistics epilogue needs a plain (no bias/act/beta, unsplit) output");
+  p.stats = g.stats;
+  if (g.stats_parts) *g.stats_parts = grid * 4;
+}
 double update_bytes(const GemmDesc& g) {
   return 8.0 + (g.upd->v ? 8.0 : 0.0) + (g.upd->shadow ? 2.0 : 0.0);
 }
@@ -1417,7 +1645,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   // wgrad: M·N tiny, K = N·P·Q up to 3.2 M); fp32 partials are summed in a
   // fixed order by splitk_reduce → deterministic.
   int splits = 1;
-  if (g.upd) splits = 1;  // the update epilogue needs the complete gradient
+  if (g.upd || g.stats) splits = 1;  // the update / statistics epilogues need the complete result
   else if (force_splits > 0) splits = std::max(1, std::min(force_splits, kblocks));
   else if (mn * 2 <= sms && kblocks >= 8) splits = std::max(1, std::min(sms / mn, kblocks / 4));
   int kps = (kblocks + splits - 1) / splits;
@@ -1439,6 +1667,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   if (g.upd) set_update(p, g);
   else setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = std::min(mn * splits, sms);
+  set_stats(p, g, grid);
   const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es +
                            (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
@@ -1492,7 +1721,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   const int mn = p.tiles_m * p.tiles_n;
   const int kblocks = (g.K + BK - 1) / BK;
   int splits = 1;
-  if (!g.upd && mn * 2 <= pairs && kblocks >= 8) splits = std::max(1, std::min(pairs / mn, kblocks / 4));
+  if (!g.upd && !g.stats && mn * 2 <= pairs && kblocks >= 8) splits = std::max(1, std::min(pairs / mn, kblocks / 4));
   int kps = (kblocks + splits - 1) / splits;
   splits = (kblocks + kps - 1) / kps;
   p.splits = splits;
@@ -1509,6 +1738,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   if (g.upd) set_update(p, g);
   else setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = 2 * std::min(mn * splits, pairs);
+  set_stats(p, g, grid);
   const double ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 +
                            (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
@@ -1606,7 +1836,7 @@ int pick_bn(int M, int N, int sms, bool x3) {
 }  // namespace
 
 template <int BN>
-void launch_conv(GemmParams& p, cudaStream_t s) {
+void launch_conv(GemmParams& p, cudaStream_t s, int* stats_parts) {
   using C = conv::Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1616,11 +1846,12 @@ void launch_conv(GemmParams& p, cudaStream_t s) {
   p.tiles_m = (p.M + BM - 1) / BM;
   p.tiles_n = (p.N + BN - 1) / BN;
   const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
+  if (p.stats && stats_parts) *stats_parts = grid * 4;
   conv_tc_kernel<BN><<<grid, conv::kThreads, C::SMEM, s>>>(p);
 }
 
 template <int BN>
-void launch_conv_small_c(GemmParams& p, cudaStream_t s) {
+void launch_conv_small_c(GemmParams& p, cudaStream_t s, int* stats_parts) {
   using C = convs::Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1630,11 +1861,12 @@ void launch_conv_small_c(GemmParams& p, cudaStream_t s) {
   p.tiles_m = (p.M + BM - 1) / BM;
   p.tiles_n = (p.N + BN - 1) / BN;
   const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
+  if (p.stats && stats_parts) *stats_parts = grid * 4;
   conv_small_c_kernel<BN><<<grid, convs::kThreads, C::SMEM, s>>>(p);
 }
 
 static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
-                         int act, float beta, cudaStream_t s) {
+                         int act, float beta, cudaStream_t s, float* stats, int* stats_parts) {
   const int RSC = g.R * g.S * g.C;
   if (!(g.C == 8 || g.C == 16 || g.C == 32) || g.K % 16 != 0 || (RSC + 63) / 64 * 8 > convs::kMaxChunks) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
@@ -1643,6 +1875,7 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
   p.M = g.N * g.P * g.Q; p.N = g.K; p.K = RSC;
   p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
   p.D = y; p.ldd = g.K; p.d_f32 = yd == BE_F32; p.beta = beta; p.bias = bias; p.act = act;
+  p.stats = (stats && !bias && !act && beta == 0.f) ? stats : nullptr;
   p.x = reinterpret_cast<const uint16_t*>(x);
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
   p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
@@ -1653,8 +1886,8 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_small_c", flops, bytes, p.M, g.K, RSC, s);
   setup_store(p, y, p.d_f32 != 0, p.M, g.K, g.K);
-  if (bn == 128) launch_conv_small_c<128>(p, s);
-  else launch_conv_small_c<64>(p, s);
+  if (bn == 128) launch_conv_small_c<128>(p, s, stats_parts);
+  else launch_conv_small_c<64>(p, s, stats_parts);
   prof_end(pidx, s);
   after_launch("conv_tc_small_c");
   g_tc_calls++;
@@ -1662,11 +1895,11 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
 }
 
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
-                   float beta, cudaStream_t s) {
+                   float beta, cudaStream_t s, float* stats, int* stats_parts) {
   if (g.C % 64 != 0) {
     const char* e = getenv("BE_CONV_SMALLC");
     if (e && e[0] == '0') return false;
-    return conv_small_c(x, w, y, g, yd, bias, act, beta, s);
+    return conv_small_c(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts);
   }
   if (g.K % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
@@ -1678,6 +1911,7 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   p.M = g.N * g.P * g.Q; p.N = g.K; p.K = RSC;
   p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
   p.D = y; p.ldd = g.K; p.d_f32 = yd == BE_F32; p.beta = beta; p.bias = bias; p.act = act;
+  p.stats = (stats && !bias && !act && beta == 0.f) ? stats : nullptr;
   p.x = reinterpret_cast<const uint16_t*>(x);
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
   p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
@@ -1693,9 +1927,9 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_implicit", flops, bytes, p.M, g.K, RSC, s);
   setup_store(p, y, p.d_f32 != 0, p.M, g.K, g.K);
-  if (bn == 256) launch_conv<256>(p, s);
-  else if (bn == 128) launch_conv<128>(p, s);
-  else launch_conv<64>(p, s);
+  if (bn == 256) launch_conv<256>(p, s, stats_parts);
+  else if (bn == 128) launch_conv<128>(p, s, stats_parts);
+  else launch_conv<64>(p, s, stats_parts);
   prof_end(pidx, s);
   after_launch("conv_tc_implicit");
   g_tc_calls++;
@@ -1773,6 +2007,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       const int sms = ctx().num_sms;
       const int kbl = (g.K + 63) / 64;
       for (int cbn : {256, 128}) {
+        if (g.stats) break;  // split-K cannot carry the statistics epilogue
         const int tiles = ((g.M + BM - 1) / BM) * ((g.N + cbn - 1) / cbn);
         if (tiles < sms && kbl >= 16 && g.N > cbn / 2) {
           const int sp = std::max(2, std::min(sms / tiles, kbl / 4));
@@ -1782,7 +2017,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       int v = 0;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (pm == 1 && pair_plausible(g)) v = 1;
-      else if (nc > 1) v = tune_choose("gemm:" + tune_key(g), nc, 0, &ev0, &ev1);
+      else if (nc > 1) v = tune_choose("gemm:" + tune_key(g) + (g.stats ? "s" : ""), nc, 0, &ev0, &ev1);
       const Cand c = cands[v];
       if (ev0) cudaEventRecord(ev0, s);
       if (c.kind == 1) launch_tc2(g, s);

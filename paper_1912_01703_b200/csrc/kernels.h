@@ -34,6 +34,12 @@ struct GemmDesc {
   // gradient g of the parameter P[M, N] (row-major, ld = ldd) and the epilogue
   // applies the SGD update to P, its momentum V and its bf16 shadow directly
   const struct SgdFuse* upd = nullptr;
+  // batch-norm statistics of the stored output (no bias / act / beta): per
+  // column Σ and Σx² partials [parts][N] then [parts][N] written into `stats`
+  // (zeroed by the caller, room for 4·num_sms parts); *stats_parts = parts
+  // when the launched kernel produced them (left untouched otherwise)
+  float* stats = nullptr;
+  int* stats_parts = nullptr;
 };
 struct SgdFuse {
   float* p = nullptr; float* v = nullptr; uint16_t* shadow = nullptr;
@@ -104,7 +110,7 @@ void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float
 // Implicit-GEMM convolution on tcgen05 (bf16, C % 64 == 0): y[NPQ, K] =
 // conv(x NHWC, w KRSC) (+bias, act, beta). Returns false when unsupported.
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
-                   float beta, cudaStream_t s);
+                   float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr);
 // bf16 wf[C,R,S,K] = w[K,R−1−r,S−1−s,C] (dgrad of a stride-1 conv as a convolution)
 void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s);
 // cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC
@@ -123,6 +129,10 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
               const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr);
 size_t bn_partial_floats(int64_t rows, int C);
+// mean / invstd (+ running stats) from unshifted per-part column sums: Σ in
+// partial[0..parts)[C], Σx² in partial[parts..2·parts)[C] (conv epilogue)
+void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C, float eps, float* mean,
+                            float* invstd, float* run_mean, float* run_var, float momentum, cudaStream_t s);
 // backward: dgamma, dbeta (fp32, with beta-accumulate flags) and dx
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta,

@@ -157,9 +157,22 @@ static void op_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor*
   const int64_t M = (int64_t)g.N * g.P * g.Q, RSC = (int64_t)g.R * g.S * g.C;
   const be_dtype od = (a.out_f32 || ctx().compute == BE_F32) ? BE_F32 : BE_BF16;
   TRef y = new_tensor({g.N, g.P, g.Q, g.K}, od);
+  // BN statistics from the epilogue: zeroed partial rows for up to 4·num_sms parts
+  TRef stats;
+  int parts = 0;
+  static const bool stats_on = [] { const char* e = getenv("BE_BN_STATS"); return !(e && e[0] == '0'); }();
+  // only where the epilogue has slack: reduction depth R·S·C ≥ output channels
+  // (for K-light, N-heavy convs — the 1×1 expansions — the epilogue is the
+  // bottleneck and the extra column reduction costs more than the BN pass it saves)
+  if (stats_on && a.bn_stats && !b && !a.act && M > 0 && RSC >= g.K) {
+    const int64_t cap = (int64_t)ctx().num_sms * 4;
+    stats = new_tensor({2 * cap * g.K}, BE_F32);
+    BE_CHECK_CUDA(cudaMemsetAsync(stats->data(), 0, sizeof(float) * 2 * cap * g.K, ctx().stream));
+  }
+  float* sp = stats ? stats->ptr<float>() : nullptr;
   if (is_pointwise(g) || x->dtype != BE_BF16 ||
       !k::conv_implicit(x->data(), w->data(), y->data(), g, od, b ? b->ptr<float>() : nullptr, a.act, 0.f,
-                        ctx().stream)) {
+                        ctx().stream, sp, &parts)) {
     int64_t ldc;
     TRef cols = make_cols(x.get(), g, &ldc);
     k::GemmDesc gd;
@@ -168,7 +181,13 @@ static void op_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor*
     gd.B = w->data(); gd.ldb = RSC; gd.b_kmajor = true;
     gd.ab = x->dtype; gd.D = y->data(); gd.ldd = g.K; gd.d = od;
     gd.bias = b ? b->ptr<float>() : nullptr; gd.act = a.act;
+    gd.stats = sp; gd.stats_parts = &parts;
     k::gemm(gd, ctx().stream);
+  }
+  if (parts > 0) {
+    y->bn_stats = stats.release();
+    y->bn_stats_parts = parts;
+    y->bn_stats_version = y->version();
   }
   Node* n = new_node("conv2d", BE_OP_CONV2D, vjp_conv, {x.get(), w0, b});
   if (n) {
@@ -326,8 +345,15 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   cudaStream_t s = ctx().stream;
   TRef mean = new_tensor({C}, BE_F32), inv = new_tensor({C}, BE_F32);
   TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
-  k::bn_stats(x->data(), rows, C, x->dtype, a.eps, mean->ptr<float>(), inv->ptr<float>(), part->ptr<float>(),
-              rm ? rm->ptr<float>() : nullptr, rv ? rv->ptr<float>() : nullptr, a.momentum, s);
+  if (x->bn_stats && x->bn_stats_version == x->version() && x->bn_stats->numel() >= 2LL * x->bn_stats_parts * C) {
+    // statistics already produced by the producing conv's epilogue
+    k::bn_stats_from_partials(x->bn_stats->ptr<float>(), x->bn_stats_parts, rows, C, a.eps, mean->ptr<float>(),
+                              inv->ptr<float>(), rm ? rm->ptr<float>() : nullptr, rv ? rv->ptr<float>() : nullptr,
+                              a.momentum, s);
+  } else {
+    k::bn_stats(x->data(), rows, C, x->dtype, a.eps, mean->ptr<float>(), inv->ptr<float>(), part->ptr<float>(),
+                rm ? rm->ptr<float>() : nullptr, rv ? rv->ptr<float>() : nullptr, a.momentum, s);
+  }
   if (rm) rm->bump_version();
   if (rv) rv->bump_version();
   TRef y = new_tensor(x->shape, x->rank, x->dtype);

@@ -314,6 +314,7 @@ void tensor_drop(Tensor* t) {
   if (t->refcount.fetch_sub(1, std::memory_order_acq_rel) == 1) {
     if (t->grad) tensor_drop(t->grad);
     if (t->shadow) tensor_drop(t->shadow);
+    if (t->bn_stats) tensor_drop(t->bn_stats);
     if (t->mom_block) ctx().alloc.free(t->mom_block);
     if (t->grad_fn) node_drop(t->grad_fn);
     t->storage->drop();

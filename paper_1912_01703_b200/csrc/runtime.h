@@ -123,6 +123,12 @@ struct Tensor {
   Block* mom_block = nullptr;
   int ddp_slot = -1;          // index in DDP param table
   int opt_slot = -1;          // index in the overlapped-SGD table
+  // per-channel Σ / Σx² partials of this tensor's values, produced by the
+  // epilogue of the conv that wrote it (be_conv_attrs.bn_stats); valid while
+  // the version is unchanged — batchnorm2d then skips its statistics pass
+  Tensor* bn_stats = nullptr;
+  int bn_stats_parts = 0;
+  uint64_t bn_stats_version = ~0ull;
 
   int64_t numel() const {
     int64_t n = 1;

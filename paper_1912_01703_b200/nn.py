@@ -255,15 +255,17 @@ class ResNet50(Model):
         def bn(h, name, act, residual=None):
             return T.batchnorm2d(h, P[name + ".g"], P[name + ".b"], B[name + ".rm"], B[name + ".rv"], act=act,
                                  residual=residual)
-        h = T.conv2d(x, P["conv1.w"], None, 2, 3)
+        def conv(h, w, stride, pad):  # every conv feeds a BN: statistics come from the conv epilogue
+            return T.conv2d(h, P[w], None, stride, pad, bn_stats=True)
+        h = conv(x, "conv1.w", 2, 3)
         h = bn(h, "bn1", 1)
         h = T.maxpool2d(h, 3, 2, 1)
         for (n, cin, mid, cout, stride, down) in self.blocks():
-            t = bn(T.conv2d(h, P[n + ".c1.w"], None, 1, 0), n + ".bn1", 1)
-            t = bn(T.conv2d(t, P[n + ".c2.w"], None, stride, 1), n + ".bn2", 1)
-            idn = bn(T.conv2d(h, P[n + ".ds.w"], None, stride, 0), n + ".dsbn", 0) if down else h
+            t = bn(conv(h, n + ".c1.w", 1, 0), n + ".bn1", 1)
+            t = bn(conv(t, n + ".c2.w", stride, 1), n + ".bn2", 1)
+            idn = bn(conv(h, n + ".ds.w", stride, 0), n + ".dsbn", 0) if down else h
             # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN)
-            h = bn(T.conv2d(t, P[n + ".c3.w"], None, 1, 0), n + ".bn3", 1, residual=idn)
+            h = bn(conv(t, n + ".c3.w", 1, 0), n + ".bn3", 1, residual=idn)
         h = T.avgpool_global(h)
         z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
         return T.softmax_xent(z, y)

@@ -218,3 +218,46 @@ def test_ncf_small_fp32():
     pnet = be.nn.NCF(n_users=50, n_items=30, gmf=8, mlp=(16, 16, 8))
     errs = _step_case(onet, pnet, (users, items, y), (be.tensor(users), be.tensor(items), be.tensor(y)), seed=3)
     print("ncf max err", max(errs.values()))
+
+
+@pytest.mark.parametrize("cfg", [(2, 64, 14, 14, 64, 1, 1, 0),     # 1×1 s1: plain GEMM (1-CTA / pair)
+                                 (3, 64, 17, 13, 96, 3, 1, 1),     # implicit conv, ragged M, N < tile
+                                 (2, 64, 16, 16, 160, 1, 2, 0),    # 1×1 s2: implicit conv, 2 column tiles
+                                 (2, 8, 40, 40, 64, 7, 2, 3),      # conv1 small-C kernel
+                                 (1, 128, 28, 28, 512, 1, 1, 0)])  # pair-sized GEMM
+def test_bn_statistics_from_conv_epilogue(cfg):
+    """conv2d(..., bn_stats=True) → batchnorm2d: the BN takes its mean /
+    variance from the conv epilogue's per-column partial sums of the stored
+    bf16 output (one launch fewer) and must equal the oracle's BN of the
+    device's own conv output (1e-2, bf16), forward and backward."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(np.asarray(a, np.float32)))
+    N, C, H, W, K, R, st, pd = cfg
+    rng = np.random.default_rng(sum(cfg) + 7)
+    x = q(rng.standard_normal((N, C, H, W)))
+    w = q(rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R))
+    gam = (rng.standard_normal(K) * 0.3 + 1).astype(np.float32)
+    bet = (rng.standard_normal(K) * 0.3).astype(np.float32)
+    xd = be.tensor(nchw_to_nhwc(x), dtype="bf16")
+    wd = be.tensor(nchw_to_nhwc(w), requires_grad=True)
+    gd, bd = be.tensor(gam, requires_grad=True), be.tensor(bet, requires_grad=True)
+    y = be.conv2d(xd, wd, None, st, pd, bn_stats=True)
+    l0 = be.launch_count()
+    z = be.batchnorm2d(y, gd, bd, act=1)
+    assert be.launch_count() - l0 == 2  # statistics finalize + apply: no reduction pass
+    yv = nhwc_to_nchw(y.numpy()).astype(np.float64)
+    yo, go, bo = Var(yv, True), Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
+    zo = oops.relu(oops.batchnorm2d(yo, go, bo)[0])
+    assert rel(nhwc_to_nchw(z.numpy()), zo.value) < 1e-2
+    g = q(rng.standard_normal(zo.value.shape))
+    backward(zo, g.astype(np.float64))
+    z.backward(be.tensor(nchw_to_nhwc(g), dtype="bf16"))
+    assert rel(gd.grad.numpy(), go.grad) < 1e-2 and rel(bd.grad.numpy(), bo.grad) < 1e-2
+    # the same BN without epilogue statistics agrees to bf16 rounding
+    y2 = be.conv2d(xd, wd, None, st, pd)
+    l0 = be.launch_count()
+    z2 = be.batchnorm2d(y2, gd, bd, act=1)
+    assert be.launch_count() - l0 == 3
+    assert rel(z2.numpy(), z.numpy()) < 1e-2
