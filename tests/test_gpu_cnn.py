@@ -222,9 +222,10 @@ def test_ncf_small_fp32():
 
 @pytest.mark.parametrize("cfg", [(2, 64, 14, 14, 64, 1, 1, 0),     # 1×1 s1: plain GEMM (1-CTA / pair)
                                  (3, 64, 17, 13, 96, 3, 1, 1),     # implicit conv, ragged M, N < tile
-                                 (2, 64, 16, 16, 160, 1, 2, 0),    # 1×1 s2: implicit conv, 2 column tiles
+                                 (2, 256, 16, 16, 160, 1, 2, 0),   # 1×1 s2: implicit conv, 2 column tiles
                                  (2, 8, 40, 40, 64, 7, 2, 3),      # conv1 small-C kernel
-                                 (1, 128, 28, 28, 512, 1, 1, 0)])  # pair-sized GEMM
+                                 (2, 512, 32, 32, 256, 1, 1, 0),   # pair-sized GEMM
+                                 (2, 64, 14, 14, 256, 1, 1, 0)])   # K-light expansion: statistics pass kept
 def test_bn_statistics_from_conv_epilogue(cfg):
     """conv2d(..., bn_stats=True) → batchnorm2d: the BN takes its mean /
     variance from the conv epilogue's per-column partial sums of the stored
@@ -246,7 +247,9 @@ def test_bn_statistics_from_conv_epilogue(cfg):
     y = be.conv2d(xd, wd, None, st, pd, bn_stats=True)
     l0 = be.launch_count()
     z = be.batchnorm2d(y, gd, bd, act=1)
-    assert be.launch_count() - l0 == 2  # statistics finalize + apply: no reduction pass
+    # statistics finalize + apply, no reduction pass — except where R·S·C < K
+    # (the epilogue is the bottleneck there and the conv skips the statistics)
+    assert be.launch_count() - l0 == (2 if C * R * R >= K else 3)
     yv = nhwc_to_nchw(y.numpy()).astype(np.float64)
     yo, go, bo = Var(yv, True), Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
     zo = oops.relu(oops.batchnorm2d(yo, go, bo)[0])
