@@ -708,6 +708,52 @@ __global__ void __launch_bounds__(256) bn_dx_bf16(const uint16_t* __restrict__ g
   }
 }
 
+// y = act(γ·x̂ + β [+ res]) for bf16, 4 rows in flight per thread
+__global__ void __launch_bounds__(256) bn_apply_bf16(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                                     int64_t rows, int C, const float* __restrict__ mean,
+                                                     const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, int act, int64_t rows_per_block,
+                                                     const uint16_t* __restrict__ res) {
+  const int base = blockIdx.x * kBnCG;
+  const int Cg = min(kBnCG, C - base);
+  const int lanes = Cg / 8, rpi = 256 / lanes;
+  const int t = threadIdx.x, v = t % lanes, rl = t / lanes;
+  if (rl >= rpi) return;
+  const int c = base + v * 8;
+  float sc[8], sh[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sc[j] = gamma[c + j] * invstd[c + j];
+    sh[j] = beta[c + j] - mean[c + j] * sc[j];
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  for (int64_t r = r0 + rl; r < r1; r += kBnU * rpi) {
+    uint4 xa[kBnU], ra[kBnU];
+#pragma unroll
+    for (int u = 0; u < kBnU; ++u) {
+      const int64_t rr = r + (int64_t)u * rpi;
+      const int64_t o = (rr < r1 ? rr : r) * C + c;
+      xa[u] = *reinterpret_cast<const uint4*>(x + o);
+      if (res) ra[u] = *reinterpret_cast<const uint4*>(res + o);
+    }
+#pragma unroll
+    for (int u = 0; u < kBnU; ++u) {
+      const int64_t rr = r + (int64_t)u * rpi;
+      if (rr >= r1) break;
+      float a[8], rv[8];
+      unpack8(xa[u], a);
+      if (res) unpack8(ra[u], rv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float val = fmaf(a[j], sc[j], sh[j]);
+        if (res) val += rv[j];
+        a[j] = act ? fmaxf(val, 0.f) : val;
+      }
+      *reinterpret_cast<uint4*>(y + rr * C + c) = pack8(a);
+    }
+  }
+}
+
 // Cooperative fixed-order finalize: 8 threads per channel each sum a strided
 // subset of the split partials, then combine in lane order.
 template <int MODE>  // 0: stats, 2: grads
@@ -940,7 +986,11 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
   if (bn_vec_ok(x, C) && aligned16(y) && (!res || aligned16(res))) {
     dim3 grid;
     const int64_t rpb = bn_rows_per_block(rows, C, &grid);
-    bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb, res);
+    if (dt == BE_BF16)
+      bn_apply_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C,
+                                         mean, invstd, gamma, beta, act, rpb, reinterpret_cast<const uint16_t*>(res));
+    else
+      bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb, res);
     after_launch("bn_apply_v");
     return;
   }
