@@ -708,6 +708,49 @@ __global__ void __launch_bounds__(256) bn_dx_bf16(const uint16_t* __restrict__ g
   }
 }
 
+// forward statistics, bf16: shifted sums Σ(x−K), Σ(x−K)² with K = x[0,c]
+__global__ void __launch_bounds__(256) bn_stats_bf16(const uint16_t* __restrict__ x, int64_t rows, int C,
+                                                     float* __restrict__ part0, float* __restrict__ part1,
+                                                     int64_t rows_per_split) {
+  __shared__ float sm0[kBnCG], sm1[kBnCG];
+  const int base = blockIdx.x * kBnCG;
+  const int Cg = min(kBnCG, C - base);
+  const int lanes = Cg / 8, rpi = 256 / lanes;
+  const int t = threadIdx.x, v = t % lanes, rl = t / lanes;
+  const int c = base + v * 8;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (rl < rpi) {
+    float k[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + c), k);
+    for (int64_t r = r0 + rl; r < r1; r += kBnU * rpi) {
+      uint4 xa[kBnU];
+#pragma unroll
+      for (int u = 0; u < kBnU; ++u) {
+        const int64_t rr = r + (int64_t)u * rpi;
+        xa[u] = *reinterpret_cast<const uint4*>(x + (rr < r1 ? rr : r) * C + c);
+      }
+#pragma unroll
+      for (int u = 0; u < kBnU; ++u) {
+        if (r + (int64_t)u * rpi >= r1) break;
+        float a[8];
+        unpack8(xa[u], a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { const float d = a[j] - k[j]; s0[j] += d; s1[j] += d * d; }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { sm0[rl * Cg + v * 8 + j] = s0[j]; sm1[rl * Cg + v * 8 + j] = s1[j]; }
+  }
+  __syncthreads();
+  for (int i = t; i < Cg; i += 256) {
+    float a0 = 0.f, a1 = 0.f;
+    for (int w = 0; w < rpi; ++w) { a0 += sm0[w * Cg + i]; a1 += sm1[w * Cg + i]; }
+    part0[(int64_t)blockIdx.y * C + base + i] = a0;
+    part1[(int64_t)blockIdx.y * C + base + i] = a1;
+  }
+}
+
 // y = act(γ·x̂ + β [+ res]) for bf16, 4 rows in flight per thread
 __global__ void __launch_bounds__(256) bn_apply_bf16(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
                                                      int64_t rows, int C, const float* __restrict__ mean,
@@ -950,8 +993,11 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
     const int64_t sp = bn_splits_v(rows, C);
     const int64_t rps = (rows + sp - 1) / sp;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-    bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
-                                        partial + sp * C, rps);
+    if (dt == BE_BF16)
+      bn_stats_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, rps);
+    else
+      bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
+                                          partial + sp * C, rps);
     after_launch("bn_stats_v");
     bn_finalize_v<0><<<(C + 31) / 32, 1024, 0, s>>>(partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
                                                     invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
