@@ -65,6 +65,12 @@ struct __align__(64) GemmParams {
   int cN, cH, cW, cC, cR, cS, cstride, cpad, cP, cQ;
   int use_im2col;             // conv A operand via TMA im2col map (ta[1]) instead of gather4 (ta[0])
   int b_im2col;               // conv wgrad: MN-major B operand = im2col(x) via TMA im2col map (tb[1])
+  // conv wgrad, shifted-tile mode: the GEMM's K axis is blocks of 64 output
+  // pixels = sh_hb output rows × sh_wb (≥ Q, power of 2) columns of image n;
+  // A = dY through a 4-D [N,P,Q,K] tiled map (ta[0]), B chunk (tap r,s;
+  // 64 channels) = x through a 4-D [N,H,W,C] tiled map with element strides
+  // = conv stride (tb[1]); out-of-range pixels are zero-filled by TMA
+  int b_shift, sh_wb, sh_hb, sh_pg;  // sh_pg = p-groups per image
   // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
   int tma_store;
   CUtensorMap td;
@@ -486,7 +492,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           for (int op = 0; op < C::NOPS; ++op) {
             uint8_t* sa = sbase + op * (C::A_BYTES + C::B_BYTES);
             uint8_t* sb = sa + C::A_BYTES;
-            if (p.a_kmajor) {
+            if (!X3 && p.b_shift) {
+              // dY pixel block kb = (image n, p-group) as 64 MN-major rows
+              const int ni = kb / p.sh_pg, pg = kb - ni * p.sh_pg;
+#pragma unroll
+              for (int j = 0; j < BM / C::CH; ++j)
+                sm100::tma_load_4d(&p.ta[0], &full[stage], sa + j * C::BK * 128, m0 + j * C::CH, 0, pg * p.sh_hb, ni);
+            } else if (p.a_kmajor) {
               sm100::tma_load_2d(&p.ta[op], &full[stage], sa, k0, m0);
             } else {
 #pragma unroll
@@ -495,6 +507,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             }
             if (p.b_kmajor) {
               sm100::tma_load_2d(&p.tb[op], &full[stage], sb, k0, n0);
+            } else if (!X3 && p.b_shift) {
+              // x for tap (r,s), 64 channels: window start (s−pad, p0·st+r−pad)
+              const int ni = kb / p.sh_pg, pg = kb - ni * p.sh_pg;
+              const int h0 = pg * p.sh_hb * p.cstride - p.cpad;
+#pragma unroll
+              for (int j = 0; j < BN / C::CH; ++j) {
+                const int col = n0 + j * C::CH;
+                const int tap = col / p.cC, cb = (col - tap * p.cC) / 64;
+                const int r = tap / p.cS, sx = tap - r * p.cS;
+                sm100::tma_load_4d(&p.tb[1], &full[stage], sb + j * C::BK * 128, cb * 64, sx - p.cpad, h0 + r, ni);
+              }
             } else if (!X3 && p.b_im2col) {
               // conv wgrad: B = im2col(x) read in place — 64-pixel block k0 ×
               // 64 channels of one filter tap per MN chunk (TMA im2col map tb[1])
@@ -1505,6 +1528,21 @@ void encode_2d_sw(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, u
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   BE_REQUIRE(r == CUDA_SUCCESS, BE_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
+// 4-D tiled bf16 map over an NHWC-like tensor dims {d0 (contiguous), d1, d2, d3}
+// with element strides {1, es, es, 1}, box {b0, b1·es, b2·es, 1}, SW128.
+bool encode_4d_tiled(CUtensorMap* m, const void* ptr, const uint64_t (&dims)[4], uint32_t b0, uint32_t b1, uint32_t b2,
+                     uint32_t es) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t st[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
+  cuuint32_t box[4] = {b0, b1 * es, b2 * es, 1};
+  cuuint32_t estr[4] = {1, es, es, 1};
+  if (box[1] > 256 || box[2] > 256) return false;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), d, st, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 void encode_2d(CUtensorMap* m, const void* ptr, be_dtype dt, uint64_t cols, uint64_t rows, uint64_t ld,
                uint32_t box_c, uint32_t box_r) {
   encode_2d_sw(m, ptr, dt, cols, rows, ld, box_c, box_r, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1618,7 +1656,24 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   memset(&p, 0, sizeof(p));
   const be_dtype dt = X3 ? BE_F32 : BE_BF16;
   encode_operand(&p.ta[0], a_hi, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
-  if (!X3 && g.conv_x) {
+  int Keff = g.K;  // the GEMM's reduction length as the kernel walks it
+  if (!X3 && g.conv_x && g.conv_shift) {
+    // wgrad, shifted-tile mode: pixel blocks of hb output rows × wb columns
+    const ConvGeom& cg = g.conv_g;
+    int wb = 1;
+    while (wb < cg.Q) wb *= 2;
+    BE_REQUIRE(wb <= 64 && cg.C % 64 == 0 && g.M % 8 == 0, BE_E_ARG, "shift wgrad: Q <= 64, C % 64, K % 8");
+    const int hb = 64 / wb, pg = (cg.P + hb - 1) / hb;
+    const uint64_t ddy[4] = {(uint64_t)g.M, (uint64_t)cg.Q, (uint64_t)cg.P, (uint64_t)cg.N};
+    const uint64_t dx[4] = {(uint64_t)cg.C, (uint64_t)cg.W, (uint64_t)cg.H, (uint64_t)cg.N};
+    BE_REQUIRE(encode_4d_tiled(&p.ta[0], g.A, ddy, 64, wb, hb, 1), BE_E_CUDA, "dY 4-D map encode failed");
+    BE_REQUIRE(encode_4d_tiled(&p.tb[1], g.conv_x, dx, 64, wb, hb, cg.stride), BE_E_CUDA, "x 4-D map encode failed");
+    encode_2d(&p.tb[0], g.conv_x, BE_BF16, (uint64_t)cg.C, (uint64_t)cg.N * cg.H * cg.W, (uint64_t)cg.C, 64, 64);
+    p.b_shift = 1; p.sh_wb = wb; p.sh_hb = hb; p.sh_pg = pg;
+    p.cN = cg.N; p.cH = cg.H; p.cW = cg.W; p.cC = cg.C; p.cR = cg.R; p.cS = cg.S;
+    p.cstride = cg.stride; p.cpad = cg.pad; p.cP = cg.P; p.cQ = cg.Q;
+    Keff = cg.N * pg * 64;
+  } else if (!X3 && g.conv_x) {
     // wgrad B = im2col(x): tb[1] im2col map (64 pixels × 64 channels per op);
     // tb[0] = x as a plain 2-D map (only prefetched)
     const ConvGeom& cg = g.conv_g;
@@ -1634,13 +1689,13 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
     encode_operand(&p.ta[1], a_lo, dt, g.M, g.K, g.lda, g.a_kmajor, BM, C::BK);
     encode_operand(&p.tb[1], b_lo, dt, g.N, g.K, g.ldb, g.b_kmajor, BN, C::BK);
   }
-  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.M = g.M; p.N = g.N; p.K = Keff;
   p.a_kmajor = g.a_kmajor; p.b_kmajor = g.b_kmajor;
   p.tiles_m = (g.M + BM - 1) / BM;
   p.tiles_n = (g.N + BN - 1) / BN;
   const int sms = ctx().num_sms;
   const int mn = p.tiles_m * p.tiles_n;
-  const int kblocks = (g.K + C::BK - 1) / C::BK;
+  const int kblocks = (Keff + C::BK - 1) / C::BK;
   // split-K when the output tile grid cannot fill the machine (e.g. conv
   // wgrad: M·N tiny, K = N·P·Q up to 3.2 M); fp32 partials are summed in a
   // fixed order by splitk_reduce → deterministic.

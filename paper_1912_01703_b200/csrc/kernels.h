@@ -30,6 +30,9 @@ struct GemmDesc {
   // place by TMA im2col (bf16, C % 64 == 0); B / ldb are then ignored
   const void* conv_x = nullptr;
   ConvGeom conv_g{};
+  // with conv_x: read A (= dY, [N·P·Q, K_out]) and B (= x) as shifted 4-D
+  // tiles instead of an im2col map (needs Q ≤ 64, C % 64 == 0, K_out % 8 == 0)
+  bool conv_shift = false;
   // fused SGD epilogue: when set, D is not written; the accumulator is the
   // gradient g of the parameter P[M, N] (row-major, ld = ldd) and the epilogue
   // applies the SGD update to P, its momentum V and its bf16 shadow directly

@@ -75,18 +75,23 @@ static void vjp_conv(Node* n, GradSink& sink) {
     // variant 0: B = im2col(x) read in place by TMA im2col; variant 1:
     // materialised columns + GEMM.  TMA im2col moves ~0.13 pixel/cycle/SM,
     // so which one wins depends on the shape: autotuned per shape.
+    // variant 2: A = dY and B = x read as shifted 4-D tiles (blocks of whole
+    // output rows; TMA zero-fills the padding) — tiled TMA, no im2col mode
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int variant = 1;
     if (!is_pointwise(g) && opd == BE_BF16 && g.C % 64 == 0 && (K * 2) % 16 == 0) {
       char key[160];
       snprintf(key, sizeof(key), "conv_wgrad:%d,%d,%d,%d,%d,%d,%d,%d,%d", g.N, g.H, g.W, g.C, g.K, g.R, g.S,
                g.stride, g.pad);
-      variant = tune_choose(key, 2, 0, &e0, &e1);
+      static const int shift_on = [] { const char* e = getenv("BE_WGRAD_SHIFT"); return e ? atoi(e) : 1; }();
+      const bool shift_ok = shift_on && g.Q <= 64 && g.K % 8 == 0 && g.stride <= 2;
+      variant = tune_choose(key, shift_ok ? 3 : 2, 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);
-    if (variant == 0) {
+    if (variant == 0 || variant == 2) {
       gd.conv_x = x->data();
       gd.conv_g = g;
+      gd.conv_shift = variant == 2;
     } else {
       int64_t ldc;
       cols = make_cols(x, g, &ldc);

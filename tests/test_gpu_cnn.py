@@ -264,3 +264,31 @@ def test_bn_statistics_from_conv_epilogue(cfg):
     z2 = be.batchnorm2d(y2, gd, bd, act=1)
     assert be.launch_count() - l0 == 3
     assert rel(z2.numpy(), z.numpy()) < 1e-2
+
+
+@pytest.mark.parametrize("cfg", [(2, 64, 9, 9, 64, 3, 1, 1), (2, 64, 10, 10, 128, 3, 2, 1), (1, 128, 7, 7, 256, 3, 1, 1),
+                                 (3, 64, 17, 13, 96, 3, 1, 1), (2, 64, 30, 30, 64, 3, 1, 1), (1, 64, 12, 12, 64, 5, 2, 2)])
+def test_conv_wgrad_variants_bf16(cfg):
+    """Conv weight gradient through every autotuned variant (the first calls
+    of a shape cycle through them: TMA-im2col B, materialised columns,
+    shifted 4-D tiles of dY and x) — each call's dW vs the oracle on the
+    same bf16 x and dY (fp32 accumulation → 1e-3)."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    N, C, H, W, K, R, st, pd = cfg
+    rng = np.random.default_rng(sum(cfg) + 3)
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(a.astype(np.float32)))
+    x = q(rng.standard_normal((N, C, H, W)))
+    w = q(rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R))
+    xo, wo = Var(x.astype(np.float64)), Var(w.astype(np.float64), True)
+    yo = oops.conv2d(xo, wo, None, st, pd)
+    g = q(rng.standard_normal(yo.value.shape))
+    backward(yo, g.astype(np.float64))
+    xd = be.tensor(nchw_to_nhwc(x), dtype="bf16")
+    gd = be.tensor(nchw_to_nhwc(g), dtype="bf16")
+    for _ in range(6):  # ≥ one call of each of the (up to) three variants
+        wd = be.tensor(nchw_to_nhwc(w), requires_grad=True)
+        yd = be.conv2d(xd, wd, None, st, pd)
+        yd.backward(gd)
+        assert rel(nhwc_to_nchw(wd.grad.numpy()), wo.grad) < 1e-3
