@@ -53,6 +53,80 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass(const uint32_t* __res
   }
 }
 
+// Whole sort in one CTA's shared memory (n ≤ kSmemSortMax): the same stable
+// LSD passes as radix_pass, but keys/positions never leave smem between
+// passes — one global read of the ids, one write of the sorted pairs.
+constexpr int kSmemSortMax = 10240;
+// counter (bucket b, thread t) lives at flattened f = b·T + t, skewed by f/64
+// so both access patterns — a warp counting one digit (consecutive t) and a
+// thread scanning its 64 consecutive flattened entries — avoid bank conflicts
+__device__ __forceinline__ int cidx(int f) { return f + (f >> 6); }
+// exclusive scan of one value per thread over the block (256 threads)
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t tsum = lane < kSortThreads / 32 ? warp_tot[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, tsum, o);
+      if (lane >= o) tsum += y;
+    }
+    if (lane < kSortThreads / 32) warp_tot[lane] = tsum;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const uint32_t before = w ? warp_tot[w - 1] : 0u;
+  return before + x - v;
+}
+__global__ void __launch_bounds__(kSortThreads) radix_sort_smem(const int32_t* __restrict__ ids,
+                                                               uint32_t* __restrict__ out_k,
+                                                               uint32_t* __restrict__ out_v, int n, int bits) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* cnt = sm;                                              // skewed [kBuckets][kSortThreads]
+  uint32_t* ka = cnt + kBuckets * kSortThreads + kBuckets * kSortThreads / 64;  // [n]
+  uint32_t* va = ka + n;
+  uint32_t* kb = va + n;
+  uint32_t* vb = kb + n;
+  __shared__ uint32_t warp_tot[kSortThreads / 32];
+  const int t = threadIdx.x;
+  for (int i = t; i < n; i += kSortThreads) { ka[i] = (uint32_t)ids[i]; va[i] = (uint32_t)i; }
+  __syncthreads();
+  const int E = (n + kSortThreads - 1) / kSortThreads;
+  const int lo = min(n, t * E), hi = min(n, lo + E);
+  for (int shift = 0; shift < bits; shift += kDigitBits) {
+    for (int b = 0; b < kBuckets; ++b) cnt[cidx(b * kSortThreads + t)] = 0;
+    for (int i = lo; i < hi; ++i) cnt[cidx(((ka[i] >> shift) & (kBuckets - 1)) * kSortThreads + t)]++;
+    __syncthreads();
+    uint32_t sacc = 0;
+    for (int j = 0; j < kBuckets; ++j) sacc += cnt[cidx(t * kBuckets + j)];
+    uint32_t run = block_exscan(sacc, warp_tot);
+    for (int j = 0; j < kBuckets; ++j) {
+      const int f = cidx(t * kBuckets + j);
+      const uint32_t v = cnt[f];
+      cnt[f] = run;
+      run += v;
+    }
+    __syncthreads();
+    for (int i = lo; i < hi; ++i) {
+      const uint32_t k = ka[i];
+      const uint32_t pos = cnt[cidx(((k >> shift) & (kBuckets - 1)) * kSortThreads + t)]++;
+      kb[pos] = k;
+      vb[pos] = va[i];
+    }
+    __syncthreads();
+    uint32_t* tk = ka; ka = kb; kb = tk;
+    uint32_t* tv = va; va = vb; vb = tv;
+  }
+  for (int i = t; i < n; i += kSortThreads) { out_k[i] = ka[i]; out_v[i] = va[i]; }
+}
+
 __global__ void init_pairs(const int32_t* ids, uint32_t* k, uint32_t* v, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     k[i] = (uint32_t)ids[i];
@@ -114,6 +188,21 @@ void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cud
   uint32_t* v0 = k0 + B;
   uint32_t* k1 = v0 + B;
   uint32_t* v1 = k1 + B;
+  if (B <= kSmemSortMax) {
+    int bits = 1;
+    while ((1LL << bits) < V) ++bits;
+    const size_t cwords = (size_t)kBuckets * kSortThreads + (size_t)kBuckets * kSortThreads / 64;
+    const size_t smem = sizeof(uint32_t) * (cwords + 4 * (size_t)B);
+    static bool sattr = false;
+    if (!sattr) {
+      BE_CHECK_CUDA(cudaFuncSetAttribute(radix_sort_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(uint32_t) * (cwords + 4 * kSmemSortMax))));
+      sattr = true;
+    }
+    radix_sort_smem<<<1, kSortThreads, smem, s>>>(ids, k0, v0, (int)B, bits);
+    after_launch("embedding_radix_sort_smem");
+    return;
+  }
   init_pairs<<<(int)std::min<int64_t>((B + 255) / 256, 1024), 256, 0, s>>>(ids, k0, v0, (int)B);
   after_launch("embedding_init_pairs");
   int bits = 1;

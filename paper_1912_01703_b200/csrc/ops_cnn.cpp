@@ -387,29 +387,39 @@ static void vjp_embedding(Node* n, GradSink& sink) {
   TRef gz = contiguous_like(sink.upstream[0], sink.upstream[0]->dtype);
   const int64_t B = ids->numel(), D = dt->shape[1], V = dt->shape[0];
   // Tables looked up with the same ids (NeuMF: GMF and MLP tables of a side)
-  // share one sort: cache keyed by the ids storage, its version and V.
-  static struct {
+  // share one sort: a small cache keyed by the ids storage, its version and V
+  // (several entries: backward visits the user and item tables interleaved).
+  struct Entry {
     Storage* st = nullptr;
-    uint64_t version = 0;
+    uint64_t version = 0, stamp = 0;
     int64_t B = -1, V = -1, off = 0;
     TRef sorted;
-  } cache;
-  const bool hit = cache.st == ids->storage && cache.version == ids->version() && cache.B == B && cache.V == V &&
-                   cache.off == ids->offset && cache.sorted;
-  if (!hit) {
+  };
+  static Entry cache[4];
+  static uint64_t clock = 0;
+  Entry* e = nullptr;
+  for (Entry& c : cache)
+    if (c.st == ids->storage && c.version == ids->version() && c.B == B && c.V == V && c.off == ids->offset &&
+        c.sorted)
+      e = &c;
+  if (!e) {
+    e = &cache[0];
+    for (Entry& c : cache)
+      if (c.stamp < e->stamp) e = &c;  // least recently used
     const size_t sb = k::embedding_bwd_scratch(B);
     TRef scratch = new_tensor({(int64_t)((sb + 3) / 4)}, BE_F32);
     k::embedding_sort(ids->ptr<int32_t>(), B, V, scratch->data(), ctx().stream);
-    if (cache.st) cache.st->drop();
-    cache.st = ids->storage;
-    cache.st->retain();
-    cache.version = ids->version();
-    cache.B = B;
-    cache.V = V;
-    cache.off = ids->offset;
-    cache.sorted = scratch;
+    if (e->st) e->st->drop();
+    e->st = ids->storage;
+    e->st->retain();
+    e->version = ids->version();
+    e->B = B;
+    e->V = V;
+    e->off = ids->offset;
+    e->sorted = scratch;
   }
-  k::embedding_bwd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), V, beta, cache.sorted->data(), ctx().stream);
+  e->stamp = ++clock;
+  k::embedding_bwd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), V, beta, e->sorted->data(), ctx().stream);
   sink.commit(0);
 }
 static void op_embedding(const be_tensor* in, int n_in, be_tensor* out) {
