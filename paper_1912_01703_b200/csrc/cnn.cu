@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -23,29 +24,50 @@ int grid_for(int64_t n, int per = 1) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx().num_sms * 16));
 }
 
-// ---- im2col: one thread per (m, r, u, 8-channel chunk); 16-B copies when C%8==0 (bf16) / C%4==0 (f32)
-template <typename T, int VEC>
-__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int64_t ldc, ConvGeom g, int64_t total) {
-  const int CV = g.C / VEC;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int cv = (int)(t % CV); t /= CV;
-    const int u = (int)(t % g.S); t /= g.S;
-    const int r = (int)(t % g.R); t /= g.R;
-    const int64_t m = t;
-    const int q = (int)(m % g.Q);
-    const int p = (int)((m / g.Q) % g.P);
-    const int n = (int)(m / ((int64_t)g.P * g.Q));
-    const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + u;
-    T* dst = cols + m * ldc + ((int64_t)(r * g.S + u) * g.C + cv * VEC);
-    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
-      const T* src = x + (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * VEC;
-      if (VEC * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
-      else for (int j = 0; j < VEC; ++j) dst[j] = src[j];
-    } else {
-      if (VEC * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-      else for (int j = 0; j < VEC; ++j) dst[j] = T(0);
+// Index arithmetic: the memory-bound CNN kernels decompose a flat item index
+// into (n, h, w, c)-style coordinates with run-time divisors.  The launchers
+// pick I = uint32_t whenever the item count fits (every C3/C4 shape): 64-bit
+// integer division is a ~70-instruction software routine on the GPU and was
+// the bottleneck of these kernels (e.g. conv1's wgrad im2col ran at 2 TB/s).
+// Byte offsets stay 64-bit.  Each thread keeps UNR items' loads in flight.
+constexpr int UNR = 4;
+
+// ---- im2col: one item per (m, r, u, VEC-channel chunk); 16-B copies when C%8==0 (bf16) / C%4==0 (f32)
+template <typename T, int VEC, typename I>
+__global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int64_t ldc,
+                                                     ConvGeom g, I total) {
+  using VT = typename std::conditional<VEC * sizeof(T) == 16, uint4, T>::type;
+  static_assert(VEC * sizeof(T) == 16 || VEC == 1, "im2col vector width");
+  const I CV = (I)(g.C / VEC);
+  const I stride = (I)gridDim.x * blockDim.x;
+  for (I base = (I)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += UNR * stride) {
+    VT v[UNR];
+    int64_t dst[UNR];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const I i = base + (I)k * stride;
+      dst[k] = -1;
+      if (i < total) {
+        I t = i;
+        const int cv = (int)(t % CV); t /= CV;
+        const int u = (int)(t % (I)g.S); t /= (I)g.S;
+        const int r = (int)(t % (I)g.R);
+        const I m = t / (I)g.R;
+        const int q = (int)(m % (I)g.Q);
+        const I np = m / (I)g.Q;
+        const int p = (int)(np % (I)g.P);
+        const int n = (int)(np / (I)g.P);
+        const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + u;
+        dst[k] = (int64_t)m * ldc + (int64_t)(r * g.S + u) * g.C + cv * VEC;
+        if (h >= 0 && h < g.H && w >= 0 && w < g.W)
+          v[k] = *reinterpret_cast<const VT*>(x + (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * VEC);
+        else
+          v[k] = VT{};
+      }
     }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k)
+      if (dst[k] >= 0) *reinterpret_cast<VT*>(cols + dst[k]) = v[k];
   }
 }
 
@@ -79,27 +101,38 @@ __global__ void col2im_kernel(const T* __restrict__ dcols, int64_t ldc, T* __res
   }
 }
 
-// col2im, 8 channels per thread (16-B loads of dcols / stores of dx)
-__global__ void col2im_v(const void* __restrict__ dcols, int64_t ldc, void* __restrict__ dx, ConvGeom g, float beta,
-                         int64_t nvec, be_dtype dt) {
-  const int CV = g.C / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int cv = (int)(t % CV); t /= CV;
-    const int w = (int)(t % g.W); t /= g.W;
-    const int h = (int)(t % g.H);
-    const int n = (int)(t / g.H);
+// (n, h, w, cv) of a flat NHWC item index with 8-channel vectors
+template <typename I>
+__device__ __forceinline__ void nhwc8(I i, const ConvGeom& g, int H, int W, int& n, int& h, int& w, int& cv) {
+  const I CV = (I)(g.C / 8);
+  I t = i;
+  cv = (int)(t % CV); t /= CV;
+  w = (int)(t % (I)W); t /= (I)W;
+  h = (int)(t % (I)H);
+  n = (int)(t / (I)H);
+}
+
+// col2im, 8 channels per item (16-B loads of dcols / stores of dx).  The taps
+// that reach input pixel (h, w) are enumerated by output row/column directly
+// (p ∈ [p_lo, p_hi], r = h + pad − p·stride), summed in increasing (r, u)
+// order (decreasing p, q) as the reference loop over taps.
+template <typename I>
+__global__ void __launch_bounds__(256) col2im_v(const void* __restrict__ dcols, int64_t ldc, void* __restrict__ dx,
+                                                ConvGeom g, float beta, I nvec, be_dtype dt) {
+  const I stride = (I)gridDim.x * blockDim.x;
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    int n, h, w, cv;
+    nhwc8(i, g, g.H, g.W, n, h, w, cv);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = 0; r < g.R; ++r) {
-      const int ph = h + g.pad - r;
-      if (ph < 0 || ph % g.stride) continue;
-      const int p = ph / g.stride;
-      if (p >= g.P) continue;
-      for (int u = 0; u < g.S; ++u) {
-        const int qw = w + g.pad - u;
-        if (qw < 0 || qw % g.stride) continue;
-        const int q = qw / g.stride;
-        if (q >= g.Q) continue;
+    // p·stride ∈ [h + pad − R + 1, h + pad]
+    const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
+    const int p_lo = max(0, (h + g.pad - g.R + g.stride) / g.stride);
+    const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
+    const int q_lo = max(0, (w + g.pad - g.S + g.stride) / g.stride);
+    for (int p = p_hi; p >= p_lo; --p) {
+      const int r = h + g.pad - p * g.stride;
+      for (int q = q_hi; q >= q_lo; --q) {
+        const int u = w + g.pad - q * g.stride;
         const int64_t m = ((int64_t)n * g.P + p) * g.Q + q;
         V8 a = ld8(dcols, m * ldc + (int64_t)(r * g.S + u) * g.C + cv * 8, dt);
 #pragma unroll
@@ -107,23 +140,22 @@ __global__ void col2im_v(const void* __restrict__ dcols, int64_t ldc, void* __re
       }
     }
     V8 o;
-    if (beta != 0.f) o = ld8(dx, i * 8, dt);
+    if (beta != 0.f) o = ld8(dx, (int64_t)i * 8, dt);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o.v[j] = acc[j] + (beta != 0.f ? o.v[j] : 0.f);
-    st8(dx, i * 8, dt, o);
+    st8(dx, (int64_t)i * 8, dt, o);
   }
 }
 
-// max pool, 8 channels per thread
-__global__ void maxpool_fwd_v(const void* __restrict__ x, void* __restrict__ y, uint8_t* __restrict__ am, ConvGeom g,
-                              be_dtype dt, int64_t nvec) {
-  const int CV = g.C / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int cv = (int)(t % CV); t /= CV;
-    const int q = (int)(t % g.Q); t /= g.Q;
-    const int p = (int)(t % g.P);
-    const int n = (int)(t / g.P);
+// max pool, 8 channels per item; UNR items per thread, all window loads of an
+// item issued before its compare chain
+template <typename I>
+__global__ void __launch_bounds__(256) maxpool_fwd_v(const void* __restrict__ x, void* __restrict__ y,
+                                                     uint8_t* __restrict__ am, ConvGeom g, be_dtype dt, I nvec) {
+  const I stride = (I)gridDim.x * blockDim.x;
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    int n, p, q, cv;
+    nhwc8(i, g, g.P, g.Q, n, p, q, cv);
     float best[8];
     int bi[8];
 #pragma unroll
@@ -147,44 +179,69 @@ __global__ void maxpool_fwd_v(const void* __restrict__ x, void* __restrict__ y, 
     uint8_t* pb = reinterpret_cast<uint8_t*>(&packed);
 #pragma unroll
     for (int j = 0; j < 8; ++j) { o.v[j] = best[j]; pb[j] = (uint8_t)bi[j]; }
-    st8(y, i * 8, dt, o);
-    if (am) *reinterpret_cast<uint2*>(am + i * 8) = packed;
+    st8(y, (int64_t)i * 8, dt, o);
+    if (am) *reinterpret_cast<uint2*>(am + (int64_t)i * 8) = packed;
   }
 }
-__global__ void maxpool_bwd_v(const void* __restrict__ dy, const uint8_t* __restrict__ am, void* __restrict__ dx,
-                              ConvGeom g, be_dtype dt, float beta, int64_t nvec) {
-  const int CV = g.C / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int cv = (int)(t % CV); t /= CV;
-    const int w = (int)(t % g.W); t /= g.W;
-    const int h = (int)(t % g.H);
-    const int n = (int)(t / g.H);
+// max-pool backward, gather form: dx[n,h,w,c] = Σ over the windows (p, q)
+// containing (h, w) whose recorded winner is (h, w).  With R ≤ 2·stride and
+// S ≤ 2·stride (every pool on the path) at most 2 × 2 windows: their 4
+// (dy, argmax) loads are issued together, then summed in (p, q) order.
+template <typename I, bool TWO>
+__global__ void __launch_bounds__(256) maxpool_bwd_v(const void* __restrict__ dy, const uint8_t* __restrict__ am,
+                                                     void* __restrict__ dx, ConvGeom g, be_dtype dt, float beta,
+                                                     I nvec) {
+  const I stride = (I)gridDim.x * blockDim.x;
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    int n, h, w, cv;
+    nhwc8(i, g, g.H, g.W, n, h, w, cv);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int p_lo = max(0, (h + g.pad - g.R + g.stride) / g.stride);
     const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
     const int q_lo = max(0, (w + g.pad - g.S + g.stride) / g.stride);
     const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
-    for (int p = p_lo; p <= p_hi; ++p) {
-      const int r = h - (p * g.stride - g.pad);
-      if (r < 0 || r >= g.R) continue;
-      for (int q = q_lo; q <= q_hi; ++q) {
-        const int u = w - (q * g.stride - g.pad);
-        if (u < 0 || u >= g.S) continue;
-        const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
-        const uint2 packed = *reinterpret_cast<const uint2*>(am + o);
-        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&packed);
-        V8 d = ld8(dy, o, dt);
-        const int widx = r * g.S + u;
+    if (TWO) {
+      uint2 pk[4];
+      V8 d[4];
+      int widx[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += pb[j] == widx ? d.v[j] : 0.f;
+      for (int c = 0; c < 4; ++c) {
+        const int p = p_lo + (c >> 1), q = q_lo + (c & 1);
+        widx[c] = -1;
+        if (p <= p_hi && q <= q_hi) {
+          const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
+          pk[c] = *reinterpret_cast<const uint2*>(am + o);
+          d[c] = ld8(dy, o, dt);
+          widx[c] = (h - (p * g.stride - g.pad)) * g.S + (w - (q * g.stride - g.pad));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (widx[c] < 0) continue;
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&pk[c]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += pb[j] == widx[c] ? d[c].v[j] : 0.f;
+      }
+    } else {
+      for (int p = p_lo; p <= p_hi; ++p) {
+        const int r = h - (p * g.stride - g.pad);
+        for (int q = q_lo; q <= q_hi; ++q) {
+          const int u = w - (q * g.stride - g.pad);
+          const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
+          const uint2 packed = *reinterpret_cast<const uint2*>(am + o);
+          const uint8_t* pb = reinterpret_cast<const uint8_t*>(&packed);
+          V8 d = ld8(dy, o, dt);
+          const int widx = r * g.S + u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += pb[j] == widx ? d.v[j] : 0.f;
+        }
       }
     }
     V8 o2;
-    if (beta != 0.f) o2 = ld8(dx, i * 8, dt);
+    if (beta != 0.f) o2 = ld8(dx, (int64_t)i * 8, dt);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o2.v[j] = acc[j] + (beta != 0.f ? o2.v[j] : 0.f);
-    st8(dx, i * 8, dt, o2);
+    st8(dx, (int64_t)i * 8, dt, o2);
   }
 }
 
@@ -880,29 +937,32 @@ __global__ void slice_kernel(const void* y, int64_t ldy, int64_t col0, int64_t w
 }
 }  // namespace
 
+template <typename T, int VEC>
+static void im2col_launch(const void* x, void* cols, int64_t ldc, const ConvGeom& g, int64_t total, cudaStream_t s) {
+  const int grid = grid_for(total, UNR);
+  if (total < (1LL << 31))
+    im2col_kernel<T, VEC, uint32_t><<<grid, 256, 0, s>>>((const T*)x, (T*)cols, ldc, g, (uint32_t)total);
+  else
+    im2col_kernel<T, VEC, int64_t><<<grid, 256, 0, s>>>((const T*)x, (T*)cols, ldc, g, total);
+}
 void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t M = (int64_t)g.N * g.P * g.Q;
   if (M == 0) return;
-  if (dt == BE_BF16 && g.C % 8 == 0) {
-    const int64_t total = M * g.R * g.S * (g.C / 8);
-    im2col_kernel<uint16_t, 8><<<grid_for(total), 256, 0, s>>>((const uint16_t*)x, (uint16_t*)cols, ldc, g, total);
-  } else if (dt == BE_F32 && g.C % 4 == 0) {
-    const int64_t total = M * g.R * g.S * (g.C / 4);
-    im2col_kernel<float, 4><<<grid_for(total), 256, 0, s>>>((const float*)x, (float*)cols, ldc, g, total);
-  } else if (dt == BE_BF16) {
-    const int64_t total = M * g.R * g.S * g.C;
-    im2col_kernel<uint16_t, 1><<<grid_for(total), 256, 0, s>>>((const uint16_t*)x, (uint16_t*)cols, ldc, g, total);
-  } else {
-    const int64_t total = M * g.R * g.S * g.C;
-    im2col_kernel<float, 1><<<grid_for(total), 256, 0, s>>>((const float*)x, (float*)cols, ldc, g, total);
-  }
+  const int64_t taps = M * g.R * g.S;
+  if (dt == BE_BF16 && g.C % 8 == 0) im2col_launch<uint16_t, 8>(x, cols, ldc, g, taps * (g.C / 8), s);
+  else if (dt == BE_F32 && g.C % 4 == 0) im2col_launch<float, 4>(x, cols, ldc, g, taps * (g.C / 4), s);
+  else if (dt == BE_BF16) im2col_launch<uint16_t, 1>(x, cols, ldc, g, taps * g.C, s);
+  else im2col_launch<float, 1>(x, cols, ldc, g, taps * g.C, s);
   after_launch("im2col");
 }
 void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtype dt, float beta, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
   if (g.C % 8 == 0 && ldc % 8 == 0 && aligned16(dcols) && aligned16(dx)) {
-    col2im_v<<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, total / 8, dt);
+    if (total / 8 < (1LL << 31))
+      col2im_v<uint32_t><<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, (uint32_t)(total / 8), dt);
+    else
+      col2im_v<int64_t><<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, total / 8, dt);
     after_launch("col2im_v");
     return;
   }
@@ -928,7 +988,10 @@ void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtyp
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.C;
   if (total == 0) return;
   if (g.C % 8 == 0 && aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
-    maxpool_fwd_v<<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, total / 8);
+    if (total / 8 < (1LL << 31))
+      maxpool_fwd_v<uint32_t><<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, (uint32_t)(total / 8));
+    else
+      maxpool_fwd_v<int64_t><<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, total / 8);
     after_launch("maxpool_fwd_v");
     return;
   }
@@ -940,7 +1003,15 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
   if (g.C % 8 == 0 && aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
-    maxpool_bwd_v<<<grid_for(total / 8), 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
+    const bool two = g.R <= 2 * g.stride && g.S <= 2 * g.stride;
+    const int grid = grid_for(total / 8);
+    if (total / 8 < (1LL << 31)) {
+      if (two) maxpool_bwd_v<uint32_t, true><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
+      else maxpool_bwd_v<uint32_t, false><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
+    } else {
+      if (two) maxpool_bwd_v<int64_t, true><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
+      else maxpool_bwd_v<int64_t, false><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
+    }
     after_launch("maxpool_bwd_v");
     return;
   }

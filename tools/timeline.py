@@ -12,8 +12,16 @@ be.init(0)
 be.set_compute_dtype(cfg["dtype"])
 model = bench.make_model(cfg, be)
 hb = bench.host_batch(cfg, 1)
-batch = [be.tensor(a, dtype="bf16") if (i == 0 and cfg["net"] == "mlp" and cfg["dtype"] == "bf16") else be.tensor(a)
-         for i, a in enumerate(hb)]
+batch = []
+for i, a in enumerate(hb):
+    if i == 0 and cfg["net"] != "ncf" and cfg["dtype"] == "bf16":  # bf16 bits (bench.py's dev_batch)
+        t = be.empty(a.shape, "bf16")
+        be.api.call("be_tensor_copy_from_host_async", t.handle, a.ctypes.data_as(__import__("ctypes").c_void_p),
+                    a.nbytes)
+        batch.append(t)
+    else:
+        batch.append(be.tensor(a))
+be.synchronize()
 step = lambda: be.nn.train_step(model, batch, lr=0.01, momentum=0.9, weight_decay=1e-4,  # noqa: E731
                                 overlap_sgd=mode == "overlap")
 for _ in range(15):
