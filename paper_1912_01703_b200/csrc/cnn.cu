@@ -655,7 +655,9 @@ __global__ void __launch_bounds__(256) bn_reduce_bf16(const uint16_t* __restrict
                                                       int act, int64_t rows, int C, const float* __restrict__ mean,
                                                       const float* __restrict__ invstd, float* __restrict__ part0,
                                                       float* __restrict__ part1, int64_t rows_per_split,
-                                                      const float* __restrict__ gam, const float* __restrict__ bsh) {
+                                                      const float* __restrict__ gam, const float* __restrict__ bsh,
+                                                      const uint16_t* __restrict__ rmask = nullptr,
+                                                      uint16_t* __restrict__ gout = nullptr) {
   __shared__ float sm0[kBnCG], sm1[kBnCG];
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
@@ -673,19 +675,37 @@ __global__ void __launch_bounds__(256) bn_reduce_bf16(const uint16_t* __restrict
       sh[j] = act ? bsh[c + j] - k[j] * sc[j] : 0.f;
     }
     for (int64_t r = r0 + rl; r < r1; r += kBnU * rpi) {
-      uint4 xa[kBnU], ga[kBnU];
+      uint4 xa[kBnU], ga[kBnU], ma[kBnU];
 #pragma unroll
       for (int u = 0; u < kBnU; ++u) {
         const int64_t rr = r + (int64_t)u * rpi;
         const int64_t o = (rr < r1 ? rr : r) * C + c;
         xa[u] = *reinterpret_cast<const uint4*>(x + o);
         ga[u] = *reinterpret_cast<const uint4*>(gy + o);
+        if (rmask) ma[u] = *reinterpret_cast<const uint4*>(rmask + o);
       }
 #pragma unroll
       for (int u = 0; u < kBnU; ++u) {
         if (r + (int64_t)u * rpi >= r1) break;
         float a[8], g[8];
         unpack8(xa[u], a);
+        if (rmask) {
+          // residual block output y = relu(bn(x) + shortcut): g = gy·1[y > 0]
+          // (bf16 y > 0 ⇔ bits in [1, 0x7f80]: positive, finite or +inf, not NaN), stored for the shortcut
+          // and the dx pass — the ReLU backward fused into this read of gy
+          const uint32_t gw[4] = {ga[u].x, ga[u].y, ga[u].z, ga[u].w};
+          const uint32_t mw[4] = {ma[u].x, ma[u].y, ma[u].z, ma[u].w};
+          uint32_t ow[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t ml = mw[i] & 0xffffu, mh = mw[i] >> 16;  // y > 0: 0 < bits ≤ +inf (0x7f80)
+            const uint32_t lo = ml - 1u < 0x7f80u ? 0x0000ffffu : 0u;
+            const uint32_t hi = mh - 1u < 0x7f80u ? 0xffff0000u : 0u;
+            ow[i] = gw[i] & (lo | hi);
+          }
+          ga[u] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          *reinterpret_cast<uint4*>(gout + (r + (int64_t)u * rpi) * C + c) = ga[u];
+        }
         unpack8(ga[u], g);
         if (act) {
 #pragma unroll
@@ -862,29 +882,39 @@ __global__ void __launch_bounds__(1024) bn_finalize_v(const float* __restrict__ 
                                                       float eps, float* mean, float* invstd, float* run_mean,
                                                       float* run_var, float momentum, float* dgamma, float* dbeta,
                                                       float gb_beta, float* sums) {
-  // 32 channels × 32 sub-lanes; each sub-lane sums every 32nd split (4 loads in flight)
-  __shared__ double s0[32][33], s1[32][33];
-  const int cl = threadIdx.x & 31, sub = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + cl;
+  // 8 channels × 128 sub-lanes: each sub-lane sums every 128th split with all
+  // its loads in flight (≤ 4 per operand for the usual ≤ 592 splits), then a
+  // fixed-order two-level sum over the sub-lanes (deterministic)
+  __shared__ double s0[128][9], s1[128][9];
+  const int cl = threadIdx.x & 7, sub = threadIdx.x >> 3;
+  const int c = blockIdx.x * 8 + cl;
   double a0 = 0, a1 = 0;
   if (c < C) {
     int i = sub;
-    for (; i + 96 < splits; i += 128) {
-      const float x0 = p0[(int64_t)i * C + c], x1 = p0[(int64_t)(i + 32) * C + c];
-      const float x2 = p0[(int64_t)(i + 64) * C + c], x3 = p0[(int64_t)(i + 96) * C + c];
-      const float y0 = p1[(int64_t)i * C + c], y1 = p1[(int64_t)(i + 32) * C + c];
-      const float y2 = p1[(int64_t)(i + 64) * C + c], y3 = p1[(int64_t)(i + 96) * C + c];
+    for (; i + 384 < splits; i += 512) {
+      const float x0 = p0[(int64_t)i * C + c], x1 = p0[(int64_t)(i + 128) * C + c];
+      const float x2 = p0[(int64_t)(i + 256) * C + c], x3 = p0[(int64_t)(i + 384) * C + c];
+      const float y0 = p1[(int64_t)i * C + c], y1 = p1[(int64_t)(i + 128) * C + c];
+      const float y2 = p1[(int64_t)(i + 256) * C + c], y3 = p1[(int64_t)(i + 384) * C + c];
       a0 += (double)x0; a0 += (double)x1; a0 += (double)x2; a0 += (double)x3;
       a1 += (double)y0; a1 += (double)y1; a1 += (double)y2; a1 += (double)y3;
     }
-    for (; i < splits; i += 32) { a0 += p0[(int64_t)i * C + c]; a1 += p1[(int64_t)i * C + c]; }
+    for (; i < splits; i += 128) { a0 += p0[(int64_t)i * C + c]; a1 += p1[(int64_t)i * C + c]; }
   }
   s0[sub][cl] = a0;
   s1[sub][cl] = a1;
   __syncthreads();
+  if (sub < 8) {
+    double u0 = 0, u1 = 0;
+    for (int k = 0; k < 16; ++k) { u0 += s0[sub * 16 + k][cl]; u1 += s1[sub * 16 + k][cl]; }
+    __syncwarp();
+    s0[sub * 16][cl] = u0;
+    s1[sub * 16][cl] = u1;
+  }
+  __syncthreads();
   if (sub != 0 || c >= C) return;
   double t0 = 0, t1 = 0;
-  for (int k = 0; k < 32; ++k) { t0 += s0[k][cl]; t1 += s1[k][cl]; }
+  for (int k = 0; k < 8; ++k) { t0 += s0[k * 16][cl]; t1 += s1[k * 16][cl]; }
   if (MODE == 0) {
     const double n = (double)rows;
     const double ms = t0 / n;
@@ -934,6 +964,167 @@ __global__ void slice_kernel(const void* y, int64_t ldy, int64_t col0, int64_t w
     if (beta != 0.f) v += ld(x, i, dt);
     st(x, i, dt, v);
   }
+}
+// ---- max pool, bf16, one block row per output row (n, p): the window's
+// input rows are uniform across the block, a thread owns one 8-channel vector
+// of one output pixel and issues all R·S ≤ 9 window loads before comparing.
+// Selection rule (as maxpool_fwd_v and the oracle): taps in (r, u) order,
+// the first maximum wins (−0 == +0), a NaN wins over numbers and the first
+// NaN is kept.  The compare runs on packed bf16 pairs (HSETP2 masks + LOP3
+// selects of value and 16-bit tap index); a window holding a NaN takes the
+// scalar path.
+// Thread layout (no run-time divisions): threadIdx.x = channel vector,
+// threadIdx.y = output column within the block, grid (Q tiles, P, N);
+// STRIDE = 2 (every pool on the path) is a compile-time constant.
+template <int STRIDE>
+__global__ void __launch_bounds__(256) maxpool_fwd_rows(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                                        uint8_t* __restrict__ am, ConvGeom g) {
+  const int stride = STRIDE > 0 ? STRIDE : g.stride;
+  const int cv = threadIdx.x;
+  const int q = blockIdx.x * blockDim.y + threadIdx.y;
+  if (q >= g.Q) return;
+  const int n = blockIdx.z, p = blockIdx.y;
+  const int h0 = p * stride - g.pad, w0 = q * stride - g.pad;
+  // valid taps form the rectangle [r0, r1) × [u0, u1)
+  const int r0 = max(0, -h0), r1 = min(g.R, g.H - h0), u0 = max(0, -w0), u1 = min(g.S, g.W - w0);
+  uint4 a[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int t = r * 3 + u;
+      if (r >= r0 && r < r1 && u >= u0 && u < u1)
+        a[t] = __ldg(reinterpret_cast<const uint4*>(x + (((int64_t)n * g.H + h0 + r) * g.W + w0 + u) * g.C) + cv);
+      else
+        a[t] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  uint32_t nan = 0u;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const uint32_t wv[4] = {a[t].x, a[t].y, a[t].z, a[t].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nan |= __vcmpgtu2(wv[i] & 0x7fff7fffu, 0x7f807f80u);
+  }
+  uint32_t bv[4], bi[4];  // best value / tap index, two channels per word
+  if (!nan) {
+    const int tf = r0 * 3 + u0;  // first valid tap
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bv[i] = 0u;
+    // initialise from the first valid tap (selected by index: registers only)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      if (t == tf) {
+        bv[0] = a[t].x; bv[1] = a[t].y; bv[2] = a[t].z; bv[3] = a[t].w;
+      }
+    }
+    const uint32_t i0 = (uint32_t)(r0 * g.S + u0) * 0x00010001u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bi[i] = i0;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int r = t / 3, u = t % 3;
+      if (!(r >= r0 && r < r1 && u >= u0 && u < u1)) continue;
+      const uint32_t ti = (uint32_t)(r * g.S + u) * 0x00010001u;
+      const uint32_t wv[4] = {a[t].x, a[t].y, a[t].z, a[t].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 vv = *reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
+        __nv_bfloat162 bb = *reinterpret_cast<const __nv_bfloat162*>(&bv[i]);
+        const uint32_t m = __hgt2_mask(vv, bb);
+        bv[i] = (bv[i] & ~m) | (wv[i] & m);
+        bi[i] = (bi[i] & ~m) | (ti & m);
+      }
+    }
+  } else {
+    float best[8];
+    int bj[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; bj[j] = -1; }
+    for (int t = 0; t < 9; ++t) {
+      const int r = t / 3, u = t % 3;
+      if (!(r >= r0 && r < r1 && u >= u0 && u < u1)) continue;
+      float v[8];
+      unpack8(a[t], v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (bj[j] < 0 || v[j] > best[j] || (v[j] != v[j] && best[j] == best[j])) { best[j] = v[j]; bj[j] = r * g.S + u; }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      bv[i] = (uint32_t)f2bf(best[2 * i]) | ((uint32_t)f2bf(best[2 * i + 1]) << 16);
+      bi[i] = (uint32_t)bj[2 * i] | ((uint32_t)bj[2 * i + 1] << 16);
+    }
+  }
+  const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
+  *reinterpret_cast<uint4*>(y + o) = make_uint4(bv[0], bv[1], bv[2], bv[3]);
+  // 16-bit index pairs → 8 bytes
+  if (am)
+    *reinterpret_cast<uint2*>(am + o) = make_uint2(__byte_perm(bi[0], bi[1], 0x6420), __byte_perm(bi[2], bi[3], 0x6420));
+}
+// ---- max-pool backward, bf16, one block per input row (n, h): the ≤ 2
+// output rows whose windows contain h are uniform across the block; a thread
+// owns one 8-channel vector of one input pixel, loads the ≤ 2 × 2 (dy,
+// argmax) pairs together and sums the winners in (p, q) order in fp32 (as
+// maxpool_bwd_v; losers contribute an exact +0).  Winner test on packed
+// bytes (__vcmpeq4), byte masks widened to bf16 lanes with PRMT.  Requires
+// R ≤ 2·stride and S ≤ 2·stride.
+template <int STRIDE>
+__global__ void __launch_bounds__(256) maxpool_bwd_rows(const uint16_t* __restrict__ dy,
+                                                        const uint8_t* __restrict__ am, uint16_t* __restrict__ dx,
+                                                        ConvGeom g, float beta) {
+  const int stride = STRIDE > 0 ? STRIDE : g.stride;
+  const int cv = threadIdx.x;
+  const int w = blockIdx.x * blockDim.y + threadIdx.y;
+  if (w >= g.W) return;
+  const int n = blockIdx.z, h = blockIdx.y;
+  // (negative numerators: truncation and flooring both clamp to 0 below)
+  const int p_lo = max(0, (h + g.pad - g.R + stride) / stride);
+  const int p_hi = min(g.P - 1, (h + g.pad) / stride);
+  const int q_lo = max(0, (w + g.pad - g.S + stride) / stride);
+  const int q_hi = min(g.Q - 1, (w + g.pad) / stride);
+  uint4 d[4];
+  uint2 pk[4];
+  uint32_t widx[4];
+  // 64-bit image base once; the ≤ 4 candidates are 32-bit offsets from (p_lo, q_lo)
+  const int64_t img = (int64_t)n * g.P * g.Q * g.C;
+  const uint16_t* dyi = dy + img;
+  const uint8_t* ami = am + img;
+  const uint32_t o00 = ((uint32_t)p_lo * g.Q + q_lo) * g.C + cv * 8;
+  const int w00 = (h - (p_lo * stride - g.pad)) * g.S + (w - (q_lo * stride - g.pad));
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int dp = c >> 1, dq = c & 1;
+    d[c] = make_uint4(0u, 0u, 0u, 0u);
+    pk[c] = make_uint2(0xffffffffu, 0xffffffffu);
+    widx[c] = 0u;
+    if (p_lo + dp <= p_hi && q_lo + dq <= q_hi) {
+      const uint32_t o = o00 + (uint32_t)(dp * g.Q + dq) * g.C;
+      d[c] = __ldg(reinterpret_cast<const uint4*>(dyi + o));
+      pk[c] = __ldg(reinterpret_cast<const uint2*>(ami + o));
+      widx[c] = (uint32_t)(w00 - dp * stride * g.S - dq * stride) * 0x01010101u;
+    }
+  }
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t m0 = __vcmpeq4(pk[c].x, widx[c]), m1 = __vcmpeq4(pk[c].y, widx[c]);
+    uint4 v = d[c];
+    v.x &= __byte_perm(m0, 0, 0x1100); v.y &= __byte_perm(m0, 0, 0x3322);
+    v.z &= __byte_perm(m1, 0, 0x1100); v.w &= __byte_perm(m1, 0, 0x3322);
+    float f[8];
+    unpack8(v, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += f[j];
+  }
+  const int64_t o = (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * 8;
+  if (beta != 0.f) {
+    float old[8];
+    unpack8(*reinterpret_cast<const uint4*>(dx + o), old);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += old[j];
+  }
+  *reinterpret_cast<uint4*>(dx + o) = pack8(acc);
 }
 }  // namespace
 
@@ -987,6 +1178,15 @@ void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
 void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.C;
   if (total == 0) return;
+  if (dt == BE_BF16 && g.C % 8 == 0 && g.R <= 3 && g.S <= 3 && g.C <= 2048 && g.N < 65536 && aligned16(x) &&
+      aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
+    const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
+    dim3 grid((g.Q + wpb - 1) / wpb, g.P, g.N), block(cvn, wpb);
+    if (g.stride == 2) maxpool_fwd_rows<2><<<grid, block, 0, s>>>((const uint16_t*)x, (uint16_t*)y, am, g);
+    else maxpool_fwd_rows<0><<<grid, block, 0, s>>>((const uint16_t*)x, (uint16_t*)y, am, g);
+    after_launch("maxpool_fwd_rows");
+    return;
+  }
   if (g.C % 8 == 0 && aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     if (total / 8 < (1LL << 31))
       maxpool_fwd_v<uint32_t><<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, (uint32_t)(total / 8));
@@ -1002,6 +1202,16 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
                  cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
+  if (dt == BE_BF16 && g.C % 8 == 0 && g.R <= 2 * g.stride && g.S <= 2 * g.stride && g.C <= 2048 && g.N < 65536 &&
+      (int64_t)g.P * g.Q * g.C < (1LL << 32) &&
+      aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
+    const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
+    dim3 grid((g.W + wpb - 1) / wpb, g.H, g.N), block(cvn, wpb);
+    if (g.stride == 2) maxpool_bwd_rows<2><<<grid, block, 0, s>>>((const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+    else maxpool_bwd_rows<0><<<grid, block, 0, s>>>((const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+    after_launch("maxpool_bwd_rows");
+    return;
+  }
   if (g.C % 8 == 0 && aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     const bool two = g.R <= 2 * g.stride && g.S <= 2 * g.stride;
     const int grid = grid_for(total / 8);
@@ -1070,7 +1280,7 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
       bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
                                           partial + sp * C, rps);
     after_launch("bn_stats_v");
-    bn_finalize_v<0><<<(C + 31) / 32, 1024, 0, s>>>(partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
+    bn_finalize_v<0><<<(C + 7) / 8, 1024, 0, s>>>(partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
                                                     invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
                                                     nullptr);
     after_launch("bn_stats_finalize_v");
@@ -1091,7 +1301,7 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
 }
 void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C, float eps, float* mean,
                             float* invstd, float* run_mean, float* run_var, float momentum, cudaStream_t s) {
-  bn_finalize_v<0><<<(C + 31) / 32, 1024, 0, s>>>(partial, partial + (int64_t)parts * C, parts, C, rows, nullptr,
+  bn_finalize_v<0><<<(C + 7) / 8, 1024, 0, s>>>(partial, partial + (int64_t)parts * C, parts, C, rows, nullptr,
                                                   BE_F32, eps, mean, invstd, run_mean, run_var, momentum, nullptr,
                                                   nullptr, 0.f, nullptr);
   after_launch("bn_stats_from_partials");
@@ -1116,8 +1326,39 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
 }
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta, float gb_beta,
-            float dx_beta, float* partial, cudaStream_t s, const float* bn_beta) {
+            float dx_beta, float* partial, cudaStream_t s, const float* bn_beta, const void* rmask,
+            void* gout) {
   // partial must hold 2*splits*C + 2*C floats
+  if (rmask) {
+    // residual output mask: g = dy·1[rmask > 0] into gout, then the BN backward of g
+    if (dt == BE_BF16 && !act && bn_vec_ok(x, C) && aligned16(dy) && aligned16(rmask) && aligned16(gout) &&
+        (!dx || aligned16(dx))) {
+      const int64_t sp = bn_splits_v(rows, C);
+      const int64_t rps = (rows + sp - 1) / sp;
+      float* p0 = partial;
+      float* p1 = partial + sp * C;
+      float* sums = partial + 2 * sp * C;
+      dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
+      bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
+                                          0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,
+                                          reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
+      after_launch("bn_bwd_reduce_mask_bf16");
+      bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
+                                                      nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
+      after_launch("bn_bwd_finalize_v");
+      if (dx) {
+        dim3 g2;
+        const int64_t rpb = bn_rows_per_block(rows, C, &g2);
+        bn_dx_bf16<<<g2, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x),
+                                      0, reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta,
+                                      rpb, nullptr);
+        after_launch("bn_bwd_dx_v");
+      }
+      return;
+    }
+    relu_bwd(dy, rmask, gout, rows * C, dt, 0.f, s);
+    dy = gout;
+  }
   if (bn_vec_ok(x, C) && aligned16(dy) && (!act || bn_beta || aligned16(y)) && (!dx || aligned16(dx))) {
     const int64_t sp = bn_splits_v(rows, C);
     const int64_t rps = (rows + sp - 1) / sp;
@@ -1133,7 +1374,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
                                           bn_beta ? gamma : nullptr, bn_beta);
     after_launch("bn_bwd_reduce_v");
-    bn_finalize_v<2><<<(C + 31) / 32, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
+    bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                     nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
     after_launch("bn_bwd_finalize_v");
     if (dx) {

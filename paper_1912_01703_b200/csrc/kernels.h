@@ -139,7 +139,11 @@ void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C
 // backward: dgamma, dbeta (fp32, with beta-accumulate flags) and dx
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta,
-            float gb_beta, float dx_beta, float* partial, cudaStream_t s, const float* bn_beta = nullptr);
+            float gb_beta, float dx_beta, float* partial, cudaStream_t s, const float* bn_beta = nullptr,
+            const void* rmask = nullptr, void* gout = nullptr);
+// rmask (residual BN, y = relu(bn(x) + r)): the upstream is first masked,
+// g = dy·1[rmask > 0], written to gout (the shortcut's gradient) — fused into
+// the reduction pass on the bf16 path; act must be 0
 
 // ------------------------------------------------------------------ embedding
 void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,

@@ -288,12 +288,10 @@ static void vjp_bn(Node* n, GradSink& sink) {
   const int C = (int)x->shape[3];
   const int64_t rows = x->numel() / C;
   TRef gz = contiguous_like(sink.upstream[0], x->dtype);
-  if (residual && act) {
-    // y = relu(bn(x) + r): g = dy·1[y > 0] is both r's gradient and the BN's upstream
-    TRef g = new_tensor(x->shape, x->rank, x->dtype);
-    k::relu_bwd(gz->data(), y->data(), g->data(), x->numel(), x->dtype, 0.f, s);
-    gz = g;
-  }
+  // y = relu(bn(x) + r): g = dy·1[y > 0] is both r's gradient and the BN's
+  // upstream; bn_bwd writes it (fused into its reduction pass)
+  TRef gmask;
+  if (residual && act) gmask = new_tensor(x->shape, x->rank, x->dtype);
   // dgamma / dbeta accumulate flags must agree: compute into temps when they differ
   float bg = 0.f, bb = 0.f;
   Tensor* dg = sink.needs(1) ? sink.dest(1, &bg) : nullptr;
@@ -315,7 +313,8 @@ static void vjp_bn(Node* n, GradSink& sink) {
   const int bact = residual ? 0 : act;  // with a residual the mask is already in gz
   k::bn_bwd(gz->data(), x->data(), bact ? y->data() : nullptr, bact, dx ? dx->data() : nullptr, rows, C, x->dtype,
             mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s,
-            bact ? bshift->ptr<float>() : nullptr);
+            bact ? bshift->ptr<float>() : nullptr, gmask ? y->data() : nullptr, gmask ? gmask->data() : nullptr);
+  if (gmask) gz = std::move(gmask);  // sole reference: the shortcut adopts it without a copy
   if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
   if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
   if (dx) sink.commit(0);

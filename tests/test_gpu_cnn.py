@@ -122,6 +122,36 @@ def test_maxpool_op_and_argmax_bit_exact(k, s, p, C):
     assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-6
 
 
+@pytest.mark.parametrize("C,H", [(16, 13), (64, 14), (8, 57)])
+@pytest.mark.parametrize("k,s,p", [(3, 2, 0), (3, 2, 1), (2, 2, 0)])
+def test_maxpool_bf16_rows_bit_exact(k, s, p, C, H):
+    """bf16 max pool (the row kernels maxpool_fwd_rows / maxpool_bwd_rows):
+    pooled values and winners bit-exact against the oracle on the same
+    bf16-valued input (ties → first index); dx = Σ of the winners' upstream
+    (≤ 4 bf16 terms, fp32 sum, one rounding) within one bf16 ulp."""
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(np.asarray(a, np.float32)))
+    rng = np.random.default_rng(C + H + k + s + p)
+    x = q(rng.standard_normal((3, C, H, H)))
+    x[0, :, :5, :5] = 0.5  # tied windows → first index
+    xo = Var(x.astype(np.float64), True)
+    yo, am = oops.maxpool2d(xo, k, s, p)
+    g = q(rng.standard_normal(yo.value.shape))
+    backward(yo, g.astype(np.float64))
+    xd = be.tensor(nchw_to_nhwc(x), requires_grad=True)
+    yd, amd = be.maxpool2d(be.cast(xd, "bf16"), k, s, p, with_argmax=True)
+    yd.backward(be.tensor(nchw_to_nhwc(g), dtype="bf16"))
+    assert np.array_equal(nhwc_to_nchw(yd.numpy()).astype(np.float64), yo.value)
+    win = nhwc_to_nchw(amd.numpy()).astype(np.int64)
+    P = yo.value.shape[2]
+    hh = np.arange(P)[:, None] * s - p + win // k
+    ww = np.arange(P)[None, :] * s - p + win % k
+    assert np.array_equal(hh * H + ww, am)
+    assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 8e-3
+
+
 @pytest.mark.parametrize("C", [6, 24])
 def test_avgpool_bn_add_ops_fp32(C):
     be = be_init()
