@@ -85,6 +85,11 @@ struct __align__(64) GemmParams {
   // epilogue): partial rows [gridDim.x·4][N] (Σ) then [gridDim.x·4][N] (Σx²);
   // row = CTA·4 + TMEM lane quarter; zeroed by the host before the launch
   float* stats;
+  // phase-split patch convolution (conv_stem_kernel): L columns per phase,
+  // phase block bytes, taps per (phase, row) padded even, patch buffers,
+  // weight bytes
+  int st_L, st_phb, st_taps, st_nbuf, st_wbytes;
+  const uint16_t* st_w;       // KRSC weights (C = 8), copied into smem by every CTA
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
@@ -306,7 +311,7 @@ __device__ __forceinline__ void epi_sgd32(const GemmParams& p, uint8_t* buf, int
 // (the store issued from a buffer two chunks earlier must have read it), one
 // 4 KB buffer for fp32.
 __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf, int& slot, int lane, int store_row,
-                                          int col0, const uint32_t (&r)[32]) {
+                                          int col0, const uint32_t (&r)[32], int z = -1) {
   uint8_t* buf = warp_buf;
   if (p.d_f32) {
     if (lane == 0) sm100::bulk_wait_read<0>();
@@ -353,8 +358,14 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
   sm100::fence_proxy_async();
   __syncwarp();
   if (lane == 0) {
-    if (p.tma_store == 2) sm100::tma_reduce_add_2d(&p.td, buf, col0, store_row);  // beta = 1
-    else sm100::tma_store_2d(&p.td, buf, col0, store_row);
+    if (z >= 0) {  // 3-D map (col, row, z)
+      if (p.tma_store == 2) sm100::tma_reduce_add_3d(&p.td, buf, col0, store_row, z);
+      else sm100::tma_store_3d(&p.td, buf, col0, store_row, z);
+    } else if (p.tma_store == 2) {
+      sm100::tma_reduce_add_2d(&p.td, buf, col0, store_row);  // beta = 1
+    } else {
+      sm100::tma_store_2d(&p.td, buf, col0, store_row);
+    }
     sm100::bulk_commit();
   }
   slot ^= 1;
@@ -1364,6 +1375,209 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
   }
 }
 
+// ---------------------------------------------------------------- strided small-C convolution from a phase-split patch
+// The stem convolutions (ResNet conv1 7×7/2) have C = 8 (channel-padded
+// image) and stride st > 1: a 16-B gather per tap and output pixel uses half
+// of every L2 sector and moves the 49 taps' worth of input per pixel through
+// L2 (conv_small_c_kernel: L2-bound, 945 µs at b256).
+// Here one tile is one output row (n, p) of Q ≤ 128 pixels (MMA rows ≥ Q are
+// discarded).  Its input patch — R input rows × the columns the row's
+// windows touch — is copied ONCE (coalesced 16-B cp.async along w, 4 copy
+// warps), split by column phase φ = (w + pad) mod st: phase φ holds L
+// columns j ↔ w = j·st + φ − pad as [r][j][8 channels] (16-B rows, zero-
+// filled padding).  For tap (r, s) the A rows of output pixels q = 0,1,… are
+// then CONSECUTIVE 16-B rows of phase s mod st starting at column ⌊s/st⌋,
+// i.e. exactly a K-major SWIZZLE_NONE UMMA operand (8 contiguous 16-B rows
+// per core matrix, SBO = 128 B): the MMA reads A straight from the patch,
+// no im2col anywhere.  A K = 16 MMA covers two taps (its two core matrices
+// along K are LBO apart): the taps of each (φ, r) are padded to an even count
+// T (zero weights) so pair j of row (φ, r) is A = row base + 32·j with
+// LBO = 16 and B = its weights + 2·j KB with LBO = 1 KB — descriptors are
+// the row bases plus constants.  The weights sit in smem for the whole
+// persistent CTA as [φ][r][T][k][8].  An N = 64 MMA runs 32 cycles, shorter
+// than one thread's descriptor/issue chain, so two warps issue MMAs for
+// alternate tiles into the two TMEM accumulators.  Output rows t·Q + q;
+// epilogue as conv_small_c_kernel.
+namespace stem {
+constexpr int kThreads = 512;   // w0-3 patch copy (cp.async), w4-5 MMA, w6 TMEM, w8-15 epilogue
+constexpr int kCopyThreads = 128;
+constexpr int LAG = 3;          // cp.async groups (tiles) in flight per copy thread
+constexpr int BN = 64;          // output channels (the stems' K)
+constexpr int kZeroBytes = 4096;  // past the last patch buffer: discarded rows' overrun lands in zeros
+constexpr int kSmemCap = 227 * 1024;
+}  // namespace stem
+
+__global__ void __launch_bounds__(stem::kThreads, 1) conv_stem_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nbuf = p.st_nbuf, st = p.cstride, R = p.cR, S = p.cS, L = p.st_L, T = p.st_taps;
+  const int patch_bytes = st * p.st_phb;
+  uint8_t* wsm = smem;                                   // [φ][r][T][BN][16 B]
+  uint8_t* patch = wsm + p.st_wbytes;                    // nbuf × patch_bytes
+  uint8_t* zero = patch + nbuf * patch_bytes;
+  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(        // 8 warps × 4 KB TMA-store staging (swizzle-aligned)
+      (reinterpret_cast<uintptr_t>(zero + stem::kZeroBytes) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
+  uint64_t* empty = full + nbuf;
+  uint64_t* tfull = empty + nbuf;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // weights (zeros for the padded taps s ≥ S); patch buffers and the zero
+  // block zeroed once (phase-block gaps are never written, and padded taps /
+  // discarded rows read them: must be finite)
+  for (int idx = threadIdx.x; idx < st * R * T * stem::BN; idx += blockDim.x) {
+    const int n = idx % stem::BN, sj = (idx / stem::BN) % T, r = (idx / (stem::BN * T)) % R;
+    const int ph = idx / (stem::BN * T * R);
+    const int s = sj * st + ph;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (s < S) v = __ldg(reinterpret_cast<const uint4*>(p.st_w + ((long long)(n * R + r) * S + s) * 8));
+    *reinterpret_cast<uint4*>(wsm + idx * 16) = v;
+  }
+  for (int i = threadIdx.x; i < (nbuf * patch_bytes + stem::kZeroBytes) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(patch)[i] = make_uint4(0, 0, 0, 0);
+  sm100::fence_proxy_async();  // generic-proxy smem writes → visible to the tensor core
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < nbuf; ++b) {
+      sm100::mbar_init(&full[b], stem::kCopyThreads);
+      sm100::mbar_init(&empty[b], 1);
+    }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 6) sm100::tmem_alloc<2 * stem::BN>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.cN * p.cP;
+
+  if (warp < 4) {
+    // ===================== patch copy: 16-B cp.async per (input row r, column w) =====================
+    // each thread owns columns u = tid and tid + 128 of the span (≤ 256):
+    // their phase offsets / bounds are tile-invariant, so the per-tile loop
+    // is one row address + two predicated cp.async per input row
+    const int tid = threadIdx.x;
+    const int span = L * st;
+    const int ua = tid, ub = tid + stem::kCopyThreads;
+    const int wa = ua - p.cpad, wb = ub - p.cpad;
+    const bool va = ua < span, vb = ub < span;
+    const bool oka = va && (unsigned)wa < (unsigned)p.cW, okb = vb && (unsigned)wb < (unsigned)p.cW;
+    const uint32_t da = (ua % st) * p.st_phb + (ua / st) * 16, db = (ub % st) * p.st_phb + (ub / st) * 16;
+    const long long xa = oka ? (long long)wa * 8 : 0, xb = okb ? (long long)wb * 8 : 0;
+    const uint32_t L16 = L * 16;
+    int b = 0; uint32_t phase = 0;
+    int pend[stem::LAG + 1];
+    int npend = 0, head = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int n = t / p.cP, pp = t - n * p.cP;
+      sm100::mbar_wait(&empty[b], phase ^ 1);
+      uint32_t dst = sm100::smem_u32(patch + b * patch_bytes);
+      const int h0 = pp * st - p.cpad;
+      const uint16_t* img = p.x + (long long)n * p.cH * p.cW * 8;
+      for (int r = 0; r < R; ++r, dst += L16) {
+        const int h = h0 + r;
+        const bool hok = (unsigned)h < (unsigned)p.cH;
+        const uint16_t* srow = img + (long long)(hok ? h : 0) * p.cW * 8;
+        if (va) sm100::cp_async_16(dst + da, hok && oka ? srow + xa : p.x, hok && oka ? 16u : 0u);
+        if (vb) sm100::cp_async_16(dst + db, hok && okb ? srow + xb : p.x, hok && okb ? 16u : 0u);
+      }
+      sm100::cp_async_commit();
+      pend[(head + npend) % (stem::LAG + 1)] = b;
+      ++npend;
+      if (npend > stem::LAG) {
+        sm100::cp_async_wait<stem::LAG>();
+        sm100::fence_proxy_async();
+        sm100::mbar_arrive(&full[pend[head]]);
+        head = (head + 1) % (stem::LAG + 1);
+        --npend;
+      }
+      if (++b == nbuf) { b = 0; phase ^= 1; }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    while (npend > 0) {
+      sm100::mbar_arrive(&full[pend[head]]);
+      head = (head + 1) % (stem::LAG + 1);
+      --npend;
+    }
+  } else if (warp == 4 || warp == 5) {
+    if (lane == 0) {
+      // ===================== MMA issuers: warp 4+k takes tiles 2i+k, accumulator k =====================
+      const int k = warp - 4;
+      const uint32_t idesc = sm100::make_idesc(1u, BM, stem::BN, 0, 0);
+      const uint64_t a0 = sm100::make_interleave_desc(sm100::smem_u32(patch), 16, 128);
+      const uint64_t b0 = sm100::make_interleave_desc(sm100::smem_u32(wsm), stem::BN * 16, 128);
+      const uint32_t rowA = (L * 16) >> 4, phA = p.st_phb >> 4;   // descriptor units (16 B)
+      const uint32_t rowB = (T * stem::BN * 16) >> 4;
+      uint32_t acc_phase = 0;
+      int ti = k;
+      for (int t = blockIdx.x + k * gridDim.x; t < num_tiles; t += 2 * gridDim.x, ti += 2) {
+        const int b = ti % nbuf;
+        sm100::mbar_wait(&tempty[k], acc_phase ^ 1);
+        sm100::mbar_wait(&full[b], (uint32_t)(ti / nbuf) & 1u);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + k * stem::BN;
+        uint64_t ad = a0 + (uint64_t)((b * patch_bytes) >> 4), bd = b0;
+        uint32_t accum = 0;
+        for (int ph = 0; ph < st; ++ph) {
+          for (int r = 0; r < R; ++r) {
+            for (int j = 0; j < T / 2; ++j) {
+              sm100::mma_bf16(d_tmem, ad + 2 * j, bd + 128 * j, idesc, accum);
+              accum = 1;
+            }
+            ad += rowA; bd += rowB;
+          }
+          ad += phA - R * rowA;
+        }
+        sm100::mma_commit(&empty[b]);
+        sm100::mma_commit(&tfull[k]);
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue: warp (quarter eq, column half eh) =====================
+    const int ew = warp - 8;
+    const int eq = warp & 3, eh = ew >> 2;
+    int acc = 0; uint32_t acc_phase = 0;
+    int slot = 0;
+    ColStats<1> cst;
+    cst.reset();
+    const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    const int qrow = eq * 32 + lane;
+    const bool row_ok = qrow < p.cQ;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      uint32_t r0[32];
+      sm100::tmem_ld_32x32b_x32(tmem_base + acc * stem::BN + eh * 32 + ((uint32_t)(eq * 32) << 16), r0);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (p.stats) {
+        float s_, q_;
+        colstats32(p, r0, row_ok, lane, s_, q_);
+        cst.s[0] += s_; cst.q[0] += q_;
+      }
+      // TMA store of the warp's 32 × 32 box at (k = eh·32, q = eq·32, tile t):
+      // full 128-B lines, rows q ≥ Q clipped by the map
+      if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, slot, lane, eq * 32, eh * 32, r0, t);
+      else if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, t * p.cQ + qrow, eh * 32, r0);
+    }
+    if (p.stats) cst.flush(p, blockIdx.x * 4 + eq, eh * 32, lane, 1);
+    if (lane == 0) sm100::bulk_wait<0>();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<2 * stem::BN>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -1949,11 +2163,77 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
   return true;
 }
 
+// Phase-split patch convolution (conv_stem_kernel): C = 8, K = 64, stride
+// > 1, one output row (Q ≤ 128) per tile.  Returns false when the shape
+// does not fit (caller falls back to the gather kernel).
+static bool conv_stem(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
+                      int act, float beta, cudaStream_t s, float* stats, int* stats_parts) {
+  static const int on = [] { const char* e = getenv("BE_CONV_STEM"); return e ? atoi(e) : 1; }();
+  if (!on || g.C != 8 || g.K != stem::BN || g.stride < 2 || g.Q > BM || g.Q < 1) return false;
+  const int taps = g.R * g.S;
+  const int T = ((g.S + g.stride - 1) / g.stride + 1) / 2 * 2;  // taps per (phase, row), padded even
+  const int L = g.Q + T - 1;                                      // columns per phase (padded taps included)
+  if (L * g.stride > 2 * stem::kCopyThreads) return false;       // span: 2 columns per copy thread
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+  // phase blocks offset by 128/st bytes mod 128: a warp's 16-B copies to the
+  // st phases land in different banks
+  const int phb = (g.R * L * 16 + 127) / 128 * 128 + (128 / g.stride) / 16 * 16;
+  const int patch_bytes = g.stride * phb;
+  const int wbytes = g.stride * g.R * T * stem::BN * 16;
+  const int fixed = 2048 + stem::kZeroBytes + kEpiBytes + 256;
+  const int nbuf = std::min(6, (stem::kSmemCap - fixed - wbytes) / patch_bytes);
+  if (nbuf <= stem::LAG) return false;
+  const int smem = fixed + wbytes + nbuf * patch_bytes;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = g.N * g.P * g.Q; p.N = g.K; p.K = taps * g.C;
+  p.D = y; p.ldd = g.K; p.d_f32 = yd == BE_F32; p.beta = beta; p.bias = bias; p.act = act;
+  p.stats = (stats && !bias && !act && beta == 0.f) ? stats : nullptr;
+  p.x = reinterpret_cast<const uint16_t*>(x);
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
+  p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
+  p.st_L = L; p.st_phb = phb; p.st_taps = T; p.st_nbuf = nbuf; p.st_wbytes = wbytes;
+  p.st_w = reinterpret_cast<const uint16_t*>(w);
+  // output as 3-D [N·P tiles][Q][K]: 32 × 32 TMA-store boxes, q ≥ Q clipped
+  static const int tma_on = [] { const char* e = getenv("BE_TMA_STORE"); return e ? atoi(e) : 1; }();
+  if (tma_on && (beta == 0.f || beta == 1.f) && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+    const bool f32 = yd == BE_F32;
+    const cuuint64_t es = f32 ? 4 : 2;
+    cuuint64_t od[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Q, (cuuint64_t)g.N * g.P};
+    cuuint64_t os[2] = {(cuuint64_t)g.K * es, (cuuint64_t)g.Q * g.K * es};
+    cuuint32_t ob[3] = {32, 32, 1};
+    cuuint32_t oe[3] = {1, 1, 1};
+    EncodeFn enc = get_encode();
+    if (enc && enc(&p.td, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, od, os, ob,
+                   oe, CU_TENSOR_MAP_INTERLEAVE_NONE, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.tma_store = beta == 1.f ? 2 : 1;
+  }
+  static int attr_smem = 0;
+  if (smem > attr_smem) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stem::kSmemCap));
+    attr_smem = stem::kSmemCap;
+  }
+  const int tiles = g.N * g.P;
+  const int grid = std::min(tiles, ctx().num_sms);
+  if (p.stats && stats_parts) *stats_parts = grid * 4;
+  const double flops = 2.0 * p.M * (double)g.K * taps * g.C;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * taps * g.C) * 2.0 +
+                       (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
+  const int pidx = prof_begin("conv_tc_stem", flops, bytes, p.M, g.K, taps * g.C, s);
+  conv_stem_kernel<<<grid, stem::kThreads, smem, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("conv_tc_stem");
+  g_tc_calls++;
+  return true;
+}
+
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
                    float beta, cudaStream_t s, float* stats, int* stats_parts) {
   if (g.C % 64 != 0) {
     const char* e = getenv("BE_CONV_SMALLC");
     if (e && e[0] == '0') return false;
+    if (conv_stem(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts)) return true;
     return conv_small_c(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts);
   }
   if (g.K % 16 != 0) return false;

@@ -65,6 +65,10 @@ def test_conv_op_fp32(cfg, act):
                                  (2, 64, 14, 14, 64, 1, 2, 0), (3, 64, 17, 13, 96, 3, 1, 1), (1, 192, 5, 5, 320, 3, 1, 1),
                                  # small-C gather kernel (channel-padded conv1: ResNet 7×7/2, AlexNet 11×11/4)
                                  (3, 8, 40, 40, 64, 7, 2, 3), (2, 8, 35, 35, 64, 11, 4, 2), (1, 16, 9, 11, 48, 3, 1, 1),
+                                 # phase-split patch kernel (C = 8, K = 64, stride > 1): ResNet conv1 at full
+                                 # width (Q = 112), Q = 125 (MMA rows 125..127 discarded), stride 3, AlexNet conv1
+                                 (2, 8, 224, 224, 64, 7, 2, 3), (1, 8, 250, 250, 64, 7, 2, 3), (2, 8, 20, 23, 64, 5, 3, 1),
+                                 (1, 8, 224, 224, 64, 11, 4, 2),
                                  (2, 32, 8, 8, 160, 3, 2, 1), (1, 8, 6, 6, 16, 5, 1, 0)])
 def test_conv_op_bf16_implicit_gemm(cfg):
     """bf16 conv forward through the implicit-GEMM kernel (cp.async gather, no
