@@ -1,0 +1,404 @@
+// bn_stream.cu — batch-norm passes over bf16 NHWC activations as TMA-bulk
+// streams (SURVEY §8(a) a5 forward statistics / apply, a9 backward reduce /
+// dx; formulas: SURVEY §8(c)-6, oracle/ops.py batchnorm2d).
+//
+// The four passes are HBM-bound (ResNet-50 b256: 2.85 G activation elements
+// per step through BN, ≈48 GB of traffic).  Each block owns a contiguous row
+// range [r0, r1) of the [rows, C] tensor (C a power of two ≤ 2048), i.e. a
+// contiguous byte range per input stream: one producer warp moves it into a
+// shared-memory ring with 1-D cp.async.bulk copies (ITERS × 4 KB chunks per
+// stream, NST stages, mbarrier complete_tx), so ≈64 KB per block (≈190 KB
+// per SM) are in flight without any per-thread load issue; 8 consumer warps
+// read their 16 B (8 channels of one row: thread t ↔ byte t·16 of every
+// 4 KB = 2048/C rows) from smem.  Outputs (y, dx, the masked gradient) are
+// direct 16-B coalesced stores.  Reductions finish with the same fixed-order
+// per-block combine as the register kernels (deterministic partials).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "runtime.h"
+#include "sm100.cuh"
+
+namespace be { namespace k {
+using namespace be::dev;
+
+namespace {
+constexpr int kCons = 256;              // consumer threads (8 warps)
+constexpr int kThr = kCons + 32;        // + producer warp
+constexpr int kIter = 4096;             // bytes per consumer iteration (16 B per thread)
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(sm100::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void unpack8s(uint4 v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8s(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);  // RN-even
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int NS, int ITERS, int NST>
+struct Ring {
+  static constexpr int CH = ITERS * kIter;
+  static constexpr int SMEM = NST * NS * CH + 2 * NST * 8 + 128;
+};
+
+// Streams rows [r0, r1) of NS bf16 [rows, C] tensors through the ring; body(row,
+// v[NS]) runs for each (row, 8-channel group) of this thread.  Returns after the
+// last chunk (consumers) / last copy (producer); callers __syncthreads() before
+// reusing the ring.
+template <int NS, int ITERS, int NST, typename Body>
+__device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], int64_t r0, int64_t r1, int C,
+                                            uint8_t* ring, Body&& body) {
+  using RG = Ring<NS, ITERS, NST>;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * NS * RG::CH);
+  uint64_t* empty = full + NST;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int lanes = C >> 3, rpi = kCons / lanes;
+  const int64_t crow = (int64_t)ITERS * rpi;
+  const int64_t nchunks = r1 > r0 ? (r1 - r0 + crow - 1) / crow : 0;
+  if (t == 0) {
+    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], kCons / 32); }
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == kCons / 32) {
+    if (lane == 0) {
+      for (int64_t i = 0; i < nchunks; ++i) {
+        const int st = (int)(i % NST);
+        sm100::mbar_wait(&empty[st], (uint32_t)((i / NST) & 1) ^ 1u);
+        const int64_t rs = r0 + i * crow;
+        const uint32_t bytes = (uint32_t)(min(crow, r1 - rs) * C * 2);
+        sm100::mbar_arrive_expect_tx(&full[st], bytes * NS);
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          bulk_g2s(sm100::smem_u32(ring + (st * NS + k) * RG::CH), src[k] + rs * C, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  const int rin = t / lanes;
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int st = (int)(i % NST);
+    sm100::mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
+    const int64_t rs = r0 + i * crow;
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t row = rs + it * rpi + rin;
+      if (row < r1) {
+        uint4 v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          v[k] = *reinterpret_cast<const uint4*>(ring + (st * NS + k) * RG::CH + it * kIter + t * 16);
+        body(row, v);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&empty[st]);
+  }
+}
+
+// fixed-order per-block combine of the consumers' per-row-slot sums → partial row blockIdx.x
+__device__ __forceinline__ void combine_partials(const float (&s0)[8], const float (&s1)[8], int C, float* sm,
+                                                 float* part0, float* part1) {
+  const int t = threadIdx.x, lanes = C >> 3, rpi = kCons / lanes;
+  if (t < kCons) {
+    const int v = t % lanes, rl = t / lanes;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { sm[rl * C + v * 8 + j] = s0[j]; sm[kCons * 8 + rl * C + v * 8 + j] = s1[j]; }
+  }
+  __syncthreads();
+  for (int i = t; i < C; i += blockDim.x) {
+    float a0 = 0.f, a1 = 0.f;
+    for (int w = 0; w < rpi; ++w) { a0 += sm[w * C + i]; a1 += sm[kCons * 8 + w * C + i]; }
+    part0[(int64_t)blockIdx.x * C + i] = a0;
+    part1[(int64_t)blockIdx.x * C + i] = a1;
+  }
+}
+
+// forward statistics: shifted sums Σ(x−K), Σ(x−K)² with K = x[0, c]
+__global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t* __restrict__ x, int64_t rows, int C,
+                                                               float* part0, float* part1, int64_t rps) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  float k[8], s0[8] = {}, s1[8] = {};
+  unpack8s(*reinterpret_cast<const uint4*>(x + c), k);
+  const uint16_t* src[1] = {x};
+  stream_rows<1, 4, 4>(src, r0, r1, C, ring, [&](int64_t, const uint4 (&v)[1]) {
+    float a[8];
+    unpack8s(v[0], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { const float d = a[j] - k[j]; s0[j] += d; s1[j] += d * d; }
+  });
+  __syncthreads();
+  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1);
+}
+
+// backward reduction Σg', Σg'·x̂ (g' = gy masked by act(γx̂+β) > 0 recomputed
+// from x when act; with rmask: g = gy·1[rmask > 0] written to gout first)
+template <bool MASK>
+__global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_t* __restrict__ x,
+                                                                const uint16_t* __restrict__ gy, int act,
+                                                                int64_t rows, int C, const float* __restrict__ mean,
+                                                                const float* __restrict__ invstd, float* part0,
+                                                                float* part1, int64_t rps,
+                                                                const float* __restrict__ gam,
+                                                                const float* __restrict__ bsh,
+                                                                const uint16_t* __restrict__ rmask,
+                                                                uint16_t* __restrict__ gout) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  float k[8], is[8], sc[8], sh[8], s0[8] = {}, s1[8] = {};
+  if (threadIdx.x < kCons) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      k[j] = mean[c + j]; is[j] = invstd[c + j];
+      sc[j] = act ? gam[c + j] * is[j] : 0.f;
+      sh[j] = act ? bsh[c + j] - k[j] * sc[j] : 0.f;
+    }
+  }
+  auto body = [&](int64_t row, const uint4* v) {
+    float a[8], g[8];
+    unpack8s(v[0], a);
+    uint4 gv = v[1];
+    if (MASK) {
+      // residual block output y = relu(bn(x) + shortcut): g = gy·1[y > 0]
+      // (bf16 y > 0 ⇔ bits in [1, 0x7f80]), stored for the shortcut and dx
+      const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+      const uint32_t mw[4] = {v[2].x, v[2].y, v[2].z, v[2].w};
+      uint32_t ow[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t ml = mw[i] & 0xffffu, mh = mw[i] >> 16;
+        const uint32_t lo = ml - 1u < 0x7f80u ? 0x0000ffffu : 0u;
+        const uint32_t hi = mh - 1u < 0x7f80u ? 0xffff0000u : 0u;
+        ow[i] = gw[i] & (lo | hi);
+      }
+      gv = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      *reinterpret_cast<uint4*>(gout + row * C + c) = gv;
+    }
+    unpack8s(gv, g);
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] += g[j] * (a[j] - k[j]) * is[j]; }
+  };
+  if (MASK) {
+    const uint16_t* src[3] = {x, gy, rmask};
+    stream_rows<3, 2, 3>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[3]) { body(row, v); });
+  } else {
+    const uint16_t* src[2] = {x, gy};
+    stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) { body(row, v); });
+  }
+  __syncthreads();
+  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1);
+}
+
+// y = act(γ·x̂ + β [+ res])
+template <bool RES>
+__global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t* __restrict__ x, uint16_t* y,
+                                                               int64_t rows, int C, const float* __restrict__ mean,
+                                                               const float* __restrict__ invstd,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ beta, int act, int64_t rps,
+                                                               const uint16_t* __restrict__ res) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  float sc[8], sh[8];
+  if (threadIdx.x < kCons) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j] = gamma[c + j] * invstd[c + j];
+      sh[j] = beta[c + j] - mean[c + j] * sc[j];
+    }
+  }
+  auto body = [&](int64_t row, const uint4* v) {
+    float a[8], o[8];
+    unpack8s(v[0], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(a[j], sc[j], sh[j]);
+    if (RES) {
+      float b[8];
+      unpack8s(v[1], b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += b[j];
+    }
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = fmaxf(o[j], 0.f);
+    }
+    *reinterpret_cast<uint4*>(y + row * C + c) = pack8s(o);
+  };
+  if (RES) {
+    const uint16_t* src[2] = {x, res};
+    stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) { body(row, v); });
+  } else {
+    const uint16_t* src[1] = {x};
+    stream_rows<1, 4, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[1]) { body(row, v); });
+  }
+}
+
+// dx (+)= k1·g' + k2·x + k3
+template <bool ACC>
+__global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* __restrict__ gy,
+                                                            const uint16_t* __restrict__ x, int act, uint16_t* dx,
+                                                            int64_t rows, int C, const float* __restrict__ mean,
+                                                            const float* __restrict__ invstd,
+                                                            const float* __restrict__ gamma,
+                                                            const float* __restrict__ sums, int64_t rps,
+                                                            const float* __restrict__ bsh) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  const float inv_n = 1.f / (float)rows;
+  float k1[8], k2[8], k3[8], sc[8], sh[8];
+  if (threadIdx.x < kCons) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float is = invstd[c + j], a = gamma[c + j] * is;
+      sc[j] = a;
+      sh[j] = act ? bsh[c + j] - mean[c + j] * a : 0.f;
+      const float m1 = sums[c + j] * inv_n, m2 = sums[C + c + j] * inv_n;
+      k1[j] = a;
+      k2[j] = -a * m2 * is;
+      k3[j] = -a * m1 + a * m2 * is * mean[c + j];
+    }
+  }
+  auto body = [&](int64_t row, const uint4* v) {
+    float g[8], a[8], o[8];
+    unpack8s(v[0], g);
+    unpack8s(v[1], a);
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(k1[j], g[j], fmaf(k2[j], a[j], k3[j]));
+    if (ACC) {
+      float pv[8];
+      unpack8s(v[2], pv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += pv[j];
+    }
+    *reinterpret_cast<uint4*>(dx + row * C + c) = pack8s(o);
+  };
+  if (ACC) {
+    const uint16_t* src[3] = {gy, x, dx};
+    stream_rows<3, 2, 3>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[3]) { body(row, v); });
+  } else {
+    const uint16_t* src[2] = {gy, x};
+    stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) { body(row, v); });
+  }
+}
+
+template <typename K>
+void set_smem(K kern, int bytes) {
+  BE_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+constexpr int kS1 = Ring<1, 4, 4>::SMEM;   // 64 KB ring: 3 blocks per SM
+constexpr int kS2 = Ring<2, 2, 4>::SMEM;
+constexpr int kS3 = Ring<3, 2, 3>::SMEM;
+int stream_blocks(int per_sm) { return ctx().num_sms * per_sm; }
+bool enabled() {
+  static const int on = [] { const char* e = getenv("BE_BN_STREAM"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+}  // namespace
+
+bool bn_stream_ok(const void* a, int64_t rows, int C) {
+  return enabled() && C >= 8 && C <= 2048 && (C & (C - 1)) == 0 && rows > 0 && aligned16(a);
+}
+
+int64_t bn_stream_splits(int64_t rows, int C, int64_t cap) {
+  // ≥ 4 chunks per block; 3 blocks per SM; never more than the caller's partial rows
+  const int64_t crow = 4LL * (kCons / (C >> 3));
+  int64_t sp = std::min<int64_t>(rows / (crow * 4) + 1, stream_blocks(3));
+  return std::max<int64_t>(1, std::min(sp, cap));
+}
+
+void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s) {
+  static bool once = [] { set_smem(bn_stats_stream_kernel, kS1); return true; }();
+  (void)once;
+  const int64_t rps = (rows + sp - 1) / sp;
+  bn_stats_stream_kernel<<<(unsigned)sp, kThr, kS1, s>>>(x, rows, C, part0, part1, rps);  // caller: after_launch
+}
+
+void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
+                      const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
+                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s) {
+  static bool once = [] {
+    set_smem(bn_reduce_stream_kernel<false>, kS2);
+    set_smem(bn_reduce_stream_kernel<true>, kS3);
+    return true;
+  }();
+  (void)once;
+  const int64_t rps = (rows + sp - 1) / sp;
+  if (rmask)
+    bn_reduce_stream_kernel<true><<<(unsigned)sp, kThr, kS3, s>>>(x, gy, act, rows, C, mean, invstd, part0, part1,
+                                                                  rps, gam, bsh, rmask, gout);
+  else
+    bn_reduce_stream_kernel<false><<<(unsigned)sp, kThr, kS2, s>>>(x, gy, act, rows, C, mean, invstd, part0, part1,
+                                                                   rps, gam, bsh, nullptr, nullptr);
+  after_launch("bn_reduce_stream");
+}
+
+void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
+                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s) {
+  static bool once = [] {
+    set_smem(bn_apply_stream_kernel<false>, kS1);
+    set_smem(bn_apply_stream_kernel<true>, kS2);
+    return true;
+  }();
+  (void)once;
+  const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
+  const int64_t rps = (rows + sp - 1) / sp;
+  if (res)
+    bn_apply_stream_kernel<true><<<(unsigned)sp, kThr, kS2, s>>>(x, y, rows, C, mean, invstd, gamma, beta, act, rps,
+                                                                 res);
+  else
+    bn_apply_stream_kernel<false><<<(unsigned)sp, kThr, kS1, s>>>(x, y, rows, C, mean, invstd, gamma, beta, act, rps,
+                                                                  nullptr);
+  after_launch("bn_apply_stream");
+}
+
+void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,
+                  const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
+                  const float* bsh, cudaStream_t s) {
+  static bool once = [] {
+    set_smem(bn_dx_stream_kernel<false>, kS2);
+    set_smem(bn_dx_stream_kernel<true>, kS3);
+    return true;
+  }();
+  (void)once;
+  const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
+  const int64_t rps = (rows + sp - 1) / sp;
+  if (dx_beta != 0.f)
+    bn_dx_stream_kernel<true><<<(unsigned)sp, kThr, kS3, s>>>(gy, x, act, dx, rows, C, mean, invstd, gamma, sums, rps,
+                                                              bsh);
+  else
+    bn_dx_stream_kernel<false><<<(unsigned)sp, kThr, kS2, s>>>(gy, x, act, dx, rows, C, mean, invstd, gamma, sums,
+                                                               rps, bsh);
+  after_launch("bn_dx_stream");
+}
+
+}}  // namespace be::k

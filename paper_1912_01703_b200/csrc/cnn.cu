@@ -18,6 +18,19 @@
 namespace be { namespace k {
 using namespace be::dev;
 
+// bn_stream.cu: TMA-bulk streaming BN passes (bf16, C a power of two ≤ 2048)
+bool bn_stream_ok(const void* a, int64_t rows, int C);
+int64_t bn_stream_splits(int64_t rows, int C, int64_t cap);
+void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s);
+void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
+                      const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
+                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s);
+void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
+                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s);
+void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,
+                  const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
+                  const float* bsh, cudaStream_t s);
+
 namespace {
 int grid_for(int64_t n, int per = 1) {
   int64_t b = (n + 256LL * per - 1) / (256LL * per);
@@ -1271,10 +1284,14 @@ static int64_t bn_splits_v(int64_t rows, int C) {
 void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float* mean, float* invstd, float* partial,
               float* run_mean, float* run_var, float momentum, cudaStream_t s) {
   if (bn_vec_ok(x, C)) {
-    const int64_t sp = bn_splits_v(rows, C);
+    int64_t sp = bn_splits_v(rows, C);
+    const bool stream = dt == BE_BF16 && bn_stream_ok(x, rows, C);
+    if (stream) sp = bn_stream_splits(rows, C, sp);
     const int64_t rps = (rows + sp - 1) / sp;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-    if (dt == BE_BF16)
+    if (stream)
+      bn_stats_stream(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, sp, s);
+    else if (dt == BE_BF16)
       bn_stats_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, rps);
     else
       bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
@@ -1310,6 +1327,11 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
               const float* gamma, const float* beta, int act, cudaStream_t s, const void* res) {
   const int64_t total = rows * C;
   if (total == 0) return;
+  if (dt == BE_BF16 && bn_stream_ok(x, rows, C) && aligned16(y) && (!res || aligned16(res))) {
+    bn_apply_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C, mean, invstd, gamma,
+                    beta, act, reinterpret_cast<const uint16_t*>(res), s);
+    return;
+  }
   if (bn_vec_ok(x, C) && aligned16(y) && (!res || aligned16(res))) {
     dim3 grid;
     const int64_t rpb = bn_rows_per_block(rows, C, &grid);
@@ -1333,20 +1355,31 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
     // residual output mask: g = dy·1[rmask > 0] into gout, then the BN backward of g
     if (dt == BE_BF16 && !act && bn_vec_ok(x, C) && aligned16(dy) && aligned16(rmask) && aligned16(gout) &&
         (!dx || aligned16(dx))) {
-      const int64_t sp = bn_splits_v(rows, C);
+      int64_t sp = bn_splits_v(rows, C);
+      const bool stream = bn_stream_ok(x, rows, C);
+      if (stream) sp = bn_stream_splits(rows, C, sp);
       const int64_t rps = (rows + sp - 1) / sp;
       float* p0 = partial;
       float* p1 = partial + sp * C;
       float* sums = partial + 2 * sp * C;
       dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-      bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
-                                          0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,
-                                          reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
-      after_launch("bn_bwd_reduce_mask_bf16");
+      if (stream) {
+        bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), 0, rows, C, mean,
+                         invstd, p0, p1, sp, gamma, nullptr, reinterpret_cast<const uint16_t*>(rmask),
+                         reinterpret_cast<uint16_t*>(gout), s);
+      } else {
+        bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
+                                            0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,
+                                            reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
+        after_launch("bn_bwd_reduce_mask_bf16");
+      }
       bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                       nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
       after_launch("bn_bwd_finalize_v");
-      if (dx) {
+      if (dx && stream) {
+        bn_dx_stream(reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x), 0,
+                     reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, nullptr, s);
+      } else if (dx) {
         dim3 g2;
         const int64_t rpb = bn_rows_per_block(rows, C, &g2);
         bn_dx_bf16<<<g2, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x),
@@ -1360,24 +1393,32 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
     dy = gout;
   }
   if (bn_vec_ok(x, C) && aligned16(dy) && (!act || bn_beta || aligned16(y)) && (!dx || aligned16(dx))) {
-    const int64_t sp = bn_splits_v(rows, C);
+    int64_t sp = bn_splits_v(rows, C);
+    const bool fast = dt == BE_BF16 && (!act || bn_beta) && (!dx || aligned16(dx));
+    const bool stream = fast && bn_stream_ok(x, rows, C);
+    if (stream) sp = bn_stream_splits(rows, C, sp);
     const int64_t rps = (rows + sp - 1) / sp;
     float* p0 = partial;
     float* p1 = partial + sp * C;
     float* sums = partial + 2 * sp * C;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-    const bool fast = dt == BE_BF16 && (!act || bn_beta) && (!dx || aligned16(dx));
-    if (fast)
+    if (stream)
+      bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), act, rows, C, mean,
+                       invstd, p0, p1, sp, gamma, bn_beta, nullptr, nullptr, s);
+    else if (fast)
       bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
                                           act, rows, C, mean, invstd, p0, p1, rps, gamma, bn_beta);
     else
       bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
                                           bn_beta ? gamma : nullptr, bn_beta);
-    after_launch("bn_bwd_reduce_v");
+    if (!stream) after_launch("bn_bwd_reduce_v");
     bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                     nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
     after_launch("bn_bwd_finalize_v");
-    if (dx) {
+    if (dx && stream) {
+      bn_dx_stream(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(x), act,
+                   reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, bn_beta, s);
+    } else if (dx) {
       dim3 g2;
       const int64_t rpb = bn_rows_per_block(rows, C, &g2);
       if (fast)
