@@ -1578,6 +1578,152 @@ __global__ void __launch_bounds__(stem::kThreads, 1) conv_stem_kernel(const __gr
   }
 }
 
+// ---------------------------------------------------------------- conv wgrad from a shared input patch
+// dW[k, r, s, c] = Σ_{n,p,q} dY[n,p,q,k] · x[n, p+r−pad, q+s−pad, c] for
+// stride-1 convolutions with C = 64 and K = 64 (ResNet layer-1 3×3): the
+// materialised / im2col-TMA / shifted-tile variants re-read x once per tap
+// through L2 (≥ 9× the input), the L2→SM stream bounds them (≈350 µs at
+// b256).  Here a tile is G = 128/W' output rows of one image at pitch W'
+// (power of two ≥ Q + S − 1): slot m = dp·W' + q.  Per tile TMA loads
+//   dY box {64 k, W', G, 1} → B operand (MN-major SW128, rows = slots; slots
+//     with q ≥ Q or p ≥ P are zero-filled), and
+//   x box {64 c, W', G+R−1, 1} at (−pad, p0−pad) → the patch: input pixel of
+//     slot m for tap (r, s) is patch row m + r·W' + s.
+// The A operand of tap (r, s) is the patch started at row r·W' + s: an
+// MN-major SW128 operand whose start is not a multiple of the 8-row swizzle
+// atom (valid: the swizzle is a function of the absolute smem address —
+// tools/shift_probe.cu).  One M = 128 MMA covers two taps (A's two 64-channel
+// M-atoms are LBO = their row distance apart; an odd last tap repeats itself,
+// LBO = 0, and those D rows are dropped), N = 64 = k, K = 16 slots.  D for
+// all ⌈RS/2⌉ tap pairs stays in TMEM (≤ 512 columns) for the CTA's whole
+// slot range: no per-tile epilogue.  At the end each CTA writes its partial
+// dWᵀ rows (D row = tap·64 + c, contiguous in KRSC) into an fp32 split-K slab
+// [CTA][64][RSC]; the fixed-order splitk_reduce sums them (deterministic).
+namespace wgp {
+constexpr int kThreads = 384;   // w0 TMA, w1 + w3 MMA, w2 TMEM, w4-11 epilogue
+constexpr int NBUF = 4;
+constexpr int kSlack = 2048;    // zeroed tail after each patch (discarded slots' overrun)
+}  // namespace wgp
+
+__global__ void __launch_bounds__(wgp::kThreads, 1) conv_wgrad_patch_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int Wp = p.sh_wb, G = p.sh_hb, R = p.cR, S = p.cS;
+  const int taps = R * S, pairs = (taps + 1) / 2;
+  const int patch_rows = (G + R - 1) * Wp;
+  const int xbytes = patch_rows * 128, ybytes = G * Wp * 128;
+  const int xstride = (xbytes + wgp::kSlack + 1023) / 1024 * 1024;  // per-buffer x region (1024-aligned)
+  const int ystride = (ybytes + 1023) / 1024 * 1024;
+  uint8_t* xb = smem;
+  uint8_t* yb = smem + wgp::NBUF * xstride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(yb + wgp::NBUF * ystride);
+  uint64_t* empty = full + wgp::NBUF;
+  uint64_t* done = empty + wgp::NBUF;   // [2]: one per issuing warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // zero every x buffer's slack once (TMA never writes it; discarded slots read it × dY = 0)
+  for (int b = 0; b < wgp::NBUF; ++b)
+    for (int i = threadIdx.x; i < (xstride - xbytes) / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(xb + b * xstride + xbytes)[i] = make_uint4(0, 0, 0, 0);
+  sm100::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < wgp::NBUF; ++b) { sm100::mbar_init(&full[b], 1); sm100::mbar_init(&empty[b], 2); }
+    sm100::mbar_init(&done[0], 1);
+    sm100::mbar_init(&done[1], 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.ta[0]);
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int pg = (p.cP + G - 1) / G;       // row groups per image
+  const int num_tiles = p.cN * pg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int b = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int n = t / pg, p0 = (t - n * pg) * G;
+        sm100::mbar_wait(&empty[b], phase ^ 1);
+        sm100::mbar_arrive_expect_tx(&full[b], (uint32_t)(xbytes + ybytes));
+        sm100::tma_load_4d(&p.ta[0], &full[b], xb + b * xstride, 0, -p.cpad, p0 - p.cpad, n);
+        sm100::tma_load_4d(&p.tb[0], &full[b], yb + b * ystride, 0, 0, p0, n);
+        if (++b == wgp::NBUF) { b = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    // whole warp runs the issue loop (descriptors stay warp-uniform → uniform
+    // registers, short issue chain); one elected lane issues.  Tap-pair A
+    // descriptors are built once: per tile / k-step only the start address moves.
+    // Two issuing warps own disjoint tap pairs (accumulators): an N = 64 MMA
+    // (32 cycles) is shorter than one warp's issue chain.
+    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 1, 1);
+    uint64_t adesc[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int t0 = min(2 * a, taps - 1), t1 = min(2 * a + 1, taps - 1);
+      const int sh0 = (t0 / S) * Wp + t0 % S, sh1 = (t1 / S) * Wp + t1 % S;
+      adesc[a] = sm100::make_sw128_desc(sm100::smem_u32(xb) + sh0 * 128, (sh1 - sh0) * 128, 1024);
+    }
+    const uint64_t bdesc0 = sm100::make_sw128_desc(sm100::smem_u32(yb), 16, 1024);
+    const int ksteps = G * Wp / 16;
+    const int a_lo = warp == 1 ? 0 : (pairs + 1) / 2, a_hi = warp == 1 ? (pairs + 1) / 2 : pairs;
+    int b = 0; uint32_t phase = 0;
+    uint32_t acc = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      sm100::mbar_wait(&full[b], phase);
+      sm100::tc_fence_after();
+      const uint64_t xo = (uint64_t)((b * xstride) >> 4), yo = (uint64_t)((b * ystride) >> 4);
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t ko = (uint64_t)(ks * 128);  // 16 slots × 128 B >> 4
+        const uint64_t bd = bdesc0 + yo + ko;
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (a >= a_lo && a < a_hi && sm100::elect_one())
+            sm100::mma_bf16(tmem_base + a * 64, adesc[a] + xo + ko, bd, idesc, acc);
+        acc = 1;
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&empty[b]);
+      __syncwarp();
+      if (++b == wgp::NBUF) { b = 0; phase ^= 1; }
+    }
+    if (sm100::elect_one()) sm100::mma_commit(&done[warp == 1 ? 0 : 1]);
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===================== epilogue: partial dWᵀ rows into this CTA's slab =====================
+    const int ew = warp - 4, eq = warp & 3, eh = ew >> 2;
+    const int RSC = taps * 64;
+    float* slab = reinterpret_cast<float*>(p.D) + (long long)blockIdx.x * p.split_stride;
+    const bool any = blockIdx.x < num_tiles;
+    if (any) {
+      sm100::mbar_wait(&done[0], 0);
+      sm100::mbar_wait(&done[1], 0);
+      sm100::tc_fence_after();
+    }
+    for (int a = 0; a < pairs; ++a) {
+      const int col = 128 * a + eq * 32 + lane;  // D row → dW column (tap·64 + c)
+      uint32_t r[32];
+      if (any) {
+        sm100::tmem_ld_32x32b_x32(tmem_base + a * 64 + eh * 32 + ((uint32_t)(eq * 32) << 16), r);
+        sm100::tmem_ld_wait();
+      }
+      if (col < RSC) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) slab[(long long)(eh * 32 + j) * RSC + col] = any ? __uint_as_float(r[j]) : 0.f;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -2160,6 +2306,55 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
   prof_end(pidx, s);
   after_launch("conv_tc_small_c");
   g_tc_calls++;
+  return true;
+}
+
+bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
+                      cudaStream_t s) {
+  static const int on = [] { const char* e = getenv("BE_WGRAD_PATCH"); return e ? atoi(e) : 1; }();
+  if (!on || g.stride != 1 || g.C != 64 || g.K != 64 || g.R * g.S > 16 || dwt != BE_F32) return false;
+  int Wp = 16;
+  while (Wp < g.Q + g.S - 1) Wp *= 2;
+  if (Wp > BM) return false;
+  const int G = BM / Wp;
+  if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const int xbytes = (G + g.R - 1) * Wp * 128, ybytes = G * Wp * 128;
+  const int xstride = (xbytes + wgp::kSlack + 1023) / 1024 * 1024, ystride = (ybytes + 1023) / 1024 * 1024;
+  const int smem = 1024 + wgp::NBUF * (xstride + ystride) + 256;
+  if (smem > 227 * 1024 || G + g.R - 1 > 256) return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const uint64_t dx4[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
+  const uint64_t dy4[4] = {(uint64_t)g.K, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.N};
+  if (!encode_4d_tiled(&p.ta[0], x, dx4, 64, Wp, G + g.R - 1, 1)) return false;
+  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, Wp, G, 1)) return false;
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
+  p.cstride = 1; p.cpad = g.pad; p.sh_wb = Wp; p.sh_hb = G;
+  const int RSC = g.R * g.S * g.C;
+  const int tiles = g.N * ((g.P + G - 1) / G);
+  const int grid = std::min(tiles, ctx().num_sms);
+  p.split_stride = 64LL * RSC;
+  Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)grid * p.split_stride, s);
+  p.D = ws->ptr;
+  static bool attr = false;
+  if (!attr) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    attr = true;
+  }
+  const double flops = 2.0 * g.N * g.P * g.Q * (double)g.K * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.N * g.P * g.Q * g.K) * 2.0 + 4.0 * g.K * RSC;
+  const int pidx = prof_begin("conv_wgrad_patch", flops, bytes, g.K, RSC, g.N * g.P * g.Q, s);
+  conv_wgrad_patch_kernel<<<grid, wgp::kThreads, smem, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("conv_wgrad_patch");
+  g_tc_calls++;
+  const long long total = 64LL * RSC;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw,
+                                       RSC, 1, beta, nullptr, 0);
+  after_launch("conv_wgrad_patch_reduce");
+  ctx().alloc.free(ws);
   return true;
 }
 

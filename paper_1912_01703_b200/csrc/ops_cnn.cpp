@@ -85,9 +85,17 @@ static void vjp_conv(Node* n, GradSink& sink) {
                g.stride, g.pad);
       static const int shift_on = [] { const char* e = getenv("BE_WGRAD_SHIFT"); return e ? atoi(e) : 1; }();
       const bool shift_ok = shift_on && g.Q <= 64 && g.K % 8 == 0 && g.stride <= 2;
-      variant = tune_choose(key, shift_ok ? 3 : 2, 0, &e0, &e1);
+      // variant 3: shared input patch per tile, shifted UMMA operands (stride 1, C = K = 64)
+      const bool patch_ok = shift_ok && g.stride == 1 && g.C == 64 && g.K == 64 && dw->dtype == BE_F32 &&
+                            g.R * g.S <= 16 && g.Q + g.S - 1 <= 128;
+      variant = tune_choose(key, patch_ok ? 4 : (shift_ok ? 3 : 2), 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);
+    if (variant == 3 && k::conv_wgrad_patch(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
+      if (e1) cudaEventRecord(e1, s);
+      sink.commit(1);
+    } else {
+    if (variant == 3) variant = 1;
     if (variant == 0 || variant == 2) {
       gd.conv_x = x->data();
       gd.conv_g = g;
@@ -100,6 +108,7 @@ static void vjp_conv(Node* n, GradSink& sink) {
     k::gemm(gd, s);
     if (e1) cudaEventRecord(e1, s);
     sink.commit(1);
+    }
   }
   if (sink.needs(0)) {
     float bx;

@@ -301,7 +301,10 @@ def test_bn_statistics_from_conv_epilogue(cfg):
 
 
 @pytest.mark.parametrize("cfg", [(2, 64, 9, 9, 64, 3, 1, 1), (2, 64, 10, 10, 128, 3, 2, 1), (1, 128, 7, 7, 256, 3, 1, 1),
-                                 (3, 64, 17, 13, 96, 3, 1, 1), (2, 64, 30, 30, 64, 3, 1, 1), (1, 64, 12, 12, 64, 5, 2, 2)])
+                                 (3, 64, 17, 13, 96, 3, 1, 1), (2, 64, 30, 30, 64, 3, 1, 1), (1, 64, 12, 12, 64, 5, 2, 2),
+                                 # shared-patch variant (stride 1, C = K = 64): ResNet layer-1 size, a ragged last
+                                 # row group (P = 27, G = 4), a 2×2 kernel (even tap count)
+                                 (2, 64, 56, 56, 64, 3, 1, 1), (2, 64, 27, 25, 64, 3, 1, 1), (1, 64, 10, 12, 64, 2, 1, 0)])
 def test_conv_wgrad_variants_bf16(cfg):
     """Conv weight gradient through every autotuned variant (the first calls
     of a shape cycle through them: TMA-im2col B, materialised columns,
