@@ -1724,6 +1724,130 @@ __global__ void __launch_bounds__(wgp::kThreads, 1) conv_wgrad_patch_kernel(cons
   }
 }
 
+// ---------------------------------------------------------------- stride-1 conv from a shared input patch
+// Y[n, p, q, k] = Σ_{r,s,c} x[n, p+r−pad, q+s−pad, c] · W[k, r, s, c] for
+// stride-1 convolutions with C = K = 64 (ResNet layer 1: the 3×3 forward and,
+// with flipped weights, its dgrad).  The im2col-TMA kernel loads one
+// 128 × 64 A tile per tap (9× the input through L2: ≈190 B/clk/SM for an
+// N = 64 MMA — L2-bound).  Here a tile is G = 128/W' output rows at pitch W'
+// (slot m = dp·W' + q) whose input rows + halo are loaded once (TMA box
+// {64 c, W', G+R−1, 1}); tap (r, s)'s A operand is the patch started at row
+// r·W' + s — a K-major SW128 operand with an unaligned start (the swizzle
+// follows the absolute address: tools/shift_probe.cu) — against the tap's
+// 64 × 64 weight tile, resident in smem for the whole CTA.  Two MMA warps
+// take alternate tiles (accumulator = tile parity); the epilogue stores each
+// warp's 32 slots (one output row segment, W' ≥ 32) through a 3-D
+// [N·P][Q][K] TMA map, clipping q ≥ Q; rows past P are skipped.
+namespace cfp {
+constexpr int kThreads = 384;   // w0 TMA, w1 + w3 MMA, w2 TMEM, w4-11 epilogue
+constexpr int NBUF = 3;
+constexpr int kSlack = 2048;
+}  // namespace cfp
+
+__global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int Wp = p.sh_wb, G = p.sh_hb, R = p.cR, S = p.cS, taps = R * S;
+  const int xbytes = (G + R - 1) * Wp * 128;
+  const int xstride = (xbytes + cfp::kSlack + 1023) / 1024 * 1024;
+  uint8_t* wsm = smem;                                  // [tap][64 k][128 B] SW128
+  uint8_t* xb = wsm + taps * 8192;
+  uint8_t* epi_smem = xb + cfp::NBUF * xstride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
+  uint64_t* empty = full + cfp::NBUF;
+  uint64_t* tfull = empty + cfp::NBUF;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* wbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = 0; b < cfp::NBUF; ++b)
+    for (int i = threadIdx.x; i < (xstride - xbytes) / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(xb + b * xstride + xbytes)[i] = make_uint4(0, 0, 0, 0);
+  sm100::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < cfp::NBUF; ++b) { sm100::mbar_init(&full[b], 1); sm100::mbar_init(&empty[b], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
+    sm100::mbar_init(wbar, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.ta[0]);
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 2) sm100::tmem_alloc<128>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int pg = (p.cP + G - 1) / G;
+  const int num_tiles = p.cN * pg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      sm100::mbar_arrive_expect_tx(wbar, (uint32_t)(taps * 8192));
+      for (int t = 0; t < taps; ++t) sm100::tma_load_2d(&p.tb[0], wbar, wsm + t * 8192, t * 64, 0);
+      int b = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int n = t / pg, p0 = (t - n * pg) * G;
+        sm100::mbar_wait(&empty[b], phase ^ 1);
+        sm100::mbar_arrive_expect_tx(&full[b], (uint32_t)xbytes);
+        sm100::tma_load_4d(&p.ta[0], &full[b], xb + b * xstride, 0, -p.cpad, p0 - p.cpad, n);
+        if (++b == cfp::NBUF) { b = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    const int k = warp == 1 ? 0 : 1;
+    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 0, 0);
+    const uint64_t a0 = sm100::make_sw128_desc(sm100::smem_u32(xb), 16, 1024);
+    const uint64_t w0 = sm100::make_sw128_desc(sm100::smem_u32(wsm), 16, 1024);
+    sm100::mbar_wait(wbar, 0);
+    int ti = k;
+    for (int t = blockIdx.x + k * gridDim.x; t < num_tiles; t += 2 * gridDim.x, ti += 2) {
+      const int b = ti % cfp::NBUF;
+      sm100::mbar_wait(&tempty[k], (uint32_t)((ti >> 1) & 1) ^ 1u);
+      sm100::mbar_wait(&full[b], (uint32_t)((ti / cfp::NBUF) & 1));
+      sm100::tc_fence_after();
+      const uint64_t ab = a0 + (uint64_t)((b * xstride) >> 4);
+      const uint32_t d = tmem_base + k * 64;
+      for (int tp = 0; tp < taps; ++tp) {
+        const uint64_t ad = ab + (uint64_t)((((tp / S) * Wp + tp % S) * 128) >> 4);
+        const uint64_t bd = w0 + (uint64_t)(tp * 512);  // 8 KB >> 4
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (sm100::elect_one()) sm100::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (tp | kk) ? 1u : 0u);
+      }
+      if (sm100::elect_one()) {
+        sm100::mma_commit(&empty[b]);
+        sm100::mma_commit(&tfull[k]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4, eq = warp & 3, eh = ew >> 2;
+    const int dp = (eq * 32) / Wp, q0 = (eq * 32) % Wp;
+    int slot = 0, ti = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+      const int acc = ti & 1;
+      const int n = t / pg, p0 = (t - n * pg) * G;
+      sm100::mbar_wait(&tfull[acc], (uint32_t)((ti >> 1) & 1));
+      sm100::tc_fence_after();
+      uint32_t r[32];
+      sm100::tmem_ld_32x32b_x32(tmem_base + acc * 64 + eh * 32 + ((uint32_t)(eq * 32) << 16), r);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (p0 + dp < p.cP && q0 < p.cQ)
+        epi_tma32(p, epi_smem + ew * 4096, slot, lane, q0, eh * 32, r, n * p.cP + p0 + dp);
+    }
+    if (lane == 0) sm100::bulk_wait<0>();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<128>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -2358,6 +2482,65 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   return true;
 }
 
+// stride-1 conv from a shared input patch (conv_fwd_patch_kernel): C = K = 64,
+// ≤ 9 taps, W' = pow2 ≥ Q + S − 1 in [32, 128]; false when not applicable
+static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
+                           int act, float beta, cudaStream_t s) {
+  static const int on = [] { const char* e = getenv("BE_CONV_PATCH"); return e ? atoi(e) : 1; }();
+  if (!on || g.stride != 1 || g.C != 64 || g.K != 64 || g.R * g.S > 9 || (beta != 0.f && beta != 1.f)) return false;
+  int Wp = 32;
+  while (Wp < g.Q + g.S - 1) Wp *= 2;
+  if (Wp > BM) return false;
+  const int G = BM / Wp;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15) ||
+      (reinterpret_cast<uintptr_t>(y) & 15))
+    return false;
+  const int xbytes = (G + g.R - 1) * Wp * 128;
+  const int xstride = (xbytes + cfp::kSlack + 1023) / 1024 * 1024;
+  const int smem = 1024 + g.R * g.S * 8192 + cfp::NBUF * xstride + kEpiBytes + 256;
+  if (smem > 227 * 1024 || G + g.R - 1 > 256) return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const uint64_t dx4[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
+  if (!encode_4d_tiled(&p.ta[0], x, dx4, 64, Wp, G + g.R - 1, 1)) return false;
+  const int RSC = g.R * g.S * g.C;
+  encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, 64, 64);
+  const bool f32 = yd == BE_F32;
+  {
+    const cuuint64_t es = f32 ? 4 : 2;
+    cuuint64_t od[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Q, (cuuint64_t)g.N * g.P};
+    cuuint64_t os[2] = {(cuuint64_t)g.K * es, (cuuint64_t)g.Q * g.K * es};
+    cuuint32_t ob[3] = {32, 32, 1};
+    cuuint32_t oe[3] = {1, 1, 1};
+    EncodeFn enc = get_encode();
+    if (!enc || enc(&p.td, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, od, os, ob,
+                    oe, CU_TENSOR_MAP_INTERLEAVE_NONE, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  p.tma_store = beta == 1.f ? 2 : 1;
+  p.M = g.N * g.P * g.Q; p.N = g.K; p.K = RSC;
+  p.D = y; p.ldd = g.K; p.d_f32 = f32; p.beta = beta; p.bias = bias; p.act = act;
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
+  p.cstride = 1; p.cpad = g.pad; p.sh_wb = Wp; p.sh_hb = G;
+  static bool attr = false;
+  if (!attr) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_fwd_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    attr = true;
+  }
+  const int tiles = g.N * ((g.P + G - 1) / G);
+  const int grid = std::min(tiles, ctx().num_sms);
+  const double flops = 2.0 * p.M * (double)g.K * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 + (double)p.M * g.K * (f32 ? 4 : 2);
+  const int pidx = prof_begin("conv_tc_patch", flops, bytes, p.M, g.K, RSC, s);
+  conv_fwd_patch_kernel<<<grid, cfp::kThreads, smem, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("conv_tc_patch");
+  g_tc_calls++;
+  return true;
+}
+
 // Phase-split patch convolution (conv_stem_kernel): C = 8, K = 64, stride
 // > 1, one output row (Q ≤ 128) per tile.  Returns false when the shape
 // does not fit (caller falls back to the gather kernel).
@@ -2433,6 +2616,7 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   }
   if (g.K % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+  if (!stats && conv_fwd_patch(x, w, y, g, yd, bias, act, beta, s)) return true;
   const char* e = getenv("BE_CONV_IMPLICIT");
   if (e && e[0] == '0') return false;
   GemmParams p;

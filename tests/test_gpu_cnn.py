@@ -69,6 +69,8 @@ def test_conv_op_fp32(cfg, act):
                                  # width (Q = 112), Q = 125 (MMA rows 125..127 discarded), stride 3, AlexNet conv1
                                  (2, 8, 224, 224, 64, 7, 2, 3), (1, 8, 250, 250, 64, 7, 2, 3), (2, 8, 20, 23, 64, 5, 3, 1),
                                  (1, 8, 224, 224, 64, 11, 4, 2),
+                                 # shared-patch stride-1 kernel (C = K = 64): ResNet layer-1 size, ragged row groups
+                                 (2, 64, 56, 56, 64, 3, 1, 1), (1, 64, 30, 20, 64, 3, 1, 1), (2, 64, 12, 12, 64, 2, 1, 0),
                                  (2, 32, 8, 8, 160, 3, 2, 1), (1, 8, 6, 6, 16, 5, 1, 0)])
 def test_conv_op_bf16_implicit_gemm(cfg):
     """bf16 conv forward through the implicit-GEMM kernel (cp.async gather, no
