@@ -1601,33 +1601,53 @@ __global__ void __launch_bounds__(stem::kThreads, 1) conv_stem_kernel(const __gr
 // [CTA][64][RSC]; the fixed-order splitk_reduce sums them (deterministic).
 namespace wgp {
 constexpr int kThreads = 384;   // w0 TMA, w1 + w3 MMA, w2 TMEM, w4-11 epilogue
-constexpr int NBUF = 4;
-constexpr int kSlack = 2048;    // zeroed tail after each patch (discarded slots' overrun)
+constexpr int kSlack = 2048;    // zeroed tail after each x plane (discarded slots' overrun)
+// geometry shared by host and device: C = 64·CP, K = 64·KP (CP, KP ∈ {1, 2});
+// a unit = one M = 128 MMA row block = two taps (C = 64) or one tap (C = 128);
+// units are split into ngroups groups of gs (≤ 512 / K accumulators per CTA)
+struct Geo {
+  int Wp, G, CP, KP, xps, yps, bufb, nbuf, units, ngroups, gs;
+};
+__host__ __device__ inline Geo geo(int Q, int R, int S, int C, int K) {
+  Geo g{};
+  g.Wp = 16;
+  while (g.Wp < Q + S - 1) g.Wp *= 2;
+  g.G = 128 / (g.Wp > 128 ? 128 : g.Wp);
+  g.CP = C / 64; g.KP = K / 64;
+  g.xps = ((g.G + R - 1) * g.Wp * 128 + kSlack + 1023) / 1024 * 1024;
+  g.yps = (g.G * g.Wp * 128 + 1023) / 1024 * 1024;
+  g.bufb = g.CP * g.xps + g.KP * g.yps;
+  g.nbuf = (225 * 1024) / g.bufb;
+  if (g.nbuf > 4) g.nbuf = 4;
+  const int taps = R * S;
+  g.units = g.CP == 1 ? (taps + 1) / 2 : taps;
+  const int maxacc = 512 / K;
+  g.ngroups = (g.units + maxacc - 1) / maxacc;
+  g.gs = (g.units + g.ngroups - 1) / g.ngroups;
+  return g;
+}
 }  // namespace wgp
 
 __global__ void __launch_bounds__(wgp::kThreads, 1) conv_wgrad_patch_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int Wp = p.sh_wb, G = p.sh_hb, R = p.cR, S = p.cS;
-  const int taps = R * S, pairs = (taps + 1) / 2;
-  const int patch_rows = (G + R - 1) * Wp;
-  const int xbytes = patch_rows * 128, ybytes = G * Wp * 128;
-  const int xstride = (xbytes + wgp::kSlack + 1023) / 1024 * 1024;  // per-buffer x region (1024-aligned)
-  const int ystride = (ybytes + 1023) / 1024 * 1024;
-  uint8_t* xb = smem;
-  uint8_t* yb = smem + wgp::NBUF * xstride;
-  uint64_t* full = reinterpret_cast<uint64_t*>(yb + wgp::NBUF * ystride);
-  uint64_t* empty = full + wgp::NBUF;
-  uint64_t* done = empty + wgp::NBUF;   // [2]: one per issuing warp
+  const wgp::Geo gg = wgp::geo(p.cQ, p.cR, p.cS, p.cC, p.N);
+  const int Wp = gg.Wp, G = gg.G, S = p.cS, taps = p.cR * p.cS, N = p.N;
+  const int xbytes = (G + p.cR - 1) * Wp * 128, ybytes = G * Wp * 128;
+  const int nbuf = gg.nbuf;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nbuf * gg.bufb);
+  uint64_t* empty = full + nbuf;
+  uint64_t* done = empty + nbuf;   // [2]: one per issuing warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // zero every x buffer's slack once (TMA never writes it; discarded slots read it × dY = 0)
-  for (int b = 0; b < wgp::NBUF; ++b)
-    for (int i = threadIdx.x; i < (xstride - xbytes) / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(xb + b * xstride + xbytes)[i] = make_uint4(0, 0, 0, 0);
+  // zero every x plane's slack once (TMA never writes it; discarded slots read it × dY = 0)
+  for (int b = 0; b < nbuf; ++b)
+    for (int c = 0; c < gg.CP; ++c)
+      for (int i = threadIdx.x; i < (gg.xps - xbytes) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem + b * gg.bufb + c * gg.xps + xbytes)[i] = make_uint4(0, 0, 0, 0);
   sm100::fence_proxy_async();
   if (threadIdx.x == 0) {
-    for (int b = 0; b < wgp::NBUF; ++b) { sm100::mbar_init(&full[b], 1); sm100::mbar_init(&empty[b], 2); }
+    for (int b = 0; b < nbuf; ++b) { sm100::mbar_init(&full[b], 1); sm100::mbar_init(&empty[b], 2); }
     sm100::mbar_init(&done[0], 1);
     sm100::mbar_init(&done[1], 1);
     sm100::fence_barrier_init();
@@ -1641,78 +1661,98 @@ __global__ void __launch_bounds__(wgp::kThreads, 1) conv_wgrad_patch_kernel(cons
   const uint32_t tmem_base = *tmem_slot;
   const int pg = (p.cP + G - 1) / G;       // row groups per image
   const int num_tiles = p.cN * pg;
+  const int grp = blockIdx.x % gg.ngroups, split = blockIdx.x / gg.ngroups, splits = gridDim.x / gg.ngroups;
+  const int u_lo = grp * gg.gs, u_hi = min(gg.units, u_lo + gg.gs);
 
   if (warp == 0) {
     if (lane == 0) {
       int b = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = split; t < num_tiles; t += splits) {
         const int n = t / pg, p0 = (t - n * pg) * G;
         sm100::mbar_wait(&empty[b], phase ^ 1);
-        sm100::mbar_arrive_expect_tx(&full[b], (uint32_t)(xbytes + ybytes));
-        sm100::tma_load_4d(&p.ta[0], &full[b], xb + b * xstride, 0, -p.cpad, p0 - p.cpad, n);
-        sm100::tma_load_4d(&p.tb[0], &full[b], yb + b * ystride, 0, 0, p0, n);
-        if (++b == wgp::NBUF) { b = 0; phase ^= 1; }
+        sm100::mbar_arrive_expect_tx(&full[b], (uint32_t)(gg.CP * xbytes + gg.KP * ybytes));
+        uint8_t* base = smem + b * gg.bufb;
+        for (int c = 0; c < gg.CP; ++c)
+          sm100::tma_load_4d(&p.ta[0], &full[b], base + c * gg.xps, c * 64, -p.cpad, p0 - p.cpad, n);
+        for (int k = 0; k < gg.KP; ++k)
+          sm100::tma_load_4d(&p.tb[0], &full[b], base + gg.CP * gg.xps + k * gg.yps, k * 64, 0, p0, n);
+        if (++b == nbuf) { b = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1 || warp == 3) {
     // whole warp runs the issue loop (descriptors stay warp-uniform → uniform
-    // registers, short issue chain); one elected lane issues.  Tap-pair A
-    // descriptors are built once: per tile / k-step only the start address moves.
-    // Two issuing warps own disjoint tap pairs (accumulators): an N = 64 MMA
-    // (32 cycles) is shorter than one warp's issue chain.
-    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 1, 1);
+    // registers, short issue chain); one elected lane issues.  Unit A
+    // descriptors are built once: per tile / k-step only the start address
+    // moves.  Two issuing warps own disjoint units (accumulators): an N = 64
+    // MMA (32 cycles) is shorter than one warp's issue chain.
+    const uint32_t idesc = sm100::make_idesc(1u, BM, N, 1, 1);
+    const int half = (u_hi - u_lo + 1) / 2;
+    const int a_lo = warp == 1 ? 0 : half, a_hi = warp == 1 ? half : u_hi - u_lo;
     uint64_t adesc[8];
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-      const int t0 = min(2 * a, taps - 1), t1 = min(2 * a + 1, taps - 1);
-      const int sh0 = (t0 / S) * Wp + t0 % S, sh1 = (t1 / S) * Wp + t1 % S;
-      adesc[a] = sm100::make_sw128_desc(sm100::smem_u32(xb) + sh0 * 128, (sh1 - sh0) * 128, 1024);
+      const int u = min(u_lo + a, gg.units - 1);
+      int sh0, lbo;
+      if (gg.CP == 1) {
+        const int t0 = min(2 * u, taps - 1), t1 = min(2 * u + 1, taps - 1);
+        sh0 = (t0 / S) * Wp + t0 % S;
+        lbo = ((t1 / S) * Wp + t1 % S - sh0) * 128;       // second tap's 64 channels
+      } else {
+        sh0 = (u / S) * Wp + u % S;
+        lbo = gg.xps;                                      // channels 64..127: the second plane
+      }
+      adesc[a] = sm100::make_sw128_desc(sm100::smem_u32(smem) + sh0 * 128, lbo, 1024);
     }
-    const uint64_t bdesc0 = sm100::make_sw128_desc(sm100::smem_u32(yb), 16, 1024);
+    const uint64_t bdesc0 = sm100::make_sw128_desc(sm100::smem_u32(smem + gg.CP * gg.xps), gg.yps, 1024);
     const int ksteps = G * Wp / 16;
-    const int a_lo = warp == 1 ? 0 : (pairs + 1) / 2, a_hi = warp == 1 ? (pairs + 1) / 2 : pairs;
     int b = 0; uint32_t phase = 0;
     uint32_t acc = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = split; t < num_tiles; t += splits) {
       sm100::mbar_wait(&full[b], phase);
       sm100::tc_fence_after();
-      const uint64_t xo = (uint64_t)((b * xstride) >> 4), yo = (uint64_t)((b * ystride) >> 4);
+      const uint64_t bo = (uint64_t)((b * gg.bufb) >> 4);
       for (int ks = 0; ks < ksteps; ++ks) {
         const uint64_t ko = (uint64_t)(ks * 128);  // 16 slots × 128 B >> 4
-        const uint64_t bd = bdesc0 + yo + ko;
+        const uint64_t bd = bdesc0 + bo + ko;
 #pragma unroll
         for (int a = 0; a < 8; ++a)
           if (a >= a_lo && a < a_hi && sm100::elect_one())
-            sm100::mma_bf16(tmem_base + a * 64, adesc[a] + xo + ko, bd, idesc, acc);
+            sm100::mma_bf16(tmem_base + a * N, adesc[a] + bo + ko, bd, idesc, acc);
         acc = 1;
       }
       if (sm100::elect_one()) sm100::mma_commit(&empty[b]);
       __syncwarp();
-      if (++b == wgp::NBUF) { b = 0; phase ^= 1; }
+      if (++b == nbuf) { b = 0; phase ^= 1; }
     }
     if (sm100::elect_one()) sm100::mma_commit(&done[warp == 1 ? 0 : 1]);
     __syncwarp();
   } else if (warp >= 4) {
-    // ===================== epilogue: partial dWᵀ rows into this CTA's slab =====================
+    // ===================== epilogue: partial dWᵀ rows into this split's slab =====================
+    // D row r of unit u ↔ dW column 128·u + r (tap·C + c, contiguous in KRSC)
     const int ew = warp - 4, eq = warp & 3, eh = ew >> 2;
-    const int RSC = taps * 64;
-    float* slab = reinterpret_cast<float*>(p.D) + (long long)blockIdx.x * p.split_stride;
-    const bool any = blockIdx.x < num_tiles;
+    const int RSC = taps * p.cC;
+    float* slab = reinterpret_cast<float*>(p.D) + (long long)split * p.split_stride;
+    const bool any = split < num_tiles && split < splits;
     if (any) {
       sm100::mbar_wait(&done[0], 0);
       sm100::mbar_wait(&done[1], 0);
       sm100::tc_fence_after();
     }
-    for (int a = 0; a < pairs; ++a) {
-      const int col = 128 * a + eq * 32 + lane;  // D row → dW column (tap·64 + c)
-      uint32_t r[32];
-      if (any) {
-        sm100::tmem_ld_32x32b_x32(tmem_base + a * 64 + eh * 32 + ((uint32_t)(eq * 32) << 16), r);
-        sm100::tmem_ld_wait();
-      }
-      if (col < RSC) {
+    if (split < splits) {
+      for (int a = 0; a < u_hi - u_lo; ++a) {
+        const int col = 128 * (u_lo + a) + eq * 32 + lane;
+        for (int ch = 0; ch < N / 64; ++ch) {
+          const int k0 = eh * (N / 2) + ch * 32;
+          uint32_t r[32];
+          if (any) {
+            sm100::tmem_ld_32x32b_x32(tmem_base + a * N + k0 + ((uint32_t)(eq * 32) << 16), r);
+            sm100::tmem_ld_wait();
+          }
+          if (col < RSC) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) slab[(long long)(eh * 32 + j) * RSC + col] = any ? __uint_as_float(r[j]) : 0.f;
+            for (int j = 0; j < 32; ++j) slab[(long long)(k0 + j) * RSC + col] = any ? __uint_as_float(r[j]) : 0.f;
+          }
+        }
       }
     }
   }
@@ -2436,29 +2476,27 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
 bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                       cudaStream_t s) {
   static const int on = [] { const char* e = getenv("BE_WGRAD_PATCH"); return e ? atoi(e) : 1; }();
-  if (!on || g.stride != 1 || g.C != 64 || g.K != 64 || g.R * g.S > 16 || dwt != BE_F32) return false;
-  int Wp = 16;
-  while (Wp < g.Q + g.S - 1) Wp *= 2;
-  if (Wp > BM) return false;
-  const int G = BM / Wp;
+  if (!on || g.stride != 1 || dwt != BE_F32 || g.R * g.S > 16) return false;
+  if (!((g.C == 64 && g.K == 64) || (g.C == 128 && g.K == 128))) return false;
+  const wgp::Geo gg = wgp::geo(g.Q, g.R, g.S, g.C, g.K);
+  if (gg.Wp > BM || gg.nbuf < 2 || gg.G + g.R - 1 > 256 || gg.ngroups * 2 > ctx().num_sms) return false;
   if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
-  const int xbytes = (G + g.R - 1) * Wp * 128, ybytes = G * Wp * 128;
-  const int xstride = (xbytes + wgp::kSlack + 1023) / 1024 * 1024, ystride = (ybytes + 1023) / 1024 * 1024;
-  const int smem = 1024 + wgp::NBUF * (xstride + ystride) + 256;
-  if (smem > 227 * 1024 || G + g.R - 1 > 256) return false;
+  const int smem = 1024 + gg.nbuf * gg.bufb + 256;
+  if (smem > 227 * 1024) return false;
   GemmParams p;
   memset(&p, 0, sizeof(p));
   const uint64_t dx4[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
   const uint64_t dy4[4] = {(uint64_t)g.K, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.N};
-  if (!encode_4d_tiled(&p.ta[0], x, dx4, 64, Wp, G + g.R - 1, 1)) return false;
-  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, Wp, G, 1)) return false;
+  if (!encode_4d_tiled(&p.ta[0], x, dx4, 64, gg.Wp, gg.G + g.R - 1, 1)) return false;
+  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, gg.Wp, gg.G, 1)) return false;
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
-  p.cstride = 1; p.cpad = g.pad; p.sh_wb = Wp; p.sh_hb = G;
+  p.cstride = 1; p.cpad = g.pad; p.N = g.K;
   const int RSC = g.R * g.S * g.C;
-  const int tiles = g.N * ((g.P + G - 1) / G);
-  const int grid = std::min(tiles, ctx().num_sms);
-  p.split_stride = 64LL * RSC;
-  Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)grid * p.split_stride, s);
+  const int tiles = g.N * ((g.P + gg.G - 1) / gg.G);
+  const int splits = std::max(1, std::min(tiles, ctx().num_sms / gg.ngroups));
+  const int grid = splits * gg.ngroups;
+  p.split_stride = (long long)g.K * RSC;
+  Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * p.split_stride, s);
   p.D = ws->ptr;
   static bool attr = false;
   if (!attr) {
@@ -2473,9 +2511,9 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   prof_end(pidx, s);
   after_launch("conv_wgrad_patch");
   g_tc_calls++;
-  const long long total = 64LL * RSC;
+  const long long total = (long long)g.K * RSC;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw,
+  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
                                        RSC, 1, beta, nullptr, 0);
   after_launch("conv_wgrad_patch_reduce");
   ctx().alloc.free(ws);

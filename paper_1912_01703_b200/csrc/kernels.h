@@ -112,7 +112,7 @@ void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float
 // ------------------------------------------------------------------ conv / pool / bn
 // Implicit-GEMM convolution on tcgen05 (bf16, C % 64 == 0): y[NPQ, K] =
 // conv(x NHWC, w KRSC) (+bias, act, beta). Returns false when unsupported.
-// stride-1 conv weight gradient (C = K = 64) from one shared input patch per
+// stride-1 conv weight gradient (C = K ∈ {64, 128}) from one shared input patch per
 // tile with shifted UMMA operands (gemm_sm100.cu conv_wgrad_patch_kernel);
 // dw fp32 [K, R·S·C], dw = (beta ? dw : 0) + dW.  false: shape not supported
 bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
