@@ -2506,7 +2506,7 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   }
   const double flops = 2.0 * g.N * g.P * g.Q * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.N * g.P * g.Q * g.K) * 2.0 + 4.0 * g.K * RSC;
-  const int pidx = prof_begin("conv_wgrad_patch", flops, bytes, g.K, RSC, g.N * g.P * g.Q, s);
+  const int pidx = prof_begin("conv_tc_wgrad_patch", flops, bytes, g.K, RSC, g.N * g.P * g.Q, s);
   conv_wgrad_patch_kernel<<<grid, wgp::kThreads, smem, s>>>(p);
   prof_end(pidx, s);
   after_launch("conv_wgrad_patch");
