@@ -1888,6 +1888,231 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------- stem conv wgrad: im2col built in smem from the patch
+// dW[k, r, s, c] = Σ_{n,p,q} dY[n,p,q,k] · x[n, p·st−pad+r, q·st−pad+s, c] for
+// the C = 8 stem (ResNet conv1 7×7/2): the materialised im2col is 2.5 GB at
+// b256 (≈0.9 ms to write + 0.45 ms for the GEMM to read).  Here a tile is one
+// output row: its input patch is copied once into the stem kernel's
+// phase-split layout (cp.async, 4 warps); 4 build warps then assemble, 16
+// output pixels at a time, the im2col slice [16 pixels × R·S·8] in smem as an
+// MN-major SW128 operand (M = (tap, c) — 8 taps of 8 channels per 128-B atom,
+// K = pixels; 16-B smem→smem copies) — the columns never leave the SM.
+// D[(tap, c), k] = Σ slice · dY slice (dY row by TMA, MN-major SW128, q ≥ Q
+// zero-filled) accumulates in TMEM (⌈R·S·8/128⌉ M-tiles × 64 columns) over
+// the CTA's rows; one fp32 split-K slab per CTA, fixed-order splitk_reduce.
+namespace wgs {
+constexpr int kThreads = 512;   // w0-3 patch copy, w4-7 slice build, w8 MMA, w9 dY TMA, w10 TMEM, w12-15 epilogue
+constexpr int kCopy = 128;
+constexpr int NY = 2;           // dY row buffers (16 KB each)
+constexpr int kZeroBytes = 4096;
+struct Geo { int L, phb, patch_bytes, Mt, slb, ns, np, smem; };
+inline Geo geo(const ConvGeom& g) {
+  Geo e{};
+  e.L = g.Q + (g.S - 1) / g.stride;
+  e.phb = (g.R * e.L * 16 + 127) / 128 * 128 + (128 / g.stride) / 16 * 16;
+  e.patch_bytes = g.stride * e.phb;
+  e.Mt = (g.R * g.S * 8 + 127) / 128;
+  e.slb = e.Mt * 4096;
+  const int fixed = 1024 + NY * 16384 + kZeroBytes + 512;
+  // deep slice ring (the build → MMA → release loop is latency-bound), two patch buffers
+  e.np = 2;
+  e.ns = (227 * 1024 - fixed - e.np * e.patch_bytes) / e.slb;
+  if (e.ns > 8) e.ns = 8;
+  e.smem = fixed + e.ns * e.slb + e.np * e.patch_bytes;
+  return e;
+}
+}  // namespace wgs
+
+__global__ void __launch_bounds__(wgs::kThreads, 1) conv_wgrad_stem_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int st = p.cstride, R = p.cR, S = p.cS, L = p.st_L, taps = R * S;
+  const int NS = p.st_nbuf & 0xff, NP = p.st_nbuf >> 8, Mt = p.st_taps, slb = Mt * 4096;
+  const int patch_bytes = st * p.st_phb;
+  uint8_t* slices = smem;                              // NS × Mt × [2 atoms × 16 rows × 128 B]
+  uint8_t* ybuf = slices + NS * slb;                   // NY × 128 rows × 128 B
+  uint8_t* patch = ybuf + wgs::NY * 16384;             // NP × patch_bytes
+  uint8_t* zero = patch + NP * patch_bytes;
+  int* tab = reinterpret_cast<int*>(zero + wgs::kZeroBytes);   // per tap: patch offset at q = 0
+  uint64_t* full_p = reinterpret_cast<uint64_t*>(tab + 128);
+  uint64_t* empty_p = full_p + 4;
+  uint64_t* full_y = empty_p + 4;
+  uint64_t* empty_y = full_y + wgs::NY;
+  uint64_t* full_s = empty_y + wgs::NY;
+  uint64_t* empty_s = full_s + 8;
+  uint64_t* done = empty_s + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < (NS * slb) / 16; i += blockDim.x) reinterpret_cast<uint4*>(slices)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < (NP * patch_bytes + wgs::kZeroBytes) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(patch)[i] = make_uint4(0, 0, 0, 0);
+  for (int t = threadIdx.x; t < taps; t += blockDim.x) {
+    const int r = t / S, s_ = t % S;
+    tab[t] = (s_ % st) * p.st_phb + (r * L + s_ / st) * 16;
+  }
+  sm100::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NP; ++b) { sm100::mbar_init(&full_p[b], wgs::kCopy); sm100::mbar_init(&empty_p[b], 4); }
+    for (int b = 0; b < wgs::NY; ++b) { sm100::mbar_init(&full_y[b], 1); sm100::mbar_init(&empty_y[b], 1); }
+    for (int b = 0; b < NS; ++b) { sm100::mbar_init(&full_s[b], 4); sm100::mbar_init(&empty_s[b], 1); }
+    sm100::mbar_init(done, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 10) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.cN * p.cP;
+  const int nks = (p.cQ + 15) / 16;
+
+  if (warp < 4) {
+    // ===================== patch copy (as conv_stem_kernel), one group in flight =====================
+    const int tid = threadIdx.x, span = L * st;
+    const int ua = tid, ub = tid + wgs::kCopy;
+    const int wa = ua - p.cpad, wb = ub - p.cpad;
+    const bool va = ua < span, vb = ub < span;
+    const bool oka = va && (unsigned)wa < (unsigned)p.cW, okb = vb && (unsigned)wb < (unsigned)p.cW;
+    const uint32_t da = (ua % st) * p.st_phb + (ua / st) * 16, db = (ub % st) * p.st_phb + (ub / st) * 16;
+    const long long xa = oka ? (long long)wa * 8 : 0, xb = okb ? (long long)wb * 8 : 0;
+    const uint32_t L16 = L * 16;
+    int b = 0; uint32_t phase = 0;
+    int prev = -1;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int n = t / p.cP, pp = t - n * p.cP;
+      sm100::mbar_wait_sleep(&empty_p[b], phase ^ 1, 200);
+      uint32_t dst = sm100::smem_u32(patch + b * patch_bytes);
+      const int h0 = pp * st - p.cpad;
+      const uint16_t* img = p.x + (long long)n * p.cH * p.cW * 8;
+      for (int r = 0; r < R; ++r, dst += L16) {
+        const int h = h0 + r;
+        const bool hok = (unsigned)h < (unsigned)p.cH;
+        const uint16_t* srow = img + (long long)(hok ? h : 0) * p.cW * 8;
+        if (va) sm100::cp_async_16(dst + da, hok && oka ? srow + xa : p.x, hok && oka ? 16u : 0u);
+        if (vb) sm100::cp_async_16(dst + db, hok && okb ? srow + xb : p.x, hok && okb ? 16u : 0u);
+      }
+      sm100::cp_async_commit();
+      if (prev >= 0) {
+        sm100::cp_async_wait<1>();
+        sm100::fence_proxy_async();
+        sm100::mbar_arrive(&full_p[prev]);
+      }
+      prev = b;
+      if (++b == NP) { b = 0; phase ^= 1; }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    if (prev >= 0) sm100::mbar_arrive(&full_p[prev]);
+  } else if (warp < 8) {
+    // ===================== im2col slice build: 16 pixels × taps × 16 B =====================
+    // thread tid owns items idx = tid + 128·j (pixel i = idx & 15, tap = idx >> 4),
+    // the same for every slice: its patch / slice offsets are computed once and
+    // each slice is up to 16 independent ld.shared.v4 → st.shared.v4 pairs
+    const int tid = threadIdx.x - 128;
+    const int nitems = 16 * taps;
+    uint32_t so[16], dof[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int idx = tid + 128 * j;
+      const int i = idx & 15, tap = idx >> 4;
+      so[j] = idx < nitems ? (uint32_t)(tab[tap] + i * 16) : 0u;
+      dof[j] = idx < nitems ? (uint32_t)((tap >> 3) * 2048 + i * 128 + (((tap & 7) ^ (i & 7)) << 4)) : 0u;
+    }
+    const uint32_t patch_s = sm100::smem_u32(patch), slices_s = sm100::smem_u32(slices);
+    int ti = 0, si = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+      const int bp = ti % NP;
+      sm100::mbar_wait(&full_p[bp], (uint32_t)((ti / NP) & 1));
+      const uint32_t pb = patch_s + bp * patch_bytes;
+      for (int ks = 0; ks < nks; ++ks, ++si) {
+        const int sb = si % NS;
+        sm100::mbar_wait(&empty_s[sb], (uint32_t)((si / NS) & 1) ^ 1u);
+        const uint32_t src = pb + ks * 256, dst = slices_s + sb * slb;  // 16 pixels × 16 B per slice step
+        uint4 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (tid + 128 * j < nitems)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w) : "r"(src + so[j]));
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (tid + 128 * j < nitems)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};"
+                         :: "r"(dst + dof[j]), "r"(v[j].x), "r"(v[j].y), "r"(v[j].z), "r"(v[j].w) : "memory");
+        sm100::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&full_s[sb]);
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&empty_p[bp]);
+    }
+  } else if (warp == 8) {
+    // ===================== MMA: per slice, Mt × (M = 128, N = 64, K = 16) =====================
+    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 1, 1);
+    const uint64_t a0 = sm100::make_sw128_desc(sm100::smem_u32(slices), 2048, 1024);
+    const uint64_t b0 = sm100::make_sw128_desc(sm100::smem_u32(ybuf), 16, 1024);
+    int ti = 0, si = 0;
+    uint32_t acc = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+      const int by = ti % wgs::NY;
+      sm100::mbar_wait(&full_y[by], (uint32_t)((ti / wgs::NY) & 1));
+      for (int ks = 0; ks < nks; ++ks, ++si) {
+        const int sb = si % NS;
+        sm100::mbar_wait(&full_s[sb], (uint32_t)((si / NS) & 1));
+        sm100::tc_fence_after();
+        const uint64_t bd = b0 + (uint64_t)((by * 16384 + ks * 2048) >> 4);
+        const uint64_t ab = a0 + (uint64_t)((sb * slb) >> 4);
+        for (int mt = 0; mt < Mt; ++mt)
+          if (sm100::elect_one()) sm100::mma_bf16(tmem_base + mt * 64, ab + (uint64_t)(mt * 256), bd, idesc, acc);
+        acc = 1;
+        if (sm100::elect_one()) sm100::mma_commit(&empty_s[sb]);
+        __syncwarp();
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&empty_y[by]);
+      __syncwarp();
+    }
+    if (sm100::elect_one()) sm100::mma_commit(done);
+    __syncwarp();
+  } else if (warp == 9) {
+    if (lane == 0) {
+      int ti = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+        const int by = ti % wgs::NY, n = t / p.cP, pp = t - n * p.cP;
+        sm100::mbar_wait(&empty_y[by], (uint32_t)((ti / wgs::NY) & 1) ^ 1u);
+        sm100::mbar_arrive_expect_tx(&full_y[by], 16384u);
+        sm100::tma_load_4d(&p.tb[0], &full_y[by], ybuf + by * 16384, 0, 0, pp, n);
+      }
+    }
+  } else if (warp >= 12) {
+    // ===================== epilogue: D row m = tap·8 + c → slab[k][m] =====================
+    const int eq = warp & 3;
+    const int RSC = taps * 8;
+    float* slab = reinterpret_cast<float*>(p.D) + (long long)blockIdx.x * p.split_stride;
+    sm100::mbar_wait_sleep(done, 0, 2000);
+    sm100::tc_fence_after();
+    for (int mt = 0; mt < Mt; ++mt) {
+      const int m = mt * 128 + eq * 32 + lane;
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + mt * 64 + h * 32 + ((uint32_t)(eq * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        if (m < RSC) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) slab[(long long)(h * 32 + j) * RSC + m] = __uint_as_float(r[j]);
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 10) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -2516,6 +2741,50 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
                                        RSC, 1, beta, nullptr, 0);
   after_launch("conv_wgrad_patch_reduce");
+  ctx().alloc.free(ws);
+  return true;
+}
+
+// stem conv weight gradient (conv_wgrad_stem_kernel): C = 8, K = 64, Q ≤ 128,
+// R·S ≤ 128; dw fp32 [64, R·S·8] (+)= dW; false when not applicable
+bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
+                     cudaStream_t s) {
+  static const int on = [] { const char* e = getenv("BE_WGRAD_STEM"); return e ? atoi(e) : 1; }();
+  if (!on || g.C != 8 || g.K != 64 || dwt != BE_F32 || g.Q > BM || g.Q < 1 || g.R * g.S > 128) return false;
+  const wgs::Geo e = wgs::geo(g);
+  if (e.L * g.stride > 2 * wgs::kCopy || e.ns < 2 || e.smem > 227 * 1024) return false;
+  if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const uint64_t dy4[4] = {(uint64_t)g.K, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.N};
+  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, 128, 1, 1)) return false;
+  p.x = reinterpret_cast<const uint16_t*>(x);
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
+  p.cstride = g.stride; p.cpad = g.pad;
+  p.st_L = e.L; p.st_phb = e.phb; p.st_taps = e.Mt; p.st_nbuf = e.ns | (e.np << 8);
+  const int RSC = g.R * g.S * 8;
+  const int grid = std::min(g.N * g.P, ctx().num_sms);
+  p.split_stride = 64LL * RSC;
+  Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)grid * p.split_stride, s);
+  p.D = ws->ptr;
+  static bool attr = false;
+  if (!attr) {
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    attr = true;
+  }
+  const double flops = 2.0 * g.N * g.P * g.Q * 64.0 * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * 8 + (double)g.N * g.P * g.Q * 64) * 2.0 + 4.0 * 64 * RSC;
+  const int pidx = prof_begin("conv_tc_wgrad_stem", flops, bytes, 64, RSC, g.N * g.P * g.Q, s);
+  conv_wgrad_stem_kernel<<<grid, wgs::kThreads, e.smem, s>>>(p);
+  prof_end(pidx, s);
+  after_launch("conv_wgrad_stem");
+  g_tc_calls++;
+  const long long total = 64LL * RSC;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw, RSC,
+                                       1, beta, nullptr, 0);
+  after_launch("conv_wgrad_stem_reduce");
   ctx().alloc.free(ws);
   return true;
 }

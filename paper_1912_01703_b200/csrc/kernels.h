@@ -117,6 +117,10 @@ void sgd_multi(const SgdEntry* e, int n_entries, float lr, float momentum, float
 // dw fp32 [K, R·S·C], dw = (beta ? dw : 0) + dW.  false: shape not supported
 bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                       cudaStream_t s);
+// stem conv weight gradient (C = 8, K = 64): im2col slices built in smem from
+// a per-row input patch (gemm_sm100.cu conv_wgrad_stem_kernel); false: not applicable
+bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
+                     cudaStream_t s);
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
                    float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr);
 // bf16 wf[C,R,S,K] = w[K,R−1−r,S−1−s,C] (dgrad of a stride-1 conv as a convolution)

@@ -91,7 +91,9 @@ static void vjp_conv(Node* n, GradSink& sink) {
       variant = tune_choose(key, patch_ok ? 4 : (shift_ok ? 3 : 2), 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);
-    if (variant == 3 && k::conv_wgrad_patch(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
+    if (g.C == 8 && opd == BE_BF16 && !e0 && k::conv_wgrad_stem(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
+      sink.commit(1);
+    } else if (variant == 3 && k::conv_wgrad_patch(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
       if (e1) cudaEventRecord(e1, s);
       sink.commit(1);
     } else {

@@ -41,6 +41,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(addr), "r"(parity) : "memory");
 }
 
+// wait with back-off: for warps that wait long (an epilogue waiting for the
+// whole main loop, producers running far ahead) — their spinning would take
+// issue slots from the warps doing the work on the same SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 // L2 prefetch of a 2-D tensor-map box (no smem, no barrier)
 __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
