@@ -69,7 +69,8 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * NS * RG::CH);
   uint64_t* empty = full + NST;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int lanes = C >> 3, rpi = kCons / lanes;
+  const int lanes = C >> 3, rpi = kCons / lanes;   // rows per iteration (threads ≥ rpi·lanes idle when C ∤ 2048)
+  const int iterb = rpi * C * 2;                    // bytes per iteration (4 KB when C | 2048)
   const int64_t crow = (int64_t)ITERS * rpi;
   const int64_t nchunks = r1 > r0 ? (r1 - r0 + crow - 1) / crow : 0;
   if (t == 0) {
@@ -93,6 +94,7 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
     return;
   }
   const int rin = t / lanes;
+  const bool active = rin < rpi;
   for (int64_t i = 0; i < nchunks; ++i) {
     const int st = (int)(i % NST);
     sm100::mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
@@ -100,11 +102,11 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int64_t row = rs + it * rpi + rin;
-      if (row < r1) {
+      if (active && row < r1) {
         uint4 v[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k)
-          v[k] = *reinterpret_cast<const uint4*>(ring + (st * NS + k) * RG::CH + it * kIter + t * 16);
+          v[k] = *reinterpret_cast<const uint4*>(ring + (st * NS + k) * RG::CH + it * iterb + t * 16);
         body(row, v);
       }
     }
@@ -117,7 +119,7 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
 __device__ __forceinline__ void combine_partials(const float (&s0)[8], const float (&s1)[8], int C, float* sm,
                                                  float* part0, float* part1) {
   const int t = threadIdx.x, lanes = C >> 3, rpi = kCons / lanes;
-  if (t < kCons) {
+  if (t < rpi * lanes) {
     const int v = t % lanes, rl = t / lanes;
 #pragma unroll
     for (int j = 0; j < 8; ++j) { sm[rl * C + v * 8 + j] = s0[j]; sm[kCons * 8 + rl * C + v * 8 + j] = s1[j]; }
@@ -311,6 +313,41 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
   }
 }
 
+// fused ReLU backward + bias gradient: dz = gy·1[y > 0] (stored), Σ_rows dz per column
+__global__ void __launch_bounds__(kThr, 3) relu_colsum_stream_kernel(const uint16_t* __restrict__ gy,
+                                                                 const uint16_t* __restrict__ y, uint16_t* dz,
+                                                                 int64_t rows, int C, float* part, int64_t rps) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  float s0[8] = {}, s1[8] = {};
+  const uint16_t* src[2] = {gy, y};
+  stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) {
+    float g[8], m[8];
+    unpack8s(v[0], g);
+    unpack8s(v[1], m);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { g[j] = m[j] > 0.f ? g[j] : 0.f; s0[j] += g[j]; }
+    *reinterpret_cast<uint4*>(dz + row * C + c) = pack8s(g);
+  });
+  __syncthreads();
+  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part, part + (int64_t)gridDim.x * C);
+}
+// out[c] = Σ_split part[split][c] (fixed order, four running sums) (+ out[c] when beta ≠ 0)
+__global__ void colsum_partials_finalize(const float* __restrict__ part, int splits, int C, float* out, float beta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  int i = 0;
+  for (; i + 4 <= splits; i += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] += part[(int64_t)(i + u) * C + c];
+  }
+  for (int u = 0; i < splits; ++i, ++u) a[u] += part[(int64_t)i * C + c];
+  const float v = (a[0] + a[1]) + (a[2] + a[3]);
+  out[c] = v + (beta != 0.f ? out[c] : 0.f);
+}
+
 template <typename K>
 void set_smem(K kern, int bytes) {
   BE_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -327,6 +364,27 @@ bool enabled() {
 
 bool bn_stream_ok(const void* a, int64_t rows, int C) {
   return enabled() && C >= 8 && C <= 2048 && (C & (C - 1)) == 0 && rows > 0 && aligned16(a);
+}
+
+bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int64_t rows, int C, float* out,
+                        float beta, cudaStream_t s) {
+  if (!enabled() || C < 8 || C > 2048 || C % 8 != 0 || rows <= 0 || !aligned16(gy) || !aligned16(y) ||
+      !aligned16(dz))
+    return false;
+  static bool once = [] { set_smem(relu_colsum_stream_kernel, kS2); return true; }();
+  (void)once;
+  const int64_t rpi = kCons / (C / 8);
+  const int64_t crow = 2 * rpi;
+  const int64_t sp = std::max<int64_t>(1, std::min<int64_t>(rows / (crow * 4) + 1, stream_blocks(3)));
+  const int64_t rps = (rows + sp - 1) / sp;
+  Block* tmp = ctx().alloc.allocate(sizeof(float) * 2 * sp * C, s);
+  float* part = reinterpret_cast<float*>(tmp->ptr);
+  relu_colsum_stream_kernel<<<(unsigned)sp, kThr, kS2, s>>>(gy, y, dz, rows, C, part, rps);
+  after_launch("relu_colsum_stream");
+  colsum_partials_finalize<<<(C + 255) / 256, 256, 0, s>>>(part, (int)sp, C, out, beta);
+  after_launch("relu_colsum_finalize");
+  ctx().alloc.free(tmp);
+  return true;
 }
 
 int64_t bn_stream_splits(int64_t rows, int C, int64_t cap) {

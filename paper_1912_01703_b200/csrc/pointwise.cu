@@ -597,8 +597,14 @@ void add_bcast(const void* a, const void* b, void* y, const BcastDesc& d, be_dty
 void colsum(const void* x, int64_t rows, int64_t cols, be_dtype dt, float* out, float beta, cudaStream_t s) {
   colsum_impl(0, x, nullptr, nullptr, rows, cols, dt, out, beta, s);
 }
+bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int64_t rows, int C, float* out,
+                        float beta, cudaStream_t s);  // bn_stream.cu
 void relu_bwd_colsum(const void* dy, const void* y, void* dz, int64_t rows, int64_t cols, be_dtype dt, float* db,
                      float db_beta, int act, cudaStream_t s) {
+  if (act && dt == BE_BF16 && cols <= 2048 &&
+      relu_colsum_stream(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(y),
+                         reinterpret_cast<uint16_t*>(dz), rows, (int)cols, db, db_beta, s))
+    return;
   if (act) colsum_impl(1, dy, y, dz, rows, cols, dt, db, db_beta, s);
   else colsum_impl(0, dy, nullptr, nullptr, rows, cols, dt, db, db_beta, s);
 }
