@@ -136,6 +136,7 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
 // forward statistics: shifted sums Σ(x−K), Σ(x−K)² with K = x[0, c]
 __global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t* __restrict__ x, int64_t rows, int C,
                                                                float* part0, float* part1, int64_t rps) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
                                                                 const float* __restrict__ bsh,
                                                                 const uint16_t* __restrict__ rmask,
                                                                 uint16_t* __restrict__ gout) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, int act, int64_t rps,
                                                                const uint16_t* __restrict__ res) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ sums, int64_t rps,
                                                             const float* __restrict__ bsh) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
 __global__ void __launch_bounds__(kThr, 3) relu_colsum_stream_kernel(const uint16_t* __restrict__ gy,
                                                                  const uint16_t* __restrict__ y, uint16_t* dz,
                                                                  int64_t rows, int C, float* part, int64_t rps) {
+  pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(kThr, 3) relu_colsum_stream_kernel(const uint1
 // thread than one thread per column)
 __global__ void __launch_bounds__(256) colsum_partials_finalize(const float* __restrict__ part, int splits, int C,
                                                                 float* out, float beta) {
+  pdl_entry();
   __shared__ float sm[32][9];
   const int cl = threadIdx.x & 7, sub = threadIdx.x >> 3;
   const int c = blockIdx.x * 8 + cl;
@@ -388,9 +394,9 @@ bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int
   const int64_t rps = (rows + sp - 1) / sp;
   Block* tmp = ctx().alloc.allocate(sizeof(float) * 2 * sp * C, s);
   float* part = reinterpret_cast<float*>(tmp->ptr);
-  relu_colsum_stream_kernel<<<(unsigned)sp, kThr, kS2, s>>>(gy, y, dz, rows, C, part, rps);
+  launch_pdl(relu_colsum_stream_kernel, (unsigned)sp, kThr, kS2, s, gy, y, dz, rows, C, part, rps);
   after_launch("relu_colsum_stream");
-  colsum_partials_finalize<<<(C + 7) / 8, 256, 0, s>>>(part, (int)sp, C, out, beta);
+  launch_pdl(colsum_partials_finalize, (C + 7) / 8, 256, 0, s, part, (int)sp, C, out, beta);
   after_launch("relu_colsum_finalize");
   ctx().alloc.free(tmp);
   return true;
@@ -407,7 +413,7 @@ void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float
   static bool once = [] { set_smem(bn_stats_stream_kernel, kS1); return true; }();
   (void)once;
   const int64_t rps = (rows + sp - 1) / sp;
-  bn_stats_stream_kernel<<<(unsigned)sp, kThr, kS1, s>>>(x, rows, C, part0, part1, rps);  // caller: after_launch
+  launch_pdl(bn_stats_stream_kernel, (unsigned)sp, kThr, kS1, s, x, rows, C, part0, part1, rps);  // caller: after_launch
 }
 
 void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
@@ -421,10 +427,10 @@ void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
   (void)once;
   const int64_t rps = (rows + sp - 1) / sp;
   if (rmask)
-    bn_reduce_stream_kernel<true><<<(unsigned)sp, kThr, kS3, s>>>(x, gy, act, rows, C, mean, invstd, part0, part1,
+    launch_pdl(bn_reduce_stream_kernel<true>, (unsigned)sp, kThr, kS3, s, x, gy, act, rows, C, mean, invstd, part0, part1,
                                                                   rps, gam, bsh, rmask, gout);
   else
-    bn_reduce_stream_kernel<false><<<(unsigned)sp, kThr, kS2, s>>>(x, gy, act, rows, C, mean, invstd, part0, part1,
+    launch_pdl(bn_reduce_stream_kernel<false>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
                                                                    rps, gam, bsh, nullptr, nullptr);
   after_launch("bn_reduce_stream");
 }
@@ -440,10 +446,10 @@ void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const 
   const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
   const int64_t rps = (rows + sp - 1) / sp;
   if (res)
-    bn_apply_stream_kernel<true><<<(unsigned)sp, kThr, kS2, s>>>(x, y, rows, C, mean, invstd, gamma, beta, act, rps,
+    launch_pdl(bn_apply_stream_kernel<true>, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
                                                                  res);
   else
-    bn_apply_stream_kernel<false><<<(unsigned)sp, kThr, kS1, s>>>(x, y, rows, C, mean, invstd, gamma, beta, act, rps,
+    launch_pdl(bn_apply_stream_kernel<false>, (unsigned)sp, kThr, kS1, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
                                                                   nullptr);
   after_launch("bn_apply_stream");
 }
@@ -460,10 +466,10 @@ void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, 
   const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
   const int64_t rps = (rows + sp - 1) / sp;
   if (dx_beta != 0.f)
-    bn_dx_stream_kernel<true><<<(unsigned)sp, kThr, kS3, s>>>(gy, x, act, dx, rows, C, mean, invstd, gamma, sums, rps,
+    launch_pdl(bn_dx_stream_kernel<true>, (unsigned)sp, kThr, kS3, s, gy, x, act, dx, rows, C, mean, invstd, gamma, sums, rps,
                                                               bsh);
   else
-    bn_dx_stream_kernel<false><<<(unsigned)sp, kThr, kS2, s>>>(gy, x, act, dx, rows, C, mean, invstd, gamma, sums,
+    launch_pdl(bn_dx_stream_kernel<false>, (unsigned)sp, kThr, kS2, s, gy, x, act, dx, rows, C, mean, invstd, gamma, sums,
                                                                rps, bsh);
   after_launch("bn_dx_stream");
 }

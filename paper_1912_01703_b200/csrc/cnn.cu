@@ -895,6 +895,7 @@ __global__ void __launch_bounds__(1024) bn_finalize_v(const float* __restrict__ 
                                                       float eps, float* mean, float* invstd, float* run_mean,
                                                       float* run_var, float momentum, float* dgamma, float* dbeta,
                                                       float gb_beta, float* sums) {
+  pdl_entry();
   // 8 channels × 128 sub-lanes: each sub-lane sums every 128th split with all
   // its loads in flight (≤ 4 per operand for the usual ≤ 592 splits), then a
   // fixed-order two-level sum over the sub-lanes (deterministic)
@@ -1297,7 +1298,7 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
       bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
                                           partial + sp * C, rps);
     after_launch("bn_stats_v");
-    bn_finalize_v<0><<<(C + 7) / 8, 1024, 0, s>>>(partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
+    launch_pdl(bn_finalize_v<0>, (C + 7) / 8, 1024, 0, s, partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
                                                     invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
                                                     nullptr);
     after_launch("bn_stats_finalize_v");
@@ -1318,7 +1319,7 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
 }
 void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C, float eps, float* mean,
                             float* invstd, float* run_mean, float* run_var, float momentum, cudaStream_t s) {
-  bn_finalize_v<0><<<(C + 7) / 8, 1024, 0, s>>>(partial, partial + (int64_t)parts * C, parts, C, rows, nullptr,
+  launch_pdl(bn_finalize_v<0>, (C + 7) / 8, 1024, 0, s, partial, partial + (int64_t)parts * C, parts, C, rows, nullptr,
                                                   BE_F32, eps, mean, invstd, run_mean, run_var, momentum, nullptr,
                                                   nullptr, 0.f, nullptr);
   after_launch("bn_stats_from_partials");
@@ -1373,7 +1374,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
                                             reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
         after_launch("bn_bwd_reduce_mask_bf16");
       }
-      bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
+      launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                       nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
       after_launch("bn_bwd_finalize_v");
       if (dx && stream) {
@@ -1412,7 +1413,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
                                           bn_beta ? gamma : nullptr, bn_beta);
     if (!stream) after_launch("bn_bwd_reduce_v");
-    bn_finalize_v<2><<<(C + 7) / 8, 1024, 0, s>>>(p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
+    launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
                                                     nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
     after_launch("bn_bwd_finalize_v");
     if (dx && stream) {

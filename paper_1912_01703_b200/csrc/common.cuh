@@ -7,6 +7,18 @@
 
 namespace be { namespace dev {
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// become resident while its stream predecessor is still finishing; it must
+// execute pdl_entry() before touching global memory.  griddepcontrol.wait
+// returns once the predecessor grid has completed and its writes are
+// visible; launch_dependents then lets this kernel's own successor launch
+// early.  (Hides the launch latency between the step's ~1.2 k dependent
+// kernels.)  BE_PDL=0 launches everything conventionally.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 __device__ __forceinline__ uint16_t f2bf(float x) {
   __nv_bfloat16 h = __float2bfloat16_rn(x);  // round-to-nearest-even
@@ -66,3 +78,30 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 }}  // namespace be::dev
+
+#include <cuda_runtime.h>
+#include <cstdlib>
+#include <utility>
+namespace be { namespace dev {
+inline bool pdl_enabled() {
+  static const bool on = [] { const char* e = std::getenv("BE_PDL"); return !e || e[0] != '0'; }();
+  return on;
+}
+// kernel<<<grid, block, smem, s>>>(args...) with the PDL attribute (the kernel
+// must call pdl_entry() first)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}}  // namespace be::dev
+

@@ -31,12 +31,15 @@
 #include <string>
 #include <unordered_map>
 
+#include "common.cuh"
 #include "kernels.h"
 #include "runtime.h"
 #include "sgd_math.cuh"
 #include "sm100.cuh"
 
 namespace be { namespace k {
+using be::dev::launch_pdl;
+using be::dev::pdl_entry;
 
 namespace {
 std::atomic<uint64_t> g_tc_calls{0}, g_simt_calls{0};
@@ -448,6 +451,7 @@ __device__ __forceinline__ void upd_epilogue(const GemmParams& p, uint8_t* epi_s
 
 template <int BN, bool X3, bool UPD = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   using C = Cfg<BN, X3, UPD>;
   static_assert(C::STAGES >= 2, "pipeline needs at least two stages");
   extern __shared__ uint8_t smem_raw[];
@@ -930,6 +934,7 @@ struct Cfg {
 
 template <int BN>
 __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   using C = conv::Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1163,6 +1168,7 @@ struct Cfg {
 
 template <int BN>
 __global__ void __launch_bounds__(convs::kThreads, 1) conv_small_c_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   using C = convs::Cfg<BN>;
   static_assert(C::STAGES > convs::LAG, "gather pipeline needs more stages than cp.async groups in flight");
   extern __shared__ uint8_t smem_raw[];
@@ -1408,6 +1414,7 @@ constexpr int kSmemCap = 227 * 1024;
 }  // namespace stem
 
 __global__ void __launch_bounds__(stem::kThreads, 1) conv_stem_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nbuf = p.st_nbuf, st = p.cstride, R = p.cR, S = p.cS, L = p.st_L, T = p.st_taps;
@@ -1629,6 +1636,7 @@ __host__ __device__ inline Geo geo(int Q, int R, int S, int C, int K) {
 }  // namespace wgp
 
 __global__ void __launch_bounds__(wgp::kThreads, 1) conv_wgrad_patch_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const wgp::Geo gg = wgp::geo(p.cQ, p.cR, p.cS, p.cC, p.N);
@@ -1785,6 +1793,7 @@ constexpr int kSlack = 2048;
 }  // namespace cfp
 
 __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int Wp = p.sh_wb, G = p.sh_hb, R = p.cR, S = p.cS, taps = R * S;
@@ -1924,6 +1933,7 @@ inline Geo geo(const ConvGeom& g) {
 }  // namespace wgs
 
 __global__ void __launch_bounds__(wgs::kThreads, 1) conv_wgrad_stem_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int st = p.cstride, R = p.cR, S = p.cS, L = p.st_L, taps = R * S;
@@ -2182,6 +2192,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, con
 
 __global__ void splitk_reduce(const float* __restrict__ ws, int splits, long long sstride, int M, int N, void* D, long long ldd,
                               int d_f32, float beta, const float* bias, int act) {
+  pdl_entry();
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     float v = 0.f;
@@ -2486,19 +2497,19 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
                                            CU::SMEM));
         upd_attr = true;
       }
-      gemm_tc_kernel<BN, false, true><<<grid, kThreads, CU::SMEM, s>>>(p);
+      launch_pdl(gemm_tc_kernel<BN, false, true>, grid, kThreads, CU::SMEM, s, p);
     } else {
       fail(BE_E_ARG, "gemm: the update epilogue runs on the bf16 kernel");
     }
   } else {
-    gemm_tc_kernel<BN, X3><<<grid, kThreads, C::SMEM, s>>>(p);
+    launch_pdl(gemm_tc_kernel<BN, X3>, grid, kThreads, C::SMEM, s, p);
   }
   prof_end(pidx, s);
   after_launch("gemm_tc");
   if (ws) {
     const long long total = (long long)g.M * g.N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
+    launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -2554,7 +2565,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   if (ws) {
     const long long total = (long long)g.M * g.N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-    splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
+    launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -2651,7 +2662,7 @@ void launch_conv(GemmParams& p, cudaStream_t s, int* stats_parts) {
   p.tiles_n = (p.N + BN - 1) / BN;
   const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
   if (p.stats && stats_parts) *stats_parts = grid * 4;
-  conv_tc_kernel<BN><<<grid, conv::kThreads, C::SMEM, s>>>(p);
+  launch_pdl(conv_tc_kernel<BN>, grid, conv::kThreads, C::SMEM, s, p);
 }
 
 template <int BN>
@@ -2666,7 +2677,7 @@ void launch_conv_small_c(GemmParams& p, cudaStream_t s, int* stats_parts) {
   p.tiles_n = (p.N + BN - 1) / BN;
   const int grid = std::min(p.tiles_m * p.tiles_n, ctx().num_sms);
   if (p.stats && stats_parts) *stats_parts = grid * 4;
-  conv_small_c_kernel<BN><<<grid, convs::kThreads, C::SMEM, s>>>(p);
+  launch_pdl(conv_small_c_kernel<BN>, grid, convs::kThreads, C::SMEM, s, p);
 }
 
 static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
@@ -2732,13 +2743,13 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   const double flops = 2.0 * g.N * g.P * g.Q * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.N * g.P * g.Q * g.K) * 2.0 + 4.0 * g.K * RSC;
   const int pidx = prof_begin("conv_tc_wgrad_patch", flops, bytes, g.K, RSC, g.N * g.P * g.Q, s);
-  conv_wgrad_patch_kernel<<<grid, wgp::kThreads, smem, s>>>(p);
+  launch_pdl(conv_wgrad_patch_kernel, grid, wgp::kThreads, smem, s, p);
   prof_end(pidx, s);
   after_launch("conv_wgrad_patch");
   g_tc_calls++;
   const long long total = (long long)g.K * RSC;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
+  launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
                                        RSC, 1, beta, nullptr, 0);
   after_launch("conv_wgrad_patch_reduce");
   ctx().alloc.free(ws);
@@ -2776,13 +2787,13 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   const double flops = 2.0 * g.N * g.P * g.Q * 64.0 * RSC;
   const double bytes = ((double)g.N * g.H * g.W * 8 + (double)g.N * g.P * g.Q * 64) * 2.0 + 4.0 * 64 * RSC;
   const int pidx = prof_begin("conv_tc_wgrad_stem", flops, bytes, 64, RSC, g.N * g.P * g.Q, s);
-  conv_wgrad_stem_kernel<<<grid, wgs::kThreads, e.smem, s>>>(p);
+  launch_pdl(conv_wgrad_stem_kernel, grid, wgs::kThreads, e.smem, s, p);
   prof_end(pidx, s);
   after_launch("conv_wgrad_stem");
   g_tc_calls++;
   const long long total = 64LL * RSC;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-  splitk_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw, RSC,
+  launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw, RSC,
                                        1, beta, nullptr, 0);
   after_launch("conv_wgrad_stem_reduce");
   ctx().alloc.free(ws);
@@ -2841,7 +2852,7 @@ static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom
   const double flops = 2.0 * p.M * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 + (double)p.M * g.K * (f32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_patch", flops, bytes, p.M, g.K, RSC, s);
-  conv_fwd_patch_kernel<<<grid, cfp::kThreads, smem, s>>>(p);
+  launch_pdl(conv_fwd_patch_kernel, grid, cfp::kThreads, smem, s, p);
   prof_end(pidx, s);
   after_launch("conv_tc_patch");
   g_tc_calls++;
@@ -2906,7 +2917,7 @@ static bool conv_stem(const void* x, const void* w, void* y, const ConvGeom& g, 
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * taps * g.C) * 2.0 +
                        (double)p.M * g.K * (yd == BE_F32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_stem", flops, bytes, p.M, g.K, taps * g.C, s);
-  conv_stem_kernel<<<grid, stem::kThreads, smem, s>>>(p);
+  launch_pdl(conv_stem_kernel, grid, stem::kThreads, smem, s, p);
   prof_end(pidx, s);
   after_launch("conv_tc_stem");
   g_tc_calls++;
@@ -3076,7 +3087,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
   if (ws) {
     const long long total = (long long)g.M * g.N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-    splitk_reduce<<<blocks, 256, 0, s>>>(wsp, splits, total, g.M, g.N, g.D, g.ldd, g.d == BE_F32, g.beta, g.bias,
+    launch_pdl(splitk_reduce, blocks, 256, 0, s, wsp, splits, total, g.M, g.N, g.D, g.ldd, g.d == BE_F32, g.beta, g.bias,
                                          g.act);
     after_launch("gemm_simt_splitk_reduce");
     ctx().alloc.free(ws);
