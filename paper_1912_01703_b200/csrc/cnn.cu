@@ -49,6 +49,7 @@ constexpr int UNR = 4;
 template <typename T, int VEC, typename I>
 __global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, int64_t ldc,
                                                      ConvGeom g, I total) {
+  pdl_entry();
   using VT = typename std::conditional<VEC * sizeof(T) == 16, uint4, T>::type;
   static_assert(VEC * sizeof(T) == 16 || VEC == 1, "im2col vector width");
   const I CV = (I)(g.C / VEC);
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, T*
 template <typename T>
 __global__ void col2im_kernel(const T* __restrict__ dcols, int64_t ldc, T* __restrict__ dx, ConvGeom g, float beta,
                               int64_t total, be_dtype dt) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int c = (int)(t % g.C); t /= g.C;
@@ -132,6 +134,7 @@ __device__ __forceinline__ void nhwc8(I i, const ConvGeom& g, int H, int W, int&
 template <typename I>
 __global__ void __launch_bounds__(256) col2im_v(const void* __restrict__ dcols, int64_t ldc, void* __restrict__ dx,
                                                 ConvGeom g, float beta, I nvec, be_dtype dt) {
+  pdl_entry();
   const I stride = (I)gridDim.x * blockDim.x;
   for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
     int n, h, w, cv;
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(256) col2im_v(const void* __restrict__ dcols, 
 template <typename I>
 __global__ void __launch_bounds__(256) maxpool_fwd_v(const void* __restrict__ x, void* __restrict__ y,
                                                      uint8_t* __restrict__ am, ConvGeom g, be_dtype dt, I nvec) {
+  pdl_entry();
   const I stride = (I)gridDim.x * blockDim.x;
   for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
     int n, p, q, cv;
@@ -204,6 +208,7 @@ template <typename I, bool TWO>
 __global__ void __launch_bounds__(256) maxpool_bwd_v(const void* __restrict__ dy, const uint8_t* __restrict__ am,
                                                      void* __restrict__ dx, ConvGeom g, be_dtype dt, float beta,
                                                      I nvec) {
+  pdl_entry();
   const I stride = (I)gridDim.x * blockDim.x;
   for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
     int n, h, w, cv;
@@ -262,6 +267,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_v(const void* __restrict__ dy
 // wf[c, r, s, k] = w[k, R−1−r, S−1−s, c]
 __global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ wf, int K, int R, int S,
                                     int C, int64_t total) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int k = (int)(t % K); t /= K;
@@ -273,6 +279,7 @@ __global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __
 }
 
 __global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
+  pdl_entry();
   const int64_t RSC = (int64_t)g.R * g.S * g.C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / RSC, kk = i % RSC;
@@ -289,6 +296,7 @@ __global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
 
 // ---- max pool NHWC; window scanned r outer, u inner; first strictly greater wins; NaN wins at first sight
 __global__ void maxpool_fwd_kernel(const void* x, void* y, uint8_t* am, ConvGeom g, be_dtype dt, int64_t total) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int c = (int)(t % g.C); t /= g.C;
@@ -313,6 +321,7 @@ __global__ void maxpool_fwd_kernel(const void* x, void* y, uint8_t* am, ConvGeom
 }
 __global__ void maxpool_bwd_kernel(const void* dy, const uint8_t* am, void* dx, ConvGeom g, be_dtype dt, float beta,
                                    int64_t total) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = i;
     const int c = (int)(t % g.C); t /= g.C;
@@ -342,6 +351,7 @@ __global__ void maxpool_bwd_kernel(const void* dy, const uint8_t* am, void* dx, 
 
 // ---- global average pool: block per (n, 64-channel group)
 __global__ void avgpool_fwd_kernel(const void* x, void* y, int HW, int C, be_dtype dt) {
+  pdl_entry();
   const int n = blockIdx.y;
   const int c = blockIdx.x * 64 + (threadIdx.x & 63);
   const int part = threadIdx.x >> 6;  // 4 parts
@@ -354,6 +364,7 @@ __global__ void avgpool_fwd_kernel(const void* x, void* y, int HW, int C, be_dty
   if (part == 0 && c < C) st(y, (int64_t)n * C + c, dt, (sm[0][threadIdx.x] + sm[1][threadIdx.x] + sm[2][threadIdx.x] + sm[3][threadIdx.x]) / (float)HW);
 }
 __global__ void avgpool_bwd_kernel(const void* dy, void* dx, int HW, int C, be_dtype dt, float beta, int64_t total) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     const int64_t n = i / ((int64_t)HW * C);
@@ -369,6 +380,7 @@ template <int MODE>  // 0: Σx   1: Σ(x−mean)²   2: Σg', Σg'·x̂  (g' = g
 __global__ void bn_reduce_kernel(const void* x, const void* gy, const void* yv, int act, int64_t rows, int C,
                                  be_dtype dt, const float* mean, const float* invstd, float* part0, float* part1,
                                  int64_t rows_per_split) {
+  pdl_entry();
   const int cl = threadIdx.x & 63, lane_r = threadIdx.x >> 6;
   const int c = blockIdx.x * 64 + cl;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
@@ -399,6 +411,7 @@ __global__ void bn_reduce_kernel(const void* x, const void* gy, const void* yv, 
   }
 }
 __global__ void bn_mean_finalize(const float* part, int splits, int C, int64_t rows, float* mean) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s = 0.f;
@@ -407,6 +420,7 @@ __global__ void bn_mean_finalize(const float* part, int splits, int C, int64_t r
 }
 __global__ void bn_var_finalize(const float* part, int splits, int C, int64_t rows, float eps, const float* mean,
                                 float* invstd, float* run_mean, float* run_var, float momentum) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s = 0.f;
@@ -418,6 +432,7 @@ __global__ void bn_var_finalize(const float* part, int splits, int C, int64_t ro
 }
 __global__ void bn_grad_finalize(const float* p0, const float* p1, int splits, int C, float* dgamma, float* dbeta,
                                  float gb_beta, float* sums) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s0 = 0.f, s1 = 0.f;
@@ -430,6 +445,7 @@ __global__ void bn_grad_finalize(const float* p0, const float* p1, int splits, i
 __global__ void bn_apply_kernel(const void* x, void* y, int64_t total, int C, be_dtype dt, const float* mean,
                                 const float* invstd, const float* gamma, const float* beta, int act,
                                 const void* res) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     float v = gamma[c] * (ld(x, i, dt) - mean[c]) * invstd[c] + beta[c];
@@ -441,6 +457,7 @@ __global__ void bn_apply_kernel(const void* x, void* y, int64_t total, int C, be
 __global__ void bn_dx_kernel(const void* gy, const void* x, const void* yv, int act, void* dx, int64_t total, int C,
                              int64_t rows, be_dtype dt, const float* mean, const float* invstd, const float* gamma,
                              const float* sums, float dx_beta) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     float g = ld(gy, i, dt);
@@ -466,6 +483,7 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
                                                    float* __restrict__ part1, int64_t rows_per_split,
                                                    const float* __restrict__ gam = nullptr,
                                                    const float* __restrict__ bsh = nullptr) {
+  pdl_entry();
   // act with gam/bsh: the ReLU mask is recomputed as fma(x, γ·is, β − μ·γ·is) > 0
   // — the forward's exact expression — instead of reading the saved output.
   __shared__ float sm0[kBnCG], sm1[kBnCG];
@@ -536,6 +554,7 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
 __global__ void bn_stats_finalize_v(const float* p0, const float* p1, int splits, int C, int64_t rows, const void* x,
                                     be_dtype dt, float eps, float* mean, float* invstd, float* run_mean,
                                     float* run_var, float momentum) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   double s1 = 0, s2 = 0;
@@ -558,6 +577,7 @@ __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, vo
                                                   const float* __restrict__ invstd, const float* __restrict__ gamma,
                                                   const float* __restrict__ beta, int act, int64_t rows_per_block,
                                                   const void* __restrict__ res) {
+  pdl_entry();
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -595,6 +615,7 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
                                                const float* __restrict__ invstd, const float* __restrict__ gamma,
                                                const float* __restrict__ sums, float dx_beta, int64_t rows_per_block,
                                                const float* __restrict__ bsh = nullptr) {
+  pdl_entry();
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -671,6 +692,7 @@ __global__ void __launch_bounds__(256) bn_reduce_bf16(const uint16_t* __restrict
                                                       const float* __restrict__ gam, const float* __restrict__ bsh,
                                                       const uint16_t* __restrict__ rmask = nullptr,
                                                       uint16_t* __restrict__ gout = nullptr) {
+  pdl_entry();
   __shared__ float sm0[kBnCG], sm1[kBnCG];
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
@@ -746,6 +768,7 @@ __global__ void __launch_bounds__(256) bn_dx_bf16(const uint16_t* __restrict__ g
                                                   const float* __restrict__ mean, const float* __restrict__ invstd,
                                                   const float* __restrict__ gamma, const float* __restrict__ sums,
                                                   float dx_beta, int64_t rows_per_block, const float* __restrict__ bsh) {
+  pdl_entry();
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -802,6 +825,7 @@ __global__ void __launch_bounds__(256) bn_dx_bf16(const uint16_t* __restrict__ g
 __global__ void __launch_bounds__(256) bn_stats_bf16(const uint16_t* __restrict__ x, int64_t rows, int C,
                                                      float* __restrict__ part0, float* __restrict__ part1,
                                                      int64_t rows_per_split) {
+  pdl_entry();
   __shared__ float sm0[kBnCG], sm1[kBnCG];
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
@@ -847,6 +871,7 @@ __global__ void __launch_bounds__(256) bn_apply_bf16(const uint16_t* __restrict_
                                                      const float* __restrict__ invstd, const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, int act, int64_t rows_per_block,
                                                      const uint16_t* __restrict__ res) {
+  pdl_entry();
   const int base = blockIdx.x * kBnCG;
   const int Cg = min(kBnCG, C - base);
   const int lanes = Cg / 8, rpi = 256 / lanes;
@@ -950,6 +975,7 @@ __global__ void __launch_bounds__(1024) bn_finalize_v(const float* __restrict__ 
 // ---- embedding gather
 __global__ void embedding_fwd_kernel(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out,
                                      be_dtype od) {
+  pdl_entry();
   const int64_t total = B * D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = i / D, d = i % D;
@@ -960,6 +986,7 @@ __global__ void embedding_fwd_kernel(const float* table, int64_t D, const int32_
 // ---- concat / slice along columns
 struct ConcatArgs { const void* x[8]; int64_t w[8]; int64_t off[9]; int n; };
 __global__ void concat_kernel(ConcatArgs a, int64_t rows, void* y, be_dtype dt) {
+  pdl_entry();
   const int64_t W = a.off[a.n];
   const int64_t total = rows * W;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -971,6 +998,7 @@ __global__ void concat_kernel(ConcatArgs a, int64_t rows, void* y, be_dtype dt) 
 }
 __global__ void slice_kernel(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x,
                              be_dtype dt, float beta) {
+  pdl_entry();
   const int64_t total = rows * width;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / width, c = i % width;
@@ -993,6 +1021,7 @@ __global__ void slice_kernel(const void* y, int64_t ldy, int64_t col0, int64_t w
 template <int STRIDE>
 __global__ void __launch_bounds__(256) maxpool_fwd_rows(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
                                                         uint8_t* __restrict__ am, ConvGeom g) {
+  pdl_entry();
   const int stride = STRIDE > 0 ? STRIDE : g.stride;
   const int cv = threadIdx.x;
   const int q = blockIdx.x * blockDim.y + threadIdx.y;
@@ -1087,6 +1116,7 @@ template <int STRIDE>
 __global__ void __launch_bounds__(256) maxpool_bwd_rows(const uint16_t* __restrict__ dy,
                                                         const uint8_t* __restrict__ am, uint16_t* __restrict__ dx,
                                                         ConvGeom g, float beta) {
+  pdl_entry();
   const int stride = STRIDE > 0 ? STRIDE : g.stride;
   const int cv = threadIdx.x;
   const int w = blockIdx.x * blockDim.y + threadIdx.y;
@@ -1146,9 +1176,9 @@ template <typename T, int VEC>
 static void im2col_launch(const void* x, void* cols, int64_t ldc, const ConvGeom& g, int64_t total, cudaStream_t s) {
   const int grid = grid_for(total, UNR);
   if (total < (1LL << 31))
-    im2col_kernel<T, VEC, uint32_t><<<grid, 256, 0, s>>>((const T*)x, (T*)cols, ldc, g, (uint32_t)total);
+    launch_pdl(im2col_kernel<T, VEC, uint32_t>, grid, 256, 0, s, (const T*)x, (T*)cols, ldc, g, (uint32_t)total);
   else
-    im2col_kernel<T, VEC, int64_t><<<grid, 256, 0, s>>>((const T*)x, (T*)cols, ldc, g, total);
+    launch_pdl(im2col_kernel<T, VEC, int64_t>, grid, 256, 0, s, (const T*)x, (T*)cols, ldc, g, total);
 }
 void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t M = (int64_t)g.N * g.P * g.Q;
@@ -1165,28 +1195,28 @@ void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtyp
   if (total == 0) return;
   if (g.C % 8 == 0 && ldc % 8 == 0 && aligned16(dcols) && aligned16(dx)) {
     if (total / 8 < (1LL << 31))
-      col2im_v<uint32_t><<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, (uint32_t)(total / 8), dt);
+      launch_pdl(col2im_v<uint32_t>, grid_for(total / 8), 256, 0, s, dcols, ldc, dx, g, beta, (uint32_t)(total / 8), dt);
     else
-      col2im_v<int64_t><<<grid_for(total / 8), 256, 0, s>>>(dcols, ldc, dx, g, beta, total / 8, dt);
+      launch_pdl(col2im_v<int64_t>, grid_for(total / 8), 256, 0, s, dcols, ldc, dx, g, beta, total / 8, dt);
     after_launch("col2im_v");
     return;
   }
   if (dt == BE_BF16)
-    col2im_kernel<uint16_t><<<grid_for(total), 256, 0, s>>>((const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, total, dt);
+    launch_pdl(col2im_kernel<uint16_t>, grid_for(total), 256, 0, s, (const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, total, dt);
   else
-    col2im_kernel<float><<<grid_for(total), 256, 0, s>>>((const float*)dcols, ldc, (float*)dx, g, beta, total, dt);
+    launch_pdl(col2im_kernel<float>, grid_for(total), 256, 0, s, (const float*)dcols, ldc, (float*)dx, g, beta, total, dt);
   after_launch("col2im");
 }
 void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s) {
   const int64_t total = (int64_t)K * R * S * C;
   if (total == 0) return;
-  flip_weights_kernel<<<grid_for(total), 256, 0, s>>>((const uint16_t*)w, (uint16_t*)wf, K, R, S, C, total);
+  launch_pdl(flip_weights_kernel, grid_for(total), 256, 0, s, (const uint16_t*)w, (uint16_t*)wf, K, R, S, C, total);
   after_launch("flip_weights");
 }
 void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.R * g.S * g.C;
   if (total == 0) return;
-  im2col_offsets_kernel<<<grid_for(total), 256, 0, s>>>(g, out, total);
+  launch_pdl(im2col_offsets_kernel, grid_for(total), 256, 0, s, g, out, total);
   after_launch("im2col_offsets");
 }
 void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
@@ -1196,20 +1226,20 @@ void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtyp
       aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
     dim3 grid((g.Q + wpb - 1) / wpb, g.P, g.N), block(cvn, wpb);
-    if (g.stride == 2) maxpool_fwd_rows<2><<<grid, block, 0, s>>>((const uint16_t*)x, (uint16_t*)y, am, g);
-    else maxpool_fwd_rows<0><<<grid, block, 0, s>>>((const uint16_t*)x, (uint16_t*)y, am, g);
+    if (g.stride == 2) launch_pdl(maxpool_fwd_rows<2>, grid, block, 0, s, (const uint16_t*)x, (uint16_t*)y, am, g);
+    else launch_pdl(maxpool_fwd_rows<0>, grid, block, 0, s, (const uint16_t*)x, (uint16_t*)y, am, g);
     after_launch("maxpool_fwd_rows");
     return;
   }
   if (g.C % 8 == 0 && aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     if (total / 8 < (1LL << 31))
-      maxpool_fwd_v<uint32_t><<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, (uint32_t)(total / 8));
+      launch_pdl(maxpool_fwd_v<uint32_t>, grid_for(total / 8), 256, 0, s, x, y, am, g, dt, (uint32_t)(total / 8));
     else
-      maxpool_fwd_v<int64_t><<<grid_for(total / 8), 256, 0, s>>>(x, y, am, g, dt, total / 8);
+      launch_pdl(maxpool_fwd_v<int64_t>, grid_for(total / 8), 256, 0, s, x, y, am, g, dt, total / 8);
     after_launch("maxpool_fwd_v");
     return;
   }
-  maxpool_fwd_kernel<<<grid_for(total), 256, 0, s>>>(x, y, am, g, dt, total);
+  launch_pdl(maxpool_fwd_kernel, grid_for(total), 256, 0, s, x, y, am, g, dt, total);
   after_launch("maxpool_fwd");
 }
 void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g, be_dtype dt, float beta,
@@ -1221,8 +1251,8 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
       aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
     dim3 grid((g.W + wpb - 1) / wpb, g.H, g.N), block(cvn, wpb);
-    if (g.stride == 2) maxpool_bwd_rows<2><<<grid, block, 0, s>>>((const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
-    else maxpool_bwd_rows<0><<<grid, block, 0, s>>>((const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+    if (g.stride == 2) launch_pdl(maxpool_bwd_rows<2>, grid, block, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+    else launch_pdl(maxpool_bwd_rows<0>, grid, block, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
     after_launch("maxpool_bwd_rows");
     return;
   }
@@ -1230,28 +1260,28 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
     const bool two = g.R <= 2 * g.stride && g.S <= 2 * g.stride;
     const int grid = grid_for(total / 8);
     if (total / 8 < (1LL << 31)) {
-      if (two) maxpool_bwd_v<uint32_t, true><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
-      else maxpool_bwd_v<uint32_t, false><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
+      if (two) launch_pdl(maxpool_bwd_v<uint32_t, true>, grid, 256, 0, s, dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
+      else launch_pdl(maxpool_bwd_v<uint32_t, false>, grid, 256, 0, s, dy, am, dx, g, dt, beta, (uint32_t)(total / 8));
     } else {
-      if (two) maxpool_bwd_v<int64_t, true><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
-      else maxpool_bwd_v<int64_t, false><<<grid, 256, 0, s>>>(dy, am, dx, g, dt, beta, total / 8);
+      if (two) launch_pdl(maxpool_bwd_v<int64_t, true>, grid, 256, 0, s, dy, am, dx, g, dt, beta, total / 8);
+      else launch_pdl(maxpool_bwd_v<int64_t, false>, grid, 256, 0, s, dy, am, dx, g, dt, beta, total / 8);
     }
     after_launch("maxpool_bwd_v");
     return;
   }
-  maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(dy, am, dx, g, dt, beta, total);
+  launch_pdl(maxpool_bwd_kernel, grid_for(total), 256, 0, s, dy, am, dx, g, dt, beta, total);
   after_launch("maxpool_bwd");
 }
 void avgpool_fwd(const void* x, void* y, int N, int HW, int C, be_dtype dt, cudaStream_t s) {
   if (N == 0 || C == 0) return;
   dim3 grid((C + 63) / 64, N);
-  avgpool_fwd_kernel<<<grid, 256, 0, s>>>(x, y, HW, C, dt);
+  launch_pdl(avgpool_fwd_kernel, grid, 256, 0, s, x, y, HW, C, dt);
   after_launch("avgpool_fwd");
 }
 void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, float beta, cudaStream_t s) {
   const int64_t total = (int64_t)N * HW * C;
   if (total == 0) return;
-  avgpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(dy, dx, HW, C, dt, beta, total);
+  launch_pdl(avgpool_bwd_kernel, grid_for(total), 256, 0, s, dy, dx, HW, C, dt, beta, total);
   after_launch("avgpool_bwd");
 }
 
@@ -1293,10 +1323,10 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
     if (stream)
       bn_stats_stream(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, sp, s);
     else if (dt == BE_BF16)
-      bn_stats_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, rps);
+      launch_pdl(bn_stats_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, rps);
     else
-      bn_reduce_v<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
-                                          partial + sp * C, rps);
+      launch_pdl(bn_reduce_v<0>, grid, 256, 0, s, x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
+                                          partial + sp * C, rps, nullptr, nullptr);
     after_launch("bn_stats_v");
     launch_pdl(bn_finalize_v<0>, (C + 7) / 8, 1024, 0, s, partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
                                                     invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
@@ -1307,13 +1337,13 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
   const int64_t sp = bn_splits(rows, C);
   const int64_t rps = (rows + sp - 1) / sp;
   dim3 grid((C + 63) / 64, (unsigned)sp);
-  bn_reduce_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial, nullptr, rps);
+  launch_pdl(bn_reduce_kernel<0>, grid, 256, 0, s, x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial, nullptr, rps);
   after_launch("bn_sum");
-  bn_mean_finalize<<<(C + 255) / 256, 256, 0, s>>>(partial, (int)sp, C, rows, mean);
+  launch_pdl(bn_mean_finalize, (C + 255) / 256, 256, 0, s, partial, (int)sp, C, rows, mean);
   after_launch("bn_mean");
-  bn_reduce_kernel<1><<<grid, 256, 0, s>>>(x, nullptr, nullptr, 0, rows, C, dt, mean, nullptr, partial, nullptr, rps);
+  launch_pdl(bn_reduce_kernel<1>, grid, 256, 0, s, x, nullptr, nullptr, 0, rows, C, dt, mean, nullptr, partial, nullptr, rps);
   after_launch("bn_sqdev");
-  bn_var_finalize<<<(C + 255) / 256, 256, 0, s>>>(partial, (int)sp, C, rows, eps, mean, invstd, run_mean, run_var,
+  launch_pdl(bn_var_finalize, (C + 255) / 256, 256, 0, s, partial, (int)sp, C, rows, eps, mean, invstd, run_mean, run_var,
                                                   momentum);
   after_launch("bn_var");
 }
@@ -1337,14 +1367,14 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
     dim3 grid;
     const int64_t rpb = bn_rows_per_block(rows, C, &grid);
     if (dt == BE_BF16)
-      bn_apply_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C,
+      launch_pdl(bn_apply_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C,
                                          mean, invstd, gamma, beta, act, rpb, reinterpret_cast<const uint16_t*>(res));
     else
-      bn_apply_v<<<grid, 256, 0, s>>>(x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb, res);
+      launch_pdl(bn_apply_v, grid, 256, 0, s, x, y, rows, C, dt, mean, invstd, gamma, beta, act, rpb, res);
     after_launch("bn_apply_v");
     return;
   }
-  bn_apply_kernel<<<grid_for(total), 256, 0, s>>>(x, y, total, C, dt, mean, invstd, gamma, beta, act, res);
+  launch_pdl(bn_apply_kernel, grid_for(total), 256, 0, s, x, y, total, C, dt, mean, invstd, gamma, beta, act, res);
   after_launch("bn_apply");
 }
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
@@ -1369,7 +1399,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
                          invstd, p0, p1, sp, gamma, nullptr, reinterpret_cast<const uint16_t*>(rmask),
                          reinterpret_cast<uint16_t*>(gout), s);
       } else {
-        bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
+        launch_pdl(bn_reduce_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
                                             0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,
                                             reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
         after_launch("bn_bwd_reduce_mask_bf16");
@@ -1383,7 +1413,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       } else if (dx) {
         dim3 g2;
         const int64_t rpb = bn_rows_per_block(rows, C, &g2);
-        bn_dx_bf16<<<g2, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x),
+        launch_pdl(bn_dx_bf16, g2, 256, 0, s, reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x),
                                       0, reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta,
                                       rpb, nullptr);
         after_launch("bn_bwd_dx_v");
@@ -1407,10 +1437,10 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), act, rows, C, mean,
                        invstd, p0, p1, sp, gamma, bn_beta, nullptr, nullptr, s);
     else if (fast)
-      bn_reduce_bf16<<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
-                                          act, rows, C, mean, invstd, p0, p1, rps, gamma, bn_beta);
+      launch_pdl(bn_reduce_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
+                                          act, rows, C, mean, invstd, p0, p1, rps, gamma, bn_beta, nullptr, nullptr);
     else
-      bn_reduce_v<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
+      launch_pdl(bn_reduce_v<2>, grid, 256, 0, s, x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
                                           bn_beta ? gamma : nullptr, bn_beta);
     if (!stream) after_launch("bn_bwd_reduce_v");
     launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
@@ -1423,11 +1453,11 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       dim3 g2;
       const int64_t rpb = bn_rows_per_block(rows, C, &g2);
       if (fast)
-        bn_dx_bf16<<<g2, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(x), act,
+        launch_pdl(bn_dx_bf16, g2, 256, 0, s, reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(x), act,
                                       reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, rpb,
                                       bn_beta);
       else
-        bn_dx_v<<<g2, 256, 0, s>>>(dy, x, y, act, dx, rows, C, dt, mean, invstd, gamma, sums, dx_beta, rpb, bn_beta);
+        launch_pdl(bn_dx_v, g2, 256, 0, s, dy, x, y, act, dx, rows, C, dt, mean, invstd, gamma, sums, dx_beta, rpb, bn_beta);
       after_launch("bn_bwd_dx_v");
     }
     return;
@@ -1438,13 +1468,13 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
   float* p1 = partial + sp * C;
   float* sums = partial + 2 * sp * C;
   dim3 grid((C + 63) / 64, (unsigned)sp);
-  bn_reduce_kernel<2><<<grid, 256, 0, s>>>(x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps);
+  launch_pdl(bn_reduce_kernel<2>, grid, 256, 0, s, x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps);
   after_launch("bn_bwd_reduce");
-  bn_grad_finalize<<<(C + 255) / 256, 256, 0, s>>>(p0, p1, (int)sp, C, dgamma, dbeta, gb_beta, sums);
+  launch_pdl(bn_grad_finalize, (C + 255) / 256, 256, 0, s, p0, p1, (int)sp, C, dgamma, dbeta, gb_beta, sums);
   after_launch("bn_bwd_finalize");
   if (dx) {
     const int64_t total = rows * C;
-    bn_dx_kernel<<<grid_for(total), 256, 0, s>>>(dy, x, y, act, dx, total, C, rows, dt, mean, invstd, gamma, sums,
+    launch_pdl(bn_dx_kernel, grid_for(total), 256, 0, s, dy, x, y, act, dx, total, C, rows, dt, mean, invstd, gamma, sums,
                                                  dx_beta);
     after_launch("bn_bwd_dx");
   }
@@ -1456,7 +1486,7 @@ size_t bn_partial_floats(int64_t rows, int C) {
 void embedding_fwd(const float* table, int64_t D, const int32_t* ids, int64_t B, void* out, be_dtype od,
                    cudaStream_t s) {
   if (B * D == 0) return;
-  embedding_fwd_kernel<<<grid_for(B * D), 256, 0, s>>>(table, D, ids, B, out, od);
+  launch_pdl(embedding_fwd_kernel, grid_for(B * D), 256, 0, s, table, D, ids, B, out, od);
   after_launch("embedding_fwd");
 }
 void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t rows, void* y, be_dtype dt,
@@ -1466,13 +1496,13 @@ void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t ro
   a.off[0] = 0;
   for (int i = 0; i < n; ++i) { a.x[i] = xs[i]; a.w[i] = widths[i]; a.off[i + 1] = a.off[i] + widths[i]; }
   if (rows * a.off[n] == 0) return;
-  concat_kernel<<<grid_for(rows * a.off[n]), 256, 0, s>>>(a, rows, y, dt);
+  launch_pdl(concat_kernel, grid_for(rows * a.off[n]), 256, 0, s, a, rows, y, dt);
   after_launch("concat");
 }
 void slice_cols(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x, be_dtype dt,
                 float beta, cudaStream_t s) {
   if (rows * width == 0) return;
-  slice_kernel<<<grid_for(rows * width), 256, 0, s>>>(y, ldy, col0, width, rows, x, dt, beta);
+  launch_pdl(slice_kernel, grid_for(rows * width), 256, 0, s, y, ldy, col0, width, rows, x, dt, beta);
   after_launch("slice");
 }
 

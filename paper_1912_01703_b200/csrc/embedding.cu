@@ -23,6 +23,7 @@ constexpr int kBuckets = 1 << kDigitBits;
 __global__ void __launch_bounds__(kSortThreads) radix_pass(const uint32_t* __restrict__ kin,
                                                           const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                                                           uint32_t* __restrict__ vout, int n, int shift) {
+  pdl_entry();
   extern __shared__ uint32_t cnt[];  // [kBuckets][kSortThreads]
   const int t = threadIdx.x;
   const int E = (n + kSortThreads - 1) / kSortThreads;
@@ -88,6 +89,7 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_tot)
 __global__ void __launch_bounds__(kSortThreads) radix_sort_smem(const int32_t* __restrict__ ids,
                                                                uint32_t* __restrict__ out_k,
                                                                uint32_t* __restrict__ out_v, int n, int bits) {
+  pdl_entry();
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                              // skewed [kBuckets][kSortThreads]
   uint32_t* ka = cnt + kBuckets * kSortThreads + kBuckets * kSortThreads / 64;  // [n]
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_sort_smem(const int32_t* _
 }
 
 __global__ void init_pairs(const int32_t* ids, uint32_t* k, uint32_t* v, int n) {
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     k[i] = (uint32_t)ids[i];
     v[i] = (uint32_t)i;
@@ -137,6 +140,7 @@ __global__ void init_pairs(const int32_t* ids, uint32_t* k, uint32_t* v, int n) 
 // one warp per sorted element; segment heads sum their segment in order
 __global__ void segment_sum(const uint32_t* keys, const uint32_t* pos, int n, const void* drows, be_dtype dd,
                             int64_t D, float* dtable, float beta) {
+  pdl_entry();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -177,7 +181,7 @@ void embedding_bwd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, 
   const uint32_t* k0 = reinterpret_cast<const uint32_t*>(sorted);
   const uint32_t* v0 = k0 + B;
   const int64_t threads = B * 32;
-  segment_sum<<<(int)((threads + 255) / 256), 256, 0, s>>>(k0, v0, (int)B, drows, dd, D, dtable, beta);
+  launch_pdl(segment_sum, (int)((threads + 255) / 256), 256, 0, s, k0, v0, (int)B, drows, dd, D, dtable, beta);
   after_launch("embedding_segment_sum");
 }
 
@@ -199,7 +203,7 @@ void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cud
                                          (int)(sizeof(uint32_t) * (cwords + 4 * kSmemSortMax))));
       sattr = true;
     }
-    radix_sort_smem<<<1, kSortThreads, smem, s>>>(ids, k0, v0, (int)B, bits);
+    launch_pdl(radix_sort_smem, 1, kSortThreads, smem, s, ids, k0, v0, (int)B, bits);
     after_launch("embedding_radix_sort_smem");
     return;
   }
@@ -214,7 +218,7 @@ void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cud
     attr = true;
   }
   for (int shift = 0; shift < bits; shift += kDigitBits) {
-    radix_pass<<<1, kSortThreads, smem, s>>>(k0, v0, k1, v1, (int)B, shift);
+    launch_pdl(radix_pass, 1, kSortThreads, smem, s, k0, v0, k1, v1, (int)B, shift);
     after_launch("embedding_radix_pass");
     std::swap(k0, k1);
     std::swap(v0, v1);

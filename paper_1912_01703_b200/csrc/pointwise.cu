@@ -25,6 +25,7 @@ int ew_grid(int64_t n, int per_thread = 8) {
 // Generic vectorised unary/binary elementwise: op(i, a, b, y) on 8 lanes.
 template <typename F>
 __global__ void ew_kernel(int64_t n, bool vec, F f) {
+  pdl_entry();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (vec) {
     const int64_t n8 = n / 8;
@@ -37,7 +38,7 @@ __global__ void ew_kernel(int64_t n, bool vec, F f) {
 template <typename F>
 void launch_ew(int64_t n, bool vec, F f, cudaStream_t s, const char* name) {
   if (n <= 0) return;
-  ew_kernel<<<ew_grid(n), 256, 0, s>>>(n, vec, f);
+  launch_pdl(ew_kernel<F>, ew_grid(n), 256, 0, s, n, vec, f);
   after_launch(name);
 }
 
@@ -190,6 +191,7 @@ struct BcastScalarF {
 
 __global__ void add_bcast_kernel(const void* a, const void* b, void* y, BcastDesc d, be_dtype dt, int act,
                                  int64_t n) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t rem = i, oa = 0, ob = 0;
     for (int r = d.rank - 1; r >= 0; --r) {
@@ -208,6 +210,7 @@ __global__ void add_bcast_kernel(const void* a, const void* b, void* y, BcastDes
 template <int MODE>
 __global__ void colsum_kernel(const void* x, const void* yv, void* dz, int64_t rows, int64_t cols, be_dtype dt,
                               float* partial, int64_t rows_per_split) {
+  pdl_entry();
   __shared__ float sm[8][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * 64 + lane * 2;
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(256) colsum_v_kernel(const void* __restrict__ 
                                                        float* __restrict__ partial, int64_t rows_per_split,
                                                        unsigned* __restrict__ counters, float* __restrict__ out,
                                                        float beta) {
+  pdl_entry();
   __shared__ float sm[8][257];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t c = ((int64_t)blockIdx.x * 32 + tx) * 8;
@@ -330,6 +334,7 @@ __global__ void __launch_bounds__(256) colsum_v_kernel(const void* __restrict__ 
 }
 
 __global__ void colsum_finalize(const float* partial, int splits, int64_t cols, float* out, float beta) {
+  pdl_entry();
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
     float t = 0.f;
     for (int s = 0; s < splits; ++s) t += partial[(int64_t)s * cols + c];
@@ -366,9 +371,9 @@ void colsum_impl(int mode, const void* x, const void* y, void* dz, int64_t rows,
     dim3 grid((unsigned)cg, (unsigned)splits);
     unsigned* counters = colsum_counters(cg);
     if (mode == 0)
-      colsum_v_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, rows, cols, dt, partial, rps, counters, out, beta);
+      launch_pdl(colsum_v_kernel<0>, grid, 256, 0, s, x, nullptr, nullptr, rows, cols, dt, partial, rps, counters, out, beta);
     else
-      colsum_v_kernel<1><<<grid, 256, 0, s>>>(x, y, dz, rows, cols, dt, partial, rps, counters, out, beta);
+      launch_pdl(colsum_v_kernel<1>, grid, 256, 0, s, x, y, dz, rows, cols, dt, partial, rps, counters, out, beta);
     after_launch(mode == 0 ? "colsum_v" : "relu_bwd_colsum_v");
     ctx().alloc.free(tmp);
     return;
@@ -384,10 +389,10 @@ void colsum_impl(int mode, const void* x, const void* y, void* dz, int64_t rows,
   if (rows == 0) {
     cudaMemsetAsync(partial, 0, sizeof(float) * cols, s);
   } else if (mode == 0) {
-    colsum_kernel<0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, rows, cols, dt, partial, rps);
+    launch_pdl(colsum_kernel<0>, grid, 256, 0, s, x, nullptr, nullptr, rows, cols, dt, partial, rps);
     after_launch("colsum");
   } else {
-    colsum_kernel<1><<<grid, 256, 0, s>>>(x, y, dz, rows, cols, dt, partial, rps);
+    launch_pdl(colsum_kernel<1>, grid, 256, 0, s, x, y, dz, rows, cols, dt, partial, rps);
     after_launch("relu_bwd_colsum");
   }
   colsum_finalize<<<(unsigned)std::min<int64_t>((cols + 255) / 256, 1024), 256, 0, s>>>(partial, (int)splits, cols,
@@ -398,6 +403,7 @@ void colsum_impl(int mode, const void* x, const void* y, void* dz, int64_t rows,
 
 // ---- full reduction: two-pass, deterministic
 __global__ void reduce_partial(const void* x, int64_t n, be_dtype dt, float* partial) {
+  pdl_entry();
   float s = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     s += ld(x, i, dt);
@@ -412,6 +418,7 @@ __global__ void reduce_partial(const void* x, int64_t n, be_dtype dt, float* par
   }
 }
 __global__ void reduce_final(const float* partial, int n, float* out, float scale) {
+  pdl_entry();
   float s = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
   s = warp_sum(s);
@@ -429,6 +436,7 @@ __global__ void reduce_final(const float* partial, int n, float* out, float scal
 __global__ void __launch_bounds__(256) xent_kernel(const void* z, be_dtype zd, int64_t ldz, const int32_t* y,
                                                    int64_t B, int64_t C, float* row_loss, void* dz, be_dtype dzd,
                                                    int32_t* am) {
+  pdl_entry();
   const int64_t row = blockIdx.x;
   const void* zr = reinterpret_cast<const char*>(z) + row * ldz * (zd == BE_BF16 ? 2 : 4);
   __shared__ float smax[8], ssum[8];
@@ -473,6 +481,7 @@ __global__ void __launch_bounds__(256) xent_kernel(const void* z, be_dtype zd, i
 }
 __global__ void bce_kernel(const void* z, be_dtype zd, const int32_t* y, int64_t B, float* row_loss, void* dz,
                            be_dtype dzd) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     float v = ld(z, i, zd);
     float t = (float)y[i];
@@ -498,6 +507,7 @@ constexpr int kSgdChunk = 4096;
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ SgdTable t, float lr, float mu, float wd,
                                                   float scale) {
+  pdl_entry();
   const int64_t total_chunks = t.start[t.n];
   for (int64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
     int lo = 0, hi = t.n - 1;
@@ -591,7 +601,7 @@ void add_bcast(const void* a, const void* b, void* y, const BcastDesc& d, be_dty
   int64_t n = 1;
   for (int i = 0; i < d.rank; ++i) n *= d.shape[i];
   if (n == 0) return;
-  add_bcast_kernel<<<ew_grid(n, 1), 256, 0, s>>>(a, b, y, d, dt, act, n);
+  launch_pdl(add_bcast_kernel, ew_grid(n, 1), 256, 0, s, a, b, y, d, dt, act, n);
   after_launch("add_bcast");
 }
 void colsum(const void* x, int64_t rows, int64_t cols, be_dtype dt, float* out, float beta, cudaStream_t s) {
@@ -610,25 +620,25 @@ void relu_bwd_colsum(const void* dy, const void* y, void* dz, int64_t rows, int6
 }
 void reduce_sum(const void* x, int64_t n, be_dtype dt, float* out, float scale, float* scratch, cudaStream_t s) {
   const int blocks = std::max(1, std::min<int>((int)((n + 2047) / 2048), 1024));
-  reduce_partial<<<blocks, 256, 0, s>>>(x, n, dt, scratch);
+  launch_pdl(reduce_partial, blocks, 256, 0, s, x, n, dt, scratch);
   after_launch("reduce_partial");
-  reduce_final<<<1, 1024, 0, s>>>(scratch, blocks, out, scale);
+  launch_pdl(reduce_final, 1, 1024, 0, s, scratch, blocks, out, scale);
   after_launch("reduce_final");
 }
 void softmax_xent(const void* z, be_dtype zd, int64_t ldz, const int32_t* y, int64_t B, int64_t C, float* row_loss,
                   float* loss_out, void* dz, be_dtype dzd, int32_t* am, cudaStream_t s) {
   if (B == 0) return;
-  xent_kernel<<<(unsigned)B, 256, 0, s>>>(z, zd, ldz, y, B, C, row_loss, dz, dzd, am);
+  launch_pdl(xent_kernel, (unsigned)B, 256, 0, s, z, zd, ldz, y, B, C, row_loss, dz, dzd, am);
   after_launch("softmax_xent");
-  reduce_final<<<1, 1024, 0, s>>>(row_loss, (int)B, loss_out, 1.f / (float)B);
+  launch_pdl(reduce_final, 1, 1024, 0, s, row_loss, (int)B, loss_out, 1.f / (float)B);
   after_launch("xent_mean");
 }
 void bce_logits(const void* z, be_dtype zd, const int32_t* y, int64_t B, float* row_loss, float* loss_out, void* dz,
                 be_dtype dzd, cudaStream_t s) {
   if (B == 0) return;
-  bce_kernel<<<ew_grid(B, 1), 256, 0, s>>>(z, zd, y, B, row_loss, dz, dzd);
+  launch_pdl(bce_kernel, ew_grid(B, 1), 256, 0, s, z, zd, y, B, row_loss, dz, dzd);
   after_launch("bce");
-  reduce_final<<<1, 1024, 0, s>>>(row_loss, (int)B, loss_out, 1.f / (float)B);
+  launch_pdl(reduce_final, 1, 1024, 0, s, row_loss, (int)B, loss_out, 1.f / (float)B);
   after_launch("bce_mean");
 }
 void sgd_multi(const SgdEntry* e, int n, float lr, float mu, float wd, float scale, cudaStream_t s, int blocks_per_sm) {
@@ -647,7 +657,7 @@ void sgd_multi(const SgdEntry* e, int n, float lr, float mu, float wd, float sca
     for (int i = 0; i < t.n; ++i)
       bytes += (double)t.e[i].n * (12 + (t.e[i].mom ? 8 : 0) + (t.e[i].shadow ? 2 : 0));
     const int pidx = prof_begin("sgd", 0.0, bytes, t.n, 0, 0, s);
-    sgd_kernel<<<grid, 256, 0, s>>>(t, lr, mu, wd, scale);
+    launch_pdl(sgd_kernel, grid, 256, 0, s, t, lr, mu, wd, scale);
     prof_end(pidx, s);
     after_launch("sgd_multi");
   }
