@@ -714,6 +714,7 @@ constexpr int SMEM_UPD = STAGES_UPD * STAGE_BYTES + kUpdWarps * kUpdWarpBytes + 
 template <bool UPD = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
   using namespace pair;
   constexpr int NST = UPD ? STAGES_UPD : STAGES;
   constexpr int EPI = UPD ? kUpdWarps * kUpdWarpBytes : kEpiBytes;
@@ -2558,8 +2559,8 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * 2.0 +
                            (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
   const int pidx = prof_begin(g.upd ? "gemm_upd2" : "gemm_tc2_bf16", 2.0 * g.M * g.N * g.K, alg_bytes, g.M, g.N, g.K, s);
-  if (g.upd) gemm_tc2_kernel<true><<<grid, kThreads, SMEM_UPD, s>>>(p);
-  else gemm_tc2_kernel<false><<<grid, kThreads, SMEM, s>>>(p);
+  if (g.upd) launch_pdl(gemm_tc2_kernel<true>, grid, kThreads, SMEM_UPD, s, p);
+  else launch_pdl(gemm_tc2_kernel<false>, grid, kThreads, SMEM, s, p);
   prof_end(pidx, s);
   after_launch("gemm_tc2");
   if (ws) {
