@@ -2213,6 +2213,82 @@ __global__ void splitk_reduce(const float* __restrict__ ws, int splits, long lon
   }
 }
 
+// ---------------------------------------------------------------- skinny shapes (N = 1 / K = 1)
+// Heads such as NCF's [B, 128]·[128, 1] have row strides TMA cannot describe
+// (2 B) and almost no work; the 64×64 SIMT tiles wasted ≥ 98 % of their lanes
+// (23 µs per call).  N = 1: a dot product per output row — K-major A: one
+// warp per row, lanes stride over k, fixed-order shuffle reduce; MN-major A:
+// lanes over 32 consecutive rows (coalesced), 8 warps over k, split over k
+// across blocks with a fixed-order split-K reduce.  K = 1: an outer product.
+template <typename TA>
+__global__ void __launch_bounds__(256) gemv_kmajor_kernel(int M, int K, const TA* A, long long lda, const TA* B,
+                                                          long long bstride, void* D, long long ldd, int d_f32,
+                                                          float beta, const float* bias, int act) {
+  pdl_entry();
+  const int m = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (m >= M) return;
+  float acc = 0.f;
+  for (int k = lane; k < K; k += 32) acc = fmaf(ldv(A, (long long)m * lda + k), ldv(B, (long long)k * bstride), acc);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    float v = acc + (bias ? bias[0] : 0.f);
+    if (act == 1) v = fmaxf(v, 0.f);
+    if (d_f32) {
+      float* d = reinterpret_cast<float*>(D) + (long long)m * ldd;
+      *d = v + (beta != 0.f ? *d : 0.f);
+    } else {
+      uint16_t* d = reinterpret_cast<uint16_t*>(D) + (long long)m * ldd;
+      const float x = v + (beta != 0.f ? bf16_bits_to_f32(*d) : 0.f);
+      __nv_bfloat16 h = __float2bfloat16_rn(x);
+      *d = *reinterpret_cast<uint16_t*>(&h);
+    }
+  }
+}
+// MN-major A (A(m, k) = A[k·lda + m]): partial sums over k-range split blockIdx.y → ws[split][m]
+template <typename TA>
+__global__ void __launch_bounds__(256) gemv_mnmajor_kernel(int M, int K, const TA* A, long long lda, const TA* B,
+                                                           long long bstride, int kchunk, float* ws) {
+  pdl_entry();
+  __shared__ float sm[8][33];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 32 + lane;
+  const int kbeg = blockIdx.y * kchunk, kend = min(K, kbeg + kchunk);
+  float acc = 0.f;
+  if (m < M)
+    for (int k = kbeg + w; k < kend; k += 8) acc = fmaf(ldv(A, (long long)k * lda + m), ldv(B, (long long)k * bstride), acc);
+  sm[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && m < M) {
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v += sm[j][lane];
+    ws[(long long)blockIdx.y * M + m] = v;
+  }
+}
+// K = 1: D[m, n] = A(m, 0)·B(0, n) (+ bias, act, beta)
+template <typename TA>
+__global__ void __launch_bounds__(256) outer_kernel(int M, int N, const TA* A, long long astride, const TA* B,
+                                                    long long bstride, void* D, long long ldd, int d_f32, float beta,
+                                                    const float* bias, int act) {
+  pdl_entry();
+  const long long total = (long long)M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i - (long long)m * N);
+    float v = ldv(A, (long long)m * astride) * ldv(B, (long long)n * bstride) + (bias ? bias[n] : 0.f);
+    if (act == 1) v = fmaxf(v, 0.f);
+    if (d_f32) {
+      float* d = reinterpret_cast<float*>(D) + (long long)m * ldd + n;
+      *d = v + (beta != 0.f ? *d : 0.f);
+    } else {
+      uint16_t* d = reinterpret_cast<uint16_t*>(D) + (long long)m * ldd + n;
+      const float x = v + (beta != 0.f ? bf16_bits_to_f32(*d) : 0.f);
+      __nv_bfloat16 h = __float2bfloat16_rn(x);
+      *d = *reinterpret_cast<uint16_t*>(&h);
+    }
+  }
+}
+
 // tf32 split into K-major hi/lo operands: out[mn, k] (ld2) from x (K-major
 // x[mn*ldx + k] or MN-major x[k*ldx + mn]); 32x32 smem tiles keep both the
 // read and the write coalesced.
@@ -3061,6 +3137,53 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
     }
     if (tmp) ctx().alloc.free(tmp);  // stream-ordered reuse is safe
     return "tcgen05";
+  }
+  if (g.N == 1 || g.K == 1) {
+    g_simt_calls++;
+    const double es = g.ab == BE_F32 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
+    const int pidx = prof_begin("gemm_skinny", 2.0 * g.M * g.N * g.K,
+                                ((double)g.M * g.K + (double)g.N * g.K) * es + (double)g.M * g.N * ds, g.M, g.N, g.K, s);
+    const bool bf = g.ab == BE_BF16;
+    if (g.K == 1) {
+      // A(m, 0) at m·(a_kmajor ? lda : 1); B(0, n) at n·(b_kmajor ? ldb : 1)
+      const long long as = g.a_kmajor ? g.lda : 1, bs = g.b_kmajor ? g.ldb : 1;
+      const long long total = (long long)g.M * g.N;
+      const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+      if (bf) launch_pdl(outer_kernel<uint16_t>, blocks, 256, 0, s, g.M, g.N, (const uint16_t*)g.A, as, (const uint16_t*)g.B, bs,
+                         g.D, (long long)g.ldd, (int)(g.d == BE_F32), g.beta, g.bias, g.act);
+      else launch_pdl(outer_kernel<float>, blocks, 256, 0, s, g.M, g.N, (const float*)g.A, as, (const float*)g.B, bs, g.D,
+                      (long long)g.ldd, (int)(g.d == BE_F32), g.beta, g.bias, g.act);
+      after_launch("gemm_outer");
+    } else if (g.a_kmajor) {
+      const long long bs = g.b_kmajor ? 1 : g.ldb;  // B(k, 0)
+      const int blocks = (g.M + 7) / 8;
+      if (bf) launch_pdl(gemv_kmajor_kernel<uint16_t>, blocks, 256, 0, s, g.M, g.K, (const uint16_t*)g.A, (long long)g.lda,
+                         (const uint16_t*)g.B, bs, g.D, (long long)g.ldd, (int)(g.d == BE_F32), g.beta, g.bias, g.act);
+      else launch_pdl(gemv_kmajor_kernel<float>, blocks, 256, 0, s, g.M, g.K, (const float*)g.A, (long long)g.lda,
+                      (const float*)g.B, bs, g.D, (long long)g.ldd, (int)(g.d == BE_F32), g.beta, g.bias, g.act);
+      after_launch("gemm_gemv");
+    } else {
+      const long long bs = g.b_kmajor ? 1 : g.ldb;
+      const int mb = (g.M + 31) / 32;
+      int splits = std::max(1, std::min<int>(ctx().num_sms * 2 / mb, g.K / 256));
+      const int kchunk = (g.K + splits - 1) / splits;
+      splits = (g.K + kchunk - 1) / kchunk;
+      Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * g.M, s);
+      float* wsp = reinterpret_cast<float*>(ws->ptr);
+      dim3 grid(mb, splits);
+      if (bf) launch_pdl(gemv_mnmajor_kernel<uint16_t>, grid, 256, 0, s, g.M, g.K, (const uint16_t*)g.A, (long long)g.lda,
+                         (const uint16_t*)g.B, bs, kchunk, wsp);
+      else launch_pdl(gemv_mnmajor_kernel<float>, grid, 256, 0, s, g.M, g.K, (const float*)g.A, (long long)g.lda,
+                      (const float*)g.B, bs, kchunk, wsp);
+      after_launch("gemm_gemv_mn");
+      const int blocks = (int)std::min<long long>((g.M + 255) / 256, (long long)ctx().num_sms * 16);
+      launch_pdl(splitk_reduce, blocks, 256, 0, s, (const float*)wsp, splits, (long long)g.M, g.M, 1, g.D, (long long)g.ldd,
+                 (int)(g.d == BE_F32), g.beta, g.bias, g.act);
+      after_launch("gemm_gemv_reduce");
+      ctx().alloc.free(ws);
+    }
+    prof_end(pidx, s);
+    return "skinny";
   }
   g_simt_calls++;
   const int tiles = ((g.N + 63) / 64) * ((g.M + 63) / 64);
