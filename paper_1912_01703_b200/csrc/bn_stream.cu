@@ -64,7 +64,10 @@ struct Ring {
 // reusing the ring.
 template <int NS, int ITERS, int NST, typename Body>
 __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], int64_t r0, int64_t r1, int C,
-                                            uint8_t* ring, Body&& body) {
+                                            uint8_t* ring, Body&& body, int64_t ld = 0) {
+  // ld (row stride, elements) > C: a column group of a wider tensor — one
+  // bulk copy per row instead of one per chunk
+  if (ld == 0) ld = C;
   using RG = Ring<NS, ITERS, NST>;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * NS * RG::CH);
   uint64_t* empty = full + NST;
@@ -84,11 +87,19 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
         const int st = (int)(i % NST);
         sm100::mbar_wait(&empty[st], (uint32_t)((i / NST) & 1) ^ 1u);
         const int64_t rs = r0 + i * crow;
-        const uint32_t bytes = (uint32_t)(min(crow, r1 - rs) * C * 2);
+        const int nr = (int)min(crow, r1 - rs);
+        const uint32_t bytes = (uint32_t)(nr * C * 2);
         sm100::mbar_arrive_expect_tx(&full[st], bytes * NS);
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-          bulk_g2s(sm100::smem_u32(ring + (st * NS + k) * RG::CH), src[k] + rs * C, bytes, &full[st]);
+        for (int k = 0; k < NS; ++k) {
+          if (ld == C) {
+            bulk_g2s(sm100::smem_u32(ring + (st * NS + k) * RG::CH), src[k] + rs * C, bytes, &full[st]);
+          } else {
+            for (int r = 0; r < nr; ++r)
+              bulk_g2s(sm100::smem_u32(ring + (st * NS + k) * RG::CH + r * C * 2), src[k] + (rs + r) * ld,
+                       (uint32_t)(C * 2), &full[st]);
+          }
+        }
       }
     }
     return;
@@ -117,7 +128,8 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
 
 // fixed-order per-block combine of the consumers' per-row-slot sums → partial row blockIdx.x
 __device__ __forceinline__ void combine_partials(const float (&s0)[8], const float (&s1)[8], int C, float* sm,
-                                                 float* part0, float* part1) {
+                                                 float* part0, float* part1, int Ctot = 0, int col0 = 0) {
+  if (Ctot == 0) Ctot = C;
   const int t = threadIdx.x, lanes = C >> 3, rpi = kCons / lanes;
   if (t < rpi * lanes) {
     const int v = t % lanes, rl = t / lanes;
@@ -128,8 +140,8 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
   for (int i = t; i < C; i += blockDim.x) {
     float a0 = 0.f, a1 = 0.f;
     for (int w = 0; w < rpi; ++w) { a0 += sm[w * C + i]; a1 += sm[kCons * 8 + w * C + i]; }
-    part0[(int64_t)blockIdx.x * C + i] = a0;
-    part1[(int64_t)blockIdx.x * C + i] = a1;
+    part0[(int64_t)blockIdx.x * Ctot + col0 + i] = a0;
+    part1[(int64_t)blockIdx.x * Ctot + col0 + i] = a1;
   }
 }
 
@@ -318,25 +330,27 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
 }
 
 // fused ReLU backward + bias gradient: dz = gy·1[y > 0] (stored), Σ_rows dz per column
+// (column group blockIdx.y of width Cg = C / gridDim.y)
 __global__ void __launch_bounds__(kThr, 3) relu_colsum_stream_kernel(const uint16_t* __restrict__ gy,
                                                                  const uint16_t* __restrict__ y, uint16_t* dz,
                                                                  int64_t rows, int C, float* part, int64_t rps) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
+  const int Cg = C / gridDim.y, col0 = blockIdx.y * Cg;
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
-  const int c = (threadIdx.x % (C >> 3)) * 8;
+  const int c = col0 + (threadIdx.x % (Cg >> 3)) * 8;
   float s0[8] = {}, s1[8] = {};
-  const uint16_t* src[2] = {gy, y};
-  stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) {
+  const uint16_t* src[2] = {gy + col0, y + col0};
+  stream_rows<2, 2, 4>(src, r0, r1, Cg, ring, [&](int64_t row, const uint4 (&v)[2]) {
     float g[8], m[8];
     unpack8s(v[0], g);
     unpack8s(v[1], m);
 #pragma unroll
     for (int j = 0; j < 8; ++j) { g[j] = m[j] > 0.f ? g[j] : 0.f; s0[j] += g[j]; }
     *reinterpret_cast<uint4*>(dz + row * C + c) = pack8s(g);
-  });
+  }, (int64_t)C);
   __syncthreads();
-  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part, part + (int64_t)gridDim.x * C);
+  combine_partials(s0, s1, Cg, reinterpret_cast<float*>(ring), part, part + (int64_t)gridDim.x * C, C, col0);
 }
 // out[c] = Σ_split part[split][c] (+ out[c] when beta ≠ 0): 8 columns × 32
 // sub-lanes per block, each sub-lane sums every 32nd split, then a fixed-order
@@ -383,18 +397,22 @@ bool bn_stream_ok(const void* a, int64_t rows, int C) {
 
 bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int64_t rows, int C, float* out,
                         float beta, cudaStream_t s) {
-  if (!enabled() || C < 8 || C > 2048 || C % 8 != 0 || rows <= 0 || !aligned16(gy) || !aligned16(y) ||
-      !aligned16(dz))
+  // column groups of ≤ 2048 (one consumer thread per 8 channels)
+  const int groups = (C + 2047) / 2048;
+  if (!enabled() || C < 8 || C % groups != 0 || (C / groups) % 8 != 0 || rows <= 0 || !aligned16(gy) ||
+      !aligned16(y) || !aligned16(dz))
     return false;
+  const int Cg = C / groups;
   static bool once = [] { set_smem(relu_colsum_stream_kernel, kS2); return true; }();
   (void)once;
-  const int64_t rpi = kCons / (C / 8);
+  const int64_t rpi = kCons / (Cg / 8);
   const int64_t crow = 2 * rpi;
-  const int64_t sp = std::max<int64_t>(1, std::min<int64_t>(rows / (crow * 4) + 1, stream_blocks(3)));
+  const int64_t sp = std::max<int64_t>(1, std::min<int64_t>(rows / (crow * 4) + 1, stream_blocks(3) / groups));
   const int64_t rps = (rows + sp - 1) / sp;
   Block* tmp = ctx().alloc.allocate(sizeof(float) * 2 * sp * C, s);
   float* part = reinterpret_cast<float*>(tmp->ptr);
-  launch_pdl(relu_colsum_stream_kernel, (unsigned)sp, kThr, kS2, s, gy, y, dz, rows, C, part, rps);
+  launch_pdl(relu_colsum_stream_kernel, dim3((unsigned)sp, (unsigned)groups), kThr, kS2, s, gy, y, dz, rows, C, part,
+             rps);
   after_launch("relu_colsum_stream");
   launch_pdl(colsum_partials_finalize, (C + 7) / 8, 256, 0, s, part, (int)sp, C, out, beta);
   after_launch("relu_colsum_finalize");

@@ -611,7 +611,7 @@ bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int
                         float beta, cudaStream_t s);  // bn_stream.cu
 void relu_bwd_colsum(const void* dy, const void* y, void* dz, int64_t rows, int64_t cols, be_dtype dt, float* db,
                      float db_beta, int act, cudaStream_t s) {
-  if (act && dt == BE_BF16 && cols <= 2048 &&
+  if (act && dt == BE_BF16 && (cols <= 2048 || (cols <= 16384 && rows >= 1024)) &&
       relu_colsum_stream(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(y),
                          reinterpret_cast<uint16_t*>(dz), rows, (int)cols, db, db_beta, s))
     return;
