@@ -2445,7 +2445,12 @@ bool gemm_update_ok(const GemmDesc& g) {
   if (!g.upd || g.ab != BE_BF16) return false;
   const uintptr_t pa = reinterpret_cast<uintptr_t>(g.upd->p), va = reinterpret_cast<uintptr_t>(g.upd->v),
                   sa = reinterpret_cast<uintptr_t>(g.upd->shadow);
-  return g.ldd % 8 == 0 && ((pa | va | sa) & 15) == 0;  // TMA: 16-B aligned bases and row pitches
+  if (g.ldd % 8 != 0 || ((pa | va | sa) & 15) != 0) return false;  // TMA: 16-B aligned bases and row pitches
+  // the update epilogue needs the whole K sum in one CTA (no split-K): a
+  // small-output, long-K wgrad (NCF's 256×256 tower layers, K = 8192: 4–16
+  // tiles on 148 SMs, 45 µs) runs faster as a split-K GEMM + the SGD kernel
+  const long long tiles = (long long)((g.M + 127) / 128) * ((g.N + 127) / 128);
+  return !(tiles * 4 < ctx().num_sms && g.K > 2048);
 }
 namespace {
 void set_update(GemmParams& p, const GemmDesc& g) {
