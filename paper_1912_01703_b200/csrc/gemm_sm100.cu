@@ -2794,10 +2794,10 @@ static bool conv_small_c(const void* x, const void* w, void* y, const ConvGeom& 
 bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                       cudaStream_t s) {
   static const int on = [] { const char* e = getenv("BE_WGRAD_PATCH"); return e ? atoi(e) : 1; }();
-  if (!on || g.stride != 1 || dwt != BE_F32 || g.R * g.S > 16) return false;
-  if (!((g.C == 64 && g.K == 64) || (g.C == 128 && g.K == 128))) return false;
+  if (!on || g.stride != 1 || dwt != BE_F32 || g.R * g.S > 64) return false;
+  if (!((g.C == 64 && g.K % 64 == 0 && g.K <= 256) || (g.C == 128 && g.K == 128))) return false;
   const wgp::Geo gg = wgp::geo(g.Q, g.R, g.S, g.C, g.K);
-  if (gg.Wp > BM || gg.nbuf < 2 || gg.G + g.R - 1 > 256 || gg.ngroups * 2 > ctx().num_sms) return false;
+  if (gg.Wp > BM || gg.nbuf < 2 || gg.G + g.R - 1 > 256 || gg.gs > 8 || gg.ngroups * 2 > ctx().num_sms) return false;
   if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
   const int smem = 1024 + gg.nbuf * gg.bufb + 256;
   if (smem > 227 * 1024) return false;

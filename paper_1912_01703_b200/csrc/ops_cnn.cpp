@@ -86,8 +86,8 @@ static void vjp_conv(Node* n, GradSink& sink) {
       static const int shift_on = [] { const char* e = getenv("BE_WGRAD_SHIFT"); return e ? atoi(e) : 1; }();
       const bool shift_ok = shift_on && g.Q <= 64 && g.K % 8 == 0 && g.stride <= 2;
       // variant 3: shared input patch per tile, shifted UMMA operands (stride 1, C = K = 64)
-      const bool patch_ok = shift_ok && g.stride == 1 && ((g.C == 64 && g.K == 64) || (g.C == 128 && g.K == 128)) &&
-                            dw->dtype == BE_F32 && g.R * g.S <= 16 && g.Q + g.S - 1 <= 128;
+      const bool patch_ok = shift_ok && g.stride == 1 && ((g.C == 64 && g.K % 64 == 0 && g.K <= 256) || (g.C == 128 && g.K == 128)) &&
+                            dw->dtype == BE_F32 && g.R * g.S <= 64 && g.Q + g.S - 1 <= 128;
       variant = tune_choose(key, patch_ok ? 4 : (shift_ok ? 3 : 2), 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);

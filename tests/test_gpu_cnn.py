@@ -308,7 +308,9 @@ def test_bn_statistics_from_conv_epilogue(cfg):
                                  # row group (P = 27, G = 4), a 2×2 kernel (even tap count)
                                  (2, 64, 56, 56, 64, 3, 1, 1), (2, 64, 27, 25, 64, 3, 1, 1), (1, 64, 10, 12, 64, 2, 1, 0),
                                  # C = K = 128 (one tap per MMA, 3 tap groups): ResNet layer-2 size, ragged
-                                 (2, 128, 28, 28, 128, 3, 1, 1), (1, 128, 13, 11, 128, 3, 1, 1)])
+                                 (2, 128, 28, 28, 128, 3, 1, 1), (1, 128, 13, 11, 128, 3, 1, 1),
+                                 # C = 64, K = 192 (AlexNet conv2 5×5: three dY planes, N = 192, 7 tap groups)
+                                 (2, 64, 27, 27, 192, 5, 1, 2)])
 def test_conv_wgrad_variants_bf16(cfg):
     """Conv weight gradient through every autotuned variant (the first calls
     of a shape cycle through them: TMA-im2col B, materialised columns,
