@@ -260,21 +260,37 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- end-to-end through the public API: every step's batch goes pinned host → device
     # (double-buffered on a copy stream so batch i+1 transfers while step i computes, the
     # data loader's pinned-memory path) and the loss comes back device → host
-    pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in hb]
+    # CNN images travel as the real 3 channels (bf16 NHWC, 2.7x fewer bytes over
+    # the host link); the device pads them to the kernels' 8-channel layout
+    # (concat with a resident zero block) inside the timed step
+    hb_e2e, dts_e2e, pad = list(hb), list(dts), None
+    if cfg["net"] in ("alexnet", "resnet50") and cfg["dtype"] == "bf16":
+        img = hb[0]
+        npix = img.shape[0] * img.shape[1] * img.shape[2]
+        hb_e2e[0] = np.ascontiguousarray(img[..., :3]).reshape(npix, 3)
+        zeros5 = be.tensor(np.zeros((npix, 5), np.float32), dtype="bf16")
+        pad = (zeros5, tuple(img.shape))
+    pinned = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in hb_e2e]
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
     shapes = [(a.shape, d or {np.dtype(np.int32): "i32", np.dtype(np.float32): "f32"}[a.dtype])
-              for a, d in zip(hb, dts)]
+              for a, d in zip(hb_e2e, dts_e2e)]
     pipe = be.api.InputPipeline(shapes)
     host = [(p.data_ptr(), p.numel() * p.element_size()) for p in pinned]
     import ctypes as C
-    h2d = sum(a.nbytes for a in hb)
+    h2d = sum(a.nbytes for a in hb_e2e)
+
+    def e2e_batch(b):
+        if pad is None:
+            return b
+        x8 = be.reshape(be.concat([b[0], pad[0]]), pad[1])
+        return [x8] + list(b[1:])
 
     def e2e_loop(n):
         pipe.put(0, host)
         loss = None
         for i in range(n):
             cur = i % 2
-            loss = step(pipe.get(cur))
+            loss = step(e2e_batch(pipe.get(cur)))
             pipe.release(cur)
             if i + 1 < n:
                 pipe.put(1 - cur, host)
