@@ -205,6 +205,13 @@ be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum,
  * Params that get no gradient in a backward are not updated. */
 be_status be_sgd_overlap(const be_tensor* params, int n, float lr, float momentum,
                          float weight_decay);
+/* The SGD momentum buffer v of f32 parameter `param` (SPEC S:578-586 update
+ * above; the paper names the optimizer without formulas): *out receives a NEW
+ * f32 tensor of the param's shape holding a copy of v, taken on the compute
+ * stream after every update enqueued so far (caller owns one reference), or
+ * NULL when no momentum step has run for this param.  Inspection / parity
+ * only; BE_E_BAD_HANDLE on an invalid handle. */
+be_status be_sgd_momentum(be_tensor param, be_tensor* out);
 
 /* ------------------------------------------------------------------ allocator */
 struct be_alloc_stats {
@@ -228,11 +235,22 @@ be_status be_raw_free(uint64_t dptr);
  * via be_dist_unique_id), distributed by the caller (torch.distributed). */
 be_status be_dist_unique_id(void* out128);
 be_status be_dist_init(int rank, int world, const void* nccl_unique_id);
-/* Attach params for DDP: broadcast from rank 0; grads become
- * views into fp32 buckets of ~bucket_bytes in reverse param order; each bucket
- * is all-reduced (sum) on a comm stream as soon as its last grad lands during
- * backward; be_sgd_step waits for all buckets and folds in 1/world. */
+/* Attach params for DDP: broadcast from rank 0;
+ * grads become views into fp32 buckets of ~bucket_bytes in reverse param
+ * order; each bucket is all-reduced (ncclAvg: the bucket holds the MEAN
+ * gradient) on a comm stream as soon as the last gradient
+ * of every parameter in it is final (all tape edges into a tied / shared
+ * weight have run) during backward.  be_backward returns with the compute
+ * stream ordered after every bucket, so grads read afterwards are reduced and
+ * a second (accumulating) backward gives mean(g1) + mean(g2).  Fails
+ * (BE_E_ARG) without side effects if a param is invalid or listed twice. */
 be_status be_ddp_attach(const be_tensor* params, int n, size_t bucket_bytes);
+/* Broadcast f32 buffers (e.g. BatchNorm running mean / var) from rank 0 on the
+ * compute stream, as data-parallel training does before each forward; BN
+ * statistics used by the step stay local to each replica (DESIGN R6). */
+be_status be_ddp_sync_buffers(const be_tensor* bufs, int n);
+/* rank / world of the communicator (BE_E_NOT_INIT before be_dist_init). */
+be_status be_dist_world(int* rank, int* world);
 be_status be_ddp_detach(void);
 /* Pure host function (no GPU needed): the bucket plan be_ddp_attach uses.
  * numels[n] = parameter sizes in registration order.  Buckets are filled in
@@ -279,9 +297,14 @@ be_status be_tensor_copy_from_host_on(be_tensor t, const void* src, size_t nbyte
 be_status be_synchronize(void);
 /* Read a 1-element tensor as double (synchronises). */
 be_status be_item(be_tensor t, double* out);
-/* Parity hook: the conv im2col offset table the device path uses,
- * conv_geom = {N,C,H,W,R,S,stride,pad}; out[M*R*S*C] int64 (NHWC offsets,
- * -1 in padding) computed ON THE DEVICE by the kernel's own index math. */
+/* Parity hook for the bit-exact "im2col offsets" object (
+ * SPEC S:113-121 conv geometry): runs the product's own im2col kernel (the
+ * column builder of the stride-2 dgrad / materialised wgrad paths) on a probe
+ * input whose NHWC element i holds the int32 i + 1, and returns the gathered
+ * values − 1: out[M*R*S*C] int64 = the NHWC offset each column entry was
+ * copied from, -1 in the zero padding.  conv_geom = {N,C,H,W,R,S,stride,pad}.
+ * Synchronises.  (The implicit-GEMM conv kernels' gathers are checked through
+ * the conv op itself with one-hot weights, tests/test_gpu_cnn.py.) */
 be_status be_debug_im2col_offsets(const int64_t* conv_geom, int64_t* out);
 /* Direct GEMM entry (tests): D[M,N] = A[M,K]·B[K,N] (+bias[N]) (act),
  * all row-major contiguous device tensors; A/B dtype f32 (3xTF32) or bf16;

@@ -50,8 +50,7 @@ class MLP:
         h = x
         L = len(self.sizes) - 1
         for i in range(L):
-            # logits are produced in fp32 (not a bf16 storage point)
-            h = ops.linear(h, P[f"fc{i}.w"], P[f"fc{i}.b"], store_out=i < L - 1)
+            h = ops.linear(h, P[f"fc{i}.w"], P[f"fc{i}.b"])
             if i < L - 1:
                 h = ops.relu(h)
         return h

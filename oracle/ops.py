@@ -15,40 +15,6 @@ from .autograd import Var, record
 
 f64 = np.float64
 
-# ---------------------------------------------------------------- storage precision
-# The method is fp32 in the paper.  For the bf16 path the
-# device stores activations, weight operands and activation gradients in bf16
-# and lets those stored values decide ReLU masks / max-pool winners.  Per
-# SURVEY §8(c) reading 16 / DESIGN.md reading R7, integer decisions taken from
-# floating point must be taken in the same precision on both sides, so the
-# oracle can round (RN-even) at exactly those storage points.  Arithmetic
-# between storage points stays float64.  Default "f64": no rounding.
-_STORAGE = ["f64"]
-
-
-def set_storage(p: str):
-    assert p in ("f64", "bf16")
-    _STORAGE[0] = p
-
-
-def bf16_round(a):
-    """Round-to-nearest-even to bfloat16 (8-bit significand), returned as
-    float64.  Written from the IEEE definition: round the float32 value to
-    the nearest multiple of 2^(e-7), ties to even; NaN/inf pass through."""
-    x = np.asarray(a, dtype=np.float64).astype(np.float32)
-    bits = x.view(np.uint32).astype(np.uint64)
-    lsb = (bits >> 16) & 1
-    rounded = ((bits + 0x7FFF + lsb) >> 16) << 16
-    out = rounded.astype(np.uint32).view(np.float32).astype(np.float64)
-    special = ~np.isfinite(x)
-    return np.where(special, x.astype(np.float64), out)
-
-
-def q(a):
-    """Value as the device stores it (identity in f64 mode)."""
-    return bf16_round(a) if _STORAGE[0] == "bf16" else np.asarray(a, dtype=f64)
-
-
 def _unbroadcast(g, shape):
     """Sum a broadcast gradient back to `shape` (SPEC S:83-91 right-aligned
     broadcasting; S:278 'broadcasted leaf receives column-summed gradient')."""
@@ -90,29 +56,18 @@ def matmul(a: Var, b: Var) -> Var:
     return record("matmul", [a, b], av @ bv, lambda g: [g @ bv.T, av.T @ g])
 
 
-def linear(x: Var, w: Var, b: Var | None, act=None, store_out=True) -> Var:
+def linear(x: Var, w: Var, b: Var | None) -> Var:
     """Listing 1 LinearLayer.forward: Y = X·W + b.
-    dX = dY·Wᵀ, dW = Xᵀ·dY, db = Σ_n dY[n,:].
-    act="relu" fuses y = max(Y, 0), dY ← dY·1[y>0] (same as linear → relu).
-    Storage points (bf16 mode only): operands X, W, the output y (unless
-    store_out=False, e.g. fp32 logits), the incoming dY and the dX it emits."""
-    xv, wv = q(x.value), q(w.value)
+    dX = dY·Wᵀ, dW = Xᵀ·dY, db = Σ_n dY[n,:]."""
+    xv, wv = x.value.astype(f64), w.value.astype(f64)
     y = xv @ wv
     ins = [x, w]
     if b is not None:
         y = y + b.value.astype(f64)[None, :]
         ins.append(b)
-    if act == "relu":
-        y = np.maximum(y, 0.0)
-    if store_out:
-        y = q(y)
-    mask = (y > 0).astype(f64) if act == "relu" else None
 
     def vjp(g):
-        g = q(g)
-        if mask is not None:
-            g = g * mask
-        out = [q(g @ wv.T), xv.T @ g]
+        out = [g @ wv.T, xv.T @ g]
         if b is not None:
             out.append(g.sum(axis=0))
         return out

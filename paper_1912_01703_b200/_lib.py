@@ -106,6 +106,7 @@ def lib():
             "be_zero_grad": [P(T), C.c_int],
             "be_sgd_step": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
             "be_sgd_overlap": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
+            "be_sgd_momentum": [T, P(T)],
             "be_alloc_stats": [P(be_alloc_stats)],
             "be_alloc_reset_peak": [],
             "be_empty_cache": [P(C.c_uint64)],
@@ -116,6 +117,8 @@ def lib():
             "be_dist_init": [C.c_int, C.c_int, C.c_void_p],
             "be_ddp_attach": [P(T), C.c_int, C.c_size_t],
             "be_ddp_detach": [],
+            "be_ddp_sync_buffers": [P(T), C.c_int],
+            "be_dist_world": [P(C.c_int), P(C.c_int)],
             "be_allreduce_": [T],
             "be_synchronize": [],
             "be_item": [T, P(C.c_double)],
@@ -165,4 +168,5 @@ EXPORTED = [
     "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
     "be_stream_create", "be_stream_destroy", "be_event_create", "be_event_destroy", "be_event_record",
     "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap",
+    "be_sgd_momentum", "be_ddp_sync_buffers", "be_dist_world",
 ]

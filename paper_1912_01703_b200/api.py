@@ -340,6 +340,13 @@ def sgd_overlap(params, lr=0.0, momentum=0.0, weight_decay=0.0):
          C.c_float(weight_decay))
 
 
+def sgd_momentum(param):
+    """Copy of the SGD momentum buffer v of `param` (None before the first momentum step)."""
+    out = C.c_void_p()
+    call("be_sgd_momentum", param._h, C.byref(out))
+    return Tensor(out.value) if out.value else None
+
+
 def zero_grad(params):
     call("be_zero_grad", _handles(params), len(params))
 
@@ -475,6 +482,18 @@ def ddp_attach(params, bucket_bytes=25 << 20):
 
 def ddp_detach():
     call("be_ddp_detach")
+
+
+def ddp_sync_buffers(bufs):
+    """Broadcast f32 buffers (BN running statistics) from rank 0."""
+    if bufs:
+        call("be_ddp_sync_buffers", _handles(bufs), len(bufs))
+
+
+def dist_world():
+    r, w = C.c_int(), C.c_int()
+    call("be_dist_world", C.byref(r), C.byref(w))
+    return r.value, w.value
 
 
 def allreduce_(t):

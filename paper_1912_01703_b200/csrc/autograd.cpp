@@ -15,10 +15,7 @@
 // buffers are released the moment their node has run, so their blocks go
 // back to the stream pool immediately.
 #include <algorithm>
-#include <map>
 #include <queue>
-#include <unordered_map>
-#include <unordered_set>
 
 #include "kernels.h"
 #include "runtime.h"
@@ -86,7 +83,41 @@ Tensor* unpack(Node* n, int i, TRef& holder) {
   return t;
 }
 
-// ------------------------------------------------------------------ GradSink
+// ------------------------------------------------------------------ engine
+// Engine state of one backward pass.  Per-node scratch (dependency count,
+// pending output gradients) lives in the Node and per-leaf scratch (edges
+// still to run) in the Tensor, stamped with the pass id, so the sweep does no
+// hashing and no per-node heap allocation beyond the gradient buffers.
+struct Engine {
+  uint64_t epoch = 0;
+  bool retain = false;
+  bool opt = false;      // overlapped SGD (non-DDP): per-leaf readiness
+  bool ddp = false;      // DDP attached: per-leaf readiness → bucket launch
+  std::vector<Tensor*> final_leaves;    // completed by the current node's VJP
+  std::vector<Tensor*> partial_leaves;  // got a gradient, edges outstanding
+  std::vector<Node*> touched;           // nodes holding pending buffers
+
+  bool tracks(Tensor* leaf) const {
+    return (ddp && leaf->ddp_slot >= 0) || (opt && opt_param(leaf));
+  }
+  void leaf_ready(Tensor* leaf) {
+    if (ddp) ddp_on_leaf_grad_ready(leaf);
+    else opt_on_grad_final(leaf);
+  }
+  Tensor*& pend(Node* m, int k) {
+    if (m->pend.size() < m->outs.size()) {
+      if (m->pend.empty()) touched.push_back(m);
+      m->pend.resize(m->outs.size(), nullptr);
+    }
+    return m->pend[k];
+  }
+  void drop_pending(Node* m) {
+    for (Tensor*& t : m->pend)
+      if (t) { tensor_drop(t); t = nullptr; }
+    m->pend.clear();
+  }
+};
+
 bool GradSink::needs(int i) const { return node->edges[i].kind != Edge::NONE; }
 
 Tensor* GradSink::dest(int i, float* beta) {
@@ -137,16 +168,82 @@ void GradSink::commit(int i) {
   s.used = false;
 }
 
-// ------------------------------------------------------------------ engine
+Tensor* GradSink::acquire(int i, bool* existing) {
+  Edge& e = node->edges[i];
+  if (e.kind == Edge::LEAF) {
+    Tensor* leaf = e.leaf;
+    if (leaf->grad) { *existing = true; return leaf->grad; }
+    TRef g = eng->ddp ? TRef(ddp_grad_view(leaf)) : TRef();
+    if (!g) g = new_tensor(leaf->shape, leaf->rank, BE_F32);
+    leaf->grad = g.release();
+    *existing = false;
+    return leaf->grad;
+  }
+  Tensor*& slot = eng->pend(e.node, e.output_nr);
+  if (slot) { *existing = true; return slot; }
+  const OutMeta& m = e.node->outs[e.output_nr];
+  slot = new_tensor(m.shape, m.rank, m.dtype).release();
+  *existing = false;
+  return slot;
+}
+
+bool GradSink::adopt(int i, Tensor* t) {
+  Edge& e = node->edges[i];
+  if (e.kind == Edge::LEAF) {
+    Tensor* leaf = e.leaf;
+    if (leaf->grad || eng->ddp || t->dtype != BE_F32 || !t->is_contiguous() || t->numel() != leaf->numel())
+      return false;
+    t->rank = leaf->rank;
+    int64_t st = 1;
+    for (int d = leaf->rank - 1; d >= 0; --d) { t->shape[d] = leaf->shape[d]; t->strides[d] = st; st *= leaf->shape[d]; }
+    leaf->grad = t;
+    return true;
+  }
+  Tensor*& slot = eng->pend(e.node, e.output_nr);
+  if (slot) return false;
+  const OutMeta& m = e.node->outs[e.output_nr];
+  int64_t mn = 1;
+  for (int d = 0; d < m.rank; ++d) mn *= m.shape[d];
+  if (m.dtype != t->dtype || !t->is_contiguous() || mn != t->numel()) return false;
+  t->rank = m.rank;
+  int64_t st = 1;
+  for (int d = m.rank - 1; d >= 0; --d) { t->shape[d] = m.shape[d]; t->strides[d] = st; st *= m.shape[d]; }
+  slot = t;
+  return true;
+}
+
+bool GradSink::fuse(int i, k::SgdFuse* f) {
+  if (!eng || !eng->opt) return false;
+  Edge& e = node->edges[i];
+  if (e.kind != Edge::LEAF || !opt_param(e.leaf) || e.leaf->grad) return false;
+  if (e.leaf->bw_epoch != eng->epoch || e.leaf->bw_uses != 1) return false;  // more contributions to come
+  return opt_fuse_desc(e.leaf, f);
+}
+
+void GradSink::fused(int i) {
+  Tensor* leaf = node->edges[i].leaf;
+  --leaf->bw_uses;
+  opt_fused_done(leaf);
+}
+
+void GradSink::finalize(int i, Tensor* t) {
+  Edge& e = node->edges[i];
+  if (e.kind != Edge::LEAF) return;
+  t->bump_version();
+  Tensor* leaf = e.leaf;
+  if (!eng->tracks(leaf)) return;
+  // a tracked leaf is ready (DDP bucket / overlapped update) only once every
+  // edge into it has run — tied or shared weights get several contributions
+  if (--leaf->bw_uses == 0) {
+    leaf->bw_partial = false;
+    eng->final_leaves.push_back(leaf);
+  } else if (!leaf->bw_partial) {
+    leaf->bw_partial = true;
+    eng->partial_leaves.push_back(leaf);
+  }
+}
+
 namespace {
-struct PKey {
-  Node* n;
-  int k;
-  bool operator==(const PKey& o) const { return n == o.n && k == o.k; }
-};
-struct PKeyHash {
-  size_t operator()(const PKey& p) const { return std::hash<void*>()(p.n) * 31 + p.k; }
-};
 struct BySeq {
   bool operator()(Node* a, Node* b) const { return a->seq < b->seq; }
 };
@@ -165,6 +262,15 @@ void accumulate_leaf(Tensor* leaf, Tensor* g) {
   if (ddp_active()) ddp_on_leaf_grad_ready(leaf);
   else if (opt_param(leaf)) opt_on_grad_final(leaf);
 }
+
+// End of every backward: DDP buckets that did not fire are reduced and the
+// compute stream waits on every bucket allreduce, so a gradient read (or a
+// second, accumulating backward) after be_backward sees the reduced values;
+// the overlapped optimizer's updates are joined likewise.
+void end_backward() {
+  if (ddp_active()) ddp_wait_all();
+  opt_end_backward();
+}
 }  // namespace
 
 void run_backward(Tensor* root, Tensor* upstream, bool retain) {
@@ -181,125 +287,70 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
     k::fill(seed->data(), 1, seed->dtype, 1.0, s);
     ones = true;
   }
-  if (ddp_active()) ddp_begin_backward();
+  Engine eng;
+  eng.epoch = ++ctx().bw_epoch;
+  eng.retain = retain;
+  eng.ddp = ddp_active();
+  eng.opt = opt_active() && !eng.ddp;
+  if (eng.ddp) ddp_begin_backward();
   if (!root->grad_fn) {  // leaf root
     accumulate_leaf(root, seed.get());
-    opt_end_backward();
+    end_backward();
     return;
   }
-  // 1. dependency counts (+ per-leaf use counts for the overlapped optimizer:
-  // a registered parameter's gradient is final once every edge to it is done)
-  const bool opt = opt_active() && !ddp_active();
-  std::unordered_map<Node*, int> deps;
-  std::unordered_map<Tensor*, int> leaf_uses;
+  // 1. dependency counts (+ per-leaf edge counts for tracked leaves: an
+  // overlapped-SGD or DDP parameter is ready once every edge to it has run)
+  const bool opt_any = opt_active();
   std::vector<Node*> stack{root->grad_fn};
-  std::unordered_set<Node*> seen{root->grad_fn};
+  root->grad_fn->bw_epoch = eng.epoch;
+  root->grad_fn->bw_deps = 0;
   while (!stack.empty()) {
     Node* n = stack.back();
     stack.pop_back();
     BE_REQUIRE(!n->consumed, BE_E_DOUBLE_BACKWARD,
                std::string("backward through ") + n->name + " a second time without retain_graph");
     for (Edge& e : n->edges) {
-      if (opt && e.kind == Edge::LEAF && opt_param(e.leaf)) leaf_uses[e.leaf]++;
+      if (e.kind == Edge::LEAF) {
+        Tensor* leaf = e.leaf;
+        if (eng.ddp && opt_any && opt_param(leaf))
+          BE_REQUIRE(leaf->ddp_slot >= 0, BE_E_ARG,
+                     "a parameter registered for overlapped SGD is not attached to DDP (it would never be updated)");
+        if (eng.tracks(leaf)) {
+          if (leaf->bw_epoch != eng.epoch) { leaf->bw_epoch = eng.epoch; leaf->bw_uses = 0; leaf->bw_partial = false; }
+          leaf->bw_uses++;
+        }
+        continue;
+      }
       if (e.kind != Edge::NODE) continue;
-      deps[e.node]++;
-      if (seen.insert(e.node).second) stack.push_back(e.node);
+      Node* m = e.node;
+      if (m->bw_epoch != eng.epoch) {
+        m->bw_epoch = eng.epoch;
+        m->bw_deps = 0;
+        stack.push_back(m);
+      }
+      m->bw_deps++;
     }
   }
-  std::vector<Tensor*> final_leaves;             // completed by the current node's VJP
-  std::vector<Tensor*> ddp_leaves;               // DDP: grads landed in the current node's VJP
-  std::unordered_set<Tensor*> partial_leaves;    // got a gradient, some edges never ran
-  // 2. reverse-topological sweep
-  std::unordered_map<PKey, Tensor*, PKeyHash> pending;  // owned refs
-  pending[{root->grad_fn, root->output_nr}] = seed.release();
-  std::priority_queue<Node*, std::vector<Node*>, BySeq> ready;
+  // 2. reverse-topological sweep (max creation sequence first)
+  eng.pend(root->grad_fn, root->output_nr) = seed.release();
+  std::vector<Node*> heap_store;
+  heap_store.reserve(64);
+  std::priority_queue<Node*, std::vector<Node*>, BySeq> ready(BySeq(), std::move(heap_store));
   ready.push(root->grad_fn);
   root->grad_fn->upstream_is_ones = ones;
-  std::vector<Node*> to_release;
+  GradSink sink;
+  sink.eng = &eng;
+  sink.retain = retain;
   try {
     while (!ready.empty()) {
       Node* n = ready.top();
       ready.pop();
-      GradSink sink;
       sink.node = n;
-      sink.retain = retain;
       sink.upstream.assign(n->outs.size(), nullptr);
       bool any = false;
-      for (int k2 = 0; k2 < (int)n->outs.size(); ++k2) {
-        auto it = pending.find({n, k2});
-        if (it != pending.end()) { sink.upstream[k2] = it->second; any = true; }
-      }
+      for (size_t k2 = 0; k2 < n->pend.size(); ++k2)
+        if (n->pend[k2]) { sink.upstream[k2] = n->pend[k2]; any = true; }
       sink.slots.assign(n->edges.size(), GradSink::Slot());
-      sink.acquire = [&](int i, bool* existing) -> Tensor* {
-        Edge& e = n->edges[i];
-        if (e.kind == Edge::LEAF) {
-          Tensor* leaf = e.leaf;
-          if (leaf->grad) { *existing = true; return leaf->grad; }
-          TRef g = ddp_active() ? TRef(ddp_grad_view(leaf)) : TRef();
-          if (!g) g = new_tensor(leaf->shape, leaf->rank, BE_F32);
-          leaf->grad = g.release();
-          *existing = false;
-          return leaf->grad;
-        }
-        PKey key{e.node, e.output_nr};
-        auto it = pending.find(key);
-        if (it != pending.end()) { *existing = true; return it->second; }
-        const OutMeta& m = e.node->outs[e.output_nr];
-        TRef g = new_tensor(m.shape, m.rank, m.dtype);
-        Tensor* raw = g.release();
-        pending[key] = raw;
-        *existing = false;
-        return raw;
-      };
-      sink.adopt = [&](int i, Tensor* t) -> bool {
-        Edge& e = n->edges[i];
-        if (e.kind == Edge::LEAF) {
-          Tensor* leaf = e.leaf;
-          if (leaf->grad || ddp_active() || t->dtype != BE_F32 || !t->is_contiguous() ||
-              t->numel() != leaf->numel())
-            return false;
-          t->rank = leaf->rank;
-          int64_t st = 1;
-          for (int d = leaf->rank - 1; d >= 0; --d) { t->shape[d] = leaf->shape[d]; t->strides[d] = st; st *= leaf->shape[d]; }
-          leaf->grad = t;
-          return true;
-        }
-        PKey key{e.node, e.output_nr};
-        if (pending.count(key)) return false;
-        const OutMeta& m = e.node->outs[e.output_nr];
-        int64_t mn = 1;
-        for (int d = 0; d < m.rank; ++d) mn *= m.shape[d];
-        if (m.dtype != t->dtype || !t->is_contiguous() || mn != t->numel()) return false;
-        t->rank = m.rank;
-        int64_t st = 1;
-        for (int d = m.rank - 1; d >= 0; --d) { t->shape[d] = m.shape[d]; t->strides[d] = st; st *= m.shape[d]; }
-        pending[key] = t;
-        return true;
-      };
-      sink.fuse = [&](int i, k::SgdFuse* f) -> bool {
-        if (!opt) return false;
-        Edge& e = n->edges[i];
-        if (e.kind != Edge::LEAF || !opt_param(e.leaf) || e.leaf->grad) return false;
-        auto it = leaf_uses.find(e.leaf);
-        if (it == leaf_uses.end() || it->second != 1) return false;  // more contributions to come
-        return opt_fuse_desc(e.leaf, f);
-      };
-      sink.fused = [&](int i) {
-        Edge& e = n->edges[i];
-        --leaf_uses[e.leaf];
-        opt_fused_done(e.leaf);
-      };
-      sink.finalize = [&](int i, Tensor* t) {
-        Edge& e = n->edges[i];
-        if (e.kind == Edge::LEAF) {
-          t->bump_version();
-          if (ddp_active()) ddp_leaves.push_back(e.leaf);
-          else if (opt && opt_param(e.leaf)) {
-            partial_leaves.insert(e.leaf);
-            if (--leaf_uses[e.leaf] == 0) { final_leaves.push_back(e.leaf); partial_leaves.erase(e.leaf); }
-          }
-        }
-      };
       if (any) {
         for (size_t k2 = 0; k2 < n->saved.size(); ++k2) {  // version check at unpack
           SavedVar& sv = n->saved[k2];
@@ -308,33 +359,29 @@ void run_backward(Tensor* root, Tensor* upstream, bool retain) {
                                    " was modified in place after it was saved");
         }
         n->vjp(n, sink);
-        // updates are enqueued only after every kernel of this VJP (which may
-        // still read the parameter or its bf16 shadow after committing dW)
-        for (Tensor* leaf : final_leaves) opt_on_grad_final(leaf);
-        final_leaves.clear();
-        // likewise DDP bucket launches (their allreduce may be followed by
-        // the overlapped update of the bucket's parameters)
-        for (Tensor* leaf : ddp_leaves) ddp_on_leaf_grad_ready(leaf);
-        ddp_leaves.clear();
+        // updates / bucket launches are enqueued only after every kernel of
+        // this VJP (which may still read the parameter or its bf16 shadow
+        // after committing dW)
+        for (Tensor* leaf : eng.final_leaves) eng.leaf_ready(leaf);
+        eng.final_leaves.clear();
       }
       n->upstream_is_ones = false;
-      for (int k2 = 0; k2 < (int)n->outs.size(); ++k2) {
-        auto it = pending.find({n, k2});
-        if (it != pending.end()) { tensor_drop(it->second); pending.erase(it); }
-      }
+      eng.drop_pending(n);
       if (!retain) { release_saved(n); n->consumed = true; }
       for (Edge& e : n->edges) {
         if (e.kind != Edge::NODE) continue;
-        if (--deps[e.node] == 0) ready.push(e.node);
+        if (--e.node->bw_deps == 0) ready.push(e.node);
       }
     }
   } catch (...) {
-    for (auto& kv : pending) tensor_drop(kv.second);
+    for (Node* m : eng.touched) eng.drop_pending(m);
     throw;
   }
-  for (auto& kv : pending) tensor_drop(kv.second);
-  for (Tensor* leaf : partial_leaves) opt_on_grad_final(leaf);
-  opt_end_backward();
+  for (Node* m : eng.touched) eng.drop_pending(m);
+  // leaves that got a gradient through some but not all of their edges
+  for (Tensor* leaf : eng.partial_leaves)
+    if (leaf->bw_partial) { leaf->bw_partial = false; eng.leaf_ready(leaf); }
+  end_backward();
 }
 
 }  // namespace be

@@ -278,20 +278,18 @@ __global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __
   }
 }
 
-__global__ void im2col_offsets_kernel(ConvGeom g, int64_t* out, int64_t total) {
+// Index probe for be_debug_im2col_offsets: element i of the probe input holds
+// the bits of the int32 i + 1 (the im2col kernel is a pure bit copy, so the
+// column matrix it builds holds 1 + the NHWC offset it gathered, 0 = padding).
+__global__ void iota1_kernel(int32_t* x, int64_t n) {
   pdl_entry();
-  const int64_t RSC = (int64_t)g.R * g.S * g.C;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / RSC, kk = i % RSC;
-    const int c = (int)(kk % g.C);
-    const int u = (int)((kk / g.C) % g.S);
-    const int r = (int)(kk / ((int64_t)g.C * g.S));
-    const int q = (int)(m % g.Q);
-    const int p = (int)((m / g.Q) % g.P);
-    const int64_t n = m / ((int64_t)g.P * g.Q);
-    const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + u;
-    out[i] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? ((n * g.H + h) * g.W + w) * g.C + c : -1;
-  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (int32_t)(i + 1);
+}
+__global__ void cols_to_offsets_kernel(const int32_t* cols, int64_t* out, int64_t n) {
+  pdl_entry();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)cols[i] - 1;
 }
 
 // ---- max pool NHWC; window scanned r outer, u inner; first strictly greater wins; NaN wins at first sight
@@ -1214,10 +1212,20 @@ void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStrea
   after_launch("flip_weights");
 }
 void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
+  // the product's im2col kernel (f32 element path) run on an index-encoded input
+  const int64_t nx = (int64_t)g.N * g.H * g.W * g.C;
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.R * g.S * g.C;
   if (total == 0) return;
-  launch_pdl(im2col_offsets_kernel, grid_for(total), 256, 0, s, g, out, total);
+  BE_REQUIRE(nx < (1ll << 31) - 1, BE_E_ARG, "im2col_offsets: input too large for the int32 probe");
+  int32_t *x = nullptr, *cols = nullptr;
+  BE_CHECK_CUDA(cudaMallocAsync(&x, std::max<int64_t>(nx, 1) * 4, s));
+  BE_CHECK_CUDA(cudaMallocAsync(&cols, total * 4, s));
+  launch_pdl(iota1_kernel, grid_for(nx), 256, 0, s, x, nx);
+  im2col(x, cols, (int64_t)g.R * g.S * g.C, g, BE_F32, s);
+  launch_pdl(cols_to_offsets_kernel, grid_for(total), 256, 0, s, (const int32_t*)cols, out, total);
   after_launch("im2col_offsets");
+  BE_CHECK_CUDA(cudaFreeAsync(x, s));
+  BE_CHECK_CUDA(cudaFreeAsync(cols, s));
 }
 void maxpool_fwd(const void* x, void* y, uint8_t* am, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t total = (int64_t)g.N * g.P * g.Q * g.C;

@@ -7,10 +7,14 @@
 // reverse registration order, i.e. the order backward produces them), so no
 // gradient is ever copied.  When the last gradient of a bucket lands (the
 // engine's leaf-finalize hook), the compute stream records an event, the comm
-// stream waits on it and runs ncclAllReduce(sum) on the bucket — concurrently
-// with the remaining backward kernels.  be_sgd_step makes the compute stream
-// wait for every bucket and folds 1/world into the SGD kernel.  Replicas stay
-// bitwise identical because every rank applies the same reduced bytes.
+// stream waits on it and runs ncclAllReduce(avg) on the bucket — concurrently
+// with the remaining backward kernels.  The bucket therefore holds the MEAN
+// gradient (g = (1/R)·Σ_r g_r), so a second backward before
+// the step (gradient accumulation) adds its local gradient to an identical
+// mean on every rank and its re-reduction gives mean(g1) + mean(g2).  The end
+// of every backward makes the compute stream wait for every bucket, so
+// gradients read after be_backward are reduced.  Replicas stay bitwise
+// identical because every rank applies the same reduced bytes.
 //
 // NCCL is resolved with dlopen (the torch-bundled libnccl.so.2 that
 // torch.distributed already loaded), so the library has no link-time NCCL
@@ -94,14 +98,14 @@ void launch_bucket(Bucket& b) {
   Context& c = ctx();
   BE_CHECK_CUDA(cudaEventRecord(b.ready, c.stream));
   BE_CHECK_CUDA(cudaStreamWaitEvent(c.comm_stream, b.ready, 0));
-  BE_CHECK_NCCL(nccl().allReduce(b.storage->ptr, b.storage->ptr, b.numel, ncclFloat, ncclSum, d.comm, c.comm_stream));
+  BE_CHECK_NCCL(nccl().allReduce(b.storage->ptr, b.storage->ptr, b.numel, ncclFloat, ncclAvg, d.comm, c.comm_stream));
   if (opt_active()) {
     // overlapped SGD: the bucket's parameters are updated on the comm stream
-    // right behind their allreduce (1/world folded into the kernel)
+    // right behind their allreduce
     std::vector<Tensor*> ps;
     for (int i : b.params)
       if (d.ready[i]) ps.push_back(d.params[i]);
-    opt_launch_params(ps, c.comm_stream, 1.f / (float)d.world);
+    opt_launch_params(ps, c.comm_stream, 1.f);
   }
   BE_CHECK_CUDA(cudaEventRecord(b.done, c.comm_stream));
   b.launched = true;
@@ -137,7 +141,7 @@ void plan_buckets(const int64_t* numels, int n, size_t bucket_bytes, int* bucket
 }  // namespace
 
 bool ddp_active() { return ddp().active; }
-float ddp_grad_scale() { return 1.f / (float)ddp().world; }
+int ddp_world() { return ddp().world; }
 
 Tensor* ddp_grad_view(Tensor* leaf) {
   DDP& d = ddp();
@@ -225,18 +229,32 @@ be_status be_ddp_attach(const be_tensor* params, int n, size_t bucket_bytes) {
   if (bucket_bytes == 0) bucket_bytes = 25u << 20;
   Context& c = ctx();
   d.params.clear();
+  // validate everything first so a failed attach leaves no parameter marked
   for (int i = 0; i < n; ++i) {
     Tensor* p = check_handle(params[i]);
     BE_REQUIRE(p->dtype == BE_F32 && p->is_contiguous() && p->requires_grad, BE_E_ARG,
                "DDP params must be contiguous f32 leaves requiring grad");
     BE_REQUIRE(p->ddp_slot < 0, BE_E_ARG, "parameter listed twice");
+    for (int j = 0; j < i; ++j)
+      BE_REQUIRE(params[j] != params[i], BE_E_ARG, "parameter listed twice");
+  }
+  for (int i = 0; i < n; ++i) {
+    Tensor* p = check_handle(params[i]);
     p->retain();
     p->ddp_slot = i;
     d.params.push_back(p);
-    // replicas start identical: broadcast from rank 0
-    BE_CHECK_NCCL(nccl().broadcast(p->data(), p->data(), (size_t)p->numel(), ncclFloat, 0, d.comm, c.stream));
-    p->bump_version();
-    if (p->grad) { tensor_drop(p->grad); p->grad = nullptr; }
+  }
+  try {
+    for (Tensor* p : d.params) {
+      // replicas start identical: broadcast from rank 0
+      BE_CHECK_NCCL(nccl().broadcast(p->data(), p->data(), (size_t)p->numel(), ncclFloat, 0, d.comm, c.stream));
+      p->bump_version();
+      if (p->grad) { tensor_drop(p->grad); p->grad = nullptr; }
+    }
+  } catch (...) {
+    for (Tensor* p : d.params) { p->ddp_slot = -1; tensor_drop(p); }
+    d.params.clear();
+    throw;
   }
   d.bucket_of.assign(n, -1);
   d.offset_of.assign(n, 0);
@@ -288,6 +306,28 @@ be_status be_ddp_detach(void) {
   d.buckets.clear();
   d.params.clear();
   d.active = false;
+  BE_API_END
+}
+
+be_status be_ddp_sync_buffers(const be_tensor* bufs, int n) {
+  BE_API_BEGIN
+  DDP& d = ddp();
+  BE_REQUIRE(d.comm_ready, BE_E_NOT_INIT, "be_dist_init() was not called");
+  for (int i = 0; i < n; ++i) {
+    Tensor* t = check_handle(bufs[i]);
+    BE_REQUIRE(t->dtype == BE_F32 && t->is_contiguous(), BE_E_ARG, "ddp_sync_buffers: contiguous f32 buffers");
+    BE_CHECK_NCCL(nccl().broadcast(t->data(), t->data(), (size_t)t->numel(), ncclFloat, 0, d.comm, ctx().stream));
+    t->bump_version();
+  }
+  BE_API_END
+}
+
+be_status be_dist_world(int* rank, int* world) {
+  BE_API_BEGIN
+  DDP& d = ddp();
+  BE_REQUIRE(d.comm_ready, BE_E_NOT_INIT, "be_dist_init() was not called");
+  *rank = d.rank;
+  *world = d.world;
   BE_API_END
 }
 

@@ -140,7 +140,7 @@ static void vjp_linear(Node* n, GradSink& sink) {
   // wgrad GEMM applies the update in its epilogue (no dW tensor, no separate
   // SGD pass) — after dX, which still reads the pre-update weight
   k::SgdFuse fz;
-  bool fuse = sink.needs(1) && opd == BE_BF16 && k::gemm_tc_ok(gw) && sink.fuse && sink.fuse(1, &fz);
+  bool fuse = sink.needs(1) && opd == BE_BF16 && k::gemm_tc_ok(gw) && sink.fuse(1, &fz);
   if (fuse) {
     gw.upd = &fz;
     fuse = k::gemm_update_ok(gw);

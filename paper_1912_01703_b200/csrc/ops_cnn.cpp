@@ -399,9 +399,12 @@ static void vjp_embedding(Node* n, GradSink& sink) {
   // Tables looked up with the same ids (NeuMF: GMF and MLP tables of a side)
   // share one sort: a small cache keyed by the ids storage, its version and V
   // (several entries: backward visits the user and item tables interleaved).
+  // Entries are valid only within ONE backward pass (ctx().bw_epoch): every
+  // step sorts its ids afresh, so ids rewritten in place without a version
+  // bump (zero-copy external buffers) can never meet a stale sort.
   struct Entry {
     Storage* st = nullptr;
-    uint64_t version = 0, stamp = 0;
+    uint64_t version = 0, stamp = 0, epoch = 0;
     int64_t B = -1, V = -1, off = 0;
     TRef sorted;
   };
@@ -410,7 +413,7 @@ static void vjp_embedding(Node* n, GradSink& sink) {
   Entry* e = nullptr;
   for (Entry& c : cache)
     if (c.st == ids->storage && c.version == ids->version() && c.B == B && c.V == V && c.off == ids->offset &&
-        c.sorted)
+        c.epoch == ctx().bw_epoch && c.sorted)
       e = &c;
   if (!e) {
     e = &cache[0];
@@ -426,6 +429,7 @@ static void vjp_embedding(Node* n, GradSink& sink) {
     e->B = B;
     e->V = V;
     e->off = ids->offset;
+    e->epoch = ctx().bw_epoch;
     e->sorted = scratch;
   }
   e->stamp = ++clock;

@@ -175,9 +175,22 @@ be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum, 
     ts.push_back(p);
   }
   if (ddp_active()) ddp_wait_all();
-  k::sgd_multi(es.data(), (int)es.size(), lr, momentum, weight_decay, ddp_active() ? ddp_grad_scale() : 1.f,
-               ctx().stream);
+  // DDP buckets already hold the mean gradient (ncclAvg): scale 1
+  k::sgd_multi(es.data(), (int)es.size(), lr, momentum, weight_decay, 1.f, ctx().stream);
   for (size_t i = 0; i < ts.size(); ++i) bump_after_update(ts[i], es[i]);
+  BE_API_END
+}
+
+be_status be_sgd_momentum(be_tensor param, be_tensor* out) {
+  BE_API_BEGIN
+  Tensor* p = check_handle(param);
+  BE_REQUIRE(out != nullptr, BE_E_ARG, "sgd_momentum: out is NULL");
+  *out = nullptr;
+  if (!p->mom) return BE_OK;
+  TRef v = new_tensor(p->shape, p->rank, BE_F32);
+  BE_CHECK_CUDA(cudaMemcpyAsync(v->data(), p->mom, sizeof(float) * p->numel(), cudaMemcpyDeviceToDevice,
+                                ctx().stream));
+  *out = reinterpret_cast<be_tensor>(v.release());
   BE_API_END
 }
 
@@ -197,6 +210,8 @@ be_status be_sgd_overlap(const be_tensor* params, int n, float lr, float momentu
     BE_REQUIRE(p->dtype == BE_F32 && p->is_contiguous() && p->requires_grad && p->is_leaf(), BE_E_ARG,
                "sgd_overlap: params must be contiguous f32 leaves requiring grad");
     BE_REQUIRE(p->opt_slot < 0, BE_E_ARG, "sgd_overlap: parameter listed twice");
+    BE_REQUIRE(!ddp_active() || p->ddp_slot >= 0, BE_E_ARG,
+               "sgd_overlap: with DDP attached every registered parameter must be DDP-attached");
     p->retain();
     p->opt_slot = i;
     o.params.push_back(p);

@@ -129,6 +129,11 @@ struct Tensor {
   Tensor* bn_stats = nullptr;
   int bn_stats_parts = 0;
   uint64_t bn_stats_version = ~0ull;
+  // engine scratch for leaves (per backward pass): edges still to run into
+  // this leaf (overlapped SGD / DDP readiness), and whether some already ran
+  uint64_t bw_epoch = 0;
+  int bw_uses = 0;
+  bool bw_partial = false;
 
   int64_t numel() const {
     int64_t n = 1;
@@ -206,13 +211,21 @@ struct Node {
   int64_t iattr[8]{};
   bool consumed = false;
   bool upstream_is_ones = false;    // set by the engine for the root
+  // engine scratch of the backward pass `bw_epoch` (reset when first reached)
+  uint64_t bw_epoch = 0;
+  int bw_deps = 0;
+  std::vector<Tensor*> pend;        // pending output gradients (owned refs)
 };
 
 // The engine hands each VJP a sink: grads for input i are written into
 // sink.dest(i) (allocated on demand with beta=0, or the existing buffer with
 // beta=1 to accumulate); kernels that cannot accumulate call dest_fresh().
+// All engine callbacks are plain member functions over the engine state of
+// the running backward (no per-node closures: host enqueue cost).
+struct Engine;
 struct GradSink {
   Node* node = nullptr;
+  Engine* eng = nullptr;
   std::vector<Tensor*> upstream;    // per output (borrowed)
   // returns nullptr when input i needs no grad
   Tensor* dest(int i, float* beta);
@@ -224,20 +237,20 @@ struct GradSink {
   bool needs(int i) const;
   bool upstream_ones() const { return node->upstream_is_ones; }
   bool retain = false;
-  std::function<bool(int, Tensor*)> adopt;      // engine callback: try to adopt t as input i's grad
   // Fused SGD (overlapped optimizer): true when input i is a parameter
   // registered with be_sgd_overlap whose gradient is complete with this one
   // contribution; *f then describes the update the VJP's weight-gradient GEMM
   // applies in its epilogue (no gradient tensor is stored), after which the
   // VJP calls fused(i).  Every reader of the parameter in this VJP must be
   // enqueued before that GEMM.
-  std::function<bool(int, k::SgdFuse*)> fuse;
-  std::function<void(int)> fused;
+  bool fuse(int i, k::SgdFuse* f);
+  void fused(int i);
   // engine internals
   struct Slot { Tensor* target = nullptr; Tensor* tmp = nullptr; bool acc = false; bool used = false; };
   std::vector<Slot> slots;
-  std::function<Tensor*(int, bool*)> acquire;   // engine callback: (input idx, &existing)
-  std::function<void(int, Tensor*)> finalize;   // engine callback after commit
+  Tensor* acquire(int i, bool* existing);
+  bool adopt(int i, Tensor* t);
+  void finalize(int i, Tensor* t);
 };
 
 Tensor* unpack(Node* n, int i, TRef& holder);   // version-checked view of saved[i]
@@ -258,6 +271,7 @@ struct Context {
   CachingAllocator alloc;
   std::atomic<uint64_t> seq{0};
   std::atomic<uint64_t> launches{0};
+  uint64_t bw_epoch = 0;               // id of the current / last backward pass
 };
 Context& ctx();
 bool grad_enabled();
@@ -278,7 +292,7 @@ void ddp_on_leaf_grad_ready(Tensor* leaf);
 bool ddp_active();
 Tensor* ddp_grad_view(Tensor* leaf);     // bucket view for a param grad or nullptr
 void ddp_wait_all();                     // compute stream waits on all bucket allreduces
-float ddp_grad_scale();
+int ddp_world();
 void ddp_begin_backward();
 // DDP: params of a reduced bucket (for the overlapped optimizer, launched on
 // the comm stream right after the bucket's allreduce)

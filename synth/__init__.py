@@ -19,7 +19,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "generator", "normal", "uniform", "labels", "make_params", "ncf_batch",
+    "generator", "normal", "uniform", "labels", "make_params", "ncf_batch", "bf16_values",
 ]
 
 
@@ -68,3 +68,15 @@ def ncf_batch(batch: int, n_users: int, n_items: int, seed: int):
     items = g.integers(0, n_items, size=(batch,), dtype=np.int64).astype(np.int32)
     y = (g.random(size=(batch,)) < 0.2).astype(np.int32)
     return users, items, y
+
+
+def bf16_values(a) -> np.ndarray:
+    """The bf16 configs' inputs are bfloat16 numbers (BASELINE configs C2-C5:
+    "bf16"): round a draw to the nearest bfloat16 (RN-even on the float32
+    bits; NaN/inf pass through) and return it as float32.  Data generation
+    only — both sides receive these identical values."""
+    x = np.ascontiguousarray(np.asarray(a, dtype=np.float64).astype(np.float32))
+    bits = x.view(np.uint32).astype(np.uint64)
+    rounded = ((bits + 0x7FFF + ((bits >> 16) & 1)) >> 16) << 16
+    out = rounded.astype(np.uint32).view(np.float32)
+    return np.where(np.isfinite(x), out, x).astype(np.float32)

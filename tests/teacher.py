@@ -1,0 +1,469 @@
+"""Teacher-forced, full-depth per-op parity (test infrastructure).
+
+SURVEY §8(c) reading 15: a deep bf16 network's end-to-end gradient error has
+no closed form ("parity unpinned"), so every op of the FULL architecture is
+gated instead, each fed the device's own inputs:
+
+  1. trace: run the network's eager forward on the device with the api
+     functions wrapped; every op call records its attributes and a host copy
+     of every input and output tensor (the device's own activations);
+  2. replay, last op first: re-run the op on the device on fresh leaves
+     holding exactly the traced input values, backpropagate the upstream
+     gradient the device produced for that op's output, and compute the
+     SAME op with the float64 oracle (oracle/ops.py) on the same values;
+     compare forward output, every input gradient, and (BN) running
+     statistics, element-wise (∞-norm relative, oracle/compare.py) at the
+     north_star tolerance (2e-2 bf16, 1e-4 fp32);
+  3. the device's input gradients become the upstream of the producing ops
+     (fan-out contributions summed).
+
+Integer decisions are compared bit-exactly on identical inputs (max-pool
+winners, softmax argmax).  ReLU masks fused into an op are taken from the
+device's own output (SURVEY §8(c) reading 16: a decision taken from floating
+point is taken from the same value on both sides).  Layout: the device is
+NHWC / KRSC; the oracle is NCHW / KCRS; Linear weights are [in, out] on both.
+"""
+from __future__ import annotations
+
+import inspect
+
+import numpy as np
+
+import synth
+from oracle import ops as oops
+from oracle.autograd import Var, backward
+from oracle.compare import rel_err
+
+F64 = np.float64
+
+
+def nhwc_to_nchw(a):
+    return np.ascontiguousarray(np.asarray(a).transpose(0, 3, 1, 2))
+
+
+def nchw_to_nhwc(a):
+    return np.ascontiguousarray(np.asarray(a).transpose(0, 2, 3, 1))
+
+
+class _Ref:
+    __slots__ = ("key",)
+
+    def __init__(self, key):
+        self.key = key
+
+    def __repr__(self):
+        return f"<{self.key}>"
+
+
+class OpTrace:
+    """Wraps the api ops a model calls (be.nn uses the module global `T`)."""
+
+    OPS = ("conv2d", "batchnorm2d", "maxpool2d", "avgpool_global", "reshape", "linear", "softmax_xent",
+           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_dw")
+
+    def __init__(self, api, model):
+        self.api = api
+        self.model = model
+        self.recs = []
+        self.vals = {}       # key -> host value (float32 / int32), device layout
+        self.dtypes = {}     # key -> dtype code
+        self.keep = []       # keep traced tensors alive (stable ids)
+        self.ids = {}
+        self.producer = {}   # key -> record index
+        for n, p in model.params.items():
+            self.ids[id(p)] = ("param", n)
+        for n, b in model.buffers.items():
+            self.ids[id(b)] = ("buf", n)
+
+    # ------------------------------------------------------------ tracing
+    def _key(self, t):
+        k = self.ids.get(id(t))
+        if k is None:
+            k = ("act", len(self.ids))
+            self.ids[id(t)] = k
+            self.keep.append(t)
+        if k not in self.vals:
+            self.vals[k] = t.numpy()
+            self.dtypes[k] = t.dtype
+        return k
+
+    def _wrap(self, name):
+        fn = getattr(self.api, name)
+        sig = inspect.signature(fn)
+
+        def traced(*args, **kw):
+            b = sig.bind(*args, **kw)
+            b.apply_defaults()
+            a = dict(b.arguments)
+            rec_args = {}
+            for k, v in a.items():
+                if isinstance(v, self.api.Tensor):
+                    rec_args[k] = _Ref(self._key(v))
+                elif isinstance(v, (list, tuple)) and v and isinstance(v[0], self.api.Tensor):
+                    rec_args[k] = [_Ref(self._key(t)) for t in v]
+                else:
+                    rec_args[k] = v
+            extra = None
+            if name in ("maxpool2d", "softmax_xent"):
+                a["with_argmax"] = True
+                out, am = fn(**a)
+                extra = am.numpy()
+            else:
+                out = fn(**a)
+            ok = ("act", len(self.ids))
+            self.ids[id(out)] = ok
+            self.keep.append(out)
+            self.vals[ok] = out.numpy()
+            self.dtypes[ok] = out.dtype
+            self.producer[ok] = len(self.recs)
+            self.recs.append(dict(op=name, args=rec_args, out=ok, extra=extra))
+            return out
+        return traced
+
+    def install(self, nn_module):
+        class Proxy:
+            pass
+        proxy = Proxy()
+        for n in dir(self.api):
+            if not n.startswith("__"):
+                setattr(proxy, n, getattr(self.api, n))
+        for n in self.OPS:
+            if hasattr(self.api, n):
+                setattr(proxy, n, self._wrap(n))
+        self._saved = nn_module.T
+        nn_module.T = proxy
+        return self
+
+    def uninstall(self, nn_module):
+        nn_module.T = self._saved
+
+
+# ------------------------------------------------------------------ replay
+def _leaf(be, val, dt, requires_grad):
+    """Fresh device leaf holding exactly `val`; bf16 values go through a
+    differentiable cast of an f32 leaf (bf16→f32 gradient widening is exact)."""
+    if dt == be._lib.BE_BF16:
+        base = be.tensor(val.astype(np.float32), requires_grad=requires_grad)
+        return base, be.cast(base, "bf16")
+    if dt in (be._lib.BE_I32, be._lib.BE_I64, be._lib.BE_U8):
+        t = be.tensor(val)
+        return t, t
+    t = be.tensor(val.astype(np.float32), requires_grad=requires_grad)
+    return t, t
+
+
+def _as_dtype_values(be, g, dt):
+    g = np.asarray(g, np.float32)
+    return synth.bf16_values(g) if dt == be._lib.BE_BF16 else g
+
+
+class Replay:
+    def __init__(self, be, trace: OpTrace, tol: float, param_logical=None):
+        self.be = be
+        self.tr = trace
+        self.tol = tol
+        self.errs = []          # (record idx, op, what, err)
+        self.grads = {}         # key -> float64 accumulated upstream (device layout)
+        self.param_grads = {}   # param name -> device per-op grads summed (device layout)
+
+    def _upstream(self, key):
+        return self.grads.get(key)
+
+    def _push(self, key, g):
+        if key[0] == "act" and key not in self.tr.producer:
+            return  # a network input (no producer): nothing upstream
+        if key[0] == "param":
+            self.param_grads[key[1]] = self.param_grads.get(key[1], 0) + np.asarray(g, F64)
+            return
+        if key[0] == "buf":
+            return
+        self.grads[key] = self.grads.get(key, 0) + np.asarray(g, F64)
+
+    def record(self, i, op, what, dev, orc, exact=False):
+        if exact:
+            e = 0.0 if np.array_equal(np.asarray(dev), np.asarray(orc)) else float("inf")
+        else:
+            e = rel_err(dev, orc)
+        self.errs.append((i, op, what, e))
+
+    def run(self):
+        be = self.be
+        for i in reversed(range(len(self.tr.recs))):
+            rec = self.tr.recs[i]
+            getattr(self, "_op_" + rec["op"])(i, rec)
+        return self
+
+    # ------------------------------------------------------------ helpers
+    def _val(self, r):
+        return self.tr.vals[r.key]
+
+    def _dt(self, r):
+        return self.tr.dtypes[r.key]
+
+    def _req(self, r):
+        return r.key[0] == "param" or (r.key[0] == "act" and r.key in self.tr.producer)
+
+    def _dev_inputs(self, rec, names):
+        """Fresh leaves for the named tensor args: {name: (leaf, operand)}."""
+        out = {}
+        for n in names:
+            r = rec["args"].get(n)
+            if r is None:
+                out[n] = (None, None)
+            elif isinstance(r, list):
+                out[n] = [_leaf(self.be, self._val(x), self._dt(x), self._req(x)) for x in r]
+            else:
+                out[n] = _leaf(self.be, self._val(r), self._dt(r), self._req(r))
+        return out
+
+    def _g_out(self, rec):
+        g = self.grads.pop(rec["out"], None)
+        return g
+
+    def _dev_backward(self, out, g, rec):
+        be = self.be
+        if g is None:
+            return False
+        dt = self.tr.dtypes[rec["out"]]
+        if np.ndim(g) == 0 and out.numel() == 1 and dt == be._lib.BE_F32 and float(g) == 1.0:
+            out.backward()
+        else:
+            gv = _as_dtype_values(be, np.asarray(g).reshape(out.shape), dt)
+            out.backward(be.tensor(gv, dtype="bf16" if dt == be._lib.BE_BF16 else None))
+        return True
+
+    def _finish(self, i, rec, leaves, orc_grads, names, to_dev=None):
+        """Compare device leaf grads with oracle grads (both device layout) and push upstream."""
+        for n in names:
+            r = rec["args"].get(n)
+            if r is None or not self._req(r):
+                continue
+            leaf = leaves[n][0]
+            gd = leaf.grad.numpy() if leaf.grad is not None else np.zeros_like(self._val(r))
+            go = orc_grads[n]
+            self.record(i, rec["op"], "d" + n + (":" + r.key[1] if r.key[0] == "param" else ""), gd, go)
+            self._push(r.key, gd)
+
+    # ------------------------------------------------------------ ops
+    def _op_conv2d(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x", "w", "b"])
+        y = be.conv2d(L["x"][1], L["w"][1], L["b"][1], a["stride"], a["pad"], act=a["act"], out_f32=a["out_f32"])
+        x = nhwc_to_nchw(self._val(a["x"])).astype(F64)
+        w = nhwc_to_nchw(self._val(a["w"])).astype(F64)      # KRSC -> KCRS
+        xo, wo = Var(x, True), Var(w, True)
+        bo = Var(self._val(a["b"]).astype(F64), True) if a["b"] is not None else None
+        zo = oops.conv2d(xo, wo, bo, a["stride"], a["pad"])
+        ydev = self.tr.vals[rec["out"]]
+        mask = (nhwc_to_nchw(ydev) > 0) if a["act"] else None
+        fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
+        self.record(i, "conv2d", "y", nhwc_to_nchw(ydev), fwd)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        gn = nhwc_to_nchw(np.asarray(g).reshape(ydev.shape))
+        if mask is not None:
+            gn = gn * mask
+        backward(zo, gn)
+        og = {"x": nchw_to_nhwc(xo.grad), "w": nchw_to_nhwc(wo.grad)}
+        if bo is not None:
+            og["b"] = bo.grad
+        self._finish(i, rec, L, og, ["x", "w", "b"])
+
+    def _op_batchnorm2d(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x", "gamma", "beta", "residual"])
+        rm0 = self._val(a["running_mean"]) if a["running_mean"] is not None else None
+        rv0 = self._val(a["running_var"]) if a["running_var"] is not None else None
+        rmd = be.tensor(rm0) if rm0 is not None else None
+        rvd = be.tensor(rv0) if rv0 is not None else None
+        y = be.batchnorm2d(L["x"][1], L["gamma"][1], L["beta"][1], rmd, rvd, eps=a["eps"], momentum=a["momentum"],
+                           act=a["act"], residual=L["residual"][1])
+        xo = Var(nhwc_to_nchw(self._val(a["x"])).astype(F64), True)
+        go = Var(self._val(a["gamma"]).astype(F64), True)
+        bo = Var(self._val(a["beta"]).astype(F64), True)
+        zo, (rm, rv) = oops.batchnorm2d(xo, go, bo, eps=a["eps"], momentum=a["momentum"],
+                                        running_mean=None if rm0 is None else rm0.astype(F64),
+                                        running_var=None if rv0 is None else rv0.astype(F64))
+        ro = None
+        if a["residual"] is not None:
+            ro = Var(nhwc_to_nchw(self._val(a["residual"])).astype(F64), True)
+            zo = oops.add(zo, ro)
+        ydev = self.tr.vals[rec["out"]]
+        fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
+        self.record(i, "batchnorm2d", "y", nhwc_to_nchw(ydev), fwd)
+        if rmd is not None:
+            self.record(i, "batchnorm2d", "running_mean", rmd.numpy(), rm)
+            self.record(i, "batchnorm2d", "running_var", rvd.numpy(), rv)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        gn = nhwc_to_nchw(np.asarray(g).reshape(ydev.shape))
+        if a["act"]:
+            gn = gn * (nhwc_to_nchw(ydev) > 0)
+        backward(zo, gn)
+        og = {"x": nchw_to_nhwc(xo.grad), "gamma": go.grad, "beta": bo.grad}
+        if ro is not None:
+            og["residual"] = nchw_to_nhwc(ro.grad)
+        self._finish(i, rec, L, og, ["x", "gamma", "beta", "residual"])
+
+    def _op_maxpool2d(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x"])
+        y = be.maxpool2d(L["x"][1], a["k"], a["stride"], a["pad"])
+        xv = nhwc_to_nchw(self._val(a["x"])).astype(F64)
+        xo = Var(xv, True)
+        yo, am = oops.maxpool2d(xo, a["k"], a["stride"], a["pad"])
+        ydev = self.tr.vals[rec["out"]]
+        self.record(i, "maxpool2d", "y", nhwc_to_nchw(ydev), yo.value)
+        # device winner (window index r·k+u, NHWC) → plane index h·W+w: bit-exact
+        win = nhwc_to_nchw(rec["extra"]).astype(np.int64)
+        P, Q = yo.value.shape[2], yo.value.shape[3]
+        hh = np.arange(P)[:, None] * a["stride"] - a["pad"] + win // a["k"]
+        ww = np.arange(Q)[None, :] * a["stride"] - a["pad"] + win % a["k"]
+        self.record(i, "maxpool2d", "argmax", hh * xv.shape[3] + ww, am, exact=True)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, nhwc_to_nchw(np.asarray(g).reshape(ydev.shape)))
+        self._finish(i, rec, L, {"x": nchw_to_nhwc(xo.grad)}, ["x"])
+
+    def _op_avgpool_global(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x"])
+        y = be.avgpool_global(L["x"][1])
+        xo = Var(nhwc_to_nchw(self._val(a["x"])).astype(F64), True)
+        yo = oops.avgpool_global(xo)
+        self.record(i, "avgpool", "y", self.tr.vals[rec["out"]], yo.value)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, np.asarray(g, F64))
+        self._finish(i, rec, L, {"x": nchw_to_nhwc(xo.grad)}, ["x"])
+
+    def _op_reshape(self, i, rec):
+        a = rec["args"]
+        # a view: values must be identical, the gradient is reshaped back
+        self.record(i, "reshape", "y", self.tr.vals[rec["out"]],
+                    self._val(a["x"]).reshape(self.tr.vals[rec["out"]].shape), exact=True)
+        g = self._g_out(rec)
+        if g is not None and self._req(a["x"]):
+            self._push(a["x"].key, np.asarray(g).reshape(self._val(a["x"]).shape))
+
+    def _op_linear(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x", "w", "b"])
+        y = be.linear(L["x"][1], L["w"][1], L["b"][1], act=a["act"], out_f32=a["out_f32"])
+        xo = Var(self._val(a["x"]).astype(F64), True)
+        wo = Var(self._val(a["w"]).astype(F64), True)
+        bo = Var(self._val(a["b"]).astype(F64), True) if a["b"] is not None else None
+        zo = oops.linear(xo, wo, bo)
+        ydev = self.tr.vals[rec["out"]]
+        fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
+        self.record(i, "linear", "y", ydev, fwd)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        gn = np.asarray(g, F64).reshape(ydev.shape)
+        if a["act"]:
+            gn = gn * (ydev > 0)
+        backward(zo, gn)
+        og = {"x": xo.grad, "w": wo.grad}
+        if bo is not None:
+            og["b"] = bo.grad
+        self._finish(i, rec, L, og, ["x", "w", "b"])
+
+    def _op_softmax_xent(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["z"])
+        lab = self._val(a["labels"])
+        loss = be.softmax_xent(L["z"][1], be.tensor(lab))
+        zo = Var(self._val(a["z"]).astype(F64), True)
+        lo = oops.softmax_cross_entropy(zo, lab.astype(np.int64))
+        self.record(i, "softmax_xent", "loss", np.array(self.tr.vals[rec["out"]]), lo.value)
+        self.record(i, "softmax_xent", "argmax", rec["extra"].astype(np.int64),
+                    oops.argmax_rows(self._val(a["z"]).astype(F64)), exact=True)
+        self.grads[rec["out"]] = np.float64(1.0)
+        self._dev_backward(loss, self._g_out(rec), rec)
+        backward(lo)
+        self._finish(i, rec, L, {"z": zo.grad}, ["z"])
+
+    def _op_bce_logits(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["z"])
+        lab = self._val(a["labels"])
+        loss = be.bce_logits(L["z"][1], be.tensor(lab))
+        zv = self._val(a["z"]).astype(F64)
+        zo = Var(zv, True)
+        lo = oops.bce_as_two_class_ce(zo, lab.astype(np.int64))
+        self.record(i, "bce_logits", "loss", np.array(self.tr.vals[rec["out"]]), lo.value)
+        self.grads[rec["out"]] = np.float64(1.0)
+        self._dev_backward(loss, self._g_out(rec), rec)
+        backward(lo)
+        self._finish(i, rec, L, {"z": zo.grad}, ["z"])
+
+    def _op_embedding(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["table"])
+        ids = self._val(a["ids"])
+        y = be.embedding(L["table"][1], be.tensor(ids))
+        to = Var(self._val(a["table"]).astype(F64), True)
+        yo = oops.embedding(to, ids.astype(np.int64))
+        self.record(i, "embedding", "rows", self.tr.vals[rec["out"]], yo.value, exact=True)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, np.asarray(g, F64))
+        self._finish(i, rec, L, {"table": to.grad}, ["table"])
+
+    def _op_mul(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["a", "b"])
+        y = be.mul(L["a"][1], L["b"][1])
+        ao, bo = Var(self._val(a["a"]).astype(F64), True), Var(self._val(a["b"]).astype(F64), True)
+        yo = oops.mul(ao, bo)
+        self.record(i, "mul", "y", self.tr.vals[rec["out"]], yo.value)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, np.asarray(g, F64))
+        self._finish(i, rec, L, {"a": ao.grad, "b": bo.grad}, ["a", "b"])
+
+    def _op_concat(self, i, rec):
+        be, a = self.be, rec["args"]
+        refs = a["xs"]
+        leaves = [_leaf(be, self._val(r), self._dt(r), self._req(r)) for r in refs]
+        y = be.concat([l[1] for l in leaves])
+        vo = [Var(self._val(r).astype(F64), True) for r in refs]
+        yo = oops.concat(vo, 1)
+        self.record(i, "concat", "y", self.tr.vals[rec["out"]], yo.value, exact=True)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, np.asarray(g, F64))
+        for j, (r, l, v) in enumerate(zip(refs, leaves, vo)):
+            if not self._req(r):
+                continue
+            gd = l[0].grad.numpy()
+            self.record(i, "concat", f"dx{j}", gd, v.grad)
+            self._push(r.key, gd)
+
+    # ------------------------------------------------------------ report
+    def worst(self, n=8):
+        return sorted(self.errs, key=lambda e: -e[3])[:n]
+
+    def failures(self):
+        return [e for e in self.errs if not e[3] <= self.tol]
+
+
+def teacher_forced(be, model, batch, tol):
+    """Trace the model's forward on the device, then replay every op (see the
+    module docstring).  Returns the Replay (errs, worst(), failures())."""
+    tr = OpTrace(be.api, model).install(be.nn)
+    try:
+        loss = model.loss(*batch)
+    finally:
+        tr.uninstall(be.nn)
+    del loss
+    rp = Replay(be, tr, tol).run()
+    return rp

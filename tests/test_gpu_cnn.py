@@ -32,6 +32,51 @@ def test_im2col_offsets_bit_exact(geom):
     assert np.array_equal(dev, ref)
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("geom", [
+    (2, 64, 9, 9, 64, 3, 1, 1),      # bf16: shared-patch stride-1 kernel (C = K = 64)
+    (2, 64, 10, 10, 128, 3, 2, 1),   # TMA-im2col implicit GEMM (C % 64 == 0), stride 2
+    (1, 128, 7, 7, 128, 3, 1, 1),    # TMA-im2col, C = K = 128
+    (2, 8, 40, 40, 64, 7, 2, 3),     # stem (C = 8, K = 64, stride 2): phase-split patch
+    (1, 8, 35, 35, 64, 11, 4, 2),    # AlexNet-conv1-like (small-C gather)
+    (1, 16, 9, 11, 48, 3, 1, 1),     # small-C gather, stride 1
+    (2, 256, 6, 6, 64, 1, 2, 0)])    # 1×1 stride 2
+def test_conv_kernels_gather_offsets_bit_exact(geom, dtype):
+    """Index parity of the conv kernels themselves (not a side kernel): with
+    one-hot weights (output channel k selects column j0 + k of the im2col
+    matrix) and an input holding base-b digits of (NHWC offset + 1), every
+    output element is exactly one gathered input value; the digits
+    reassemble the offset table the kernel used, which must equal the
+    oracle's im2col_table bit-exactly (−1 in the padding).  b = 128 in bf16
+    (integers ≤ 256 are exact), 2048 with 3xTF32."""
+    be = be_init()
+    be.set_compute_dtype(dtype)
+    N, C, H, W, K, R, st, pd = geom
+    P, Q = (H + 2 * pd - R) // st + 1, (W + 2 * pd - R) // st + 1
+    RSC = R * R * C
+    base = 128 if dtype == "bf16" else 2048
+    off1 = np.arange(1, N * H * W * C + 1, dtype=np.int64).reshape(N, H, W, C)  # NHWC offset + 1
+    nd = 1
+    while base ** nd <= off1.max():
+        nd += 1
+    digits = [((off1 // base ** d) % base).astype(np.float32) for d in range(nd)]
+    xs = [be.tensor(dg, dtype=dtype) for dg in digits]
+    got = np.zeros((N * P * Q, RSC), np.int64)
+    for j0 in range(0, RSC, K):
+        wk = np.zeros((K, RSC), np.float32)
+        cols = np.arange(j0, min(j0 + K, RSC))
+        wk[cols - j0, cols] = 1.0
+        wd = be.tensor(wk.reshape(K, R, R, C))          # KRSC
+        acc = np.zeros((N * P * Q, K), np.int64)
+        for d, x in enumerate(xs):
+            y = be.conv2d(x, wd, None, st, pd).numpy().reshape(N * P * Q, K)
+            assert np.array_equal(y, np.round(y))
+            acc += y.astype(np.int64) * base ** d
+        got[:, cols] = acc[:, :len(cols)]
+    ref = oops.im2col_table(N, C, H, W, R, R, st, pd)
+    assert np.array_equal(got - 1, ref)
+
+
 @pytest.mark.parametrize("cfg", [(2, 8, 9, 9, 16, 3, 1, 1), (2, 8, 10, 10, 12, 3, 2, 1), (3, 16, 7, 7, 32, 1, 1, 0),
                                  (2, 16, 8, 8, 24, 1, 2, 0), (2, 8, 23, 23, 16, 11, 4, 2), (1, 8, 12, 12, 8, 5, 1, 2)])
 @pytest.mark.parametrize("act", [0, 1])

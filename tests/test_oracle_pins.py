@@ -89,22 +89,68 @@ def test_sgd_momentum_closed_form():
     assert abs(float(p2["p"]) - (0.95 - 0.1 * (0.9 * 0.5 + 0.5))) < 1e-15
 
 
-def test_bf16_round_known_values():
-    """RN-even to bfloat16 (8-bit significand): exact values, halfway ties to
-    even, carries into the exponent, specials."""
-    r = ops.bf16_round
+def test_bf16_values_known_values():
+    """synth.bf16_values (the bf16 configs' input values; data generation, not
+    oracle arithmetic): RN-even to bfloat16 (8-bit significand): exact values,
+    halfway ties to even, carries into the exponent, specials."""
+    r = lambda v: float(synth.bf16_values(np.array([v]))[0])
     assert r(1.0) == 1.0
     assert r(1 + 2 ** -8) == 1.0                      # tie → even (mantissa ...0)
     assert r(1 + 3 * 2 ** -8) == 1 + 2 ** -6          # tie → even (round up)
     assert r(1 + 2 ** -8 + 2 ** -12) == 1 + 2 ** -7   # above halfway → up
     assert r(2 - 2 ** -9) == 2.0                       # carry into exponent
     assert r(-3.0) == -3.0 and np.isnan(r(np.nan)) and r(np.inf) == np.inf
-    # equivalence with the float32 rounding of a 7-bit-truncated neighbourhood
     x = np.random.default_rng(0).standard_normal(1000)
-    y = r(x)
+    y = synth.bf16_values(x).astype(np.float64)
     assert np.all(np.abs(y - x) <= np.abs(x) * 2 ** -8 * 1.0000001)
     m = np.frexp(y)[0] * 2 ** 8
     assert np.all(m == np.round(m))  # at most 8 significant bits
+
+
+def test_rel_err_hand_values():
+    """The parity comparator: ∞-norm relative error
+    max|x−o| / max|o|, hand-computed cases; a uniformly 0.8×-scaled tensor
+    reads 0.2 and fails both gates."""
+    from oracle.compare import rel_err, TOL
+    assert rel_err([1.0, 2.0], [1.0, 2.0]) == 0.0
+    assert rel_err([1.5, 2.0], [1.0, 2.0]) == 0.25            # 0.5 / 2
+    assert rel_err([-3.0, 1.0], [-4.0, 1.0]) == 0.25          # 1 / 4
+    assert rel_err([[0.0, 0.0]], [[0.0, 0.0]]) == 0.0         # both exactly zero
+    assert rel_err([1e-3, 0.0], [0.0, 0.0]) == float("inf")   # reference zero, candidate not
+    assert rel_err(np.zeros((0, 3)), np.zeros((0, 3))) == 0.0
+    o = np.random.default_rng(1).standard_normal(100)
+    assert abs(rel_err(0.8 * o, o) - 0.2) < 1e-15
+    assert rel_err(0.8 * o, o) > TOL["bf16"] > TOL["f32"]
+    with pytest.raises(AssertionError):
+        rel_err(np.zeros(3), np.zeros(4))
+
+
+def test_argmax_rows_first_max():
+    """argmax for accuracy = first maximum per row (SURVEY §8(c)-9 / reading 7)."""
+    z = np.array([[1.0, 3.0, 3.0], [2.0, 2.0, 1.0], [-1.0, -5.0, -1.0], [0.0, 0.0, 7.0]])
+    assert ops.argmax_rows(z).tolist() == [1, 0, 0, 2]
+    assert ops.argmax_rows(z).dtype == np.int64
+
+
+def test_batchnorm_running_stats_hand_values():
+    """Running statistics (DESIGN R6): momentum 0.1, biased
+    variance for normalisation, UNBIASED variance in the running estimate.
+    Channel 0 holds 1, 2, 3, 4 over (n, h, w): mean 2.5, biased var 1.25,
+    unbiased var 5/3; channel 1 is constant 7 (variance 0)."""
+    x = np.zeros((2, 2, 1, 2))
+    x[:, 0, 0, :] = [[1.0, 2.0], [3.0, 4.0]]
+    x[:, 1] = 7.0
+    y, (rm, rv) = ops.batchnorm2d(V(x), V(np.ones(2)), V(np.zeros(2)))
+    assert np.allclose(rm, [0.25, 0.7], atol=1e-15)
+    assert np.allclose(rv, [0.9 + 0.1 * 5 / 3, 0.9], atol=1e-15)
+    # normalised with the biased variance: x̂ = (x − 2.5)/√(1.25 + 1e-5)
+    assert np.allclose(y.value[:, 0, 0, :].ravel(), (np.array([1, 2, 3, 4]) - 2.5) / math.sqrt(1.25 + 1e-5),
+                       rtol=1e-14)
+    assert np.all(y.value[:, 1] == 0.0)
+    # second update from given running stats
+    _, (rm2, rv2) = ops.batchnorm2d(V(x), V(np.ones(2)), V(np.zeros(2)), running_mean=rm, running_var=rv)
+    assert np.allclose(rm2, [0.9 * 0.25 + 0.25, 0.9 * 0.7 + 0.7], atol=1e-15)
+    assert np.allclose(rv2, [0.9 * (0.9 + 0.1 * 5 / 3) + 0.1 * 5 / 3, 0.81], atol=1e-15)
 
 
 # ------------------------------------------------------------ closed forms
