@@ -42,3 +42,32 @@ def compare_step(oracle_out, loss, grads, new, tol, skip_zero_grad_names=()):
     bad = {k: v for k, v in errs.items() if not v <= tol}
     assert not bad, f"tolerance {tol} exceeded: {bad}"
     return errs
+
+
+TOL = {"bf16": 2e-2, "f32": 1e-4}
+
+
+def e2e_gate(be, onet, pnet, P, obatch, dbatch, dtype, verbose=True, name=""):
+    """One SGD step on both sides vs the plain float64 oracle: every tensor's
+    ∞-norm error reported beside the oracle's own conditioning floor κ
+    (tests/conditioning.py); gated at the north_star tolerance on the loss and
+    on every gradient with κ ≤ tol/2 (a 0.8×-scaled gradient fails)."""
+    from oracle.step import train_step
+    from conditioning import UNIT_ROUNDOFF, sensitivity
+    tol = TOL[dtype]
+    ref = train_step(onet, P, obatch, lr=0.01)
+    loss, grads, new = run_product_step(be, pnet, P, dbatch)
+    errs = {"loss": rel(np.array(loss), np.array(ref["loss"]))}
+    for k in grads:
+        errs["grad:" + k] = rel(grads[k], ref["grads"][k])
+    kappa = sensitivity(onet, P, obatch, UNIT_ROUNDOFF[dtype], ref=ref)
+    gated = [k for k in errs if kappa[k] <= tol / 2]
+    if verbose:
+        print(f"{name} {dtype} e2e: loss err {errs['loss']:.2e}; {sum(errs[k] <= tol for k in errs)}/{len(errs)} "
+              f"tensors ≤ {tol}; gated {len(gated)}")
+        for k in sorted(errs, key=lambda k: -errs[k])[:8]:
+            print(f"   {k:24s} err {errs[k]:.2e}   κ {kappa[k]:.2e}")
+    assert errs["loss"] <= tol, errs["loss"]
+    bad = {k: (errs[k], kappa[k]) for k in gated if not errs[k] <= tol}
+    assert not bad, bad
+    return errs, kappa

@@ -254,7 +254,7 @@ class Replay:
         xo, wo = Var(x, True), Var(w, True)
         bo = Var(self._val(a["b"]).astype(F64), True) if a["b"] is not None else None
         zo = oops.conv2d(xo, wo, bo, a["stride"], a["pad"])
-        ydev = self.tr.vals[rec["out"]]
+        ydev = y.numpy()  # the re-run's own output: its ReLU mask is the one its backward uses
         mask = (nhwc_to_nchw(ydev) > 0) if a["act"] else None
         fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
         self.record(i, "conv2d", "y", nhwc_to_nchw(ydev), fwd)
@@ -289,7 +289,7 @@ class Replay:
         if a["residual"] is not None:
             ro = Var(nhwc_to_nchw(self._val(a["residual"])).astype(F64), True)
             zo = oops.add(zo, ro)
-        ydev = self.tr.vals[rec["out"]]
+        ydev = y.numpy()
         fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
         self.record(i, "batchnorm2d", "y", nhwc_to_nchw(ydev), fwd)
         if rmd is not None:
@@ -358,7 +358,7 @@ class Replay:
         wo = Var(self._val(a["w"]).astype(F64), True)
         bo = Var(self._val(a["b"]).astype(F64), True) if a["b"] is not None else None
         zo = oops.linear(xo, wo, bo)
-        ydev = self.tr.vals[rec["out"]]
+        ydev = y.numpy()
         fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
         self.record(i, "linear", "y", ydev, fwd)
         g = self._g_out(rec)
@@ -409,7 +409,9 @@ class Replay:
         y = be.embedding(L["table"][1], be.tensor(ids))
         to = Var(self._val(a["table"]).astype(F64), True)
         yo = oops.embedding(to, ids.astype(np.int64))
-        self.record(i, "embedding", "rows", self.tr.vals[rec["out"]], yo.value, exact=True)
+        # f32 rows are copies (exact); bf16 rows are the table rounded once
+        self.record(i, "embedding", "rows", self.tr.vals[rec["out"]], yo.value,
+                    exact=self.tr.dtypes[rec["out"]] == be._lib.BE_F32)
         g = self._g_out(rec)
         if not self._dev_backward(y, g, rec):
             return
@@ -467,3 +469,58 @@ def teacher_forced(be, model, batch, tol):
     del loss
     rp = Replay(be, tr, tol).run()
     return rp
+
+
+def forward_drift(be, trace: OpTrace):
+    """Diagnostic: the oracle's OWN end-to-end forward, op by op over the traced
+    graph (each op fed the oracle's previous outputs, parameters from the
+    trace), against the device's traced outputs.  Returns [(idx, op, err)] —
+    where the two forwards drift apart, not a gate."""
+    ov = {}
+
+    def val(r):
+        k = r.key
+        if k in ov:
+            return ov[k]
+        v = trace.vals[k].astype(F64)
+        return v
+
+    out = []
+    for i, rec in enumerate(trace.recs):
+        a, op = rec["args"], rec["op"]
+        dev = trace.vals[rec["out"]].astype(F64)
+        if op == "conv2d":
+            x = nhwc_to_nchw(val(a["x"]))
+            w = nhwc_to_nchw(val(a["w"]))
+            b = Var(val(a["b"])) if a["b"] is not None else None
+            y = oops.conv2d(Var(x), Var(w), b, a["stride"], a["pad"]).value
+            if a["act"]:
+                y = np.maximum(y, 0)
+            y = nchw_to_nhwc(y)
+        elif op == "batchnorm2d":
+            y, _ = oops.batchnorm2d(Var(nhwc_to_nchw(val(a["x"]))), Var(val(a["gamma"])), Var(val(a["beta"])),
+                                    eps=a["eps"])
+            y = y.value
+            if a["residual"] is not None:
+                y = y + nhwc_to_nchw(val(a["residual"]))
+            if a["act"]:
+                y = np.maximum(y, 0)
+            y = nchw_to_nhwc(y)
+        elif op == "maxpool2d":
+            y = nchw_to_nhwc(oops.maxpool2d(Var(nhwc_to_nchw(val(a["x"]))), a["k"], a["stride"], a["pad"])[0].value)
+        elif op == "avgpool_global":
+            y = oops.avgpool_global(Var(nhwc_to_nchw(val(a["x"])))).value
+        elif op == "reshape":
+            y = val(a["x"]).reshape(dev.shape)
+        elif op == "linear":
+            b = Var(val(a["b"])) if a["b"] is not None else None
+            y = oops.linear(Var(val(a["x"])), Var(val(a["w"])), b).value
+            if a["act"]:
+                y = np.maximum(y, 0)
+        elif op == "softmax_xent":
+            y = np.asarray(oops.softmax_cross_entropy(Var(val(a["z"])), trace.vals[a["labels"].key].astype(np.int64)).value)
+        else:
+            y = dev
+        ov[rec["out"]] = y
+        out.append((i, op, rel_err(dev, y)))
+    return out

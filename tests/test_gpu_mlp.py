@@ -41,69 +41,22 @@ def test_mlp_fp32_ragged_batches(B):
 
 
 def test_mlp_bf16_small():
-    ref, loss, grads, new = _mlp_case((256, 512, 384, 100), 200, "bf16", 1, False)
-    compare_step(ref, loss, grads, new, 2e-2)
-
-
-def test_c2_mlp_bf16_full_size():
-    """C2 at its full size: MLP 4096-4096-4096-1000, batch 1024, bf16, one SGD
-    step against the plain float64 oracle: loss, every gradient and every
-    updated parameter element-wise (∞-norm relative) at 2e-2."""
-    ref, loss, grads, new = _mlp_case((4096, 4096, 4096, 1000), 1024, "bf16", 2, False)
-    errs = compare_step(ref, loss, grads, new, 2e-2)
-    print("C2 bf16 errors:", {k: f"{v:.2e}" for k, v in errs.items()})
-
-
-def test_c2_per_op_parity():
-    """Each C2 layer's forward and VJP fed the SAME inputs on both sides
-    (the GPU's own activations, upstream gradients and ReLU masks):
-    element-wise (∞-norm) ≤ 2e-2 on every output (SURVEY §8(c) reading 15)."""
+    """bf16 MLP (ragged sizes, B = 200): every op teacher-forced at 2e-2, and
+    one end-to-end step against the plain float64 oracle gated on the loss and
+    on every well-conditioned gradient (gpu_common.e2e_gate)."""
+    from teacher import teacher_forced
+    from gpu_common import e2e_gate
     be = be_init()
     be.set_compute_dtype("bf16")
-    from oracle import ops as oops
-    from oracle.autograd import Var, backward
-    sizes, B, seed = (4096, 4096, 4096, 1000), 1024, 5
-    onet = onets.MLP(sizes)
-    P = synth.make_params(onet.param_specs(), seed)
-    x = synth.bf16_values(synth.normal((B, sizes[0]), seed, 1))
-    y = synth.labels(B, sizes[-1], seed)
-    L = len(sizes) - 1
-    # device forward, layer by layer, each layer's input a fresh leaf so we can read its grad
-    acts, outs, leaves = [x], [], []
-    for i in range(L):
-        xin = be.tensor(acts[-1], dtype="bf16")
-        W = be.tensor(P[f"fc{i}.w"], requires_grad=True)
-        b = be.tensor(P[f"fc{i}.b"], requires_grad=True)
-        last = i == L - 1
-        out = be.linear(xin, W, b, act=0 if last else 1, out_f32=last)
-        outs.append(out)
-        leaves.append((xin, W, b))
-        acts.append(out.numpy())
-    loss = be.softmax_xent(outs[-1], be.tensor(y))
-    zv = Var(acts[-1], requires_grad=True)
-    ol = oops.softmax_cross_entropy(zv, y)
-    backward(ol)
-    assert rel(np.array(loss.item()), ol.value) < 2e-2
-    g = zv.grad  # oracle dz for the device logits
-    for i in reversed(range(L)):
-        xin, W, b = leaves[i]
-        last = i == L - 1
-        # device: re-run the op on a grad-requiring copy of its input and backprop g
-        xl = be.tensor(acts[i], requires_grad=True)
-        outd = be.linear(xl, W, b, act=0 if last else 1, out_f32=last)
-        be.zero_grad([W, b])
-        outd.backward(be.tensor(g.astype(np.float32), dtype="f32" if last else "bf16"))
-        # oracle: same inputs, mask taken from the device output
-        xv = Var(acts[i], True)
-        Wv, bv = Var(P[f"fc{i}.w"].astype(np.float64), True), Var(P[f"fc{i}.b"].astype(np.float64), True)
-        yo = oops.linear(xv, Wv, bv)
-        assert rel(outd.numpy(), np.maximum(yo.value, 0) if not last else yo.value) < 2e-2, f"fwd {i}"
-        mask = (acts[i + 1] > 0) if not last else np.ones_like(acts[i + 1], bool)
-        backward(yo, g * mask)
-        for name, dev, orc in (("dx", xl.grad, xv.grad), ("dW", W.grad, Wv.grad), ("db", b.grad, bv.grad)):
-            e = rel(dev.numpy(), orc)
-            assert e < 2e-2, (i, name, e)
-        g = xl.grad.numpy().astype(np.float64)  # device upstream for the layer below
+    sizes, B = (256, 512, 384, 100), 200
+    onet, pnet = onets.MLP(sizes), be.nn.MLP(sizes)
+    P = synth.make_params(onet.param_specs(), 1)
+    x = synth.bf16_values(synth.normal((B, sizes[0]), 1, 1))
+    y = synth.labels(B, sizes[-1], 1)
+    pnet.load(P)
+    rp = teacher_forced(be, pnet, (be.tensor(x, dtype="bf16"), be.tensor(y)), 2e-2)
+    assert not rp.failures(), rp.failures()
+    e2e_gate(be, onet, pnet, P, (x, y), (be.tensor(x, dtype="bf16"), be.tensor(y)), "bf16", name="mlp-small")
 
 
 def test_loss_backward_accumulates_and_zero_grad_releases():

@@ -445,3 +445,23 @@ def test_param_counts():
     cnt = lambda net: sum(int(np.prod(s[1])) for s in net.param_specs())
     assert cnt(nets.ResNet50()) == 25557032
     assert cnt(nets.AlexNet()) == 61100840
+
+
+def test_conditioning_floor_bounds_end_to_end_parity():
+    """Why the bf16 end-to-end gate covers only well-conditioned tensors
+    (tests/conditioning.py, DESIGN R8): perturbing the smoke MLP's parameters
+    and inputs by ±2^-8 (bf16 unit roundoff) moves the ORACLE's own first-layer
+    gradient by > 10 % (∞-norm) — more than the 2e-2 tolerance, so no bf16
+    implementation can meet it end to end — while at fp32 roundoff (2^-24)
+    the same gradients move by < 1e-6 and the loss stays within 1e-3 at bf16."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from conditioning import UNIT_ROUNDOFF, sensitivity
+    net = nets.MLP((256, 384, 128, 10))
+    P = synth.make_params(net.param_specs(), 0)
+    x = synth.bf16_values(synth.normal((96, 256), 0, 1))
+    y = synth.labels(96, 10, 0)
+    kb = sensitivity(net, P, (x, y), UNIT_ROUNDOFF["bf16"])
+    kf = sensitivity(net, P, (x, y), UNIT_ROUNDOFF["f32"])
+    assert kb["grad:fc0.w"] > 0.1 and kb["loss"] < 1e-3
+    assert max(kf.values()) < 1e-6
