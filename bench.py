@@ -4,8 +4,11 @@ on synthetic data (BASELINE.json metric), one process per GPU.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
     torchrun --nproc-per-node N ... bench.py --gpus N      (N > 1: data parallel, NCCL buckets)
 
-Default workload = BASELINE.json configs[1] (C2: MLP 4096-4096-4096-1000,
-batch 1024/GPU, bf16).  Prints ONE JSON line on rank 0.
+Default workload = the north-star configuration (BASELINE.json configs[3],
+C4: ResNet-50 v1.5, 224x224, batch 256/GPU, bf16); `--config c1|c2|c3|c5`
+selects the others.  Prints ONE JSON line on rank 0.  `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N
+ranks (127.0.0.1 rendezvous).
 
 `--impl reference` times the float64 CPU oracle (oracle/) on this host — the
 reference arm of this tier (no reference implementation exists; see
@@ -161,10 +164,35 @@ def oracle_time(cfg, budget_s=15.0, max_steps=None, min_steps=1):
         el = time.perf_counter() - t0
         if (el >= budget_s and n >= min_steps) or (max_steps and n >= max_steps):
             break
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    return {"value": n * sb / el, "unit": "samples/s", "cores": cores, "kind": "oracle",
+    host_cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    threads = blas_threads() or host_cores
+    return {"value": n * sb / el, "unit": "samples/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "threads": threads, "host_cores": host_cores,
             "sample": f"{n} float64 oracle step(s) of {cfg['net']} at batch {sb} (of {B}) in {el:.1f}s, "
                       f"NumPy/OpenBLAS on all host cores"}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def blas_threads():
+    """Threads the oracle's BLAS actually runs with (threadpoolctl), else the env setting."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads") for d in threadpool_info() if d.get("user_api") == "blas"]
+        if n:
+            return max(n)
+    except Exception:
+        pass
+    return int(os.environ.get("OPENBLAS_NUM_THREADS", "0")) or None
 
 
 # ---------------------------------------------------------------- our arm
@@ -222,7 +250,24 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         be.synchronize()
 
+    # host cost of the eager step itself: one step enqueued onto an idle GPU
+    # (empty launch queue).  In the back-to-back loops the host blocks inside
+    # the driver once the launch queue is full, so their host time tracks the
+    # GPU time rather than the enqueue cost (Fig. 1).
+    idle = []
+    for _ in range(5):
+        be.synchronize()
+        ta = time.perf_counter()
+        step(batch)
+        idle.append((time.perf_counter() - ta) * 1e3)
+    be.synchronize()
+    host_idle_ms = statistics.median(idle)
+    stats_warm = be.alloc_stats()
+    trace = bool(os.environ.get("BE_ALLOC_TRACE"))
+
     # ---- device-resident timed region
+    if trace:
+        print("=== timed region start", file=sys.stderr, flush=True)
     clocks = ClockSampler(local_rank)
     clocks.start()
     barrier()
@@ -237,6 +282,21 @@ def run_ours(args, cfg, rank, world, local_rank):
     barrier()
     ms = e0.elapsed_time(e1)
     launches = be.launch_count() - l0
+    stats_timed = be.alloc_stats()
+    if trace:
+        print("=== timed region end", file=sys.stderr, flush=True)
+    # further timed passes of the same K steps (the paper's mean ± sd convention,
+    # PAPER.md:271-276); the headline value is the first pass
+    rep_ms = [ms]
+    for _ in range(max(args.repeats, 1) - 1):
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        r0.record(stream)
+        for _ in range(args.steps):
+            loss = step(batch)
+        r1.record(stream)
+        barrier()
+        rep_ms.append(r0.elapsed_time(r1))
     # second, profiled pass of the same K steps: every tcgen05 GEMM / conv launch
     # bracketed by CUDA events on its stream (the brackets cost a little, so the
     # headline value comes from the unprofiled pass above)
@@ -252,10 +312,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     prof = be.prof_read()
     clk = clocks.stop()
     stats_after = be.alloc_stats()
+    nccl_info = None
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor(rep_ms, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        rep_ms = [float(v) for v in t.tolist()]
+        ms = rep_ms[0]
+        r_, nr = be.api.dist_world()
+        nccl_info = {"nranks": nr, "backend": "libbe NCCL communicator (ncclCommCount)",
+                     "allreduce": "bucketed ncclAllReduce(avg), 25 MB fp32 buckets, comm stream"}
 
     # ---- end-to-end through the public API: every step's batch goes pinned host → device
     # (double-buffered on a copy stream so batch i+1 transfers while step i computes, the
@@ -338,7 +403,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     gemm_ms = sum(r["ms"] for r in tc)
     flops = sum(r["flops"] for r in tc)
     achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    # burst peak (a kernel timed alone at full clock) unless the clocks record of
+    # this region shows the power cap / a clock well below max, then sustained
+    capped = ("sw_power_cap" in clk["reasons"]) or (clk["sm_mhz"] and clk["sm_max_mhz"]
+                                                     and clk["sm_mhz"] < 0.93 * clk["sm_max_mhz"])
+    peak_key = "bf16_tflops_sustained" if capped else "bf16_tflops"
+    peak = pk.get(peak_key, pk.get("bf16_tflops"))
     dt_bench = "bf16" if cfg["dtype"] == "bf16" else "f32"
     if cfg["dtype"] == "f32":
         peak = peak / 2.0 / 3.0  # tf32 nominal = bf16/2; 3xTF32 issues 3 MMAs per algorithmic product
@@ -348,7 +418,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "launches_per_step": len(tc) / args.steps,
             "share_of_step": round(gemm_ms / ms_prof, 4) if ms_prof else None,
             "profiled_pass_ms_per_step": round(ms_prof / args.steps, 4),
-            "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({pk_kind})"}
+            "peak_source": f"MEASURED_PEAKS.json {peak_key} ({pk_kind}; "
+                           + ("power cap / low clock seen in the region)" if capped else "no power cap in the region)")}
     shapes = {}
     for r in tc:
         key = f"{r['m']}x{r['n']}x{r['k']}"
@@ -374,9 +445,15 @@ def run_ours(args, cfg, rank, world, local_rank):
                                   "achieved_gbs": round(ub / (ums / 1e3) / 1e9, 1), "peak_gbs": pk.get("hbm_gbs"),
                                   "frac": round(ub / (ums / 1e3) / hbm, 4),
                                   "tflops": round(sum(r["flops"] for r in upd) / (ums / 1e3) / 1e12, 1)}
+    # traffic: DRAM bytes per launch of this class, from one ncu capture of this
+    # config's step (tools/ncu_class.py writes profiles/traffic_<config>.json);
+    # used only if that capture is of the same kernel class, else null
     trafficf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(trafficf):
-        roof["traffic"] = json.load(open(trafficf)).get("dram_bytes_per_launch")
+        tj = json.load(open(trafficf))
+        if tj.get("kernel_class") == "gemm_tc*,conv_tc*":
+            roof["traffic"] = tj.get("dram_bytes_per_launch")
+            roof["traffic_source"] = tj.get("source")
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = oracle_time(cfg, budget_s=args.cpu_budget)
@@ -391,12 +468,21 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "autotune_steps": args.tune_steps},
         "e2e": {"value": round(B * world * args.steps / (ms_e2e / 1e3), 2), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
-                "host_enqueue_ms_per_step": round(host_ms_e2e, 4)},
+                "host_loop_ms_per_step": round(host_ms_e2e, 4),
+                "host_enqueue_ms_per_step": round(host_idle_ms, 4),
+                "host_enqueue_note": "host time to enqueue one step onto an idle GPU (median of 5); the e2e loop's "
+                                     "host time (host_loop_ms_per_step) includes blocking on the full launch queue"},
+        "repeats": {"n": len(rep_ms), "steps_each": args.steps,
+                    "samples_per_s": [round(B * world * args.steps / (m / 1e3), 1) for m in rep_ms],
+                    "mean": round(statistics.mean(B * world * args.steps / (m / 1e3) for m in rep_ms), 1),
+                    "sd": round(statistics.pstdev(B * world * args.steps / (m / 1e3) for m in rep_ms), 1)},
+        "nccl": nccl_info,
         "gpu_launches": int(launches),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
-        "alloc": {"raw_alloc_count_delta_timed": stats_after["raw_alloc_count"] - stats_warm["raw_alloc_count"],
+        "alloc": {"raw_alloc_count_delta_timed": stats_timed["raw_alloc_count"] - stats_warm["raw_alloc_count"],
+                  "raw_alloc_count_delta_all_passes": stats_after["raw_alloc_count"] - stats_warm["raw_alloc_count"],
                   "peak_bytes_in_use": stats_after["peak_bytes_in_use"]},
         "final_loss": final_loss,
     }
@@ -428,16 +514,26 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--tune-steps", type=int, default=24, help="untimed autotuning steps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--repeats", type=int, default=5, help="timed passes of K steps (mean ± sd reported)")
     ap.add_argument("--sgd", default="overlap", choices=["overlap", "fused"],
                     help="overlap: per-parameter SGD inside backward on a side stream; fused: one launch after")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own launch form)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -446,6 +542,9 @@ def main():
             print(json.dumps(run_reference(args, cfg)), flush=True)
         return
     if world > 1:
+        # the communicator's init line (nranks, NVLS) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -464,6 +464,13 @@ def dist_init(rank, world, uid: bytes):
     call("be_dist_init", int(rank), int(world), buf)
 
 
+def dist_world():
+    """(rank, nranks) as the NCCL communicator reports them (ncclCommCount)."""
+    r, w = C.c_int(), C.c_int()
+    call("be_dist_world", C.byref(r), C.byref(w))
+    return r.value, w.value
+
+
 def ddp_plan(numels, bucket_bytes=25 << 20):
     """Bucket plan of be_ddp_attach (pure host function): (bucket_of, offset_of, bucket_numel)."""
     n = len(numels)

@@ -37,6 +37,7 @@ struct NcclApi {
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
 };
 NcclApi& nccl() {
   static NcclApi api;
@@ -56,6 +57,7 @@ NcclApi& nccl() {
   api.broadcast = (decltype(api.broadcast))dlsym(api.h, "ncclBroadcast");
   api.getErrorString = (decltype(api.getErrorString))dlsym(api.h, "ncclGetErrorString");
   api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
+  api.commCount = (decltype(api.commCount))dlsym(api.h, "ncclCommCount");
   BE_REQUIRE(api.getUniqueId && api.commInitRank && api.allReduce && api.broadcast, BE_E_NCCL,
              "libnccl is missing required symbols");
   return api;
@@ -328,6 +330,11 @@ be_status be_dist_world(int* rank, int* world) {
   BE_REQUIRE(d.comm_ready, BE_E_NOT_INIT, "be_dist_init() was not called");
   *rank = d.rank;
   *world = d.world;
+  if (nccl().commCount) {  // the communicator's own rank count, not the argument we passed
+    int nr = 0;
+    BE_CHECK_NCCL(nccl().commCount(d.comm, &nr));
+    *world = nr;
+  }
   BE_API_END
 }
 

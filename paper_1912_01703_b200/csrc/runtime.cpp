@@ -9,6 +9,8 @@
 // are parked until an event recorded on that stream completes.
 // Exact rounded-size reuse, LIFO; on cudaMalloc failure
 // empty_cache() and retry once.
+#include <execinfo.h>
+
 #include "runtime.h"
 
 #include <cstdio>
@@ -202,6 +204,28 @@ Block* CachingAllocator::allocate(size_t nbytes, cudaStream_t s) {
     if (poison) cudaMemsetAsync(b->ptr, 0xFF, sz, s);  // debug: stale data shows as NaN
     return b;
   }
+  // A block of this size and stream still waiting on another stream's use
+  // (record_stream) is reused in stream order instead of growing the pool:
+  // stream s waits on that use's event, no host synchronisation (the host may
+  // run ahead of the side streams, so their events are often still pending).
+  for (size_t i = 0; i < deferred_.size(); ++i) {
+    Block* b = deferred_[i].b;
+    if (b->stream != s || b->size != sz) continue;
+    for (cudaEvent_t e : deferred_[i].events) {
+      cudaStreamWaitEvent(s, e, 0);
+      cudaEventDestroy(e);
+    }
+    b->extra_streams.clear();
+    deferred_[i] = deferred_.back();
+    deferred_.pop_back();
+    b->in_use = true;
+    st_.cache_hit_count++;
+    st_.bytes_cached -= sz;
+    st_.bytes_in_use += sz;
+    st_.peak_bytes_in_use = std::max(st_.peak_bytes_in_use, st_.bytes_in_use);
+    if (poison) cudaMemsetAsync(b->ptr, 0xFF, sz, s);
+    return b;
+  }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, sz);
   if (e != cudaSuccess) {
@@ -214,6 +238,13 @@ Block* CachingAllocator::allocate(size_t nbytes, cudaStream_t s) {
       cudaGetLastError();
       fail(BE_E_OOM, "out of memory allocating " + std::to_string(sz) + " bytes");
     }
+  }
+  static const bool trace = getenv("BE_ALLOC_TRACE") != nullptr;
+  if (trace) {  // debug: who grows the pool (size, stream, native call stack)
+    fprintf(stderr, "be raw alloc #%llu: %zu B on stream %p\n", (unsigned long long)st_.raw_alloc_count + 1, sz,
+            (void*)s);
+    void* bt[16];
+    backtrace_symbols_fd(bt, backtrace(bt, 16), 2);
   }
   Block* b = new Block();
   b->ptr = p;

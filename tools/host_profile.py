@@ -21,12 +21,29 @@ step = lambda: be.nn.train_step(model, batch, lr=0.01, momentum=0.9, weight_deca
 for _ in range(30):
     step()
 be.synchronize()
+import ctypes  # noqa: E402
+try:  # tools/sampler.c, when LD_PRELOADed: sample the C++ side during the timed host loop
+    arm = ctypes.CDLL(None).sampler_arm
+except AttributeError:
+    arm = lambda on: None  # noqa: E731
+arm(1)
 t0 = time.perf_counter()
 for _ in range(steps):
     step()
 t1 = time.perf_counter()
+arm(0)
 be.synchronize()
 print(f"host enqueue {1e3 * (t1 - t0) / steps:.2f} ms/step (GPU drained after: {1e3 * (time.perf_counter() - t0) / steps:.2f})")
+# one step enqueued onto an idle GPU (empty launch queue): the host's own cost
+one = []
+for _ in range(steps):
+    be.synchronize()
+    ta = time.perf_counter()
+    step()
+    one.append(time.perf_counter() - ta)
+be.synchronize()
+one.sort()
+print(f"host enqueue of one step onto an idle GPU: median {1e3 * one[len(one) // 2]:.2f} ms, min {1e3 * one[0]:.2f} ms")
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(steps):
