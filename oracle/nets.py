@@ -221,3 +221,104 @@ class NCF:
             h = ops.relu(ops.linear(h, P[f"mlp{i}.w"], P[f"mlp{i}.b"]))
         z = ops.linear(ops.concat([g, h], 1), P["head.w"], P["head.b"])
         return ops.bce_as_two_class_ce(z, y), {"logits": z.value}
+
+
+# ---------------------------------------------------------------- VGG-19 (Table 1)
+class VGG19:
+    """VGG-19 (Table 1; configuration "E" of Simonyan & Zisserman,
+    the torchvision form — DESIGN.md reading R15): sixteen 3×3/1/1 convs with
+    bias + ReLU in five stages of 64, 128, 256, 512, 512 channels, each stage
+    closed by maxpool 2×2/2; flatten (NCHW order; the adaptive 7×7 pool is the
+    identity at 224²); classifier fc6 25088→4096, ReLU, dropout, fc7
+    4096→4096, ReLU, dropout, fc8 4096→1000.  Dropout masks are the
+    counter-based draws of ops.dropout with (seed, offset = 6 | 7)."""
+    STAGES = ((64, 2), (128, 2), (256, 4), (512, 4), (512, 4))
+
+    def __init__(self, classes=1000, width=1.0, image=224, dropout=0.5, seed=0):
+        self.classes, self.image, self.p, self.seed = classes, image, dropout, seed
+        chain, prev, hw = [], 3, image
+        for si, (k, n) in enumerate(self.STAGES):
+            k = max(1, int(k * width))
+            for j in range(n):
+                chain.append((f"conv{si + 1}_{j + 1}", k, prev, j == n - 1))
+                prev = k
+            hw //= 2
+        self.convs, self.feat = chain, prev * hw * hw
+        self.hidden = max(1, int(4096 * width))
+
+    def param_specs(self):
+        s = []
+        for (n, k, c, pool) in self.convs:
+            s += _conv(n, k, c, 3, True)
+        return s + _lin("fc6", self.feat, self.hidden) + _lin("fc7", self.hidden, self.hidden) + \
+            _lin("fc8", self.hidden, self.classes)
+
+    def loss(self, P, batch, state=None):
+        x, y = batch
+        h = Var(x)
+        for (n, k, c, pool) in self.convs:
+            h = ops.relu(ops.conv2d(h, P[n + ".w"], P[n + ".b"], 1, 1))
+            if pool:
+                h, _ = ops.maxpool2d(h, 2, 2, 0)
+        h = ops.flatten(h)
+        h = ops.dropout(ops.relu(ops.linear(h, P["fc6.w"], P["fc6.b"])), self.p, self.seed, 6)
+        h = ops.dropout(ops.relu(ops.linear(h, P["fc7.w"], P["fc7.b"])), self.p, self.seed, 7)
+        z = ops.linear(h, P["fc8.w"], P["fc8.b"])
+        return ops.softmax_cross_entropy(z, y), {"logits": z.value}
+
+
+# ---------------------------------------------------------------- MobileNetV2 (Table 1)
+class MobileNetV2:
+    """MobileNet (Table 1) read as MobileNetV2 (Sandler et al.
+    2018, the torchvision model; reading R13): stem conv 3×3/2
+    3→32 + BN + ReLU6; inverted residual blocks (t, c, n, s) =
+    (1,16,1,1) (6,24,2,2) (6,32,3,2) (6,64,4,2) (6,96,3,1) (6,160,3,2)
+    (6,320,1,1): [1×1 expand + BN + ReLU6 when t > 1] → 3×3 depthwise
+    (stride s on the first block of a group) + BN + ReLU6 → 1×1 project + BN,
+    plus the identity when stride 1 and C_in = C_out; head 1×1 → 1280 + BN +
+    ReLU6; global avgpool; dropout(p); Linear(1280, classes).  Convs have no
+    bias.  3,504,872 parameters at the defaults."""
+    SETTINGS = ((1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2),
+                (6, 320, 1, 1))
+
+    def __init__(self, classes=1000, width=1.0, dropout=0.2, seed=0, settings=None):
+        self.classes, self.p, self.seed = classes, dropout, seed
+        w = lambda c: max(8, int(c * width))  # noqa: E731
+        self.stem = w(32)
+        self.last = max(1280, w(1280)) if width >= 1.0 else w(1280)
+        blocks, cin = [], self.stem
+        for gi, (t, c, n, s) in enumerate(settings or self.SETTINGS):
+            cout = w(c)
+            for j in range(n):
+                blocks.append((f"b{len(blocks)}", cin, cin * t, cout, s if j == 0 else 1, t))
+                cin = cout
+        self.blocks, self.cfinal = blocks, cin
+
+    def param_specs(self):
+        s = _conv("stem", self.stem, 3, 3, False) + _bn("stem_bn", self.stem)
+        for (n, cin, hid, cout, st, t) in self.blocks:
+            if t != 1:
+                s += _conv(n + ".exp", hid, cin, 1, False) + _bn(n + ".exp_bn", hid)
+            s += [(n + ".dw.w", (hid, 1, 3, 3), "normal", 9)] + _bn(n + ".dw_bn", hid)
+            s += _conv(n + ".proj", cout, hid, 1, False) + _bn(n + ".proj_bn", cout)
+        s += _conv("head", self.last, self.cfinal, 1, False) + _bn("head_bn", self.last)
+        return s + _lin("fc", self.last, self.classes)
+
+    def loss(self, P, batch, state=None):
+        x, y = batch
+
+        def bn(h, name):
+            o, _ = ops.batchnorm2d(h, P[name + ".g"], P[name + ".b"])
+            return o
+        h = ops.relu6(bn(ops.conv2d(Var(x), P["stem.w"], None, 2, 1), "stem_bn"))
+        for (n, cin, hid, cout, st, t) in self.blocks:
+            u = h
+            if t != 1:
+                u = ops.relu6(bn(ops.conv2d(u, P[n + ".exp.w"], None, 1, 0), n + ".exp_bn"))
+            u = ops.relu6(bn(ops.conv2d_depthwise(u, P[n + ".dw.w"], st, 1), n + ".dw_bn"))
+            u = bn(ops.conv2d(u, P[n + ".proj.w"], None, 1, 0), n + ".proj_bn")
+            h = ops.add(u, h) if (st == 1 and cin == cout) else u
+        h = ops.relu6(bn(ops.conv2d(h, P["head.w"], None, 1, 0), "head_bn"))
+        h = ops.dropout(ops.avgpool_global(h), self.p, self.seed, 0)
+        z = ops.linear(h, P["fc.w"], P["fc.b"])
+        return ops.softmax_cross_entropy(z, y), {"logits": z.value}

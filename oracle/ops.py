@@ -310,3 +310,120 @@ def embedding(table: Var, ids: np.ndarray) -> Var:
         np.add.at(d, ids, g)
         return [d]
     return record("embedding", [table], tv[ids], vjp)
+
+
+# ---------------------------------------------------------------- ReLU6 (MobileNetV2)
+def relu6(x: Var) -> Var:
+    """y = min(max(x, 0), 6); dx = dy·1[0 < x < 6] (gradient 0 at both kinks,
+    the ReLU convention of SPEC S:203 extended to the upper clamp).  MobileNetV2's
+    activation (Table 1 "MobileNet"; reading R13)."""
+    xv = x.value.astype(f64)
+    mask = ((xv > 0) & (xv < 6)).astype(f64)
+    return record("relu6", [x], np.clip(xv, 0.0, 6.0), lambda g: [g * mask])
+
+
+# ---------------------------------------------------------------- depthwise convolution
+def conv2d_depthwise(x: Var, w: Var, stride=1, pad=0) -> Var:
+    """Depthwise convolution (groups = C, one R×S filter per channel; the
+    separable convolutions of MobileNet, Table 1):
+        y[n,c,p,q] = Σ_{r,s} x[n, c, p·stride − pad + r, q·stride − pad + s] · w[c, 0, r, s]
+    with zero padding (cross-correlation, no flip, as conv2d / SPEC S:113-121).
+    dx[n,c,h,w] = Σ over the (p,q,r,s) with h = p·stride−pad+r, w = q·stride−pad+s of dy·w;
+    dw[c,0,r,s] = Σ_{n,p,q} dy[n,c,p,q] · x[n,c,p·stride−pad+r, q·stride−pad+s]."""
+    xv = x.value.astype(f64)
+    wv = w.value.astype(f64)
+    N, C, H, W = xv.shape
+    C2, one, R, S = wv.shape
+    assert C == C2 and one == 1, "ShapeMismatch"
+    P, Q = conv_out_size(H, R, stride, pad), conv_out_size(W, S, stride, pad)
+    xp = np.zeros((N, C, H + 2 * pad + R, W + 2 * pad + S), dtype=f64)
+    xp[:, :, pad:pad + H, pad:pad + W] = xv
+    y = np.zeros((N, C, P, Q), dtype=f64)
+    for r in range(R):
+        for s in range(S):
+            win = xp[:, :, r:r + stride * (P - 1) + 1:stride, s:s + stride * (Q - 1) + 1:stride]
+            y += win * wv[None, :, 0, r, s, None, None]
+
+    def vjp(g):
+        dxp = np.zeros_like(xp)
+        dw = np.zeros_like(wv)
+        for r in range(R):
+            for s in range(S):
+                win = xp[:, :, r:r + stride * (P - 1) + 1:stride, s:s + stride * (Q - 1) + 1:stride]
+                dw[:, 0, r, s] = (g * win).sum(axis=(0, 2, 3))
+                dxp[:, :, r:r + stride * (P - 1) + 1:stride, s:s + stride * (Q - 1) + 1:stride] += \
+                    g * wv[None, :, 0, r, s, None, None]
+        return [np.ascontiguousarray(dxp[:, :, pad:pad + H, pad:pad + W]), dw]
+    return record("conv2d_depthwise", [x, w], y, vjp)
+
+
+# ---------------------------------------------------------------- dropout
+_PHILOX_M0, _PHILOX_M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+_M64 = (1 << 64) - 1
+
+
+def _mulhilo64(a, b):
+    """(hi, lo) 64-bit halves of the 128-bit product of uint64 arrays a·b,
+    from 32-bit limbs (plain schoolbook multiplication)."""
+    m32 = np.uint64(0xFFFFFFFF)
+    s32 = np.uint64(32)
+    a_lo, a_hi = a & m32, a >> s32
+    b_lo, b_hi = b & m32, b >> s32
+    ll = a_lo * b_lo
+    lh = a_lo * b_hi
+    hl = a_hi * b_lo
+    hh = a_hi * b_hi
+    mid = (ll >> s32) + (lh & m32) + (hl & m32)
+    lo = (ll & m32) | ((mid & m32) << s32)
+    hi = hh + (lh >> s32) + (hl >> s32) + (mid >> s32)
+    return hi, lo
+
+
+def philox4x64_10(counter, key):
+    """Philox4x64-10 (Salmon et al., SC'11 "Parallel random numbers: as easy
+    as 1, 2, 3"): counter uint64[..., 4], key uint64[2] → uint64[..., 4].
+    Each round: (hi0, lo0) = M0·c0, (hi1, lo1) = M1·c2;
+    c ← (hi1 ⊕ c1 ⊕ k0, lo1, hi0 ⊕ c3 ⊕ k1, lo0); then the key is bumped by
+    the Weyl constants (W0, W1).  Ten rounds."""
+    with np.errstate(over="ignore"):
+        c = [np.asarray(counter[..., i], dtype=np.uint64).copy() for i in range(4)]
+        k0 = np.uint64(int(key[0]) & _M64)
+        k1 = np.uint64(int(key[1]) & _M64)
+        for rnd in range(10):
+            if rnd:
+                k0 = np.uint64((int(k0) + _PHILOX_W0) & _M64)
+                k1 = np.uint64((int(k1) + _PHILOX_W1) & _M64)
+            hi0, lo0 = _mulhilo64(np.uint64(_PHILOX_M0), c[0])
+            hi1, lo1 = _mulhilo64(np.uint64(_PHILOX_M1), c[2])
+            c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+        return np.stack(c, axis=-1)
+
+
+def dropout_keep_mask(n, p, seed, offset):
+    """Keep decisions of dropout for elements i = 0..n-1 (row-major over the
+    logical tensor) — a counter-based draw, so the backward pass and every
+    replica regenerate it from (seed, offset) alone (reading R14):
+      word_i = Philox4x64-10(counter = (i // 4, offset, 0, 0), key = (seed, 0))[i % 4]
+      keep_i = (word_i >> 32) >= T,  T = floor(p · 2^32)   (integer compare)."""
+    i = np.arange(n, dtype=np.uint64)
+    blocks = np.arange((n + 3) // 4, dtype=np.uint64)
+    ctr = np.zeros((len(blocks), 4), dtype=np.uint64)
+    ctr[:, 0] = blocks
+    ctr[:, 1] = np.uint64(int(offset) & _M64)
+    words = philox4x64_10(ctr, (seed, 0)).reshape(-1)[:n]
+    T = int(np.floor(float(p) * 4294967296.0))
+    del i
+    return (words >> np.uint64(32)) >= np.uint64(T)
+
+
+def dropout(x: Var, p: float, seed: int, offset: int = 0, training: bool = True) -> Var:
+    """Inverted dropout (Listing 1 / §4.1 names dropout,
+    PAPER.md:64): y = x·keep/(1−p) in training, y = x otherwise; dx = dy·keep/(1−p).
+    p = 1 drops everything (y = 0)."""
+    xv = x.value.astype(f64)
+    if not training or p == 0.0:
+        return record("dropout", [x], xv.copy(), lambda g: [g])
+    keep = dropout_keep_mask(xv.size, p, seed, offset).reshape(xv.shape).astype(f64)
+    scale = 0.0 if p >= 1.0 else 1.0 / (1.0 - p)
+    return record("dropout", [x], xv * keep * scale, lambda g: [g * keep * scale])

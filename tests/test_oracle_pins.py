@@ -465,3 +465,156 @@ def test_conditioning_floor_bounds_end_to_end_parity():
     kf = sensitivity(net, P, (x, y), UNIT_ROUNDOFF["f32"])
     assert kb["grad:fc0.w"] > 0.1 and kb["loss"] < 1e-3
     assert max(kf.values()) < 1e-5
+
+
+# ------------------------------------------------------------ round 2: VGG-19 / MobileNetV2 ops
+def test_param_counts_vgg19_mobilenetv2():
+    """VGG-19 has 143,667,240 parameters and MobileNetV2 3,504,872 (the
+    torchvision models' published counts; readings R13, R15)."""
+    cnt = lambda net: sum(int(np.prod(s[1])) for s in net.param_specs())
+    assert cnt(nets.VGG19()) == 143667240
+    assert cnt(nets.MobileNetV2()) == 3504872
+
+
+def test_philox4x64_matches_numpy_philox():
+    """oracle.ops.philox4x64_10 against NumPy's own Philox4x64-10 bit generator
+    (an independent library implementation): NumPy increments its counter
+    before each block, so NumPy at counter c yields our block at c + 1."""
+    for key, ctr in [((7, 0), (0, 0, 0, 0)), ((3, 0), (41, 5, 0, 0)), ((2**63 + 11, 2**40), (2**64 - 2, 9, 1, 3))]:
+        g = np.random.Philox(key=np.array(key, np.uint64), counter=np.array(ctr, np.uint64))
+        raw = g.random_raw(8).reshape(2, 4)
+        for j in range(2):
+            v = sum(int(ctr[i]) << (64 * i) for i in range(4)) + 1 + j  # 256-bit counter, carries
+            c = [(v >> (64 * i)) & (2**64 - 1) for i in range(4)]
+            ours = ops.philox4x64_10(np.array([c], np.uint64), key)[0]
+            assert np.array_equal(ours, raw[j]), (key, ctr, j)
+
+
+def test_dropout_spec_values():
+    """eval mode and p = 0 return x bitwise; the mean of
+    dropout(ones(100000), 0.5, seed=3) is 1 ± 0.02 (expectation preserved);
+    the kept fraction is within 5 binomial standard deviations of 1 − p;
+    p = 1 drops everything."""
+    x = np.random.default_rng(0).standard_normal((7, 13))
+    assert np.array_equal(ops.dropout(V(x), 0.5, 3, training=False).value, x)
+    assert np.array_equal(ops.dropout(V(x), 0.0, 3, training=True).value, x)
+    y = ops.dropout(V(np.ones(100000)), 0.5, 3).value
+    assert abs(y.mean() - 1.0) <= 0.02
+    for p in (0.2, 0.5, 0.9):
+        keep = ops.dropout_keep_mask(200000, p, 11, 4)
+        sd = math.sqrt(200000 * p * (1 - p))
+        assert abs(keep.sum() - 200000 * (1 - p)) <= 5 * sd, p
+    assert not ops.dropout(V(np.ones(64)), 1.0, 1).value.any()
+    # the mask depends on (seed, offset) and element index only: a prefix is stable
+    assert np.array_equal(ops.dropout_keep_mask(10, 0.5, 9, 2), ops.dropout_keep_mask(1000, 0.5, 9, 2)[:10])
+    assert not np.array_equal(ops.dropout_keep_mask(1000, 0.5, 9, 2), ops.dropout_keep_mask(1000, 0.5, 9, 3))
+
+
+def test_dropout_threshold_is_integer_compare():
+    """keep_i ⇔ (word_i >> 32) ≥ floor(p·2^32), recomputed here from the raw
+    Philox words for a handful of elements (element i uses word i mod 4 of
+    block i div 4, counter (i div 4, offset, 0, 0))."""
+    p, seed, off = 0.3, 5, 2
+    keep = ops.dropout_keep_mask(10, p, seed, off)
+    T = int(p * 2**32)
+    for i in range(10):
+        w = ops.philox4x64_10(np.array([[i // 4, off, 0, 0]], np.uint64), (seed, 0))[0, i % 4]
+        assert keep[i] == ((int(w) >> 32) >= T)
+
+
+def test_relu6_hand_values():
+    x = V(np.array([-1.0, 0.0, 0.5, 6.0, 7.5, 5.99]), True)
+    y = ops.relu6(x)
+    assert np.array_equal(y.value, [0.0, 0.0, 0.5, 6.0, 6.0, 5.99])
+    backward(ops.sum_all(y))
+    assert np.array_equal(x.grad, [0.0, 0.0, 1.0, 0.0, 0.0, 1.0])
+
+
+def _direct_depthwise(x, w, stride, pad):
+    N, C, H, W = x.shape
+    _, _, R, S = w.shape
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    y = np.zeros((N, C, P, Q))
+    for n in range(N):
+        for c in range(C):
+            for p in range(P):
+                for q in range(Q):
+                    for r in range(R):
+                        for u in range(S):
+                            h, ww = p * stride - pad + r, q * stride - pad + u
+                            if 0 <= h < H and 0 <= ww < W:
+                                y[n, c, p, q] += x[n, c, h, ww] * w[c, 0, r, u]
+    return y
+
+
+@pytest.mark.parametrize("stride,pad", [(1, 1), (2, 1), (1, 0), (2, 0)])
+def test_depthwise_brute_force_and_dense_equivalence(stride, pad):
+    """Depthwise conv vs the 6-loop textbook definition, and vs the dense
+    conv2d with a block-diagonal weight (groups = C is a dense conv whose
+    off-diagonal filters are zero) — values and both gradients."""
+    rng = np.random.default_rng(stride * 7 + pad)
+    x = rng.standard_normal((2, 5, 7, 6))
+    w = rng.standard_normal((5, 1, 3, 3))
+    y = ops.conv2d_depthwise(V(x), V(w), stride, pad).value
+    assert np.allclose(y, _direct_depthwise(x, w, stride, pad), rtol=1e-12, atol=1e-12)
+    wd = np.zeros((5, 5, 3, 3))
+    for c in range(5):
+        wd[c, c] = w[c, 0]
+    g = rng.standard_normal(y.shape)
+    xa, wa = V(x, True), V(w, True)
+    backward(ops.conv2d_depthwise(xa, wa, stride, pad), g)
+    xb, wb = V(x, True), V(wd, True)
+    yd = ops.conv2d(xb, wb, None, stride, pad)
+    assert np.allclose(yd.value, y, rtol=1e-12, atol=1e-12)
+    backward(yd, g)
+    assert np.allclose(xa.grad, xb.grad, rtol=1e-12, atol=1e-12)
+    assert np.allclose(wa.grad[:, 0], np.stack([wb.grad[c, c] for c in range(5)]), rtol=1e-12, atol=1e-12)
+
+
+def test_depthwise_vs_scipy_correlate():
+    from scipy.signal import correlate
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((2, 4, 8, 7))
+    w = rng.standard_normal((4, 1, 3, 3))
+    y = ops.conv2d_depthwise(V(x), V(w), 1, 0).value
+    for n in range(2):
+        for c in range(4):
+            assert np.allclose(y[n, c], correlate(x[n, c], w[c, 0], mode="valid"), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_gradcheck_mobilenet_ops(seed):
+    """Central differences through depthwise conv (stride 2), BN, ReLU6,
+    dropout with its fixed counter-based mask, avgpool and a Linear head."""
+    rng = np.random.default_rng(100 + seed)
+    x = Var(rng.standard_normal((2, 3, 7, 7)), True, "x")
+    w = Var(rng.standard_normal((3, 1, 3, 3)) * 0.5, True, "w")
+    g = Var(rng.standard_normal(3) + 1.0, True, "g")
+    be = Var(rng.standard_normal(3), True, "be")
+    fw = Var(rng.standard_normal((3, 4)) * 0.3, True, "fw")
+    fb = Var(rng.standard_normal(4), True, "fb")
+    y = rng.integers(0, 4, 2)
+
+    def f():
+        h = ops.conv2d_depthwise(x, w, 2, 1)
+        h, _ = ops.batchnorm2d(h, g, be)
+        h = ops.relu6(ops.add(h, h))
+        h = ops.dropout(ops.avgpool_global(h), 0.3, seed, 1)
+        return ops.softmax_cross_entropy(ops.linear(h, fw, fb), y)
+    _gradcheck(f, [x, w, g, be, fw, fb], seed=seed)
+
+
+def test_gradcheck_tiny_mobilenet_and_vgg():
+    net = nets.MobileNetV2(classes=5, width=0.25, settings=((1, 16, 1, 1), (6, 24, 2, 2)), dropout=0.2, seed=3)
+    P0 = synth.make_params(net.param_specs(), 4)
+    x = synth.normal((2, 3, 16, 16), 4, 1).astype(np.float64)
+    y = synth.labels(2, 5, 4)
+    P = {k: Var(v.astype(np.float64), True, k) for k, v in P0.items()}
+    _gradcheck(lambda: net.loss(P, (x, y))[0], [P["stem.w"], P["b0.dw.w"], P["b1.exp.w"], P["b2.proj_bn.g"],
+                                                 P["fc.w"]], n_coords=5)
+    vgg = nets.VGG19(classes=5, width=1 / 16, image=32, dropout=0.5, seed=2)
+    P0 = synth.make_params(vgg.param_specs(), 5)
+    x = synth.normal((2, 3, 32, 32), 5, 1).astype(np.float64)
+    P = {k: Var(v.astype(np.float64), True, k) for k, v in P0.items()}
+    _gradcheck(lambda: vgg.loss(P, (x, y))[0], [P["conv1_1.w"], P["conv5_4.b"], P["fc6.w"], P["fc8.b"]], n_coords=5)
