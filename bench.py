@@ -39,8 +39,12 @@ CONFIGS = {
     "c3": dict(workload="C3 AlexNet (single tower), 224x224, batch 256/GPU, bf16", net="alexnet", batch=256,
                dtype="bf16"),
     "c4": dict(workload="C4 ResNet-50 v1.5, 224x224, batch 256/GPU, bf16", net="resnet50", batch=256, dtype="bf16"),
-    "c5": dict(workload="C5 NCF NeuMF (ML-20M tables), batch 8192/GPU (65536 global on 8), bf16", net="ncf",
-               batch=8192, dtype="bf16"),
+    "c6": dict(workload="C6 VGG-19, 224x224, batch 256/GPU, bf16 (Table 1 CNN; dropout 0.5 on fc6/fc7)", net="vgg19",
+               batch=256, dtype="bf16"),
+    "c7": dict(workload="C7 MobileNetV2, 224x224, batch 256/GPU, bf16 (Table 1 \"MobileNet\"; depthwise convs, "
+                        "ReLU6, dropout 0.2)", net="mobilenetv2", batch=256, dtype="bf16"),
+    "c5": dict(workload="C5 NCF NeuMF (ML-20M tables), batch 8192/GPU (65536 global on 8), bf16; embedding "
+                        "tables on sparse touched-rows SGD", net="ncf", batch=8192, dtype="bf16", sparse=True),
 }
 METRIC = "train samples/s (fwd+bwd+SGD) at 1/2/4/8 B200; per-kernel % of roofline"
 
@@ -62,6 +66,10 @@ def make_model(cfg, be, seed=0):
         m = be.nn.AlexNet()
     elif cfg["net"] == "resnet50":
         m = be.nn.ResNet50()
+    elif cfg["net"] == "vgg19":
+        m = be.nn.VGG19()
+    elif cfg["net"] == "mobilenetv2":
+        m = be.nn.MobileNetV2()
     else:
         m = be.nn.NCF()
     m.load(synth.make_params(m.param_specs(), seed))
@@ -78,7 +86,7 @@ def host_batch(cfg, seed, rank=0):
         y = synth.labels(B, cfg["sizes"][-1], seed + rank)
         xd = f32_to_bf16_bits(x) if cfg["dtype"] == "bf16" else x
         return [xd, y]
-    if cfg["net"] in ("alexnet", "resnet50"):
+    if cfg["net"] in ("alexnet", "resnet50", "vgg19", "mobilenetv2"):
         x = synth.normal((B, 3, 224, 224), seed, 1 + rank)
         nhwc = np.zeros((B, 224, 224, 8), np.float32)
         nhwc[..., :3] = x.transpose(0, 2, 3, 1)
@@ -146,8 +154,9 @@ def oracle_time(cfg, budget_s=15.0, max_steps=None, min_steps=1):
         sb = min(B, 256 if cfg["sizes"][0] > 1000 else B)
         batch = ((synth.uniform if cfg["sizes"][0] == 784 else synth.normal)((sb, cfg["sizes"][0]), 0, 1),
                  synth.labels(sb, cfg["sizes"][-1], 0))
-    elif cfg["net"] in ("alexnet", "resnet50"):
-        net = onets.AlexNet() if cfg["net"] == "alexnet" else onets.ResNet50()
+    elif cfg["net"] in ("alexnet", "resnet50", "vgg19", "mobilenetv2"):
+        net = {"alexnet": onets.AlexNet, "resnet50": onets.ResNet50, "vgg19": onets.VGG19,
+               "mobilenetv2": onets.MobileNetV2}[cfg["net"]]()
         sb = 2
         batch = (synth.normal((sb, 3, 224, 224), 0, 1), synth.labels(sb, 1000, 0))
     else:
@@ -214,7 +223,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world > 1:
         be.ddp_attach(params, 25 << 20)
     hb = host_batch(cfg, seed=1, rank=rank)
-    dts = ["bf16" if (i == 0 and cfg["net"] != "ncf" and cfg["dtype"] == "bf16") else None for i in range(len(hb))]
+    dts = ["bf16" if (i == 0 and cfg["net"] not in ("ncf",) and cfg["dtype"] == "bf16") else None
+           for i in range(len(hb))]
 
     def dev_batch():
         out = []
@@ -231,7 +241,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     batch = dev_batch()
 
     def step(b, overlap=args.sgd == "overlap"):
-        return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4, overlap_sgd=overlap)
+        return be.nn.train_step(model, b, lr=0.01, momentum=0.9, weight_decay=1e-4, overlap_sgd=overlap,
+                                sparse_embeddings=cfg.get("sparse", False))
 
     # setup: on-line kernel-variant autotuning (each tuned shape runs every
     # candidate twice, cudnn.benchmark-style) before the W warm-up steps
@@ -329,7 +340,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # the host link); the device pads them to the kernels' 8-channel layout
     # (concat with a resident zero block) inside the timed step
     hb_e2e, dts_e2e, pad = list(hb), list(dts), None
-    if cfg["net"] in ("alexnet", "resnet50") and cfg["dtype"] == "bf16":
+    if cfg["net"] in ("alexnet", "resnet50", "vgg19", "mobilenetv2") and cfg["dtype"] == "bf16":
         img = hb[0]
         npix = img.shape[0] * img.shape[1] * img.shape[2]
         hb_e2e[0] = np.ascontiguousarray(img[..., :3]).reshape(npix, 3)
@@ -464,7 +475,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["workload"], "global_batch": B * world, "per_gpu_batch": B,
                    "parallelism": f"dp{world}", "l2": "working set > L2 (params+grads+momentum stream through "
                    "every step)", "optimizer": "SGD momentum 0.9 wd 1e-4, "
-                   + ("overlapped with backward (be_sgd_overlap)" if args.sgd == "overlap" else "fused after backward"),
+                   + ("overlapped with backward (be_sgd_overlap)" if args.sgd == "overlap" else "fused after backward")
+                   + ("; embedding tables: plain SGD on the touched rows inside backward (be_sgd_sparse)"
+                      if cfg.get("sparse") else ""),
                    "autotune_steps": args.tune_steps},
         "e2e": {"value": round(B * world * args.steps / (ms_e2e / 1e3), 2), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,

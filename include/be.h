@@ -142,7 +142,13 @@ typedef enum {
   BE_OP_SUM = 15,          /* in: x; out: [] */
   BE_OP_MEAN = 16,         /* in: x; out: [] */
   BE_OP_CAST = 17,         /* in: x; attrs be_dtype*; out: x cast (RN-even for f32→bf16) */
-  BE_OP_ADD_RELU = 18      /* residual: y = relu(a + b), same shape */
+  BE_OP_ADD_RELU = 18,     /* residual: y = relu(a + b), same shape */
+  BE_OP_DROPOUT = 19,      /* in: x (contiguous f32|bf16); attrs be_dropout_attrs; out: y = x·keep/(1−p) (
+                              PAPER.md:64).  keep_i = (Philox4x64-10(counter (i/4, offset, 0, 0), key (seed, 0))[i%4] >> 32)
+                              >= floor(p·2^32), i the row-major element index — regenerated in backward, no mask stored */
+  BE_OP_CONV2D_DEPTHWISE = 20 /* in: x NHWC[N,H,W,C] (C % 8 == 0), w f32 RSC [3,3,C]; attrs be_dwconv_attrs;
+                              out NHWC[N,P,Q,C]: y[n,p,q,c] = Σ_{r,s} x[n, p·st−pad+r, q·st−pad+s, c]·w[r,s,c]
+                              (MobileNet's depthwise conv, Table 1; oracle conv2d_depthwise) */
 } be_op_id;
 
 typedef struct { int act; /* 0 none, 1 relu */ int out_f32; /* 1: fp32 output even in bf16 mode */ } be_linear_attrs;
@@ -155,11 +161,19 @@ typedef struct {
 typedef struct { int k, stride, pad; } be_pool_attrs;
 typedef struct {
   float eps, momentum;
-  int act;       /* fused ReLU after the affine (and after the residual add) */
+  int act;       /* fused activation after the affine (and after the residual add): 0 none, 1 ReLU, 2 ReLU6
+                    (MobileNetV2; not with residual) */
   int residual;  /* 1: the LAST input is a residual r (x's shape/dtype): y = act(bn(x) + r) — the ResNet block
                     output in one pass; r receives the gradient act'(y)·dy */
 } be_bn_attrs;
 typedef struct { int rank; int64_t shape[6]; } be_shape_attrs;
+typedef struct {
+  double p;          /* drop probability in [0, 1]; p = 1 drops everything */
+  int training;      /* 0: identity (eval mode) */
+  uint64_t seed;     /* Philox key word 0 */
+  uint64_t offset;   /* Philox counter word 1: distinct per dropout site / step */
+} be_dropout_attrs;
+typedef struct { int stride, pad; } be_dwconv_attrs;
 
 be_status be_op(int op_id, const be_tensor* in, int n_in, const void* attrs,
                 be_tensor* out, int n_out);
@@ -205,6 +219,20 @@ be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum,
  * Params that get no gradient in a backward are not updated. */
 be_status be_sgd_overlap(const be_tensor* params, int n, float lr, float momentum,
                          float weight_decay);
+/* Sparse SGD of embedding tables (NCF): registers
+ * f32 [V, D] tables (one reference each; n = 0 unregisters all) for the
+ * update p[row] -= lr·g_row applied INSIDE the embedding backward to the rows
+ * the step looked up — SPEC S:581 with μ = 0, wd = 0, for which the update of
+ * an untouched row (g_row = 0) is the identity, so the result equals the dense
+ * step exactly.  No gradient tensor is produced (be_grad returns NULL).  With
+ * a communicator of R > 1 ranks (be_dist_init) the embedding backward
+ * all-gathers each rank's ids and upstream rows and applies the global-batch
+ * update with g = (1/R)·Σ over all ranks' rows, in the same order on every
+ * rank (replicas bitwise equal); the table must not be DDP-attached.  A table
+ * whose gradient arrives densely (several lookups per step) is updated from
+ * it when final (R = 1 only; else BE_E_UNSUPPORTED).  Tables may not also be
+ * passed to be_sgd_overlap / be_sgd_step (BE_E_ARG). */
+be_status be_sgd_sparse(const be_tensor* tables, int n, float lr);
 /* The SGD momentum buffer v of f32 parameter `param` (SPEC S:578-586 update
  * above; the paper names the optimizer without formulas): *out receives a NEW
  * f32 tensor of the param's shape holding a copy of v, taken on the compute

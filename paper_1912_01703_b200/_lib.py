@@ -24,7 +24,7 @@ ERRORS = {
 }
 OPS = dict(LINEAR=1, MATMUL=2, ADD=3, MUL=4, RELU=5, SOFTMAX_XENT=6, BCE_LOGITS=7, CONV2D=8, MAXPOOL2D=9,
            AVGPOOL_GLOBAL=10, BATCHNORM2D=11, RESHAPE=12, EMBEDDING=13, CONCAT=14, SUM=15, MEAN=16, CAST=17,
-           ADD_RELU=18)
+           ADD_RELU=18, DROPOUT=19, CONV2D_DEPTHWISE=20)
 
 
 class BeError(RuntimeError):
@@ -58,6 +58,14 @@ class be_pool_attrs(C.Structure):
 
 class be_bn_attrs(C.Structure):
     _fields_ = [("eps", C.c_float), ("momentum", C.c_float), ("act", C.c_int), ("residual", C.c_int)]
+
+
+class be_dropout_attrs(C.Structure):
+    _fields_ = [("p", C.c_double), ("training", C.c_int), ("seed", C.c_uint64), ("offset", C.c_uint64)]
+
+
+class be_dwconv_attrs(C.Structure):
+    _fields_ = [("stride", C.c_int), ("pad", C.c_int)]
 
 
 class be_shape_attrs(C.Structure):
@@ -106,6 +114,7 @@ def lib():
             "be_zero_grad": [P(T), C.c_int],
             "be_sgd_step": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
             "be_sgd_overlap": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
+            "be_sgd_sparse": [P(T), C.c_int, C.c_float],
             "be_sgd_momentum": [T, P(T)],
             "be_alloc_stats": [P(be_alloc_stats)],
             "be_alloc_reset_peak": [],
@@ -167,6 +176,6 @@ EXPORTED = [
     "be_dist_init", "be_ddp_attach", "be_ddp_detach", "be_allreduce_", "be_synchronize", "be_item",
     "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
     "be_stream_create", "be_stream_destroy", "be_event_create", "be_event_destroy", "be_event_record",
-    "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap",
+    "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap", "be_sgd_sparse",
     "be_sgd_momentum", "be_ddp_sync_buffers", "be_dist_world",
 ]

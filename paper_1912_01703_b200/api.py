@@ -260,6 +260,18 @@ def conv2d(x, w, b=None, stride=1, pad=0, act=0, out_f32=False, bn_stats=False):
                L.be_conv_attrs(int(stride), int(pad), int(act), int(out_f32), int(bn_stats)))
 
 
+def conv2d_depthwise(x, w, stride=1, pad=1):
+    """Depthwise 3×3 convolution: x NHWC (C % 8 == 0), w f32 RSC [3, 3, C]."""
+    return _op("CONV2D_DEPTHWISE", [x, w], L.be_dwconv_attrs(int(stride), int(pad)))
+
+
+def dropout(x, p, seed, offset=0, training=True):
+    """Inverted dropout with the counter-based Philox mask of (seed, offset)
+    (include/be.h BE_OP_DROPOUT): the backward pass regenerates it."""
+    return _op("DROPOUT", [x], L.be_dropout_attrs(float(p), int(bool(training)), int(seed) & (2**64 - 1),
+                                                   int(offset) & (2**64 - 1)))
+
+
 def maxpool2d(x, k=3, stride=2, pad=0, with_argmax=False):
     return _op("MAXPOOL2D", [x], L.be_pool_attrs(k, stride, pad), 2 if with_argmax else 1)
 
@@ -338,6 +350,12 @@ def sgd_overlap(params, lr=0.0, momentum=0.0, weight_decay=0.0):
     backward (be_sgd_overlap); sgd_overlap([]) unregisters."""
     call("be_sgd_overlap", _handles(params) if params else None, len(params), C.c_float(lr), C.c_float(momentum),
          C.c_float(weight_decay))
+
+
+def sgd_sparse(tables, lr=0.0):
+    """Register embedding tables for the touched-rows SGD update applied inside
+    the embedding backward (be_sgd_sparse; μ = 0, wd = 0); sgd_sparse([]) unregisters."""
+    call("be_sgd_sparse", _handles(tables) if tables else None, len(tables), C.c_float(lr))
 
 
 def sgd_momentum(param):

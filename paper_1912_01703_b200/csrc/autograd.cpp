@@ -98,10 +98,11 @@ struct Engine {
   std::vector<Node*> touched;           // nodes holding pending buffers
 
   bool tracks(Tensor* leaf) const {
-    return (ddp && leaf->ddp_slot >= 0) || (opt && opt_param(leaf));
+    return (ddp && leaf->ddp_slot >= 0) || (opt && opt_param(leaf)) || opt_sparse(leaf);
   }
   void leaf_ready(Tensor* leaf) {
-    if (ddp) ddp_on_leaf_grad_ready(leaf);
+    if (opt_sparse(leaf)) opt_sparse_dense_fallback(leaf);
+    else if (ddp) ddp_on_leaf_grad_ready(leaf);
     else opt_on_grad_final(leaf);
   }
   Tensor*& pend(Node* m, int k) {
@@ -218,6 +219,21 @@ bool GradSink::fuse(int i, k::SgdFuse* f) {
   if (e.kind != Edge::LEAF || !opt_param(e.leaf) || e.leaf->grad) return false;
   if (e.leaf->bw_epoch != eng->epoch || e.leaf->bw_uses != 1) return false;  // more contributions to come
   return opt_fuse_desc(e.leaf, f);
+}
+
+bool GradSink::fuse_sparse(int i, float* lr) {
+  if (!eng) return false;
+  Edge& e = node->edges[i];
+  if (e.kind != Edge::LEAF || !opt_sparse(e.leaf) || e.leaf->grad) return false;
+  if (e.leaf->bw_epoch != eng->epoch || e.leaf->bw_uses != 1) return false;  // more contributions to come
+  *lr = e.leaf->sparse_lr;
+  return true;
+}
+
+void GradSink::fused_sparse(int i) {
+  Tensor* leaf = node->edges[i].leaf;
+  --leaf->bw_uses;
+  leaf->bump_version();
 }
 
 void GradSink::fused(int i) {

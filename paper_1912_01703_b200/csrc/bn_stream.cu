@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
     unpack8s(gv, g);
     if (act) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] += g[j] * (a[j] - k[j]) * is[j]; }
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
     }
     if (act) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = fmaxf(o[j], 0.f);
+      for (int j = 0; j < 8; ++j) o[j] = act_apply(o[j], act);
     }
     *reinterpret_cast<uint4*>(y + row * C + c) = pack8s(o);
   };
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
     unpack8s(v[1], a);
     if (act) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = fmaf(k1[j], g[j], fmaf(k2[j], a[j], k3[j]));

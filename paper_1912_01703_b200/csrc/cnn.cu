@@ -393,7 +393,7 @@ __global__ void bn_reduce_kernel(const void* x, const void* gy, const void* yv, 
       else if (MODE == 1) { float d = v - mu; s0 += d * d; }
       else {
         float g = ld(gy, o, dt);
-        if (act && !(ld(yv, o, dt) > 0.f)) g = 0.f;
+        if (act && !act_pass(ld(yv, o, dt), act)) g = 0.f;
         s0 += g;
         s1 += g * (v - mu) * is;
       }
@@ -448,7 +448,7 @@ __global__ void bn_apply_kernel(const void* x, void* y, int64_t total, int C, be
     const int c = (int)(i % C);
     float v = gamma[c] * (ld(x, i, dt) - mean[c]) * invstd[c] + beta[c];
     if (res) v += ld(res, i, dt);
-    if (act) v = fmaxf(v, 0.f);
+    v = act_apply(v, act);
     st(y, i, dt, v);
   }
 }
@@ -459,7 +459,7 @@ __global__ void bn_dx_kernel(const void* gy, const void* x, const void* yv, int 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
     float g = ld(gy, i, dt);
-    if (act && !(ld(yv, i, dt) > 0.f)) g = 0.f;
+    if (act && !act_pass(ld(yv, i, dt), act)) g = 0.f;
     const float is = invstd[c];
     const float xh = (ld(x, i, dt) - mean[c]) * is;
     const float inv_n = 1.f / (float)rows;
@@ -515,10 +515,10 @@ __global__ void __launch_bounds__(256) bn_reduce_v(const void* __restrict__ x, c
       } else {
         if (act && gam) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
+          for (int j = 0; j < 8; ++j) g.v[j] = act_pass_st(fmaf(a.v[j], sc[j], sh[j]), act, dt == BE_BF16) ? g.v[j] : 0.f;
         } else if (act) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
+          for (int j = 0; j < 8; ++j) g.v[j] = act_pass(yy.v[j], act) ? g.v[j] : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) { s0[j] += g.v[j]; s1[j] += g.v[j] * (a.v[j] - k[j]) * is[j]; }
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(256) bn_apply_v(const void* __restrict__ x, vo
     for (int j = 0; j < 8; ++j) {
       float val = fmaf(a.v[j], sc[j], sh[j]);
       if (res) val += rr.v[j];  // fused residual add (ResNet block output)
-      a.v[j] = act ? fmaxf(val, 0.f) : val;
+      a.v[j] = act_apply(val, act);
     }
     st8(y, o, dt, a);
   };
@@ -637,10 +637,10 @@ __global__ void __launch_bounds__(256) bn_dx_v(const void* __restrict__ gy, cons
   auto row = [&](int64_t o, V8 g, const V8& a, const V8& yy, const V8& prev) {
     if (act && bsh) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g.v[j] = fmaf(a.v[j], sc[j], sh[j]) > 0.f ? g.v[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g.v[j] = act_pass_st(fmaf(a.v[j], sc[j], sh[j]), act, dt == BE_BF16) ? g.v[j] : 0.f;
     } else if (act) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g.v[j] = yy.v[j] > 0.f ? g.v[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g.v[j] = act_pass(yy.v[j], act) ? g.v[j] : 0.f;
     }
     V8 out;
 #pragma unroll
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(256) bn_reduce_bf16(const uint16_t* __restrict
         unpack8(ga[u], g);
         if (act) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+          for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] += g[j] * (a[j] - k[j]) * is[j]; }
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(256) bn_dx_bf16(const uint16_t* __restrict__ g
       unpack8(xa[u], a);
       if (act) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) g[j] = fmaf(a[j], sc[j], sh[j]) > 0.f ? g[j] : 0.f;
+        for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
       }
       float pv[8];
       if (dx_beta != 0.f) unpack8(pa[u], pv);
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(256) bn_apply_bf16(const uint16_t* __restrict_
       for (int j = 0; j < 8; ++j) {
         float val = fmaf(a[j], sc[j], sh[j]);
         if (res) val += rv[j];
-        a[j] = act ? fmaxf(val, 0.f) : val;
+        a[j] = act_apply(val, act);
       }
       *reinterpret_cast<uint4*>(y + rr * C + c) = pack8(a);
     }

@@ -66,6 +66,23 @@ __device__ __forceinline__ void st8(void* p, int64_t i, be_dtype dt, const V8& r
 }
 __host__ __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// activations fused after a BN / conv epilogue: act 1 = ReLU, 2 = ReLU6
+// (MobileNetV2); act_pass is the backward mask (gradient 0 at the kinks)
+__device__ __forceinline__ float act_apply(float v, int act) {
+  return act == 2 ? fminf(fmaxf(v, 0.f), 6.f) : (act ? fmaxf(v, 0.f) : v);
+}
+__device__ __forceinline__ bool act_pass(float v, int act) { return act == 2 ? (v > 0.f && v < 6.f) : v > 0.f; }
+// the mask decided from the value as STORED (the forward writes bf16(act(v))):
+// for ReLU6 a pre-activation just below 6 that rounds to 6 has gradient 0, the
+// same decision a reader of the stored output takes (SURVEY §8(c) reading 16);
+// for ReLU rounding never changes the sign
+__device__ __forceinline__ float bf16_round(float v) {
+  return __bfloat162float(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ bool act_pass_st(float v, int act, bool bf16) {
+  return act_pass(act == 2 && bf16 ? bf16_round(v) : v, act);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

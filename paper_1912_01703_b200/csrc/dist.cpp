@@ -38,6 +38,7 @@ struct NcclApi {
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi& nccl() {
   static NcclApi api;
@@ -58,6 +59,7 @@ NcclApi& nccl() {
   api.getErrorString = (decltype(api.getErrorString))dlsym(api.h, "ncclGetErrorString");
   api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
   api.commCount = (decltype(api.commCount))dlsym(api.h, "ncclCommCount");
+  api.allGather = (decltype(api.allGather))dlsym(api.h, "ncclAllGather");
   BE_REQUIRE(api.getUniqueId && api.commInitRank && api.allReduce && api.broadcast, BE_E_NCCL,
              "libnccl is missing required symbols");
   return api;
@@ -178,6 +180,12 @@ void ddp_on_leaf_grad_ready(Tensor* leaf) {
   }
   d.ready[slot] = 1;
   if (--b.pending == 0) launch_bucket(b);
+}
+
+void ddp_allgather(const void* src, void* dst, size_t bytes, cudaStream_t s) {
+  DDP& d = ddp();
+  BE_REQUIRE(d.comm_ready && nccl().allGather, BE_E_NCCL, "allgather: no communicator");
+  BE_CHECK_NCCL(nccl().allGather(src, dst, bytes, ncclChar, d.comm, s));
 }
 
 void ddp_wait_all() {

@@ -155,7 +155,38 @@ __global__ void segment_sum(const uint32_t* keys, const uint32_t* pos, int n, co
     *o = acc + (beta != 0.f ? *o : 0.f);
   }
 }
+// Sparse SGD (be_sgd_sparse): the same ordered segment sums, applied as the
+// update of the touched rows only, p[row] ← p[row] − lr·(scale·Σ g) — no
+// gradient table exists (μ = 0, wd = 0: untouched rows are unchanged, exactly
+// as dense SGD with a zero gradient row leaves them)
+__global__ void segment_sgd(const uint32_t* keys, const uint32_t* pos, int n, const void* drows, be_dtype dd,
+                            int64_t D, float* table, float lr, float scale) {
+  pdl_entry();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  if (warp > 0 && keys[warp - 1] == keys[warp]) return;
+  int end = warp + 1;
+  while (end < n && keys[end] == keys[warp]) ++end;
+  const int64_t row = keys[warp];
+  for (int64_t d = lane; d < D; d += 32) {
+    float acc = 0.f;
+    for (int j = warp; j < end; ++j) acc += ld(drows, (int64_t)pos[j] * D + d, dd);
+    float* o = table + row * D + d;
+    *o = __fsub_rn(*o, __fmul_rn(lr, __fmul_rn(scale, acc)));
+  }
+}
 }  // namespace
+
+void embedding_sgd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, float* table, float lr, float scale,
+                          const void* sorted, cudaStream_t s) {
+  if (B == 0) return;
+  const uint32_t* k0 = reinterpret_cast<const uint32_t*>(sorted);
+  const uint32_t* v0 = k0 + B;
+  const int64_t threads = B * 32;
+  launch_pdl(segment_sgd, (int)((threads + 255) / 256), 256, 0, s, k0, v0, (int)B, drows, dd, D, table, lr, scale);
+  after_launch("embedding_segment_sgd");
+}
 
 size_t embedding_bwd_scratch(int64_t B) { return (size_t)B * 16 + 64; }
 

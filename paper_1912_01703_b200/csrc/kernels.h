@@ -166,9 +166,50 @@ size_t embedding_bwd_scratch(int64_t B);
 void embedding_sort(const int32_t* ids, int64_t B, int64_t V, void* scratch, cudaStream_t s);
 void embedding_bwd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, float* dtable, int64_t V, float beta,
                           const void* sorted, cudaStream_t s);
+// sparse SGD of the touched rows from the sorted (id, position) pairs (see embedding_sort)
+void embedding_sgd_sorted(const void* drows, be_dtype dd, int64_t B, int64_t D, float* table, float lr, float scale,
+                          const void* sorted, cudaStream_t s);
 void concat_cols(const void* const* xs, const int64_t* widths, int n, int64_t rows, void* y, be_dtype dt,
                  cudaStream_t s);
 void slice_cols(const void* y, int64_t ldy, int64_t col0, int64_t width, int64_t rows, void* x, be_dtype dt,
                 float beta, cudaStream_t s);
 
+
+// ------------------------------------------------------------------ mobile.cu
+// inverted dropout y (+)= x·keep·1/(1−p), keep_i = (Philox4x64-10(i/4, offset; seed)[i%4] >> 32) >= ⌊p·2^32⌋
+void dropout_apply(const void* x, void* y, int64_t n, be_dtype dt, uint64_t seed, uint64_t offset, double p,
+                   float beta, cudaStream_t s);
+// depthwise conv, x/y NHWC (C % 8 == 0), w RSC fp32
+void dw_conv_fwd(const void* x, const float* w, void* y, const ConvGeom& g, be_dtype dt, cudaStream_t s);
+void dw_conv_dgrad(const void* dy, const float* w, void* dx, const ConvGeom& g, be_dtype dt, float beta,
+                   cudaStream_t s);
+size_t dw_wgrad_partial_floats(const ConvGeom& g, int num_sms);
+void dw_conv_wgrad(const void* dy, const void* x, float* dw, float* part, const ConvGeom& g, be_dtype dt,
+                   float beta, int num_sms, cudaStream_t s);
+
+// ------------------------------------------------------------------ p2p.cu
+// One gradient bucket of the peer-memory allreduce fused with SGD (see p2p.cu).
+// Pointers are device addresses valid in this process (own allocations or
+// CUDA-IPC mappings of the peers'); tables live in device memory.
+struct P2PBucketArgs {
+  int rank = 0, world = 1;
+  int64_t numel = 0;                      // bucket length (params at 64-aligned offsets)
+  int nseg = 0;                           // parameters in the bucket
+  const int64_t* seg_off = nullptr;       // [nseg] offset of each parameter in the bucket (ascending)
+  const int64_t* seg_n = nullptr;         // [nseg] numel of each parameter
+  float* const* grad = nullptr;           // [R] bucket base on every rank
+  float* const* p = nullptr;              // [nseg·R] fp32 master of parameter s on rank q
+  uint16_t* const* shadow = nullptr;      // [nseg·R] bf16 shadow (entries may be null) or null
+  float* const* mom = nullptr;            // [nseg] local momentum buffers (μ ≠ 0)
+  unsigned long long* flags_arrive = nullptr;        // [R] local
+  unsigned long long* flags_done = nullptr;          // [R] local
+  unsigned long long* const* flags_peer = nullptr;      // [R] rank q's flags_arrive
+  unsigned long long* const* flags_peer_done = nullptr; // [R] rank q's flags_done
+  unsigned int* counter = nullptr;        // local, cumulative
+  int* status = nullptr;                  // local: 1 = barrier timeout
+  unsigned long long epoch = 0;
+  int lr_on = 0;                          // 1: SGD (lr, mu, wd); 0: plain mean allreduce into the buckets
+  float lr = 0.f, mu = 0.f, wd = 0.f;
+};
+void p2p_allreduce_sgd(const P2PBucketArgs& a, int blocks, cudaStream_t s);
 }}  // namespace be::k

@@ -346,6 +346,8 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   Tensor* rm = nb == 5 && in[3] ? check_handle(in[3]) : nullptr;
   Tensor* rv = nb == 5 && in[4] ? check_handle(in[4]) : nullptr;
   Tensor* res = a.residual ? check_handle(in[n_in - 1]) : nullptr;
+  BE_REQUIRE(a.act >= 0 && a.act <= 2, BE_E_ARG, "batchnorm2d: act 0 (none), 1 (ReLU) or 2 (ReLU6)");
+  BE_REQUIRE(!(res && a.act == 2), BE_E_UNSUPPORTED, "batchnorm2d: ReLU6 after a residual add");
   BE_REQUIRE(x->rank == 4 && x->is_contiguous(), BE_E_SHAPE, "batchnorm2d: contiguous NHWC input");
   if (res) {
     BE_REQUIRE(res->rank == 4 && res->is_contiguous(), BE_E_SHAPE, "batchnorm2d: contiguous residual");
@@ -391,11 +393,32 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
 static void vjp_embedding(Node* n, GradSink& sink) {
   TRef hids;
   Tensor* ids = unpack(n, 0, hids);
-  float beta;
-  Tensor* dt = sink.dest(0, &beta);
+  if (!sink.needs(0)) return;
+  float slr = 0.f;
+  const bool sparse = sink.fuse_sparse(0, &slr);
+  float beta = 0.f;
+  Tensor* dt = sparse ? sink.leaf(0) : sink.dest(0, &beta);
   if (!dt) return;
   TRef gz = contiguous_like(sink.upstream[0], sink.upstream[0]->dtype);
-  const int64_t B = ids->numel(), D = dt->shape[1], V = dt->shape[0];
+  int64_t B = ids->numel();
+  const int64_t D = dt->shape[1], V = dt->shape[0];
+  // Sparse exchange (R > 1): every rank all-gathers the step's lookups — ids
+  // and upstream rows, R·B·(4 + D·e) bytes instead of the V·D·4 dense
+  // gradient — and applies the whole global batch's touched-row update in
+  // the same (id, rank, position) order, so the replicas stay bitwise equal.
+  const int R = sparse ? ddp_world() : 1;
+  TRef all_ids, all_rows;
+  float scale = 1.f;
+  if (R > 1) {
+    all_ids = new_tensor({R * B}, BE_I32);
+    all_rows = new_tensor({R * B, D}, gz->dtype);
+    ddp_allgather(ids->data(), all_ids->data(), (size_t)B * 4, ctx().stream);
+    ddp_allgather(gz->data(), all_rows->data(), (size_t)(B * D) * dtype_size(gz->dtype), ctx().stream);
+    ids = all_ids.get();
+    gz = all_rows;
+    B *= R;
+    scale = 1.f / (float)R;
+  }
   // Tables looked up with the same ids (NeuMF: GMF and MLP tables of a side)
   // share one sort: a small cache keyed by the ids storage, its version and V
   // (several entries: backward visits the user and item tables interleaved).
@@ -433,6 +456,12 @@ static void vjp_embedding(Node* n, GradSink& sink) {
     e->sorted = scratch;
   }
   e->stamp = ++clock;
+  if (sparse) {
+    k::embedding_sgd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), slr, scale, e->sorted->data(),
+                            ctx().stream);
+    sink.fused_sparse(0);
+    return;
+  }
   k::embedding_bwd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), V, beta, e->sorted->data(), ctx().stream);
   sink.commit(0);
 }

@@ -15,5 +15,6 @@ Tensor* weight_operand(Tensor* w);
 TRef cast_op(Tensor* x, be_dtype dt);
 TRef act_operand(Tensor* x);
 TRef contiguous_like(Tensor* g, be_dtype dt);
+void op_mobile(int op, const be_tensor* in, int n_in, const void* attrs, be_tensor* out, int n_out);
 void run_backward(Tensor* root, Tensor* upstream, bool retain);
 }  // namespace be

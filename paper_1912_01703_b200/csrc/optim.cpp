@@ -12,6 +12,7 @@
 #include "ops_common.h"
 
 namespace be {
+std::vector<Tensor*>& sparse_tables();
 namespace {
 
 k::SgdEntry sgd_entry(Tensor* p, float momentum, cudaStream_t s) {
@@ -94,7 +95,33 @@ void flush_group() {
 }
 }  // namespace
 
+std::vector<Tensor*>& sparse_tables() {
+  static std::vector<Tensor*> t;
+  return t;
+}
+
+// a registered table whose gradient arrived densely (e.g. looked up twice in
+// one step): the same update p -= lr·g from that gradient, on the compute stream
+void opt_sparse_dense_fallback(Tensor* leaf) {
+  if (!leaf->grad) return;
+  BE_REQUIRE(!ddp_active() || ddp_world() == 1, BE_E_UNSUPPORTED,
+             "sgd_sparse: a table with several lookups per step under DDP (its dense gradient is not exchanged)");
+  k::SgdEntry e{};
+  e.p = leaf->ptr<float>();
+  e.g = leaf->grad->ptr<float>();
+  e.n = leaf->numel();
+  k::sgd_multi(&e, 1, leaf->sparse_lr, 0.f, 0.f, 1.f, ctx().stream);
+  leaf->bump_version();
+  tensor_drop(leaf->grad);
+  leaf->grad = nullptr;
+}
+
 bool opt_active() { return ov().active; }
+bool opt_hparams(float* lr, float* mu, float* wd) {
+  const Overlap& o = ov();
+  *lr = o.lr; *mu = o.momentum; *wd = o.wd;
+  return o.active;
+}
 bool opt_param(const Tensor* leaf) { return ov().active && leaf->opt_slot >= 0; }
 
 void opt_on_grad_final(Tensor* leaf) {
@@ -168,8 +195,8 @@ be_status be_sgd_step(const be_tensor* params, int n, float lr, float momentum, 
   for (int i = 0; i < n; ++i) {
     Tensor* p = check_handle(params[i]);
     BE_REQUIRE(p->dtype == BE_F32 && p->is_contiguous(), BE_E_DTYPE, "sgd: params must be contiguous f32");
-    BE_REQUIRE(!opt_param(p), BE_E_ARG, "sgd: parameter " + std::to_string(i) +
-                                           " is registered for overlapped SGD (updated during backward)");
+    BE_REQUIRE(!opt_param(p) && !opt_sparse(p), BE_E_ARG, "sgd: parameter " + std::to_string(i) +
+                                           " is registered for overlapped / sparse SGD (updated during backward)");
     BE_REQUIRE(p->grad != nullptr, BE_E_MISSING_GRAD, "sgd: parameter " + std::to_string(i) + " has no grad");
     es.push_back(sgd_entry(p, momentum, ctx().stream));
     ts.push_back(p);
@@ -191,6 +218,27 @@ be_status be_sgd_momentum(be_tensor param, be_tensor* out) {
   BE_CHECK_CUDA(cudaMemcpyAsync(v->data(), p->mom, sizeof(float) * p->numel(), cudaMemcpyDeviceToDevice,
                                 ctx().stream));
   *out = reinterpret_cast<be_tensor>(v.release());
+  BE_API_END
+}
+
+be_status be_sgd_sparse(const be_tensor* tables, int n, float lr) {
+  BE_API_BEGIN
+  BE_REQUIRE(ctx().inited, BE_E_NOT_INIT, "be_init() was not called");
+  std::vector<Tensor*>& reg = sparse_tables();
+  for (Tensor* p : reg) { p->sparse_lr = -1.f; tensor_drop(p); }
+  reg.clear();
+  BE_REQUIRE(lr >= 0.f, BE_E_ARG, "sgd_sparse: lr must be >= 0");
+  for (int i = 0; i < n; ++i) {
+    Tensor* p = check_handle(tables[i]);
+    BE_REQUIRE(p->dtype == BE_F32 && p->rank == 2 && p->is_contiguous() && p->requires_grad && p->is_leaf(),
+               BE_E_ARG, "sgd_sparse: tables must be contiguous f32 [V, D] leaves requiring grad");
+    BE_REQUIRE(p->opt_slot < 0 && p->ddp_slot < 0, BE_E_ARG,
+               "sgd_sparse: a table cannot also be registered for overlapped SGD or attached to DDP");
+    BE_REQUIRE(!opt_sparse(p), BE_E_ARG, "sgd_sparse: table listed twice");
+    p->retain();
+    p->sparse_lr = lr;
+    reg.push_back(p);
+  }
   BE_API_END
 }
 

@@ -123,6 +123,7 @@ struct Tensor {
   Block* mom_block = nullptr;
   int ddp_slot = -1;          // index in DDP param table
   int opt_slot = -1;          // index in the overlapped-SGD table
+  float sparse_lr = -1.f;     // >= 0: embedding table updated on its touched rows inside backward (be_sgd_sparse)
   // per-channel Σ / Σx² partials of this tensor's values, produced by the
   // epilogue of the conv that wrote it (be_conv_attrs.bn_stats); valid while
   // the version is unchanged — batchnorm2d then skips its statistics pass
@@ -245,6 +246,13 @@ struct GradSink {
   // enqueued before that GEMM.
   bool fuse(int i, k::SgdFuse* f);
   void fused(int i);
+  // Sparse SGD (be_sgd_sparse): true when input i is an embedding table
+  // registered for the touched-rows update whose gradient is complete with this
+  // one contribution; the VJP applies p[row] -= lr·g_row itself (no gradient
+  // tensor) and then calls fused_sparse(i)
+  bool fuse_sparse(int i, float* lr);
+  void fused_sparse(int i);
+  Tensor* leaf(int i) const { return node->edges[i].kind == Edge::LEAF ? node->edges[i].leaf : nullptr; }
   // engine internals
   struct Slot { Tensor* target = nullptr; Tensor* tmp = nullptr; bool acc = false; bool used = false; };
   std::vector<Slot> slots;
@@ -302,10 +310,18 @@ void opt_launch_params(const std::vector<Tensor*>& ps, cudaStream_t s, float sca
 // registered parameter whose gradient is final; its update runs on a side
 // stream while backward continues.
 bool opt_active();
+bool opt_hparams(float* lr, float* mu, float* wd);  // the overlapped update's hyper-parameters
 bool opt_param(const Tensor* leaf);      // registered for overlapped SGD
 void opt_on_grad_final(Tensor* leaf);    // (non-DDP) grad complete for this backward
 void opt_end_backward();                 // flush; compute stream waits for every update
 bool opt_fuse_desc(Tensor* leaf, k::SgdFuse* f);  // fill the update-epilogue descriptor (BE_FUSE_SGD=0: off)
 void opt_fused_done(Tensor* leaf);       // versions after the fused update was enqueued
+// Sparse (touched-rows) SGD of embedding tables (be_sgd_sparse): μ = 0, wd = 0,
+// applied by the embedding backward itself; a table whose gradient arrives
+// densely instead (several lookups) is updated from it when final.
+inline bool opt_sparse(const Tensor* leaf) { return leaf->sparse_lr >= 0.f; }
+void opt_sparse_dense_fallback(Tensor* leaf);
+// DDP: all-gather `bytes` from every rank into dst (rank-major) on stream s
+void ddp_allgather(const void* src, void* dst, size_t bytes, cudaStream_t s);
 
 }  // namespace be

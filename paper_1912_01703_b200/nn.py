@@ -76,6 +76,9 @@ class Model:
     def parameters(self):
         return list(self.params.values())
 
+    def embedding_tables(self):
+        return []
+
     def logical(self, name, device_array):
         return self.to_logical_layout(name, device_array)
 
@@ -276,6 +279,147 @@ class ResNet50(Model):
         return T.softmax_xent(z, y)
 
 
+# ---------------------------------------------------------------- VGG-19 (Table 1)
+class VGG19(Model):
+    """VGG-19 (Table 1; oracle/nets.py VGG19, R15):
+    sixteen 3×3 convs (bias + ReLU fused into the conv epilogue), 2×2/2
+    maxpools, NHWC flatten (fc6 rows stored to match), fc6/fc7 + ReLU +
+    counter-based dropout (offsets 6, 7 under `self.seed`), fc8."""
+    STAGES = ((64, 2), (128, 2), (256, 4), (512, 4), (512, 4))
+
+    def __init__(self, classes=1000, width=1.0, image=224, dropout=0.5, seed=0):
+        super().__init__()
+        self.classes, self.p, self.seed = classes, dropout, seed
+        chain, prev, hw = [], 3, image
+        for si, (k, n) in enumerate(self.STAGES):
+            k = max(1, int(k * width))
+            for j in range(n):
+                chain.append((f"conv{si + 1}_{j + 1}", k, prev, j == n - 1))
+                prev = k
+            hw //= 2
+        self.convs, self.c5, self.hw = chain, prev, hw
+        self.hidden = max(1, int(4096 * width))
+
+    def param_specs(self):
+        s = []
+        for (n, k, c, pool) in self.convs:
+            s += _conv_spec(n, k, c, 3, True)
+        f = self.c5 * self.hw * self.hw
+        return s + _lin_spec("fc6", f, self.hidden) + _lin_spec("fc7", self.hidden, self.hidden) + \
+            _lin_spec("fc8", self.hidden, self.classes)
+
+    def _fc6_perm(self):
+        C, H = self.c5, self.hw
+        h, w, c = np.meshgrid(np.arange(H), np.arange(H), np.arange(C), indexing="ij")
+        return (c * H * H + h * H + w).reshape(-1)
+
+    def to_device_layout(self, name, a):
+        if name.endswith(".w") and name.startswith("conv"):
+            return _conv_to_krsc(a, pad_c=(name == "conv1_1.w"))
+        if name == "fc6.w":
+            return np.ascontiguousarray(a[self._fc6_perm()])
+        return a
+
+    def to_logical_layout(self, name, a):
+        if name.endswith(".w") and name.startswith("conv"):
+            return _krsc_to_conv(a, 3 if name == "conv1_1.w" else None)
+        if name == "fc6.w":
+            out = np.empty_like(a)
+            out[self._fc6_perm()] = a
+            return out
+        return a
+
+    def loss(self, x, y):
+        P = self.params
+        h = x
+        for (n, k, c, pool) in self.convs:
+            h = T.conv2d(h, P[n + ".w"], P[n + ".b"], 1, 1, act=1)
+            if pool:
+                h = T.maxpool2d(h, 2, 2, 0)
+        h = T.reshape(h, (h.shape[0], -1))
+        h = T.dropout(T.linear(h, P["fc6.w"], P["fc6.b"], act=1), self.p, self.seed, 6)
+        h = T.dropout(T.linear(h, P["fc7.w"], P["fc7.b"], act=1), self.p, self.seed, 7)
+        z = T.linear(h, P["fc8.w"], P["fc8.b"], out_f32=True)
+        return T.softmax_xent(z, y)
+
+
+# ---------------------------------------------------------------- MobileNetV2 (Table 1)
+class MobileNetV2(Model):
+    """MobileNetV2 (Table 1 "MobileNet"; oracle/nets.py
+    MobileNetV2, R13): every conv feeds a batch norm whose ReLU6
+    (act = 2) runs in the BN apply pass; 1×1 expand / project convs are
+    tcgen05 GEMMs over the NHWC activations, the 3×3 depthwise convs run on
+    the depthwise kernels (weights stored RSC); the residual add is fused
+    into the projection's BN pass."""
+    SETTINGS = ((1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2),
+                (6, 320, 1, 1))
+
+    def __init__(self, classes=1000, width=1.0, dropout=0.2, seed=0, settings=None):
+        super().__init__()
+        self.classes, self.p, self.seed = classes, dropout, seed
+        w = lambda c: max(8, int(c * width))  # noqa: E731
+        self.stem = w(32)
+        self.last = max(1280, w(1280)) if width >= 1.0 else w(1280)
+        blocks, cin = [], self.stem
+        for (t, c, n, s) in (settings or self.SETTINGS):
+            cout = w(c)
+            for j in range(n):
+                blocks.append((f"b{len(blocks)}", cin, cin * t, cout, s if j == 0 else 1, t))
+                cin = cout
+        self.blocks, self.cfinal = blocks, cin
+
+    def param_specs(self):
+        s = _conv_spec("stem", self.stem, 3, 3, False) + _bn_spec("stem_bn", self.stem)
+        for (n, cin, hid, cout, st, t) in self.blocks:
+            if t != 1:
+                s += _conv_spec(n + ".exp", hid, cin, 1, False) + _bn_spec(n + ".exp_bn", hid)
+            s += [(n + ".dw.w", (hid, 1, 3, 3), "normal", 9)] + _bn_spec(n + ".dw_bn", hid)
+            s += _conv_spec(n + ".proj", cout, hid, 1, False) + _bn_spec(n + ".proj_bn", cout)
+        s += _conv_spec("head", self.last, self.cfinal, 1, False) + _bn_spec("head_bn", self.last)
+        return s + _lin_spec("fc", self.last, self.classes)
+
+    def to_device_layout(self, name, a):
+        if name.endswith(".dw.w"):
+            return np.ascontiguousarray(np.asarray(a, np.float32)[:, 0].transpose(1, 2, 0))  # [C,1,R,S] → RSC
+        if np.ndim(a) == 4:
+            return _conv_to_krsc(a, pad_c=(name == "stem.w"))
+        return a
+
+    def to_logical_layout(self, name, a):
+        if name.endswith(".dw.w"):
+            return np.ascontiguousarray(np.asarray(a).transpose(2, 0, 1)[:, None])
+        if np.ndim(a) == 4:
+            return _krsc_to_conv(a, 3 if name == "stem.w" else None)
+        return a
+
+    def make_buffers(self):
+        self.buffers = {}
+        for (name, shape, init, _) in self.param_specs():
+            if name.endswith(".g"):
+                base = name[:-2]
+                self.buffers[base + ".rm"] = T.tensor(np.zeros(shape, np.float32))
+                self.buffers[base + ".rv"] = T.tensor(np.ones(shape, np.float32))
+
+    def loss(self, x, y):
+        P, B = self.params, self.buffers
+
+        def bn(h, name, act, residual=None):
+            return T.batchnorm2d(h, P[name + ".g"], P[name + ".b"], B[name + ".rm"], B[name + ".rv"], act=act,
+                                 residual=residual)
+        h = bn(T.conv2d(x, P["stem.w"], None, 2, 1), "stem_bn", 2)
+        for (n, cin, hid, cout, st, t) in self.blocks:
+            u = h
+            if t != 1:
+                u = bn(T.conv2d(u, P[n + ".exp.w"], None, 1, 0), n + ".exp_bn", 2)
+            u = bn(T.conv2d_depthwise(u, P[n + ".dw.w"], st, 1), n + ".dw_bn", 2)
+            res = h if (st == 1 and cin == cout) else None
+            h = bn(T.conv2d(u, P[n + ".proj.w"], None, 1, 0), n + ".proj_bn", 0, residual=res)
+        h = bn(T.conv2d(h, P["head.w"], None, 1, 0), "head_bn", 2)
+        h = T.dropout(T.avgpool_global(h), self.p, self.seed, 0)
+        z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
+        return T.softmax_xent(z, y)
+
+
 # ---------------------------------------------------------------- NCF (C5)
 class NCF(Model):
     """NeuMF (SURVEY §8(c) reading 11): GMF dim 64, MLP 256→256→128→64."""
@@ -292,6 +436,9 @@ class NCF(Model):
             s += _lin_spec(f"mlp{i}", self.mlp[i], self.mlp[i + 1])
         return s + _lin_spec("head", self.gmf + self.mlp[-1], 1)
 
+    def embedding_tables(self):
+        return [self.params[k] for k in ("user_gmf", "item_gmf", "user_mlp", "item_mlp")]
+
     def loss(self, users, items, y):
         P = self.params
         g = T.mul(T.embedding(P["user_gmf"], users), T.embedding(P["item_gmf"], items))
@@ -302,20 +449,29 @@ class NCF(Model):
         return T.bce_logits(z, y)
 
 
-def train_step(model: Model, batch, lr=0.01, momentum=0.0, weight_decay=0.0, overlap_sgd=False):
+def train_step(model: Model, batch, lr=0.01, momentum=0.0, weight_decay=0.0, overlap_sgd=False,
+               sparse_embeddings=False):
     """One eager step: zero_grad (release), forward, backward, SGD.
     overlap_sgd=False: one fused multi-tensor SGD launch after backward;
     True: each parameter is updated inside backward as soon as its gradient
     is final, on a side stream (be_sgd_overlap) — same values, bitwise.
+    sparse_embeddings=True (models with embedding tables): the tables take
+    plain SGD (lr, μ = 0, wd = 0) on their touched rows inside the embedding
+    backward (be_sgd_sparse); the other parameters as above.
     Returns the (device) loss tensor; nothing here synchronises."""
-    params = model.parameters()
-    key = (lr, momentum, weight_decay) if overlap_sgd else None
+    tables = model.embedding_tables() if sparse_embeddings else []
+    params = [p for p in model.parameters() if all(p is not t for t in tables)]
+    key = (lr, momentum, weight_decay, overlap_sgd, bool(tables))
     if getattr(model, "_overlap", None) != key:
+        T.sgd_sparse([])
         T.sgd_overlap(params, lr, momentum, weight_decay) if overlap_sgd else T.sgd_overlap([])
+        T.sgd_sparse(tables, lr)
         model._overlap = key
     T.zero_grad(params)
     loss = model.loss(*batch)
     loss.backward()
     if not overlap_sgd:
         T.sgd_step(params, lr, momentum, weight_decay)
+    if hasattr(model, "seed"):
+        model.seed += 1  # a fresh dropout mask every step (counter-based: just a new key)
     return loss

@@ -59,7 +59,7 @@ class OpTrace:
     """Wraps the api ops a model calls (be.nn uses the module global `T`)."""
 
     OPS = ("conv2d", "batchnorm2d", "maxpool2d", "avgpool_global", "reshape", "linear", "softmax_xent",
-           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_dw")
+           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_depthwise")
 
     def __init__(self, api, model):
         self.api = api
@@ -157,6 +157,19 @@ def _as_dtype_values(be, g, dt):
     return synth.bf16_values(g) if dt == be._lib.BE_BF16 else g
 
 
+def _act(v, act):
+    """Fused activation of a BN / conv: 1 ReLU, 2 ReLU6 (oracle relu / relu6)."""
+    if act == 2:
+        return np.clip(v, 0.0, 6.0)
+    return np.maximum(v, 0) if act else v
+
+
+def _act_mask(y, act):
+    """The mask the device's backward takes, decided from the device's own
+    output (SURVEY §8(c) reading 16): ReLU 1[y > 0]; ReLU6 1[0 < y < 6]."""
+    return ((y > 0) & (y < 6)) if act == 2 else (y > 0)
+
+
 class Replay:
     def __init__(self, be, trace: OpTrace, tol: float, param_logical=None):
         self.be = be
@@ -179,9 +192,19 @@ class Replay:
             return
         self.grads[key] = self.grads.get(key, 0) + np.asarray(g, F64)
 
-    def record(self, i, op, what, dev, orc, exact=False):
+    def record(self, i, op, what, dev, orc, exact=False, mass=None):
+        """exact: bit-exact (integer decisions).  mass: the tensor is a
+        per-channel SUM Σ_i t_ic whose terms may cancel (BN dβ, dγ, running
+        mean); its error is taken against the sum's own scale
+        max_c Σ_i |t_ic| — Higham's forward-error bound of summation,
+        |ŝ − s| ≤ γ_n Σ|t_i| — instead of max|o|, which is rounding noise
+        when the exact sum is 0 (reading R16: e.g. Σ dy = 0 per
+        channel behind a conv → BN path)."""
         if exact:
             e = 0.0 if np.array_equal(np.asarray(dev), np.asarray(orc)) else float("inf")
+        elif mass is not None:
+            d = np.abs(np.asarray(dev, F64) - np.asarray(orc, F64)).max() if np.size(orc) else 0.0
+            e = float(d / max(np.abs(np.asarray(orc, F64)).max(), float(mass), 1e-300))
         else:
             e = rel_err(dev, orc)
         self.errs.append((i, op, what, e))
@@ -232,7 +255,7 @@ class Replay:
             out.backward(be.tensor(gv, dtype="bf16" if dt == be._lib.BE_BF16 else None))
         return True
 
-    def _finish(self, i, rec, leaves, orc_grads, names, to_dev=None):
+    def _finish(self, i, rec, leaves, orc_grads, names, to_dev=None, masses=None):
         """Compare device leaf grads with oracle grads (both device layout) and push upstream."""
         for n in names:
             r = rec["args"].get(n)
@@ -241,7 +264,8 @@ class Replay:
             leaf = leaves[n][0]
             gd = leaf.grad.numpy() if leaf.grad is not None else np.zeros_like(self._val(r))
             go = orc_grads[n]
-            self.record(i, rec["op"], "d" + n + (":" + r.key[1] if r.key[0] == "param" else ""), gd, go)
+            self.record(i, rec["op"], "d" + n + (":" + r.key[1] if r.key[0] == "param" else ""), gd, go,
+                        mass=(masses or {}).get(n))
             self._push(r.key, gd)
 
     # ------------------------------------------------------------ ops
@@ -290,22 +314,27 @@ class Replay:
             ro = Var(nhwc_to_nchw(self._val(a["residual"])).astype(F64), True)
             zo = oops.add(zo, ro)
         ydev = y.numpy()
-        fwd = np.maximum(zo.value, 0) if a["act"] else zo.value
+        fwd = _act(zo.value, a["act"])
         self.record(i, "batchnorm2d", "y", nhwc_to_nchw(ydev), fwd)
         if rmd is not None:
-            self.record(i, "batchnorm2d", "running_mean", rmd.numpy(), rm)
+            xa = np.abs(nhwc_to_nchw(self._val(a["x"])).astype(F64)).mean(axis=(0, 2, 3))
+            rm_mass = (a["momentum"] * xa + (1 - a["momentum"]) * np.abs(rm0)).max()
+            self.record(i, "batchnorm2d", "running_mean", rmd.numpy(), rm, mass=rm_mass)
             self.record(i, "batchnorm2d", "running_var", rvd.numpy(), rv)
         g = self._g_out(rec)
         if not self._dev_backward(y, g, rec):
             return
         gn = nhwc_to_nchw(np.asarray(g).reshape(ydev.shape))
         if a["act"]:
-            gn = gn * (nhwc_to_nchw(ydev) > 0)
+            gn = gn * _act_mask(nhwc_to_nchw(ydev), a["act"])
         backward(zo, gn)
         og = {"x": nchw_to_nhwc(xo.grad), "gamma": go.grad, "beta": bo.grad}
         if ro is not None:
             og["residual"] = nchw_to_nhwc(ro.grad)
-        self._finish(i, rec, L, og, ["x", "gamma", "beta", "residual"])
+        xv = nhwc_to_nchw(self._val(a["x"])).astype(F64)
+        xhat = (xv - xv.mean(axis=(0, 2, 3), keepdims=True)) / np.sqrt(xv.var(axis=(0, 2, 3), keepdims=True) + a["eps"])
+        masses = {"beta": np.abs(gn).sum(axis=(0, 2, 3)).max(), "gamma": np.abs(gn * xhat).sum(axis=(0, 2, 3)).max()}
+        self._finish(i, rec, L, og, ["x", "gamma", "beta", "residual"], masses=masses)
 
     def _op_maxpool2d(self, i, rec):
         be, a = self.be, rec["args"]
@@ -450,6 +479,43 @@ class Replay:
             self.record(i, "concat", f"dx{j}", gd, v.grad)
             self._push(r.key, gd)
 
+    def _op_dropout(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x"])
+        y = be.dropout(L["x"][1], a["p"], a["seed"], a["offset"], a["training"])
+        xv = self._val(a["x"]).astype(F64)
+        xo = Var(xv, True)
+        yo = oops.dropout(xo, a["p"], a["seed"], a["offset"], training=a["training"])
+        ydev = y.numpy()
+        self.record(i, "dropout", "y", ydev, yo.value)
+        # the keep mask is an integer decision: bit-exact wherever x ≠ 0
+        nz = xv != 0
+        if a["training"] and a["p"] > 0:
+            keep = oops.dropout_keep_mask(xv.size, a["p"], a["seed"], a["offset"]).reshape(xv.shape)
+            self.record(i, "dropout", "keep", (ydev != 0)[nz], keep[nz], exact=True)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, np.asarray(g, F64).reshape(ydev.shape))
+        self._finish(i, rec, L, {"x": xo.grad}, ["x"])
+
+    def _op_conv2d_depthwise(self, i, rec):
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x", "w"])
+        y = be.conv2d_depthwise(L["x"][1], L["w"][1], a["stride"], a["pad"])
+        x = nhwc_to_nchw(self._val(a["x"])).astype(F64)
+        w = np.ascontiguousarray(self._val(a["w"]).astype(F64).transpose(2, 0, 1)[:, None])  # RSC -> [C,1,R,S]
+        xo, wo = Var(x, True), Var(w, True)
+        zo = oops.conv2d_depthwise(xo, wo, a["stride"], a["pad"])
+        ydev = y.numpy()
+        self.record(i, "conv2d_depthwise", "y", nhwc_to_nchw(ydev), zo.value)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(zo, nhwc_to_nchw(np.asarray(g).reshape(ydev.shape)))
+        og = {"x": nchw_to_nhwc(xo.grad), "w": np.ascontiguousarray(wo.grad[:, 0].transpose(1, 2, 0))}
+        self._finish(i, rec, L, og, ["x", "w"])
+
     # ------------------------------------------------------------ report
     def worst(self, n=8):
         return sorted(self.errs, key=lambda e: -e[3])[:n]
@@ -503,11 +569,23 @@ def forward_drift(be, trace: OpTrace):
             y = y.value
             if a["residual"] is not None:
                 y = y + nhwc_to_nchw(val(a["residual"]))
-            if a["act"]:
-                y = np.maximum(y, 0)
-            y = nchw_to_nhwc(y)
+            y = nchw_to_nhwc(_act(y, a["act"]))
         elif op == "maxpool2d":
-            y = nchw_to_nhwc(oops.maxpool2d(Var(nhwc_to_nchw(val(a["x"]))), a["k"], a["stride"], a["pad"])[0].value)
+            yv, am = oops.maxpool2d(Var(nhwc_to_nchw(val(a["x"]))), a["k"], a["stride"], a["pad"])
+            y = nchw_to_nhwc(yv.value)
+            if rec.get("extra") is not None:  # winner flips between the two forwards (window index r·k+u)
+                xs = nhwc_to_nchw(val(a["x"])).shape
+                win = nhwc_to_nchw(rec["extra"]).astype(np.int64)
+                P, Q = win.shape[2], win.shape[3]
+                hh = np.arange(P)[:, None] * a["stride"] - a["pad"] + win // a["k"]
+                ww = np.arange(Q)[None, :] * a["stride"] - a["pad"] + win % a["k"]
+                flips = int((hh * xs[3] + ww != am).sum())
+                out.append((i, "argmax flips", float(flips)))
+        elif op == "dropout":
+            y = oops.dropout(Var(val(a["x"])), a["p"], a["seed"], a["offset"], training=a["training"]).value
+        elif op == "conv2d_depthwise":
+            w = np.ascontiguousarray(val(a["w"]).transpose(2, 0, 1)[:, None])
+            y = nchw_to_nhwc(oops.conv2d_depthwise(Var(nhwc_to_nchw(val(a["x"]))), Var(w), a["stride"], a["pad"]).value)
         elif op == "avgpool_global":
             y = oops.avgpool_global(Var(nhwc_to_nchw(val(a["x"])))).value
         elif op == "reshape":

@@ -39,6 +39,13 @@ def _case(name, dtype):
         y = synth.labels(2, 1000, seed)
         return (onets.AlexNet(), be.nn.AlexNet(), (x, y),
                 lambda: (be.nn.images_to_device(x, dtype), be.tensor(y)), seed)
+    if name in ("vgg19", "mobilenetv2"):
+        seed = 25 if name == "vgg19" else 26
+        x = inp(synth.normal((2, 3, 224, 224), seed, 1))
+        y = synth.labels(2, 1000, seed)
+        onet = onets.VGG19(seed=seed) if name == "vgg19" else onets.MobileNetV2(seed=seed)
+        pnet = be.nn.VGG19(seed=seed) if name == "vgg19" else be.nn.MobileNetV2(seed=seed)
+        return (onet, pnet, (x, y), lambda: (be.nn.images_to_device(x, dtype), be.tensor(y)), seed)
     if name == "ncf":
         seed = 23
         u, it, y = synth.ncf_batch(8192, 138493, 26744, seed)
@@ -55,7 +62,7 @@ def _case(name, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2"])
+@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2", "vgg19", "mobilenetv2"])
 def test_teacher_forced_full_depth(name, dtype):
     be = be_init()
     be.set_compute_dtype(dtype)
@@ -82,13 +89,13 @@ def _e2e_gate(name, dtype):
     e2e_gate(be, onet, pnet, P, obatch, dev_batch(), dtype, name=name)
 
 
-@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf"])
+@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "vgg19", "mobilenetv2"])
 def test_full_arch_one_step_fp32(name):
     """One fp32 (3xTF32) SGD step of the full architecture vs the oracle."""
     _e2e_gate(name, "f32")
 
 
-@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2"])
+@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2", "vgg19", "mobilenetv2"])
 def test_full_arch_one_step_bf16(name):
     """One bf16 step of the full architecture vs the plain float64 oracle."""
     _e2e_gate(name, "bf16")

@@ -48,7 +48,14 @@ def linear_probe(B, IN, OUT, act, xrelu):
 
 def drift(name, dtype):
     be.set_compute_dtype(dtype)
-    if name == "resnet50":
+    if name in ("vgg19", "mobilenetv2"):
+        seed = 25 if name == "vgg19" else 26
+        onet = onets.VGG19(seed=seed) if name == "vgg19" else onets.MobileNetV2(seed=seed)
+        pnet = be.nn.VGG19(seed=seed) if name == "vgg19" else be.nn.MobileNetV2(seed=seed)
+        x = synth.normal((2, 3, 224, 224), seed, 1)
+        x = synth.bf16_values(x) if dtype == "bf16" else x
+        batch = (be.nn.images_to_device(x, dtype), be.tensor(synth.labels(2, 1000, seed)))
+    elif name == "resnet50":
         onet, pnet = onets.ResNet50(), be.nn.ResNet50()
         x = synth.normal((2, 3, 224, 224), 21, 1)
         x = synth.bf16_values(x) if dtype == "bf16" else x
@@ -99,6 +106,9 @@ def repeat_probe(B, IN, OUT, reps=8):
 
 if __name__ == "__main__":
     be.init(0)
+    if len(sys.argv) > 2:
+        drift(sys.argv[1], sys.argv[2])
+        sys.exit(0)
     for args in [(1024, 4096, 4096, 1, True), (1024, 4096, 4096, 0, True), (1024, 4096, 4096, 1, False),
                  (96, 384, 128, 1, False), (96, 256, 384, 1, False)]:
         linear_probe(*args)
