@@ -220,8 +220,21 @@ def run_ours(args, cfg, rank, world, local_rank):
         be.dist_init(rank, world, uid[0])
     model = make_model(cfg, be, seed=0)
     params = model.parameters()
+    dp_mode = None
     if world > 1:
-        be.ddp_attach(params, 25 << 20)
+        # embedding tables on the sparse path exchange lookups, not gradients
+        tables = model.embedding_tables() if cfg.get("sparse") else []
+        dp_params = [p for p in params if all(p is not t for t in tables)]
+        if args.dp == "p2p":
+            # fused allreduce + SGD over CUDA-IPC peer memory (be_p2p_*);
+            # every rank built identical parameters from the same seed
+            blob = be.p2p_attach(dp_params, rank, world, 25 << 20)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
+            be.p2p_connect(blobs)
+        else:
+            be.ddp_attach(dp_params, 25 << 20)
+        dp_mode = args.dp
     hb = host_batch(cfg, seed=1, rank=rank)
     dts = ["bf16" if (i == 0 and cfg["net"] not in ("ncf",) and cfg["dtype"] == "bf16") else None
            for i in range(len(hb))]
@@ -331,7 +344,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         ms = rep_ms[0]
         r_, nr = be.api.dist_world()
         nccl_info = {"nranks": nr, "backend": "libbe NCCL communicator (ncclCommCount)",
-                     "allreduce": "bucketed ncclAllReduce(avg), 25 MB fp32 buckets, comm stream"}
+                     "allreduce": ("fused peer-memory allreduce + SGD kernel per 25 MB bucket (be_p2p_*, CUDA IPC "
+                                   "over NVLink), p2p_status=%d" % be.api.p2p_status()) if dp_mode == "p2p" else
+                     "bucketed ncclAllReduce(avg), 25 MB fp32 buckets, comm stream"}
 
     # ---- end-to-end through the public API: every step's batch goes pinned host → device
     # (double-buffered on a copy stream so batch i+1 transfers while step i computes, the
@@ -533,6 +548,8 @@ def main():
     ap.add_argument("--tune-steps", type=int, default=24, help="untimed autotuning steps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--repeats", type=int, default=5, help="timed passes of K steps (mean ± sd reported)")
+    ap.add_argument("--dp", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: p2p = fused allreduce+SGD over peer memory; nccl = bucketed ncclAllReduce")
     ap.add_argument("--sgd", default="overlap", choices=["overlap", "fused"],
                     help="overlap: per-parameter SGD inside backward on a side stream; fused: one launch after")
     args = ap.parse_args()

@@ -288,6 +288,31 @@ be_status be_ddp_detach(void);
  * (elements), bucket_numel[*n_buckets] (cap entries). */
 be_status be_ddp_plan(const int64_t* numels, int n, size_t bucket_bytes, int* bucket_of, int64_t* offset_of,
                       int64_t* bucket_numel, int cap, int* n_buckets);
+/* Peer-memory data parallelism (§5.4): the
+ * bucketed gradient allreduce FUSED with the SGD update, one kernel per bucket
+ * (p2p.cu) working over CUDA-IPC mappings of every rank's buckets, parameters
+ * and bf16 shadows: rank r reduces its 1/R slice of the bucket by loading it
+ * from every rank (NVLink peer loads, fixed rank order), applies ×1/R and the
+ * overlapped-SGD update (be_sgd_overlap's lr / momentum / wd; bitwise the
+ * update of be_sgd_step at R = 1) to that slice, and stores the new fp32
+ * master and bf16 shadow into every rank's copy; cross-GPU barriers are
+ * system-scope flags in peer memory (10 s timeout → be_p2p_status = 1).
+ * Buckets whose parameters are not all registered for overlapped SGD are
+ * plain mean-allreduced into the buckets instead (then be_sgd_step).
+ *   be_p2p_attach: bucket params as be_ddp_attach does (NO broadcast: every
+ *     rank must load identical parameters), allocate the barrier flags, create
+ *     the bf16 shadows (bf16 mode) and momentum buffers, and write this rank's
+ *     export blob (a header + one cudaIpcMemHandle_t per allocation) into
+ *     blob (cap bytes; *blob_bytes = size needed; blob may be NULL to query).
+ *   be_p2p_connect: `all` = the world blobs, rank-major, gathered by the
+ *     caller over any transport (torch.distributed, gloo); maps the peers'
+ *     allocations and arms DDP.  Needs no NCCL communicator.  be_ddp_detach
+ *     unmaps everything. */
+be_status be_p2p_attach(const be_tensor* params, int n, size_t bucket_bytes, int rank, int world, void* blob,
+                        size_t cap, size_t* blob_bytes);
+be_status be_p2p_connect(const void* all, size_t blob_bytes);
+/* 0 healthy; 1 = some bucket kernel timed out waiting for a peer.  Synchronises. */
+be_status be_p2p_status(int* status);
 /* Plain allreduce (sum, fp32/bf16) of a contiguous tensor on the compute stream. */
 be_status be_allreduce_(be_tensor t);
 

@@ -115,6 +115,9 @@ def lib():
             "be_sgd_step": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
             "be_sgd_overlap": [P(T), C.c_int, C.c_float, C.c_float, C.c_float],
             "be_sgd_sparse": [P(T), C.c_int, C.c_float],
+            "be_p2p_attach": [P(T), C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_void_p, C.c_size_t, P(C.c_size_t)],
+            "be_p2p_connect": [C.c_void_p, C.c_size_t],
+            "be_p2p_status": [P(C.c_int)],
             "be_sgd_momentum": [T, P(T)],
             "be_alloc_stats": [P(be_alloc_stats)],
             "be_alloc_reset_peak": [],
@@ -176,6 +179,6 @@ EXPORTED = [
     "be_dist_init", "be_ddp_attach", "be_ddp_detach", "be_allreduce_", "be_synchronize", "be_item",
     "be_debug_im2col_offsets", "be_gemm", "be_prof_enable", "be_prof_read", "be_ddp_plan",
     "be_stream_create", "be_stream_destroy", "be_event_create", "be_event_destroy", "be_event_record",
-    "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap", "be_sgd_sparse",
+    "be_stream_wait_event", "be_tensor_copy_from_host_on", "be_sgd_overlap", "be_sgd_sparse", "be_p2p_attach", "be_p2p_connect", "be_p2p_status",
     "be_sgd_momentum", "be_ddp_sync_buffers", "be_dist_world",
 ]

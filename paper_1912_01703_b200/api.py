@@ -489,6 +489,32 @@ def dist_world():
     return r.value, w.value
 
 
+def p2p_attach(params, rank, world, bucket_bytes=25 << 20) -> bytes:
+    """Bucket params for the peer-memory fused allreduce + SGD (be_p2p_attach);
+    returns this rank's export blob, to be all-gathered by the caller and
+    handed to p2p_connect."""
+    cap = 16 + (3 * len(params) + 2) * 64  # header + ≤ 1 + (n + 1) + 2n handles
+    buf = (C.c_char * cap)()
+    need = C.c_size_t()
+    call("be_p2p_attach", _handles(params), len(params), C.c_size_t(bucket_bytes), int(rank), int(world), buf,
+         cap, C.byref(need))
+    return bytes(buf[:need.value])
+
+
+def p2p_connect(blobs):
+    """blobs: every rank's p2p_attach output, in rank order."""
+    n = len(blobs[0])
+    assert all(len(b) == n for b in blobs)
+    allb = b"".join(blobs)
+    call("be_p2p_connect", C.c_char_p(allb), C.c_size_t(n))
+
+
+def p2p_status() -> int:
+    v = C.c_int()
+    call("be_p2p_status", C.byref(v))
+    return v.value
+
+
 def ddp_plan(numels, bucket_bytes=25 << 20):
     """Bucket plan of be_ddp_attach (pure host function): (bucket_of, offset_of, bucket_numel)."""
     n = len(numels)
