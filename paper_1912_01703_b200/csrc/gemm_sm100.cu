@@ -104,7 +104,11 @@ constexpr int kUpdBufs = 3;
 constexpr int kUpdBufBytes = 4096 + 4096 + 2048;
 constexpr int kUpdWarpBytes = kUpdBufs * kUpdBufBytes;
 
-template <int BN, bool X3, bool UPD = false>
+// NSLOT: 2-KB bf16 staging slots per epilogue warp (TMA stores in flight per
+// warp = NSLOT − 1).  4 for store-heavy short-K shapes (the 1×1 convs: the
+// epilogue, not the mainloop, is the critical path), 2 otherwise (more
+// mainloop stages for long K).
+template <int BN, bool X3, bool UPD = false, int NSLOT = 2>
 struct Cfg {
   static constexpr int ESIZE = X3 ? 4 : 2;
   static constexpr int BK = 128 / ESIZE;           // one 128-B swizzle row of K
@@ -113,7 +117,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;         // BM rows x 128 B
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int EPI_BYTES = UPD ? kUpdWarps * kUpdWarpBytes : kEpiBytes;
+  static constexpr int EPI_BYTES = UPD ? kUpdWarps * kUpdWarpBytes : kEpiWarps * NSLOT * 2048;
   static constexpr int STAGES_RAW = (226 * 1024 - EPI_BYTES - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -313,14 +317,17 @@ __device__ __forceinline__ void epi_sgd32(const GemmParams& p, uint8_t* buf, int
 // Each warp owns a 4 KB staging area: two 2 KB buffers alternating for bf16
 // (the store issued from a buffer two chunks earlier must have read it), one
 // 4 KB buffer for fp32.
+template <int NSLOT = 2>
 __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf, int& slot, int lane, int store_row,
                                           int col0, const uint32_t (&r)[32], int z = -1) {
+  static_assert(NSLOT == 2 || NSLOT == 4, "staging slots");
   uint8_t* buf = warp_buf;
-  if (p.d_f32) {
-    if (lane == 0) sm100::bulk_wait_read<0>();
+  if (p.d_f32) {  // 4-KB fp32 chunks: NSLOT / 2 buffers
+    buf += (slot % (NSLOT / 2)) * 4096;
+    if (lane == 0) sm100::bulk_wait_read<NSLOT / 2 - 1>();
   } else {
     buf += slot * 2048;
-    if (lane == 0) sm100::bulk_wait_read<1>();
+    if (lane == 0) sm100::bulk_wait_read<NSLOT - 1>();
   }
   __syncwarp();
   float v[32];
@@ -371,7 +378,7 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
     }
     sm100::bulk_commit();
   }
-  slot ^= 1;
+  slot = (slot + 1) % (p.d_f32 ? NSLOT / 2 : NSLOT);
 }
 
 // Fused-SGD epilogue of a persistent GEMM (warp = TMEM lane quarter eq):
@@ -449,10 +456,10 @@ __device__ __forceinline__ void upd_epilogue(const GemmParams& p, uint8_t* epi_s
   if (lane == 0) sm100::bulk_wait<0>();  // stores complete before exit
 }
 
-template <int BN, bool X3, bool UPD = false>
+template <int BN, bool X3, bool UPD = false, int NSLOT = 2>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
   pdl_entry();
-  using C = Cfg<BN, X3, UPD>;
+  using C = Cfg<BN, X3, UPD, NSLOT>;
   static_assert(C::STAGES >= 2, "pipeline needs at least two stages");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -644,8 +651,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           }
         }
         if (p.tma_store) {
-          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
-          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+          epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col1, r1);
         } else if (row_ok) {
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
@@ -665,8 +672,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
         if (p.tma_store) {
-          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
-          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+          epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col1, r1);
         } else if (row_ok) {
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
@@ -2485,13 +2492,14 @@ double update_bytes(const GemmDesc& g) {
   return 8.0 + (g.upd->v ? 8.0 : 0.0) + (g.upd->shadow ? 2.0 : 0.0);
 }
 
-template <int BN, bool X3>
+template <int BN, bool X3, int NSLOT = 2>
 void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo,
                cudaStream_t s, int force_splits = 0) {
-  using C = Cfg<BN, X3>;
+  using C = Cfg<BN, X3, false, NSLOT>;
   static bool attr_set = false;
   if (!attr_set) {
-    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3, false, NSLOT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   GemmParams p;
@@ -2584,7 +2592,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
       fail(BE_E_ARG, "gemm: the update epilogue runs on the bf16 kernel");
     }
   } else {
-    launch_pdl(gemm_tc_kernel<BN, X3>, grid, kThreads, C::SMEM, s, p);
+    launch_pdl(gemm_tc_kernel<BN, X3, false, NSLOT>, grid, kThreads, C::SMEM, s, p);
   }
   prof_end(pidx, s);
   after_launch("gemm_tc");
@@ -3120,6 +3128,12 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       if (pm != 0 && pair_plausible(g)) cands[nc++] = {1, 256, 0};
       const int sms = ctx().num_sms;
       const int kbl = (g.K + 63) / 64;
+      // store-heavy short-K shapes (1×1 convs): the same tile with 4 staging
+      // slots per epilogue warp (3 TMA stores in flight) for fewer stages
+      // BE_GEMM_EPI4=0 drops the candidate, =1 forces it where it applies (tests)
+      static const int epi4 = [] { const char* e = getenv("BE_GEMM_EPI4"); return e ? atoi(e) : -1; }();
+      const int tiles_bn = ((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn);
+      if (epi4 != 0 && kbl <= 8 && tiles_bn >= sms) cands[nc++] = {2, bn, 0};
       for (int cbn : {256, 128}) {
         if (g.stats) break;  // split-K cannot carry the statistics epilogue
         const int tiles = ((g.M + BM - 1) / BM) * ((g.N + cbn - 1) / cbn);
@@ -3130,11 +3144,18 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       }
       int v = 0;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-      if (pm == 1 && pair_plausible(g)) v = 1;
+      int deep = -1;
+      for (int i = 0; i < nc; ++i)
+        if (cands[i].kind == 2) deep = i;
+      if (epi4 == 1 && deep >= 0) v = deep;  // tests: force the 4-slot epilogue where it applies
+      else if (pm == 1 && pair_plausible(g)) v = 1;
       else if (nc > 1) v = tune_choose("gemm:" + tune_key(g) + (g.stats ? "s" : ""), nc, 0, &ev0, &ev1);
       const Cand c = cands[v];
       if (ev0) cudaEventRecord(ev0, s);
       if (c.kind == 1) launch_tc2(g, s);
+      else if (c.kind == 2 && c.bn == 256) launch_tc<256, false, 4>(g, ahi, alo, bhi, blo, s);
+      else if (c.kind == 2 && c.bn == 128) launch_tc<128, false, 4>(g, ahi, alo, bhi, blo, s);
+      else if (c.kind == 2) launch_tc<64, false, 4>(g, ahi, alo, bhi, blo, s);
       else if (c.bn == 256) launch_tc<256, false>(g, ahi, alo, bhi, blo, s, c.splits);
       else if (c.bn == 128) launch_tc<128, false>(g, ahi, alo, bhi, blo, s, c.splits);
       else launch_tc<64, false>(g, ahi, alo, bhi, blo, s, c.splits);

@@ -97,3 +97,47 @@ def test_gemm_misaligned_uses_simt_and_matches():
     D = be.empty((M, N), "f32")
     be.gemm(be.tensor(a), be.tensor(b), D)
     assert rel(D.numpy(), _ref(a, b, 0, 0)) < 1e-6
+
+
+_EPI4_SCRIPT = r'''
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+import paper_1912_01703_b200 as be
+from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+be.init(0)
+worst = 0.0
+for (M, N, K, out, beta, act) in [(148 * 128 + 77, 256, 64, "bf16", 0.0, 0), (148 * 128 * 2, 128, 128, "f32", 0.0, 1),
+                                  (148 * 128 + 5, 64, 200, "bf16", 1.0, 0), (148 * 128, 1024, 256, "bf16", 0.0, 1)]:
+    rng = np.random.default_rng(M + N)
+    a = bf16_bits_to_f32(f32_to_bf16_bits(rng.standard_normal((M, K)).astype(np.float32)))
+    b = bf16_bits_to_f32(f32_to_bf16_bits(rng.standard_normal((N, K)).astype(np.float32)))
+    bias = rng.standard_normal(N).astype(np.float32)
+    d0 = bf16_bits_to_f32(f32_to_bf16_bits(rng.standard_normal((M, N)).astype(np.float32)))
+    D = be.tensor(d0, dtype=out if out == "bf16" else None)
+    be.gemm(be.tensor(a, dtype="bf16"), be.tensor(b, dtype="bf16"), D, trans_b=True, bias=be.tensor(bias),
+            act=act, beta=beta)
+    ref = a.astype(np.float64) @ b.T.astype(np.float64) + bias
+    if act:
+        ref = np.maximum(ref, 0)
+    ref = ref + beta * d0
+    e = float(np.abs(D.numpy() - ref).max() / np.abs(ref).max())
+    worst = max(worst, e)
+print(worst)
+'''
+
+
+def test_gemm_four_slot_epilogue(tmp_path):
+    """The 4-slot (3 TMA stores in flight per warp) epilogue variant of the
+    1-CTA kernel, forced with BE_GEMM_EPI4=1 on short-K store-heavy shapes
+    (ragged M, bf16 / fp32 out, bias, ReLU, beta = 1 reduce-add store), vs
+    float64 at the storage rounding of the output (2^-8 relative for bf16)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    f = tmp_path / "epi4.py"
+    f.write_text(_EPI4_SCRIPT)
+    env = dict(os.environ, BE_GEMM_EPI4="1")
+    out = subprocess.run([sys.executable, str(f), root], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) < 8e-3
