@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t
 
 // backward reduction Σg', Σg'·x̂ (g' = gy masked by act(γx̂+β) > 0 recomputed
 // from x when act; with rmask: g = gy·1[rmask > 0] written to gout first)
-template <bool MASK>
+// MASK 1: the residual mask read from the stored block output (bf16 y > 0);
+// MASK 2: read from the forward's 1-bit mask (bit j of byte row·C/8 + c/8 =
+// channel c + j passed the ReLU) — 1/16 of the bytes of y
+template <int MASK>
 __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_t* __restrict__ x,
                                                                 const uint16_t* __restrict__ gy, int act,
                                                                 int64_t rows, int C, const float* __restrict__ mean,
@@ -176,7 +179,8 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
                                                                 const float* __restrict__ gam,
                                                                 const float* __restrict__ bsh,
                                                                 const uint16_t* __restrict__ rmask,
-                                                                uint16_t* __restrict__ gout) {
+                                                                uint16_t* __restrict__ gout,
+                                                                const uint8_t* __restrict__ rbits) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
@@ -194,7 +198,16 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
     float a[8], g[8];
     unpack8s(v[0], a);
     uint4 gv = v[1];
-    if (MASK) {
+    if (MASK == 2) {
+      const uint32_t b = rbits[row * (C >> 3) + (c >> 3)];
+      uint32_t ow[4];
+      const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        ow[i] = gw[i] & (((b >> (2 * i)) & 1u ? 0x0000ffffu : 0u) | ((b >> (2 * i + 1)) & 1u ? 0xffff0000u : 0u));
+      gv = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      *reinterpret_cast<uint4*>(gout + row * C + c) = gv;
+    } else if (MASK == 1) {
       // residual block output y = relu(bn(x) + shortcut): g = gy·1[y > 0]
       // (bf16 y > 0 ⇔ bits in [1, 0x7f80]), stored for the shortcut and dx
       const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
 #pragma unroll
     for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] += g[j] * (a[j] - k[j]) * is[j]; }
   };
-  if (MASK) {
+  if (MASK == 1) {
     const uint16_t* src[3] = {x, gy, rmask};
     stream_rows<3, 2, 3>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[3]) { body(row, v); });
   } else {
@@ -236,7 +249,8 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
                                                                const float* __restrict__ invstd,
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, int act, int64_t rps,
-                                                               const uint16_t* __restrict__ res) {
+                                                               const uint16_t* __restrict__ res,
+                                                               uint8_t* __restrict__ mbits) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
@@ -264,7 +278,18 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] = act_apply(o[j], act);
     }
-    *reinterpret_cast<uint4*>(y + row * C + c) = pack8s(o);
+    const uint4 pk = pack8s(o);
+    *reinterpret_cast<uint4*>(y + row * C + c) = pk;
+    if (mbits) {  // 1-bit mask of the stored value: bf16 bits in [1, 0x7f80] ⇔ y > 0
+      const uint32_t w[4] = {pk.x, pk.y, pk.z, pk.w};
+      uint32_t b = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        b |= ((w[i] & 0xffffu) - 1u < 0x7f80u ? 1u : 0u) << (2 * i);
+        b |= ((w[i] >> 16) - 1u < 0x7f80u ? 1u : 0u) << (2 * i + 1);
+      }
+      mbits[row * (C >> 3) + (c >> 3)] = (uint8_t)b;
+    }
   };
   if (RES) {
     const uint16_t* src[2] = {x, res};
@@ -436,25 +461,31 @@ void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float
 
 void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
                       const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
-                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s) {
+                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
+                      const uint8_t* rbits) {
   static bool once = [] {
-    set_smem(bn_reduce_stream_kernel<false>, kS2);
-    set_smem(bn_reduce_stream_kernel<true>, kS3);
+    set_smem(bn_reduce_stream_kernel<0>, kS2);
+    set_smem(bn_reduce_stream_kernel<1>, kS3);
+    set_smem(bn_reduce_stream_kernel<2>, kS2);
     return true;
   }();
   (void)once;
   const int64_t rps = (rows + sp - 1) / sp;
-  if (rmask)
-    launch_pdl(bn_reduce_stream_kernel<true>, (unsigned)sp, kThr, kS3, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-                                                                  rps, gam, bsh, rmask, gout);
+  if (rbits)
+    launch_pdl(bn_reduce_stream_kernel<2>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
+               rps, gam, bsh, (const uint16_t*)nullptr, gout, rbits);
+  else if (rmask)
+    launch_pdl(bn_reduce_stream_kernel<1>, (unsigned)sp, kThr, kS3, s, x, gy, act, rows, C, mean, invstd, part0, part1,
+               rps, gam, bsh, rmask, gout, (const uint8_t*)nullptr);
   else
-    launch_pdl(bn_reduce_stream_kernel<false>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-                                                                   rps, gam, bsh, nullptr, nullptr);
+    launch_pdl(bn_reduce_stream_kernel<0>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
+               rps, gam, bsh, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr);
   after_launch("bn_reduce_stream");
 }
 
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
-                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s) {
+                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s,
+                     uint8_t* mbits) {
   static bool once = [] {
     set_smem(bn_apply_stream_kernel<false>, kS1);
     set_smem(bn_apply_stream_kernel<true>, kS2);
@@ -465,10 +496,10 @@ void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const 
   const int64_t rps = (rows + sp - 1) / sp;
   if (res)
     launch_pdl(bn_apply_stream_kernel<true>, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-                                                                 res);
+               res, mbits);
   else
     launch_pdl(bn_apply_stream_kernel<false>, (unsigned)sp, kThr, kS1, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-                                                                  nullptr);
+               (const uint16_t*)nullptr, mbits);
   after_launch("bn_apply_stream");
 }
 

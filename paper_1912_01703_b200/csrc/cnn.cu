@@ -24,9 +24,11 @@ int64_t bn_stream_splits(int64_t rows, int C, int64_t cap);
 void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s);
 void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
                       const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
-                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s);
+                      const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
+                      const uint8_t* rbits = nullptr);
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
-                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s);
+                     const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s,
+                     uint8_t* mbits = nullptr);
 void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,
                   const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
                   const float* bsh, cudaStream_t s);
@@ -1362,13 +1364,16 @@ void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C
                                                   nullptr, 0.f, nullptr);
   after_launch("bn_stats_from_partials");
 }
+bool bn_mask_bits_ok(const void* x, const void* y, const void* res, int64_t rows, int C, be_dtype dt) {
+  return dt == BE_BF16 && bn_stream_ok(x, rows, C) && aligned16(y) && (!res || aligned16(res));
+}
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
-              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res) {
+              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res, uint8_t* mbits) {
   const int64_t total = rows * C;
   if (total == 0) return;
   if (dt == BE_BF16 && bn_stream_ok(x, rows, C) && aligned16(y) && (!res || aligned16(res))) {
     bn_apply_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C, mean, invstd, gamma,
-                    beta, act, reinterpret_cast<const uint16_t*>(res), s);
+                    beta, act, reinterpret_cast<const uint16_t*>(res), s, mbits);
     return;
   }
   if (bn_vec_ok(x, C) && aligned16(y) && (!res || aligned16(res))) {
@@ -1388,11 +1393,12 @@ void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const fl
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta, float gb_beta,
             float dx_beta, float* partial, cudaStream_t s, const float* bn_beta, const void* rmask,
-            void* gout) {
+            void* gout, const uint8_t* rbits) {
   // partial must hold 2*splits*C + 2*C floats
-  if (rmask) {
+  BE_REQUIRE(!rbits || (dt == BE_BF16 && bn_stream_ok(x, rows, C)), BE_E_ARG, "bn_bwd: bit mask needs the stream path");
+  if (rmask || rbits) {
     // residual output mask: g = dy·1[rmask > 0] into gout, then the BN backward of g
-    if (dt == BE_BF16 && !act && bn_vec_ok(x, C) && aligned16(dy) && aligned16(rmask) && aligned16(gout) &&
+    if (dt == BE_BF16 && !act && bn_vec_ok(x, C) && aligned16(dy) && (rbits || aligned16(rmask)) && aligned16(gout) &&
         (!dx || aligned16(dx))) {
       int64_t sp = bn_splits_v(rows, C);
       const bool stream = bn_stream_ok(x, rows, C);
@@ -1405,7 +1411,7 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       if (stream) {
         bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), 0, rows, C, mean,
                          invstd, p0, p1, sp, gamma, nullptr, reinterpret_cast<const uint16_t*>(rmask),
-                         reinterpret_cast<uint16_t*>(gout), s);
+                         reinterpret_cast<uint16_t*>(gout), s, rbits);
       } else {
         launch_pdl(bn_reduce_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
                                             0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,

@@ -139,7 +139,11 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
               float* partial, float* run_mean, float* run_var, float momentum, cudaStream_t s);
 // y = act(γ·(x − μ)·is + β [+ res])   (res: optional residual, same layout/dtype as x)
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
-              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr);
+              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr,
+              uint8_t* mbits = nullptr);
+// true when bn_apply can also write the 1-bit ReLU mask of its output (mbits:
+// rows·C/8 bytes, bit j of byte r·C/8 + c/8 ⇔ y[r, c + j] > 0) for bn_bwd's rbits
+bool bn_mask_bits_ok(const void* x, const void* y, const void* res, int64_t rows, int C, be_dtype dt);
 size_t bn_partial_floats(int64_t rows, int C);
 // mean / invstd (+ running stats) from unshifted per-part column sums: Σ in
 // partial[0..parts)[C], Σx² in partial[parts..2·parts)[C] (conv epilogue)
@@ -149,7 +153,7 @@ void bn_stats_from_partials(const float* partial, int parts, int64_t rows, int C
 void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int64_t rows, int C, be_dtype dt,
             const float* mean, const float* invstd, const float* gamma, float* dgamma, float* dbeta,
             float gb_beta, float dx_beta, float* partial, cudaStream_t s, const float* bn_beta = nullptr,
-            const void* rmask = nullptr, void* gout = nullptr);
+            const void* rmask = nullptr, void* gout = nullptr, const uint8_t* rbits = nullptr);
 // rmask (residual BN, y = relu(bn(x) + r)): the upstream is first masked,
 // g = dy·1[rmask > 0], written to gout (the shortcut's gradient) — fused into
 // the reduction pass on the bf16 path; act must be 0

@@ -69,138 +69,194 @@ __global__ void dropout_kernel(const T* __restrict__ x, T* __restrict__ y, int64
 }
 
 // ------------------------------------------------------------------ depthwise conv
-// x NHWC [N,H,W,C], w RSC [R,S,C] fp32, y NHWC [N,P,Q,C]; C % 8 == 0
+// x NHWC [N,H,W,C], w RSC [3,3,C] fp32, y NHWC [N,P,Q,C]; C % 8 == 0.
+// Every kernel runs blocks of C/8 · ⌊256 / (C/8)⌋ threads and strides over
+// pixels in multiples of C/8, so a thread owns ONE 8-channel group for its
+// whole life: its 9 × 8 filter taps sit in registers, loaded once; per pixel
+// the 9 neighbourhood vectors are issued back to back (predicated, fully
+// unrolled) before any arithmetic.
 __device__ __forceinline__ void ldw8(const float* __restrict__ w, int64_t i, float (&o)[8]) {
   const float4 a = *reinterpret_cast<const float4*>(w + i), b = *reinterpret_cast<const float4*>(w + i + 4);
   o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
 }
+// 8 channels as loaded: bf16 stays packed (4 registers) until used
+template <bool BF> struct Pk;
+template <> struct Pk<true> {
+  uint4 u;
+  __device__ __forceinline__ float operator[](int j) const {
+    const uint32_t w = j < 2 ? u.x : j < 4 ? u.y : j < 6 ? u.z : u.w;
+    return __uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16));
+  }
+};
+template <> struct Pk<false> {
+  float4 a, b;
+  __device__ __forceinline__ float operator[](int j) const {
+    const float4& h = j < 4 ? a : b;
+    const int k = j & 3;
+    return k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w;
+  }
+};
+template <bool BF>
+__device__ __forceinline__ Pk<BF> ldpk(const void* p, int64_t i, bool ok) {
+  Pk<BF> r;
+  if constexpr (BF) {
+    r.u = ok ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p) + i)) : make_uint4(0, 0, 0, 0);
+  } else {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    r.a = ok ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p) + i)) : z;
+    r.b = ok ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p) + i) + 1) : z;
+  }
+  return r;
+}
+template <bool BF>
+__device__ __forceinline__ void stpk(void* p, int64_t i, const float (&o)[8]) {
+  V8 v;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v.v[j] = o[j];
+  st8(p, i, BF ? BE_BF16 : BE_F32, v);
+}
 
+template <int ST, bool BF>
 __global__ void __launch_bounds__(256) dw_fwd_kernel(const void* __restrict__ x, const float* __restrict__ w,
-                                                     void* __restrict__ y, k::ConvGeom g, be_dtype dt) {
+                                                     void* __restrict__ y, k::ConvGeom g) {
   pdl_entry();
-  const int C8 = g.C >> 3;
-  const int64_t total = (int64_t)g.N * g.P * g.Q * C8;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t % C8) * 8;
-    int64_t pix = t / C8;
+  const int C8 = g.C >> 3, ppb = blockDim.x / C8;
+  if ((int)threadIdx.x >= ppb * C8) return;
+  const int c = (threadIdx.x % C8) * 8;
+  float wr[9][8];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) ldw8(w, (int64_t)t * g.C + c, wr[t]);
+  const int64_t npix = (int64_t)g.N * g.P * g.Q;
+  for (int64_t pix = (int64_t)blockIdx.x * ppb + threadIdx.x / C8; pix < npix; pix += (int64_t)gridDim.x * ppb) {
     const int q = (int)(pix % g.Q);
-    pix /= g.Q;
-    const int p = (int)(pix % g.P);
-    const int n = (int)(pix / g.P);
-    float acc[8] = {};
-    for (int r = 0; r < g.R; ++r) {
-      const int h = p * g.stride - g.pad + r;
-      if (h < 0 || h >= g.H) continue;
-      for (int s = 0; s < g.S; ++s) {
-        const int wc = q * g.stride - g.pad + s;
-        if (wc < 0 || wc >= g.W) continue;
-        const V8 xv = ld8(x, (((int64_t)n * g.H + h) * g.W + wc) * g.C + c, dt);
-        float wv[8];
-        ldw8(w, (int64_t)(r * g.S + s) * g.C + c, wv);
+    const int64_t np_ = pix / g.Q;
+    const int p = (int)(np_ % g.P), n = (int)(np_ / g.P);
+    const int h0 = p * ST - g.pad, w0 = q * ST - g.pad;
+    const int64_t base = (((int64_t)n * g.H + h0) * g.W + w0) * g.C + c;
+    Pk<BF> v[9];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(xv.v[j], wv[j], acc[j]);
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) {
+        const bool ok = (unsigned)(h0 + r) < (unsigned)g.H && (unsigned)(w0 + s2) < (unsigned)g.W;
+        v[r * 3 + s2] = ldpk<BF>(x, base + ((int64_t)r * g.W + s2) * g.C, ok);
       }
-    }
-    V8 o;
+    float o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o.v[j] = acc[j];
-    st8(y, t * 8, dt, o);
+    for (int j = 0; j < 8; ++j) {
+      float a = 0.f;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) a = fmaf(v[t][j], wr[t][j], a);
+      o[j] = a;
+    }
+    stpk<BF>(y, pix * g.C + c, o);
   }
 }
 
-// dx[n,h,w,c] (+)= Σ_{r,s: (h+pad−r), (w+pad−s) divisible by stride, in range} dy[n,p,q,c]·w[r,s,c]
+// dx[n,h,w,c] (+)= Σ_{r,s: (h+pad−r), (w+pad−s) divisible by ST, in range} dy[n,p,q,c]·w[r,s,c]
+template <int ST, bool BF>
 __global__ void __launch_bounds__(256) dw_dgrad_kernel(const void* __restrict__ dy, const float* __restrict__ w,
-                                                       void* dx, k::ConvGeom g, be_dtype dt, float beta) {
+                                                       void* dx, k::ConvGeom g, float beta) {
   pdl_entry();
-  const int C8 = g.C >> 3;
-  const int64_t total = (int64_t)g.N * g.H * g.W * C8;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t % C8) * 8;
-    int64_t pix = t / C8;
-    const int wc = (int)(pix % g.W);
-    pix /= g.W;
-    const int h = (int)(pix % g.H);
-    const int n = (int)(pix / g.H);
-    float acc[8] = {};
-    for (int r = 0; r < g.R; ++r) {
-      const int ph = h + g.pad - r;
-      if (ph < 0 || ph % g.stride) continue;
-      const int p = ph / g.stride;
-      if (p >= g.P) continue;
-      for (int s = 0; s < g.S; ++s) {
-        const int qw = wc + g.pad - s;
-        if (qw < 0 || qw % g.stride) continue;
-        const int q = qw / g.stride;
-        if (q >= g.Q) continue;
-        const V8 gv = ld8(dy, (((int64_t)n * g.P + p) * g.Q + q) * g.C + c, dt);
-        float wv[8];
-        ldw8(w, (int64_t)(r * g.S + s) * g.C + c, wv);
+  const int C8 = g.C >> 3, ppb = blockDim.x / C8;
+  if ((int)threadIdx.x >= ppb * C8) return;
+  const int c = (threadIdx.x % C8) * 8;
+  float wr[9][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(gv.v[j], wv[j], acc[j]);
+  for (int t = 0; t < 9; ++t) ldw8(w, (int64_t)t * g.C + c, wr[t]);
+  const int64_t npix = (int64_t)g.N * g.H * g.W;
+  for (int64_t pix = (int64_t)blockIdx.x * ppb + threadIdx.x / C8; pix < npix; pix += (int64_t)gridDim.x * ppb) {
+    const int wc = (int)(pix % g.W);
+    const int64_t nh = pix / g.W;
+    const int h = (int)(nh % g.H), n = (int)(nh / g.H);
+    const int64_t img = (int64_t)n * g.P * g.Q;
+    Pk<BF> v[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int ph = h + g.pad - r;
+      const int p = ph / ST;
+      const bool rok = ph >= 0 && (ST == 1 || (ph & 1) == 0) && p < g.P;
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) {
+        const int qw = wc + g.pad - s2;
+        const int q = qw / ST;
+        const bool ok = rok && qw >= 0 && (ST == 1 || (qw & 1) == 0) && q < g.Q;
+        v[r * 3 + s2] = ldpk<BF>(dy, (img + (int64_t)p * g.Q + q) * g.C + c, ok);
       }
     }
-    V8 o;
-    if (beta != 0.f) {
-      const V8 prev = ld8(dx, t * 8, dt);
+    float o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o.v[j] = acc[j] + prev.v[j];
-    } else {
+    for (int j = 0; j < 8; ++j) {
+      float a = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o.v[j] = acc[j];
+      for (int t = 0; t < 9; ++t) a = fmaf(v[t][j], wr[t][j], a);
+      o[j] = a;
     }
-    st8(dx, t * 8, dt, o);
+    if (beta != 0.f) {
+      const Pk<BF> prev = ldpk<BF>(dx, pix * g.C + c, true);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += prev[j];
+    }
+    stpk<BF>(dx, pix * g.C + c, o);
   }
 }
 
 // dw partials: block b sums dy·x over its output-pixel range for every
-// (r, s, c); thread (pl, c8) strides the range by npl pixels; the block then
-// combines its npl lanes in lane order.  partial[b][(r·S + s)·C + c].
-template <int RS>
+// (r, s, c); thread (pl, c8) strides the range by ppb pixels with the 9
+// neighbourhood loads of a pixel issued together; the block then combines
+// its ppb lanes in lane order.  partial[b][(r·3 + s)·C + c].
+template <int ST, bool BF>
 __global__ void __launch_bounds__(256) dw_wgrad_partial_kernel(const void* __restrict__ dy,
                                                                const void* __restrict__ x, float* __restrict__ part,
-                                                               k::ConvGeom g, be_dtype dt, int64_t ppb) {
+                                                               k::ConvGeom g, int64_t pix_per_block) {
   pdl_entry();
   extern __shared__ float red[];
-  const int C8 = g.C >> 3, npl = blockDim.x / C8;
+  const int C8 = g.C >> 3, ppb = blockDim.x / C8;
   const int c8 = threadIdx.x % C8, pl = threadIdx.x / C8;
   const int c = c8 * 8;
   const int64_t npq = (int64_t)g.N * g.P * g.Q;
-  const int64_t p0 = blockIdx.x * ppb, p1 = min(npq, p0 + ppb);
-  float acc[RS][8];
+  const int64_t p0 = blockIdx.x * pix_per_block, p1 = min(npq, p0 + pix_per_block);
+  float acc[9][8];
 #pragma unroll
-  for (int k = 0; k < RS; ++k)
+  for (int k = 0; k < 9; ++k)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[k][j] = 0.f;
-  if (pl < npl) {
-    for (int64_t pix = p0 + pl; pix < p1; pix += npl) {
+  if (pl < ppb) {
+    for (int64_t pix = p0 + pl; pix < p1; pix += ppb) {
       const int q = (int)(pix % g.Q);
       const int64_t np_ = pix / g.Q;
-      const int p = (int)(np_ % g.P);
-      const int n = (int)(np_ / g.P);
-      const V8 gv = ld8(dy, pix * g.C + c, dt);
+      const int p = (int)(np_ % g.P), n = (int)(np_ / g.P);
+      const int h0 = p * ST - g.pad, w0 = q * ST - g.pad;
+      const int64_t base = (((int64_t)n * g.H + h0) * g.W + w0) * g.C + c;
+      const Pk<BF> gv = ldpk<BF>(dy, pix * g.C + c, true);
+      Pk<BF> v[9];
 #pragma unroll
-      for (int k = 0; k < RS; ++k) {
-        const int r = k / g.S, s = k % g.S;
-        const int h = p * g.stride - g.pad + r, wc = q * g.stride - g.pad + s;
-        if (h < 0 || h >= g.H || wc < 0 || wc >= g.W) continue;
-        const V8 xv = ld8(x, (((int64_t)n * g.H + h) * g.W + wc) * g.C + c, dt);
+      for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[k][j] = fmaf(gv.v[j], xv.v[j], acc[k][j]);
+        for (int s2 = 0; s2 < 3; ++s2) {
+          const bool ok = (unsigned)(h0 + r) < (unsigned)g.H && (unsigned)(w0 + s2) < (unsigned)g.W;
+          v[r * 3 + s2] = ldpk<BF>(x, base + ((int64_t)r * g.W + s2) * g.C, ok);
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float gj = gv[j];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[t][j] = fmaf(gj, v[t][j], acc[t][j]);
       }
     }
-    float* mine = red + ((int64_t)pl * C8 + c8) * (RS * 8);
+    float* mine = red + ((int64_t)pl * C8 + c8) * 72;
 #pragma unroll
-    for (int k = 0; k < RS; ++k)
+    for (int t = 0; t < 9; ++t)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mine[k * 8 + j] = acc[k][j];
+      for (int j = 0; j < 8; ++j) mine[t * 8 + j] = acc[t][j];
   }
   __syncthreads();
-  const int per = C8 * RS * 8;
+  const int per = C8 * 72;
   for (int e = threadIdx.x; e < per; e += blockDim.x) {
     float sum = 0.f;
-    for (int l = 0; l < npl; ++l) sum += red[(int64_t)l * per + e];
-    const int cc = e / (RS * 8), k = (e / 8) % RS, j = e % 8;
-    part[(int64_t)blockIdx.x * RS * g.C + (int64_t)k * g.C + cc * 8 + j] = sum;
+    for (int l = 0; l < ppb; ++l) sum += red[(int64_t)l * per + e];
+    const int cc = e / 72, t = (e / 8) % 9, j = e % 8;
+    part[(int64_t)blockIdx.x * 9 * g.C + (int64_t)t * g.C + cc * 8 + j] = sum;
   }
 }
 
@@ -240,45 +296,78 @@ void dropout_apply(const void* x, void* y, int64_t n, be_dtype dt, uint64_t seed
   after_launch("dropout");
 }
 
+static int dw_block(int C) {
+  const int c8 = C / 8;
+  return c8 * std::max(1, 256 / c8);
+}
+static int dw_grid(int64_t pixels, int C, int per_sm) {
+  const int ppb = dw_block(C) / (C / 8);
+  const int64_t want = (pixels + ppb - 1) / ppb;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148LL * per_sm));
+}
+
 void dw_conv_fwd(const void* x, const float* w, void* y, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
-  const int64_t items = (int64_t)g.N * g.P * g.Q * (g.C / 8);
-  if (items <= 0) return;
-  launch_pdl(dw_fwd_kernel, grid_ew(items), 256, 0, s, x, w, y, g, dt);
+  const int64_t npix = (int64_t)g.N * g.P * g.Q;
+  if (npix <= 0) return;
+  BE_REQUIRE(g.R == 3 && g.S == 3 && (g.stride == 1 || g.stride == 2) && g.C / 8 <= 256, BE_E_UNSUPPORTED,
+             "depthwise conv: 3x3, stride 1|2, C <= 2048");
+  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
+  const bool bf = dt == BE_BF16;
+  if (g.stride == 1 && bf) launch_pdl(dw_fwd_kernel<1, true>, grid, block, 0, s, x, w, y, g);
+  else if (g.stride == 1) launch_pdl(dw_fwd_kernel<1, false>, grid, block, 0, s, x, w, y, g);
+  else if (bf) launch_pdl(dw_fwd_kernel<2, true>, grid, block, 0, s, x, w, y, g);
+  else launch_pdl(dw_fwd_kernel<2, false>, grid, block, 0, s, x, w, y, g);
   after_launch("dw_fwd");
 }
 
 void dw_conv_dgrad(const void* dy, const float* w, void* dx, const ConvGeom& g, be_dtype dt, float beta,
                    cudaStream_t s) {
-  const int64_t items = (int64_t)g.N * g.H * g.W * (g.C / 8);
-  if (items <= 0) return;
-  launch_pdl(dw_dgrad_kernel, grid_ew(items), 256, 0, s, dy, w, dx, g, dt, beta);
+  const int64_t npix = (int64_t)g.N * g.H * g.W;
+  if (npix <= 0) return;
+  BE_REQUIRE(g.R == 3 && g.S == 3 && (g.stride == 1 || g.stride == 2) && g.C / 8 <= 256, BE_E_UNSUPPORTED,
+             "depthwise conv: 3x3, stride 1|2, C <= 2048");
+  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
+  const bool bf = dt == BE_BF16;
+  if (g.stride == 1 && bf) launch_pdl(dw_dgrad_kernel<1, true>, grid, block, 0, s, dy, w, dx, g, beta);
+  else if (g.stride == 1) launch_pdl(dw_dgrad_kernel<1, false>, grid, block, 0, s, dy, w, dx, g, beta);
+  else if (bf) launch_pdl(dw_dgrad_kernel<2, true>, grid, block, 0, s, dy, w, dx, g, beta);
+  else launch_pdl(dw_dgrad_kernel<2, false>, grid, block, 0, s, dy, w, dx, g, beta);
   after_launch("dw_dgrad");
 }
 
-size_t dw_wgrad_partial_floats(const ConvGeom& g, int num_sms) {
+static int64_t dw_wgrad_blocks(const ConvGeom& g, int num_sms) {
   const int64_t npq = (int64_t)g.N * g.P * g.Q;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(4LL * num_sms, (npq + 63) / 64));
-  return (size_t)blocks * g.R * g.S * g.C;
+  return std::max<int64_t>(1, std::min<int64_t>(2LL * num_sms, (npq + 255) / 256));
+}
+size_t dw_wgrad_partial_floats(const ConvGeom& g, int num_sms) {
+  return (size_t)dw_wgrad_blocks(g, num_sms) * g.R * g.S * g.C;
 }
 
 void dw_conv_wgrad(const void* dy, const void* x, float* dw, float* part, const ConvGeom& g, be_dtype dt,
                    float beta, int num_sms, cudaStream_t s) {
   const int64_t npq = (int64_t)g.N * g.P * g.Q;
   const int RSC = g.R * g.S * g.C;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(4LL * num_sms, (npq + 63) / 64));
+  BE_REQUIRE(g.R == 3 && g.S == 3 && (g.stride == 1 || g.stride == 2), BE_E_UNSUPPORTED,
+             "depthwise conv: 3x3 filters, stride 1|2");
+  BE_REQUIRE(g.C / 8 <= 256, BE_E_UNSUPPORTED, "depthwise conv: C <= 2048");
+  const int64_t blocks = dw_wgrad_blocks(g, num_sms);
   const int64_t ppb = (npq + blocks - 1) / blocks;
-  const int C8 = g.C / 8;
-  BE_REQUIRE(g.R == 3 && g.S == 3, BE_E_UNSUPPORTED, "depthwise conv: 3x3 filters only");
-  BE_REQUIRE(C8 <= 256, BE_E_UNSUPPORTED, "depthwise conv: C <= 2048");
-  const int npl = 256 / C8;
-  const size_t smem = (size_t)npl * C8 * 9 * 8 * sizeof(float);
+  const int block = dw_block(g.C);
+  const size_t smem = (size_t)block * 72 * sizeof(float);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dw_wgrad_partial_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(dw_wgrad_partial_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(dw_wgrad_partial_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(dw_wgrad_partial_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(dw_wgrad_partial_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
   if (npq > 0) {
-    launch_pdl(dw_wgrad_partial_kernel<9>, (unsigned)blocks, 256, smem, s, dy, x, part, g, dt, ppb);
+    const bool bf = dt == BE_BF16;
+    if (g.stride == 1 && bf) launch_pdl(dw_wgrad_partial_kernel<1, true>, (unsigned)blocks, block, smem, s, dy, x, part, g, ppb);
+    else if (g.stride == 1) launch_pdl(dw_wgrad_partial_kernel<1, false>, (unsigned)blocks, block, smem, s, dy, x, part, g, ppb);
+    else if (bf) launch_pdl(dw_wgrad_partial_kernel<2, true>, (unsigned)blocks, block, smem, s, dy, x, part, g, ppb);
+    else launch_pdl(dw_wgrad_partial_kernel<2, false>, (unsigned)blocks, block, smem, s, dy, x, part, g, ppb);
     after_launch("dw_wgrad_partial");
   } else {
     cudaMemsetAsync(part, 0, (size_t)blocks * RSC * sizeof(float), s);

@@ -322,9 +322,11 @@ static void vjp_bn(Node* n, GradSink& sink) {
   float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
   float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
   const int bact = residual ? 0 : act;  // with a residual the mask is already in gz
+  const bool bits = n->iattr[2] != 0;  // saved[4] is the 1-bit residual mask
   k::bn_bwd(gz->data(), x->data(), bact ? y->data() : nullptr, bact, dx ? dx->data() : nullptr, rows, C, x->dtype,
             mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s,
-            bact ? bshift->ptr<float>() : nullptr, gmask ? y->data() : nullptr, gmask ? gmask->data() : nullptr);
+            bact ? bshift->ptr<float>() : nullptr, gmask && !bits ? y->data() : nullptr,
+            gmask ? gmask->data() : nullptr, gmask && bits ? y->ptr<uint8_t>() : nullptr);
   if (gmask) gz = std::move(gmask);  // sole reference: the shortcut adopts it without a copy
   if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
   if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
@@ -374,15 +376,24 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   if (rm) rm->bump_version();
   if (rv) rv->bump_version();
   TRef y = new_tensor(x->shape, x->rank, x->dtype);
+  // residual block output relu(bn(x) + r): the backward needs only the sign of
+  // y — a 1-bit mask written by the apply pass (1/16 of y's bytes to re-read)
+  const bool want_grad = grad_enabled() && (x->requires_grad || gamma->requires_grad || beta->requires_grad ||
+                                            (res && res->requires_grad));
+  TRef bits;
+  if (res && a.act == 1 && want_grad && k::bn_mask_bits_ok(x->data(), y->data(), res->data(), rows, C, x->dtype))
+    bits = new_tensor({rows * (C / 8)}, BE_U8);
   k::bn_apply(x->data(), y->data(), rows, C, x->dtype, mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(),
-              beta->ptr<float>(), a.act, s, res ? res->data() : nullptr);
+              beta->ptr<float>(), a.act, s, res ? res->data() : nullptr, bits ? bits->ptr<uint8_t>() : nullptr);
   Node* n = res ? new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta, res})
                 : new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
   if (n) {
-    save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, a.act ? y.get() : nullptr);
+    save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma);
+    save(n, bits ? bits.get() : (a.act ? y.get() : nullptr));
     save(n, beta);
     n->iattr[0] = a.act;
     n->iattr[1] = res != nullptr;
+    n->iattr[2] = bits ? 1 : 0;
     set_output(n, y.get(), 0);
     finish_node(n);
   }
