@@ -275,17 +275,28 @@ def run_ours(args, cfg, rank, world, local_rank):
         idle.append((time.perf_counter() - ta) * 1e3)
     be.synchronize()
     host_idle_ms = statistics.median(idle)
+    loss = None
     for _ in range(args.warmup):
-        step(batch)
+        loss = step(batch)  # held like the timed loop does (the previous loss stays alive one step)
     be.synchronize()
-    stats_warm = be.alloc_stats()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         be.synchronize()
-
+    # settle: the allocator's pools reach their steady state when a step that
+    # starts from a synchronised GPU (as the timed region does) makes no new
+    # cudaMalloc; at most 10 such extra warm-up steps
+    settle = 0
+    for settle in range(1, 11):
+        barrier()
+        a0 = be.alloc_stats()["raw_alloc_count"]
+        loss = step(batch)
+        loss = step(batch)
+        be.synchronize()
+        if be.alloc_stats()["raw_alloc_count"] == a0:
+            break
     stats_warm = be.alloc_stats()
     trace = bool(os.environ.get("BE_ALLOC_TRACE"))
 
@@ -509,7 +520,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
-        "alloc": {"raw_alloc_count_delta_timed": stats_timed["raw_alloc_count"] - stats_warm["raw_alloc_count"],
+        "alloc": {"settle_steps": settle,
+                  "raw_alloc_count_delta_timed": stats_timed["raw_alloc_count"] - stats_warm["raw_alloc_count"],
                   "raw_alloc_count_delta_all_passes": stats_after["raw_alloc_count"] - stats_warm["raw_alloc_count"],
                   "peak_bytes_in_use": stats_after["peak_bytes_in_use"]},
         "final_loss": final_loss,

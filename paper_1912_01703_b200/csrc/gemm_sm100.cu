@@ -2198,6 +2198,19 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, con
   }
 }
 
+// Copy a [rows, cols] matrix (row stride lds) into a buffer with row stride
+// ldd ≥ cols, zero-filling columns [cols, ldd): operands whose rows are not
+// 16-byte multiples (e.g. an N = 10 head) become TMA-describable.
+template <typename T>
+__global__ void pad_rows_kernel(const T* __restrict__ src, long long lds, T* __restrict__ dst, long long ldd,
+                                long long rows, long long cols) {
+  pdl_entry();
+  const long long total = rows * ldd;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ldd, c = i % ldd;
+    dst[i] = c < cols ? src[r * lds + c] : T(0);
+  }
+}
 __global__ void splitk_reduce(const float* __restrict__ ws, int splits, long long sstride, int M, int N, void* D, long long ldd,
                               int d_f32, float beta, const float* bias, int act) {
   pdl_entry();
@@ -3163,6 +3176,35 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
     }
     if (tmp) ctx().alloc.free(tmp);  // stream-ordered reuse is safe
     return "tcgen05";
+  }
+  if (g.K > 0 && g.N > 1 && g.K > 1 && !g.conv_x && !g.upd) {
+    // TMA-indescribable operand rows (not 16-B multiples, e.g. a 10-class
+    // head): pad them into temporaries and stay on the tcgen05 path
+    const int es = x3 ? 4 : 2, q = 16 / es;
+    GemmDesc gp = g;
+    Block* tmpa = nullptr;
+    Block* tmpb = nullptr;
+    auto pad = [&](const void* src, int64_t ld, bool kmajor, int MN, Block** blk, int64_t* ldo) -> const void* {
+      const int64_t rows = kmajor ? MN : g.K, cols = kmajor ? g.K : MN;
+      const int64_t ldp = (cols + q - 1) / q * q;
+      *blk = ctx().alloc.allocate((size_t)(rows * ldp) * es, s);
+      const int blocks = (int)std::min<long long>((rows * ldp + 255) / 256, (long long)ctx().num_sms * 16);
+      if (x3)
+        launch_pdl(pad_rows_kernel<float>, blocks, 256, 0, s, (const float*)src, (long long)ld, (float*)(*blk)->ptr,
+                   (long long)ldp, (long long)rows, (long long)cols);
+      else
+        launch_pdl(pad_rows_kernel<uint16_t>, blocks, 256, 0, s, (const uint16_t*)src, (long long)ld,
+                   (uint16_t*)(*blk)->ptr, (long long)ldp, (long long)rows, (long long)cols);
+      after_launch("gemm_pad_operand");
+      *ldo = ldp;
+      return (*blk)->ptr;
+    };
+    if (!tma_ok(g.A, g.lda, g.ab)) gp.A = pad(g.A, g.lda, g.a_kmajor, g.M, &tmpa, &gp.lda);
+    if (!tma_ok(g.B, g.ldb, g.ab)) gp.B = pad(g.B, g.ldb, g.b_kmajor, g.N, &tmpb, &gp.ldb);
+    const char* r = gemm(gp, s);
+    if (tmpa) ctx().alloc.free(tmpa);  // stream-ordered reuse is safe
+    if (tmpb) ctx().alloc.free(tmpb);
+    return r;
   }
   if (g.N == 1 || g.K == 1) {
     g_simt_calls++;

@@ -241,8 +241,17 @@ Block* CachingAllocator::allocate(size_t nbytes, cudaStream_t s) {
   }
   static const bool trace = getenv("BE_ALLOC_TRACE") != nullptr;
   if (trace) {  // debug: who grows the pool (size, stream, native call stack)
-    fprintf(stderr, "be raw alloc #%llu: %zu B on stream %p\n", (unsigned long long)st_.raw_alloc_count + 1, sz,
-            (void*)s);
+    size_t same_other = 0, defer_same = 0, defer_other = 0;
+    for (auto& kv : pools_)
+      if (kv.first != s) {
+        auto it2 = kv.second.find(sz);
+        if (it2 != kv.second.end()) same_other += it2->second.size();
+      }
+    for (auto& d : deferred_)
+      if (d.b->size == sz) (d.b->stream == s ? defer_same : defer_other)++;
+    fprintf(stderr, "be raw alloc #%llu: %zu B on stream %p (free on other streams %zu, deferred same-stream %zu, "
+            "deferred other %zu, deferred total %zu)\n", (unsigned long long)st_.raw_alloc_count + 1, sz, (void*)s,
+            same_other, defer_same, defer_other, deferred_.size());
     void* bt[16];
     backtrace_symbols_fd(bt, backtrace(bt, 16), 2);
   }

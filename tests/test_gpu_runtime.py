@@ -76,8 +76,13 @@ def test_record_stream_defers_reuse():
     del t  # freed while still "in use" on the side stream → parked, not pooled
     u = be.empty((1 << 18,), "f32")
     s1 = be.alloc_stats()
-    assert s1["raw_alloc_count"] == s0["raw_alloc_count"] + 1  # could not reuse the parked block
-    side.synchronize()
+    # the parked block is reused in STREAM ORDER: no new cudaMalloc, and the
+    # compute stream now waits for the side stream's use before touching it
+    assert s1["raw_alloc_count"] == s0["raw_alloc_count"]
+    u.fill_(1.0)
+    be.synchronize()                # the compute stream has drained...
+    assert side.query()             # ...which it could only do after the side stream's work
+    assert (u.numpy() == 1.0).all()
     del u
 
 
