@@ -116,7 +116,13 @@ def test_conv_op_fp32(cfg, act):
                                  (1, 8, 224, 224, 64, 11, 4, 2),
                                  # shared-patch stride-1 kernel (C = K = 64): ResNet layer-1 size, ragged row groups
                                  (2, 64, 56, 56, 64, 3, 1, 1), (1, 64, 30, 20, 64, 3, 1, 1), (2, 64, 12, 12, 64, 2, 1, 0),
-                                 (2, 32, 8, 8, 160, 3, 2, 1), (1, 8, 6, 6, 16, 5, 1, 0)])
+                                 (2, 32, 8, 8, 160, 3, 2, 1), (1, 8, 6, 6, 16, 5, 1, 0),
+                                 # TMA-im2col kernel at ResNet layer-2/3/4 and VGG shapes (C ≥ 128), ragged
+                                 # rows and columns, K = 512 (two N tiles), 1×1 and 2×2 filters
+                                 (2, 128, 28, 28, 128, 3, 1, 1), (2, 256, 14, 14, 256, 3, 1, 1),
+                                 (1, 512, 7, 7, 512, 3, 1, 1), (1, 128, 60, 50, 128, 3, 1, 1),
+                                 (1, 128, 13, 11, 256, 3, 1, 1), (2, 256, 20, 9, 128, 3, 1, 1),
+                                 (1, 192, 17, 30, 128, 2, 1, 0), (3, 128, 9, 9, 256, 1, 1, 0)])
 def test_conv_op_bf16_implicit_gemm(cfg):
     """bf16 conv forward through the implicit-GEMM kernel (cp.async gather, no
     im2col) vs the oracle on the same bf16-rounded x and W: fp32 accumulate,
