@@ -4,13 +4,14 @@
 //
 // The four passes are HBM-bound (ResNet-50 b256: 2.85 G activation elements
 // per step through BN, ≈48 GB of traffic).  Each block owns a contiguous row
-// range [r0, r1) of the [rows, C] tensor (C a power of two ≤ 2048), i.e. a
+// range [r0, r1) of the [rows, C] tensor (C a multiple of 8, ≤ 2048), i.e. a
 // contiguous byte range per input stream: one producer warp moves it into a
 // shared-memory ring with 1-D cp.async.bulk copies (ITERS × 4 KB chunks per
 // stream, NST stages, mbarrier complete_tx), so ≈64 KB per block (≈190 KB
 // per SM) are in flight without any per-thread load issue; 8 consumer warps
 // read their 16 B (8 channels of one row: thread t ↔ byte t·16 of every
-// 4 KB = 2048/C rows) from smem.  Outputs (y, dx, the masked gradient) are
+// ⌊256/(C/8)⌋ rows, ≤ 4 KB; when C/8 does not divide 256 the last
+// 256 mod (C/8) consumer threads idle — MobileNetV2's 24 … 1280 channels) from smem.  Outputs (y, dx, the masked gradient) are
 // direct 16-B coalesced stores.  Reductions finish with the same fixed-order
 // per-block combine as the register kernels (deterministic partials).
 #include <cuda_runtime.h>
@@ -417,7 +418,7 @@ bool enabled() {
 }  // namespace
 
 bool bn_stream_ok(const void* a, int64_t rows, int C) {
-  return enabled() && C >= 8 && C <= 2048 && (C & (C - 1)) == 0 && rows > 0 && aligned16(a);
+  return enabled() && C >= 8 && C <= 2048 && C % 8 == 0 && rows > 0 && aligned16(a);
 }
 
 bool relu_colsum_stream(const uint16_t* gy, const uint16_t* y, uint16_t* dz, int64_t rows, int C, float* out,

@@ -18,7 +18,7 @@
 namespace be { namespace k {
 using namespace be::dev;
 
-// bn_stream.cu: TMA-bulk streaming BN passes (bf16, C a power of two ≤ 2048)
+// bn_stream.cu: TMA-bulk streaming BN passes (bf16, C % 8 == 0, C ≤ 2048)
 bool bn_stream_ok(const void* a, int64_t rows, int C);
 int64_t bn_stream_splits(int64_t rows, int C, int64_t cap);
 void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s);
