@@ -76,6 +76,11 @@ struct __align__(64) GemmParams {
   int b_shift, sh_wb, sh_hb, sh_pg;  // sh_pg = p-groups per image
   // TMA-store epilogue: D (or the split-K workspace) as [rows, N], box 32×32
   int tma_store;
+  // epilogue split by tile instead of by column half (BN = 64, no stats): the
+  // warp pair of each TMEM lane quarter takes alternate tiles, each pair owns
+  // one accumulator buffer — two tiles' epilogues in flight for the narrow
+  // outputs (MobileNet's 16–64-channel 1×1 convs) where a tile is one chunk
+  int epi_split;
   CUtensorMap td;
   // fused SGD epilogue (kernels.h SgdFuse): acc = gradient of P[M, N]
   int upd;
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
-      sm100::mbar_init(&tempty[a], UPD ? kUpdWarps : kEpiWarps);
+      sm100::mbar_init(&tempty[a], UPD ? kUpdWarps : (p.epi_split ? kEpiWarps / 2 : kEpiWarps));
     }
     if (UPD)
       for (int i = 0; i < kUpdWarps * kUpdBufs; ++i) sm100::mbar_init(&ubar[i], 1);
@@ -619,6 +624,38 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     ColStats<(BN / 64 > 2 ? BN / 64 : 2)> cst;
     cst.reset();
     const bool vec_ok = (p.ldd % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.D) & 15) == 0);
+    if (BN == 64 && p.epi_split) {
+      // tile-split epilogue: pair eh takes this CTA's tiles eh, eh + 2, … —
+      // exactly the tiles the MMA warp accumulates into buffer eh
+      uint32_t ph = 0;
+      for (int t = blockIdx.x + eh * (int)gridDim.x; t < num_tiles; t += 2 * (int)gridDim.x, ph ^= 1u) {
+        const int mn = t % mn_tiles, sp = t / mn_tiles;
+        const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
+        char* Dbase = reinterpret_cast<char*>(p.D) + (long long)sp * p.split_stride * 4;
+        sm100::mbar_wait(&tfull[eh], ph);
+        sm100::tc_fence_after();
+        const int row = tm * BM + eq * 32 + lane;
+        const bool row_ok = row < p.M;
+        const int store_row = sp * p.split_rows + tm * BM + eq * 32;
+        const int col0 = tn * BN, col1 = col0 + 32;
+        const bool h1 = col1 < p.N;
+        const uint32_t ta = tmem_base + eh * BN + ((uint32_t)(eq * 32) << 16);
+        uint32_t r0[32], r1[32];
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&tempty[eh]);  // accumulator free before the stores
+        if (p.tma_store) {
+          epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col0, r0);
+          if (h1) epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col1, r1);
+        } else if (row_ok) {
+          epi_store32(p, Dbase, vec_ok, row, col0, r0);
+          if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
+        }
+      }
+    } else
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int mn = t % mn_tiles, sp = t / mn_tiles;
       const int tm = mn % p.tiles_m, tn = mn / p.tiles_m;
@@ -659,12 +696,14 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         }
       }
       } else {
+      // column pieces of 64 interleaved between the two warps of a lane
+      // quarter (a ragged N such as 144 stays balanced); BN = 64: 32 each
       #pragma unroll 1
-      for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
-        const int c0 = eh * (BN / 2) + it * 64;
+      for (int it = 0; it < (BN >= 128 ? BN / 128 : 1); ++it) {
+        const int c0 = BN >= 128 ? (2 * it + eh) * 64 : eh * 32;
         // two TMEM loads in flight per wait (warp-uniform predicates)
         const int col0 = tn * BN + c0, col1 = col0 + 32;
-        const bool h0 = col0 < p.N, h1 = col1 < p.N && c0 + 32 < (eh + 1) * (BN / 2);
+        const bool h0 = col0 < p.N, h1 = BN >= 128 && col1 < p.N;
         if (!h0) break;
         const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
         uint32_t r0[32], r1[32];
@@ -2233,6 +2272,10 @@ __global__ void splitk_reduce(const float* __restrict__ ws, int splits, long lon
   }
 }
 
+inline int splitk_blocks(long long total) {
+  return (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
+}
+
 // ---------------------------------------------------------------- skinny shapes (N = 1 / K = 1)
 // Heads such as NCF's [B, 128]·[128, 1] have row strides TMA cannot describe
 // (2 B) and almost no work; the 64×64 SIMT tiles wasted ≥ 98 % of their lanes
@@ -2586,6 +2629,8 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   else setup_store(p, p.D, p.d_f32 != 0, splits > 1 ? (long long)splits * p.split_rows : g.M, g.N, p.ldd);
   const int grid = std::min(mn * splits, sms);
   set_stats(p, g, grid);
+  static const int split_on = [] { const char* e = getenv("BE_EPI_SPLIT"); return e ? atoi(e) : 1; }();
+  p.epi_split = (BN == 64 && !X3 && !g.upd && !p.stats && split_on) ? 1 : 0;
   const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es +
                            (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
@@ -2611,8 +2656,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   after_launch("gemm_tc");
   if (ws) {
     const long long total = (long long)g.M * g.N;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-    launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
+    launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -2667,8 +2711,7 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   after_launch("gemm_tc2");
   if (ws) {
     const long long total = (long long)g.M * g.N;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-    launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
+    launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.M, g.N, g.D, g.ldd,
                                          g.d == BE_F32, g.beta, g.bias, g.act);
     after_launch("gemm_splitk_reduce");
     ctx().alloc.free(ws);
@@ -2851,8 +2894,7 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
   after_launch("conv_wgrad_patch");
   g_tc_calls++;
   const long long total = (long long)g.K * RSC;
-  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-  launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
+  launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits, p.split_stride, g.K, RSC, dw,
                                        RSC, 1, beta, nullptr, 0);
   after_launch("conv_wgrad_patch_reduce");
   ctx().alloc.free(ws);
@@ -2895,8 +2937,7 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   after_launch("conv_wgrad_stem");
   g_tc_calls++;
   const long long total = 64LL * RSC;
-  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-  launch_pdl(splitk_reduce, blocks, 256, 0, s, reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw, RSC,
+  launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, reinterpret_cast<const float*>(ws->ptr), grid, p.split_stride, 64, RSC, dw, RSC,
                                        1, beta, nullptr, 0);
   after_launch("conv_wgrad_stem_reduce");
   ctx().alloc.free(ws);
@@ -3134,7 +3175,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       // when the tile grid under-fills the 148 SMs, BN=256 / BN=128 with
       // split-K sized to fill the machine.
       struct Cand { int kind, bn, splits; };
-      Cand cands[5];
+      Cand cands[6];
       int nc = 0;
       cands[nc++] = {0, bn, 0};
       const int pm = pair_mode();
@@ -3147,6 +3188,11 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       static const int epi4 = [] { const char* e = getenv("BE_GEMM_EPI4"); return e ? atoi(e) : -1; }();
       const int tiles_bn = ((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn);
       if (epi4 != 0 && kbl <= 8 && tiles_bn >= sms) cands[nc++] = {2, bn, 0};
+      // short K, narrow N (MobileNet's 1×1 convs): one tile covering all of N
+      // reads A once — the wave-efficiency rule counts MMA work, which these
+      // HBM-bound shapes do not spend (N = 144 → three BN = 64 tiles re-read A)
+      const int bn_cover = g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256);
+      if (kbl <= 8 && g.N <= 256 && bn_cover != bn) cands[nc++] = {0, bn_cover, 0};
       for (int cbn : {256, 128}) {
         if (g.stats) break;  // split-K cannot carry the statistics epilogue
         const int tiles = ((g.M + BM - 1) / BM) * ((g.N + cbn - 1) / cbn);
@@ -3244,8 +3290,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       else launch_pdl(gemv_mnmajor_kernel<float>, grid, 256, 0, s, g.M, g.K, (const float*)g.A, (long long)g.lda,
                       (const float*)g.B, bs, kchunk, wsp);
       after_launch("gemm_gemv_mn");
-      const int blocks = (int)std::min<long long>((g.M + 255) / 256, (long long)ctx().num_sms * 16);
-      launch_pdl(splitk_reduce, blocks, 256, 0, s, (const float*)wsp, splits, (long long)g.M, g.M, 1, g.D, (long long)g.ldd,
+      launch_pdl(splitk_reduce, splitk_blocks((long long)g.M), 256, 0, s, (const float*)wsp, splits, (long long)g.M, g.M, 1, g.D, (long long)g.ldd,
                  (int)(g.d == BE_F32), g.beta, g.bias, g.act);
       after_launch("gemm_gemv_reduce");
       ctx().alloc.free(ws);
@@ -3278,8 +3323,7 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
   after_launch("gemm_simt");
   if (ws) {
     const long long total = (long long)g.M * g.N;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)ctx().num_sms * 16);
-    launch_pdl(splitk_reduce, blocks, 256, 0, s, wsp, splits, total, g.M, g.N, g.D, g.ldd, g.d == BE_F32, g.beta, g.bias,
+    launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, wsp, splits, total, g.M, g.N, g.D, g.ldd, g.d == BE_F32, g.beta, g.bias,
                                          g.act);
     after_launch("gemm_simt_splitk_reduce");
     ctx().alloc.free(ws);

@@ -154,3 +154,28 @@ def test_gemm_four_slot_epilogue(tmp_path):
     out = subprocess.run([sys.executable, str(f), root], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) < 8e-3
+
+
+@pytest.mark.parametrize("M,N,K,act,beta,out", [(50000, 16, 96, 0, 0.0, "bf16"), (40000, 24, 144, 1, 0.0, "bf16"),
+                                                (30011, 64, 32, 0, 1.0, "bf16"), (20000, 40, 70, 1, 0.0, "f32"),
+                                                (60000, 144, 24, 0, 0.0, "bf16"), (9000, 200, 64, 1, 1.0, "f32")])
+def test_gemm_narrow_outputs_tile_split_epilogue(M, N, K, act, beta, out):
+    """Narrow outputs (BN = 64: the tile-split epilogue, each warp pair taking
+    alternate tiles) and ragged N on wider tiles (interleaved 64-column
+    pieces), many tiles per CTA, bias / ReLU / beta-accumulate, bf16 and fp32
+    outputs — vs float64 at the output's storage rounding."""
+    be = be_init()
+    rng = np.random.default_rng(M + N + K)
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(a.astype(np.float32)))  # noqa: E731
+    a, b = q(rng.standard_normal((M, K))), q(rng.standard_normal((N, K)))
+    bias = rng.standard_normal(N).astype(np.float32)
+    d0 = q(rng.standard_normal((M, N)))
+    D = be.tensor(d0, dtype=out if out == "bf16" else None)
+    be.gemm(be.tensor(a, dtype="bf16"), be.tensor(b, dtype="bf16"), D, trans_b=True, bias=be.tensor(bias), act=act,
+            beta=beta)
+    ref = a.astype(np.float64) @ b.T.astype(np.float64) + bias
+    if act:
+        ref = np.maximum(ref, 0)
+    ref = ref + beta * d0
+    assert rel(D.numpy(), ref) < (8e-3 if out == "bf16" else 1e-5)

@@ -11,7 +11,9 @@ import paper_1912_01703_b200 as be  # noqa: E402
 be.init(0)
 shapes = [(802816, 256, 64, 0, 1), (200704, 512, 128, 0, 1), (50176, 1024, 256, 0, 1), (802816, 64, 256, 0, 1),
           (802816, 64, 64, 0, 1), (200704, 128, 512, 0, 1), (50176, 256, 1024, 0, 1), (802816, 128, 256, 0, 1)]
-if len(sys.argv) > 1:
+if len(sys.argv) > 1 and "x" in sys.argv[1]:
+    shapes = [tuple(map(int, a.split("x"))) + (0, 1) for a in sys.argv[1:]]
+elif len(sys.argv) > 1:
     shapes = shapes[:int(sys.argv[1])]
 HBM = 6547.2e9
 rng = np.random.default_rng(0)
