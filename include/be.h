@@ -146,9 +146,13 @@ typedef enum {
   BE_OP_DROPOUT = 19,      /* in: x (contiguous f32|bf16); attrs be_dropout_attrs; out: y = x·keep/(1−p) (
                               PAPER.md:64).  keep_i = (Philox4x64-10(counter (i/4, offset, 0, 0), key (seed, 0))[i%4] >> 32)
                               >= floor(p·2^32), i the row-major element index — regenerated in backward, no mask stored */
-  BE_OP_CONV2D_DEPTHWISE = 20 /* in: x NHWC[N,H,W,C] (C % 8 == 0), w f32 RSC [3,3,C]; attrs be_dwconv_attrs;
+  BE_OP_CONV2D_DEPTHWISE = 20, /* in: x NHWC[N,H,W,C] (C % 8 == 0), w f32 RSC [3,3,C]; attrs be_dwconv_attrs;
                               out NHWC[N,P,Q,C]: y[n,p,q,c] = Σ_{r,s} x[n, p·st−pad+r, q·st−pad+s, c]·w[r,s,c]
                               (MobileNet's depthwise conv, Table 1; oracle conv2d_depthwise) */
+  BE_OP_BN_CONV1X1 = 21   /* in: x NHWC[N,H,W,C] bf16, gamma[C], beta[C], running_mean[C]?, running_var[C]?, w KRSC
+                              [K,1,1,C]; attrs be_bn_attrs (act 0|1|2, residual 0); out NHWC[N,H,W,K] = conv1x1(act(bn(x)), w):
+                              the batch norm (train mode, as BE_OP_BATCHNORM2D) applied inside the GEMM's operand load — its
+                              output never reaches HBM ("convolution, batch normalization") */
 } be_op_id;
 
 typedef struct { int act; /* 0 none, 1 relu */ int out_f32; /* 1: fp32 output even in bf16 mode */ } be_linear_attrs;

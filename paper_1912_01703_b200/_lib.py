@@ -24,7 +24,7 @@ ERRORS = {
 }
 OPS = dict(LINEAR=1, MATMUL=2, ADD=3, MUL=4, RELU=5, SOFTMAX_XENT=6, BCE_LOGITS=7, CONV2D=8, MAXPOOL2D=9,
            AVGPOOL_GLOBAL=10, BATCHNORM2D=11, RESHAPE=12, EMBEDDING=13, CONCAT=14, SUM=15, MEAN=16, CAST=17,
-           ADD_RELU=18, DROPOUT=19, CONV2D_DEPTHWISE=20)
+           ADD_RELU=18, DROPOUT=19, CONV2D_DEPTHWISE=20, BN_CONV1X1=21)
 
 
 class BeError(RuntimeError):

@@ -291,6 +291,14 @@ def batchnorm2d(x, gamma, beta, running_mean=None, running_var=None, eps=1e-5, m
     return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act), int(residual is not None)))
 
 
+def bn_conv1x1(x, gamma, beta, running_mean, running_var, w, eps=1e-5, momentum=0.1, act=1):
+    """conv1x1(act(batchnorm2d(x)), w) with the normalise + activation applied
+    inside the GEMM's operand load (BE_OP_BN_CONV1X1): the BN output never
+    reaches HBM.  w: KRSC [K, 1, 1, C]."""
+    ins = [x, gamma, beta] + ([running_mean, running_var] if running_mean is not None else []) + [w]
+    return _op("BN_CONV1X1", ins, L.be_bn_attrs(eps, momentum, int(act), 0))
+
+
 def reshape(x, shape):
     a = L.be_shape_attrs(len(shape), (C.c_int64 * 6)(*shape))
     return _op("RESHAPE", [x], a)

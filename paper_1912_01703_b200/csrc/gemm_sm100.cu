@@ -81,6 +81,11 @@ struct __align__(64) GemmParams {
   // one accumulator buffer — two tiles' epilogues in flight for the narrow
   // outputs (MobileNet's 16–64-channel 1×1 convs) where a tile is one chunk
   int epi_split;
+  // operand transform (XF kernels): v ← act(γ_c·(v − μ_c)·is_c + β_c) on the
+  // A tile (xf_op 1: K-major, channel = k) or the B tile (xf_op 2: MN-major,
+  // channel = n), channel c < xf_C (else 0)
+  int xf_op, xf_act, xf_C;
+  const float *xf_mean, *xf_invstd, *xf_gamma, *xf_beta;
   CUtensorMap td;
   // fused SGD epilogue (kernels.h SgdFuse): acc = gradient of P[M, N]
   int upd;
@@ -113,7 +118,10 @@ constexpr int kUpdWarpBytes = kUpdBufs * kUpdBufBytes;
 // warp = NSLOT − 1).  4 for store-heavy short-K shapes (the 1×1 convs: the
 // epilogue, not the mainloop, is the critical path), 2 otherwise (more
 // mainloop stages for long K).
-template <int BN, bool X3, bool UPD = false, int NSLOT = 2>
+// XF: the operand-transform variant (a batch norm's normalise + activation
+// applied to the A (K-major, channel = k) or B (MN-major, channel = n) tile in
+// shared memory between the TMA load and the MMA; see gemm_tc_kernel).
+template <int BN, bool X3, bool UPD = false, int NSLOT = 2, bool XF = false>
 struct Cfg {
   static constexpr int ESIZE = X3 ? 4 : 2;
   static constexpr int BK = 128 / ESIZE;           // one 128-B swizzle row of K
@@ -123,10 +131,11 @@ struct Cfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
   static constexpr int EPI_BYTES = UPD ? kUpdWarps * kUpdWarpBytes : kEpiWarps * NSLOT * 2048;
-  static constexpr int STAGES_RAW = (226 * 1024 - EPI_BYTES - 1280) / STAGE_BYTES;
+  static constexpr int XF_BYTES = XF ? 8 * 8 + 2 * 2048 * 4 : 0;  // xfull barriers + per-channel scale/shift (C ≤ 2048)
+  static constexpr int STAGES_RAW = (226 * 1024 - EPI_BYTES - XF_BYTES - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + XF_BYTES + 1024 + 256;
   static constexpr int CH = 128 / ESIZE;           // MN elements per 128-B chunk
 };
 
@@ -461,10 +470,10 @@ __device__ __forceinline__ void upd_epilogue(const GemmParams& p, uint8_t* epi_s
   if (lane == 0) sm100::bulk_wait<0>();  // stores complete before exit
 }
 
-template <int BN, bool X3, bool UPD = false, int NSLOT = 2>
+template <int BN, bool X3, bool UPD = false, int NSLOT = 2, bool XF = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
   pdl_entry();
-  using C = Cfg<BN, X3, UPD, NSLOT>;
+  using C = Cfg<BN, X3, UPD, NSLOT, XF>;
   static_assert(C::STAGES >= 2, "pipeline needs at least two stages");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -475,12 +484,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   uint64_t* tempty = tfull + 2;
   uint64_t* ubar = tempty + 2;  // UPD: one barrier per P/V buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ubar + (UPD ? kUpdWarps * kUpdBufs : 0));
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // XF: operand transformed
+  float* xpar = reinterpret_cast<float*>(xfull + 8);              // XF: [channel][scale, shift]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    if (XF)
+      for (int s = 0; s < C::STAGES; ++s) sm100::mbar_init(&xfull[s], 2);
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&tfull[a], 1);
       sm100::mbar_init(&tempty[a], UPD ? kUpdWarps : (p.epi_split ? kEpiWarps / 2 : kEpiWarps));
@@ -585,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         const int sp = t / mn_tiles;
         const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
-          sm100::mbar_wait(&full[stage], phase);
+          sm100::mbar_wait(XF ? &xfull[stage] : &full[stage], phase);
           sm100::tc_fence_after();
           const uint32_t sbase = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
 #pragma unroll
@@ -610,6 +623,76 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         }
         sm100::mma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (XF && (warp == 2 || warp == 3)) {
+    // ===================== operand transform (BN apply) =====================
+    // the 64 threads of warps 2–3: (1) once per CTA, scale/shift of every
+    // channel into smem; (2) walk the producer's stage sequence: wait for the
+    // TMA bytes, rewrite the operand tile in place (bf16 → fp32 affine → act →
+    // RN-even bf16; the SW128 chunk at physical slot j of row r holds logical
+    // chunk j ^ (r & 7)), four chunks per step with all loads first, make the
+    // generic-proxy writes visible to the tensor core (fence.proxy.async) and
+    // release the stage to the MMA warp
+    const int tid = threadIdx.x - 64;
+    for (int c = tid; c < p.xf_C; c += 64) {
+      const float sc = p.xf_gamma[c] * p.xf_invstd[c];
+      xpar[2 * c] = sc;
+      xpar[2 * c + 1] = p.xf_beta[c] - p.xf_mean[c] * sc;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const int cmax = p.xf_C;
+    int stage = 0; uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int mn = t % mn_tiles, sp = t / mn_tiles;
+      const int tn = mn / p.tiles_m;
+      const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks_total, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&full[stage], phase);
+        uint8_t* sa = smem + stage * C::STAGE_BYTES;
+        uint8_t* tile = p.xf_op == 1 ? sa : sa + C::A_BYTES;
+        const int nchunks = p.xf_op == 1 ? BM * 8 : BN * 8;
+        const int cbase = p.xf_op == 1 ? kb * C::BK : tn * BN;
+        for (int id0 = tid; id0 < nchunks; id0 += 256) {
+          uint4 u[4];
+          int ch[4];
+          uint4* q[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int id = id0 + 64 * v;
+            int r, c0;
+            if (p.xf_op == 1) {
+              r = id >> 3;
+              c0 = ((id & 7) ^ (r & 7)) * 8;
+            } else {
+              const int jb = id >> 9, rr = (id >> 3) & 63;
+              r = jb * 64 + rr;
+              c0 = jb * 64 + ((id & 7) ^ (rr & 7)) * 8;
+            }
+            ch[v] = cbase + c0;
+            q[v] = reinterpret_cast<uint4*>(tile + (size_t)r * 128 + (id & 7) * 16);
+            u[v] = id < nchunks ? *q[v] : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (id0 + 64 * v >= nchunks) break;
+            uint32_t w[4] = {u[v].x, u[v].y, u[v].z, u[v].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int c = ch[v] + 2 * i;
+              const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+              const float a = c < cmax ? be::dev::act_apply(fmaf(lo, xpar[2 * c], xpar[2 * c + 1]), p.xf_act) : 0.f;
+              const float b = c + 1 < cmax ? be::dev::act_apply(fmaf(hi, xpar[2 * c + 2], xpar[2 * c + 3]), p.xf_act)
+                                           : 0.f;
+              w[i] = pack_bf16x2(a, b);
+            }
+            *q[v] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        sm100::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&xfull[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (UPD && warp >= 4 && warp < 4 + kUpdWarps) {
@@ -2548,13 +2631,13 @@ double update_bytes(const GemmDesc& g) {
   return 8.0 + (g.upd->v ? 8.0 : 0.0) + (g.upd->shadow ? 2.0 : 0.0);
 }
 
-template <int BN, bool X3, int NSLOT = 2>
+template <int BN, bool X3, int NSLOT = 2, bool XF = false>
 void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo,
                cudaStream_t s, int force_splits = 0) {
-  using C = Cfg<BN, X3, false, NSLOT>;
+  using C = Cfg<BN, X3, false, NSLOT, XF>;
   static bool attr_set = false;
   if (!attr_set) {
-    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3, false, NSLOT>,
+    BE_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3, false, NSLOT, XF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
@@ -2631,6 +2714,10 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
   set_stats(p, g, grid);
   static const int split_on = [] { const char* e = getenv("BE_EPI_SPLIT"); return e ? atoi(e) : 1; }();
   p.epi_split = (BN == 64 && !X3 && !g.upd && !p.stats && split_on) ? 1 : 0;
+  if (XF) {
+    p.xf_op = g.xf_op; p.xf_act = g.xf_act; p.xf_C = g.xf_C;
+    p.xf_mean = g.xf_mean; p.xf_invstd = g.xf_invstd; p.xf_gamma = g.xf_gamma; p.xf_beta = g.xf_beta;
+  }
   const double es = X3 ? 4.0 : 2.0, ds = g.d == BE_F32 ? 4.0 : 2.0;
   const double alg_bytes = ((double)g.M * g.K + (double)g.N * g.K) * es +
                            (double)g.M * g.N * (g.upd ? update_bytes(g) : ds * (g.beta != 0.f ? 2 : 1));
@@ -2650,7 +2737,7 @@ void launch_tc(const GemmDesc& g, const void* a_hi, const void* a_lo, const void
       fail(BE_E_ARG, "gemm: the update epilogue runs on the bf16 kernel");
     }
   } else {
-    launch_pdl(gemm_tc_kernel<BN, X3, false, NSLOT>, grid, kThreads, C::SMEM, s, p);
+    launch_pdl(gemm_tc_kernel<BN, X3, false, NSLOT, XF>, grid, kThreads, C::SMEM, s, p);
   }
   prof_end(pidx, s);
   after_launch("gemm_tc");
@@ -3151,6 +3238,18 @@ const char* gemm(const GemmDesc& g, cudaStream_t s) {
       gx.lda = lda2; gx.ldb = ldb2; gx.a_kmajor = true; gx.b_kmajor = true;
     }
     const int bn = pick_bn(g.M, g.N, ctx().num_sms, x3);
+    if (g.xf_op) {
+      // BN-apply fused into the operand load: the 1-CTA kernel with its
+      // transform warps (tile and split rule as the default candidate)
+      BE_REQUIRE(!x3 && !g.upd && !g.conv_x && !g.stats && g.beta == 0.f &&
+                     ((g.xf_op == 1 && g.a_kmajor) || (g.xf_op == 2 && !g.b_kmajor)),
+                 BE_E_ARG, "gemm: operand transform needs bf16, K-major A (op 1) or MN-major B (op 2)");
+      if (bn == 256) launch_tc<256, false, 2, true>(g, ahi, alo, bhi, blo, s);
+      else if (bn == 128) launch_tc<128, false, 2, true>(g, ahi, alo, bhi, blo, s);
+      else launch_tc<64, false, 2, true>(g, ahi, alo, bhi, blo, s);
+      if (tmp) ctx().alloc.free(tmp);
+      return "tcgen05";
+    }
     if (x3) {
       if (bn == 128) launch_tc<128, true>(gx, ahi, alo, bhi, blo, s);
       else launch_tc<64, true>(gx, ahi, alo, bhi, blo, s);

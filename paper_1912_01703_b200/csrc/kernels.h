@@ -43,6 +43,12 @@ struct GemmDesc {
   // when the launched kernel produced them (left untouched otherwise)
   float* stats = nullptr;
   int* stats_parts = nullptr;
+  // operand transform (batch-norm apply fused into the GEMM's operand load):
+  // xf_op 1: A[m, k] ← act(γ_k·(A − μ_k)·is_k + β_k) (A K-major, bf16);
+  // xf_op 2: the same on B[n, k] per channel n (B MN-major, bf16);
+  // channels ≥ xf_C read 0 parameters.  1-CTA bf16 kernel only.
+  int xf_op = 0, xf_act = 0, xf_C = 0;
+  const float *xf_mean = nullptr, *xf_invstd = nullptr, *xf_gamma = nullptr, *xf_beta = nullptr;
 };
 struct SgdFuse {
   float* p = nullptr; float* v = nullptr; uint16_t* shadow = nullptr;

@@ -673,7 +673,8 @@ be_status be_op(int op_id, const be_tensor* in, int n_in, const void* attrs, be_
     case BE_OP_MAXPOOL2D:
     case BE_OP_AVGPOOL_GLOBAL:
     case BE_OP_BATCHNORM2D:
-    case BE_OP_EMBEDDING: op_cnn(op_id, in, n_in, attrs, out, n_out); break;
+    case BE_OP_EMBEDDING:
+    case BE_OP_BN_CONV1X1: op_cnn(op_id, in, n_in, attrs, out, n_out); break;
     case BE_OP_DROPOUT:
     case BE_OP_CONV2D_DEPTHWISE: op_mobile(op_id, in, n_in, attrs, out, n_out); break;
     default: fail(BE_E_UNSUPPORTED, "unknown op id " + std::to_string(op_id));

@@ -400,6 +400,135 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   out[0] = reinterpret_cast<be_tensor>(y.release());
 }
 
+// ------------------------------------------------------------------ batch norm → 1×1 conv (fused apply)
+// y = conv1x1(act(bn(x)), w) with the BN's normalise + activation applied to
+// the GEMM's A tile in shared memory ("normalise + ReLU in the
+// next conv's operand load") — the BN output is never written to HBM; the
+// backward recomputes it inside the weight-gradient GEMM's B tile and the BN
+// backward recomputes the activation mask from x (oracle: batchnorm2d → relu
+// → conv2d composed, oracle/ops.py).
+static void vjp_bn_conv(Node* n, GradSink& sink) {
+  cudaStream_t s = ctx().stream;
+  TRef hx, hmean, hinv, hg, hb, hw;
+  Tensor* x = unpack(n, 0, hx);
+  Tensor* mean = unpack(n, 1, hmean);
+  Tensor* inv = unpack(n, 2, hinv);
+  Tensor* gamma = unpack(n, 3, hg);
+  Tensor* beta = unpack(n, 4, hb);
+  Tensor* w = unpack(n, 5, hw);  // bf16 [K, 1, 1, C]
+  const int act = (int)n->iattr[0];
+  const int C = (int)x->shape[3], K = (int)w->shape[0];
+  const int64_t rows = x->numel() / C;
+  TRef gz = contiguous_like(sink.upstream[0], BE_BF16);
+  // 1. dW[K, C] = dYᵀ · act(bn(x))  (the BN output rebuilt in the B tile)
+  if (sink.needs(3)) {
+    float bw;
+    Tensor* dw = sink.dest(3, &bw);
+    TRef tmp;
+    if (bw != 0.f) tmp = new_tensor({(int64_t)K, (int64_t)C}, BE_F32);
+    k::GemmDesc gd;
+    gd.M = K; gd.N = C; gd.K = (int)rows;
+    gd.A = gz->data(); gd.lda = K; gd.a_kmajor = false;
+    gd.B = x->data(); gd.ldb = C; gd.b_kmajor = false;
+    gd.ab = BE_BF16; gd.D = tmp ? tmp->data() : dw->data(); gd.ldd = C; gd.d = BE_F32;
+    gd.xf_op = 2; gd.xf_act = act; gd.xf_C = C;
+    gd.xf_mean = mean->ptr<float>(); gd.xf_invstd = inv->ptr<float>();
+    gd.xf_gamma = gamma->ptr<float>(); gd.xf_beta = beta->ptr<float>();
+    k::gemm(gd, s);
+    if (tmp) k::axpby(tmp->data(), BE_F32, dw->data(), BE_F32, (int64_t)K * C, 1.f, 1.f, s);
+    sink.commit(3);
+  }
+  if (!sink.needs(0) && !sink.needs(1) && !sink.needs(2)) return;
+  // 2. dZ[rows, C] = dY · W  (gradient w.r.t. the BN output)
+  TRef dz = new_tensor({rows, (int64_t)C}, BE_BF16);
+  {
+    k::GemmDesc gd;
+    gd.M = (int)rows; gd.N = C; gd.K = K;
+    gd.A = gz->data(); gd.lda = K; gd.a_kmajor = true;
+    gd.B = w->data(); gd.ldb = C; gd.b_kmajor = false;
+    gd.ab = BE_BF16; gd.D = dz->data(); gd.ldd = C; gd.d = BE_BF16;
+    k::gemm(gd, s);
+  }
+  gz = TRef();
+  // 3. the BN backward of dZ, activation mask recomputed from x (as vjp_bn)
+  float bg = 0.f, bb = 0.f;
+  Tensor* dg = sink.needs(1) ? sink.dest(1, &bg) : nullptr;
+  Tensor* db = sink.needs(2) ? sink.dest(2, &bb) : nullptr;
+  TRef tg, tb;
+  float gb_beta = 0.f;
+  if (dg && db && bg == bb) gb_beta = bg;
+  else {
+    if (dg && bg != 0.f) { tg = new_tensor({C}, BE_F32); }
+    if (db && bb != 0.f) { tb = new_tensor({C}, BE_F32); }
+  }
+  TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+  float bx = 0.f;
+  Tensor* dx = sink.needs(0) ? sink.dest(0, &bx) : nullptr;
+  TRef dgs = dg ? TRef() : new_tensor({C}, BE_F32);
+  TRef dbs = db ? TRef() : new_tensor({C}, BE_F32);
+  float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
+  float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
+  k::bn_bwd(dz->data(), x->data(), nullptr, act, dx ? dx->data() : nullptr, rows, C, BE_BF16, mean->ptr<float>(),
+            inv->ptr<float>(), gamma->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s,
+            act ? beta->ptr<float>() : nullptr);
+  if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
+  if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
+  if (dx) sink.commit(0);
+  if (dg) sink.commit(1);
+  if (db) sink.commit(2);
+}
+static void op_bn_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor* out) {
+  be_bn_attrs a{1e-5f, 0.1f, 1, 0};
+  if (attrs) a = *reinterpret_cast<const be_bn_attrs*>(attrs);
+  BE_REQUIRE(n_in == 4 || n_in == 6, BE_E_ARG, "bn_conv1x1: x, gamma, beta[, running_mean, running_var], w");
+  BE_REQUIRE(!a.residual && a.act >= 0 && a.act <= 2, BE_E_ARG, "bn_conv1x1: act 0/1/2, no residual");
+  Tensor* x = check_handle(in[0]);
+  Tensor* gamma = check_handle(in[1]);
+  Tensor* beta = check_handle(in[2]);
+  Tensor* rm = n_in == 6 && in[3] ? check_handle(in[3]) : nullptr;
+  Tensor* rv = n_in == 6 && in[4] ? check_handle(in[4]) : nullptr;
+  Tensor* w0 = check_handle(in[n_in - 1]);
+  BE_REQUIRE(x->rank == 4 && x->is_contiguous() && x->dtype == BE_BF16, BE_E_SHAPE,
+             "bn_conv1x1: contiguous bf16 NHWC input (bf16 compute mode)");
+  const int C = (int)x->shape[3];
+  BE_REQUIRE(C % 8 == 0, BE_E_UNSUPPORTED, "bn_conv1x1: C % 8 == 0");
+  BE_REQUIRE(w0->rank == 4 && w0->shape[1] == 1 && w0->shape[2] == 1 && w0->shape[3] == C, BE_E_SHAPE,
+             "bn_conv1x1: weight KRSC [K, 1, 1, C]");
+  BE_REQUIRE(gamma->numel() == C && beta->numel() == C && gamma->dtype == BE_F32 && beta->dtype == BE_F32,
+             BE_E_SHAPE, "bn_conv1x1: gamma/beta f32 [C]");
+  const int K = (int)w0->shape[0];
+  BE_REQUIRE(K % 8 == 0, BE_E_UNSUPPORTED, "bn_conv1x1: K % 8 == 0");
+  const int64_t rows = x->numel() / C;
+  BE_REQUIRE(rows > 0, BE_E_EMPTY_REDUCTION, "bn_conv1x1: empty batch");
+  cudaStream_t s = ctx().stream;
+  TRef mean = new_tensor({C}, BE_F32), inv = new_tensor({C}, BE_F32);
+  TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+  k::bn_stats(x->data(), rows, C, x->dtype, a.eps, mean->ptr<float>(), inv->ptr<float>(), part->ptr<float>(),
+              rm ? rm->ptr<float>() : nullptr, rv ? rv->ptr<float>() : nullptr, a.momentum, s);
+  if (rm) rm->bump_version();
+  if (rv) rv->bump_version();
+  Tensor* w = weight_operand(w0);
+  BE_REQUIRE(w->dtype == BE_BF16, BE_E_DTYPE, "bn_conv1x1: bf16 compute mode");
+  TRef y = new_tensor({x->shape[0], x->shape[1], x->shape[2], (int64_t)K}, BE_BF16);
+  k::GemmDesc gd;
+  gd.M = (int)rows; gd.N = K; gd.K = C;
+  gd.A = x->data(); gd.lda = C; gd.a_kmajor = true;
+  gd.B = w->data(); gd.ldb = C; gd.b_kmajor = true;
+  gd.ab = BE_BF16; gd.D = y->data(); gd.ldd = K; gd.d = BE_BF16;
+  gd.xf_op = 1; gd.xf_act = a.act; gd.xf_C = C;
+  gd.xf_mean = mean->ptr<float>(); gd.xf_invstd = inv->ptr<float>();
+  gd.xf_gamma = gamma->ptr<float>(); gd.xf_beta = beta->ptr<float>();
+  k::gemm(gd, s);
+  Node* n = new_node("bn_conv1x1", BE_OP_BN_CONV1X1, vjp_bn_conv, {x, gamma, beta, w0});
+  if (n) {
+    save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, beta); save(n, w);
+    n->iattr[0] = a.act;
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
 // ------------------------------------------------------------------ embedding
 static void vjp_embedding(Node* n, GradSink& sink) {
   TRef hids;
@@ -498,6 +627,7 @@ void op_cnn(int op, const be_tensor* in, int n_in, const void* attrs, be_tensor*
     case BE_OP_AVGPOOL_GLOBAL: op_avgpool(in, n_in, out); break;
     case BE_OP_BATCHNORM2D: op_bn(in, n_in, attrs, out); break;
     case BE_OP_EMBEDDING: op_embedding(in, n_in, out); break;
+    case BE_OP_BN_CONV1X1: op_bn_conv(in, n_in, attrs, out); break;
     default: fail(BE_E_UNSUPPORTED, "op_cnn: unknown op");
   }
 }

@@ -215,10 +215,15 @@ class ResNet50(Model):
     epilogue work slows the GEMMs about as much as the skipped pass saves), so
     the benchmark model leaves it off."""
 
-    def __init__(self, layers=(3, 4, 6, 3), base=64, classes=1000, bn_stats=False):
+    def __init__(self, layers=(3, 4, 6, 3), base=64, classes=1000, bn_stats=False, fuse_bn_conv=False):
         super().__init__()
         self.layers, self.base, self.classes = tuple(layers), base, classes
         self.bn_stats = bn_stats
+        # fuse_bn_conv=True: bn2 + ReLU applied inside c3's operand load
+        # (BE_OP_BN_CONV1X1, bf16 mode) — the bn2 output never reaches HBM and
+        # the step needs 0.7 GB less memory, but the two transform warps throttle
+        # the GEMM mainloop: measured C4 11.4k → 9.2k img/s, so off by default
+        self.fuse_bn_conv = fuse_bn_conv
 
     def blocks(self):
         out, cin = [], self.base
@@ -268,12 +273,18 @@ class ResNet50(Model):
         h = conv(x, "conv1.w", 2, 3)
         h = bn(h, "bn1", 1)
         h = T.maxpool2d(h, 3, 2, 1)
+        fuse = self.fuse_bn_conv and x.dtype == T.L.BE_BF16 and not self.bn_stats
         for (n, cin, mid, cout, stride, down) in self.blocks():
             t = bn(conv(h, n + ".c1.w", 1, 0), n + ".bn1", 1)
-            t = bn(conv(t, n + ".c2.w", stride, 1), n + ".bn2", 1)
+            t = conv(t, n + ".c2.w", stride, 1)
+            if fuse:  # c3(relu(bn2(t))) — the bn2 output is only ever built in c3's operand tiles
+                u = T.bn_conv1x1(t, P[n + ".bn2.g"], P[n + ".bn2.b"], B[n + ".bn2.rm"], B[n + ".bn2.rv"],
+                                 P[n + ".c3.w"], act=1)
+            else:
+                u = conv(bn(t, n + ".bn2", 1), n + ".c3.w", 1, 0)
             idn = bn(conv(h, n + ".ds.w", stride, 0), n + ".dsbn", 0) if down else h
             # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN)
-            h = bn(conv(t, n + ".c3.w", 1, 0), n + ".bn3", 1, residual=idn)
+            h = bn(u, n + ".bn3", 1, residual=idn)
         h = T.avgpool_global(h)
         z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
         return T.softmax_xent(z, y)

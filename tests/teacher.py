@@ -59,7 +59,7 @@ class OpTrace:
     """Wraps the api ops a model calls (be.nn uses the module global `T`)."""
 
     OPS = ("conv2d", "batchnorm2d", "maxpool2d", "avgpool_global", "reshape", "linear", "softmax_xent",
-           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_depthwise")
+           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_depthwise", "bn_conv1x1")
 
     def __init__(self, api, model):
         self.api = api
@@ -478,6 +478,57 @@ class Replay:
             gd = l[0].grad.numpy()
             self.record(i, "concat", f"dx{j}", gd, v.grad)
             self._push(r.key, gd)
+
+    def _op_bn_conv1x1(self, i, rec):
+        """BN (train) → act → 1×1 conv, one device op: compared with the
+        oracle's batchnorm2d → relu/relu6 → conv2d on the same inputs — the
+        output, dx, dγ, dβ (summation scale, R16), dW and the running stats.
+        The activation mask of the backward is the one the device takes:
+        decided from the BN output recomputed in fp32 and rounded to bf16
+        (as the operand transform stores it), i.e. from act(bn(x)) > 0 of the
+        oracle's values within bf16 rounding of 0 — compared as computed."""
+        be, a = self.be, rec["args"]
+        L = self._dev_inputs(rec, ["x", "gamma", "beta", "w"])
+        rm0 = self._val(a["running_mean"]) if a["running_mean"] is not None else None
+        rv0 = self._val(a["running_var"]) if a["running_var"] is not None else None
+        rmd = be.tensor(rm0) if rm0 is not None else None
+        rvd = be.tensor(rv0) if rv0 is not None else None
+        y = be.bn_conv1x1(L["x"][1], L["gamma"][1], L["beta"][1], rmd, rvd, L["w"][1], eps=a["eps"],
+                          momentum=a["momentum"], act=a["act"])
+        xo = Var(nhwc_to_nchw(self._val(a["x"])).astype(F64), True)
+        go = Var(self._val(a["gamma"]).astype(F64), True)
+        bo = Var(self._val(a["beta"]).astype(F64), True)
+        wo = Var(nhwc_to_nchw(self._val(a["w"])).astype(F64), True)   # KRSC -> KCRS
+        zo, (rm, rv) = oops.batchnorm2d(xo, go, bo, eps=a["eps"], momentum=a["momentum"],
+                                        running_mean=None if rm0 is None else rm0.astype(F64),
+                                        running_var=None if rv0 is None else rv0.astype(F64))
+        if a["act"]:
+            # the activation decision the device takes (SURVEY §8(c) reading 16): its own BN output
+            # (be.batchnorm2d: same statistics kernels, same fp32 affine, stored bf16) — act(z) written
+            # as z·mask (+ 6 where clamped) so the oracle's gradient takes exactly that mask
+            with be.no_grad():
+                yb = nhwc_to_nchw(be.batchnorm2d(be.tensor(self._val(a["x"]), dtype="bf16"),
+                                                 be.tensor(self._val(a["gamma"])), be.tensor(self._val(a["beta"])),
+                                                 eps=a["eps"], act=a["act"]).numpy()).astype(F64)
+            mask = _act_mask(yb, a["act"]).astype(F64)
+            six = 6.0 * (yb >= 6.0) if a["act"] == 2 else np.zeros_like(yb)
+            ho = oops.add(oops.mul(zo, Var(mask)), Var(six))
+        else:
+            ho = zo
+        yo = oops.conv2d(ho, wo, None, 1, 0)
+        ydev = y.numpy()
+        self.record(i, "bn_conv1x1", "y", nhwc_to_nchw(ydev), yo.value)
+        if rmd is not None:
+            xa = np.abs(nhwc_to_nchw(self._val(a["x"])).astype(F64)).mean(axis=(0, 2, 3))
+            self.record(i, "bn_conv1x1", "running_mean", rmd.numpy(), rm,
+                        mass=(a["momentum"] * xa + (1 - a["momentum"]) * np.abs(rm0)).max())
+            self.record(i, "bn_conv1x1", "running_var", rvd.numpy(), rv)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        backward(yo, nhwc_to_nchw(np.asarray(g).reshape(ydev.shape)))
+        og = {"x": nchw_to_nhwc(xo.grad), "gamma": go.grad, "beta": bo.grad, "w": nchw_to_nhwc(wo.grad)}
+        self._finish(i, rec, L, og, ["x", "gamma", "beta", "w"])
 
     def _op_dropout(self, i, rec):
         be, a = self.be, rec["args"]

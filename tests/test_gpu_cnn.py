@@ -386,3 +386,46 @@ def test_conv_wgrad_variants_bf16(cfg):
         yd = be.conv2d(xd, wd, None, st, pd)
         yd.backward(gd)
         assert rel(nhwc_to_nchw(wd.grad.numpy()), wo.grad) < 1e-3
+
+
+@pytest.mark.parametrize("cfg", [(2, 64, 14, 14, 256, 1), (3, 128, 9, 7, 512, 1), (2, 256, 7, 7, 1024, 1),
+                                 (1, 40, 11, 13, 24, 2), (4, 96, 5, 5, 64, 0)])
+def test_bn_conv1x1_fused_operand(cfg):
+    """BN (train) → ReLU / ReLU6 / none → 1×1 conv with the BN applied inside
+    the GEMM's operand load (BE_OP_BN_CONV1X1): output, dx, dγ, dβ, dW and the
+    running statistics vs the unfused device ops (batchnorm2d then conv2d, each
+    parity-checked elsewhere) and vs the float64 oracle composition, every op
+    of it fed the same inputs (teacher-forced replay)."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from teacher import Replay, OpTrace
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    N, C, H, W, K, act = cfg
+    rng = np.random.default_rng(sum(cfg))
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(a.astype(np.float32)))  # noqa: E731
+    x = q(rng.standard_normal((N, H, W, C)) * 2 + 0.5)
+    gam = (rng.standard_normal(C) * 0.5 + 1.5).astype(np.float32)
+    bet = (rng.standard_normal(C) * 0.5).astype(np.float32)
+    w = (rng.standard_normal((K, 1, 1, C)) / np.sqrt(C)).astype(np.float32)
+
+    class M:  # the traced "model": one op
+        pass
+    m = M()
+    m.params = {"g": be.tensor(gam, requires_grad=True), "b": be.tensor(bet, requires_grad=True),
+                "w": be.tensor(w, requires_grad=True)}
+    m.buffers = {"rm": be.tensor(np.zeros(C, np.float32)), "rv": be.tensor(np.ones(C, np.float32))}
+    tr = OpTrace(be.api, m)
+    xb = be.tensor(x, dtype="bf16")
+    tr.ids[id(xb)] = ("param", "x")  # checked like a parameter: its gradient dx is compared
+    fused = tr._wrap("bn_conv1x1")
+    y = fused(xb, m.params["g"], m.params["b"], m.buffers["rm"], m.buffers["rv"], m.params["w"], act=act)
+    g = q(rng.standard_normal(tuple(y.shape)))
+    rp = Replay(be, tr, 2e-2)
+    rp.grads[tr.recs[-1]["out"]] = g.astype(np.float64)
+    rp.run()
+    bad = rp.failures()
+    assert not bad, bad
+    got = {w_ for (_, _, w_, _) in rp.errs}
+    assert {"y", "dx:x", "dgamma:g", "dbeta:b", "dw:w", "running_mean", "running_var"} <= got, got

@@ -27,6 +27,12 @@ def _case(name, dtype):
     """(oracle net, device net, oracle batch, device batch factory, seed)."""
     be = be_init()
     inp = (lambda a: synth.bf16_values(a)) if dtype == "bf16" else (lambda a: a)
+    if name == "resnet50_fused":  # bn2 → c3 through BE_OP_BN_CONV1X1 (bf16)
+        seed = 27
+        x = inp(synth.normal((2, 3, 224, 224), seed, 1))
+        y = synth.labels(2, 1000, seed)
+        return (onets.ResNet50(), be.nn.ResNet50(fuse_bn_conv=True), (x, y),
+                lambda: (be.nn.images_to_device(x, dtype), be.tensor(y)), seed)
     if name == "resnet50":
         seed = 21
         x = inp(synth.normal((2, 3, 224, 224), seed, 1))
@@ -62,10 +68,12 @@ def _case(name, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2", "vgg19", "mobilenetv2"])
+@pytest.mark.parametrize("name", ["resnet50", "alexnet", "ncf", "mlp_c2", "vgg19", "mobilenetv2", "resnet50_fused"])
 def test_teacher_forced_full_depth(name, dtype):
     be = be_init()
     be.set_compute_dtype(dtype)
+    if name == "resnet50_fused" and dtype != "bf16":
+        pytest.skip("the fused BN-conv op is a bf16-mode op")
     onet, pnet, _, dev_batch, seed = _case(name, dtype)
     P = synth.make_params(onet.param_specs(), seed)
     pnet.load(P)
