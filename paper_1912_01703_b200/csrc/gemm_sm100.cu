@@ -106,13 +106,23 @@ struct __align__(64) GemmParams {
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
-// Fused-SGD epilogue: 4 warps (one per TMEM lane quarter), each with three
-// 10 KB buffers; a buffer holds one 32 × 32 chunk of P (4 KB) and V (4 KB) in
-// the TMA SW128 layout, updated in place, + its bf16 shadow (2 KB, SW64).
-constexpr int kUpdWarps = 4;
+// Fused-SGD epilogue: 8 warps (two per TMEM lane quarter, alternating
+// 16-column chunks of a tile), each with three 5 KB buffers; a buffer holds
+// one 32 × 16 chunk of P (2 KB) and V (2 KB) in the TMA SW64 layout, updated
+// in place, + its bf16 shadow (1 KB, SW32).  The update is latency-bound per
+// warp (dependent smem round trips per chunk), so twice the warps over
+// half-width chunks keep twice the chunks in flight in the same 120 KB.
+constexpr int kUpdWarps = 8;
 constexpr int kUpdBufs = 3;
-constexpr int kUpdBufBytes = 4096 + 4096 + 2048;
+constexpr int kUpdCW = 16;  // chunk width (columns)
+constexpr int kUpdBufBytes = 2048 + 2048 + 1024;
 constexpr int kUpdWarpBytes = kUpdBufs * kUpdBufBytes;
+// BN ≥ 128 tiles: two buffers per warp (prefetch distance 1) so that one more
+// mainloop stage fits (BN 256: 3 × 48 KB, BN 128: 4 × 32 KB) — with two
+// stages the operand loads, not the update traffic, bound the kernel (ncu:
+// the update warps waited on the accumulator 42 % of their time; 4096² K=1024
+// launch 80 → 75 µs, BN 128 90 → 79 µs)
+constexpr int upd_bufs(int bn) { return bn >= 128 ? 2 : kUpdBufs; }
 
 // NSLOT: 2-KB bf16 staging slots per epilogue warp (TMA stores in flight per
 // warp = NSLOT − 1).  4 for store-heavy short-K shapes (the 1×1 convs: the
@@ -130,7 +140,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;         // BM rows x 128 B
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int EPI_BYTES = UPD ? kUpdWarps * kUpdWarpBytes : kEpiWarps * NSLOT * 2048;
+  static constexpr int EPI_BYTES = UPD ? kUpdWarps * upd_bufs(BN) * kUpdBufBytes : kEpiWarps * NSLOT * 2048;
   static constexpr int XF_BYTES = XF ? 8 * 8 + 2 * 2048 * 4 : 0;  // xfull barriers + per-channel scale/shift (C ≤ 2048)
   static constexpr int STAGES_RAW = (226 * 1024 - EPI_BYTES - XF_BYTES - 1280) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -284,21 +294,22 @@ struct ColStats {
 // Fused SGD epilogue for one 32-row × 32-column accumulator chunk held by a
 // warp (lane = row): the accumulator is the fp32 gradient g of parameter
 // elements P[row, col] (never stored).  All global traffic is TMA: the
-// chunk's P and V arrive in smem in the SW128 layout (row r's 16-B piece c at
-// c ^ (r & 7): a lane reading its own row is bank-conflict-optimal), are
-// updated in place with sgd_elem (the multi-tensor SGD kernel's arithmetic →
-// bitwise the same parameters), the bf16 shadow row is written in the SW64
-// layout, and lane 0 issues three bulk tensor stores (edges clipped by TMA).
+// chunk's P and V (32 rows × 16 columns) arrive in smem in the SW64 layout (a
+// lane reading its own row is bank-conflict-optimal), are updated in place
+// with sgd_elem (the multi-tensor SGD kernel's arithmetic → bitwise the same
+// parameters), the bf16 shadow row is written in the SW32 layout, and lane 0
+// issues three bulk tensor stores (edges clipped by TMA).
 // The caller waited for the loads (mbarrier) before calling.
-__device__ __forceinline__ void epi_sgd32(const GemmParams& p, uint8_t* buf, int lane, int row0, int col0,
-                                          const uint32_t (&r)[32]) {
+__device__ __forceinline__ void epi_sgd16(const GemmParams& p, uint8_t* buf, int lane, int row0, int col0,
+                                          const uint32_t (&r)[16]) {
   uint8_t* sp = buf;
-  uint8_t* sv = buf + 4096;
-  uint8_t* ss = buf + 8192;
+  uint8_t* sv = buf + 2048;
+  uint8_t* ss = buf + 4096;
   const bool mom = p.upd_v != nullptr;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int off = lane * 128 + ((c ^ (lane & 7)) << 4);
+  for (int c = 0; c < 4; ++c) {
+    // SW64: the row's 16-B piece c sits at c ^ ((row >> 1) & 3)
+    const int off = lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4);
     const float4 p4 = *reinterpret_cast<const float4*>(sp + off);
     const float4 v4 = mom ? *reinterpret_cast<const float4*>(sv + off) : make_float4(0.f, 0.f, 0.f, 0.f);
     float pv[4] = {p4.x, p4.y, p4.z, p4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -307,9 +318,9 @@ __device__ __forceinline__ void epi_sgd32(const GemmParams& p, uint8_t* buf, int
     *reinterpret_cast<float4*>(sp + off) = make_float4(pv[0], pv[1], pv[2], pv[3]);
     if (mom) *reinterpret_cast<float4*>(sv + off) = make_float4(vv[0], vv[1], vv[2], vv[3]);
     if (p.upd_shadow) {
-      // 8 bf16 per 16-B SW64 piece: fp32 pieces 2h, 2h+1 → bf16 piece h
+      // 8 bf16 per 16-B SW32 piece (piece h at h ^ ((row >> 2) & 1)): fp32 pieces 2h, 2h+1 → bf16 piece h
       const int h = c >> 1;
-      uint2* dst = reinterpret_cast<uint2*>(ss + lane * 64 + ((h ^ ((lane >> 1) & 3)) << 4) + (c & 1) * 8);
+      uint2* dst = reinterpret_cast<uint2*>(ss + lane * 32 + ((h ^ ((lane >> 2) & 1)) << 4) + (c & 1) * 8);
       *dst = make_uint2(pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]));
     }
   }
@@ -395,69 +406,83 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
   slot = (slot + 1) % (p.d_f32 ? NSLOT / 2 : NSLOT);
 }
 
-// Fused-SGD epilogue of a persistent GEMM (warp = TMEM lane quarter eq):
-// 32 rows × TILE_N columns per tile, as a flat sequence of 32-column chunks
-// over this CTA's tiles (t0, t0 + tstride, …).  Chunk i's P,V are TMA-loaded
-// two chunks ahead into buffer i % 3 (no dependence on the accumulator), then
-// updated in place and TMA-stored with the shadow (epi_sgd32).  CLUSTER: the
-// accumulator-empty arrival goes to the pair leader's barrier.
-template <int TILE_N, bool CLUSTER>
+// Fused-SGD epilogue of a persistent GEMM (warp = TMEM lane quarter eq, column
+// parity half): 32 rows × the tile's 16-column chunks j ≡ half (mod 2), as a
+// flat sequence over this CTA's tiles (t0, t0 + tstride, …).  Chunk i's P,V
+// are TMA-loaded two chunks ahead into buffer i % 3 (no dependence on the
+// accumulator), then updated in place and TMA-stored with the shadow
+// (epi_sgd16).  CLUSTER: the accumulator-empty arrival goes to the pair
+// leader's barrier.
+template <int TILE_N, bool CLUSTER, int NBUF = kUpdBufs>
 __device__ __forceinline__ void upd_epilogue(const GemmParams& p, uint8_t* epi_smem, uint64_t* ubar, uint64_t* tfull,
-                                             uint64_t* tempty, uint32_t tempty_leader, uint32_t tmem_base, int eq,
+                                             uint64_t* tempty, uint32_t tempty_leader, uint32_t tmem_base, int uw,
                                              int lane, int t0, int tstride, int num_tiles, int mn_tiles, int tile_m,
                                              int row_off) {
-  uint8_t* bufs = epi_smem + eq * kUpdWarpBytes;
-  uint64_t* mb = ubar + eq * kUpdBufs;
-  const uint32_t tx = p.upd_v ? 8192u : 4096u;
-  const int cpt = (min(p.N, TILE_N) + 31) / 32;  // chunks per tile (tail chunks past N skipped)
-  auto chunk_at = [&](int i, int* row0, int* col0) -> bool {
-    const int t = t0 + (i / cpt) * tstride;
+  static_assert(NBUF == 2 || NBUF == 3, "update buffers");
+  const int eq = uw & 3, half = uw >> 2;
+  uint8_t* bufs = epi_smem + uw * NBUF * kUpdBufBytes;
+  uint64_t* mb = ubar + uw * kUpdBufs;
+  const uint32_t tx = p.upd_v ? 4096u : 2048u;
+  const int cpt = (min(p.N, TILE_N) + kUpdCW - 1) / kUpdCW;  // chunks per tile (tail chunks past N skipped)
+  const int cpw = (cpt - half + 1) / 2;                       // this warp's chunks per tile
+  auto chunk_at = [&](int i, int* row0, int* col0, int* j) -> bool {
+    const int t = t0 + (i / cpw) * tstride;
     if (t >= num_tiles) return false;
     const int tm = (t % mn_tiles) % p.tiles_m, tn = (t % mn_tiles) / p.tiles_m;
+    *j = half + 2 * (i % cpw);
     *row0 = tm * tile_m + row_off + eq * 32;
-    *col0 = tn * TILE_N + (i % cpt) * 32;
+    *col0 = tn * TILE_N + *j * kUpdCW;
     return true;
   };
   auto issue = [&](int i) {
-    int r0, c0;
-    if (!chunk_at(i, &r0, &c0) || c0 >= p.N) return;
+    int r0, c0, j;
+    if (!chunk_at(i, &r0, &c0, &j) || c0 >= p.N) return;
     if (lane == 0) {
-      uint8_t* b = bufs + (i % kUpdBufs) * kUpdBufBytes;
-      uint64_t* bar = &mb[i % kUpdBufs];
+      uint8_t* b = bufs + (i % NBUF) * kUpdBufBytes;
+      uint64_t* bar = &mb[i % NBUF];
       sm100::mbar_arrive_expect_tx(bar, tx);
       sm100::tma_load_2d(&p.tp[0], bar, b, c0, r0);
-      if (p.upd_v) sm100::tma_load_2d(&p.tp[1], bar, b + 4096, c0, r0);
+      if (p.upd_v) sm100::tma_load_2d(&p.tp[1], bar, b + 2048, c0, r0);
     }
   };
   uint32_t uph = 0u;  // bit k: phase of buffer k
   issue(0);
-  issue(1);
+  if (NBUF == 3) issue(1);
   int acc = 0; uint32_t acc_phase = 0;
   int i = 0;
   for (int t = t0; t < num_tiles; t += tstride) {
     sm100::mbar_wait(&tfull[acc], acc_phase);
     sm100::tc_fence_after();
-    for (int j = 0; j < cpt; ++j, ++i) {
-      int row0, col0;
-      chunk_at(i, &row0, &col0);
+    for (int q = 0; q < cpw; ++q, ++i) {
+      int row0, col0, j;
+      chunk_at(i, &row0, &col0, &j);
       const bool live = col0 < p.N;
+      if (NBUF == 2) {
+        // buffer (i+1) % 2 was last used by chunk i−1 (the latest commit
+        // group): wait until its stores have read it, then refill
+        if (lane == 0) sm100::bulk_wait_read<0>();
+        __syncwarp();
+        issue(i + 1);
+      }
       if (live) {
-        uint32_t ru[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * TILE_N + j * 32 + ((uint32_t)(eq * 32) << 16), ru);
+        uint32_t ru[16];
+        sm100::tmem_ld_32x32b_x16(tmem_base + acc * TILE_N + j * kUpdCW + ((uint32_t)(eq * 32) << 16), ru);
         sm100::tmem_ld_wait();
-        const int k = i % kUpdBufs;
+        const int k = i % NBUF;
         sm100::mbar_wait(&mb[k], (uph >> k) & 1u);
         uph ^= 1u << k;
-        epi_sgd32(p, bufs + k * kUpdBufBytes, lane, row0, col0, ru);
+        epi_sgd16(p, bufs + k * kUpdBufBytes, lane, row0, col0, ru);
       }
-      // buffer (i+2) % 3 was last used by chunk i−1, whose stores went out
-      // one commit group ago: wait until they have read it, then refill
-      if (lane == 0) {
-        if (live) sm100::bulk_wait_read<1>();
-        else sm100::bulk_wait_read<0>();
+      if (NBUF == 3) {
+        // buffer (i+2) % 3 was last used by chunk i−1, whose stores went out
+        // one commit group ago: wait until they have read it, then refill
+        if (lane == 0) {
+          if (live) sm100::bulk_wait_read<1>();
+          else sm100::bulk_wait_read<0>();
+        }
+        __syncwarp();
+        issue(i + 2);
       }
-      __syncwarp();
-      issue(i + 2);
     }
     sm100::tc_fence_before();
     __syncwarp();
@@ -696,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       }
     }
   } else if (UPD && warp >= 4 && warp < 4 + kUpdWarps) {
-    upd_epilogue<BN, false>(p, epi_smem, ubar, tfull, tempty, 0u, tmem_base, warp & 3, lane, blockIdx.x, gridDim.x,
+    upd_epilogue<BN, false, upd_bufs(BN)>(p, epi_smem, ubar, tfull, tempty, 0u, tmem_base, warp - 4, lane, blockIdx.x, gridDim.x,
                             num_tiles, mn_tiles, BM, 0);
   } else if (!UPD && warp >= 4) {
     // ===================== epilogue =====================
@@ -949,7 +974,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (UPD && warp >= 4 && warp < 4 + kUpdWarps) {
     upd_epilogue<TN, true>(p, epi_smem, ubar, tfull, tempty, sm100::mapa(sm100::smem_u32(&tempty[0]), 0), tmem_base,
-                           warp & 3, lane, pair_id, npairs, num_tiles, mn_tiles, TM, (int)rank * HM);
+                           warp - 4, lane, pair_id, npairs, num_tiles, mn_tiles, TM, (int)rank * HM);
   } else if (!UPD && warp >= 4) {
     // ===================== epilogue (both CTAs, own TMEM half) =====================
     const int ew = warp - 4;               // 0..7
@@ -2601,15 +2626,15 @@ bool gemm_update_ok(const GemmDesc& g) {
 namespace {
 void set_update(GemmParams& p, const GemmDesc& g) {
   BE_REQUIRE(gemm_update_ok(g), BE_E_ARG, "gemm: update epilogue needs 16-B aligned P/V rows, 8-B aligned shadow");
-  // P / V chunks are TMA-loaded as 32 × 32 fp32 boxes (zero fill past the edges)
-  encode_2d_sw(&p.tp[0], g.upd->p, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
-               CU_TENSOR_MAP_SWIZZLE_128B);
+  // P / V chunks are TMA-loaded as 32 × 16 fp32 boxes (zero fill past the edges)
+  encode_2d_sw(&p.tp[0], g.upd->p, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, kUpdCW, 32,
+               CU_TENSOR_MAP_SWIZZLE_64B);
   if (g.upd->v)
-    encode_2d_sw(&p.tp[1], g.upd->v, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
-                 CU_TENSOR_MAP_SWIZZLE_128B);
-  if (g.upd->shadow)
-    encode_2d_sw(&p.td, g.upd->shadow, BE_BF16, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, 32, 32,
+    encode_2d_sw(&p.tp[1], g.upd->v, BE_F32, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, kUpdCW, 32,
                  CU_TENSOR_MAP_SWIZZLE_64B);
+  if (g.upd->shadow)
+    encode_2d_sw(&p.td, g.upd->shadow, BE_BF16, (uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.ldd, kUpdCW, 32,
+                 CU_TENSOR_MAP_SWIZZLE_32B);
   p.upd = 1;
   p.upd_p = g.upd->p; p.upd_v = g.upd->v; p.upd_shadow = g.upd->shadow;
   p.lr = g.upd->lr; p.mu = g.upd->mu; p.wd = g.upd->wd; p.gscale = g.upd->scale;
