@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -146,9 +147,110 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
   }
 }
 
+}  // namespace
+// Finalize folded into the statistics / reduction pass (replaces the separate
+// bn_finalize_v launch).  Every block writes its partial row, takes a ticket;
+// the last nf blocks to arrive wait until all partial rows are written (all
+// blocks of these grids are co-resident: ≤ 3 per SM, 3 fit) and each reduces
+// 8-channel groups g ≡ (ticket − (sp − nf)) (mod nf): 32 sub-lanes per group sum
+// every 32nd split in double, combined in sub-lane order — a fixed order, so
+// the result does not depend on which blocks arrive last.  The last finalizer
+// to depart resets the two counters for the next launch on this stream.
+struct BnFin {
+  int mode = 0;                 // 0: caller finalizes; 1: statistics; 2: backward sums
+  unsigned int* ctr = nullptr;  // [0] arrivals, [1] departures
+  int nf = 0;
+  int64_t rows = 0;
+  const uint16_t* shift = nullptr;  // mode 1: x (row 0 = the shift K)
+  float eps = 0.f, momentum = 0.f;
+  float* mean = nullptr;
+  float* invstd = nullptr;
+  float* run_mean = nullptr;
+  float* run_var = nullptr;
+  float* dgamma = nullptr;
+  float* dbeta = nullptr;
+  float* sums = nullptr;
+  float gb_beta = 0.f;
+};
+namespace {
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ void fold_finalize(const BnFin& f, const float* __restrict__ p0, const float* __restrict__ p1, int C,
+                              uint8_t* smem) {
+  __shared__ unsigned int s_ticket;
+  const int sp = (int)gridDim.x;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&f.ctr[0], 1u);
+  __syncthreads();
+  const int first = sp - f.nf;
+  if ((int)s_ticket < first) return;
+  const int fi = (int)s_ticket - first;
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(&f.ctr[0]) < (unsigned)sp) __nanosleep(32);
+  __syncthreads();
+  double* s0 = reinterpret_cast<double*>(smem);  // [32][8]
+  double* s1 = s0 + 256;
+  const int t = threadIdx.x, cl = t & 7, sub = t >> 3;
+  const int groups = C >> 3;
+  for (int g = fi; g < groups; g += f.nf) {
+    const int c = g * 8 + cl;
+    if (t < 256) {
+      double a0 = 0, a1 = 0;
+      int i = sub;
+      for (; i + 96 < sp; i += 128) {
+        const float x0 = __ldcg(p0 + (int64_t)i * C + c), x1 = __ldcg(p0 + (int64_t)(i + 32) * C + c);
+        const float x2 = __ldcg(p0 + (int64_t)(i + 64) * C + c), x3 = __ldcg(p0 + (int64_t)(i + 96) * C + c);
+        const float y0 = __ldcg(p1 + (int64_t)i * C + c), y1 = __ldcg(p1 + (int64_t)(i + 32) * C + c);
+        const float y2 = __ldcg(p1 + (int64_t)(i + 64) * C + c), y3 = __ldcg(p1 + (int64_t)(i + 96) * C + c);
+        a0 += (double)x0; a0 += (double)x1; a0 += (double)x2; a0 += (double)x3;
+        a1 += (double)y0; a1 += (double)y1; a1 += (double)y2; a1 += (double)y3;
+      }
+      for (; i < sp; i += 32) { a0 += __ldcg(p0 + (int64_t)i * C + c); a1 += __ldcg(p1 + (int64_t)i * C + c); }
+      s0[sub * 8 + cl] = a0;
+      s1[sub * 8 + cl] = a1;
+    }
+    __syncthreads();
+    if (t < 8) {
+      double t0 = 0, t1 = 0;
+      for (int k = 0; k < 32; ++k) { t0 += s0[k * 8 + cl]; t1 += s1[k * 8 + cl]; }
+      if (f.mode == 1) {
+        const double n = (double)f.rows;
+        const double ms = t0 / n;
+        double var = t1 / n - ms * ms;  // biased (normalisation)
+        if (var < 0) var = 0;
+        const float mu = bf2f(f.shift[c]) + (float)ms;
+        f.mean[c] = mu;
+        f.invstd[c] = rsqrtf((float)var + f.eps);
+        if (f.run_mean) f.run_mean[c] = (1.f - f.momentum) * f.run_mean[c] + f.momentum * mu;
+        if (f.run_var)
+          f.run_var[c] = (1.f - f.momentum) * f.run_var[c] +
+                         f.momentum * (float)(var * n / (f.rows > 1 ? n - 1 : 1));
+      } else {
+        f.sums[c] = (float)t0;
+        f.sums[C + c] = (float)t1;
+        if (f.dbeta) f.dbeta[c] = (float)t0 + (f.gb_beta != 0.f ? f.dbeta[c] : 0.f);
+        if (f.dgamma) f.dgamma[c] = (float)t1 + (f.gb_beta != 0.f ? f.dgamma[c] : 0.f);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&f.ctr[1], 1u) == (unsigned)f.nf - 1u) {
+      f.ctr[0] = 0u;
+      f.ctr[1] = 0u;
+    }
+  }
+}
+
 // forward statistics: shifted sums Σ(x−K), Σ(x−K)² with K = x[0, c]
 __global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t* __restrict__ x, int64_t rows, int C,
-                                                               float* part0, float* part1, int64_t rps) {
+                                                               float* part0, float* part1, int64_t rps,
+                                                               const __grid_constant__ BnFin fin) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
@@ -164,6 +266,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t
   });
   __syncthreads();
   combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1);
+  if (fin.mode) fold_finalize(fin, part0, part1, C, ring);
 }
 
 // backward reduction Σg', Σg'·x̂ (g' = gy masked by act(γx̂+β) > 0 recomputed
@@ -181,7 +284,8 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
                                                                 const float* __restrict__ bsh,
                                                                 const uint16_t* __restrict__ rmask,
                                                                 uint16_t* __restrict__ gout,
-                                                                const uint8_t* __restrict__ rbits) {
+                                                                const uint8_t* __restrict__ rbits,
+                                                                const __grid_constant__ BnFin fin) {
   pdl_entry();
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
@@ -241,6 +345,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
   }
   __syncthreads();
   combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1);
+  if (fin.mode) fold_finalize(fin, part0, part1, C, ring);
 }
 
 // y = act(γ·x̂ + β [+ res])
@@ -453,17 +558,49 @@ int64_t bn_stream_splits(int64_t rows, int C, int64_t cap) {
   return std::max<int64_t>(1, std::min(sp, cap));
 }
 
-void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s) {
+namespace {
+// per-stream arrival / departure counters of the folded finalize (zeroed once;
+// every launch leaves them zero)
+unsigned int* fin_counters(cudaStream_t s) {
+  static std::unordered_map<cudaStream_t, Block*> m;
+  auto it = m.find(s);
+  if (it != m.end()) return reinterpret_cast<unsigned int*>(it->second->ptr);
+  Block* b = ctx().alloc.allocate(64, s);
+  BE_CHECK_CUDA(cudaMemsetAsync(b->ptr, 0, 64, s));
+  m[s] = b;
+  return reinterpret_cast<unsigned int*>(b->ptr);
+}
+bool fold_on() {
+  static const int on = [] { const char* e = getenv("BE_BN_FOLD"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+void fin_setup(BnFin& f, int C, int64_t sp, cudaStream_t s) {
+  f.ctr = fin_counters(s);
+  f.nf = (int)std::min<int64_t>(sp, C / 8);
+}
+}  // namespace
+
+bool bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s,
+                     float eps, float* mean, float* invstd, float* run_mean, float* run_var, float momentum) {
   static bool once = [] { set_smem(bn_stats_stream_kernel, kS1); return true; }();
   (void)once;
   const int64_t rps = (rows + sp - 1) / sp;
-  launch_pdl(bn_stats_stream_kernel, (unsigned)sp, kThr, kS1, s, x, rows, C, part0, part1, rps);  // caller: after_launch
+  BnFin fin;
+  if (fold_on() && mean) {
+    fin_setup(fin, C, sp, s);
+    fin.mode = 1;
+    fin.rows = rows; fin.shift = x; fin.eps = eps; fin.momentum = momentum;
+    fin.mean = mean; fin.invstd = invstd; fin.run_mean = run_mean; fin.run_var = run_var;
+  }
+  launch_pdl(bn_stats_stream_kernel, (unsigned)sp, kThr, kS1, s, x, rows, C, part0, part1, rps, fin);
+  after_launch("bn_stats_stream");
+  return fin.mode != 0;
 }
 
-void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
+bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
                       const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
                       const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
-                      const uint8_t* rbits) {
+                      const uint8_t* rbits, float* sums, float* dgamma, float* dbeta, float gb_beta) {
   static bool once = [] {
     set_smem(bn_reduce_stream_kernel<0>, kS2);
     set_smem(bn_reduce_stream_kernel<1>, kS3);
@@ -472,16 +609,23 @@ void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
   }();
   (void)once;
   const int64_t rps = (rows + sp - 1) / sp;
+  BnFin fin;
+  if (fold_on() && sums) {
+    fin_setup(fin, C, sp, s);
+    fin.mode = 2;
+    fin.sums = sums; fin.dgamma = dgamma; fin.dbeta = dbeta; fin.gb_beta = gb_beta;
+  }
   if (rbits)
     launch_pdl(bn_reduce_stream_kernel<2>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, (const uint16_t*)nullptr, gout, rbits);
+               rps, gam, bsh, (const uint16_t*)nullptr, gout, rbits, fin);
   else if (rmask)
     launch_pdl(bn_reduce_stream_kernel<1>, (unsigned)sp, kThr, kS3, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, rmask, gout, (const uint8_t*)nullptr);
+               rps, gam, bsh, rmask, gout, (const uint8_t*)nullptr, fin);
   else
     launch_pdl(bn_reduce_stream_kernel<0>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr);
+               rps, gam, bsh, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr, fin);
   after_launch("bn_reduce_stream");
+  return fin.mode != 0;
 }
 
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,

@@ -21,11 +21,15 @@ using namespace be::dev;
 // bn_stream.cu: TMA-bulk streaming BN passes (bf16, C % 8 == 0, C ≤ 2048)
 bool bn_stream_ok(const void* a, int64_t rows, int C);
 int64_t bn_stream_splits(int64_t rows, int C, int64_t cap);
-void bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s);
-void bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
+// (stats / reduce: true = the finalize ran inside the pass — no bn_finalize_v launch)
+bool bn_stats_stream(const uint16_t* x, int64_t rows, int C, float* part0, float* part1, int64_t sp, cudaStream_t s,
+                     float eps = 0.f, float* mean = nullptr, float* invstd = nullptr, float* run_mean = nullptr,
+                     float* run_var = nullptr, float momentum = 0.f);
+bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t rows, int C, const float* mean,
                       const float* invstd, float* part0, float* part1, int64_t sp, const float* gam,
                       const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
-                      const uint8_t* rbits = nullptr);
+                      const uint8_t* rbits = nullptr, float* sums = nullptr, float* dgamma = nullptr,
+                      float* dbeta = nullptr, float gb_beta = 0.f);
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
                      const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s,
                      uint8_t* mbits = nullptr);
@@ -162,6 +166,78 @@ __global__ void __launch_bounds__(256) col2im_v(const void* __restrict__ dcols, 
 #pragma unroll
     for (int j = 0; j < 8; ++j) o.v[j] = acc[j] + (beta != 0.f ? o.v[j] : 0.f);
     st8(dx, (int64_t)i * 8, dt, o);
+  }
+}
+
+// col2im for stride-2 R×R (R ∈ {1, 3}) bf16 convolutions (ResNet's
+// down-sampling 1×1 and 3×3 dgrads): every pixel gets at most ⌈R/2⌉² taps, so
+// all of an item's loads (2 items per thread) are issued before the sums,
+// which run in the same increasing-(r, u) order as col2im_v.  When
+// accumulating (beta ≠ 0) the pixels no tap reaches (3 of 4 for R = 1) are
+// left untouched instead of read and rewritten.
+template <int R>
+__global__ void __launch_bounds__(256) col2im_s2_bf16(const uint16_t* __restrict__ dcols, int64_t ldc,
+                                                      uint16_t* __restrict__ dx, ConvGeom g, float beta, uint32_t nvec) {
+  pdl_entry();
+  constexpr int T = (R + 1) / 2;  // taps per dimension
+  constexpr int UNR = 2;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * UNR) {
+    uint4 a[UNR][T * T];
+    int nt[UNR][2];
+    uint32_t idx[UNR];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const uint32_t i = base + k * stride;
+      idx[k] = i;
+      nt[k][0] = nt[k][1] = 0;
+      if (i >= nvec) continue;
+      int n, h, w, cv;
+      nhwc8(i, g, g.H, g.W, n, h, w, cv);
+      const int p_hi = min(g.P - 1, (h + g.pad) >> 1), p_lo = max(0, (h + g.pad - R + 2) >> 1);
+      const int q_hi = min(g.Q - 1, (w + g.pad) >> 1), q_lo = max(0, (w + g.pad - R + 2) >> 1);
+      nt[k][0] = max(0, p_hi - p_lo + 1);
+      nt[k][1] = max(0, q_hi - q_lo + 1);
+#pragma unroll
+      for (int dp = 0; dp < T; ++dp)
+#pragma unroll
+        for (int dq = 0; dq < T; ++dq) {
+          const int p = p_hi - dp, q = q_hi - dq;
+          if (dp < nt[k][0] && dq < nt[k][1]) {
+            const int r = h + g.pad - 2 * p, u = w + g.pad - 2 * q;
+            const int64_t m = ((int64_t)n * g.P + p) * g.Q + q;
+            a[k][dp * T + dq] = __ldg(reinterpret_cast<const uint4*>(dcols + m * ldc + (int64_t)(r * R + u) * g.C + cv * 8));
+          }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      if (idx[k] >= nvec) continue;
+      const bool none = nt[k][0] == 0 || nt[k][1] == 0;
+      if (none && beta != 0.f) continue;  // dx += 0 (beta is an accumulate flag, as in col2im_v)
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int dp = 0; dp < T; ++dp)
+#pragma unroll
+        for (int dq = 0; dq < T; ++dq)
+          if (dp < nt[k][0] && dq < nt[k][1]) {
+            const uint16_t* hv = reinterpret_cast<const uint16_t*>(&a[k][dp * T + dq]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += bf2f(hv[j]);
+          }
+      uint16_t* dst = dx + (int64_t)idx[k] * 8;
+      if (beta != 0.f) {
+        const uint4 o = *reinterpret_cast<const uint4*>(dst);
+        const uint16_t* hv = reinterpret_cast<const uint16_t*>(&o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += bf2f(hv[j]);
+      }
+      uint4 o;
+      uint16_t* ho = reinterpret_cast<uint16_t*>(&o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ho[j] = f2bf(acc[j]);
+      *reinterpret_cast<uint4*>(dst) = o;
+    }
   }
 }
 
@@ -1194,6 +1270,16 @@ void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtyp
   const int64_t total = (int64_t)g.N * g.H * g.W * g.C;
   if (total == 0) return;
   if (g.C % 8 == 0 && ldc % 8 == 0 && aligned16(dcols) && aligned16(dx)) {
+    if (dt == BE_BF16 && g.stride == 2 && g.R == g.S && (g.R == 1 || g.R == 3) && total / 8 < (1LL << 31)) {
+      const uint32_t nvec = (uint32_t)(total / 8);
+      const int64_t blocks = std::min<int64_t>(((int64_t)nvec + 511) / 512, (int64_t)ctx().num_sms * 8);
+      if (g.R == 1)
+        launch_pdl(col2im_s2_bf16<1>, (unsigned)blocks, 256, 0, s, (const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, nvec);
+      else
+        launch_pdl(col2im_s2_bf16<3>, (unsigned)blocks, 256, 0, s, (const uint16_t*)dcols, ldc, (uint16_t*)dx, g, beta, nvec);
+      after_launch("col2im_s2");
+      return;
+    }
     if (total / 8 < (1LL << 31))
       launch_pdl(col2im_v<uint32_t>, grid_for(total / 8), 256, 0, s, dcols, ldc, dx, g, beta, (uint32_t)(total / 8), dt);
     else
@@ -1330,14 +1416,19 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
     if (stream) sp = bn_stream_splits(rows, C, sp);
     const int64_t rps = (rows + sp - 1) / sp;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
-    if (stream)
-      bn_stats_stream(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, sp, s);
-    else if (dt == BE_BF16)
-      launch_pdl(bn_stats_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, rps);
-    else
-      launch_pdl(bn_reduce_v<0>, grid, 256, 0, s, x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
-                                          partial + sp * C, rps, nullptr, nullptr);
-    after_launch("bn_stats_v");
+    if (stream) {
+      if (bn_stats_stream(reinterpret_cast<const uint16_t*>(x), rows, C, partial, partial + sp * C, sp, s, eps, mean,
+                          invstd, run_mean, run_var, momentum))
+        return;
+    } else {
+      if (dt == BE_BF16)
+        launch_pdl(bn_stats_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), rows, C, partial,
+                   partial + sp * C, rps);
+      else
+        launch_pdl(bn_reduce_v<0>, grid, 256, 0, s, x, nullptr, nullptr, 0, rows, C, dt, nullptr, nullptr, partial,
+                   partial + sp * C, rps, nullptr, nullptr);
+      after_launch("bn_stats_v");
+    }
     launch_pdl(bn_finalize_v<0>, (C + 7) / 8, 1024, 0, s, partial, partial + sp * C, (int)sp, C, rows, x, dt, eps, mean,
                                                     invstd, run_mean, run_var, momentum, nullptr, nullptr, 0.f,
                                                     nullptr);
@@ -1408,19 +1499,23 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       float* p1 = partial + sp * C;
       float* sums = partial + 2 * sp * C;
       dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
+      bool folded = false;
       if (stream) {
-        bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), 0, rows, C, mean,
-                         invstd, p0, p1, sp, gamma, nullptr, reinterpret_cast<const uint16_t*>(rmask),
-                         reinterpret_cast<uint16_t*>(gout), s, rbits);
+        folded = bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), 0, rows,
+                                  C, mean, invstd, p0, p1, sp, gamma, nullptr,
+                                  reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout), s, rbits,
+                                  sums, dgamma, dbeta, gb_beta);
       } else {
         launch_pdl(bn_reduce_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
                                             0, rows, C, mean, invstd, p0, p1, rps, gamma, nullptr,
                                             reinterpret_cast<const uint16_t*>(rmask), reinterpret_cast<uint16_t*>(gout));
         after_launch("bn_bwd_reduce_mask_bf16");
       }
-      launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
-                                                      nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
-      after_launch("bn_bwd_finalize_v");
+      if (!folded) {
+        launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr,
+                   nullptr, nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
+        after_launch("bn_bwd_finalize_v");
+      }
       if (dx && stream) {
         bn_dx_stream(reinterpret_cast<const uint16_t*>(gout), reinterpret_cast<const uint16_t*>(x), 0,
                      reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, nullptr, s);
@@ -1447,9 +1542,11 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
     float* p1 = partial + sp * C;
     float* sums = partial + 2 * sp * C;
     dim3 grid((C + kBnCG - 1) / kBnCG, (unsigned)sp);
+    bool folded = false;
     if (stream)
-      bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), act, rows, C, mean,
-                       invstd, p0, p1, sp, gamma, bn_beta, nullptr, nullptr, s);
+      folded = bn_reduce_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy), act, rows,
+                                C, mean, invstd, p0, p1, sp, gamma, bn_beta, nullptr, nullptr, s, nullptr, sums,
+                                dgamma, dbeta, gb_beta);
     else if (fast)
       launch_pdl(bn_reduce_bf16, grid, 256, 0, s, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(dy),
                                           act, rows, C, mean, invstd, p0, p1, rps, gamma, bn_beta, nullptr, nullptr);
@@ -1457,9 +1554,11 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       launch_pdl(bn_reduce_v<2>, grid, 256, 0, s, x, dy, y, act, rows, C, dt, mean, invstd, p0, p1, rps,
                                           bn_beta ? gamma : nullptr, bn_beta);
     if (!stream) after_launch("bn_bwd_reduce_v");
-    launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr, nullptr,
-                                                    nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
-    after_launch("bn_bwd_finalize_v");
+    if (!folded) {
+      launch_pdl(bn_finalize_v<2>, (C + 7) / 8, 1024, 0, s, p0, p1, (int)sp, C, rows, nullptr, dt, 0.f, nullptr,
+                 nullptr, nullptr, nullptr, 0.f, dgamma, dbeta, gb_beta, sums);
+      after_launch("bn_bwd_finalize_v");
+    }
     if (dx && stream) {
       bn_dx_stream(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(x), act,
                    reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, bn_beta, s);
