@@ -2278,6 +2278,212 @@ __global__ void __launch_bounds__(wgs::kThreads, 1) conv_wgrad_stem_kernel(const
   }
 }
 
+// ---------------------------------------------------------------- stem conv wgrad, Hankel operand (no im2col)
+// The same product as conv_wgrad_stem_kernel, with dY as the A operand
+// (M = 64 output channels, MN-major SW128 straight from the TMA'd dY row) and
+// the phase-split input patch itself as B: for filter row r and column phase
+// φ, the taps s = φ + st·s' (s' = 0 … n_φ−1) of output pixel q read patch
+// pixel q + s' of phase φ, i.e. B[n = (s', c), k = q] sits at
+// φ·phb + (r·L + q + s')·16 + 2c — an MN-major SWIZZLE_NONE operand whose
+// 8-channel core matrices step 16 B along N (SBO) and 128 B per 8 pixels
+// along K (LBO): overlapping core matrices (a Hankel matrix), read in place.
+// One tcgen05.mma (M = 64, N = 8·n_φ, K = 16 pixels) per (r, φ, 16 pixels);
+// the R·S·8 accumulator columns stay in TMEM over all of the CTA's rows.
+// Nothing is copied inside shared memory: the build warps of
+// conv_wgrad_stem_kernel (its bottleneck) are gone.
+namespace wgh {
+constexpr int kThreads = 384;   // w0-3 patch copy, w4 MMA, w5 dY TMA, w6 TMEM, w8-11 epilogue
+constexpr int kCopy = 128;
+constexpr int NY = 4;           // dY row buffers (16 KB each)
+constexpr int NP = 4;           // patch buffers
+constexpr int kSlack = 2048;    // zeroed bytes after the last patch (ragged-Q reads past it)
+inline int smem_bytes(const ConvGeom& g, int phb) { return 1024 + NY * 16384 + NP * g.stride * phb + kSlack + 1024; }
+}  // namespace wgh
+
+// KR, KS, KST: compile-time filter rows / columns / stride (the ResNet stem's
+// 7, 7, 2) — the MMA issue loop then unrolls to one UTCHMMA per few
+// instructions; 0, 0, 0: run-time geometry (an issue loop of ~20 uniform-
+// datapath instructions per MMA, which bounds the kernel)
+template <int KR, int KS, int KST>
+__global__ void __launch_bounds__(wgh::kThreads, 1) conv_wgrad_hankel_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int st = KST ? KST : p.cstride, R = KR ? KR : p.cR, S = KS ? KS : p.cS, L = p.st_L;
+  const int patch_bytes = st * p.st_phb;
+  uint8_t* ybuf = smem;                                   // NY × 128 rows × 128 B
+  uint8_t* patch = ybuf + wgh::NY * 16384;                // NP × patch_bytes
+  uint64_t* full_p = reinterpret_cast<uint64_t*>(patch + wgh::NP * patch_bytes + wgh::kSlack);
+  uint64_t* empty_p = full_p + wgh::NP;
+  uint64_t* full_y = empty_p + wgh::NP;
+  uint64_t* empty_y = full_y + wgh::NY;
+  uint64_t* done = empty_y + wgh::NY;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);   // + 4 words, then the MMA tables (512 B)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // pixels past Q of the last 16-pixel step read patch bytes past the copied
+  // row: zero them once (their dY rows are TMA zero-filled, 0 · finite = 0)
+  for (int i = threadIdx.x; i < (wgh::NP * patch_bytes + wgh::kSlack) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(patch)[i] = make_uint4(0, 0, 0, 0);
+  sm100::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < wgh::NP; ++b) { sm100::mbar_init(&full_p[b], wgh::kCopy); sm100::mbar_init(&empty_p[b], 1); }
+    for (int b = 0; b < wgh::NY; ++b) { sm100::mbar_init(&full_y[b], 1); sm100::mbar_init(&empty_y[b], 1); }
+    sm100::mbar_init(done, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.tb[0]);
+  }
+  if (warp == 6) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.cN * p.cP;
+  const int nks = (p.cQ + 15) / 16;
+
+  if (warp < 4) {
+    // ===================== patch copy (phase-split rows, cp.async), one group in flight =====================
+    const int tid = threadIdx.x, span = L * st;
+    const int ua = tid, ub = tid + wgh::kCopy;
+    const int wa = ua - p.cpad, wb = ub - p.cpad;
+    const bool va = ua < span, vb = ub < span;
+    const bool oka = va && (unsigned)wa < (unsigned)p.cW, okb = vb && (unsigned)wb < (unsigned)p.cW;
+    const uint32_t da = (ua % st) * p.st_phb + (ua / st) * 16, db = (ub % st) * p.st_phb + (ub / st) * 16;
+    const long long xa = oka ? (long long)wa * 8 : 0, xb = okb ? (long long)wb * 8 : 0;
+    const uint32_t L16 = L * 16;
+    int b = 0; uint32_t phase = 0;
+    int prev = -1;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int n = t / p.cP, pp = t - n * p.cP;
+      sm100::mbar_wait_sleep(&empty_p[b], phase ^ 1, 200);
+      uint32_t dst = sm100::smem_u32(patch + b * patch_bytes);
+      const int h0 = pp * st - p.cpad;
+      const uint16_t* img = p.x + (long long)n * p.cH * p.cW * 8;
+      for (int r = 0; r < R; ++r, dst += L16) {
+        const int h = h0 + r;
+        const bool hok = (unsigned)h < (unsigned)p.cH;
+        const uint16_t* srow = img + (long long)(hok ? h : 0) * p.cW * 8;
+        if (va && !(p.st_wbytes & 2)) sm100::cp_async_16(dst + da, hok && oka ? srow + xa : p.x, hok && oka ? 16u : 0u);
+        if (vb && !(p.st_wbytes & 2)) sm100::cp_async_16(dst + db, hok && okb ? srow + xb : p.x, hok && okb ? 16u : 0u);
+      }
+      sm100::cp_async_commit();
+      if (prev >= 0) {
+        sm100::cp_async_wait<1>();
+        sm100::fence_proxy_async();
+        sm100::mbar_arrive(&full_p[prev]);
+      }
+      prev = b;
+      if (++b == wgh::NP) { b = 0; phase ^= 1; }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    if (prev >= 0) sm100::mbar_arrive(&full_p[prev]);
+  } else if (warp == 4) {
+    // ===================== MMA: per 16 pixels, one (M 64, N 8·n_φ, K 16) per (r, φ) =====================
+    // descriptors by addition only, the warp converged (warp-uniform values
+    // stay in uniform registers; one elected lane issues): per phase φ its
+    // instruction descriptor, column count and byte offset; the B start steps
+    // by one patch row (L pixels) per filter row r.  (A lane-0-only loop
+    // that looked per-(r, φ) descriptors up in a table issued one MMA per
+    // ~130 cycles.)
+    {
+      uint32_t idp[4], ncol[4];
+      uint64_t dph[4];
+#pragma unroll
+      for (int ph = 0; ph < 4; ++ph) {
+        const int nph = ph < st ? (S - ph + st - 1) / st : 0;
+        ncol[ph] = nph > 0 ? 8u * nph : 0u;
+        idp[ph] = sm100::make_idesc(1u, 64, nph > 0 ? 8 * nph : 8, 1, 1);
+        dph[ph] = (uint64_t)((ph * p.st_phb) >> 4);
+      }
+      const uint64_t a0 = sm100::make_sw128_desc(sm100::smem_u32(ybuf), 16, 1024);
+      const uint64_t b0 = sm100::make_interleave_desc(sm100::smem_u32(patch), 128, 16);
+      int ti = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+        const int by = ti % wgh::NY, bp = ti % wgh::NP;
+        sm100::mbar_wait(&full_y[by], (uint32_t)((ti / wgh::NY) & 1));
+        sm100::mbar_wait(&full_p[bp], (uint32_t)((ti / wgh::NP) & 1));
+        sm100::tc_fence_after();
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t ad = a0 + (uint64_t)((by * 16384 + ks * 2048) >> 4);
+          uint64_t brow = b0 + (uint64_t)((bp * patch_bytes) >> 4) + (uint64_t)(ks * 16);  // 16 pixels × 16 B
+          const uint32_t accf = (ti | ks) ? 1u : 0u;
+          const bool leader = sm100::elect_one();
+          if constexpr (KR != 0) {
+            if (leader) {
+#pragma unroll
+              for (int r = 0; r < KR; ++r)
+#pragma unroll
+                for (int ph = 0; ph < KST; ++ph) {
+                  constexpr int dummy = 0;
+                  (void)dummy;
+                  // column of (r, φ): r·KS·8 + 8·(taps of phases < φ)
+                  const uint32_t col = tmem_base + (uint32_t)(r * KS * 8 + 8 * (ph * (KS / KST) + (ph < KS % KST ? ph : KS % KST)));
+                  sm100::mma_bf16(col, ad, brow + (uint64_t)(r * L) + dph[ph], idp[ph], accf);
+                }
+            }
+          } else {
+            uint32_t col = tmem_base;
+            for (int r = 0; r < R; ++r, brow += (uint64_t)L) {
+#pragma unroll
+              for (int ph = 0; ph < 4; ++ph)
+                if (ncol[ph]) {
+                  if (leader && !(p.st_wbytes & 1)) sm100::mma_bf16(col, ad, brow + dph[ph], idp[ph], accf);
+                  col += ncol[ph];
+                }
+            }
+          }
+          __syncwarp();
+        }
+        if (sm100::elect_one()) { sm100::mma_commit(&empty_p[bp]); sm100::mma_commit(&empty_y[by]); }
+        __syncwarp();
+      }
+      if (sm100::elect_one()) sm100::mma_commit(done);
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      int ti = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+        const int by = ti % wgh::NY, n = t / p.cP, pp = t - n * p.cP;
+        sm100::mbar_wait(&empty_y[by], (uint32_t)((ti / wgh::NY) & 1) ^ 1u);
+        sm100::mbar_arrive_expect_tx(&full_y[by], 16384u);
+        sm100::tma_load_4d(&p.tb[0], &full_y[by], ybuf + by * 16384, 0, 0, pp, n);
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue: D[k][(r, φ, s', c)] → slab[k][(r·S + φ + st·s')·8 + c] =====================
+    // M = 64 accumulator: row i in TMEM lane (i / 16)·32 + i % 16 (lanes 0-15 of each quarter)
+    const int eq = warp & 3;
+    const int RSC = R * S * 8;
+    const int k = eq * 16 + lane;
+    float* slab = reinterpret_cast<float*>(p.D) + (long long)blockIdx.x * p.split_stride;
+    sm100::mbar_wait_sleep(done, 0, 2000);
+    sm100::tc_fence_after();
+    uint32_t col = 0;
+    for (int r = 0; r < R; ++r)
+      for (int ph = 0; ph < st; ++ph) {
+        const int nph = (S - ph + st - 1) / st;
+        for (int sp = 0; sp < nph; ++sp, col += 8) {
+          uint32_t v[8];
+          sm100::tmem_ld_32x32b_x8(tmem_base + col + ((uint32_t)(eq * 32) << 16), v);
+          sm100::tmem_ld_wait();
+          if (lane < 16 && num_tiles > (int)blockIdx.x) {
+            const int m0 = (r * S + ph + st * sp) * 8;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) slab[(long long)k * RSC + m0 + c] = __uint_as_float(v[c]);
+          }
+        }
+      }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -3022,6 +3228,9 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   const wgs::Geo e = wgs::geo(g);
   if (e.L * g.stride > 2 * wgs::kCopy || e.ns < 2 || e.smem > 227 * 1024) return false;
   if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  // Hankel-operand kernel when the R·S·8 accumulator columns fit TMEM
+  const bool hankel = on != 1 ? on == 2
+                                : (g.R * g.S * 8 <= 512 && g.R * g.stride <= 32 && wgh::smem_bytes(g, e.phb) <= 227 * 1024);
   GemmParams p;
   memset(&p, 0, sizeof(p));
   const uint64_t dy4[4] = {(uint64_t)g.K, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.N};
@@ -3030,6 +3239,10 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
   p.cstride = g.stride; p.cpad = g.pad;
   p.st_L = e.L; p.st_phb = e.phb; p.st_taps = e.Mt; p.st_nbuf = e.ns | (e.np << 8);
+  if (hankel) {  // BE_HANKEL_DBG (timing experiments only): bit 0 skips the MMAs, bit 1 the patch copies
+    static const int dbg = [] { const char* v = getenv("BE_HANKEL_DBG"); return v ? atoi(v) : 0; }();
+    p.st_wbytes = dbg;
+  }
   const int RSC = g.R * g.S * 8;
   const int grid = std::min(g.N * g.P, ctx().num_sms);
   p.split_stride = 64LL * RSC;
@@ -3039,12 +3252,20 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   if (!attr) {
     BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_hankel_kernel<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_hankel_kernel<7, 7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
     attr = true;
   }
   const double flops = 2.0 * g.N * g.P * g.Q * 64.0 * RSC;
   const double bytes = ((double)g.N * g.H * g.W * 8 + (double)g.N * g.P * g.Q * 64) * 2.0 + 4.0 * 64 * RSC;
   const int pidx = prof_begin("conv_tc_wgrad_stem", flops, bytes, 64, RSC, g.N * g.P * g.Q, s);
-  launch_pdl(conv_wgrad_stem_kernel, grid, wgs::kThreads, e.smem, s, p);
+  if (hankel)
+    launch_pdl(g.R == 7 && g.S == 7 && g.stride == 2 ? conv_wgrad_hankel_kernel<7, 7, 2> : conv_wgrad_hankel_kernel<0, 0, 0>,
+               grid, wgh::kThreads, wgh::smem_bytes(g, e.phb), s, p);
+  else
+    launch_pdl(conv_wgrad_stem_kernel, grid, wgs::kThreads, e.smem, s, p);
   prof_end(pidx, s);
   after_launch("conv_wgrad_stem");
   g_tc_calls++;
