@@ -2484,6 +2484,144 @@ __global__ void __launch_bounds__(wgh::kThreads, 1) conv_wgrad_hankel_kernel(con
   }
 }
 
+// ---------------------------------------------------------------- stem wgrad, two output rows per MMA
+// ResNet stem (7×7, stride 2, C = 8): output rows p and p+1 read input rows
+// 2p−3 … 2p+5 — nine patch rows j, row p with filter row r = j, row p+1 with
+// r = j − 2.  Stacking the two dY rows as the M = 128 A operand (M-atoms
+// 16 KB apart) makes one tcgen05.mma per (patch row j, phase φ, 16 pixels)
+// serve both rows: 126 MMAs per row pair instead of 196, at M = 128.  Both
+// operands arrive by TMA, one stage per row pair: the dY rows (SW128) and
+// the patch, each column phase φ one strided 4-D box (W traversal stride 2,
+// start w = φ − pad, zero fill outside the image) landing in exactly the
+// phase-split layout the Hankel descriptors read.  TMEM region j
+// (56 columns): lanes 0-63 accumulate filter row j (row p), lanes 64-127
+// filter row j − 2 (row p+1); the epilogue adds the two halves in a fixed
+// order.  9 × 56 = 504 of the 512 columns.
+namespace wgh2 {
+constexpr int kThreads = 384;    // w0 TMA, w4 MMA, w6 TMEM, w8-11 epilogue
+constexpr int NS = 3;            // stages (dY row pair + patch)
+constexpr int RJ = 9;            // patch rows
+constexpr int kSlack = 2048;
+inline int phb(int L) { return (RJ * L * 16 + 64 + 511) / 512 * 512; }  // stages stay 1024-B aligned (SW128 dY)
+inline int stage_bytes(int L) { return 32768 + 2 * phb(L); }
+inline int smem_bytes(int L) { return 1024 + NS * stage_bytes(L) + kSlack + 1024; }
+}  // namespace wgh2
+
+__global__ void __launch_bounds__(wgh2::kThreads, 1) conv_wgrad_hankel2_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
+  constexpr int R = 7, S = 7, RJ = wgh2::RJ;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int L = p.st_L, phb = p.st_phb;
+  const int sbytes = 32768 + 2 * phb;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + wgh2::NS * sbytes + wgh2::kSlack);
+  uint64_t* empty = full + wgh2::NS;
+  uint64_t* done = empty + wgh2::NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // the patch slack past each phase block (and past the last stage) is read
+  // for pixels ≥ Q, whose dY rows are zero: zero it once (TMA never writes it)
+  for (int i = threadIdx.x; i < (wgh2::NS * sbytes + wgh2::kSlack) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  sm100::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < wgh2::NS; ++b) { sm100::mbar_init(&full[b], 1); sm100::mbar_init(&empty[b], 1); }
+    sm100::mbar_init(done, 1);
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.tb[0]);
+    sm100::tma_prefetch(&p.ta[0]);
+  }
+  if (warp == 6) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int PP = (p.cP + 1) >> 1;
+  const int num_tiles = p.cN * PP;
+  const int nks = (p.cQ + 15) / 16;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA: dY rows p, p+1 and the two patch phases =====================
+      const uint32_t tx = 32768u + 2u * (uint32_t)(RJ * L * 16);
+      int ti = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+        const int b = ti % wgh2::NS, n = t / PP, p0 = (t - n * PP) * 2;
+        sm100::mbar_wait(&empty[b], (uint32_t)((ti / wgh2::NS) & 1) ^ 1u);
+        uint8_t* st = smem + b * sbytes;
+        sm100::mbar_arrive_expect_tx(&full[b], tx);
+        sm100::tma_load_4d(&p.tb[0], &full[b], st, 0, 0, p0, n);
+        const int h0 = p0 * 2 - p.cpad;
+        sm100::tma_load_4d(&p.ta[0], &full[b], st + 32768, 0, -p.cpad, h0, n);
+        sm100::tma_load_4d(&p.ta[0], &full[b], st + 32768 + phb, 0, 1 - p.cpad, h0, n);
+      }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA: (M 128 = two dY rows, N 32 | 24, K 16) per (j, φ, 16 pixels) =====================
+    const uint32_t id0 = sm100::make_idesc(1u, 128, 32, 1, 1), id1 = sm100::make_idesc(1u, 128, 24, 1, 1);
+    const uint64_t a0 = sm100::make_sw128_desc(sm100::smem_u32(smem), 16384, 1024);
+    const uint64_t b0 = sm100::make_interleave_desc(sm100::smem_u32(smem + 32768), 128, 16);
+    const uint64_t dph1 = (uint64_t)(phb >> 4);
+    int ti = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
+      const int b = ti % wgh2::NS;
+      sm100::mbar_wait(&full[b], (uint32_t)((ti / wgh2::NS) & 1));
+      sm100::tc_fence_after();
+      const uint64_t so = (uint64_t)((b * sbytes) >> 4);
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t ad = a0 + so + (uint64_t)(ks * 128);   // 16 pixels × 128 B
+        const uint64_t brow = b0 + so + (uint64_t)(ks * 16);  // 16 pixels × 16 B
+        const uint32_t accf = (ti | ks) ? 1u : 0u;
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) {
+            sm100::mma_bf16(tmem_base + j * 56, ad, brow + (uint64_t)(j * L), id0, accf);
+            sm100::mma_bf16(tmem_base + j * 56 + 32, ad, brow + (uint64_t)(j * L) + dph1, id1, accf);
+          }
+        }
+        __syncwarp();
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&empty[b]);
+      __syncwarp();
+    }
+    if (sm100::elect_one()) sm100::mma_commit(done);
+    __syncwarp();
+  } else if (warp >= 8) {
+    // ===================== epilogue: slab[k][(r·7 + s)·8 + c] = top[j = r] + bottom[j = r + 2] =====================
+    const int eq = warp & 3, half = eq >> 1;
+    const int k = (eq & 1) * 32 + lane;
+    constexpr int RSC = R * S * 8;
+    float* slab = reinterpret_cast<float*>(p.D) + (long long)blockIdx.x * p.split_stride;
+    sm100::mbar_wait_sleep(done, 0, 2000);
+    sm100::tc_fence_after();
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == half) {
+        const int j0 = half ? 2 : 0;
+        for (int j = j0; j < j0 + R; ++j) {
+          const int r = j - j0;
+          for (int g8 = 0; g8 < 7; ++g8) {   // column groups of region j: φ 0 (s' 0..3), φ 1 (s' 0..2)
+            uint32_t v[8];
+            sm100::tmem_ld_32x32b_x8(tmem_base + j * 56 + g8 * 8 + ((uint32_t)(eq * 32) << 16), v);
+            sm100::tmem_ld_wait();
+            const int sidx = g8 < 4 ? 2 * g8 : 2 * (g8 - 4) + 1;   // tap column s
+            float* dst = slab + (long long)k * RSC + (r * S + sidx) * 8;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dst[c] = half ? dst[c] + __uint_as_float(v[c]) : __uint_as_float(v[c]);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT path
 // 64x64 tiles, 256 threads, 4x4 outputs per thread, fp32 accumulate.
 template <typename TA>
@@ -3234,17 +3372,35 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
   GemmParams p;
   memset(&p, 0, sizeof(p));
   const uint64_t dy4[4] = {(uint64_t)g.K, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.N};
-  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, 128, 1, 1)) return false;
   p.x = reinterpret_cast<const uint16_t*>(x);
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S; p.cP = g.P; p.cQ = g.Q;
   p.cstride = g.stride; p.cpad = g.pad;
   p.st_L = e.L; p.st_phb = e.phb; p.st_taps = e.Mt; p.st_nbuf = e.ns | (e.np << 8);
+  // two output rows per MMA for the ResNet stem geometry
+  bool two_rows = hankel && g.R == 7 && g.S == 7 && g.stride == 2 && on != 3 && wgh2::smem_bytes(e.L) <= 227 * 1024;
   if (hankel) {  // BE_HANKEL_DBG (timing experiments only): bit 0 skips the MMAs, bit 1 the patch copies
     static const int dbg = [] { const char* v = getenv("BE_HANKEL_DBG"); return v ? atoi(v) : 0; }();
     p.st_wbytes = dbg;
   }
+  if (two_rows) {
+    // patch map: x [N, H, W, 8] bf16, W traversed with stride 2 (one column
+    // phase per load), box 8 × L × 9 rows, no swizzle (phase-split layout)
+    EncodeFn enc = get_encode();
+    cuuint64_t d[4] = {8, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    cuuint64_t st4[3] = {16, (cuuint64_t)g.W * 16, (cuuint64_t)g.H * g.W * 16};
+    cuuint32_t box[4] = {8, (cuuint32_t)(2 * e.L), (cuuint32_t)wgh2::RJ, 1};
+    cuuint32_t estr[4] = {1, 2, 1, 1};
+    if (!enc || 2 * e.L > 256 ||
+        enc(&p.ta[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), d, st4, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      two_rows = false;
+    else
+      p.st_phb = wgh2::phb(e.L);
+  }
+  if (!encode_4d_tiled(&p.tb[0], dy, dy4, 64, 128, two_rows ? 2 : 1, 1)) return false;
   const int RSC = g.R * g.S * 8;
-  const int grid = std::min(g.N * g.P, ctx().num_sms);
+  const int grid = std::min(two_rows ? g.N * ((g.P + 1) / 2) : g.N * g.P, ctx().num_sms);
   p.split_stride = 64LL * RSC;
   Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)grid * p.split_stride, s);
   p.D = ws->ptr;
@@ -3256,12 +3412,16 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
                                        227 * 1024));
     BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_hankel_kernel<7, 7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024));
+    BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_hankel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
     attr = true;
   }
   const double flops = 2.0 * g.N * g.P * g.Q * 64.0 * RSC;
   const double bytes = ((double)g.N * g.H * g.W * 8 + (double)g.N * g.P * g.Q * 64) * 2.0 + 4.0 * 64 * RSC;
   const int pidx = prof_begin("conv_tc_wgrad_stem", flops, bytes, 64, RSC, g.N * g.P * g.Q, s);
-  if (hankel)
+  if (two_rows)
+    launch_pdl(conv_wgrad_hankel2_kernel, grid, wgh2::kThreads, wgh2::smem_bytes(e.L), s, p);
+  else if (hankel)
     launch_pdl(g.R == 7 && g.S == 7 && g.stride == 2 ? conv_wgrad_hankel_kernel<7, 7, 2> : conv_wgrad_hankel_kernel<0, 0, 0>,
                grid, wgh::kThreads, wgh::smem_bytes(g, e.phb), s, p);
   else
