@@ -91,6 +91,49 @@ __global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, T*
   }
 }
 
+// ---- im2col, tap loop: one item per (m, VEC-channel chunk); the (n, p, q)
+// decomposition is done once per item and the R·S taps are copied with their
+// loads batched (8 in flight).  The per-(m, r, u, chunk) form above spends
+// ~6 run-time divisions per 16-B copy and ran ALU-bound (~2.9 TB/s on the
+// ResNet layer-3 wgrad columns); consecutive threads take consecutive channel
+// chunks of one pixel, so each tap's loads and stores stay coalesced.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) im2col_taps_kernel(const T* __restrict__ x, T* __restrict__ cols, int64_t ldc,
+                                                          ConvGeom g, uint32_t total) {
+  pdl_entry();
+  using VT = typename std::conditional<VEC * sizeof(T) == 16, uint4, T>::type;
+  constexpr int B = 8;
+  const uint32_t CV = (uint32_t)(g.C / VEC);
+  const int RS = g.R * g.S;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int cv = (int)(i % CV);
+    const uint32_t m = i / CV;
+    const int q = (int)(m % (uint32_t)g.Q);
+    const uint32_t np = m / (uint32_t)g.Q;
+    const int p = (int)(np % (uint32_t)g.P);
+    const int n = (int)(np / (uint32_t)g.P);
+    const int h0 = p * g.stride - g.pad, w0 = q * g.stride - g.pad;
+    const T* xn = x + (int64_t)n * g.H * g.W * g.C + cv * VEC;
+    T* dst = cols + (int64_t)m * ldc + cv * VEC;
+    for (int t0 = 0; t0 < RS; t0 += B) {
+      VT v[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const int t = t0 + k;
+        const int r = t / g.S, u = t - r * g.S;
+        const int h = h0 + r, w = w0 + u;
+        v[k] = VT{};
+        if (t < RS && h >= 0 && h < g.H && w >= 0 && w < g.W)
+          v[k] = *reinterpret_cast<const VT*>(xn + ((int64_t)h * g.W + w) * g.C);
+      }
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+        if (t0 + k < RS) *reinterpret_cast<VT*>(dst + (int64_t)(t0 + k) * g.C) = v[k];
+    }
+  }
+}
+
 // ---- col2im (gather form): dx[n,h,w,c] = Σ_{r,u: h=p·s−pad+r, w=q·s−pad+u} dcols[(n,p,q),(r,u,c)]
 template <typename T>
 __global__ void col2im_kernel(const T* __restrict__ dcols, int64_t ldc, T* __restrict__ dx, ConvGeom g, float beta,
@@ -353,6 +396,41 @@ __global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __
     const int r = (int)(t % R);
     const int c = (int)(t / R);
     wf[i] = w[(((int64_t)k * R + (R - 1 - r)) * S + (S - 1 - s)) * C + c];
+  }
+}
+
+// Phase-convolution weights (conv_dgrad_phases): source tap (r, s) of
+// w[K, R, S, C] belongs to phase (ρh, ρw) = ((r − pad) mod st, (s − pad) mod st)
+// and sits at [c, t_r, t_s, k] of that phase's block, t = (ρ + pad − r)/st − dmin[ρ]
+struct PhaseW {
+  int64_t off[16];
+  int cr[4], dr[4], cs[4], ds[4];
+};
+__global__ void phase_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ wp, int K, int R, int S,
+                                     int C, int st, int pad, PhaseW pw, int64_t total) {
+  pdl_entry();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int k = (int)(t % K); t /= K;
+    const int s = (int)(t % S); t /= S;
+    const int r = (int)(t % R);
+    const int c = (int)(t / R);
+    const int rh = ((r - pad) % st + st) % st, rw = ((s - pad) % st + st) % st;
+    const int tr = (rh + pad - r) / st - pw.dr[rh], ts = (rw + pad - s) / st - pw.ds[rw];
+    wp[pw.off[rh * st + rw] + (((int64_t)c * pw.cr[rh] + tr) * pw.cs[rw] + ts) * K + k] =
+        w[(((int64_t)k * R + r) * S + s) * C + c];
+  }
+}
+// zero dx pixels (n, h, w) of the phases without taps, 8 channels per item
+__global__ void phase_zero_kernel(uint16_t* __restrict__ dx, ConvGeom g, uint32_t live, int64_t total) {
+  pdl_entry();
+  const int CV = g.C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i / CV;
+    const int w = (int)(t % g.W); t /= g.W;
+    const int h = (int)(t % g.H);
+    const int ph = (h % g.stride) * g.stride + (w % g.stride);
+    if (!((live >> ph) & 1u)) *reinterpret_cast<uint4*>(dx + i * 8) = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -1250,6 +1328,12 @@ __global__ void __launch_bounds__(256) maxpool_bwd_rows(const uint16_t* __restri
 
 template <typename T, int VEC>
 static void im2col_launch(const void* x, void* cols, int64_t ldc, const ConvGeom& g, int64_t total, cudaStream_t s) {
+  const int64_t items = total / ((int64_t)g.R * g.S);
+  if (VEC > 1 && items < (1LL << 31)) {  // tap-loop form (total = items · R·S)
+    launch_pdl(im2col_taps_kernel<T, VEC>, grid_for(items, 2), 256, 0, s, (const T*)x, (T*)cols, ldc, g,
+               (uint32_t)items);
+    return;
+  }
   const int grid = grid_for(total, UNR);
   if (total < (1LL << 31))
     launch_pdl(im2col_kernel<T, VEC, uint32_t>, grid, 256, 0, s, (const T*)x, (T*)cols, ldc, g, (uint32_t)total);
@@ -1298,6 +1382,28 @@ void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStrea
   if (total == 0) return;
   launch_pdl(flip_weights_kernel, grid_for(total), 256, 0, s, (const uint16_t*)w, (uint16_t*)wf, K, R, S, C, total);
   after_launch("flip_weights");
+}
+void conv_phase_weights(const void* w, uint16_t* wp, const ConvGeom& g, const int* cr, const int* dr, const int* cs,
+                        const int* ds, const int64_t* woff, cudaStream_t s) {
+  PhaseW pw;
+  for (int i = 0; i < 16; ++i) pw.off[i] = woff[i];
+  for (int i = 0; i < 4; ++i) {
+    pw.cr[i] = i < g.stride ? cr[i] : 0; pw.dr[i] = i < g.stride ? dr[i] : 0;
+    pw.cs[i] = i < g.stride ? cs[i] : 0; pw.ds[i] = i < g.stride ? ds[i] : 0;
+  }
+  const int64_t total = (int64_t)g.K * g.R * g.S * g.C;
+  launch_pdl(phase_weights_kernel, grid_for(total), 256, 0, s, (const uint16_t*)w, wp, g.K, g.R, g.S, g.C, g.stride,
+             g.pad, pw, total);
+  after_launch("conv_phase_weights");
+}
+void conv_phase_zero(void* dx, const ConvGeom& g, const int* cr, const int* cs, cudaStream_t s) {
+  uint32_t live = 0;
+  for (int a = 0; a < g.stride; ++a)
+    for (int b = 0; b < g.stride; ++b)
+      if (cr[a] > 0 && cs[b] > 0) live |= 1u << (a * g.stride + b);
+  const int64_t total = (int64_t)g.N * g.H * g.W * (g.C / 8);
+  launch_pdl(phase_zero_kernel, grid_for(total), 256, 0, s, (uint16_t*)dx, g, live, total);
+  after_launch("conv_phase_zero");
 }
 void im2col_offsets(const ConvGeom& g, int64_t* out, cudaStream_t s) {
   // the product's im2col kernel (f32 element path) run on an index-encoded input

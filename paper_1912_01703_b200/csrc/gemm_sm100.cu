@@ -103,6 +103,12 @@ struct __align__(64) GemmParams {
   // weight bytes
   int st_L, st_phb, st_taps, st_nbuf, st_wbytes;
   const uint16_t* st_w;       // KRSC weights (C = 8), copied into smem by every CTA
+  // conv_tc_kernel: extra window offset on the w axis (w pad = cpad + cpad_w_off)
+  int cpad_w_off;
+  // phase store (stride-ph_st dgrad as ph_st² stride-1 phase convolutions):
+  // output row m = (n, i, j) of the phase grid [N, cP, cQ] is stored to pixel
+  // (n, ph_st·i + ph_h, ph_st·j + ph_w) of the [N, ph_H, ph_W] tensor D (ld = ldd)
+  int ph_st, ph_h, ph_w, ph_H, ph_W;
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
@@ -1129,7 +1135,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
         const int m0 = tm * BM;
         const int q0 = m0 % p.cQ, pq = m0 / p.cQ;
         const int p0 = pq % p.cP, n0 = pq / p.cP;
-        const int ws = q0 * p.cstride - p.cpad, hs = p0 * p.cstride - p.cpad;
+        const int ws = q0 * p.cstride - p.cpad - p.cpad_w_off, hs = p0 * p.cstride - p.cpad;
         for (int kb = 0; kb < kblocks; ++kb) {
           const int tap = kb / CB, cb = kb - tap * CB;
           const int r = tap / p.cS, s = tap - r * p.cS;
@@ -1158,7 +1164,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
           const int pp = pq % p.cP;
           nb[i] = (pq / p.cP) * p.cH;
           hb[i] = pp * p.cstride - p.cpad;
-          wb[i] = q * p.cstride - p.cpad;
+          wb[i] = q * p.cstride - p.cpad - p.cpad_w_off;
         } else {
           nb[i] = 0; hb[i] = -(1 << 20); wb[i] = 0;  // always out of range
         }
@@ -1256,6 +1262,13 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         }
       }
       } else {
+      // phase store: the row's pixel in the full-resolution output
+      int orow = row;
+      if (p.ph_st && row_ok) {
+        const int j = row % p.cQ, ni = row / p.cQ;
+        const int i = ni % p.cP, n = ni / p.cP;
+        orow = (n * p.ph_H + p.ph_st * i + p.ph_h) * p.ph_W + p.ph_st * j + p.ph_w;
+      }
       #pragma unroll 1
       for (int it = 0; it < (BN / 2 + 63) / 64; ++it) {
         const int c0 = eh * (BN / 2) + it * 64;
@@ -1272,8 +1285,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
           if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
         } else if (row_ok) {
-          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
-          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
+          epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, orow, col0, r0);
+          if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, orow, col1, r1);
         }
       }
       }
@@ -2906,7 +2919,8 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-bool encode_im2col_4d(CUtensorMap* m, const void* x, const ConvGeom& g, int chans, int pixels) {
+bool encode_im2col_4d(CUtensorMap* m, const void* x, const ConvGeom& g, int chans, int pixels,
+                      const int* corners = nullptr) {
   static EncodeIm2colFn fn = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -2920,6 +2934,10 @@ bool encode_im2col_4d(CUtensorMap* m, const void* x, const ConvGeom& g, int chan
   cuuint64_t strides[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)g.W * g.C * 2, (cuuint64_t)g.H * g.W * g.C * 2};
   int lower[2] = {-g.pad, -g.pad};
   int upper[2] = {g.pad - (g.S - 1), g.pad - (g.R - 1)};
+  if (corners) {  // explicit {lower w, lower h, upper w, upper h}
+    lower[0] = corners[0]; lower[1] = corners[1]; upper[0] = corners[2]; upper[1] = corners[3];
+    if (lower[0] < -128 || lower[1] < -128 || upper[0] > 127 || upper[1] > 127) return false;
+  }
   cuuint32_t es[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
                   (cuuint32_t)chans, (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -3602,6 +3620,103 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   prof_end(pidx, s);
   after_launch("conv_tc_implicit");
   g_tc_calls++;
+  return true;
+}
+
+// Taps of a stride-st convolution that reach input rows h ≡ rho (mod st):
+// r = rho + pad − st·d for the d with 0 ≤ r < R; count and the smallest d.
+static void phase_taps(int R, int st, int pad, int rho, int* cnt, int* dmin) {
+  *cnt = 0; *dmin = 0;
+  for (int r = R - 1; r >= 0; --r) {
+    const int num = rho + pad - r;
+    if (((num % st) + st) % st != 0) continue;
+    if (*cnt == 0) *dmin = num / st;  // r descending → d ascending; first hit is the smallest
+    ++*cnt;
+  }
+}
+
+// Stride-st data gradient as st² stride-1 phase convolutions:
+// for output rows h = st·i + ρh, dx[n, h, w, :] = Σ_{t_r, t_s} dY[n, i + dminh + t_r,
+// j + dminw + t_s, :] · W[:, r(t_r), s(t_s), :] with r(t) = ρh + pad − st·(dminh + t)
+// (likewise s) — every term of the transposed convolution, none of the
+// zero-inserted ones.  Each phase is one conv_tc_kernel launch: A = dY through
+// a TMA im2col map whose corners give the phase's window, B = the phase's
+// taps of W gathered into [C, R', S', K] (conv_phase_weights), and the epilogue
+// stores row (n, i, j) straight to dx pixel (n, st·i + ρh, st·j + ρw) (beta 1:
+// read-add-write).  Phases with no taps are zero-filled (beta 0) or left
+// untouched (beta 1).  Replaces the dcols GEMM + col2im.
+bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& g, float beta, cudaStream_t s) {
+  static const int on = [] { const char* e = getenv("BE_DGRAD_PHASE"); return e ? atoi(e) : 1; }();
+  const int st = g.stride;
+  if (!on || st < 2 || st > 4 || g.K % 64 != 0 || g.C % 16 != 0 || (beta != 0.f && beta != 1.f)) return false;
+  if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(w) & 15) ||
+      (reinterpret_cast<uintptr_t>(dx) & 15))
+    return false;
+  int cr[4], dr[4], cs[4], ds[4];
+  for (int rho = 0; rho < st; ++rho) {
+    phase_taps(g.R, st, g.pad, rho, &cr[rho], &dr[rho]);
+    phase_taps(g.S, st, g.pad, rho, &cs[rho], &ds[rho]);
+  }
+  // every phase map must be encodable before anything is launched
+  GemmParams ps[16];
+  int nph = 0;
+  bool zero_needed = false;
+  int64_t woff[16] = {};
+  int64_t wtot = 0;
+  const int bn = g.C >= 256 ? 256 : (g.C >= 128 ? 128 : 64);
+  for (int rh = 0; rh < st; ++rh)
+    for (int rw = 0; rw < st; ++rw) {
+      const int Hp = (g.H - rh + st - 1) / st, Wp = (g.W - rw + st - 1) / st;
+      if (Hp <= 0 || Wp <= 0) continue;
+      if (cr[rh] == 0 || cs[rw] == 0) { zero_needed = true; continue; }
+      woff[rh * st + rw] = wtot;
+      wtot += (int64_t)cr[rh] * cs[rw] * g.K * g.C;
+    }
+  Block* wb = wtot ? ctx().alloc.allocate(sizeof(uint16_t) * (size_t)wtot, s) : nullptr;
+  uint16_t* wp = wb ? reinterpret_cast<uint16_t*>(wb->ptr) : nullptr;
+  for (int rh = 0; rh < st; ++rh)
+    for (int rw = 0; rw < st; ++rw) {
+      const int Hp = (g.H - rh + st - 1) / st, Wp = (g.W - rw + st - 1) / st;
+      if (Hp <= 0 || Wp <= 0 || cr[rh] == 0 || cs[rw] == 0) continue;
+      GemmParams& p = ps[nph];
+      memset(&p, 0, sizeof(p));
+      ConvGeom t;  // the phase convolution over dY
+      t.N = g.N; t.H = g.P; t.W = g.Q; t.C = g.K; t.K = g.C; t.R = cr[rh]; t.S = cs[rw];
+      t.stride = 1; t.pad = -dr[rh]; t.P = Hp; t.Q = Wp;
+      const int lw = dr[rw], lh = dr[rh];
+      // window starts lower = dmin; base positions per row = Q_in + upper − lower = Wp
+      const int corners[4] = {lw, lh, Wp - g.Q + lw, Hp - g.P + lh};
+      if (!encode_im2col_4d(&p.ta[1], dy, t, 64, BM, corners)) {
+        if (wb) ctx().alloc.free(wb);
+        return false;
+      }
+      encode_2d(&p.ta[0], dy, BE_BF16, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, (uint64_t)g.K, 64, 1);
+      const int RSC = t.R * t.S * t.C;
+      encode_operand(&p.tb[0], wp + woff[rh * st + rw], BE_BF16, t.K, RSC, RSC, true, bn, 64);
+      p.use_im2col = 1;
+      p.M = t.N * t.P * t.Q; p.N = t.K; p.K = RSC;
+      p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
+      p.D = dx; p.ldd = g.C; p.d_f32 = 0; p.beta = beta;
+      p.x = reinterpret_cast<const uint16_t*>(dy);
+      p.cN = t.N; p.cH = t.H; p.cW = t.W; p.cC = t.C; p.cR = t.R; p.cS = t.S;
+      p.cstride = 1; p.cpad = -lh; p.cpad_w_off = lh - lw; p.cP = t.P; p.cQ = t.Q;
+      p.ph_st = st; p.ph_h = rh; p.ph_w = rw; p.ph_H = g.H; p.ph_W = g.W;
+      ++nph;
+    }
+  if (zero_needed && beta == 0.f) conv_phase_zero(dx, g, cr, cs, s);
+  if (wtot) conv_phase_weights(w, wp, g, cr, dr, cs, ds, woff, s);
+  const double flops = 2.0 * g.N * (double)g.P * g.Q * g.K * g.R * g.S * g.C;
+  const double bytes = ((double)g.N * g.P * g.Q * g.K + (double)g.K * g.R * g.S * g.C + (double)g.N * g.H * g.W * g.C) * 2.0;
+  const int pidx = prof_begin("conv_tc_dgrad_phase", flops, bytes, g.N * g.H * g.W, g.C, g.R * g.S * g.K, s);
+  for (int i = 0; i < nph; ++i) {
+    if (bn == 256) launch_conv<256>(ps[i], s, nullptr);
+    else if (bn == 128) launch_conv<128>(ps[i], s, nullptr);
+    else launch_conv<64>(ps[i], s, nullptr);
+    g_tc_calls++;
+  }
+  prof_end(pidx, s);
+  after_launch("conv_tc_dgrad_phase");
+  if (wb) ctx().alloc.free(wb);
   return true;
 }
 

@@ -131,6 +131,15 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
                    float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr);
 // bf16 wf[C,R,S,K] = w[K,R−1−r,S−1−s,C] (dgrad of a stride-1 conv as a convolution)
 void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s);
+// stride-2+ dgrad by phases (gemm_sm100.cu conv_dgrad_phases; false = not applicable)
+bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& g, float beta, cudaStream_t s);
+// the phase convolutions' weights: tap (r, s) of w[K, R, S, C] (bf16) goes to phase
+// (ρh, ρw) = ((r − pad) mod st, (s − pad) mod st) at [c, t_r, t_s, k] of the block
+// at woff[ρh·st + ρw], t = (ρ + pad − r)/st − dmin[ρ]
+void conv_phase_weights(const void* w, uint16_t* wp, const ConvGeom& g, const int* cr, const int* dr, const int* cs,
+                        const int* ds, const int64_t* woff, cudaStream_t s);
+// zero the dx pixels of phases without taps (cr[ρh] == 0 or cs[ρw] == 0)
+void conv_phase_zero(void* dx, const ConvGeom& g, const int* cr, const int* cs, cudaStream_t s);
 // cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC
 void im2col(const void* x, void* cols, int64_t ldc, const ConvGeom& g, be_dtype dt, cudaStream_t s);
 // dx NHWC (+)= col2im(dcols)   (gather formulation, deterministic)

@@ -133,6 +133,11 @@ static void vjp_conv(Node* n, GradSink& sink) {
         return;
       }
     }
+    // stride ≥ 2: st² stride-1 phase convolutions stored straight into dx
+    if (g.stride >= 2 && opd == BE_BF16 && k::conv_dgrad_phases(dz->data(), w->data(), dx->data(), g, bx, s)) {
+      sink.commit(0);
+      return;
+    }
     k::GemmDesc gd;
     gd.M = (int)M; gd.N = (int)RSC; gd.K = (int)K;
     gd.A = dz->data(); gd.lda = K; gd.a_kmajor = true;

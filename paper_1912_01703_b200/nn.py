@@ -275,6 +275,11 @@ class ResNet50(Model):
         h = T.maxpool2d(h, 3, 2, 1)
         fuse = self.fuse_bn_conv and x.dtype == T.L.BE_BF16 and not self.bn_stats
         for (n, cin, mid, cout, stride, down) in self.blocks():
+            # the projection shortcut first: the engine runs the later-recorded
+            # c1 branch's backward first, so c1's dgrad writes dL/dh in full
+            # (beta 0) and the stride-2 projection's phase dgrad only adds into
+            # its one live phase (no zero fill of the other three)
+            idn = bn(conv(h, n + ".ds.w", stride, 0), n + ".dsbn", 0) if down else h
             t = bn(conv(h, n + ".c1.w", 1, 0), n + ".bn1", 1)
             t = conv(t, n + ".c2.w", stride, 1)
             if fuse:  # c3(relu(bn2(t))) — the bn2 output is only ever built in c3's operand tiles
@@ -282,7 +287,6 @@ class ResNet50(Model):
                                  P[n + ".c3.w"], act=1)
             else:
                 u = conv(bn(t, n + ".bn2", 1), n + ".c3.w", 1, 0)
-            idn = bn(conv(h, n + ".ds.w", stride, 0), n + ".dsbn", 0) if down else h
             # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN)
             h = bn(u, n + ".bn3", 1, residual=idn)
         h = T.avgpool_global(h)

@@ -186,6 +186,54 @@ def test_conv_stride2_dgrad_accumulates(R, pd, H):
     assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-2
 
 
+@pytest.mark.parametrize("cfg", [
+    # (N, C, H, W, K, R, stride, pad): ResNet-50 v1.5 stride-2 3×3 (layers 2-4) and 1×1 projections
+    (2, 128, 56, 56, 128, 3, 2, 1), (2, 256, 28, 28, 256, 3, 2, 1), (4, 512, 14, 14, 512, 3, 2, 1),
+    (2, 256, 56, 56, 512, 1, 2, 0), (2, 1024, 14, 14, 2048, 1, 2, 0),
+    # odd sizes (phases of unequal height), pad 0 and 2, 5×5, stride 3 (nine phases, some empty)
+    (1, 96, 15, 13, 64, 3, 2, 1), (2, 64, 17, 17, 128, 3, 2, 0), (1, 48, 19, 16, 192, 5, 2, 2),
+    (1, 64, 20, 22, 64, 3, 3, 1), (2, 32, 9, 9, 64, 2, 3, 0)])
+@pytest.mark.parametrize("first", [True, False])
+def test_conv_dgrad_phases(cfg, first):
+    """Stride ≥ 2 data gradient as stride² phase convolutions (conv_dgrad_phases):
+    every phase's implicit GEMM stores its rows straight into dx.  `first`:
+    the stride-2 conv's backward runs first (beta 0: phases without taps are
+    zero-filled) or after a 1×1 consumer of the same input (beta 1: its live
+    phases accumulate, the rest keep the other consumer's gradient).  Against
+    the float64 oracle on the same bf16 inputs: fp32 accumulate, one bf16
+    rounding of each stored gradient (≤ 2^-8 relative) → 1e-2."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(a.astype(np.float32)))
+    N, C, H, W, K, R, st, pd = cfg
+    rng = np.random.default_rng(sum(cfg) + first)
+    x = q(rng.standard_normal((N, C, H, W)))
+    w1 = q(rng.standard_normal((64, C, 1, 1)) / np.sqrt(C))
+    w2 = q(rng.standard_normal((K, C, R, R)) / np.sqrt(C * R * R))
+    xo = Var(x.astype(np.float64), True)
+    y1 = oops.conv2d(xo, Var(w1.astype(np.float64)), None, 1, 0)
+    y2 = oops.conv2d(xo, Var(w2.astype(np.float64)), None, st, pd)
+    g1 = q(rng.standard_normal(y1.value.shape))
+    g2 = q(rng.standard_normal(y2.value.shape))
+    backward(y1, g1.astype(np.float64))
+    backward(y2, g2.astype(np.float64))
+    xd = be.tensor(nchw_to_nhwc(x), requires_grad=True)
+    xb = be.cast(xd, "bf16")
+    # the engine runs the later-recorded consumer's backward first
+    if first:
+        z1 = be.conv2d(xb, be.tensor(nchw_to_nhwc(w1)), None, 1, 0)
+        z2 = be.conv2d(xb, be.tensor(nchw_to_nhwc(w2)), None, st, pd)
+    else:
+        z2 = be.conv2d(xb, be.tensor(nchw_to_nhwc(w2)), None, st, pd)
+        z1 = be.conv2d(xb, be.tensor(nchw_to_nhwc(w1)), None, 1, 0)
+    l1 = be.sum(be.mul(z1, be.tensor(nchw_to_nhwc(g1), dtype="bf16")))
+    l2 = be.sum(be.mul(z2, be.tensor(nchw_to_nhwc(g2), dtype="bf16")))
+    loss = be.add(l1, l2) if first else be.add(l2, l1)
+    loss.backward()
+    assert rel(nhwc_to_nchw(xd.grad.numpy()), xo.grad) < 1e-2
+
+
 @pytest.mark.parametrize("C", [5, 16])
 @pytest.mark.parametrize("k,s,p", [(3, 2, 0), (3, 2, 1)])
 def test_maxpool_op_and_argmax_bit_exact(k, s, p, C):
