@@ -65,7 +65,7 @@ def make_model(cfg, be, seed=0):
     elif cfg["net"] == "alexnet":
         m = be.nn.AlexNet()
     elif cfg["net"] == "resnet50":
-        m = be.nn.ResNet50(bn_stats=os.environ.get("BENCH_BN_STATS") == "1")
+        m = be.nn.ResNet50(bn_stats=os.environ.get("BENCH_BN_STATS", "1") == "1")
     elif cfg["net"] == "vgg19":
         m = be.nn.VGG19()
     elif cfg["net"] == "mobilenetv2":

@@ -348,9 +348,36 @@ __device__ __forceinline__ void epi_sgd16(const GemmParams& p, uint8_t* buf, int
 // Each warp owns a 4 KB staging area: two 2 KB buffers alternating for bf16
 // (the store issued from a buffer two chunks earlier must have read it), one
 // 4 KB buffer for fp32.
+// Column Σ / Σx² of a bf16 32 × 32 chunk staged in the SW64 layout (the
+// stored values; rows ≥ nvalid count 0): lane l reads the 2-column pair
+// (l & 15) of rows 2k + (l >> 4) as one 32-bit word (16 conflict-free LDS per
+// chunk instead of a 31-step shuffle transpose per sum), the two row parities
+// are combined, then lane l takes column l's sums.
+__device__ __forceinline__ void colstats_staged(const uint8_t* buf, int lane, int nvalid, float* stq) {
+  const int half = lane >> 4, cp = lane & 15;
+  float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int row = 2 * k + half;
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(buf + row * 64 + (((cp >> 2) ^ ((row >> 1) & 3)) << 4) +
+                                                          (cp & 3) * 4);
+    const float lo = row < nvalid ? __uint_as_float(w << 16) : 0.f;
+    const float hi = row < nvalid ? __uint_as_float(w & 0xffff0000u) : 0.f;
+    s0 += lo; q0 = fmaf(lo, lo, q0);
+    s1 += hi; q1 = fmaf(hi, hi, q1);
+  }
+  s0 += __shfl_xor_sync(0xffffffffu, s0, 16); s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  q0 += __shfl_xor_sync(0xffffffffu, q0, 16); q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
+  const float a0 = __shfl_sync(0xffffffffu, s0, lane >> 1), a1 = __shfl_sync(0xffffffffu, s1, lane >> 1);
+  const float b0 = __shfl_sync(0xffffffffu, q0, lane >> 1), b1 = __shfl_sync(0xffffffffu, q1, lane >> 1);
+  stq[0] = (lane & 1) ? a1 : a0;
+  stq[1] = (lane & 1) ? b1 : b0;
+}
+
 template <int NSLOT = 2>
 __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf, int& slot, int lane, int store_row,
-                                          int col0, const uint32_t (&r)[32], int z = -1) {
+                                          int col0, const uint32_t (&r)[32], int z = -1, float* stq = nullptr,
+                                          int nvalid = 32) {
   static_assert(NSLOT == 2 || NSLOT == 4, "staging slots");
   uint8_t* buf = warp_buf;
   if (p.d_f32) {  // 4-KB fp32 chunks: NSLOT / 2 buffers
@@ -398,6 +425,7 @@ __device__ __forceinline__ void epi_tma32(const GemmParams& p, uint8_t* warp_buf
   }
   sm100::fence_proxy_async();
   __syncwarp();
+  if (stq) colstats_staged(buf, lane, nvalid, stq);  // bf16 staging only (callers check d_f32)
   if (lane == 0) {
     if (z >= 0) {  // 3-D map (col, row, z)
       if (p.tma_store == 2) sm100::tma_reduce_add_3d(&p.td, buf, col0, store_row, z);
@@ -792,7 +820,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.stats) {  // batch-norm statistics of the stored values
+        const bool sfast = p.tma_store && !p.d_f32;  // statistics from the bf16 staging buffer
+        if (p.stats && !sfast) {  // batch-norm statistics of the stored values
           float s_, q_;
           colstats32(p, r0, row_ok, lane, s_, q_);
           cst.s[2 * it] += s_; cst.q[2 * it] += q_;
@@ -802,8 +831,14 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           }
         }
         if (p.tma_store) {
-          epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col0, r0);
-          if (h1) epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col1, r1);
+          float sq[2];
+          const int nv = p.M - (row - lane);
+          epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col0, r0, -1, sfast ? sq : nullptr, nv);
+          if (sfast) { cst.s[2 * it] += sq[0]; cst.q[2 * it] += sq[1]; }
+          if (h1) {
+            epi_tma32<NSLOT>(p, epi_smem + ew * (NSLOT * 2048), slot, lane, store_row, col1, r1, -1, sfast ? sq : nullptr, nv);
+            if (sfast) { cst.s[2 * it + 1] += sq[0]; cst.q[2 * it + 1] += sq[1]; }
+          }
         } else if (row_ok) {
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
@@ -1013,7 +1048,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.stats) {  // batch-norm statistics of the stored values
+        const bool sfast = p.tma_store && !p.d_f32;  // statistics from the bf16 staging buffer
+        if (p.stats && !sfast) {  // batch-norm statistics of the stored values
           float s_, q_;
           colstats32(p, r0, row_ok, lane, s_, q_);
           cst.s[2 * it] += s_; cst.q[2 * it] += q_;
@@ -1023,8 +1059,14 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           }
         }
         if (p.tma_store) {
-          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
-          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1);
+          float sq[2];
+          const int nv = p.M - (row - lane);
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0, -1, sfast ? sq : nullptr, nv);
+          if (sfast) { cst.s[2 * it] += sq[0]; cst.q[2 * it] += sq[1]; }
+          if (h1) {
+            epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col1, r1, -1, sfast ? sq : nullptr, nv);
+            if (sfast) { cst.s[2 * it + 1] += sq[0]; cst.q[2 * it + 1] += sq[1]; }
+          }
         } else if (row_ok) {
           epi_store32(p, Dbase, vec_ok, row, col0, r0);
           if (h1) epi_store32(p, Dbase, vec_ok, row, col1, r1);
@@ -1244,7 +1286,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.stats) {  // batch-norm statistics of the stored values
+        const bool sfast = p.tma_store && !p.d_f32;  // statistics from the bf16 staging buffer
+        if (p.stats && !sfast) {  // batch-norm statistics of the stored values
           float s_, q_;
           colstats32(p, r0, row_ok, lane, s_, q_);
           cst.s[2 * it] += s_; cst.q[2 * it] += q_;
@@ -1254,8 +1297,14 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           }
         }
         if (p.tma_store) {
-          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
-          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+          float sq[2];
+          const int nv = p.M - (row - lane);
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0, -1, sfast ? sq : nullptr, nv);
+          if (sfast) { cst.s[2 * it] += sq[0]; cst.q[2 * it] += sq[1]; }
+          if (h1) {
+            epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1, -1, sfast ? sq : nullptr, nv);
+            if (sfast) { cst.s[2 * it + 1] += sq[0]; cst.q[2 * it + 1] += sq[1]; }
+          }
         } else if (row_ok) {
           epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
           if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
@@ -1492,7 +1541,8 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.stats) {  // batch-norm statistics of the stored values
+        const bool sfast = p.tma_store && !p.d_f32;  // statistics from the bf16 staging buffer
+        if (p.stats && !sfast) {  // batch-norm statistics of the stored values
           float s_, q_;
           colstats32(p, r0, row_ok, lane, s_, q_);
           cst.s[2 * it] += s_; cst.q[2 * it] += q_;
@@ -1502,8 +1552,14 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
           }
         }
         if (p.tma_store) {
-          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
-          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
+          float sq[2];
+          const int nv = p.M - (row - lane);
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0, -1, sfast ? sq : nullptr, nv);
+          if (sfast) { cst.s[2 * it] += sq[0]; cst.q[2 * it] += sq[1]; }
+          if (h1) {
+            epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1, -1, sfast ? sq : nullptr, nv);
+            if (sfast) { cst.s[2 * it + 1] += sq[0]; cst.q[2 * it + 1] += sq[1]; }
+          }
         } else if (row_ok) {
           epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col0, r0);
           if (h1) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, row, col1, r1);
@@ -1732,14 +1788,19 @@ __global__ void __launch_bounds__(stem::kThreads, 1) conv_stem_kernel(const __gr
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (p.stats) {
+      const bool sfast = p.stats && p.tma_store && !p.d_f32;  // statistics from the bf16 staging buffer
+      if (p.stats && !sfast) {
         float s_, q_;
         colstats32(p, r0, row_ok, lane, s_, q_);
         cst.s[0] += s_; cst.q[0] += q_;
       }
       // TMA store of the warp's 32 × 32 box at (k = eh·32, q = eq·32, tile t):
       // full 128-B lines, rows q ≥ Q clipped by the map
-      if (p.tma_store) epi_tma32(p, epi_smem + ew * 4096, slot, lane, eq * 32, eh * 32, r0, t);
+      if (p.tma_store) {
+        float sq[2];
+        epi_tma32(p, epi_smem + ew * 4096, slot, lane, eq * 32, eh * 32, r0, t, sfast ? sq : nullptr, p.cQ - eq * 32);
+        if (sfast) { cst.s[0] += sq[0]; cst.q[0] += sq[1]; }
+      }
       else if (row_ok) epi_store32(p, reinterpret_cast<char*>(p.D), vec_ok, t * p.cQ + qrow, eh * 32, r0);
     }
     if (p.stats) cst.flush(p, blockIdx.x * 4 + eq, eh * 32, lane, 1);
@@ -2041,6 +2102,8 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
     const int ew = warp - 4, eq = warp & 3, eh = ew >> 2;
     const int dp = (eq * 32) / Wp, q0 = (eq * 32) % Wp;
     int slot = 0, ti = 0;
+    ColStats<1> cst;  // BN statistics of the stored bf16 values (p.stats; host: bf16 output only)
+    cst.reset();
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++ti) {
       const int acc = ti & 1;
       const int n = t / pg, p0 = (t - n * pg) * G;
@@ -2052,9 +2115,14 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
-      if (p0 + dp < p.cP && q0 < p.cQ)
-        epi_tma32(p, epi_smem + ew * 4096, slot, lane, q0, eh * 32, r, n * p.cP + p0 + dp);
+      if (p0 + dp < p.cP && q0 < p.cQ) {
+        float sq[2];
+        epi_tma32(p, epi_smem + ew * 4096, slot, lane, q0, eh * 32, r, n * p.cP + p0 + dp, p.stats ? sq : nullptr,
+                  p.cQ - q0);
+        if (p.stats) { cst.s[0] += sq[0]; cst.q[0] += sq[1]; }
+      }
     }
+    if (p.stats) cst.flush(p, blockIdx.x * 4 + eq, eh * 32, lane, 1);
     if (lane == 0) sm100::bulk_wait<0>();
   }
   sm100::tc_fence_before();
@@ -3458,7 +3526,8 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
 // stride-1 conv from a shared input patch (conv_fwd_patch_kernel): C = K = 64,
 // ≤ 9 taps, W' = pow2 ≥ Q + S − 1 in [32, 128]; false when not applicable
 static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
-                           int act, float beta, cudaStream_t s) {
+                           int act, float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr) {
+  if (stats && (yd != BE_BF16 || bias || act || beta != 0.f)) return false;
   static const int on = [] { const char* e = getenv("BE_CONV_PATCH"); return e ? atoi(e) : 1; }();
   if (!on || g.stride != 1 || g.C != 64 || g.K != 64 || g.R * g.S > 9 || (beta != 0.f && beta != 1.f)) return false;
   int Wp = 32;
@@ -3504,6 +3573,8 @@ static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom
   }
   const int tiles = g.N * ((g.P + G - 1) / G);
   const int grid = std::min(tiles, ctx().num_sms);
+  p.stats = stats;
+  if (stats && stats_parts) *stats_parts = grid * 4;
   const double flops = 2.0 * p.M * (double)g.K * RSC;
   const double bytes = ((double)g.N * g.H * g.W * g.C + (double)g.K * RSC) * 2.0 + (double)p.M * g.K * (f32 ? 4 : 2);
   const int pidx = prof_begin("conv_tc_patch", flops, bytes, p.M, g.K, RSC, s);
@@ -3589,7 +3660,7 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   }
   if (g.K % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
-  if (!stats && conv_fwd_patch(x, w, y, g, yd, bias, act, beta, s)) return true;
+  if (conv_fwd_patch(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts)) return true;
   const char* e = getenv("BE_CONV_IMPLICIT");
   if (e && e[0] == '0') return false;
   GemmParams p;

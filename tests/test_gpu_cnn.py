@@ -394,7 +394,12 @@ def test_ncf_small_fp32():
                                  (2, 256, 16, 16, 160, 1, 2, 0),   # 1×1 s2: implicit conv, 2 column tiles
                                  (2, 8, 40, 40, 64, 7, 2, 3),      # conv1 small-C kernel
                                  (2, 512, 32, 32, 256, 1, 1, 0),   # pair-sized GEMM
-                                 (2, 64, 14, 14, 256, 1, 1, 0)])   # K-light expansion: statistics pass kept
+                                 (2, 64, 14, 14, 256, 1, 1, 0),    # K-light expansion: statistics pass kept
+                                 (2, 64, 30, 30, 64, 3, 1, 1),     # shared-patch kernel (C = K = 64), ragged rows
+                                 (2, 64, 56, 56, 64, 3, 1, 1),     # ResNet layer-1 3×3 (shared patch)
+                                 (2, 128, 28, 28, 128, 3, 1, 1),   # ResNet layer-2 3×3 (TMA im2col)
+                                 (1, 8, 224, 224, 64, 7, 2, 3),    # ResNet stem (phase-split patch kernel)
+                                 (3, 256, 14, 14, 64, 1, 1, 0)])   # bottleneck c1: 1×1 reduce, ragged M
 def test_bn_statistics_from_conv_epilogue(cfg):
     """conv2d(..., bn_stats=True) → batchnorm2d: the BN takes its mean /
     variance from the conv epilogue's per-column partial sums of the stored

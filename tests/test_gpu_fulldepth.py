@@ -31,7 +31,7 @@ def _case(name, dtype):
         seed = 27
         x = inp(synth.normal((2, 3, 224, 224), seed, 1))
         y = synth.labels(2, 1000, seed)
-        return (onets.ResNet50(), be.nn.ResNet50(fuse_bn_conv=True), (x, y),
+        return (onets.ResNet50(), be.nn.ResNet50(bn_stats=False, fuse_bn_conv=True), (x, y),
                 lambda: (be.nn.images_to_device(x, dtype), be.tensor(y)), seed)
     if name == "resnet50":
         seed = 21
