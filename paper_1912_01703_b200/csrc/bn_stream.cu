@@ -64,9 +64,12 @@ struct Ring {
 // v[NS]) runs for each (row, 8-channel group) of this thread.  Returns after the
 // last chunk (consumers) / last copy (producer); callers __syncthreads() before
 // reusing the ring.
-template <int NS, int ITERS, int NST, typename Body>
+struct NoPre {
+  __device__ __forceinline__ void operator()(int64_t) const {}
+};
+template <int NS, int ITERS, int NST, typename Body, typename Pre = NoPre>
 __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], int64_t r0, int64_t r1, int C,
-                                            uint8_t* ring, Body&& body, int64_t ld = 0) {
+                                            uint8_t* ring, Body&& body, int64_t ld = 0, Pre&& pre = Pre{}) {
   // ld (row stride, elements) > C: a column group of a wider tensor — one
   // bulk copy per row instead of one per chunk
   if (ld == 0) ld = C;
@@ -110,6 +113,7 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
   const bool active = rin < rpi;
   for (int64_t i = 0; i < nchunks; ++i) {
     const int st = (int)(i % NST);
+    pre(i);  // consumer-side loads for chunk i (+1) issued before waiting on the ring
     sm100::mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
     const int64_t rs = r0 + i * crow;
 #pragma unroll
@@ -130,7 +134,8 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
 
 // fixed-order per-block combine of the consumers' per-row-slot sums → partial row blockIdx.x
 __device__ __forceinline__ void combine_partials(const float (&s0)[8], const float (&s1)[8], int C, float* sm,
-                                                 float* part0, float* part1, int Ctot = 0, int col0 = 0) {
+                                                 float* part0, float* part1, int Ctot = 0, int col0 = 0,
+                                                 const float* __restrict__ scale1 = nullptr) {
   if (Ctot == 0) Ctot = C;
   const int t = threadIdx.x, lanes = C >> 3, rpi = kCons / lanes;
   if (t < rpi * lanes) {
@@ -143,7 +148,7 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
     float a0 = 0.f, a1 = 0.f;
     for (int w = 0; w < rpi; ++w) { a0 += sm[w * C + i]; a1 += sm[kCons * 8 + w * C + i]; }
     part0[(int64_t)blockIdx.x * Ctot + col0 + i] = a0;
-    part1[(int64_t)blockIdx.x * Ctot + col0 + i] = a1;
+    part1[(int64_t)blockIdx.x * Ctot + col0 + i] = scale1 ? a1 * scale1[col0 + i] : a1;
   }
 }
 
@@ -270,13 +275,19 @@ __global__ void __launch_bounds__(kThr, 3) bn_stats_stream_kernel(const uint16_t
 }
 
 // backward reduction Σg', Σg'·x̂ (g' = gy masked by act(γx̂+β) > 0 recomputed
-// from x when act; with rmask: g = gy·1[rmask > 0] written to gout first)
+// from x when ACT; with rmask: g = gy·1[rmask > 0] written to gout first)
 // MASK 1: the residual mask read from the stored block output (bf16 y > 0);
 // MASK 2: read from the forward's 1-bit mask (bit j of byte row·C/8 + c/8 =
-// channel c + j passed the ReLU) — 1/16 of the bytes of y
-template <int MASK>
+// channel c + j passed the ReLU) — 1/16 of the bytes of y; the mask bytes of
+// chunk i + 1 are loaded while chunk i is consumed (a dependent global load
+// per row otherwise stalls every consumer warp on DRAM latency).
+// Σg'·(x − μ) is accumulated per thread and scaled by invstd once per column
+// when the block's partial row is written (registers: the residual variants
+// spilled with the per-thread invstd copy).  ACT is a template parameter so
+// the residual variants (ACT 0) carry no ReLU-recompute constants.
+template <int MASK, int ACT>
 __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_t* __restrict__ x,
-                                                                const uint16_t* __restrict__ gy, int act,
+                                                                const uint16_t* __restrict__ gy,
                                                                 int64_t rows, int C, const float* __restrict__ mean,
                                                                 const float* __restrict__ invstd, float* part0,
                                                                 float* part1, int64_t rps,
@@ -290,21 +301,45 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
-  float k[8], is[8], sc[8], sh[8], s0[8] = {}, s1[8] = {};
+  float k[8], sc[8], sh[8], s0[8] = {}, s1[8] = {};
   if (threadIdx.x < kCons) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      k[j] = mean[c + j]; is[j] = invstd[c + j];
-      sc[j] = act ? gam[c + j] * is[j] : 0.f;
-      sh[j] = act ? bsh[c + j] - k[j] * sc[j] : 0.f;
+      k[j] = mean[c + j];
+      if (ACT) {
+        sc[j] = gam[c + j] * invstd[c + j];
+        sh[j] = bsh[c + j] - k[j] * sc[j];
+      }
     }
   }
+  // MASK 2: this thread's mask bytes for the rows of the current / next chunk
+  constexpr int IT = 2;  // ITERS of the ring below
+  const int lanes = C >> 3, rpi = kCons / lanes, rin = threadIdx.x / lanes;
+  const int64_t crow = (int64_t)IT * rpi;
+  uint32_t bcur[IT], bnext[IT];
+  int64_t cb = r0;  // first row of the chunk being consumed
+  auto load_bits = [&](int64_t i, uint32_t (&b)[IT]) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int64_t row = r0 + i * crow + it * rpi + rin;
+      b[it] = (rin < rpi && row < r1) ? (uint32_t)__ldg(rbits + row * (C >> 3) + (c >> 3)) : 0u;
+    }
+  };
+  if (MASK == 2) load_bits(0, bnext);
+  auto pre = [&](int64_t i) {
+    if (MASK == 2) {
+#pragma unroll
+      for (int it = 0; it < IT; ++it) bcur[it] = bnext[it];
+      load_bits(i + 1, bnext);
+      cb = r0 + i * crow;
+    }
+  };
   auto body = [&](int64_t row, const uint4* v) {
     float a[8], g[8];
     unpack8s(v[0], a);
     uint4 gv = v[1];
     if (MASK == 2) {
-      const uint32_t b = rbits[row * (C >> 3) + (c >> 3)];
+      const uint32_t b = (int)(row - cb - rin) >= rpi ? bcur[1] : bcur[0];
       uint32_t ow[4];
       const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
@@ -329,22 +364,22 @@ __global__ void __launch_bounds__(kThr, 3) bn_reduce_stream_kernel(const uint16_
       *reinterpret_cast<uint4*>(gout + row * C + c) = gv;
     }
     unpack8s(gv, g);
-    if (act) {
+    if (ACT) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), ACT, true) ? g[j] : 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] += g[j] * (a[j] - k[j]) * is[j]; }
+    for (int j = 0; j < 8; ++j) { s0[j] += g[j]; s1[j] = fmaf(g[j], a[j] - k[j], s1[j]); }
   };
   if (MASK == 1) {
     const uint16_t* src[3] = {x, gy, rmask};
     stream_rows<3, 2, 3>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[3]) { body(row, v); });
   } else {
     const uint16_t* src[2] = {x, gy};
-    stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) { body(row, v); });
+    stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) { body(row, v); }, 0, pre);
   }
   __syncthreads();
-  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1);
+  combine_partials(s0, s1, C, reinterpret_cast<float*>(ring), part0, part1, 0, 0, invstd);
   if (fin.mode) fold_finalize(fin, part0, part1, C, ring);
 }
 
@@ -406,10 +441,10 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
   }
 }
 
-// dx (+)= k1·g' + k2·x + k3
-template <bool ACC>
+// dx (+)= k1·g' + k2·x + k3 (ACT: the ReLU / ReLU6 mask recomputed from x)
+template <bool ACC, int ACT>
 __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* __restrict__ gy,
-                                                            const uint16_t* __restrict__ x, int act, uint16_t* dx,
+                                                            const uint16_t* __restrict__ x, uint16_t* dx,
                                                             int64_t rows, int C, const float* __restrict__ mean,
                                                             const float* __restrict__ invstd,
                                                             const float* __restrict__ gamma,
@@ -426,7 +461,7 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
     for (int j = 0; j < 8; ++j) {
       const float is = invstd[c + j], a = gamma[c + j] * is;
       sc[j] = a;
-      sh[j] = act ? bsh[c + j] - mean[c + j] * a : 0.f;
+      sh[j] = ACT ? bsh[c + j] - mean[c + j] * a : 0.f;
       const float m1 = sums[c + j] * inv_n, m2 = sums[C + c + j] * inv_n;
       k1[j] = a;
       k2[j] = -a * m2 * is;
@@ -437,9 +472,9 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
     float g[8], a[8], o[8];
     unpack8s(v[0], g);
     unpack8s(v[1], a);
-    if (act) {
+    if (ACT) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), act, true) ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = act_pass_st(fmaf(a[j], sc[j], sh[j]), ACT, true) ? g[j] : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = fmaf(k1[j], g[j], fmaf(k2[j], a[j], k3[j]));
@@ -602,12 +637,15 @@ bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
                       const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
                       const uint8_t* rbits, float* sums, float* dgamma, float* dbeta, float gb_beta) {
   static bool once = [] {
-    set_smem(bn_reduce_stream_kernel<0>, kS2);
-    set_smem(bn_reduce_stream_kernel<1>, kS3);
-    set_smem(bn_reduce_stream_kernel<2>, kS2);
+    set_smem(bn_reduce_stream_kernel<0, 0>, kS2);
+    set_smem(bn_reduce_stream_kernel<0, 1>, kS2);
+    set_smem(bn_reduce_stream_kernel<0, 2>, kS2);
+    set_smem(bn_reduce_stream_kernel<1, 0>, kS3);
+    set_smem(bn_reduce_stream_kernel<2, 0>, kS2);
     return true;
   }();
   (void)once;
+  BE_REQUIRE(act >= 0 && act <= 2 && (act == 0 || (!rbits && !rmask)), BE_E_ARG, "bn_reduce_stream: activation");
   const int64_t rps = (rows + sp - 1) / sp;
   BnFin fin;
   if (fold_on() && sums) {
@@ -615,15 +653,15 @@ bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
     fin.mode = 2;
     fin.sums = sums; fin.dgamma = dgamma; fin.dbeta = dbeta; fin.gb_beta = gb_beta;
   }
-  if (rbits)
-    launch_pdl(bn_reduce_stream_kernel<2>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, (const uint16_t*)nullptr, gout, rbits, fin);
-  else if (rmask)
-    launch_pdl(bn_reduce_stream_kernel<1>, (unsigned)sp, kThr, kS3, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, rmask, gout, (const uint8_t*)nullptr, fin);
-  else
-    launch_pdl(bn_reduce_stream_kernel<0>, (unsigned)sp, kThr, kS2, s, x, gy, act, rows, C, mean, invstd, part0, part1,
-               rps, gam, bsh, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr, fin);
+  auto go = [&](auto kern, int smem, const uint16_t* rm, uint16_t* go_, const uint8_t* rb) {
+    launch_pdl(kern, (unsigned)sp, kThr, smem, s, x, gy, rows, C, mean, invstd, part0, part1, rps, gam, bsh, rm, go_,
+               rb, fin);
+  };
+  if (rbits) go(bn_reduce_stream_kernel<2, 0>, kS2, (const uint16_t*)nullptr, gout, rbits);
+  else if (rmask) go(bn_reduce_stream_kernel<1, 0>, kS3, rmask, gout, (const uint8_t*)nullptr);
+  else if (act == 1) go(bn_reduce_stream_kernel<0, 1>, kS2, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr);
+  else if (act == 2) go(bn_reduce_stream_kernel<0, 2>, kS2, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr);
+  else go(bn_reduce_stream_kernel<0, 0>, kS2, (const uint16_t*)nullptr, (uint16_t*)nullptr, (const uint8_t*)nullptr);
   after_launch("bn_reduce_stream");
   return fin.mode != 0;
 }
@@ -652,19 +690,30 @@ void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, 
                   const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
                   const float* bsh, cudaStream_t s) {
   static bool once = [] {
-    set_smem(bn_dx_stream_kernel<false>, kS2);
-    set_smem(bn_dx_stream_kernel<true>, kS3);
+    set_smem(bn_dx_stream_kernel<false, 0>, kS2);
+    set_smem(bn_dx_stream_kernel<false, 1>, kS2);
+    set_smem(bn_dx_stream_kernel<false, 2>, kS2);
+    set_smem(bn_dx_stream_kernel<true, 0>, kS3);
+    set_smem(bn_dx_stream_kernel<true, 1>, kS3);
+    set_smem(bn_dx_stream_kernel<true, 2>, kS3);
     return true;
   }();
   (void)once;
+  BE_REQUIRE(act >= 0 && act <= 2, BE_E_ARG, "bn_dx_stream: activation");
   const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
   const int64_t rps = (rows + sp - 1) / sp;
-  if (dx_beta != 0.f)
-    launch_pdl(bn_dx_stream_kernel<true>, (unsigned)sp, kThr, kS3, s, gy, x, act, dx, rows, C, mean, invstd, gamma, sums, rps,
-                                                              bsh);
-  else
-    launch_pdl(bn_dx_stream_kernel<false>, (unsigned)sp, kThr, kS2, s, gy, x, act, dx, rows, C, mean, invstd, gamma, sums,
-                                                               rps, bsh);
+  auto go = [&](auto kern, int smem) {
+    launch_pdl(kern, (unsigned)sp, kThr, smem, s, gy, x, dx, rows, C, mean, invstd, gamma, sums, rps, bsh);
+  };
+  if (dx_beta != 0.f) {
+    if (act == 1) go(bn_dx_stream_kernel<true, 1>, kS3);
+    else if (act == 2) go(bn_dx_stream_kernel<true, 2>, kS3);
+    else go(bn_dx_stream_kernel<true, 0>, kS3);
+  } else {
+    if (act == 1) go(bn_dx_stream_kernel<false, 1>, kS2);
+    else if (act == 2) go(bn_dx_stream_kernel<false, 2>, kS2);
+    else go(bn_dx_stream_kernel<false, 0>, kS2);
+  }
   after_launch("bn_dx_stream");
 }
 
