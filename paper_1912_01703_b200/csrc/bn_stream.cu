@@ -152,6 +152,19 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
   }
 }
 
+// PDL entry of a stream pass whose streamed inputs were NOT written by its
+// stream predecessor (early = 1: the apply after the statistics pass / its
+// finalize, the dx pass after the backward reduction): the producer warp reads
+// only those inputs and writes nothing, so it starts filling the ring without
+// griddepcontrol.wait — the copies overlap the predecessor's reduction tail;
+// consumers (which read the statistics / sums and write) wait as usual.  The
+// inputs' own producers completed before the predecessor passed its wait,
+// which is what launched this grid.
+__device__ __forceinline__ void pdl_entry_stream(int early) {
+  if (!(early && threadIdx.x >= kCons)) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace
 // Finalize folded into the statistics / reduction pass (replaces the separate
 // bn_finalize_v launch).  Every block writes its partial row, takes a ticket;
@@ -391,8 +404,8 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, int act, int64_t rps,
                                                                const uint16_t* __restrict__ res,
-                                                               uint8_t* __restrict__ mbits) {
-  pdl_entry();
+                                                               uint8_t* __restrict__ mbits, int early) {
+  pdl_entry_stream(early);
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -449,8 +462,8 @@ __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* _
                                                             const float* __restrict__ invstd,
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ sums, int64_t rps,
-                                                            const float* __restrict__ bsh) {
-  pdl_entry();
+                                                            const float* __restrict__ bsh, int early) {
+  pdl_entry_stream(early);
   extern __shared__ __align__(128) uint8_t ring[];
   const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
   const int c = (threadIdx.x % (C >> 3)) * 8;
@@ -668,7 +681,7 @@ bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
 
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
                      const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s,
-                     uint8_t* mbits) {
+                     uint8_t* mbits, int early) {
   static bool once = [] {
     set_smem(bn_apply_stream_kernel<false>, kS1);
     set_smem(bn_apply_stream_kernel<true>, kS2);
@@ -679,16 +692,16 @@ void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const 
   const int64_t rps = (rows + sp - 1) / sp;
   if (res)
     launch_pdl(bn_apply_stream_kernel<true>, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-               res, mbits);
+               res, mbits, early);
   else
     launch_pdl(bn_apply_stream_kernel<false>, (unsigned)sp, kThr, kS1, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-               (const uint16_t*)nullptr, mbits);
+               (const uint16_t*)nullptr, mbits, early);
   after_launch("bn_apply_stream");
 }
 
 void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,
                   const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
-                  const float* bsh, cudaStream_t s) {
+                  const float* bsh, cudaStream_t s, int early) {
   static bool once = [] {
     set_smem(bn_dx_stream_kernel<false, 0>, kS2);
     set_smem(bn_dx_stream_kernel<false, 1>, kS2);
@@ -703,7 +716,7 @@ void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, 
   const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
   const int64_t rps = (rows + sp - 1) / sp;
   auto go = [&](auto kern, int smem) {
-    launch_pdl(kern, (unsigned)sp, kThr, smem, s, gy, x, dx, rows, C, mean, invstd, gamma, sums, rps, bsh);
+    launch_pdl(kern, (unsigned)sp, kThr, smem, s, gy, x, dx, rows, C, mean, invstd, gamma, sums, rps, bsh, early);
   };
   if (dx_beta != 0.f) {
     if (act == 1) go(bn_dx_stream_kernel<true, 1>, kS3);

@@ -30,12 +30,15 @@ bool bn_reduce_stream(const uint16_t* x, const uint16_t* gy, int act, int64_t ro
                       const float* bsh, const uint16_t* rmask, uint16_t* gout, cudaStream_t s,
                       const uint8_t* rbits = nullptr, float* sums = nullptr, float* dgamma = nullptr,
                       float* dbeta = nullptr, float gb_beta = 0.f);
+// early = 1: x / res (apply) or gy / x (dx) were not written by the kernel
+// launched just before on s — the pass may start streaming them before its
+// PDL wait (bn_stream.cu pdl_entry_stream)
 void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
                      const float* gamma, const float* beta, int act, const uint16_t* res, cudaStream_t s,
-                     uint8_t* mbits = nullptr);
+                     uint8_t* mbits = nullptr, int early = 0);
 void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,
                   const float* mean, const float* invstd, const float* gamma, const float* sums, float dx_beta,
-                  const float* bsh, cudaStream_t s);
+                  const float* bsh, cudaStream_t s, int early = 0);
 
 namespace {
 int grid_for(int64_t n, int per = 1) {
@@ -1565,12 +1568,13 @@ bool bn_mask_bits_ok(const void* x, const void* y, const void* res, int64_t rows
   return dt == BE_BF16 && bn_stream_ok(x, rows, C) && aligned16(y) && (!res || aligned16(res));
 }
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
-              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res, uint8_t* mbits) {
+              const float* gamma, const float* beta, int act, cudaStream_t s, const void* res, uint8_t* mbits,
+              int early) {
   const int64_t total = rows * C;
   if (total == 0) return;
   if (dt == BE_BF16 && bn_stream_ok(x, rows, C) && aligned16(y) && (!res || aligned16(res))) {
     bn_apply_stream(reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint16_t*>(y), rows, C, mean, invstd, gamma,
-                    beta, act, reinterpret_cast<const uint16_t*>(res), s, mbits);
+                    beta, act, reinterpret_cast<const uint16_t*>(res), s, mbits, early);
     return;
   }
   if (bn_vec_ok(x, C) && aligned16(y) && (!res || aligned16(res))) {
@@ -1666,8 +1670,10 @@ void bn_bwd(const void* dy, const void* x, const void* y, int act, void* dx, int
       after_launch("bn_bwd_finalize_v");
     }
     if (dx && stream) {
+      // early: dy and x were written before the reduction just launched (which
+      // writes only partial rows / sums)
       bn_dx_stream(reinterpret_cast<const uint16_t*>(dy), reinterpret_cast<const uint16_t*>(x), act,
-                   reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, bn_beta, s);
+                   reinterpret_cast<uint16_t*>(dx), rows, C, mean, invstd, gamma, sums, dx_beta, bn_beta, s, 1);
     } else if (dx) {
       dim3 g2;
       const int64_t rpb = bn_rows_per_block(rows, C, &g2);

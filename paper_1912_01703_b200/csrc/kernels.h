@@ -155,7 +155,7 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
 // y = act(γ·(x − μ)·is + β [+ res])   (res: optional residual, same layout/dtype as x)
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
               const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr,
-              uint8_t* mbits = nullptr);
+              uint8_t* mbits = nullptr, int early = 0);
 // true when bn_apply can also write the 1-bit ReLU mask of its output (mbits:
 // rows·C/8 bytes, bit j of byte r·C/8 + c/8 ⇔ y[r, c + j] > 0) for bn_bwd's rbits
 bool bn_mask_bits_ok(const void* x, const void* y, const void* res, int64_t rows, int C, be_dtype dt);

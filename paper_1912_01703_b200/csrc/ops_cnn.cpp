@@ -389,7 +389,8 @@ static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* o
   if (res && a.act == 1 && want_grad && k::bn_mask_bits_ok(x->data(), y->data(), res->data(), rows, C, x->dtype))
     bits = new_tensor({rows * (C / 8)}, BE_U8);
   k::bn_apply(x->data(), y->data(), rows, C, x->dtype, mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(),
-              beta->ptr<float>(), a.act, s, res ? res->data() : nullptr, bits ? bits->ptr<uint8_t>() : nullptr);
+              beta->ptr<float>(), a.act, s, res ? res->data() : nullptr, bits ? bits->ptr<uint8_t>() : nullptr,
+              /*early: the statistics kernels just launched write neither x nor res*/ 1);
   Node* n = res ? new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta, res})
                 : new_node("batchnorm2d", BE_OP_BATCHNORM2D, vjp_bn, {x, gamma, beta});
   if (n) {
