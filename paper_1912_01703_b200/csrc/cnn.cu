@@ -1327,6 +1327,79 @@ __global__ void __launch_bounds__(256) maxpool_bwd_rows(const uint16_t* __restri
   }
   *reinterpret_cast<uint4*>(dx + o) = pack8(acc);
 }
+// ---- max-pool backward for the 3×3 / stride-2 / pad-1 pool (ResNet's), one
+// thread per 2×2 quad of input pixels h ∈ {2i−1, 2i}, w ∈ {2j−1, 2j}: the
+// quad's pixels are reached only by the windows (p, q) ∈ {i−1, i} × {j−1, j},
+// whose (dy, argmax) pairs are loaded once for all four pixels (the per-pixel
+// kernel loads ≤ 4 pairs per pixel and was issue-bound).  Each pixel sums
+// its winners in (p, q) order in fp32, exactly as maxpool_bwd_rows: bitwise
+// the same result.  Tap index of pixel (h, w) in window (p, q) = (h − 2p + 1)·3
+// + (w − 2q + 1).
+__global__ void __launch_bounds__(256) maxpool_bwd_quad(const uint16_t* __restrict__ dy,
+                                                        const uint8_t* __restrict__ am, uint16_t* __restrict__ dx,
+                                                        ConvGeom g, float beta) {
+  pdl_entry();
+  const int cv = threadIdx.x;
+  const int j = blockIdx.x * blockDim.y + threadIdx.y;
+  if (j > g.Q) return;
+  const int n = blockIdx.z, i = blockIdx.y;
+  const int64_t img = (int64_t)n * g.P * g.Q * g.C;
+  uint4 d[2][2];
+  uint2 pk[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int p = i - 1 + a, q = j - 1 + b;
+      d[a][b] = make_uint4(0u, 0u, 0u, 0u);
+      pk[a][b] = make_uint2(0xffffffffu, 0xffffffffu);
+      if (p >= 0 && p < g.P && q >= 0 && q < g.Q) {
+        const int64_t o = img + ((int64_t)p * g.Q + q) * g.C + cv * 8;
+        d[a][b] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+        pk[a][b] = __ldg(reinterpret_cast<const uint2*>(am + o));
+      }
+    }
+#pragma unroll
+  for (int dh = 0; dh < 2; ++dh) {
+    const int h = 2 * i - 1 + dh;
+    if (h < 0 || h >= g.H) continue;
+#pragma unroll
+    for (int dw = 0; dw < 2; ++dw) {
+      const int w = 2 * j - 1 + dw;
+      if (w < 0 || w >= g.W) continue;
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      // windows reaching (h, w): odd h (dh = 0) ← p = i − 1 (r = 2), p = i (r = 0);
+      // even h (dh = 1) ← p = i (r = 1); likewise w — in (p, q) order
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        if (dh == 1 && a == 0) continue;
+        const int r = dh == 1 ? 1 : (a == 0 ? 2 : 0);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          if (dw == 1 && b == 0) continue;
+          const int u = dw == 1 ? 1 : (b == 0 ? 2 : 0);
+          const uint32_t tap = (uint32_t)(r * 3 + u) * 0x01010101u;
+          const uint32_t m0 = __vcmpeq4(pk[a][b].x, tap), m1 = __vcmpeq4(pk[a][b].y, tap);
+          uint4 v = d[a][b];
+          v.x &= __byte_perm(m0, 0, 0x1100); v.y &= __byte_perm(m0, 0, 0x3322);
+          v.z &= __byte_perm(m1, 0, 0x1100); v.w &= __byte_perm(m1, 0, 0x3322);
+          float f[8];
+          unpack8(v, f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] += f[k];
+        }
+      }
+      const int64_t o = (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * 8;
+      if (beta != 0.f) {
+        float old[8];
+        unpack8(*reinterpret_cast<const uint4*>(dx + o), old);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += old[k];
+      }
+      *reinterpret_cast<uint4*>(dx + o) = pack8(acc);
+    }
+  }
+}
 }  // namespace
 
 template <typename T, int VEC>
@@ -1455,6 +1528,15 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
       (int64_t)g.P * g.Q * g.C < (1LL << 32) &&
       aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
+    static const int quad_on = [] { const char* e = getenv("BE_MAXPOOL_QUAD"); return e ? atoi(e) : 1; }();
+    if (quad_on && g.R == 3 && g.S == 3 && g.stride == 2 && g.pad == 1 && (g.H + 1) / 2 <= g.P + 1 &&
+        (g.W + 1) / 2 <= g.Q + 1) {
+      // quads i ∈ [0, P], j ∈ [0, Q] cover h ≤ 2P, w ≤ 2Q (⊇ [0, H) × [0, W))
+      dim3 gq((g.Q + 1 + wpb) / wpb, g.P + 1, g.N), bq(cvn, wpb);
+      launch_pdl(maxpool_bwd_quad, gq, bq, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+      after_launch("maxpool_bwd_quad");
+      return;
+    }
     dim3 grid((g.W + wpb - 1) / wpb, g.H, g.N), block(cvn, wpb);
     if (g.stride == 2) launch_pdl(maxpool_bwd_rows<2>, grid, block, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
     else launch_pdl(maxpool_bwd_rows<0>, grid, block, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
