@@ -387,44 +387,6 @@ __global__ void __launch_bounds__(256) maxpool_bwd_v(const void* __restrict__ dy
   }
 }
 
-// Transposed + spatially flipped weights for dgrad-as-convolution:
-// wf[c, r, s, k] = w[k, R−1−r, S−1−s, c]
-__global__ void flip_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ wf, int K, int R, int S,
-                                    int C, int64_t total) {
-  pdl_entry();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int k = (int)(t % K); t /= K;
-    const int s = (int)(t % S); t /= S;
-    const int r = (int)(t % R);
-    const int c = (int)(t / R);
-    wf[i] = w[(((int64_t)k * R + (R - 1 - r)) * S + (S - 1 - s)) * C + c];
-  }
-}
-
-// Phase-convolution weights (conv_dgrad_phases): source tap (r, s) of
-// w[K, R, S, C] belongs to phase (ρh, ρw) = ((r − pad) mod st, (s − pad) mod st)
-// and sits at [c, t_r, t_s, k] of that phase's block, t = (ρ + pad − r)/st − dmin[ρ]
-struct PhaseW {
-  int64_t off[16];
-  int cr[4], dr[4], cs[4], ds[4];
-};
-__global__ void phase_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ wp, int K, int R, int S,
-                                     int C, int st, int pad, PhaseW pw, int64_t total) {
-  pdl_entry();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int k = (int)(t % K); t /= K;
-    const int s = (int)(t % S); t /= S;
-    const int r = (int)(t % R);
-    const int c = (int)(t / R);
-    const int rh = ((r - pad) % st + st) % st, rw = ((s - pad) % st + st) % st;
-    const int tr = (rh + pad - r) / st - pw.dr[rh], ts = (rw + pad - s) / st - pw.ds[rw];
-    wp[pw.off[rh * st + rw] + (((int64_t)c * pw.cr[rh] + tr) * pw.cs[rw] + ts) * K + k] =
-        w[(((int64_t)k * R + r) * S + s) * C + c];
-  }
-}
-// zero dx pixels (n, h, w) of the phases without taps, 8 channels per item
 __global__ void phase_zero_kernel(uint16_t* __restrict__ dx, ConvGeom g, uint32_t live, int64_t total) {
   pdl_entry();
   const int CV = g.C / 8;
@@ -1452,25 +1414,6 @@ void col2im(const void* dcols, int64_t ldc, void* dx, const ConvGeom& g, be_dtyp
   else
     launch_pdl(col2im_kernel<float>, grid_for(total), 256, 0, s, (const float*)dcols, ldc, (float*)dx, g, beta, total, dt);
   after_launch("col2im");
-}
-void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s) {
-  const int64_t total = (int64_t)K * R * S * C;
-  if (total == 0) return;
-  launch_pdl(flip_weights_kernel, grid_for(total), 256, 0, s, (const uint16_t*)w, (uint16_t*)wf, K, R, S, C, total);
-  after_launch("flip_weights");
-}
-void conv_phase_weights(const void* w, uint16_t* wp, const ConvGeom& g, const int* cr, const int* dr, const int* cs,
-                        const int* ds, const int64_t* woff, cudaStream_t s) {
-  PhaseW pw;
-  for (int i = 0; i < 16; ++i) pw.off[i] = woff[i];
-  for (int i = 0; i < 4; ++i) {
-    pw.cr[i] = i < g.stride ? cr[i] : 0; pw.dr[i] = i < g.stride ? dr[i] : 0;
-    pw.cs[i] = i < g.stride ? cs[i] : 0; pw.ds[i] = i < g.stride ? ds[i] : 0;
-  }
-  const int64_t total = (int64_t)g.K * g.R * g.S * g.C;
-  launch_pdl(phase_weights_kernel, grid_for(total), 256, 0, s, (const uint16_t*)w, wp, g.K, g.R, g.S, g.C, g.stride,
-             g.pad, pw, total);
-  after_launch("conv_phase_weights");
 }
 void conv_phase_zero(void* dx, const ConvGeom& g, const int* cr, const int* cs, cudaStream_t s) {
   uint32_t live = 0;

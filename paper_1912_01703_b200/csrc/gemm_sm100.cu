@@ -109,6 +109,12 @@ struct __align__(64) GemmParams {
   // output row m = (n, i, j) of the phase grid [N, cP, cQ] is stored to pixel
   // (n, ph_st·i + ph_h, ph_st·j + ph_w) of the [N, ph_H, ph_W] tensor D (ld = ldd)
   int ph_st, ph_h, ph_w, ph_H, ph_W;
+  // data-gradient convolutions (conv_tc / conv_fwd_patch): B read in place from
+  // the forward weights W[k, r, s, c] as an MN-major operand (tb[0] = W as
+  // [K_fwd rows, R·S·C cols], box {64 c, 64 k}): GEMM tap (t_r, t_s) reads the
+  // forward tap (bw_r0 + bw_rstep·t_r, bw_s0 + bw_sstep·t_s); no transposed /
+  // flipped weight copy is materialised.  bw_S = forward S, N = forward C.
+  int bw_inplace, bw_r0, bw_rstep, bw_s0, bw_sstep, bw_S;
 };
 constexpr int kEpiBytes = 32768;  // 8 epilogue warps × one 4 KB staging buffer
 
@@ -1184,7 +1190,15 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* sbase = smem + stage * C::STAGE_BYTES;
-          sm100::tma_load_2d(&p.tb[0], &full[stage], sbase + C::A_BYTES, kb * 64, tn * BN);
+          if (p.bw_inplace) {  // W in place, MN-major: BN/64 boxes {64 c, 64 k} of forward tap (rf, sf)
+            const int rf = p.bw_r0 + p.bw_rstep * r, sf = p.bw_s0 + p.bw_sstep * s;
+            const int col = (rf * p.bw_S + sf) * p.N + tn * BN;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              sm100::tma_load_2d(&p.tb[0], &full[stage], sbase + C::A_BYTES + j * 8192, col + j * 64, cb * 64);
+          } else {
+            sm100::tma_load_2d(&p.tb[0], &full[stage], sbase + C::A_BYTES, kb * 64, tn * BN);
+          }
           sm100::tma_load_im2col_4d(&p.ta[1], &full[stage], sbase, cb * 64, ws, hs, n0, (uint16_t)s, (uint16_t)r);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1223,7 +1237,16 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
         sm100::mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
+          if (p.bw_inplace) {
+            const int rf = p.bw_r0 + p.bw_rstep * r, sf = p.bw_s0 + p.bw_sstep * s;
+            const int col = (rf * p.bw_S + sf) * p.N + tn * BN;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES + j * 8192,
+                                 col + j * 64, cb * 64);
+          } else {
+            sm100::tma_load_2d(&p.tb[0], &full[stage], smem + stage * C::STAGE_BYTES + C::A_BYTES, kb * 64, tn * BN);
+          }
         }
         __syncwarp();
         const uint32_t dst = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + lane * 4 * 128;
@@ -1234,7 +1257,10 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
   } else if (warp == 1) {
     if (lane == 0) {
       // ===================== MMA issuer =====================
-      const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 0, 0);
+      const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 0, p.bw_inplace ? 1 : 0);
+      // B K-major (LBO 16, +32 B per K = 16) or MN-major in place (64-c chunks
+      // 8 KB apart, +16 rows · 128 B per K = 16)
+      const uint32_t b_lbo = p.bw_inplace ? 8192u : 16u, b_kstep = p.bw_inplace ? 2048u : 32u;
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -1248,7 +1274,7 @@ __global__ void __launch_bounds__(conv::kThreads, 1) conv_tc_kernel(const __grid
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = sm100::make_sw128_desc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = sm100::make_sw128_desc(sb + kk * 32, 16, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb + kk * b_kstep, b_lbo, 1024);
             sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
           sm100::mma_commit(&empty[stage]);
@@ -2061,7 +2087,14 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
   if (warp == 0) {
     if (lane == 0) {
       sm100::mbar_arrive_expect_tx(wbar, (uint32_t)(taps * 8192));
-      for (int t = 0; t < taps; ++t) sm100::tma_load_2d(&p.tb[0], wbar, wsm + t * 8192, t * 64, 0);
+      for (int t = 0; t < taps; ++t) {
+        if (p.bw_inplace) {  // W in place (MN-major box {64 c, 64 k} of the forward tap)
+          const int rf = p.bw_r0 + p.bw_rstep * (t / S), sf = p.bw_s0 + p.bw_sstep * (t % S);
+          sm100::tma_load_2d(&p.tb[0], wbar, wsm + t * 8192, (rf * p.bw_S + sf) * 64, 0);
+        } else {
+          sm100::tma_load_2d(&p.tb[0], wbar, wsm + t * 8192, t * 64, 0);
+        }
+      }
       int b = 0; uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int n = t / pg, p0 = (t - n * pg) * G;
@@ -2073,9 +2106,10 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
     }
   } else if (warp == 1 || warp == 3) {
     const int k = warp == 1 ? 0 : 1;
-    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 0, 0);
+    const uint32_t idesc = sm100::make_idesc(1u, BM, 64, 0, p.bw_inplace ? 1 : 0);
     const uint64_t a0 = sm100::make_sw128_desc(sm100::smem_u32(xb), 16, 1024);
-    const uint64_t w0 = sm100::make_sw128_desc(sm100::smem_u32(wsm), 16, 1024);
+    const uint64_t w0 = sm100::make_sw128_desc(sm100::smem_u32(wsm), p.bw_inplace ? 8192u : 16u, 1024);
+    const uint64_t wk = p.bw_inplace ? 128u : 2u;  // descriptor step per K = 16 (2 KB MN-major / 32 B K-major, >> 4)
     sm100::mbar_wait(wbar, 0);
     int ti = k;
     for (int t = blockIdx.x + k * gridDim.x; t < num_tiles; t += 2 * gridDim.x, ti += 2) {
@@ -2090,7 +2124,7 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
         const uint64_t bd = w0 + (uint64_t)(tp * 512);  // 8 KB >> 4
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          if (sm100::elect_one()) sm100::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (tp | kk) ? 1u : 0u);
+          if (sm100::elect_one()) sm100::mma_bf16(d, ad + 2 * kk, bd + wk * kk, idesc, (tp | kk) ? 1u : 0u);
       }
       if (sm100::elect_one()) {
         sm100::mma_commit(&empty[b]);
@@ -3525,8 +3559,10 @@ bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, cons
 
 // stride-1 conv from a shared input patch (conv_fwd_patch_kernel): C = K = 64,
 // ≤ 9 taps, W' = pow2 ≥ Q + S − 1 in [32, 128]; false when not applicable
+static void set_bw(GemmParams& p, const void* w, const ConvGeom& g, const int* bw);
 static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias,
-                           int act, float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr) {
+                           int act, float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr,
+                           const int* bw = nullptr) {
   if (stats && (yd != BE_BF16 || bias || act || beta != 0.f)) return false;
   static const int on = [] { const char* e = getenv("BE_CONV_PATCH"); return e ? atoi(e) : 1; }();
   if (!on || g.stride != 1 || g.C != 64 || g.K != 64 || g.R * g.S > 9 || (beta != 0.f && beta != 1.f)) return false;
@@ -3546,7 +3582,8 @@ static bool conv_fwd_patch(const void* x, const void* w, void* y, const ConvGeom
   const uint64_t dx4[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
   if (!encode_4d_tiled(&p.ta[0], x, dx4, 64, Wp, G + g.R - 1, 1)) return false;
   const int RSC = g.R * g.S * g.C;
-  encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, 64, 64);
+  if (bw) set_bw(p, w, g, bw);
+  else encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, 64, 64);
   const bool f32 = yd == BE_F32;
   {
     const cuuint64_t es = f32 ? 4 : 2;
@@ -3650,8 +3687,15 @@ static bool conv_stem(const void* x, const void* w, void* y, const ConvGeom& g, 
   return true;
 }
 
+// bw (data-gradient convolutions): {r0, rstep, s0, sstep, S_fwd, RSC_fwd} — w is the FORWARD weight
+// W[g.C rows = K_fwd][RSC_fwd] read in place as the MN-major B operand (GemmParams::bw_inplace)
+static void set_bw(GemmParams& p, const void* w, const ConvGeom& g, const int* bw) {
+  encode_operand(&p.tb[0], w, BE_BF16, bw[5], g.C, bw[5], false, 64, 64);
+  p.bw_inplace = 1;
+  p.bw_r0 = bw[0]; p.bw_rstep = bw[1]; p.bw_s0 = bw[2]; p.bw_sstep = bw[3]; p.bw_S = bw[4];
+}
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
-                   float beta, cudaStream_t s, float* stats, int* stats_parts) {
+                   float beta, cudaStream_t s, float* stats, int* stats_parts, const int* bw) {
   if (g.C % 64 != 0) {
     const char* e = getenv("BE_CONV_SMALLC");
     if (e && e[0] == '0') return false;
@@ -3660,7 +3704,7 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   }
   if (g.K % 16 != 0) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return false;
-  if (conv_fwd_patch(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts)) return true;
+  if (conv_fwd_patch(x, w, y, g, yd, bias, act, beta, s, stats, stats_parts, bw)) return true;
   const char* e = getenv("BE_CONV_IMPLICIT");
   if (e && e[0] == '0') return false;
   GemmParams p;
@@ -3674,7 +3718,8 @@ bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_
   p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
   p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
   const int bn = g.K >= 256 ? 256 : (g.K >= 128 ? 128 : 64);
-  encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
+  if (bw) set_bw(p, w, g, bw);
+  else encode_operand(&p.tb[0], w, BE_BF16, g.K, RSC, RSC, true, bn, 64);
   // x as a 2-D [N·H·W, C] matrix; tile::gather4 needs box {64, 1}
   encode_2d(&p.ta[0], x, BE_BF16, (uint64_t)g.C, (uint64_t)g.N * g.H * g.W, (uint64_t)g.C, 64, 1);
   // x as 4-D NHWC im2col map: window starts from −pad to W+pad−R (stride), 128 pixels × 64 channels
@@ -3712,7 +3757,7 @@ static void phase_taps(int R, int st, int pad, int rho, int* cnt, int* dmin) {
 // (likewise s) — every term of the transposed convolution, none of the
 // zero-inserted ones.  Each phase is one conv_tc_kernel launch: A = dY through
 // a TMA im2col map whose corners give the phase's window, B = the phase's
-// taps of W gathered into [C, R', S', K] (conv_phase_weights), and the epilogue
+// taps of W read in place as the MN-major B operand (GemmParams::bw_*), and the epilogue
 // stores row (n, i, j) straight to dx pixel (n, st·i + ρh, st·j + ρw) (beta 1:
 // read-add-write).  Phases with no taps are zero-filled (beta 0) or left
 // untouched (beta 1).  Replaces the dcols GEMM + col2im.
@@ -3732,23 +3777,12 @@ bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& 
   GemmParams ps[16];
   int nph = 0;
   bool zero_needed = false;
-  int64_t woff[16] = {};
-  int64_t wtot = 0;
   const int bn = g.C >= 256 ? 256 : (g.C >= 128 ? 128 : 64);
   for (int rh = 0; rh < st; ++rh)
     for (int rw = 0; rw < st; ++rw) {
       const int Hp = (g.H - rh + st - 1) / st, Wp = (g.W - rw + st - 1) / st;
       if (Hp <= 0 || Wp <= 0) continue;
       if (cr[rh] == 0 || cs[rw] == 0) { zero_needed = true; continue; }
-      woff[rh * st + rw] = wtot;
-      wtot += (int64_t)cr[rh] * cs[rw] * g.K * g.C;
-    }
-  Block* wb = wtot ? ctx().alloc.allocate(sizeof(uint16_t) * (size_t)wtot, s) : nullptr;
-  uint16_t* wp = wb ? reinterpret_cast<uint16_t*>(wb->ptr) : nullptr;
-  for (int rh = 0; rh < st; ++rh)
-    for (int rw = 0; rw < st; ++rw) {
-      const int Hp = (g.H - rh + st - 1) / st, Wp = (g.W - rw + st - 1) / st;
-      if (Hp <= 0 || Wp <= 0 || cr[rh] == 0 || cs[rw] == 0) continue;
       GemmParams& p = ps[nph];
       memset(&p, 0, sizeof(p));
       ConvGeom t;  // the phase convolution over dY
@@ -3757,13 +3791,12 @@ bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& 
       const int lw = dr[rw], lh = dr[rh];
       // window starts lower = dmin; base positions per row = Q_in + upper − lower = Wp
       const int corners[4] = {lw, lh, Wp - g.Q + lw, Hp - g.P + lh};
-      if (!encode_im2col_4d(&p.ta[1], dy, t, 64, BM, corners)) {
-        if (wb) ctx().alloc.free(wb);
-        return false;
-      }
+      if (!encode_im2col_4d(&p.ta[1], dy, t, 64, BM, corners)) return false;
       encode_2d(&p.ta[0], dy, BE_BF16, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, (uint64_t)g.K, 64, 1);
       const int RSC = t.R * t.S * t.C;
-      encode_operand(&p.tb[0], wp + woff[rh * st + rw], BE_BF16, t.K, RSC, RSC, true, bn, 64);
+      // the phase's taps of W read in place: t_r ↔ r = ρh + pad − st·(dminh + t_r)
+      const int bw[6] = {rh + g.pad - st * dr[rh], -st, rw + g.pad - st * ds[rw], -st, g.S, g.R * g.S * g.C};
+      set_bw(p, w, t, bw);
       p.use_im2col = 1;
       p.M = t.N * t.P * t.Q; p.N = t.K; p.K = RSC;
       p.a_kmajor = 1; p.b_kmajor = 1; p.splits = 1;
@@ -3775,19 +3808,18 @@ bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& 
       ++nph;
     }
   if (zero_needed && beta == 0.f) conv_phase_zero(dx, g, cr, cs, s);
-  if (wtot) conv_phase_weights(w, wp, g, cr, dr, cs, ds, woff, s);
-  const double flops = 2.0 * g.N * (double)g.P * g.Q * g.K * g.R * g.S * g.C;
-  const double bytes = ((double)g.N * g.P * g.Q * g.K + (double)g.K * g.R * g.S * g.C + (double)g.N * g.H * g.W * g.C) * 2.0;
-  const int pidx = prof_begin("conv_tc_dgrad_phase", flops, bytes, g.N * g.H * g.W, g.C, g.R * g.S * g.K, s);
-  for (int i = 0; i < nph; ++i) {
+  for (int i = 0; i < nph; ++i) {  // one profiler record per launch (tools/ncu_class.py pairs them with ncu's list)
+    const GemmParams& p = ps[i];
+    const double flops = 2.0 * p.M * (double)p.N * p.K;
+    const double bytes = ((double)g.N * g.P * g.Q * g.K + (double)p.N * p.K + (double)p.M * p.N * (beta != 0.f ? 2 : 1)) * 2.0;
+    const int pidx = prof_begin("conv_tc_dgrad_phase", flops, bytes, p.M, p.N, p.K, s);
     if (bn == 256) launch_conv<256>(ps[i], s, nullptr);
     else if (bn == 128) launch_conv<128>(ps[i], s, nullptr);
     else launch_conv<64>(ps[i], s, nullptr);
+    prof_end(pidx, s);
     g_tc_calls++;
   }
-  prof_end(pidx, s);
   after_launch("conv_tc_dgrad_phase");
-  if (wb) ctx().alloc.free(wb);
   return true;
 }
 

@@ -127,17 +127,14 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
 // a per-row input patch (gemm_sm100.cu conv_wgrad_stem_kernel); false: not applicable
 bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                      cudaStream_t s);
+// bw (data gradient as a convolution of dY): w is the FORWARD weight W[K_fwd = g.C][R_f, S_f, C_fwd = g.K],
+// read in place as the MN-major B operand; tap (t_r, t_s) of this convolution reads forward tap
+// (bw[0] + bw[1]·t_r, bw[2] + bw[3]·t_s); bw[4] = S_f, bw[5] = R_f·S_f·C_fwd
 bool conv_implicit(const void* x, const void* w, void* y, const ConvGeom& g, be_dtype yd, const float* bias, int act,
-                   float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr);
-// bf16 wf[C,R,S,K] = w[K,R−1−r,S−1−s,C] (dgrad of a stride-1 conv as a convolution)
-void flip_weights(const void* w, void* wf, int K, int R, int S, int C, cudaStream_t s);
+                   float beta, cudaStream_t s, float* stats = nullptr, int* stats_parts = nullptr,
+                   const int* bw = nullptr);
 // stride-2+ dgrad by phases (gemm_sm100.cu conv_dgrad_phases; false = not applicable)
 bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& g, float beta, cudaStream_t s);
-// the phase convolutions' weights: tap (r, s) of w[K, R, S, C] (bf16) goes to phase
-// (ρh, ρw) = ((r − pad) mod st, (s − pad) mod st) at [c, t_r, t_s, k] of the block
-// at woff[ρh·st + ρw], t = (ρ + pad − r)/st − dmin[ρ]
-void conv_phase_weights(const void* w, uint16_t* wp, const ConvGeom& g, const int* cr, const int* dr, const int* cs,
-                        const int* ds, const int64_t* woff, cudaStream_t s);
 // zero the dx pixels of phases without taps (cr[ρh] == 0 or cs[ρw] == 0)
 void conv_phase_zero(void* dx, const ConvGeom& g, const int* cr, const int* cs, cudaStream_t s);
 // cols[M, R*S*C] (row-major, ldc = padded RSC) from x NHWC

@@ -120,15 +120,15 @@ static void vjp_conv(Node* n, GradSink& sink) {
     // W'[c,r,s,k] = W[k,R−1−r,S−1−s,c] → implicit GEMM, no dcols / col2im
     if (!is_pointwise(g) && g.stride == 1 && opd == BE_BF16 && g.K % 64 == 0 && g.C % 16 == 0 &&
         g.pad <= g.R - 1 && g.pad <= g.S - 1) {
-      TRef wf = new_tensor({(int64_t)g.C, (int64_t)g.R, (int64_t)g.S, (int64_t)g.K}, opd);
-      k::flip_weights(w->data(), wf->data(), g.K, g.R, g.S, g.C, s);
+      // W'[c, r, s, k] = W[k, R−1−r, S−1−s, c] read in place (MN-major B operand): no flipped copy
+      const int bw[6] = {g.R - 1, -1, g.S - 1, -1, g.S, (int)RSC};
       k::ConvGeom gt;
       gt.N = g.N; gt.H = g.P; gt.W = g.Q; gt.C = g.K; gt.K = g.C; gt.R = g.R; gt.S = g.S;
       gt.stride = 1; gt.pad = g.R - 1 - g.pad;
       gt.P = (gt.H + 2 * gt.pad - gt.R) + 1;
       gt.Q = (gt.W + 2 * (g.S - 1 - g.pad) - gt.S) + 1;
       if (gt.P == g.H && gt.Q == g.W && g.R == g.S &&
-          k::conv_implicit(dz->data(), wf->data(), dx->data(), gt, opd, nullptr, 0, bx, s)) {
+          k::conv_implicit(dz->data(), w->data(), dx->data(), gt, opd, nullptr, 0, bx, s, nullptr, nullptr, bw)) {
         sink.commit(0);
         return;
       }
