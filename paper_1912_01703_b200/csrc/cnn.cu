@@ -1502,8 +1502,75 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
   launch_pdl(maxpool_bwd_kernel, grid_for(total), 256, 0, s, dy, am, dx, g, dt, beta, total);
   after_launch("maxpool_bwd");
 }
+namespace {
+// bf16, C % 8 == 0: one thread per (n, 8-channel vector); HW 16-B loads summed
+// in the scalar kernel's order (i ≡ part mod 4 partial sums, combined 0+1+2+3)
+__global__ void avgpool_fwd_v8(const uint16_t* __restrict__ x, uint16_t* __restrict__ y, int HW, int C, uint32_t total) {
+  pdl_entry();
+  const uint32_t CV = (uint32_t)C / 8;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t n = t / CV, cv = t - n * CV;
+    const uint16_t* xp = x + (int64_t)n * HW * C + cv * 8;
+    float a[4][8] = {};
+    int i = 0;
+    for (; i + 4 <= HW; i += 4) {
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = __ldg(reinterpret_cast<const uint4*>(xp + (int64_t)(i + k) * C));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float v[8];
+        unpack8(u[k], v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[k][j] += v[j];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (i + k < HW) {
+        float v[8];
+        unpack8(__ldg(reinterpret_cast<const uint4*>(xp + (int64_t)(i + k) * C)), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[k][j] += v[j];
+      }
+    }
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (a[0][j] + a[1][j] + a[2][j] + a[3][j]) / (float)HW;
+    *reinterpret_cast<uint4*>(y + (int64_t)n * C + cv * 8) = pack8(o);
+  }
+}
+// bf16, C % 8 == 0: one thread per 8 channels of one pixel (16-B load / store)
+__global__ void avgpool_bwd_v8(const uint16_t* __restrict__ dy, uint16_t* __restrict__ dx, int HW, int C, float beta,
+                               uint32_t total) {
+  pdl_entry();
+  const uint32_t CV = (uint32_t)C / 8, per_n = (uint32_t)HW * CV;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t n = t / per_n, cv = t % CV;
+    float v[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(dy + (int64_t)n * C + cv * 8)), v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] /= (float)HW;
+    uint4* o = reinterpret_cast<uint4*>(dx + (int64_t)t * 8);
+    if (beta != 0.f) {
+      float old[8];
+      unpack8(*o, old);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += old[j];
+    }
+    *o = pack8(v);
+  }
+}
+}  // namespace
 void avgpool_fwd(const void* x, void* y, int N, int HW, int C, be_dtype dt, cudaStream_t s) {
   if (N == 0 || C == 0) return;
+  const int64_t vecs = (int64_t)N * C / 8;
+  if (dt == BE_BF16 && C % 8 == 0 && HW > 0 && aligned16(x) && aligned16(y) && vecs < (1LL << 31)) {
+    launch_pdl(avgpool_fwd_v8, (int)std::max<int64_t>(1, (vecs + 127) / 128), 128, 0, s, (const uint16_t*)x,
+               (uint16_t*)y, HW, C, (uint32_t)vecs);
+    after_launch("avgpool_fwd_v8");
+    return;
+  }
   dim3 grid((C + 63) / 64, N);
   launch_pdl(avgpool_fwd_kernel, grid, 256, 0, s, x, y, HW, C, dt);
   after_launch("avgpool_fwd");
@@ -1511,6 +1578,12 @@ void avgpool_fwd(const void* x, void* y, int N, int HW, int C, be_dtype dt, cuda
 void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, float beta, cudaStream_t s) {
   const int64_t total = (int64_t)N * HW * C;
   if (total == 0) return;
+  if (dt == BE_BF16 && C % 8 == 0 && aligned16(dy) && aligned16(dx) && total / 8 < (1LL << 31)) {
+    launch_pdl(avgpool_bwd_v8, grid_for(total / 8), 256, 0, s, (const uint16_t*)dy, (uint16_t*)dx, HW, C, beta,
+               (uint32_t)(total / 8));
+    after_launch("avgpool_bwd_v8");
+    return;
+  }
   launch_pdl(avgpool_bwd_kernel, grid_for(total), 256, 0, s, dy, dx, HW, C, dt, beta, total);
   after_launch("avgpool_bwd");
 }

@@ -185,7 +185,8 @@ static void op_conv(const be_tensor* in, int n_in, const void* attrs, be_tensor*
   // only where the epilogue has slack: reduction depth R·S·C ≥ output channels
   // (for K-light, N-heavy convs — the 1×1 expansions — the epilogue is the
   // bottleneck and the extra column reduction costs more than the BN pass it saves)
-  if (stats_on && a.bn_stats && !b && !a.act && M > 0 && RSC >= g.K) {
+  static const bool stats_all = [] { const char* e = getenv("BE_BN_STATS_ALL"); return e && e[0] == '1'; }();
+  if (stats_on && a.bn_stats && !b && !a.act && M > 0 && (RSC >= g.K || stats_all)) {
     const int64_t cap = (int64_t)ctx().num_sms * 4;
     stats = new_tensor({2 * cap * g.K}, BE_F32);
     BE_CHECK_CUDA(cudaMemsetAsync(stats->data(), 0, sizeof(float) * 2 * cap * g.K, ctx().stream));
