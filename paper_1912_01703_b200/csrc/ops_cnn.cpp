@@ -88,7 +88,10 @@ static void vjp_conv(Node* n, GradSink& sink) {
       // variant 3: shared input patch per tile, shifted UMMA operands (stride 1, C = K = 64)
       const bool patch_ok = shift_ok && g.stride == 1 && ((g.C == 64 && g.K % 64 == 0 && g.K <= 256) || (g.C == 128 && g.K == 128)) &&
                             dw->dtype == BE_F32 && g.R * g.S <= 64 && g.Q + g.S - 1 <= 128;
-      variant = tune_choose(key, patch_ok ? 4 : (shift_ok ? 3 : 2), 0, &e0, &e1);
+      static const int force = [] { const char* e = getenv("BE_WGRAD_VARIANT"); return e ? atoi(e) : -1; }();
+      const int nv = patch_ok ? 4 : (shift_ok ? 3 : 2);
+      if (force >= 0 && force < nv) variant = force;  // probes / tests
+      else variant = tune_choose(key, nv, 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);
     if (g.C == 8 && opd == BE_BF16 && !e0 && k::conv_wgrad_stem(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
