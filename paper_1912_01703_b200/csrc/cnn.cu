@@ -109,6 +109,34 @@ __global__ void __launch_bounds__(256) im2col_taps_kernel(const T* __restrict__ 
   const uint32_t CV = (uint32_t)(g.C / VEC);
   const int RS = g.R * g.S;
   const uint32_t stride = gridDim.x * blockDim.x;
+  if (RS == 1) {  // 1×1 (strided) convolution: a subsampling copy — batch the items instead of the taps
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += B * stride) {
+      VT v[B];
+      int64_t dst[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const uint32_t i = i0 + k * stride;
+        dst[k] = -1;
+        if (i < total) {
+          const int cv = (int)(i % CV);
+          const uint32_t m = i / CV;
+          const int q = (int)(m % (uint32_t)g.Q);
+          const uint32_t np = m / (uint32_t)g.Q;
+          const int p = (int)(np % (uint32_t)g.P);
+          const int n = (int)(np / (uint32_t)g.P);
+          const int h = p * g.stride - g.pad, w = q * g.stride - g.pad;
+          dst[k] = (int64_t)m * ldc + cv * VEC;
+          v[k] = VT{};
+          if (h >= 0 && h < g.H && w >= 0 && w < g.W)
+            v[k] = *reinterpret_cast<const VT*>(x + (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * VEC);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+        if (dst[k] >= 0) *reinterpret_cast<VT*>(cols + dst[k]) = v[k];
+    }
+    return;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     const int cv = (int)(i % CV);
     const uint32_t m = i / CV;
