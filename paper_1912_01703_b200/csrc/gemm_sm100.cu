@@ -2167,6 +2167,209 @@ __global__ void __launch_bounds__(cfp::kThreads, 1) conv_fwd_patch_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------- conv wgrad, im2col gathered into smem
+// dW[k, (r,s,c)] = Σ_{n,p,q} dY[n,p,q,k] · x[n, p·st−pad+r, q·st−pad+s, c] (C % 64 == 0, K % 128 == 0)
+// as a split-K GEMM over pixel blocks of 64 without a materialised column
+// matrix: A = dYᵀ by TMA (MN-major, boxes {64 k, 64 pixels}); B = the
+// im2col slice [BN (tap, c) × 64 pixels] gathered by 4 warps with cp.async
+// straight into the MN-major SW128 layout UMMA reads (thread = one pixel ×
+// BN/2 channels: 16-B piece j of pixel row kk at (j ^ (kk & 7)) · 16; zero fill
+// for padding and for pixels past the end).  The materialised variant spent
+// ~40 % of its time writing 9× the input to HBM; TMA im2col (~0.13 px/clk)
+// and the shifted 4-D tiles were 3–4× slower than the GEMM on the columns.
+// Each CTA writes fp32 split slabs; the fixed-order splitk_reduce sums them.
+namespace wgg {
+constexpr int kThreads = 512;   // w0-3 gather, w4 TMA (A), w5 MMA, w6 TMEM, w8-15 epilogue
+// cp.async groups in flight per gather thread before its stage is signalled
+// full: the stages still available to the MMA are STAGES − LAG
+template <int BN> constexpr int lag() { return BN == 256 ? 1 : 2; }
+template <int BN>
+struct Cfg {
+  static constexpr int LAG = lag<BN>();
+  static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (226 * 1024 - kEpiBytes - 1280) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 + 256;
+};
+}  // namespace wgg
+
+template <int BN>
+__global__ void __launch_bounds__(wgg::kThreads, 1) conv_wgrad_gather_kernel(const __grid_constant__ GemmParams p) {
+  pdl_entry();
+  using C = wgg::Cfg<BN>;
+  static_assert(C::STAGES > C::LAG, "gather pipeline needs more stages than cp.async groups in flight");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblocks = (p.K + 63) / 64;
+  const int mn_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = mn_tiles * p.splits;
+  if (threadIdx.x == 0) {
+    // full: 128 gather threads + 1 TMA expect_tx arrival
+    for (int st = 0; st < C::STAGES; ++st) { sm100::mbar_init(&full[st], 129); sm100::mbar_init(&empty[st], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], kEpiWarps); }
+    sm100::fence_barrier_init();
+    sm100::tma_prefetch(&p.ta[0]);
+  }
+  if (warp == 6) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    // ===================== B gather (pixel kk = tid / 2, channel half = tid % 2) =====================
+    const int tid = threadIdx.x, kk = tid >> 1, half = tid & 1;
+    constexpr int CPT = BN / 128;  // 64-channel chunks per thread
+    int stage = 0; uint32_t phase = 0;
+    int pend_stage[C::LAG + 1];
+    int npend = 0, head = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int sp = t / mn_tiles, tn = (t % mn_tiles) / p.tiles_m;
+      // the thread's chunks: global column n0 + 64·ch → tap, channel offset
+      int coff[CPT], tr[CPT], ts[CPT];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int col = tn * BN + (half * CPT + i) * 64;
+        const int tap = col / p.cC;
+        coff[i] = col - tap * p.cC;
+        tr[i] = tap / p.cS; ts[i] = tap - tr[i] * p.cS;
+      }
+      const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int m = kb * 64 + kk;  // pixel
+        int hb = -(1 << 25), wb = 0;
+        long long base = 0;
+        if (m < p.K) {
+          const int q = m % p.cQ, pq = m / p.cQ;
+          const int pp = pq % p.cP, n = pq / p.cP;
+          hb = pp * p.cstride - p.cpad;
+          wb = q * p.cstride - p.cpad;
+          base = ((long long)n * p.cH * p.cW) * p.cC;
+        }
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t sbase = sm100::smem_u32(smem + stage * C::STAGE_BYTES) + C::A_BYTES + kk * 128;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const int h = hb + tr[i], w = wb + ts[i];
+          const bool ok = (unsigned)h < (unsigned)p.cH && (unsigned)w < (unsigned)p.cW;
+          const uint16_t* src = ok ? p.x + base + ((long long)h * p.cW + w) * p.cC + coff[i] : p.x;
+          const uint32_t dst = sbase + (half * CPT + i) * 8192;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sm100::cp_async_16(dst + ((j ^ (kk & 7)) << 4), src + j * 8, ok ? 16u : 0u);
+        }
+        sm100::cp_async_commit();
+        pend_stage[(head + npend) % (C::LAG + 1)] = stage;
+        ++npend;
+        if (npend > C::LAG) {
+          sm100::cp_async_wait<C::LAG>();
+          sm100::fence_proxy_async();
+          sm100::mbar_arrive(&full[pend_stage[head]]);
+          head = (head + 1) % (C::LAG + 1);
+          --npend;
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    sm100::cp_async_wait<0>();
+    sm100::fence_proxy_async();
+    while (npend > 0) {
+      sm100::mbar_arrive(&full[pend_stage[head]]);
+      head = (head + 1) % (C::LAG + 1);
+      --npend;
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      // ===================== A (dYᵀ, MN-major) TMA producer =====================
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int sp = t / mn_tiles, tm = (t % mn_tiles) % p.tiles_m;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::A_BYTES);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          sm100::tma_load_2d(&p.ta[0], &full[stage], sa, tm * BM, kb * 64);
+          sm100::tma_load_2d(&p.ta[0], &full[stage], sa + 8192, tm * BM + 64, kb * 64);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ===================== MMA issuer (A and B MN-major) =====================
+      const uint32_t idesc = sm100::make_idesc(1u, BM, BN, 1, 1);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int sp = t / mn_tiles;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kblocks, kb0 + p.kb_per_split);
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * C::STAGE_BYTES), sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const uint64_t ad = sm100::make_sw128_desc(sa + k4 * 2048, 8192, 1024);
+            const uint64_t bd = sm100::make_sw128_desc(sb + k4 * 2048, 8192, 1024);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, ((kb - kb0) | k4) ? 1u : 0u);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue: fp32 split slab by TMA store =====================
+    const int ew = warp - 8;
+    const int eq = warp & 3, eh = ew >> 2;
+    int slot = 0;
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int sp = t / mn_tiles, tm = (t % mn_tiles) % p.tiles_m, tn = (t % mn_tiles) / p.tiles_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int store_row = sp * p.split_rows + tm * BM + eq * 32;
+#pragma unroll 1
+      for (int it = 0; it < BN / 128; ++it) {
+        const int c0 = eh * (BN / 2) + it * 64;
+        const int col0 = tn * BN + c0;
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + acc * BN + c0 + ((uint32_t)(eq * 32) << 16);
+        sm100::tmem_ld_32x32b_x32(ta, r0);
+        sm100::tmem_ld_32x32b_x32(ta + 32, r1);
+        sm100::tmem_ld_wait();
+        epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0, r0);
+        epi_tma32(p, epi_smem + ew * 4096, slot, lane, store_row, col0 + 32, r1);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) sm100::bulk_wait<0>();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 6) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- stem conv wgrad: im2col built in smem from the patch
 // dW[k, r, s, c] = Σ_{n,p,q} dY[n,p,q,k] · x[n, p·st−pad+r, q·st−pad+s, c] for
 // the C = 8 stem (ResNet conv1 7×7/2): the materialised im2col is 2.5 GB at
@@ -3479,6 +3682,63 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
 
 // stem conv weight gradient (conv_wgrad_stem_kernel): C = 8, K = 64, Q ≤ 128,
 // R·S ≤ 128; dw fp32 [64, R·S·8] (+)= dW; false when not applicable
+// conv wgrad with the im2col slice gathered in smem (conv_wgrad_gather_kernel);
+// false when the shape does not fit (C % 64, K % 128, (R·S·C) % BN)
+bool conv_wgrad_gather(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
+                       cudaStream_t s) {
+  static const int on = [] { const char* e = getenv("BE_WGRAD_GATHER"); return e ? atoi(e) : 1; }();
+  const int RSC = g.R * g.S * g.C;
+  static const int bn_env = [] { const char* e = getenv("BE_WGG_BN"); return e ? atoi(e) : 0; }();
+  const int bn = (bn_env != 128 && RSC % 256 == 0 && g.C % 256 == 0) ? 256 : 128;
+  if (!on || dwt != BE_F32 || g.C % 64 != 0 || g.K % 128 != 0 || RSC % bn != 0 || (beta != 0.f && beta != 1.f))
+    return false;
+  if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const long long pixels = (long long)g.N * g.P * g.Q;
+  if (pixels >= (1LL << 31) || (long long)g.N * g.H * g.W * g.C >= (1LL << 40)) return false;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = g.K; p.N = RSC; p.K = (int)pixels;
+  p.x = reinterpret_cast<const uint16_t*>(x);
+  p.cN = g.N; p.cH = g.H; p.cW = g.W; p.cC = g.C; p.cR = g.R; p.cS = g.S;
+  p.cstride = g.stride; p.cpad = g.pad; p.cP = g.P; p.cQ = g.Q;
+  encode_operand(&p.ta[0], dy, BE_BF16, g.K, (int)pixels, g.K, false, 64, 64);  // dY as [pixels, K]: MN-major A
+  p.tiles_m = g.K / BM; p.tiles_n = RSC / bn;
+  const int mn = p.tiles_m * p.tiles_n, sms = ctx().num_sms;
+  const int kblocks = (int)((pixels + 63) / 64);
+  int splits = std::max(1, std::min(2 * sms / mn, kblocks / 4));
+  int kps = (kblocks + splits - 1) / splits;
+  splits = (kblocks + kps - 1) / kps;
+  p.splits = splits; p.kb_per_split = kps;
+  p.split_rows = p.tiles_m * BM;
+  p.split_stride = (long long)p.split_rows * RSC;
+  Block* ws = ctx().alloc.allocate(sizeof(float) * (size_t)splits * p.split_stride, s);
+  p.D = ws->ptr; p.ldd = RSC; p.d_f32 = 1; p.beta = 0.f;
+  setup_store(p, ws->ptr, true, (long long)splits * p.split_rows, RSC, RSC);
+  BE_REQUIRE(p.tma_store == 1, BE_E_CUDA, "conv_wgrad_gather: slab store map");
+  const int grid = std::min(mn * splits, sms);
+  const double flops = 2.0 * pixels * (double)g.K * RSC;
+  const double bytes = ((double)g.N * g.H * g.W * g.C + (double)pixels * g.K) * 2.0 + 4.0 * g.K * RSC;
+  const int pidx = prof_begin("conv_tc_wgrad_gather", flops, bytes, g.K, RSC, (int)pixels, s);
+  if (bn == 256) {
+    static bool a = false;
+    if (!a) { BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_gather_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgg::Cfg<256>::SMEM)); a = true; }
+    launch_pdl(conv_wgrad_gather_kernel<256>, grid, wgg::kThreads, wgg::Cfg<256>::SMEM, s, p);
+  } else {
+    static bool a = false;
+    if (!a) { BE_CHECK_CUDA(cudaFuncSetAttribute(conv_wgrad_gather_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgg::Cfg<128>::SMEM)); a = true; }
+    launch_pdl(conv_wgrad_gather_kernel<128>, grid, wgg::kThreads, wgg::Cfg<128>::SMEM, s, p);
+  }
+  prof_end(pidx, s);
+  after_launch("conv_wgrad_gather");
+  g_tc_calls++;
+  const long long total = (long long)g.K * RSC;
+  launch_pdl(splitk_reduce, splitk_blocks(total), 256, 0, s, reinterpret_cast<const float*>(ws->ptr), splits,
+             p.split_stride, g.K, RSC, dw, (long long)RSC, 1, beta, (const float*)nullptr, 0);
+  after_launch("conv_wgrad_gather_reduce");
+  ctx().alloc.free(ws);
+  return true;
+}
+
 bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                      cudaStream_t s) {
   static const int on = [] { const char* e = getenv("BE_WGRAD_STEM"); return e ? atoi(e) : 1; }();

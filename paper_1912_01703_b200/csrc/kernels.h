@@ -125,6 +125,9 @@ bool conv_wgrad_patch(const void* dy, const void* x, void* dw, be_dtype dwt, con
                       cudaStream_t s);
 // stem conv weight gradient (C = 8, K = 64): im2col slices built in smem from
 // a per-row input patch (gemm_sm100.cu conv_wgrad_stem_kernel); false: not applicable
+// dW (fp32, [K, R·S·C]) (+)= dYᵀ·im2col(x) with the im2col slice gathered in smem (C % 64, K % 128)
+bool conv_wgrad_gather(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
+                       cudaStream_t s);
 bool conv_wgrad_stem(const void* dy, const void* x, void* dw, be_dtype dwt, const ConvGeom& g, float beta,
                      cudaStream_t s);
 // bw (data gradient as a convolution of dY): w is the FORWARD weight W[K_fwd = g.C][R_f, S_f, C_fwd = g.K],

@@ -78,7 +78,7 @@ static void vjp_conv(Node* n, GradSink& sink) {
     // variant 2: A = dY and B = x read as shifted 4-D tiles (blocks of whole
     // output rows; TMA zero-fills the padding) — tiled TMA, no im2col mode
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    int variant = 1;
+    int variant = 1, gidx = -1;
     if (!is_pointwise(g) && opd == BE_BF16 && g.C % 64 == 0 && (K * 2) % 16 == 0) {
       char key[160];
       snprintf(key, sizeof(key), "conv_wgrad:%d,%d,%d,%d,%d,%d,%d,%d,%d", g.N, g.H, g.W, g.C, g.K, g.R, g.S,
@@ -89,17 +89,24 @@ static void vjp_conv(Node* n, GradSink& sink) {
       const bool patch_ok = shift_ok && g.stride == 1 && ((g.C == 64 && g.K % 64 == 0 && g.K <= 256) || (g.C == 128 && g.K == 128)) &&
                             dw->dtype == BE_F32 && g.R * g.S <= 64 && g.Q + g.S - 1 <= 128;
       static const int force = [] { const char* e = getenv("BE_WGRAD_VARIANT"); return e ? atoi(e) : -1; }();
-      const int nv = patch_ok ? 4 : (shift_ok ? 3 : 2);
+      int nv = patch_ok ? 4 : (shift_ok ? 3 : 2);
+      // last candidate: the im2col slice gathered into shared memory (conv_wgrad_gather)
+      if (dw->dtype == BE_F32 && g.K % 128 == 0 && (RSC % 128) == 0 && (bw == 0.f || bw == 1.f)) gidx = nv++;
       if (force >= 0 && force < nv) variant = force;  // probes / tests
       else variant = tune_choose(key, nv, 0, &e0, &e1);
     }
     if (e0) cudaEventRecord(e0, s);
     if (g.C == 8 && opd == BE_BF16 && !e0 && k::conv_wgrad_stem(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
       sink.commit(1);
-    } else if (variant == 3 && k::conv_wgrad_patch(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
+    } else if (variant == gidx && k::conv_wgrad_gather(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
+      if (e1) cudaEventRecord(e1, s);
+      sink.commit(1);
+    } else if (variant == 3 && gidx != 3 &&
+               k::conv_wgrad_patch(dz->data(), x->data(), dw->data(), dw->dtype, g, bw, s)) {
       if (e1) cudaEventRecord(e1, s);
       sink.commit(1);
     } else {
+    if (variant == gidx) variant = 1;
     if (variant == 3) variant = 1;
     if (variant == 0 || variant == 2) {
       gd.conv_x = x->data();

@@ -449,12 +449,17 @@ def test_bn_statistics_from_conv_epilogue(cfg):
                                  # C = K = 128 (one tap per MMA, 3 tap groups): ResNet layer-2 size, ragged
                                  (2, 128, 28, 28, 128, 3, 1, 1), (1, 128, 13, 11, 128, 3, 1, 1),
                                  # C = 64, K = 192 (AlexNet conv2 5×5: three dY planes, N = 192, 7 tap groups)
-                                 (2, 64, 27, 27, 192, 5, 1, 2)])
+                                 (2, 64, 27, 27, 192, 5, 1, 2),
+                                 # im2col gathered in smem (K % 128 == 0): stride 2 ragged, BN = 256 (C % 256 == 0),
+                                 # three M tiles (K = 384), BN = 128 with a tap boundary inside no tile
+                                 (3, 128, 15, 15, 128, 3, 2, 1), (2, 256, 9, 9, 256, 3, 1, 1),
+                                 (1, 256, 12, 10, 384, 3, 1, 1), (2, 128, 8, 8, 256, 3, 1, 1)])
 def test_conv_wgrad_variants_bf16(cfg):
     """Conv weight gradient through every autotuned variant (the first calls
     of a shape cycle through them: TMA-im2col B, materialised columns,
-    shifted 4-D tiles of dY and x) — each call's dW vs the oracle on the
-    same bf16 x and dY (fp32 accumulation → 1e-3)."""
+    shifted 4-D tiles of dY and x, shared patch, im2col gathered in smem) —
+    each call's dW vs the oracle on the same bf16 x and dY (fp32 accumulation
+    → 1e-3)."""
     be = be_init()
     be.set_compute_dtype("bf16")
     N, C, H, W, K, R, st, pd = cfg
