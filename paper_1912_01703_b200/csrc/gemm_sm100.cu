@@ -3497,19 +3497,8 @@ void launch_tc2(const GemmDesc& g, cudaStream_t s) {
   }
 }
 
-// Variant choice for bf16: 1-CTA (BN from pick_bn) or CTA pair 256×256.
-// BE_GEMM_PAIR=0/1 forces; otherwise shapes where both are plausible are
-// autotuned on the fly: the first two launches of a shape run one variant
-// each bracketed by CUDA events (no synchronisation), and once both events
-// have completed the faster variant is used for that shape from then on.
-struct TuneEntry {
-  int tried = 0;
-  int choice = -1;  // 0 = 1-CTA, 1 = pair
-  cudaEvent_t ev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-};
-std::mutex g_tune_mu;
-std::unordered_map<std::string, TuneEntry> g_tune;
-
+// CTA-pair candidate: BE_GEMM_PAIR=0 drops it, =1 forces it where plausible;
+// otherwise it is one of gemm()'s autotuned candidates (runtime.cpp tune_choose)
 int pair_mode() {
   static int mode = [] { const char* e = getenv("BE_GEMM_PAIR"); return e ? atoi(e) : -1; }();
   return mode;
@@ -3522,36 +3511,6 @@ std::string tune_key(const GemmDesc& g) {
   return std::to_string(g.M) + "x" + std::to_string(g.N) + "x" + std::to_string(g.K) + (g.a_kmajor ? "k" : "m") +
          (g.b_kmajor ? "k" : "m") + (g.d == BE_F32 ? "f" : "h");
 }
-// returns variant to run and (optionally) the event pair to bracket it with
-int tune_pick(const GemmDesc& g, cudaEvent_t* ev0, cudaEvent_t* ev1) {
-  *ev0 = *ev1 = nullptr;
-  const int mode = pair_mode();
-  if (mode == 0) return 0;
-  if (!pair_plausible(g)) return 0;
-  if (mode == 1) return 1;
-  std::lock_guard<std::mutex> lk(g_tune_mu);
-  TuneEntry& e = g_tune[tune_key(g)];
-  if (e.choice >= 0) return e.choice;
-  if (e.tried < 2) {
-    const int v = e.tried++;
-    cudaEventCreate(&e.ev[v][0]);
-    cudaEventCreate(&e.ev[v][1]);
-    *ev0 = e.ev[v][0];
-    *ev1 = e.ev[v][1];
-    return v;
-  }
-  if (cudaEventQuery(e.ev[1][1]) == cudaSuccess && cudaEventQuery(e.ev[0][1]) == cudaSuccess) {
-    float t0 = 0, t1 = 0;
-    cudaEventElapsedTime(&t0, e.ev[0][0], e.ev[0][1]);
-    cudaEventElapsedTime(&t1, e.ev[1][0], e.ev[1][1]);
-    e.choice = t1 < t0 ? 1 : 0;
-    for (auto& pr : e.ev) for (auto& x : pr) cudaEventDestroy(x);
-    return e.choice;
-  }
-  cudaGetLastError();
-  return 1;  // not measured yet: pairs are never much worse when plausible
-}
-
 int pick_bn(int M, int N, int sms, bool x3) {
   // Largest BN whose wave efficiency is within 10% of the best candidate.
   const int cands_bf16[3] = {256, 128, 64};

@@ -117,6 +117,24 @@ struct TuneState {
 };
 std::mutex g_tune_mu;
 std::unordered_map<std::string, TuneState> g_tune;
+// BE_TUNE_FILE=path: decisions already in the file are replayed (no timing),
+// new ones are appended — so a profiled run (ncu serialises and replays
+// kernels, which distorts the timings) uses the choices of an unprofiled run
+const char* tune_file() {
+  static const char* f = getenv("BE_TUNE_FILE");
+  return f && f[0] ? f : nullptr;
+}
+void tune_file_load_locked() {
+  static bool loaded = false;
+  if (loaded || !tune_file()) return;
+  loaded = true;
+  FILE* fp = fopen(tune_file(), "r");
+  if (!fp) return;
+  char key[512];
+  int v;
+  while (fscanf(fp, "%511s %d", key, &v) == 2) g_tune[key].choice = v;
+  fclose(fp);
+}
 }  // namespace
 
 int tune_choose(const std::string& key, int n, int dflt, cudaEvent_t* ev0, cudaEvent_t* ev1) {
@@ -128,8 +146,9 @@ int tune_choose(const std::string& key, int n, int dflt, cudaEvent_t* ev0, cudaE
   // timed run (robust to a run that shared the GPU with other work)
   constexpr int kRounds = 3;
   std::lock_guard<std::mutex> lk(g_tune_mu);
+  tune_file_load_locked();
   TuneState& t = g_tune[key];
-  if (t.choice >= 0) return t.choice;
+  if (t.choice >= 0) return t.choice < n ? t.choice : dflt;
   if (t.tried < (1 + kRounds) * n) {
     const int v = t.tried % n, round = t.tried / n;
     ++t.tried;
@@ -164,6 +183,12 @@ int tune_choose(const std::string& key, int n, int dflt, cudaEvent_t* ev0, cudaE
   for (cudaEvent_t e : t.ev) cudaEventDestroy(e);
   t.ev.clear();
   t.choice = bv;
+  if (tune_file()) {
+    if (FILE* fp = fopen(tune_file(), "a")) {
+      fprintf(fp, "%s %d\n", key.c_str(), bv);
+      fclose(fp);
+    }
+  }
   return bv;
 }
 

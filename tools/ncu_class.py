@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 TC_KERNELS = ("gemm_tc_kernel", "gemm_tc2_kernel", "conv_tc_kernel", "conv_small_c_kernel", "conv_stem_kernel",
               "conv_wgrad_patch_kernel", "conv_fwd_patch_kernel", "conv_wgrad_stem_kernel",
-              "conv_wgrad_hankel_kernel", "conv_wgrad_hankel2_kernel")
+              "conv_wgrad_hankel_kernel", "conv_wgrad_hankel2_kernel", "conv_wgrad_gather_kernel")
 
 
 def run(cfg_name, out):
