@@ -1356,7 +1356,12 @@ if (p.stats) {  // statistics epilogue: unrolled so the per-chunk sums stay in r
         sm100::tmem_ld_32x32b_x32(ta, r0);
         if (h1) sm100::tmem_ld_32x32b_x32(ta + 32, r1);
         sm100::tmem_ld_wait();
-        if (p.tma_store) {
+        if (p.tma_store && p.ph_st) {
+          // phase store through the 3-D [u][j][c] map: chunk rows m0.. = (u0, j0..)
+          const int m0 = tm * BM + eq * 32, u0 = m0 / p.cQ, j0 = m0 - u0 * p.cQ;
+          epi_tma32(p, epi_smem + ew * 4096, slot, lane, j0, col0, r0, u0);
+          if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, j0, col1, r1, u0);
+        } else if (p.tma_store) {
           epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col0, r0);
           if (h1) epi_tma32(p, epi_smem + ew * 4096, slot, lane, tm * BM + eq * 32, col1, r1);
         } else if (row_ok) {
@@ -4008,9 +4013,32 @@ bool conv_dgrad_phases(const void* dy, const void* w, void* dx, const ConvGeom& 
       t.N = g.N; t.H = g.P; t.W = g.Q; t.C = g.K; t.K = g.C; t.R = cr[rh]; t.S = cs[rw];
       t.stride = 1; t.pad = -dr[rh]; t.P = Hp; t.Q = Wp;
       const int lw = dr[rw], lh = dr[rh];
-      // window starts lower = dmin; base positions per row = Q_in + upper − lower = Wp
-      const int corners[4] = {lw, lh, Wp - g.Q + lw, Hp - g.P + lh};
+      // TMA-store epilogue when the phase rows have a uniform pitch (H % st == 0):
+      // each output row is padded to Qp base positions (a power of two ≤ 32, else a
+      // multiple of 32; the extra positions read only padding → zero rows, clipped
+      // by the store map) so every 32-row epilogue chunk is whole rows / one row piece
+      const bool tma_ph = g.H % st == 0 && Hp * st == g.H;
+      int Qp = Wp;
+      if (tma_ph) { if (Wp <= 32) { Qp = 1; while (Qp < Wp) Qp *= 2; } else Qp = (Wp + 31) / 32 * 32; }
+      t.Q = Qp;
+      // window starts lower = dmin; base positions per row = Q_in + upper − lower = Qp
+      const int corners[4] = {lw, lh, Qp - g.Q + lw, Hp - g.P + lh};
       if (!encode_im2col_4d(&p.ta[1], dy, t, 64, BM, corners)) return false;
+      if (tma_ph) {
+        // dx phase view [u = n·H/st + i][j][c]: strides st·W·C, st·C, 1; box {32 c, bj, 32/bj}
+        const int bj = Qp < 32 ? Qp : 32;
+        cuuint64_t od[3] = {(cuuint64_t)g.C, (cuuint64_t)Wp, (cuuint64_t)g.N * Hp};
+        cuuint64_t os[2] = {(cuuint64_t)st * g.C * 2, (cuuint64_t)st * g.W * g.C * 2};
+        cuuint32_t ob[3] = {32, (cuuint32_t)bj, (cuuint32_t)(32 / bj)};
+        cuuint32_t oe[3] = {1, 1, 1};
+        EncodeFn enc = get_encode();
+        void* base = reinterpret_cast<uint16_t*>(dx) + ((int64_t)rh * g.W + rw) * g.C;
+        if (!enc || enc(&p.td, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, od, os, ob, oe, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return false;
+        p.tma_store = beta == 1.f ? 2 : 1;
+      }
       encode_2d(&p.ta[0], dy, BE_BF16, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, (uint64_t)g.K, 64, 1);
       const int RSC = t.R * t.S * t.C;
       // the phase's taps of W read in place: t_r ↔ r = ρh + pad − st·(dminh + t_r)
