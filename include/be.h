@@ -168,7 +168,11 @@ typedef struct {
   int act;       /* fused activation after the affine (and after the residual add): 0 none, 1 ReLU, 2 ReLU6
                     (MobileNetV2; not with residual) */
   int residual;  /* 1: the LAST input is a residual r (x's shape/dtype): y = act(bn(x) + r) — the ResNet block
-                    output in one pass; r receives the gradient act'(y)·dy */
+                    output in one pass; r receives the gradient act'(y)·dy.
+                    2: the last FIVE inputs are a second batch norm's xr, gamma_r, beta_r, running_mean_r?,
+                    running_var_r? (bf16, xr of x's shape; act 0 or 1): y = act(bn(x) + bn_r(xr)) — the projection
+                    block output with the shortcut's BN applied in the same pass (its output is never stored);
+                    both BNs train-mode with their own statistics; xr, gamma_r, beta_r receive gradients */
 } be_bn_attrs;
 typedef struct { int rank; int64_t shape[6]; } be_shape_attrs;
 typedef struct {

@@ -291,6 +291,17 @@ def batchnorm2d(x, gamma, beta, running_mean=None, running_var=None, eps=1e-5, m
     return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act), int(residual is not None)))
 
 
+def batchnorm2d_add_bn(x, gamma, beta, running_mean, running_var, xr, gamma_r, beta_r, running_mean_r,
+                       running_var_r, eps=1e-5, momentum=0.1, act=1):
+    """act(batchnorm2d(x) + batchnorm2d(xr)) — the ResNet projection block
+    output with the shortcut's BN applied inside the same pass (be_bn_attrs
+    residual = 2): the shortcut's normalised tensor is never written.  Both
+    BNs are train-mode with their own (running) statistics."""
+    ins = [x, gamma, beta] + ([running_mean, running_var] if running_mean is not None else [])
+    ins += [xr, gamma_r, beta_r, running_mean_r, running_var_r]
+    return _op("BATCHNORM2D", ins, L.be_bn_attrs(eps, momentum, int(act), 2))
+
+
 def bn_conv1x1(x, gamma, beta, running_mean, running_var, w, eps=1e-5, momentum=0.1, act=1):
     """conv1x1(act(batchnorm2d(x)), w) with the normalise + activation applied
     inside the GEMM's operand load (BE_OP_BN_CONV1X1): the BN output never

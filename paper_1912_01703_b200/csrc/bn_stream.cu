@@ -454,6 +454,60 @@ __global__ void __launch_bounds__(kThr, 3) bn_apply_stream_kernel(const uint16_t
   }
 }
 
+// y = act(γ·x̂ + β + γr·x̂r + βr): the ResNet projection block output with the
+// shortcut's batch norm applied on the fly (no residual tensor written / read)
+__global__ void __launch_bounds__(kThr, 3) bn_apply2_stream_kernel(const uint16_t* __restrict__ x, uint16_t* y,
+                                                                int64_t rows, int C, const float* __restrict__ mean,
+                                                                const float* __restrict__ invstd,
+                                                                const float* __restrict__ gamma,
+                                                                const float* __restrict__ beta, int act, int64_t rps,
+                                                                const uint16_t* __restrict__ xr,
+                                                                const float* __restrict__ mean_r,
+                                                                const float* __restrict__ invstd_r,
+                                                                const float* __restrict__ gamma_r,
+                                                                const float* __restrict__ beta_r,
+                                                                uint8_t* __restrict__ mbits, int early) {
+  pdl_entry_stream(early);
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int64_t r0 = (int64_t)blockIdx.x * rps, r1 = min(rows, r0 + rps);
+  const int c = (threadIdx.x % (C >> 3)) * 8;
+  float sc[8], sh[8], sr[8];
+  if (threadIdx.x < kCons) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j] = gamma[c + j] * invstd[c + j];
+      const float scr = gamma_r[c + j] * invstd_r[c + j];
+      sr[j] = scr;
+      // both shifts folded into one constant
+      sh[j] = (beta[c + j] - mean[c + j] * sc[j]) + (beta_r[c + j] - mean_r[c + j] * scr);
+    }
+  }
+  const uint16_t* src[2] = {x, xr};
+  stream_rows<2, 2, 4>(src, r0, r1, C, ring, [&](int64_t row, const uint4 (&v)[2]) {
+    float a[8], b[8], o[8];
+    unpack8s(v[0], a);
+    unpack8s(v[1], b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(a[j], sc[j], fmaf(b[j], sr[j], sh[j]));
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = act_apply(o[j], act);
+    }
+    const uint4 pk = pack8s(o);
+    *reinterpret_cast<uint4*>(y + row * C + c) = pk;
+    if (mbits) {
+      const uint32_t w[4] = {pk.x, pk.y, pk.z, pk.w};
+      uint32_t bb = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bb |= ((w[i] & 0xffffu) - 1u < 0x7f80u ? 1u : 0u) << (2 * i);
+        bb |= ((w[i] >> 16) - 1u < 0x7f80u ? 1u : 0u) << (2 * i + 1);
+      }
+      mbits[row * (C >> 3) + (c >> 3)] = (uint8_t)bb;
+    }
+  });
+}
+
 // dx (+)= k1·g' + k2·x + k3 (ACT: the ReLU / ReLU6 mask recomputed from x)
 template <bool ACC, int ACT>
 __global__ void __launch_bounds__(kThr, 3) bn_dx_stream_kernel(const uint16_t* __restrict__ gy,
@@ -697,6 +751,20 @@ void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const 
     launch_pdl(bn_apply_stream_kernel<false>, (unsigned)sp, kThr, kS1, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
                (const uint16_t*)nullptr, mbits, early);
   after_launch("bn_apply_stream");
+}
+
+void bn_apply_stream2(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
+                      const float* gamma, const float* beta, int act, const uint16_t* xr, const float* mean_r,
+                      const float* invstd_r, const float* gamma_r, const float* beta_r, cudaStream_t s,
+                      uint8_t* mbits) {
+  static bool once = [] { set_smem(bn_apply2_stream_kernel, kS2); return true; }();
+  (void)once;
+  const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
+  const int64_t rps = (rows + sp - 1) / sp;
+  // early: x and xr were written before the statistics kernels just launched
+  launch_pdl(bn_apply2_stream_kernel, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps, xr,
+             mean_r, invstd_r, gamma_r, beta_r, mbits, 1);
+  after_launch("bn_apply2_stream");
 }
 
 void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, int64_t rows, int C,

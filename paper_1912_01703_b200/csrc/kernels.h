@@ -156,6 +156,12 @@ void bn_stats(const void* x, int64_t rows, int C, be_dtype dt, float eps, float*
 void bn_apply(const void* x, void* y, int64_t rows, int C, be_dtype dt, const float* mean, const float* invstd,
               const float* gamma, const float* beta, int act, cudaStream_t s, const void* res = nullptr,
               uint8_t* mbits = nullptr, int early = 0);
+// y = act(γ·(x − μ)·is + β + γr·(xr − μr)·isr + βr) — the ResNet projection block output with the
+// shortcut's BN applied in the same pass (bf16 stream path), optional 1-bit mask as bn_apply
+void bn_apply_stream2(const uint16_t* x, uint16_t* y, int64_t rows, int C, const float* mean, const float* invstd,
+                      const float* gamma, const float* beta, int act, const uint16_t* xr, const float* mean_r,
+                      const float* invstd_r, const float* gamma_r, const float* beta_r, cudaStream_t s,
+                      uint8_t* mbits);
 // true when bn_apply can also write the 1-bit ReLU mask of its output (mbits:
 // rows·C/8 bytes, bit j of byte r·C/8 + c/8 ⇔ y[r, c + j] > 0) for bn_bwd's rbits
 bool bn_mask_bits_ok(const void* x, const void* y, const void* res, int64_t rows, int C, be_dtype dt);

@@ -353,16 +353,138 @@ static void vjp_bn(Node* n, GradSink& sink) {
   // when nothing else has been accumulated for it yet
   if (residual && sink.needs((int)n->edges.size() - 1)) sink.give((int)n->edges.size() - 1, std::move(gz));
 }
+// ------------------------------------------------------------------ ResNet projection block output
+// y = act(bn(x) + bn_r(x_r)) in ONE apply pass (be_bn_attrs.residual = 2; the
+// residual branch's BN — the projection shortcut's, act 0 — is applied on the
+// fly instead of being written and re-read as a residual tensor).  Both BNs
+// keep their own statistics / running statistics.  Backward: the main BN's
+// backward with the residual 1-bit mask writes g = dy·1[y > 0], which is then
+// the upstream of the residual BN's backward (exactly the unfused pair's
+// gradients: batchnorm2d(x_r) → batchnorm2d(x, residual) composed).
+static void vjp_bn_add_bn(Node* n, GradSink& sink) {
+  cudaStream_t s = ctx().stream;
+  TRef hx, hmean, hinv, hg, hbits, hb, hxr, hmr, hir, hgr;
+  Tensor* x = unpack(n, 0, hx);
+  Tensor* mean = unpack(n, 1, hmean);
+  Tensor* inv = unpack(n, 2, hinv);
+  Tensor* gamma = unpack(n, 3, hg);
+  Tensor* bits = unpack(n, 4, hbits);
+  Tensor* beta = unpack(n, 5, hb);
+  Tensor* xr = unpack(n, 6, hxr);
+  Tensor* mr = unpack(n, 7, hmr);
+  Tensor* ir = unpack(n, 8, hir);
+  Tensor* gr = unpack(n, 9, hgr);
+  (void)beta;
+  const int act = (int)n->iattr[0];
+  const int C = (int)x->shape[3];
+  const int64_t rows = x->numel() / C;
+  TRef gz = contiguous_like(sink.upstream[0], x->dtype);
+  TRef gmask = act ? new_tensor(x->shape, x->rank, x->dtype) : TRef();
+  // one BN backward: upstream u, input xb → dx into edge ex (gamma/beta edges eg, eb)
+  auto bwd = [&](Tensor* u, Tensor* xb, Tensor* mb, Tensor* ib, Tensor* gb, int ex, int eg, int eb, bool first) {
+    float bg = 0.f, bbt = 0.f;
+    Tensor* dg = sink.needs(eg) ? sink.dest(eg, &bg) : nullptr;
+    Tensor* db = sink.needs(eb) ? sink.dest(eb, &bbt) : nullptr;
+    TRef tg, tb;
+    float gb_beta = 0.f;
+    if (dg && db && bg == bbt) gb_beta = bg;
+    else {
+      if (dg && bg != 0.f) tg = new_tensor({C}, BE_F32);
+      if (db && bbt != 0.f) tb = new_tensor({C}, BE_F32);
+    }
+    TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+    float bx = 0.f;
+    Tensor* dx = sink.needs(ex) ? sink.dest(ex, &bx) : nullptr;
+    TRef dgs = dg ? TRef() : new_tensor({C}, BE_F32);
+    TRef dbs = db ? TRef() : new_tensor({C}, BE_F32);
+    float* dgp = tg ? tg->ptr<float>() : (dg ? dg->ptr<float>() : dgs->ptr<float>());
+    float* dbp = tb ? tb->ptr<float>() : (db ? db->ptr<float>() : dbs->ptr<float>());
+    const bool mask = first && act;
+    k::bn_bwd(u->data(), xb->data(), nullptr, 0, dx ? dx->data() : nullptr, rows, C, xb->dtype, mb->ptr<float>(),
+              ib->ptr<float>(), gb->ptr<float>(), dgp, dbp, gb_beta, bx, part->ptr<float>(), s, nullptr, nullptr,
+              mask ? gmask->data() : nullptr, mask ? bits->ptr<uint8_t>() : nullptr);
+    if (tg) k::axpby(tg->data(), BE_F32, dg->data(), BE_F32, C, 1.f, 1.f, s);
+    if (tb) k::axpby(tb->data(), BE_F32, db->data(), BE_F32, C, 1.f, 1.f, s);
+    if (dx) sink.commit(ex);
+    if (dg) sink.commit(eg);
+    if (db) sink.commit(eb);
+  };
+  bwd(gz.get(), x, mean, inv, gamma, 0, 1, 2, true);
+  if (gmask) gz = std::move(gmask);
+  bwd(gz.get(), xr, mr, ir, gr, 3, 4, 5, false);
+}
+
+static void op_bn_add_bn(const be_tensor* in, int n_in, const be_bn_attrs& a, int nb, be_tensor* out) {
+  Tensor* x = check_handle(in[0]);
+  Tensor* gamma = check_handle(in[1]);
+  Tensor* beta = check_handle(in[2]);
+  Tensor* rm = nb == 5 && in[3] ? check_handle(in[3]) : nullptr;
+  Tensor* rv = nb == 5 && in[4] ? check_handle(in[4]) : nullptr;
+  Tensor* xr = check_handle(in[nb]);
+  Tensor* gr = check_handle(in[nb + 1]);
+  Tensor* br = check_handle(in[nb + 2]);
+  Tensor* rmr = in[nb + 3] ? check_handle(in[nb + 3]) : nullptr;
+  Tensor* rvr = in[nb + 4] ? check_handle(in[nb + 4]) : nullptr;
+  BE_REQUIRE(a.act == 0 || a.act == 1, BE_E_ARG, "batchnorm2d (residual bn): act 0 or 1");
+  BE_REQUIRE(x->rank == 4 && x->is_contiguous() && xr->rank == 4 && xr->is_contiguous(), BE_E_SHAPE,
+             "batchnorm2d: contiguous NHWC inputs");
+  for (int d = 0; d < 4; ++d) BE_REQUIRE(xr->shape[d] == x->shape[d], BE_E_SHAPE, "batchnorm2d: residual shape");
+  BE_REQUIRE(xr->dtype == x->dtype && x->dtype == BE_BF16, BE_E_DTYPE, "batchnorm2d (residual bn): bf16 inputs");
+  const int C = (int)x->shape[3];
+  const int64_t rows = x->numel() / std::max(C, 1);
+  BE_REQUIRE(rows > 0, BE_E_EMPTY_REDUCTION, "batchnorm2d: empty batch");
+  BE_REQUIRE(gamma->numel() == C && beta->numel() == C && gr->numel() == C && br->numel() == C, BE_E_SHAPE,
+             "batchnorm2d: gamma/beta f32 [C]");
+  BE_REQUIRE(k::bn_mask_bits_ok(x->data(), x->data(), xr->data(), rows, C, x->dtype), BE_E_UNSUPPORTED,
+             "batchnorm2d (residual bn): needs the stream path (C % 8 == 0, C <= 2048, 16-B aligned)");
+  cudaStream_t s = ctx().stream;
+  auto stats = [&](Tensor* t, Tensor* m, Tensor* v, TRef& mean, TRef& inv) {
+    mean = new_tensor({C}, BE_F32); inv = new_tensor({C}, BE_F32);
+    TRef part = new_tensor({(int64_t)k::bn_partial_floats(rows, C)}, BE_F32);
+    if (t->bn_stats && t->bn_stats_version == t->version() && t->bn_stats->numel() >= 2LL * t->bn_stats_parts * C)
+      k::bn_stats_from_partials(t->bn_stats->ptr<float>(), t->bn_stats_parts, rows, C, a.eps, mean->ptr<float>(),
+                                inv->ptr<float>(), m ? m->ptr<float>() : nullptr, v ? v->ptr<float>() : nullptr,
+                                a.momentum, s);
+    else
+      k::bn_stats(t->data(), rows, C, t->dtype, a.eps, mean->ptr<float>(), inv->ptr<float>(), part->ptr<float>(),
+                  m ? m->ptr<float>() : nullptr, v ? v->ptr<float>() : nullptr, a.momentum, s);
+    if (m) m->bump_version();
+    if (v) v->bump_version();
+  };
+  TRef mr, ir, mean, inv;
+  stats(xr, rmr, rvr, mr, ir);
+  stats(x, rm, rv, mean, inv);
+  TRef y = new_tensor(x->shape, x->rank, x->dtype);
+  const bool want_grad = grad_enabled() && (x->requires_grad || gamma->requires_grad || beta->requires_grad ||
+                                            xr->requires_grad || gr->requires_grad || br->requires_grad);
+  TRef bits = a.act && want_grad ? new_tensor({rows * (C / 8)}, BE_U8) : TRef();
+  k::bn_apply_stream2(reinterpret_cast<const uint16_t*>(x->data()), reinterpret_cast<uint16_t*>(y->data()), rows, C,
+                      mean->ptr<float>(), inv->ptr<float>(), gamma->ptr<float>(), beta->ptr<float>(), a.act,
+                      reinterpret_cast<const uint16_t*>(xr->data()), mr->ptr<float>(), ir->ptr<float>(),
+                      gr->ptr<float>(), br->ptr<float>(), s, bits ? bits->ptr<uint8_t>() : nullptr);
+  Node* n = new_node("batchnorm2d_add_bn", BE_OP_BATCHNORM2D, vjp_bn_add_bn, {x, gamma, beta, xr, gr, br});
+  if (n) {
+    save(n, x); save(n, mean.get()); save(n, inv.get()); save(n, gamma); save(n, bits ? bits.get() : nullptr);
+    save(n, beta); save(n, xr); save(n, mr.get()); save(n, ir.get()); save(n, gr);
+    n->iattr[0] = a.act;
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
+  out[0] = reinterpret_cast<be_tensor>(y.release());
+}
+
 static void op_bn(const be_tensor* in, int n_in, const void* attrs, be_tensor* out) {
   be_bn_attrs a{1e-5f, 0.1f, 0, 0};
   if (attrs) a = *reinterpret_cast<const be_bn_attrs*>(attrs);
-  const int nb = n_in - (a.residual ? 1 : 0);
+  BE_REQUIRE(a.residual >= 0 && a.residual <= 2, BE_E_ARG, "batchnorm2d: residual 0, 1 or 2");
+  const int nb = n_in - (a.residual == 1 ? 1 : (a.residual == 2 ? 5 : 0));
   BE_REQUIRE(nb == 3 || nb == 5, BE_E_ARG, "batchnorm2d: x, gamma, beta[, running_mean, running_var][, residual]");
   Tensor* x = check_handle(in[0]);
   Tensor* gamma = check_handle(in[1]);
   Tensor* beta = check_handle(in[2]);
   Tensor* rm = nb == 5 && in[3] ? check_handle(in[3]) : nullptr;
   Tensor* rv = nb == 5 && in[4] ? check_handle(in[4]) : nullptr;
+  if (a.residual == 2) { op_bn_add_bn(in, n_in, a, nb, out); return; }
   Tensor* res = a.residual ? check_handle(in[n_in - 1]) : nullptr;
   BE_REQUIRE(a.act >= 0 && a.act <= 2, BE_E_ARG, "batchnorm2d: act 0 (none), 1 (ReLU) or 2 (ReLU6)");
   BE_REQUIRE(!(res && a.act == 2), BE_E_UNSUPPORTED, "batchnorm2d: ReLU6 after a residual add");

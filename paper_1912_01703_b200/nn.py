@@ -216,10 +216,14 @@ class ResNet50(Model):
     TMA-store staging tile, and the layer-1 3×3 shared-patch kernel carries
     them too — C4 +0.7 % over the separate statistics pass."""
 
-    def __init__(self, layers=(3, 4, 6, 3), base=64, classes=1000, bn_stats=True, fuse_bn_conv=False):
+    def __init__(self, layers=(3, 4, 6, 3), base=64, classes=1000, bn_stats=True, fuse_bn_conv=False,
+                 fuse_shortcut_bn=True):
         super().__init__()
         self.layers, self.base, self.classes = tuple(layers), base, classes
         self.bn_stats = bn_stats
+        # fuse_shortcut_bn (bf16): projection blocks' output relu(bn3 + dsbn(ds)) in one
+        # pass (api.batchnorm2d_add_bn)
+        self.fuse_shortcut_bn = fuse_shortcut_bn
         # fuse_bn_conv=True: bn2 + ReLU applied inside c3's operand load
         # (BE_OP_BN_CONV1X1, bf16 mode) — the bn2 output never reaches HBM and
         # the step needs 0.7 GB less memory, but the two transform warps throttle
@@ -275,12 +279,14 @@ class ResNet50(Model):
         h = bn(h, "bn1", 1)
         h = T.maxpool2d(h, 3, 2, 1)
         fuse = self.fuse_bn_conv and x.dtype == T.L.BE_BF16 and not self.bn_stats
+        fuse_sc = self.fuse_shortcut_bn and x.dtype == T.L.BE_BF16
         for (n, cin, mid, cout, stride, down) in self.blocks():
             # the projection shortcut first: the engine runs the later-recorded
             # c1 branch's backward first, so c1's dgrad writes dL/dh in full
             # (beta 0) and the stride-2 projection's phase dgrad only adds into
             # its one live phase (no zero fill of the other three)
-            idn = bn(conv(h, n + ".ds.w", stride, 0), n + ".dsbn", 0) if down else h
+            yds = conv(h, n + ".ds.w", stride, 0) if down else None
+            idn = None if down and fuse_sc else (bn(yds, n + ".dsbn", 0) if down else h)
             t = bn(conv(h, n + ".c1.w", 1, 0), n + ".bn1", 1)
             t = conv(t, n + ".c2.w", stride, 1)
             if fuse:  # c3(relu(bn2(t))) — the bn2 output is only ever built in c3's operand tiles
@@ -288,8 +294,15 @@ class ResNet50(Model):
                                  P[n + ".c3.w"], act=1)
             else:
                 u = conv(bn(t, n + ".bn2", 1), n + ".c3.w", 1, 0)
-            # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN)
-            h = bn(u, n + ".bn3", 1, residual=idn)
+            # block output relu(bn3(c3) + shortcut) in one pass (fused residual BN);
+            # projection blocks: relu(bn3(c3) + dsbn(ds)) with the shortcut's BN
+            # applied inside that pass (its output never written)
+            if idn is None:
+                h = T.batchnorm2d_add_bn(u, P[n + ".bn3.g"], P[n + ".bn3.b"], B[n + ".bn3.rm"], B[n + ".bn3.rv"],
+                                         yds, P[n + ".dsbn.g"], P[n + ".dsbn.b"], B[n + ".dsbn.rm"],
+                                         B[n + ".dsbn.rv"], act=1)
+            else:
+                h = bn(u, n + ".bn3", 1, residual=idn)
         h = T.avgpool_global(h)
         z = T.linear(h, P["fc.w"], P["fc.b"], out_f32=True)
         return T.softmax_xent(z, y)

@@ -59,7 +59,8 @@ class OpTrace:
     """Wraps the api ops a model calls (be.nn uses the module global `T`)."""
 
     OPS = ("conv2d", "batchnorm2d", "maxpool2d", "avgpool_global", "reshape", "linear", "softmax_xent",
-           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_depthwise", "bn_conv1x1")
+           "embedding", "mul", "concat", "bce_logits", "add_relu", "dropout", "conv2d_depthwise", "bn_conv1x1",
+           "batchnorm2d_add_bn")
 
     def __init__(self, api, model):
         self.api = api
@@ -293,6 +294,48 @@ class Replay:
         if bo is not None:
             og["b"] = bo.grad
         self._finish(i, rec, L, og, ["x", "w", "b"])
+
+    def _op_batchnorm2d_add_bn(self, i, rec):
+        """act(bn(x) + bn_r(xr)) (the projection block output with the shortcut's
+        BN fused into the apply): oracle = the two batchnorm2d's composed."""
+        be, a = self.be, rec["args"]
+        names = ["x", "gamma", "beta", "xr", "gamma_r", "beta_r"]
+        L = self._dev_inputs(rec, names)
+        stats = {}
+        for sfx in ("", "_r"):
+            rm0, rv0 = self._val(a["running_mean" + sfx]), self._val(a["running_var" + sfx])
+            stats[sfx] = (rm0, rv0, be.tensor(rm0), be.tensor(rv0))
+        y = be.batchnorm2d_add_bn(L["x"][1], L["gamma"][1], L["beta"][1], stats[""][2], stats[""][3],
+                                  L["xr"][1], L["gamma_r"][1], L["beta_r"][1], stats["_r"][2], stats["_r"][3],
+                                  eps=a["eps"], momentum=a["momentum"], act=a["act"])
+        V = {n: Var((nhwc_to_nchw(self._val(a[n])) if n in ("x", "xr") else self._val(a[n])).astype(F64), True)
+             for n in names}
+        z1, (rm, rv) = oops.batchnorm2d(V["x"], V["gamma"], V["beta"], eps=a["eps"], momentum=a["momentum"],
+                                        running_mean=stats[""][0].astype(F64), running_var=stats[""][1].astype(F64))
+        z2, (rmr, rvr) = oops.batchnorm2d(V["xr"], V["gamma_r"], V["beta_r"], eps=a["eps"], momentum=a["momentum"],
+                                          running_mean=stats["_r"][0].astype(F64),
+                                          running_var=stats["_r"][1].astype(F64))
+        zo = oops.add(z1, z2)
+        ydev = y.numpy()
+        self.record(i, "batchnorm2d_add_bn", "y", nhwc_to_nchw(ydev), _act(zo.value, a["act"]))
+        for sfx, (rmo, rvo) in (("", (rm, rv)), ("_r", (rmr, rvr))):
+            self.record(i, "batchnorm2d_add_bn", "running_mean" + sfx, stats[sfx][2].numpy(), rmo)
+            self.record(i, "batchnorm2d_add_bn", "running_var" + sfx, stats[sfx][3].numpy(), rvo)
+        g = self._g_out(rec)
+        if not self._dev_backward(y, g, rec):
+            return
+        gn = nhwc_to_nchw(np.asarray(g).reshape(ydev.shape))
+        if a["act"]:
+            gn = gn * _act_mask(nhwc_to_nchw(ydev), a["act"])
+        backward(zo, gn)
+        og = {n: (nchw_to_nhwc(V[n].grad) if n in ("x", "xr") else V[n].grad) for n in names}
+        masses = {}
+        for sfx, xn in (("", "x"), ("_r", "xr")):
+            xv = nhwc_to_nchw(self._val(a[xn])).astype(F64)
+            xhat = (xv - xv.mean(axis=(0, 2, 3), keepdims=True)) / np.sqrt(xv.var(axis=(0, 2, 3), keepdims=True) + a["eps"])
+            masses["beta" + sfx] = np.abs(gn).sum(axis=(0, 2, 3)).max()
+            masses["gamma" + sfx] = np.abs(gn * xhat).sum(axis=(0, 2, 3)).max()
+        self._finish(i, rec, L, og, names, masses=masses)
 
     def _op_batchnorm2d(self, i, rec):
         be, a = self.be, rec["args"]
@@ -621,6 +664,12 @@ def forward_drift(be, trace: OpTrace):
             if a["residual"] is not None:
                 y = y + nhwc_to_nchw(val(a["residual"]))
             y = nchw_to_nhwc(_act(y, a["act"]))
+        elif op == "batchnorm2d_add_bn":
+            y1, _ = oops.batchnorm2d(Var(nhwc_to_nchw(val(a["x"]))), Var(val(a["gamma"])), Var(val(a["beta"])),
+                                     eps=a["eps"])
+            y2, _ = oops.batchnorm2d(Var(nhwc_to_nchw(val(a["xr"]))), Var(val(a["gamma_r"])), Var(val(a["beta_r"])),
+                                     eps=a["eps"])
+            y = nchw_to_nhwc(_act(y1.value + y2.value, a["act"]))
         elif op == "maxpool2d":
             yv, am = oops.maxpool2d(Var(nhwc_to_nchw(val(a["x"]))), a["k"], a["stride"], a["pad"])
             y = nchw_to_nhwc(yv.value)

@@ -370,3 +370,51 @@ def test_bn_fused_residual(dt, C, act):
     assert rel(tb(xd.grad.numpy()), xo.grad) < tol
     assert rel(tb(rd.grad.numpy()), ro.grad) < tol
     assert rel(gd.grad.numpy(), go.grad) < tol and rel(bd.grad.numpy(), bo.grad) < tol
+
+
+@pytest.mark.parametrize("C,act,N,H", [(64, 1, 4, 9), (256, 1, 2, 14), (24, 0, 3, 7), (2048, 1, 2, 7)])
+def test_bn_add_bn(C, act, N, H):
+    """batchnorm2d_add_bn: act(bn(x) + bn_r(xr)) — the projection block output
+    with the shortcut's BN applied in the same pass — vs the oracle's
+    composition relu(add(bn(x), bn(xr))), forward (output and both BNs'
+    running statistics) and backward (dx, dxr and the four affine gradients).
+    bf16 inputs on both sides, fp32 arithmetic, one rounding → 1e-2."""
+    be = be_init()
+    be.set_compute_dtype("bf16")
+    from paper_1912_01703_b200.api import f32_to_bf16_bits, bf16_bits_to_f32
+    from oracle.autograd import Var, backward
+    q = lambda a: bf16_bits_to_f32(f32_to_bf16_bits(np.asarray(a, np.float32)))
+    t = lambda a: np.ascontiguousarray(np.asarray(a).transpose(0, 2, 3, 1))
+    tb = lambda a: np.ascontiguousarray(np.asarray(a).transpose(0, 3, 1, 2))
+    rng = np.random.default_rng(C + act + H)
+    x = q(rng.standard_normal((N, C, H, H)) * 1.5 + 0.3)
+    xr = q(rng.standard_normal((N, C, H, H)) * 0.7 - 0.2)
+    p = [(rng.standard_normal(C) * 0.3 + 1).astype(np.float32), (rng.standard_normal(C) * 0.3).astype(np.float32),
+         (rng.standard_normal(C) * 0.3 + 1).astype(np.float32), (rng.standard_normal(C) * 0.3).astype(np.float32)]
+    rm0 = [(rng.standard_normal(C) * 0.1).astype(np.float32) for _ in range(2)]
+    rv0 = [(rng.random(C) + 0.5).astype(np.float32) for _ in range(2)]
+    xo, xro = Var(x.astype(np.float64), True), Var(xr.astype(np.float64), True)
+    po = [Var(a.astype(np.float64), True) for a in p]
+    y1, (rm1, rv1) = oops.batchnorm2d(xo, po[0], po[1], running_mean=rm0[0].astype(np.float64),
+                                      running_var=rv0[0].astype(np.float64))
+    y2, (rm2, rv2) = oops.batchnorm2d(xro, po[2], po[3], running_mean=rm0[1].astype(np.float64),
+                                      running_var=rv0[1].astype(np.float64))
+    zo = oops.add(y1, y2)
+    if act:
+        zo = oops.relu(zo)
+    xd, xrd = be.tensor(t(x), requires_grad=True), be.tensor(t(xr), requires_grad=True)
+    pd = [be.tensor(a, requires_grad=True) for a in p]
+    rmd = [be.tensor(a) for a in rm0]
+    rvd = [be.tensor(a) for a in rv0]
+    zd = be.batchnorm2d_add_bn(be.cast(xd, "bf16"), pd[0], pd[1], rmd[0], rvd[0], be.cast(xrd, "bf16"), pd[2], pd[3],
+                               rmd[1], rvd[1], act=act)
+    assert rel(tb(zd.numpy()), zo.value) < 1e-2
+    for dev, orc in ((rmd[0], rm1), (rvd[0], rv1), (rmd[1], rm2), (rvd[1], rv2)):
+        assert rel(dev.numpy(), orc) < 1e-3
+    g = q(rng.standard_normal(zo.value.shape))
+    backward(zo, g.astype(np.float64))
+    zd.backward(be.tensor(t(g), dtype="bf16"))
+    assert rel(tb(xd.grad.numpy()), xo.grad) < 1e-2
+    assert rel(tb(xrd.grad.numpy()), xro.grad) < 1e-2
+    for dev, orc in zip(pd, po):
+        assert rel(dev.grad.numpy(), orc.grad) < 1e-2
