@@ -1317,8 +1317,9 @@ __global__ void __launch_bounds__(256) maxpool_bwd_rows(const uint16_t* __restri
   }
   *reinterpret_cast<uint4*>(dx + o) = pack8(acc);
 }
-// ---- max-pool backward for the 3×3 / stride-2 / pad-1 pool (ResNet's), one
-// thread per 2×2 quad of input pixels h ∈ {2i−1, 2i}, w ∈ {2j−1, 2j}: the
+// ---- max-pool backward for the 3×3 / stride-2 pools (pad 1: ResNet's; pad 0:
+// AlexNet's), one thread per 2×2 quad of input pixels h ∈ {2i−pad, 2i−pad+1}
+// (likewise w): the
 // quad's pixels are reached only by the windows (p, q) ∈ {i−1, i} × {j−1, j},
 // whose (dy, argmax) pairs are loaded once for all four pixels (the per-pixel
 // kernel loads ≤ 4 pairs per pixel and was issue-bound).  Each pixel sums
@@ -1351,11 +1352,11 @@ __global__ void __launch_bounds__(256) maxpool_bwd_quad(const uint16_t* __restri
     }
 #pragma unroll
   for (int dh = 0; dh < 2; ++dh) {
-    const int h = 2 * i - 1 + dh;
+    const int h = 2 * i - g.pad + dh;
     if (h < 0 || h >= g.H) continue;
 #pragma unroll
     for (int dw = 0; dw < 2; ++dw) {
-      const int w = 2 * j - 1 + dw;
+      const int w = 2 * j - g.pad + dw;
       if (w < 0 || w >= g.W) continue;
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       // windows reaching (h, w): odd h (dh = 0) ← p = i − 1 (r = 2), p = i (r = 0);
@@ -1387,6 +1388,53 @@ __global__ void __launch_bounds__(256) maxpool_bwd_quad(const uint16_t* __restri
         for (int k = 0; k < 8; ++k) acc[k] += old[k];
       }
       *reinterpret_cast<uint4*>(dx + o) = pack8(acc);
+    }
+  }
+}
+// ---- max-pool backward for the 2×2 / stride-2 / pad-0 pool (VGG's): windows do
+// not overlap, so one thread per window (8 channels) loads its (dy, index)
+// once and writes the window's 4 input pixels (the winner gets dy, the rest
+// +0 — the per-pixel kernel's result, each pixel reached by one window)
+__global__ void __launch_bounds__(256) maxpool_bwd_2x2(const uint16_t* __restrict__ dy,
+                                                       const uint8_t* __restrict__ am, uint16_t* __restrict__ dx,
+                                                       ConvGeom g, float beta) {
+  pdl_entry();
+  const int cv = threadIdx.x;
+  const int q = blockIdx.x * blockDim.y + threadIdx.y;
+  if (q >= g.Q) return;
+  const int n = blockIdx.z, p = blockIdx.y;
+  const int64_t o = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cv * 8;
+  const uint4 d = __ldg(reinterpret_cast<const uint4*>(dy + o));
+  const uint2 pk = __ldg(reinterpret_cast<const uint2*>(am + o));
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int h = 2 * p + a;
+    if (h >= g.H) continue;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int w = 2 * q + b;
+      if (w >= g.W) continue;
+      const uint32_t tap = (uint32_t)(a * 2 + b) * 0x01010101u;
+      const uint32_t m0 = __vcmpeq4(pk.x, tap), m1 = __vcmpeq4(pk.y, tap);
+      uint4 v = d;
+      v.x &= __byte_perm(m0, 0, 0x1100); v.y &= __byte_perm(m0, 0, 0x3322);
+      v.z &= __byte_perm(m1, 0, 0x1100); v.w &= __byte_perm(m1, 0, 0x3322);
+      const int64_t od = (((int64_t)n * g.H + h) * g.W + w) * g.C + cv * 8;
+      if (beta != 0.f) {
+        float f[8], old[8];
+        unpack8(v, f);
+        unpack8(*reinterpret_cast<const uint4*>(dx + od), old);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = old[k] + f[k];
+        *reinterpret_cast<uint4*>(dx + od) = pack8(f);
+      } else {
+        float f[8];
+        unpack8(v, f);
+        float z[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z[k] = 0.f + f[k];  // as the gather kernel: +0 accumulator, one rounding
+        *reinterpret_cast<uint4*>(dx + od) = pack8(z);
+      }
     }
   }
 }
@@ -1500,9 +1548,18 @@ void maxpool_bwd(const void* dy, const uint8_t* am, void* dx, const ConvGeom& g,
       aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(am) & 7) == 0) {
     const int cvn = g.C / 8, wpb = std::max(1, 256 / cvn);
     static const int quad_on = [] { const char* e = getenv("BE_MAXPOOL_QUAD"); return e ? atoi(e) : 1; }();
-    if (quad_on && g.R == 3 && g.S == 3 && g.stride == 2 && g.pad == 1 && (g.H + 1) / 2 <= g.P + 1 &&
-        (g.W + 1) / 2 <= g.Q + 1) {
-      // quads i ∈ [0, P], j ∈ [0, Q] cover h ≤ 2P, w ≤ 2Q (⊇ [0, H) × [0, W))
+    if (quad_on && g.R == 2 && g.S == 2 && g.stride == 2 && g.pad == 0 && g.H <= 2 * g.P + 1 && g.W <= 2 * g.Q + 1) {
+      // non-overlapping 2×2 windows (pixels past the last window get 0: H odd)
+      if (beta == 0.f && (g.H > 2 * g.P || g.W > 2 * g.Q))
+        BE_CHECK_CUDA(cudaMemsetAsync(dx, 0, sizeof(uint16_t) * (size_t)total, s));
+      dim3 g2((g.Q + wpb - 1) / wpb, g.P, g.N), b2(cvn, wpb);
+      launch_pdl(maxpool_bwd_2x2, g2, b2, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
+      after_launch("maxpool_bwd_2x2");
+      return;
+    }
+    if (quad_on && g.R == 3 && g.S == 3 && g.stride == 2 && (g.pad == 1 || g.pad == 0) && g.H <= 2 * g.P + 2 - g.pad &&
+        g.W <= 2 * g.Q + 2 - g.pad) {
+      // quads i ∈ [0, P], j ∈ [0, Q] cover h ∈ [−pad, 2P − pad + 1] (⊇ [0, H))
       dim3 gq((g.Q + 1 + wpb) / wpb, g.P + 1, g.N), bq(cvn, wpb);
       launch_pdl(maxpool_bwd_quad, gq, bq, 0, s, (const uint16_t*)dy, am, (uint16_t*)dx, g, beta);
       after_launch("maxpool_bwd_quad");
