@@ -108,6 +108,16 @@ __device__ __forceinline__ Pk<BF> ldpk(const void* p, int64_t i, bool ok) {
   }
   return r;
 }
+// packed fp32 FMA (sm_100 FFMA2): two independent IEEE fp32 FMAs per
+// instruction — per lane exactly fmaf's result, half the FMA issue slots
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  uint64_t d, a, b;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
 template <bool BF>
 __device__ __forceinline__ void stpk(void* p, int64_t i, const float (&o)[8]) {
   V8 v;
@@ -143,11 +153,11 @@ __global__ void __launch_bounds__(256) dw_fwd_kernel(const void* __restrict__ x,
       }
     float o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float a = 0.f;
+    for (int j = 0; j < 8; j += 2) {
+      float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-      for (int t = 0; t < 9; ++t) a = fmaf(v[t][j], wr[t][j], a);
-      o[j] = a;
+      for (int t = 0; t < 9; ++t) ffma2(a0, a1, v[t][j], v[t][j + 1], wr[t][j], wr[t][j + 1]);
+      o[j] = a0; o[j + 1] = a1;
     }
     stpk<BF>(y, pix * g.C + c, o);
   }
@@ -186,11 +196,11 @@ __global__ void __launch_bounds__(256) dw_dgrad_kernel(const void* __restrict__ 
     }
     float o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float a = 0.f;
+    for (int j = 0; j < 8; j += 2) {
+      float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-      for (int t = 0; t < 9; ++t) a = fmaf(v[t][j], wr[t][j], a);
-      o[j] = a;
+      for (int t = 0; t < 9; ++t) ffma2(a0, a1, v[t][j], v[t][j + 1], wr[t][j], wr[t][j + 1]);
+      o[j] = a0; o[j + 1] = a1;
     }
     if (beta != 0.f) {
       const Pk<BF> prev = ldpk<BF>(dx, pix * g.C + c, true);
@@ -238,10 +248,10 @@ __global__ void __launch_bounds__(256) dw_wgrad_partial_kernel(const void* __res
           v[r * 3 + s2] = ldpk<BF>(x, base + ((int64_t)r * g.W + s2) * g.C, ok);
         }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float gj = gv[j];
+      for (int j = 0; j < 8; j += 2) {
+        const float g0 = gv[j], g1 = gv[j + 1];
 #pragma unroll
-        for (int t = 0; t < 9; ++t) acc[t][j] = fmaf(gj, v[t][j], acc[t][j]);
+        for (int t = 0; t < 9; ++t) ffma2(acc[t][j], acc[t][j + 1], g0, g1, v[t][j], v[t][j + 1]);
       }
     }
     float* mine = red + ((int64_t)pl * C8 + c8) * 72;
