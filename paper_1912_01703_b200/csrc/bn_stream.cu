@@ -81,12 +81,17 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
   const int iterb = rpi * C * 2;                    // bytes per iteration (4 KB when C | 2048)
   const int64_t crow = (int64_t)ITERS * rpi;
   const int64_t nchunks = r1 > r0 ? (r1 - r0 + crow - 1) / crow : 0;
-  if (t == 0) {
-    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], kCons / 32); }
-    sm100::fence_barrier_init();
-  }
-  __syncthreads();
   if (warp == kCons / 32) {
+    // the producer initialises the ring barriers and signals the consumers
+    // through named barrier 1 WITHOUT waiting for them (bar.arrive): with the
+    // PDL early start its copies begin while the consumers are still in
+    // griddepcontrol.wait
+    if (lane == 0) {
+      for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], kCons / 32); }
+      sm100::fence_barrier_init();
+    }
+    __syncwarp();
+    asm volatile("bar.arrive 1, %0;" ::"n"(kThr) : "memory");
     if (lane == 0) {
       for (int64_t i = 0; i < nchunks; ++i) {
         const int st = (int)(i % NST);
@@ -109,6 +114,7 @@ __device__ __forceinline__ void stream_rows(const uint16_t* const (&src)[NS], in
     }
     return;
   }
+  asm volatile("bar.sync 1, %0;" ::"n"(kThr) : "memory");
   const int rin = t / lanes;
   const bool active = rin < rpi;
   for (int64_t i = 0; i < nchunks; ++i) {
@@ -163,6 +169,10 @@ __device__ __forceinline__ void combine_partials(const float (&s0)[8], const flo
 __device__ __forceinline__ void pdl_entry_stream(int early) {
   if (!(early && threadIdx.x >= kCons)) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+int early_on() {
+  static const int on = [] { const char* e = getenv("BE_PDL_EARLY"); return e ? atoi(e) : 1; }();
+  return on;
 }
 
 }  // namespace
@@ -746,10 +756,10 @@ void bn_apply_stream(const uint16_t* x, uint16_t* y, int64_t rows, int C, const 
   const int64_t rps = (rows + sp - 1) / sp;
   if (res)
     launch_pdl(bn_apply_stream_kernel<true>, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-               res, mbits, early);
+               res, mbits, early && early_on());
   else
     launch_pdl(bn_apply_stream_kernel<false>, (unsigned)sp, kThr, kS1, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps,
-               (const uint16_t*)nullptr, mbits, early);
+               (const uint16_t*)nullptr, mbits, early && early_on());
   after_launch("bn_apply_stream");
 }
 
@@ -763,7 +773,7 @@ void bn_apply_stream2(const uint16_t* x, uint16_t* y, int64_t rows, int C, const
   const int64_t rps = (rows + sp - 1) / sp;
   // early: x and xr were written before the statistics kernels just launched
   launch_pdl(bn_apply2_stream_kernel, (unsigned)sp, kThr, kS2, s, x, y, rows, C, mean, invstd, gamma, beta, act, rps, xr,
-             mean_r, invstd_r, gamma_r, beta_r, mbits, 1);
+             mean_r, invstd_r, gamma_r, beta_r, mbits, early_on());
   after_launch("bn_apply2_stream");
 }
 
@@ -784,7 +794,8 @@ void bn_dx_stream(const uint16_t* gy, const uint16_t* x, int act, uint16_t* dx, 
   const int64_t sp = bn_stream_splits(rows, C, 1 << 30);
   const int64_t rps = (rows + sp - 1) / sp;
   auto go = [&](auto kern, int smem) {
-    launch_pdl(kern, (unsigned)sp, kThr, smem, s, gy, x, dx, rows, C, mean, invstd, gamma, sums, rps, bsh, early);
+    launch_pdl(kern, (unsigned)sp, kThr, smem, s, gy, x, dx, rows, C, mean, invstd, gamma, sums, rps, bsh,
+               early && early_on());
   };
   if (dx_beta != 0.f) {
     if (act == 1) go(bn_dx_stream_kernel<true, 1>, kS3);
