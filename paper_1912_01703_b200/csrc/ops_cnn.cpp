@@ -698,6 +698,24 @@ static void vjp_embedding(Node* n, GradSink& sink) {
     B *= R;
     scale = 1.f / (float)R;
   }
+  // the (id, position) sort issued at forward time on the sort stream (R = 1):
+  // the compute stream waits for it here (its event is re-recorded after every
+  // sort on an in-order stream, so the latest record covers this one)
+  if (R == 1 && n->saved.size() > 1) {
+    TRef hs;
+    Tensor* pre = unpack(n, 1, hs);
+    if (pre && n->iattr[0] == V) {
+      BE_CHECK_CUDA(cudaStreamWaitEvent(ctx().stream, ctx().sort_done, 0));
+      if (sparse) {
+        k::embedding_sgd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), slr, scale, pre->data(), ctx().stream);
+        sink.fused_sparse(0);
+        return;
+      }
+      k::embedding_bwd_sorted(gz->data(), gz->dtype, B, D, dt->ptr<float>(), V, beta, pre->data(), ctx().stream);
+      sink.commit(0);
+      return;
+    }
+  }
   // Tables looked up with the same ids (NeuMF: GMF and MLP tables of a side)
   // share one sort: a small cache keyed by the ids storage, its version and V
   // (several entries: backward visits the user and item tables interleaved).
@@ -755,7 +773,38 @@ static void op_embedding(const be_tensor* in, int n_in, be_tensor* out) {
   TRef y = new_tensor({B, D}, od);
   k::embedding_fwd(t->ptr<float>(), D, ids->ptr<int32_t>(), B, y->data(), od, ctx().stream);
   Node* n = new_node("embedding", BE_OP_EMBEDDING, vjp_embedding, {t});
-  if (n) { save(n, ids); set_output(n, y.get(), 0); finish_node(n); }
+  if (n) {
+    save(n, ids);
+    // the backward's (id, position) sort depends only on ids: issue it now on a
+    // low-priority side stream so it overlaps the rest of the step instead of
+    // sitting on the backward's critical path (single replica: with R > 1 the
+    // backward sorts the all-gathered lookups)
+    static const int pre_on = [] { const char* e = getenv("BE_EMB_PRESORT"); return e ? atoi(e) : 1; }();
+    if (pre_on && ddp_world() == 1 && B > 0 && B < (1LL << 31)) {
+      Context& c = ctx();
+      if (!c.sort_stream) {
+        int least = 0, greatest = 0;
+        BE_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        BE_CHECK_CUDA(cudaStreamCreateWithPriority(&c.sort_stream, cudaStreamNonBlocking, least));
+        BE_CHECK_CUDA(cudaEventCreateWithFlags(&c.sort_done, cudaEventDisableTiming));
+      }
+      const size_t sb = k::embedding_bwd_scratch(B);
+      TRef scratch = new_tensor({(int64_t)((sb + 3) / 4)}, BE_F32);
+      cudaEvent_t ready;
+      BE_CHECK_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      BE_CHECK_CUDA(cudaEventRecord(ready, c.stream));  // ids written, scratch allocated
+      BE_CHECK_CUDA(cudaStreamWaitEvent(c.sort_stream, ready, 0));
+      BE_CHECK_CUDA(cudaEventDestroy(ready));
+      k::embedding_sort(ids->ptr<int32_t>(), B, t->shape[0], scratch->data(), c.sort_stream);
+      BE_CHECK_CUDA(cudaEventRecord(c.sort_done, c.sort_stream));
+      if (scratch->storage->block) c.alloc.record_stream(scratch->storage->block, c.sort_stream);
+      if (ids->storage->block) c.alloc.record_stream(ids->storage->block, c.sort_stream);
+      save(n, scratch.get());
+      n->iattr[0] = t->shape[0];
+    }
+    set_output(n, y.get(), 0);
+    finish_node(n);
+  }
   out[0] = reinterpret_cast<be_tensor>(y.release());
 }
 

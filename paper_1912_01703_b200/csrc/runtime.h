@@ -274,6 +274,8 @@ struct Context {
   bool own_stream = false;
   cudaStream_t comm_stream = nullptr;
   cudaStream_t opt_stream = nullptr;   // overlapped SGD
+  cudaStream_t sort_stream = nullptr;  // embedding id sorts issued at forward time
+  cudaEvent_t sort_done = nullptr;     // re-recorded after every sort (the stream is in order)
   be_dtype compute = BE_F32;
   bool sync_mode = false;
   CachingAllocator alloc;
