@@ -418,3 +418,43 @@ def test_bn_add_bn(C, act, N, H):
     assert rel(tb(xrd.grad.numpy()), xro.grad) < 1e-2
     for dev, orc in zip(pd, po):
         assert rel(dev.grad.numpy(), orc.grad) < 1e-2
+
+
+_TUNE_SCRIPT = r'''
+import sys, json
+sys.path[:0] = [{root!r}, {root!r} + "/tests"]
+import numpy as np
+import paper_1912_01703_b200 as be
+be.init(0)
+be.set_compute_dtype("bf16")
+rng = np.random.default_rng(0)
+x = be.tensor(rng.standard_normal((2, 14, 14, 256)).astype(np.float32), dtype="bf16")
+w = be.tensor((rng.standard_normal((256, 3, 3, 256)) / 48).astype(np.float32), requires_grad=True)
+g = be.tensor(rng.standard_normal((2, 14, 14, 256)).astype(np.float32), dtype="bf16")
+outs = []
+for _ in range(30):  # past every candidate's tuning rounds (≤ 5 variants × 4 rounds)
+    be.zero_grad([w])
+    y = be.conv2d(x, w, None, 1, 1)
+    y.backward(g)
+    outs.append(float(np.abs(w.grad.numpy()).sum()))
+print(json.dumps({{"last": outs[-1]}}))
+'''
+
+
+def test_tune_file_replay(tmp_path):
+    """BE_TUNE_FILE: a first process records its autotuning decisions, a second
+    replays them without timing (no new lines) and computes the same result —
+    the mechanism that keeps profiled runs on the unprofiled run's kernels."""
+    tf = tmp_path / "tune.txt"
+    env = dict(os.environ, BE_TUNE_FILE=str(tf))
+    outs = []
+    for _ in range(2):
+        r = subprocess.run([sys.executable, "-c", _TUNE_SCRIPT.format(root=ROOT)], capture_output=True, text=True,
+                           env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1])["last"])
+        if len(outs) == 1:
+            first = tf.read_text().splitlines()
+            assert first and all(len(line.split()) == 2 for line in first)
+    assert tf.read_text().splitlines() == first  # the second run decided nothing new
+    assert outs[0] == outs[1]
