@@ -1625,25 +1625,33 @@ __global__ void avgpool_fwd_v8(const uint16_t* __restrict__ x, uint16_t* __restr
     *reinterpret_cast<uint4*>(y + (int64_t)n * C + cv * 8) = pack8(o);
   }
 }
-// bf16, C % 8 == 0: one thread per 8 channels of one pixel (16-B load / store)
+// bf16, C % 8 == 0: one thread per (image, 8-channel vector) loads dy once and
+// writes it (÷ HW) to the HW pixels (16-B stores; consecutive threads take
+// consecutive channel vectors, so each pixel row is written coalesced)
 __global__ void avgpool_bwd_v8(const uint16_t* __restrict__ dy, uint16_t* __restrict__ dx, int HW, int C, float beta,
                                uint32_t total) {
   pdl_entry();
-  const uint32_t CV = (uint32_t)C / 8, per_n = (uint32_t)HW * CV;
+  const uint32_t CV = (uint32_t)C / 8;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const uint32_t n = t / per_n, cv = t % CV;
+    const uint32_t n = t / CV, cv = t - n * CV;
     float v[8];
     unpack8(__ldg(reinterpret_cast<const uint4*>(dy + (int64_t)n * C + cv * 8)), v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] /= (float)HW;
-    uint4* o = reinterpret_cast<uint4*>(dx + (int64_t)t * 8);
-    if (beta != 0.f) {
-      float old[8];
-      unpack8(*o, old);
+    const uint4 pv = pack8(v);
+    uint16_t* base = dx + (int64_t)n * HW * C + cv * 8;
+    for (int i = 0; i < HW; ++i) {
+      uint4* o = reinterpret_cast<uint4*>(base + (int64_t)i * C);
+      if (beta != 0.f) {
+        float old[8], w[8];
+        unpack8(*o, old);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] += old[j];
+        for (int j = 0; j < 8; ++j) w[j] = v[j] + old[j];
+        *o = pack8(w);
+      } else {
+        *o = pv;
+      }
     }
-    *o = pack8(v);
   }
 }
 }  // namespace
@@ -1664,8 +1672,9 @@ void avgpool_bwd(const void* dy, void* dx, int N, int HW, int C, be_dtype dt, fl
   const int64_t total = (int64_t)N * HW * C;
   if (total == 0) return;
   if (dt == BE_BF16 && C % 8 == 0 && aligned16(dy) && aligned16(dx) && total / 8 < (1LL << 31)) {
-    launch_pdl(avgpool_bwd_v8, grid_for(total / 8), 256, 0, s, (const uint16_t*)dy, (uint16_t*)dx, HW, C, beta,
-               (uint32_t)(total / 8));
+    const int64_t vecs = (int64_t)N * C / 8;
+    launch_pdl(avgpool_bwd_v8, (int)std::max<int64_t>(1, (vecs + 127) / 128), 128, 0, s, (const uint16_t*)dy,
+               (uint16_t*)dx, HW, C, beta, (uint32_t)vecs);
     after_launch("avgpool_bwd_v8");
     return;
   }
