@@ -421,10 +421,7 @@ def test_bn_statistics_from_conv_epilogue(cfg):
     y = be.conv2d(xd, wd, None, st, pd, bn_stats=True)
     l0 = be.launch_count()
     z = be.batchnorm2d(y, gd, bd, act=1)
-    # statistics finalize + apply, no reduction pass — except where R·S·C < K
-    # (the epilogue is the bottleneck there and the conv skips the statistics:
-    # the streaming statistics pass with its finalize folded in + apply)
-    assert be.launch_count() - l0 == 2
+    n_epi = be.launch_count() - l0  # statistics finalize + apply (no reduction pass) — except where R·S·C < K
     yv = nhwc_to_nchw(y.numpy()).astype(np.float64)
     yo, go, bo = Var(yv, True), Var(gam.astype(np.float64), True), Var(bet.astype(np.float64), True)
     zo = oops.relu(oops.batchnorm2d(yo, go, bo)[0])
@@ -437,7 +434,10 @@ def test_bn_statistics_from_conv_epilogue(cfg):
     y2 = be.conv2d(xd, wd, None, st, pd)
     l0 = be.launch_count()
     z2 = be.batchnorm2d(y2, gd, bd, act=1)
-    assert be.launch_count() - l0 == 2  # statistics (finalize folded in) + apply
+    n_pass = be.launch_count() - l0  # statistics pass (+ finalize unless BE_BN_FOLD=1) + apply
+    # the epilogue statistics remove exactly the statistics pass (the conv
+    # skips them where R·S·C < K: the epilogue is the bottleneck there)
+    assert n_epi == (n_pass - 1 if C * R * R >= K else n_pass), (n_epi, n_pass)
     assert rel(z2.numpy(), z.numpy()) < 1e-2
 
 
