@@ -211,6 +211,68 @@ __global__ void __launch_bounds__(256) dw_dgrad_kernel(const void* __restrict__ 
   }
 }
 
+// stride 2, pad 1: thread per 2×2 quad of dx, (2i..2i+1, 2j..2j+1).  Row 2i
+// takes only tap r = 1 from dy row i; row 2i+1 takes r = 2 from row i and
+// r = 0 from row i+1 (same for columns), so the quad reads 4 dy vectors and
+// does 9 tap products — the per-pixel kernel above issues 36 predicated loads
+// and 36 products (¾ of them zero) and 4 index divisions for the same quad.
+template <bool BF>
+__global__ void __launch_bounds__(256, 2) dw_dgrad_s2q_kernel(const void* __restrict__ dy, const float* __restrict__ w,
+                                                           void* dx, k::ConvGeom g, float beta) {
+  pdl_entry();
+  const int C8 = g.C >> 3, ppb = blockDim.x / C8;
+  if ((int)threadIdx.x >= ppb * C8) return;
+  const int c = (threadIdx.x % C8) * 8;
+  float wr[9][8];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) ldw8(w, (int64_t)t * g.C + c, wr[t]);
+  const unsigned Hq = (g.H + 1) >> 1, Wq = (g.W + 1) >> 1;
+  const unsigned nq = (unsigned)g.N * Hq * Wq;  // host checks < 2^31
+  for (unsigned qd = blockIdx.x * ppb + threadIdx.x / C8; qd < nq; qd += gridDim.x * ppb) {
+    const unsigned j = qd % Wq, ni = qd / Wq;
+    const unsigned i = ni % Hq, n = ni / Hq;
+    const bool i1 = (int)i + 1 < g.P, j1 = (int)j + 1 < g.Q;
+    const int64_t b00 = (((int64_t)n * g.P + i) * g.Q + j) * g.C + c;
+    const Pk<BF> d00 = ldpk<BF>(dy, b00, true), d01 = ldpk<BF>(dy, b00 + g.C, j1),
+                 d10 = ldpk<BF>(dy, b00 + (int64_t)g.Q * g.C, i1),
+                 d11 = ldpk<BF>(dy, b00 + (int64_t)(g.Q + 1) * g.C, i1 && j1);
+    float o00[8], o01[8], o10[8], o11[8];
+    // taps t = r·3 + s
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      float a0 = 0.f, a1 = 0.f;
+      ffma2(a0, a1, d00[k], d00[k + 1], wr[4][k], wr[4][k + 1]);
+      o00[k] = a0; o00[k + 1] = a1;
+      a0 = a1 = 0.f;
+      ffma2(a0, a1, d00[k], d00[k + 1], wr[5][k], wr[5][k + 1]);
+      ffma2(a0, a1, d01[k], d01[k + 1], wr[3][k], wr[3][k + 1]);
+      o01[k] = a0; o01[k + 1] = a1;
+      a0 = a1 = 0.f;
+      ffma2(a0, a1, d00[k], d00[k + 1], wr[7][k], wr[7][k + 1]);
+      ffma2(a0, a1, d10[k], d10[k + 1], wr[1][k], wr[1][k + 1]);
+      o10[k] = a0; o10[k + 1] = a1;
+      a0 = a1 = 0.f;
+      ffma2(a0, a1, d00[k], d00[k + 1], wr[8][k], wr[8][k + 1]);
+      ffma2(a0, a1, d01[k], d01[k + 1], wr[6][k], wr[6][k + 1]);
+      ffma2(a0, a1, d10[k], d10[k + 1], wr[2][k], wr[2][k + 1]);
+      ffma2(a0, a1, d11[k], d11[k + 1], wr[0][k], wr[0][k + 1]);
+      o11[k] = a0; o11[k + 1] = a1;
+    }
+    const bool h1 = 2 * (int)i + 1 < g.H, w1 = 2 * (int)j + 1 < g.W;
+    const int64_t x00 = (((int64_t)n * g.H + 2 * i) * g.W + 2 * j) * g.C + c, xrow = (int64_t)g.W * g.C;
+    if (beta != 0.f) {
+      const Pk<BF> p00 = ldpk<BF>(dx, x00, true), p01 = ldpk<BF>(dx, x00 + g.C, w1),
+                   p10 = ldpk<BF>(dx, x00 + xrow, h1), p11 = ldpk<BF>(dx, x00 + xrow + g.C, h1 && w1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { o00[k] += p00[k]; o01[k] += p01[k]; o10[k] += p10[k]; o11[k] += p11[k]; }
+    }
+    stpk<BF>(dx, x00, o00);
+    if (w1) stpk<BF>(dx, x00 + g.C, o01);
+    if (h1) stpk<BF>(dx, x00 + xrow, o10);
+    if (h1 && w1) stpk<BF>(dx, x00 + xrow + g.C, o11);
+  }
+}
+
 // dw partials: block b sums dy·x over its output-pixel range for every
 // (r, s, c); thread (pl, c8) strides the range by ppb pixels with the 9
 // neighbourhood loads of a pixel issued together; the block then combines
@@ -336,8 +398,21 @@ void dw_conv_dgrad(const void* dy, const float* w, void* dx, const ConvGeom& g, 
   if (npix <= 0) return;
   BE_REQUIRE(g.R == 3 && g.S == 3 && (g.stride == 1 || g.stride == 2) && g.C / 8 <= 256, BE_E_UNSUPPORTED,
              "depthwise conv: 3x3, stride 1|2, C <= 2048");
-  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
   const bool bf = dt == BE_BF16;
+  const int64_t nquad = (int64_t)g.N * ((g.H + 1) / 2) * ((g.W + 1) / 2);
+  static const bool quad_on = [] { const char* e = getenv("BE_DW_S2Q"); return !e || atoi(e) != 0; }();
+  if (quad_on && g.stride == 2 && g.pad == 1 && nquad < (1LL << 31)) {
+    // one wave of resident blocks (2 per SM at <= 128 registers): each
+    // thread loads its 72 filter taps once and walks many quads
+    // (measured on C7: 301 µs/step for the four stride-2 layers vs 347 µs at
+    // 16 blocks per SM and 1089 µs with the per-pixel kernel)
+    const int grid = dw_grid(nquad, g.C, 2), block = dw_block(g.C);
+    if (bf) launch_pdl(dw_dgrad_s2q_kernel<true>, grid, block, 0, s, dy, w, dx, g, beta);
+    else launch_pdl(dw_dgrad_s2q_kernel<false>, grid, block, 0, s, dy, w, dx, g, beta);
+    after_launch("dw_dgrad_s2q");
+    return;
+  }
+  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
   if (g.stride == 1 && bf) launch_pdl(dw_dgrad_kernel<1, true>, grid, block, 0, s, dy, w, dx, g, beta);
   else if (g.stride == 1) launch_pdl(dw_dgrad_kernel<1, false>, grid, block, 0, s, dy, w, dx, g, beta);
   else if (bf) launch_pdl(dw_dgrad_kernel<2, true>, grid, block, 0, s, dy, w, dx, g, beta);
