@@ -211,6 +211,82 @@ __global__ void __launch_bounds__(256) dw_dgrad_kernel(const void* __restrict__ 
   }
 }
 
+// stride 1, pad 1, 3×3 (forward, and dgrad = the same correlation of dY with
+// the taps flipped): a thread owns a column strip of kVR output rows at one
+// (n, q, 8 channels) and slides its 3×3 input window down the strip, loading
+// the 3 vectors of one new input row per output row instead of 9 (the 9-load
+// form is L1-wavefront bound); lanes walk channel groups then q, so every
+// warp load is a contiguous run of one input row.
+constexpr int kVR = 8;
+template <bool BF, bool FLIP>
+__global__ void __launch_bounds__(256, 2) dw_s1_strip_kernel(const void* __restrict__ x, const float* __restrict__ w,
+                                                             void* y, k::ConvGeom g, float beta) {
+  pdl_entry();
+  const int C8 = g.C >> 3, ppb = blockDim.x / C8;
+  if ((int)threadIdx.x >= ppb * C8) return;
+  const int c = (threadIdx.x % C8) * 8;
+  float wr[9][8];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) ldw8(w, (int64_t)(FLIP ? 8 - t : t) * g.C + c, wr[t]);
+  const unsigned segs = (g.H + kVR - 1) / kVR;
+  const unsigned nitems = (unsigned)g.N * segs * g.W;  // host checks < 2^31
+  const int64_t row = (int64_t)g.W * g.C;
+  for (unsigned it = blockIdx.x * ppb + threadIdx.x / C8; it < nitems; it += gridDim.x * ppb) {
+    const int q = (int)(it % g.W);
+    const unsigned ns = it / g.W;
+    const int p0 = (int)(ns % segs) * kVR, n = (int)(ns / segs);
+    const bool lok = q > 0, rok = q + 1 < g.W;
+    const int64_t b = (((int64_t)n * g.H + p0 - 1) * g.W + q) * g.C + c;  // input (p0 − 1, q)
+    Pk<BF> v[3][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const bool ok = p0 - 1 + r >= 0;  // p0 − 1 + r ≤ p0 < H
+      v[r + 1][0] = ldpk<BF>(x, b + r * row - g.C, ok && lok);
+      v[r + 1][1] = ldpk<BF>(x, b + r * row, ok);
+      v[r + 1][2] = ldpk<BF>(x, b + r * row + g.C, ok && rok);
+    }
+    // the next input row is loaded one output row ahead (a rolled loop keeps
+    // the window + prefetch + taps in registers: no spills at 2 blocks / SM)
+    Pk<BF> nx[3];
+    {
+      const bool ok = p0 + 1 < g.H;
+      const int64_t bn = b + 2 * row;
+      nx[0] = ldpk<BF>(x, bn - g.C, ok && lok);
+      nx[1] = ldpk<BF>(x, bn, ok);
+      nx[2] = ldpk<BF>(x, bn + g.C, ok && rok);
+    }
+    const int tend = min(kVR, g.H - p0);
+#pragma unroll 1
+    for (int t = 0; t < tend; ++t) {
+      const int p = p0 + t;
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) { v[0][s2] = v[1][s2]; v[1][s2] = v[2][s2]; v[2][s2] = nx[s2]; }
+      {
+        const bool ok = p + 2 < g.H;
+        const int64_t bn = b + (int64_t)(t + 3) * row;
+        nx[0] = ldpk<BF>(x, bn - g.C, ok && lok);
+        nx[1] = ldpk<BF>(x, bn, ok);
+        nx[2] = ldpk<BF>(x, bn + g.C, ok && rok);
+      }
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < 9; ++tt) ffma2(a0, a1, v[tt / 3][tt % 3][j], v[tt / 3][tt % 3][j + 1], wr[tt][j], wr[tt][j + 1]);
+        o[j] = a0; o[j + 1] = a1;
+      }
+      const int64_t oi = b + (int64_t)(t + 1) * row;  // output (p, q): same layout as the input (P = H, Q = W)
+      if (beta != 0.f) {
+        const Pk<BF> prev = ldpk<BF>(y, oi, true);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += prev[j];
+      }
+      stpk<BF>(y, oi, o);
+    }
+  }
+}
+
 // stride 2, pad 1: thread per 2×2 quad of dx, (2i..2i+1, 2j..2j+1).  Row 2i
 // takes only tap r = 1 from dy row i; row 2i+1 takes r = 2 from row i and
 // r = 0 from row i+1 (same for columns), so the quad reads 4 dy vectors and
@@ -378,13 +454,28 @@ static int dw_grid(int64_t pixels, int C, int per_sm) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148LL * per_sm));
 }
 
+static bool dw_strip_ok(const ConvGeom& g) {
+  static const bool on = [] { const char* e = getenv("BE_DW_STRIP"); return !e || atoi(e) != 0; }();
+  return on && g.stride == 1 && g.pad == 1 && g.P == g.H && g.Q == g.W &&
+         (int64_t)g.N * ((g.H + kVR - 1) / kVR) * g.W < (1LL << 31);
+}
+static int dw_strip_grid(const ConvGeom& g) {
+  return dw_grid((int64_t)g.N * ((g.H + kVR - 1) / kVR) * g.W, g.C, 2);
+}
+
 void dw_conv_fwd(const void* x, const float* w, void* y, const ConvGeom& g, be_dtype dt, cudaStream_t s) {
   const int64_t npix = (int64_t)g.N * g.P * g.Q;
   if (npix <= 0) return;
   BE_REQUIRE(g.R == 3 && g.S == 3 && (g.stride == 1 || g.stride == 2) && g.C / 8 <= 256, BE_E_UNSUPPORTED,
              "depthwise conv: 3x3, stride 1|2, C <= 2048");
-  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
   const bool bf = dt == BE_BF16;
+  if (dw_strip_ok(g)) {
+    if (bf) launch_pdl(dw_s1_strip_kernel<true, false>, dw_strip_grid(g), dw_block(g.C), 0, s, x, w, y, g, 0.f);
+    else launch_pdl(dw_s1_strip_kernel<false, false>, dw_strip_grid(g), dw_block(g.C), 0, s, x, w, y, g, 0.f);
+    after_launch("dw_fwd_strip");
+    return;
+  }
+  const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);
   if (g.stride == 1 && bf) launch_pdl(dw_fwd_kernel<1, true>, grid, block, 0, s, x, w, y, g);
   else if (g.stride == 1) launch_pdl(dw_fwd_kernel<1, false>, grid, block, 0, s, x, w, y, g);
   else if (bf) launch_pdl(dw_fwd_kernel<2, true>, grid, block, 0, s, x, w, y, g);
@@ -410,6 +501,12 @@ void dw_conv_dgrad(const void* dy, const float* w, void* dx, const ConvGeom& g, 
     if (bf) launch_pdl(dw_dgrad_s2q_kernel<true>, grid, block, 0, s, dy, w, dx, g, beta);
     else launch_pdl(dw_dgrad_s2q_kernel<false>, grid, block, 0, s, dy, w, dx, g, beta);
     after_launch("dw_dgrad_s2q");
+    return;
+  }
+  if (dw_strip_ok(g)) {  // dx (H×W) = correlation of dY (P×Q = H×W) with the flipped taps
+    if (bf) launch_pdl(dw_s1_strip_kernel<true, true>, dw_strip_grid(g), dw_block(g.C), 0, s, dy, w, dx, g, beta);
+    else launch_pdl(dw_s1_strip_kernel<false, true>, dw_strip_grid(g), dw_block(g.C), 0, s, dy, w, dx, g, beta);
+    after_launch("dw_dgrad_strip");
     return;
   }
   const int grid = dw_grid(npix, g.C, 16), block = dw_block(g.C);

@@ -98,11 +98,13 @@ def test_depthwise_conv_op(geom, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-@pytest.mark.parametrize("geom", [(2, 24, 10, 10), (1, 40, 11, 13), (2, 96, 1, 3), (3, 16, 7, 2)])
-def test_depthwise_stride2_dgrad_accumulates(geom, dtype):
-    """Stride-2 dx (the 2×2-quad kernel) written fresh by the first VJP and
-    accumulated (beta 1) by the second: x feeds two stride-2 depthwise convs
-    with different filters; ragged odd / tiny maps."""
+@pytest.mark.parametrize("st", [1, 2])
+@pytest.mark.parametrize("geom", [(2, 24, 10, 10), (1, 40, 11, 13), (2, 96, 1, 3), (3, 16, 7, 2), (1, 32, 17, 5)])
+def test_depthwise_dgrad_accumulates(geom, st, dtype):
+    """dx (stride 2: the 2×2-quad kernel; stride 1: the column-strip kernel)
+    written fresh by the first VJP and accumulated (beta 1) by the second: x
+    feeds two depthwise convs with different filters; ragged odd / tiny maps,
+    maps taller than one strip; dw of both filters."""
     be = be_init()
     be.set_compute_dtype(dtype)
     N, C, H, W = geom
@@ -114,16 +116,18 @@ def test_depthwise_stride2_dgrad_accumulates(geom, dtype):
     xl = be.tensor(nchw_to_nhwc(x), requires_grad=True)
     xd = be.cast(xl, "bf16") if dtype == "bf16" else xl
     wl = [be.tensor(np.ascontiguousarray(w[:, 0].transpose(1, 2, 0)), requires_grad=True) for w in (w1, w2)]
-    y = be.add(be.conv2d_depthwise(xd, wl[0], 2, 1), be.conv2d_depthwise(xd, wl[1], 2, 1))
+    y = be.add(be.conv2d_depthwise(xd, wl[0], st, 1), be.conv2d_depthwise(xd, wl[1], st, 1))
     xo = Var(x.astype(np.float64), True)
-    yo = oops.add(oops.conv2d_depthwise(xo, Var(w1.astype(np.float64)), 2, 1),
-                  oops.conv2d_depthwise(xo, Var(w2.astype(np.float64)), 2, 1))
+    wo = [Var(w.astype(np.float64), True) for w in (w1, w2)]
+    yo = oops.add(oops.conv2d_depthwise(xo, wo[0], st, 1), oops.conv2d_depthwise(xo, wo[1], st, 1))
     g = synth.normal(yo.value.shape, 46, 4)
     if dtype == "bf16":
         g = synth.bf16_values(g)
     y.backward(be.tensor(nchw_to_nhwc(g), dtype="bf16" if dtype == "bf16" else None))
     backward(yo, g.astype(np.float64))
     assert rel(nhwc_to_nchw(xl.grad.numpy()), xo.grad) <= TOL[dtype]
+    for a, b in zip(wl, wo):
+        assert rel(a.grad.numpy(), b.grad[:, 0].transpose(1, 2, 0)) <= TOL[dtype]
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
